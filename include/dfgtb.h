@@ -1,0 +1,142 @@
+/* dfgtb -- B200-native (sm_100a) dual-tree fast Gauss transform: C ABI.
+ *
+ * Drop-in boundary for the reference's DFGT kernel-summation path
+ * (/root/reference/proj).  Each entry point names the reference interface it
+ * replaces.  Plain pointers and sizes only; no C++ or torch types.  Points are
+ * N x D row-major float64 (PointSet, dataset.hpp:15-41).  Host pointers unless a
+ * function name ends in _device.
+ *
+ * Return codes: DFGTB_OK 0, DFGTB_EINVAL 1 (the reference's std::invalid_argument),
+ * DFGTB_ECUDA 2 (CUDA/runtime error), DFGTB_ENOMEM 3.  dfgtb_last_error() gives the
+ * message (thread local).  A handle owns one CUDA stream and is not thread-safe,
+ * like DualTreeEngine (engine.hpp:85).
+ */
+#ifndef DFGTB_H
+#define DFGTB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFGTB_OK 0
+#define DFGTB_EINVAL 1
+#define DFGTB_ECUDA 2
+#define DFGTB_ENOMEM 3
+
+/* EngineConfig (engine.hpp:17-26) + DualTreeEngine::Mode (engine.hpp:89). */
+typedef struct dfgtb_config {
+  double epsilon;     /* relative error bound, >= 0                       (default 0.01) */
+  int leaf_threshold; /* kd-tree leaf size, >= 1                          (default 20)   */
+  int p_max;          /* series order limit; 0 = default_p_max(D)         (truncation.cpp:168) */
+  int cost_model;     /* 0 exponential, 1 term_count                      (truncation.hpp:216) */
+  int mode;           /* 0 centroid (DFD), 1 series (DFGT)                (engine.hpp:89) */
+} dfgtb_config;
+
+/* TraversalStats (engine.hpp:66-74) + level count of the BFS traversal. */
+typedef struct dfgtb_stats {
+  uint64_t kernel_evaluations;
+  uint64_t pairs_visited;
+  uint64_t base_cases;
+  uint64_t prunes_finite_diff;
+  uint64_t prunes_farfield;
+  uint64_t prunes_direct_local;
+  uint64_t prunes_far_to_local;
+  uint64_t levels;
+} dfgtb_stats;
+
+/* Device time (ms, CUDA events on the handle's stream) of the last compute. */
+typedef struct dfgtb_timings {
+  float tree_ms, traverse_ms, moments_ms, local_ms, base_ms, farfield_ms, final_ms, total_ms;
+} dfgtb_timings;
+
+/* One bandwidth of a CV sweep (CvRow, cv.hpp:49-56 + ScoreResult cv.hpp:25-32). */
+typedef struct dfgtb_cv_row {
+  double scale, h, conv_h;
+  double lk_score;  /* lkcv_from_sums  (cv.cpp:61-76) */
+  int lk_clamped;
+  double ls_score;  /* lscv_from_sums  (cv.cpp:78-97) */
+  double seconds;   /* device time of this row's computes */
+} dfgtb_cv_row;
+
+typedef struct dfgtb_handle dfgtb_handle;
+
+void dfgtb_default_config(dfgtb_config* cfg);
+
+/* DualTreeEngine(refs, mode, config)  engine.cpp:352-366 / engine.hpp:91.
+ * Uploads the reference points and builds the kd-tree on the GPU (KdTree::build). */
+int dfgtb_create(const double* refs, size_t n, size_t d, const dfgtb_config* cfg,
+                 dfgtb_handle** out);
+/* Same with refs already in device memory. */
+int dfgtb_create_device(const double* d_refs, size_t n, size_t d, const dfgtb_config* cfg,
+                        dfgtb_handle** out);
+void dfgtb_destroy(dfgtb_handle* h);
+
+/* DualTreeEngine::compute(queries, h)  engine.cpp:405-424 / engine.hpp:94-95.
+ * queries == NULL -> Q = R (the reference tree is reused as query tree).
+ * out_sums: nq (or n when Q = R) sums in input order.  stats nullable. */
+int dfgtb_compute(dfgtb_handle* h, const double* queries, size_t nq, double bandwidth,
+                  double* out_sums, dfgtb_stats* stats);
+int dfgtb_compute_device(dfgtb_handle* h, const double* d_queries, size_t nq, double bandwidth,
+                         double* d_out_sums, dfgtb_stats* stats);
+
+/* DualTreeEngine::last_stats / p_max  engine.hpp:97-99. */
+int dfgtb_last_stats(dfgtb_handle* h, dfgtb_stats* stats);
+int dfgtb_last_timings(dfgtb_handle* h, dfgtb_timings* t);
+int dfgtb_p_max(dfgtb_handle* h);
+
+/* lkcv_from_sums + lscv_from_sums on Q = R sums computed on the device at h and
+ * conv_h (cv.cpp:61-97; conv_h = 2h or sqrt(2)h, cv.cpp:27-30).  conv_h <= 0 skips
+ * the least-squares score.  Sums never leave the device. */
+int dfgtb_cv(dfgtb_handle* h, double bandwidth, double conv_h, dfgtb_cv_row* row);
+
+/* bandwidth_sweep (cv.cpp:141-182) for both scores: rows[i] at scale[i]*base_h.
+ * scales must be strictly increasing.  sqrt2 != 0 -> conv_h = sqrt(2) h. */
+int dfgtb_sweep(dfgtb_handle* h, const double* scales, size_t ns, double base_h, int sqrt2,
+                dfgtb_cv_row* rows);
+
+/* CV scores from host sums (lkcv_from_sums / lscv_from_sums, cv.cpp:61-97). */
+int dfgtb_lkcv_from_sums(size_t n, size_t d, double bandwidth, const double* sums,
+                         double* score, int* clamped);
+int dfgtb_lscv_from_sums(size_t n, size_t d, double bandwidth, const double* sums,
+                         double conv_h, const double* conv_sums, double* score);
+
+/* Reference tree export for the bit-exact check (KdTree accessors, kdtree.hpp:22-57).
+ * Arrays sized by dfgtb_tree_nodes(); begin is int64 like the reference's size_t. */
+int dfgtb_tree_nodes(dfgtb_handle* h);
+int dfgtb_tree_height(dfgtb_handle* h);
+int dfgtb_export_tree(dfgtb_handle* h, int* perm, double* lo, double* hi, double* centroid,
+                      double* max_side, int* left, int* right, int* split_dim,
+                      double* split_coord, int64_t* begin, int* count);
+
+/* naive_kde (engine.cpp:22-36): exhaustive FP64 sums on the GPU (K12). */
+int dfgtb_naive(const double* queries, size_t nq, const double* refs, size_t nr, size_t d,
+                double bandwidth, double* out);
+
+/* Series primitives on the GPU (series.cpp), tables in the reference's position
+ * layout (p_max^D entries, base-p_max digits, dimension 0 most significant).
+ * op: 0 moments(pts n, center a)            -> out table        (series.cpp:238-254)
+ *     1 eval_farfield(table in, center a, q b) -> out[0]        (series.cpp:289-303)
+ *     2 direct_local(pts n, center a, order) -> out table += ... (series.cpp:305-326)
+ *     3 far_to_local(table in, src a, dst b) -> out table += ... (series.cpp:328-353)
+ *     4 local_to_local(table in, src a, dst b) -> out table += ...(series.cpp:355-391)
+ *     5 eval_local(table in, center a, q b)  -> out[0]          (series.cpp:393-407)
+ * For op 0/2 `in` holds n points; otherwise `in` is a table.  `out` is read-modify-
+ * written for 2/3/4 like the reference's accumulate-into semantics. */
+int dfgtb_series_op(int op, size_t d, int p_max, const double* in, size_t n, const double* a,
+                    const double* b, double bandwidth, int order, double* out);
+
+/* Measured FP64 FMA instruction throughput of the device (instr/s); bench roofline. */
+double dfgtb_dfma_peak(void);
+
+/* Number of visible CUDA devices (0 when none; never raises). */
+int dfgtb_device_count(void);
+
+const char* dfgtb_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

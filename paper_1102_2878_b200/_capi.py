@@ -1,0 +1,110 @@
+"""ctypes binding of the C ABI in include/dfgtb.h (libdfgtb.so, built in-tree).
+
+The product path: every call goes to the sm_100a library.  There is no CPU
+fallback -- if libdfgtb.so is missing or fails to load, import raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdfgtb.so")
+
+OK, EINVAL, ECUDA, ENOMEM = 0, 1, 2, 3
+
+_D = C.POINTER(C.c_double)
+_I = C.POINTER(C.c_int)
+_I64 = C.POINTER(C.c_int64)
+
+
+class Config(C.Structure):
+    _fields_ = [("epsilon", C.c_double), ("leaf_threshold", C.c_int), ("p_max", C.c_int),
+                ("cost_model", C.c_int), ("mode", C.c_int)]
+
+
+class Stats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "kernel_evaluations", "pairs_visited", "base_cases", "prunes_finite_diff",
+        "prunes_farfield", "prunes_direct_local", "prunes_far_to_local", "levels")]
+
+    def as_dict(self):
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+class Timings(C.Structure):
+    _fields_ = [(n, C.c_float) for n in (
+        "tree_ms", "traverse_ms", "moments_ms", "local_ms", "base_ms", "farfield_ms", "final_ms",
+        "total_ms")]
+
+    def as_dict(self):
+        return {n: float(getattr(self, n)) for n, _ in self._fields_}
+
+
+class CvRow(C.Structure):
+    _fields_ = [("scale", C.c_double), ("h", C.c_double), ("conv_h", C.c_double),
+                ("lk_score", C.c_double), ("lk_clamped", C.c_int), ("ls_score", C.c_double),
+                ("seconds", C.c_double)]
+
+
+# every symbol include/dfgtb.h declares (tests check the .so exports all of them)
+EXPORTS = (
+    "dfgtb_default_config", "dfgtb_create", "dfgtb_create_device", "dfgtb_destroy",
+    "dfgtb_compute", "dfgtb_compute_device", "dfgtb_last_stats", "dfgtb_last_timings",
+    "dfgtb_p_max", "dfgtb_cv", "dfgtb_sweep", "dfgtb_lkcv_from_sums", "dfgtb_lscv_from_sums",
+    "dfgtb_tree_nodes", "dfgtb_tree_height", "dfgtb_export_tree", "dfgtb_naive",
+    "dfgtb_series_op", "dfgtb_dfma_peak", "dfgtb_device_count", "dfgtb_last_error",
+)
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `make -C {_HERE}` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    V = C.c_void_p
+    sz = C.c_size_t
+    sig = {
+        "dfgtb_default_config": (None, [C.POINTER(Config)]),
+        "dfgtb_create": (C.c_int, [_D, sz, sz, C.POINTER(Config), C.POINTER(V)]),
+        "dfgtb_create_device": (C.c_int, [V, sz, sz, C.POINTER(Config), C.POINTER(V)]),
+        "dfgtb_destroy": (None, [V]),
+        "dfgtb_compute": (C.c_int, [V, _D, sz, C.c_double, _D, C.POINTER(Stats)]),
+        "dfgtb_compute_device": (C.c_int, [V, V, sz, C.c_double, V, C.POINTER(Stats)]),
+        "dfgtb_last_stats": (C.c_int, [V, C.POINTER(Stats)]),
+        "dfgtb_last_timings": (C.c_int, [V, C.POINTER(Timings)]),
+        "dfgtb_p_max": (C.c_int, [V]),
+        "dfgtb_cv": (C.c_int, [V, C.c_double, C.c_double, C.POINTER(CvRow)]),
+        "dfgtb_sweep": (C.c_int, [V, _D, sz, C.c_double, C.c_int, C.POINTER(CvRow)]),
+        "dfgtb_lkcv_from_sums": (C.c_int, [sz, sz, C.c_double, _D, _D, _I]),
+        "dfgtb_lscv_from_sums": (C.c_int, [sz, sz, C.c_double, _D, C.c_double, _D, _D]),
+        "dfgtb_tree_nodes": (C.c_int, [V]),
+        "dfgtb_tree_height": (C.c_int, [V]),
+        "dfgtb_export_tree": (C.c_int, [V, _I, _D, _D, _D, _D, _I, _I, _I, _D, _I64, _I]),
+        "dfgtb_naive": (C.c_int, [_D, sz, _D, sz, sz, C.c_double, _D]),
+        "dfgtb_series_op": (C.c_int, [C.c_int, sz, C.c_int, _D, sz, _D, _D, C.c_double, C.c_int,
+                                      _D]),
+        "dfgtb_dfma_peak": (C.c_double, []),
+        "dfgtb_device_count": (C.c_int, []),
+        "dfgtb_last_error": (C.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(rc: int) -> None:
+    """Raise the Python analogue of the reference's exception for a return code."""
+    if rc == OK:
+        return
+    msg = (lib.dfgtb_last_error() or b"").decode()
+    if rc == EINVAL:
+        raise ValueError(msg)  # std::invalid_argument
+    if rc == ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)

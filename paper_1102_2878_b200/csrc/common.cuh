@@ -1,0 +1,105 @@
+// Shared helpers for the DFGT sm_100a library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace dfgtb {
+
+constexpr int kMaxDim = 16;   // digits packed 4 bits/dim in a uint64
+constexpr int kWarp = 32;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct OutOfMemory : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line)
+{
+  if (e == cudaSuccess) return;
+  std::string msg = std::string(what) + " failed at " + file + ":" + std::to_string(line) +
+                    ": " + cudaGetErrorString(e);
+  if (e == cudaErrorMemoryAllocation) throw OutOfMemory(msg);
+  throw CudaError(msg);
+}
+#define CK(x) ::dfgtb::cuda_check((x), #x, __FILE__, __LINE__)
+#define CK_LAUNCH() ::dfgtb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Growable device buffer (capacity only ever grows; contents not preserved on growth).
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release()
+  {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  // ensure room for n elements; growth is geometric to amortise cudaMalloc
+  T* reserve(size_t n)
+  {
+    if (n <= cap && p) return p;
+    size_t c = cap ? cap : 1;
+    while (c < n) c *= 2;
+    if (c < 256) c = 256;
+    release();
+    CK(cudaMalloc(&p, c * sizeof(T)));
+    cap = c;
+    return p;
+  }
+  // ensure room, preserving the first `keep` elements
+  T* grow_keep(size_t n, size_t keep, cudaStream_t s)
+  {
+    if (n <= cap && p) return p;
+    size_t c = cap ? cap : 256;
+    while (c < n) c *= 2;
+    T* q = nullptr;
+    CK(cudaMalloc(&q, c * sizeof(T)));
+    if (p && keep) CK(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    if (p) {
+      CK(cudaStreamSynchronize(s));
+      cudaFree(p);
+    }
+    p = q;
+    cap = c;
+    return p;
+  }
+};
+
+__host__ __device__ inline int digit_of(uint64_t packed, int d)
+{
+  return d < kMaxDim ? (int)((packed >> (4 * d)) & 15ull) : 0;
+}
+
+// Deterministic warp sum (xor butterfly; identical order on every call).
+__device__ inline double warp_sum(double v)
+{
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ inline int warp_sum_i(int v)
+{
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace dfgtb

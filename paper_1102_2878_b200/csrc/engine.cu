@@ -1,0 +1,1091 @@
+// DFGT engine on sm_100a: level-synchronous dual-tree traversal and the kernels
+// that execute its work lists.
+//
+// Reference path (all under /root/reference/proj/src):
+//   DualTreeEngine::compute       engine.cpp:405-424
+//   Traversal::recurse            engine.cpp:113-195   -> k_classify + k_emit (per level)
+//   choose_best_method            truncation.cpp:130-166 -> dev_choose
+//   Traversal::summarize F/D/T    engine.cpp:197-237   -> k_farfield / k_local_items
+//   Traversal::base_case          engine.cpp:239-269   -> k_base_case
+//   Traversal::post_process       engine.cpp:271-318   -> k_l2l (top-down) + k_finalize
+//   moments_for                   engine.cpp:368-403   -> k_moments (direct, per used node)
+//
+// Schedule (the reference's recursion replaced; results differ only within eps):
+// the frontier of live (Q, R) node pairs is kept grouped by query node (an antichain:
+// every query node appears at most once per level), one warp per query node.  The
+// error budget of a pair is tau = eps |R| G^l(Q) / |R_total| where G^l(Q) is a valid
+// lower bound on every G(q), q in Q:  sum of |R'| K(d_max) over all pairs retired at
+// Q or its ancestors (pruned, summarised or sent to the base case) plus over all
+// frontier pairs of Q.  Those pairs partition the reference set, so the per-query
+// error stays <= eps G(q) exactly as in the reference's proof.
+// Work items (F/D/T/base) are appended per level with a per-node rank and counting-
+// sorted by query node afterwards, so every kernel accumulates in a fixed order:
+// results are bit-reproducible run to run.
+#include "engine.cuh"
+#include "series_dev.cuh"
+
+#include <cub/device/device_scan.cuh>
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cstring>
+
+namespace dfgtb {
+
+int default_p_max(int D)
+{  // truncation.cpp:168-186
+  switch (D) {
+  case 1: return 8;
+  case 2: return 6;
+  case 3: return 4;
+  case 4:
+  case 5: return 2;
+  default: return 1;
+  }
+}
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kWarpsPerBlock = kBlock / 32;
+constexpr int kMaxGridBlocks = 148 * 16;
+enum Kind { kE = 0, kF = 1, kD = 2, kT = 3, kB = 4, kX = 5, kFD = 6 };
+
+// ------------------------------------------------------------------ truncation
+__device__ double d_binomial(int n, int k)
+{
+  double b = 1.0;
+  for (int i = 1; i <= k; ++i) b *= (double)(n - k + i) / (double)i;
+  return b;
+}
+__device__ double d_sqrt_factorial(int p)
+{
+  double f = 1.0;
+  for (int k = 2; k <= p; ++k) f *= k;
+  return sqrt(f);
+}
+__device__ double d_ipow(double x, int n)
+{
+  double r = 1.0;
+  for (int i = 0; i < n; ++i) r *= x;
+  return r;
+}
+// truncation.cpp:40-54
+__device__ double d_bound_sum(double count, double s, int dpow, double a, double b, int dim)
+{
+  double sum = 0.0;
+  for (int k = 0; k < dim; ++k) sum += d_binomial(dim, k) * d_ipow(a, k) * d_ipow(b, dim - k);
+  const double pre = count / d_ipow(1.0 - s, dim * dpow);
+  double bound = pre * sum;
+  if (!isfinite(bound) && count > 0.0 && sum > 0.0)
+    bound = exp(log(count) - (double)(dim * dpow) * log1p(-s) + log(sum));
+  return bound;
+}
+__device__ double d_ff_bound(double count, double r, int p, int dim)
+{  // truncation.cpp:58-65
+  if (count <= 0.0) return 0.0;
+  const double rp = d_ipow(r, p);
+  return d_bound_sum(count, r, 1, 1.0 - rp, rp / d_sqrt_factorial(p), dim);
+}
+__device__ double d_f2l_bound(double count, double r, int p, int dim)
+{  // truncation.cpp:72-81
+  if (count <= 0.0) return 0.0;
+  const double s = 2.0 * r, sp = d_ipow(s, p);
+  return d_bound_sum(count, s, 2, (1.0 - sp) * (1.0 - sp), sp * (2.0 - sp) / d_sqrt_factorial(p),
+                     dim);
+}
+__device__ int d_order_ff(double ratio, double count, double tau, int pmax, int dim)
+{  // truncation.cpp:85-112
+  if (ratio >= 1.0) return 0;
+  for (int p = 1; p <= pmax; ++p)
+    if (d_ff_bound(count, ratio, p, dim) <= tau) return p;
+  return 0;
+}
+__device__ int d_order_f2l(double ratio, double count, double tau, int pmax, int dim)
+{  // truncation.cpp:114-128
+  if (ratio >= 0.5) return 0;
+  for (int p = 1; p <= pmax; ++p)
+    if (d_f2l_bound(count, ratio, p, dim) <= tau) return p;
+  return 0;
+}
+// choose_best_method, truncation.cpp:130-166 (ties F > D > T > E)
+__device__ void dev_choose(double nq, double nr, double sq, double sr, double h, double tau,
+                           int pmax, int dim, int cost, int& kind, int& order)
+{
+  const int pf = d_order_ff(sr / (2.0 * h), nr, tau, pmax, dim);
+  const int pd = d_order_ff(sq / (2.0 * h), nr, tau, pmax, dim);
+  const int pt = d_order_f2l((sq < sr ? sr : sq) / (4.0 * h), nr, tau, pmax, dim);
+  const double D = (double)dim;
+  double cf = CUDART_INF, cd = CUDART_INF, ct = CUDART_INF;
+  if (cost == 0) {  // exponential model; integer powers are exact
+    if (pf) cf = nq * d_ipow(D, pf + 1);
+    if (pd) cd = nr * d_ipow(D, pd + 1);
+    if (pt) ct = d_ipow(D, 2 * pt + 1);
+  } else {
+    if (pf) cf = nq * d_ipow((double)pf, dim);
+    if (pd) cd = nr * d_ipow((double)pd, dim);
+    if (pt) ct = D * d_ipow((double)pt, 2 * dim);
+  }
+  const double ce = D * nq * nr;
+  const double m1 = cd < cf ? cd : cf, m2 = ce < ct ? ce : ct;
+  const double best = m2 < m1 ? m2 : m1;
+  if (cf == best) { kind = kF; order = pf; }
+  else if (cd == best) { kind = kD; order = pd; }
+  else if (ct == best) { kind = kT; order = pt; }
+  else { kind = kE; order = 0; }
+}
+
+// ------------------------------------------------------------------ traversal
+struct TreeView {
+  const double *lo, *hi, *cen, *side;
+  const int *left, *right, *count, *begin, *parent;
+  const double* xs;
+};
+
+struct TravArgs {
+  TreeView Q, R;
+  int D, pmax, cost, series;
+  double h, scale, eps, ntot;
+  // frontier in
+  int m;
+  const int *fq, *foff, *flen, *fr;
+  const double* fbase;
+  // scratch
+  double *pkmax, *pkmin;
+  int* dec;
+  Cnt* cnt;
+  int* childlen;
+  double* newbase;
+  double* L;
+  int T;
+  int* Lord;
+  unsigned long long* kevals;
+  // emit
+  const Cnt* cntoff;
+  int *nq, *noff, *nlen, *nr;
+  double* nbase;
+  Item *itF, *itDT, *itB;
+  int *cntF, *cntDT, *cntB;
+};
+
+template <int DT>
+__device__ __forceinline__ void box_bounds(const double* alo, const double* ahi, const double* blo,
+                                           const double* bhi, int Drt, double& lo2, double& hi2)
+{  // kdtree.cpp:122-141
+  const int D = DT ? DT : Drt;
+  double lo = 0.0, hi = 0.0;
+#pragma unroll
+  for (int k = 0; k < (DT ? DT : kMaxDim); ++k) {
+    if (!DT && k >= D) break;
+    const double g1 = blo[k] - ahi[k];
+    const double g2 = alo[k] - bhi[k];
+    const double l = 0.5 * (g1 + fabs(g1) + g2 + fabs(g2));
+    lo += l * l;
+    const double u1 = bhi[k] - alo[k], u2 = ahi[k] - blo[k];
+    const double u = u1 < u2 ? u2 : u1;
+    hi += u * u;
+  }
+  lo2 = lo;
+  hi2 = hi;
+}
+
+__device__ __forceinline__ int warp_excl_scan(int v, int lane, int& total)
+{
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  total = __shfl_sync(0xffffffffu, x, 31);
+  return x - v;
+}
+
+// One warp per frontier query node: bounds, G^l, prune/summarise/base/expand decisions.
+template <int DT>
+__global__ void __launch_bounds__(kBlock) k_classify(TravArgs a)
+{
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int D = DT ? DT : a.D;
+  for (int e = w0; e < a.m; e += nw) {
+    const int Q = a.fq[e];
+    const int off = a.foff[e], len = a.flen[e];
+    const double* qlo = a.Q.lo + (size_t)Q * D;
+    const double* qhi = a.Q.hi + (size_t)Q * D;
+    const bool qleaf = a.Q.left[Q] < 0;
+    const double nq = (double)a.Q.count[Q];
+    const double sq = a.Q.side[Q];
+    // pass 1: kernel bounds and the lower-bound mass of every live pair
+    double part = 0.0;
+    for (int j = lane; j < len; j += 32) {
+      const int R = a.fr[off + j];
+      double dl, du;
+      box_bounds<DT>(qlo, qhi, a.R.lo + (size_t)R * D, a.R.hi + (size_t)R * D, D, dl, du);
+      const double kmax = exp(a.scale * dl);  // kernel at closest approach
+      const double kmin = exp(a.scale * du);
+      a.pkmax[off + j] = kmax;
+      a.pkmin[off + j] = kmin;
+      part += (double)a.R.count[R] * kmin;
+    }
+    const double glo = a.fbase[e] + warp_sum(part);
+    // pass 2: decisions
+    double fd_dlo = 0.0, fd_const = 0.0, ret = 0.0;
+    int nF = 0, nDT = 0, nT = 0, nB = 0, nFD = 0, slots = 0;
+    unsigned long long kev = 0;
+    for (int j = lane; j < len; j += 32) {
+      const int R = a.fr[off + j];
+      const double kmax = a.pkmax[off + j], kmin = a.pkmin[off + j];
+      const double nr = (double)a.R.count[R];
+      const double dlo = nr * kmin;
+      const double tau = a.eps * nr * glo / a.ntot;
+      int kind = kX, order = 0;
+      if (0.5 * nr * (kmax - kmin) <= tau) {  // kernel-difference prune, engine.cpp:137-148
+        kind = kFD;
+        fd_dlo += dlo;
+        fd_const += 0.5 * nr * (kmax + kmin);
+        ++nFD;
+      } else {
+        if (a.series) {
+          dev_choose(nq, nr, sq, a.R.side[R], a.h, tau, a.pmax, D, a.cost, kind, order);
+          if (kind == kE) kind = kX;
+        }
+        if (kind == kX && qleaf && a.R.left[R] < 0) kind = kB;
+        if (kind == kX) {
+          slots += a.R.left[R] < 0 ? 1 : 2;
+        } else if (kind == kB) {
+          ++nB;
+          kev += (unsigned long long)a.Q.count[Q] * (unsigned long long)a.R.count[R];
+          ret += dlo;
+        } else {
+          ret += dlo;
+          if (kind == kF) ++nF;
+          else {
+            ++nDT;
+            if (kind == kT) ++nT;
+          }
+        }
+      }
+      a.dec[off + j] = kind | (order << 8);
+    }
+    fd_dlo = warp_sum(fd_dlo);
+    fd_const = warp_sum(fd_const);
+    ret = warp_sum(ret);
+    nF = warp_sum_i(nF);
+    nDT = warp_sum_i(nDT);
+    nT = warp_sum_i(nT);
+    nB = warp_sum_i(nB);
+    nFD = warp_sum_i(nFD);
+    slots = warp_sum_i(slots);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kev += __shfl_xor_sync(0xffffffffu, kev, o);
+    if (lane == 0) {
+      const int ne = slots > 0 ? (qleaf ? 1 : 2) : 0;
+      a.cnt[e] = Cnt{ ne, ne * slots, nF, nDT, nT, nB, nFD };
+      a.childlen[e] = slots;
+      a.newbase[e] = a.fbase[e] + (fd_dlo + ret);
+      if (nFD) {
+        a.L[(size_t)Q * a.T] += fd_const;  // constant local term (order 1)
+        if (a.Lord[Q] < 1) a.Lord[Q] = 1;
+      }
+      if (kev) atomicAdd(a.kevals, kev);
+    }
+  }
+}
+
+// One warp per frontier query node: write the next frontier and the work items.
+__global__ void __launch_bounds__(kBlock) k_emit(TravArgs a, int gF, int gDT, int gB)
+{
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int e = w0; e < a.m; e += nw) {
+    const Cnt o = a.cntoff[e];
+    const Cnt c = a.cnt[e];
+    const int Q = a.fq[e];
+    const int off = a.foff[e], len = a.flen[e];
+    const bool qleaf = a.Q.left[Q] < 0;
+    const int cl = a.childlen[e];
+    if (lane == 0 && c.e) {
+      const double nb = a.newbase[e];
+      if (qleaf) {
+        a.nq[o.e] = Q;
+        a.nbase[o.e] = nb;
+        a.noff[o.e] = o.p;
+        a.nlen[o.e] = cl;
+      } else {
+        a.nq[o.e] = a.Q.left[Q];
+        a.nq[o.e + 1] = a.Q.right[Q];
+        a.nbase[o.e] = nb;
+        a.nbase[o.e + 1] = nb;
+        a.noff[o.e] = o.p;
+        a.noff[o.e + 1] = o.p + cl;
+        a.nlen[o.e] = cl;
+        a.nlen[o.e + 1] = cl;
+      }
+    }
+    const int rF = a.cntF[Q], rDT = a.cntDT[Q], rB = a.cntB[Q];
+    int runX = 0, runF = 0, runDT = 0, runB = 0;
+    for (int j0 = 0; j0 < len; j0 += 32) {
+      const int j = j0 + lane;
+      int kind = kE, order = 0, R = 0;
+      if (j < len) {
+        const int dcode = a.dec[off + j];
+        kind = dcode & 0xff;
+        order = dcode >> 8;
+        R = a.fr[off + j];
+      }
+      const bool rleaf = (j < len) ? a.R.left[R] < 0 : true;
+      int tot;
+      const int px = warp_excl_scan(kind == kX ? (rleaf ? 1 : 2) : 0, lane, tot);
+      if (kind == kX) {
+        const int dst = o.p + runX + px;
+        if (rleaf) {
+          a.nr[dst] = R;
+          if (!qleaf) a.nr[dst + cl] = R;
+        } else {
+          a.nr[dst] = a.R.left[R];
+          a.nr[dst + 1] = a.R.right[R];
+          if (!qleaf) {
+            a.nr[dst + cl] = a.R.left[R];
+            a.nr[dst + cl + 1] = a.R.right[R];
+          }
+        }
+      }
+      runX += tot;
+      int t2;
+      const int pf = warp_excl_scan(kind == kF, lane, t2);
+      if (kind == kF) a.itF[gF + o.f + runF + pf] = Item{ Q, R, order | (kF << 8), rF + runF + pf };
+      runF += t2;
+      const int pd = warp_excl_scan(kind == kD || kind == kT, lane, t2);
+      if (kind == kD || kind == kT)
+        a.itDT[gDT + o.dt + runDT + pd] = Item{ Q, R, order | (kind << 8), rDT + runDT + pd };
+      runDT += t2;
+      const int pb = warp_excl_scan(kind == kB, lane, t2);
+      if (kind == kB) a.itB[gB + o.b + runB + pb] = Item{ Q, R, kB << 8, rB + runB + pb };
+      runB += t2;
+    }
+    if (lane == 0) {
+      a.cntF[Q] = rF + runF;
+      a.cntDT[Q] = rDT + runDT;
+      a.cntB[Q] = rB + runB;
+    }
+  }
+}
+
+struct CntSum {
+  __host__ __device__ Cnt operator()(const Cnt& x, const Cnt& y) const
+  {
+    return Cnt{ x.e + y.e, x.p + y.p, x.f + y.f, x.dt + y.dt, x.t + y.t, x.b + y.b, x.fd + y.fd };
+  }
+};
+
+__global__ void k_scatter_items(const Item* in, int n, const int* noff, Item* out)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const Item it = in[i];
+    out[noff[it.q] + it.rank] = it;
+  }
+}
+
+__global__ void k_mark_moments(const Item* it, int n, int* flag)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int kind = it[i].code >> 8;
+    if (kind == kF || kind == kT) flag[it[i].r] = 1;
+  }
+}
+
+// K2/K3: moments of every reference node some F/T item uses, directly from its
+// contiguous sorted points (equivalent to leaf moments + F2F, engine.cpp:384-399).
+__global__ void k_moments(DevSeries g, TreeView R, int nodes, const int* flag, double s, double* M)
+{
+  extern __shared__ double sm[];
+  for (int n = blockIdx.x; n < nodes; n += gridDim.x) {
+    if (!flag[n]) continue;
+    dev_moments_block(g, R.xs + (size_t)R.begin[n] * g.D, R.count[n], R.cen + (size_t)n * g.D, s,
+                      M + (size_t)n * g.T, sm);
+    __syncthreads();
+  }
+}
+
+// D and T items of one query node, in sorted order (summarize, engine.cpp:212-232).
+__global__ void k_local_items(DevSeries g, TreeView Q, TreeView R, int nodes, const int* cnt,
+                              const int* off, const Item* items, const double* M, double s,
+                              double* L, int* Lord)
+{
+  extern __shared__ double sm[];
+  for (int n = blockIdx.x; n < nodes; n += gridDim.x) {
+    const int c = cnt[n];
+    if (!c) continue;
+    const Item* it = items + off[n];
+    int ord = Lord[n];
+    for (int k = 0; k < c; ++k) {
+      const int kind = it[k].code >> 8, order = it[k].code & 0xff;
+      const int r = it[k].r;
+      if (kind == kD)
+        dev_direct_local_block(g, R.xs + (size_t)R.begin[r] * g.D, R.count[r],
+                               Q.cen + (size_t)n * g.D, s, order, L + (size_t)n * g.T, sm);
+      else
+        dev_f2l_block(g, M + (size_t)r * g.T, R.cen + (size_t)r * g.D, Q.cen + (size_t)n * g.D, s,
+                      order, L + (size_t)n * g.T, sm);
+      ord = max(ord, order);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) Lord[n] = ord;
+  }
+}
+
+// Top-down L2L of one depth level (post_process, engine.cpp:294-304).
+__global__ void k_l2l(DevSeries g, TreeView Q, const int* nodes_at, int m, double s, double* L,
+                      int* Lord)
+{
+  extern __shared__ double sm[];
+  for (int k = blockIdx.x; k < m; k += gridDim.x) {
+    const int n = nodes_at[k];
+    const int order = Lord[n];
+    if (Q.left[n] < 0 || order <= 0) continue;
+    const int ch[2] = { Q.left[n], Q.right[n] };
+    for (int c = 0; c < 2; ++c) {
+      dev_l2l_block(g, L + (size_t)n * g.T, Q.cen + (size_t)n * g.D, Q.cen + (size_t)ch[c] * g.D, s,
+                    order, L + (size_t)ch[c] * g.T, sm);
+      __syncthreads();
+      if (threadIdx.x == 0 && Lord[ch[c]] < order) Lord[ch[c]] = order;
+    }
+  }
+}
+
+// K10: exhaustive base case.  One warp per query leaf, lanes = its queries; the
+// leaf's (query leaf, reference leaf) items stream their reference points as
+// warp-uniform (broadcast) loads.  FP64 libdevice exp (exact to ~1 ulp).
+template <int DT>
+__global__ void __launch_bounds__(kBlock) k_base_case(TreeView Q, TreeView R, int Drt,
+                                                      const int* leaves, int nleaves,
+                                                      const int* cnt, const int* off,
+                                                      const Item* items, double scale,
+                                                      double* s_ex)
+{
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int D = DT ? DT : Drt;
+  for (int li = w0; li < nleaves; li += nw) {
+    const int leaf = leaves[li];
+    const int qb = Q.begin[leaf], qc = Q.count[leaf];
+    const int c = cnt[leaf];
+    const Item* it = items + off[leaf];
+    for (int q0 = 0; q0 < qc; q0 += 32) {
+      const int qi = q0 + lane;
+      const bool act = qi < qc;
+      double q[DT ? DT : kMaxDim];
+#pragma unroll
+      for (int d = 0; d < (DT ? DT : kMaxDim); ++d)
+        if (DT || d < D) q[d] = act ? Q.xs[(size_t)(qb + qi) * D + d] : 0.0;
+      double acc = 0.0;
+      for (int k = 0; k < c; ++k) {
+        const int r = it[k].r;
+        const double* rp = R.xs + (size_t)R.begin[r] * D;
+        const int rc = R.count[r];
+        for (int j = 0; j < rc; ++j) {
+          double d2 = 0.0;
+#pragma unroll
+          for (int d = 0; d < (DT ? DT : kMaxDim); ++d) {
+            if (DT || d < D) {
+              const double t = q[d] - rp[(size_t)j * D + d];
+              d2 += t * t;
+            }
+          }
+          acc += exp(scale * d2);
+        }
+      }
+      if (act) s_ex[qb + qi] = acc;
+    }
+  }
+}
+
+// F items: every query of a leaf evaluates the far-field expansions attached to the
+// leaf or any ancestor (eval_farfield per query, engine.cpp:200-211).
+__global__ void __launch_bounds__(kBlock) k_farfield(DevSeries g, TreeView Q, TreeView R,
+                                                     const int* leaves, int nleaves,
+                                                     const int* cnt, const int* off,
+                                                     const Item* items, const double* M, double s,
+                                                     double* s_ff)
+{
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int D = g.D;
+  for (int li = w0; li < nleaves; li += nw) {
+    const int leaf = leaves[li];
+    const int qb = Q.begin[leaf], qc = Q.count[leaf];
+    for (int q0 = 0; q0 < qc; q0 += 32) {
+      const int qi = q0 + lane;
+      const bool act = qi < qc;
+      const double* qp = Q.xs + (size_t)(qb + (act ? qi : 0)) * D;
+      double acc = 0.0;
+      // root-to-leaf order: collect the ancestor chain (depth <= 64)
+      int chain[64];
+      int depth = 0;
+      for (int n = leaf; n >= 0 && depth < 64; n = Q.parent[n]) chain[depth++] = n;
+      for (int k = depth - 1; k >= 0; --k) {
+        const int n = chain[k];
+        const int c = cnt[n];
+        const Item* it = items + off[n];
+        for (int t = 0; t < c; ++t) {
+          const int r = it[t].r, order = it[t].code & 0xff;
+          acc += dev_eval_farfield(g, M + (size_t)r * g.T, R.cen + (size_t)r * D, qp, s, order);
+        }
+      }
+      if (act) s_ff[qb + qi] = acc;
+    }
+  }
+}
+
+// Local evaluation at the leaves and the final sum (post_process leaf branch and
+// Traversal::run, engine.cpp:273-291, 85-89); results scattered to input order.
+__global__ void k_finalize(DevSeries g, TreeView Q, const int* leaf_of_pos, const int* perm, int n,
+                           const double* L, const int* Lord, const double* s_ex,
+                           const double* s_ff, double s, double* out)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int leaf = leaf_of_pos[i];
+  const int order = Lord[leaf];
+  double loc = 0.0;
+  if (order > 0)
+    loc = dev_eval_local(g, L + (size_t)leaf * g.T, Q.cen + (size_t)leaf * g.D,
+                         Q.xs + (size_t)i * g.D, s, order);
+  out[perm[i]] = loc + s_ff[i] + s_ex[i];
+}
+
+__global__ void k_leaf_of_pos(const int* leaves, int nleaves, const int* begin, const int* count,
+                              int* leaf_of_pos)
+{
+  const int i = blockIdx.x;
+  if (i >= nleaves) return;
+  const int leaf = leaves[i];
+  for (int k = threadIdx.x; k < count[leaf]; k += blockDim.x) leaf_of_pos[begin[leaf] + k] = leaf;
+}
+
+// K11: CV reductions (cv.cpp:17-25, 61-97), deterministic two-stage.
+constexpr int kRedBlocks = 148;
+__global__ void k_cv_partial(const double* sums, const double* conv, int n, double nh, double nc,
+                             double* part)
+{
+  __shared__ double sl[kBlock / 32], ss[kBlock / 32], sc[kBlock / 32];
+  double lk = 0.0, ls = 0.0, cl = 0.0;
+  const int per = (n + gridDim.x - 1) / gridDim.x;
+  const int b = blockIdx.x * per, e = min(n, b + per);
+  for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
+    double loo = sums[i] - 1.0;
+    if (loo <= 0.0) {
+      loo = DBL_MIN;
+      cl += 1.0;
+    }
+    lk += log(loo / nh);
+    if (conv) ls += (conv[i] - 1.0) / nc - 2.0 * ((sums[i] - 1.0) / nh);
+  }
+  lk = warp_sum(lk);
+  ls = warp_sum(ls);
+  cl = warp_sum(cl);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sl[w] = lk;
+    ss[w] = ls;
+    sc[w] = cl;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, b2 = 0, c = 0;
+    for (int k = 0; k < kBlock / 32; ++k) {
+      a += sl[k];
+      b2 += ss[k];
+      c += sc[k];
+    }
+    part[blockIdx.x * 3 + 0] = a;
+    part[blockIdx.x * 3 + 1] = b2;
+    part[blockIdx.x * 3 + 2] = c;
+  }
+}
+
+// K12: exhaustive FP64 sums, 128 queries per block, reference tiles through smem.
+__global__ void k_naive(const double* q, int nq, const double* r, int nr, int D, double scale,
+                        double* out)
+{
+  extern __shared__ double tile[];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double qq[kMaxDim];
+  for (int d = 0; d < D; ++d) qq[d] = i < nq ? q[(size_t)i * D + d] : 0.0;
+  double acc = 0.0;
+  const int TR = 256;
+  for (int b = 0; b < nr; b += TR) {
+    const int m = min(TR, nr - b);
+    __syncthreads();
+    for (int k = threadIdx.x; k < m * D; k += blockDim.x) tile[k] = r[(size_t)b * D + k];
+    __syncthreads();
+    for (int j = 0; j < m; ++j) {
+      double d2 = 0.0;
+      for (int d = 0; d < D; ++d) {
+        const double t = qq[d] - tile[j * D + d];
+        d2 += t * t;
+      }
+      acc += exp(scale * d2);
+    }
+  }
+  if (i < nq) out[i] = acc;
+}
+
+__global__ void k_dfma_peak(double* out, int iters)
+{
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+         a6 = a0 + 6, a7 = a0 + 7;
+  const double m = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+    a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+  }
+  if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == 42.0) out[0] = 1.0;
+}
+
+TreeView view_of(const DevTree& t)
+{
+  return TreeView{ t.lo.p, t.hi.p, t.centroid.p, t.max_side.p, t.left.p, t.right.p,
+                   t.count.p, t.begin.p, t.parent.p, t.xs.p };
+}
+
+int grid_warps(long long work)
+{
+  return (int)std::max<long long>(1, std::min<long long>(kMaxGridBlocks, (work + kWarpsPerBlock - 1) / kWarpsPerBlock));
+}
+
+void launch_classify(int D, int grid, cudaStream_t s, const TravArgs& a)
+{
+  switch (D) {
+  case 1: k_classify<1><<<grid, kBlock, 0, s>>>(a); break;
+  case 2: k_classify<2><<<grid, kBlock, 0, s>>>(a); break;
+  case 3: k_classify<3><<<grid, kBlock, 0, s>>>(a); break;
+  case 4: k_classify<4><<<grid, kBlock, 0, s>>>(a); break;
+  case 5: k_classify<5><<<grid, kBlock, 0, s>>>(a); break;
+  default: k_classify<0><<<grid, kBlock, 0, s>>>(a); break;
+  }
+  CK_LAUNCH();
+}
+
+void launch_base(int D, int grid, cudaStream_t s, TreeView Q, TreeView R, const int* leaves,
+                 int nleaves, const int* cnt, const int* off, const Item* items, double scale,
+                 double* s_ex)
+{
+  switch (D) {
+  case 1: k_base_case<1><<<grid, kBlock, 0, s>>>(Q, R, D, leaves, nleaves, cnt, off, items, scale, s_ex); break;
+  case 2: k_base_case<2><<<grid, kBlock, 0, s>>>(Q, R, D, leaves, nleaves, cnt, off, items, scale, s_ex); break;
+  case 3: k_base_case<3><<<grid, kBlock, 0, s>>>(Q, R, D, leaves, nleaves, cnt, off, items, scale, s_ex); break;
+  case 4: k_base_case<4><<<grid, kBlock, 0, s>>>(Q, R, D, leaves, nleaves, cnt, off, items, scale, s_ex); break;
+  case 5: k_base_case<5><<<grid, kBlock, 0, s>>>(Q, R, D, leaves, nleaves, cnt, off, items, scale, s_ex); break;
+  default: k_base_case<0><<<grid, kBlock, 0, s>>>(Q, R, D, leaves, nleaves, cnt, off, items, scale, s_ex); break;
+  }
+  CK_LAUNCH();
+}
+
+}  // namespace
+
+// ======================================================================= Engine
+
+Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool on_device)
+  : cfg_(cfg)
+{
+  if (n == 0 || d == 0) throw InvalidArgument("PointSet requires N >= 1 and D >= 1");
+  if (n > (size_t)INT32_MAX / 2) throw InvalidArgument("N too large for 32-bit node ids");
+  if (cfg.epsilon < 0.0) throw InvalidArgument("epsilon must be >= 0");
+  if (cfg.leaf_threshold < 1) throw InvalidArgument("leaf_threshold must be >= 1");
+  D_ = (int)d;
+  n_ = n;
+  const int pm = cfg.mode == 0 ? 1 : (cfg.p_max > 0 ? cfg.p_max : default_p_max(D_));
+  if (cfg.p_max < 0 || (cfg.mode == 1 && cfg.p_max > 15)) throw InvalidArgument("SeriesGeometry requires dim >= 1 and 1 <= p_max <= 15");
+  ser_ = SeriesTables(D_, pm);
+  if (D_ > kMaxDim) throw InvalidArgument("dimension > 16 is not supported by the device engine");
+  CK(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
+  for (auto& e : ev_) CK(cudaEventCreate(&e));
+  x_.reserve(n * d);
+  CK(cudaMemcpyAsync(x_.p, refs, sizeof(double) * n * d,
+                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s_));
+  upload_series(ser_, ser_dev_, s_);
+  CK(cudaEventRecord(ev_[0], s_));
+  build_tree(rt_, x_.p, (int)n, D_, cfg.leaf_threshold, s_);
+  CK(cudaEventRecord(ev_[1], s_));
+  CK(cudaStreamSynchronize(s_));
+  CK(cudaEventElapsedTime(&tim_.tree_ms, ev_[0], ev_[1]));
+  dstat_.reserve(4);
+}
+
+Engine::~Engine()
+{
+  if (s_) cudaStreamSynchronize(s_);
+  for (auto& e : ev_) cudaEventDestroy(e);
+  if (s_) cudaStreamDestroy(s_);
+}
+
+DevSeries Engine::dev_series() const { return series_view(ser_, ser_dev_); }
+
+void upload_series(const SeriesTables& t, DevBuf<unsigned char>& dev, cudaStream_t s)
+{
+  const int T = t.T;
+  const size_t bytes = sizeof(uint64_t) * T + sizeof(double) * 2 * T + sizeof(int) * 2 * T;
+  dev.reserve(bytes);
+  std::vector<unsigned char> blob(bytes);
+  unsigned char* p = blob.data();
+  std::memcpy(p, t.dig.data(), sizeof(uint64_t) * T);
+  p += sizeof(uint64_t) * T;
+  std::memcpy(p, t.invf.data(), sizeof(double) * T);
+  p += sizeof(double) * T;
+  std::memcpy(p, t.fact.data(), sizeof(double) * T);
+  p += sizeof(double) * T;
+  std::memcpy(p, t.degree.data(), sizeof(int) * T);
+  p += sizeof(int) * T;
+  std::memcpy(p, t.term_of_pos.data(), sizeof(int) * T);
+  CK(cudaMemcpyAsync(dev.p, blob.data(), bytes, cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+}
+
+DevSeries series_view(const SeriesTables& t, const DevBuf<unsigned char>& dev)
+{
+  const int T = t.T;
+  const unsigned char* p = dev.p;
+  DevSeries g;
+  g.D = t.D;
+  g.pmax = t.pmax;
+  g.T = T;
+  g.dig = (const uint64_t*)p;
+  p += sizeof(uint64_t) * T;
+  g.invf = (const double*)p;
+  p += sizeof(double) * T;
+  g.fact = (const double*)p;
+  p += sizeof(double) * T;
+  g.degree = (const int*)p;
+  p += sizeof(int) * T;
+  g.term_of_pos = (const int*)p;
+  return g;
+}
+
+void Engine::traverse(const DevTree& qt, double h)
+{
+  const int K = qt.nodes;
+  const int T = ser_.T;
+  cudaStream_t s = s_;
+  L_.reserve((size_t)K * T);
+  CK(cudaMemsetAsync(L_.p, 0, sizeof(double) * K * T, s));
+  for (DevBuf<int>* b : { &Lord_, &cntF_, &cntDT_, &cntB_ }) {
+    b->reserve(K);
+    CK(cudaMemsetAsync(b->p, 0, sizeof(int) * K, s));
+  }
+  CK(cudaMemsetAsync(dstat_.p, 0, sizeof(unsigned long long), s));
+
+  // initial frontier: (Q root, R root)
+  int cur = 0;
+  fq_[0].reserve(1); foff_[0].reserve(1); flen_[0].reserve(1); fbase_[0].reserve(1); fr_[0].reserve(1);
+  const int zero = 0, one = 1;
+  const double dz = 0.0;
+  CK(cudaMemcpyAsync(fq_[0].p, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(foff_[0].p, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(flen_[0].p, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(fbase_[0].p, &dz, sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(fr_[0].p, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+  int m = 1;
+  long long npairs = 1;
+  nF_ = nDT_ = nB_ = 0;
+  stats_ = Stats{};
+
+  TravArgs a{};
+  a.Q = view_of(qt);
+  a.R = view_of(rt_);
+  a.D = D_;
+  a.pmax = ser_.pmax;
+  a.cost = cfg_.cost_model;
+  a.series = cfg_.mode == 1;
+  a.h = h;
+  a.scale = -1.0 / (2.0 * h * h);
+  a.eps = cfg_.epsilon;
+  a.ntot = (double)n_;
+  a.L = L_.p;
+  a.T = T;
+  a.Lord = Lord_.p;
+  a.kevals = dstat_.p;
+  a.cntF = cntF_.p;
+  a.cntDT = cntDT_.p;
+  a.cntB = cntB_.p;
+
+  size_t scan_bytes = 0;
+  Cnt hc{};
+  while (m > 0) {
+    ++stats_.levels;
+    stats_.pairs_visited += npairs;
+    pkmax_.reserve(npairs);
+    pkmin_.reserve(npairs);
+    dec_.reserve(npairs);
+    cnt_.reserve((size_t)m + 1);
+    cntoff_.reserve((size_t)m + 1);
+    childlen_.reserve(m);
+    newbase_.reserve(m);
+    a.m = m;
+    a.fq = fq_[cur].p;
+    a.foff = foff_[cur].p;
+    a.flen = flen_[cur].p;
+    a.fr = fr_[cur].p;
+    a.fbase = fbase_[cur].p;
+    a.pkmax = pkmax_.p;
+    a.pkmin = pkmin_.p;
+    a.dec = dec_.p;
+    a.cnt = cnt_.p;
+    a.childlen = childlen_.p;
+    a.newbase = newbase_.p;
+    const int grid = grid_warps(m);
+    launch_classify(D_, grid, s, a);
+    // exclusive scan of per-entry counts (m+1 entries, last = totals)
+    CK(cudaMemsetAsync(cnt_.p + m, 0, sizeof(Cnt), s));
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveScan(nullptr, need, cnt_.p, cntoff_.p, CntSum(), Cnt{}, m + 1, s);
+    if (need > scan_bytes || !scan_tmp_.p) {
+      scan_tmp_.reserve(need + 256);
+      scan_bytes = scan_tmp_.cap;
+    }
+    size_t have = scan_tmp_.cap;
+    cub::DeviceScan::ExclusiveScan(scan_tmp_.p, have, cnt_.p, cntoff_.p, CntSum(), Cnt{}, m + 1, s);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(&hc, cntoff_.p + m, sizeof(Cnt), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if ((long long)hc.p > INT32_MAX / 2) throw OutOfMemory("frontier exceeds 2^30 pairs");
+    stats_.prunes_finite_diff += hc.fd;
+    stats_.prunes_farfield += hc.f;
+    stats_.prunes_direct_local += hc.dt - hc.t;
+    stats_.prunes_far_to_local += hc.t;
+    stats_.base_cases += hc.b;
+    // room for the next frontier and this level's items (keep earlier items)
+    const int nxt = cur ^ 1;
+    fq_[nxt].reserve(std::max(hc.e, 1));
+    foff_[nxt].reserve(std::max(hc.e, 1));
+    flen_[nxt].reserve(std::max(hc.e, 1));
+    fbase_[nxt].reserve(std::max(hc.e, 1));
+    fr_[nxt].reserve(std::max(hc.p, 1));
+    itF_.grow_keep(nF_ + hc.f + 1, nF_, s);
+    itDT_.grow_keep(nDT_ + hc.dt + 1, nDT_, s);
+    itB_.grow_keep(nB_ + hc.b + 1, nB_, s);
+    a.cntoff = cntoff_.p;
+    a.nq = fq_[nxt].p;
+    a.noff = foff_[nxt].p;
+    a.nlen = flen_[nxt].p;
+    a.nr = fr_[nxt].p;
+    a.nbase = fbase_[nxt].p;
+    a.itF = itF_.p;
+    a.itDT = itDT_.p;
+    a.itB = itB_.p;
+    k_emit<<<grid, kBlock, 0, s>>>(a, (int)nF_, (int)nDT_, (int)nB_);
+    CK_LAUNCH();
+    nF_ += hc.f;
+    nDT_ += hc.dt;
+    nB_ += hc.b;
+    m = hc.e;
+    npairs = hc.p;
+    cur = nxt;
+  }
+  unsigned long long kev = 0;
+  CK(cudaMemcpyAsync(&kev, dstat_.p, sizeof(kev), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  stats_.kernel_evaluations = 2ull * stats_.pairs_visited + kev;
+
+  // counting sort of the items by query node (stable: level order, then emit order)
+  auto sort_items = [&](DevBuf<Item>& in, long long nitems, DevBuf<int>& cnt, DevBuf<int>& off,
+                        DevBuf<Item>& out) {
+    off.reserve((size_t)K + 1);
+    if (nitems == 0) return;
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, cnt.p, off.p, K, s);
+    scan_tmp_.reserve(need + 256);
+    size_t have = scan_tmp_.cap;
+    cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, cnt.p, off.p, K, s);
+    out.reserve(nitems);
+    k_scatter_items<<<ceil_div(nitems, 256), 256, 0, s>>>(in.p, (int)nitems, off.p, out.p);
+    CK_LAUNCH();
+  };
+  sort_items(itF_, nF_, cntF_, offF_, sF_);
+  sort_items(itDT_, nDT_, cntDT_, offDT_, sDT_);
+  sort_items(itB_, nB_, cntB_, offB_, sB_);
+}
+
+void Engine::run_phases(const DevTree& qt, double h, double* d_out)
+{
+  cudaStream_t s = s_;
+  const DevSeries g = dev_series();
+  const double sc = inv_scale(h);
+  const TreeView Q = view_of(qt), R = view_of(rt_);
+  const int K = qt.nodes;
+  CK(cudaEventRecord(ev_[2], s));
+  traverse(qt, h);
+  CK(cudaEventRecord(ev_[3], s));
+  // moments of the reference nodes used by F/T items
+  const bool need_m = stats_.prunes_farfield + stats_.prunes_far_to_local > 0;
+  if (need_m) {
+    mflag_.reserve(rt_.nodes);
+    CK(cudaMemsetAsync(mflag_.p, 0, sizeof(int) * rt_.nodes, s));
+    if (nF_) k_mark_moments<<<ceil_div(nF_, 256), 256, 0, s>>>(sF_.p, (int)nF_, mflag_.p);
+    if (nDT_) k_mark_moments<<<ceil_div(nDT_, 256), 256, 0, s>>>(sDT_.p, (int)nDT_, mflag_.p);
+    M_.reserve((size_t)rt_.nodes * ser_.T);
+    const int smem = 32 * D_ * ser_.pmax * (int)sizeof(double);
+    k_moments<<<std::min(rt_.nodes, 148 * 8), 128, smem, s>>>(g, R, rt_.nodes, mflag_.p, sc, M_.p);
+    CK_LAUNCH();
+  }
+  CK(cudaEventRecord(ev_[4], s));
+  // D/T items, then L2L down the query tree
+  if (nDT_) {
+    const int smem = std::max(32 * D_ * ser_.pmax, D_ * (2 * ser_.pmax)) * (int)sizeof(double);
+    k_local_items<<<std::min(K, 148 * 8), 128, smem, s>>>(g, Q, R, K, cntDT_.p, offDT_.p, sDT_.p,
+                                                           M_.p, sc, L_.p, Lord_.p);
+    CK_LAUNCH();
+  }
+  if (stats_.prunes_finite_diff + stats_.prunes_direct_local + stats_.prunes_far_to_local > 0) {
+    const int smem = D_ * ser_.pmax * (int)sizeof(double);
+    for (int d = 0; d + 1 < qt.height; ++d) {
+      const int b = qt.depth_off[d], e = qt.depth_off[d + 1];
+      k_l2l<<<std::min(e - b, 148 * 8), 64, smem, s>>>(g, Q, qt.by_depth.p + b, e - b, sc, L_.p,
+                                                       Lord_.p);
+    }
+    CK_LAUNCH();
+  }
+  CK(cudaEventRecord(ev_[5], s));
+  // base cases (dominant kernel)
+  s_ex_.reserve(qt.n);
+  s_ff_.reserve(qt.n);
+  const int nleaves = (int)qleaves_host_.size();
+  launch_base(D_, grid_warps(nleaves), s, Q, R, leaves_.p, nleaves, cntB_.p, offB_.p, sB_.p,
+              -1.0 / (2.0 * h * h), s_ex_.p);
+  CK(cudaEventRecord(ev_[6], s));
+  if (nF_) {
+    k_farfield<<<grid_warps(nleaves), kBlock, 0, s>>>(g, Q, R, leaves_.p, nleaves, cntF_.p, offF_.p,
+                                                     sF_.p, M_.p, sc, s_ff_.p);
+    CK_LAUNCH();
+  } else {
+    CK(cudaMemsetAsync(s_ff_.p, 0, sizeof(double) * qt.n, s));
+  }
+  CK(cudaEventRecord(ev_[7], s));
+  k_finalize<<<ceil_div(qt.n, 128), 128, 0, s>>>(g, Q, leaf_of_pos_.p, qt.perm.p, qt.n, L_.p,
+                                                 Lord_.p, s_ex_.p, s_ff_.p, sc, d_out);
+  CK_LAUNCH();
+  CK(cudaEventRecord(ev_[8], s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaEventElapsedTime(&tim_.traverse_ms, ev_[2], ev_[3]));
+  CK(cudaEventElapsedTime(&tim_.moments_ms, ev_[3], ev_[4]));
+  CK(cudaEventElapsedTime(&tim_.local_ms, ev_[4], ev_[5]));
+  CK(cudaEventElapsedTime(&tim_.base_ms, ev_[5], ev_[6]));
+  CK(cudaEventElapsedTime(&tim_.farfield_ms, ev_[6], ev_[7]));
+  CK(cudaEventElapsedTime(&tim_.final_ms, ev_[7], ev_[8]));
+  CK(cudaEventElapsedTime(&tim_.total_ms, ev_[2], ev_[8]));
+}
+
+static void setup_leaves(const DevTree& t, DevBuf<int>& leaves, DevBuf<int>& leaf_of_pos,
+                         std::vector<int>& host, cudaStream_t s)
+{
+  host.clear();
+  for (int i = 0; i < t.nodes; ++i)
+    if (t.h_left[i] < 0) host.push_back(i);
+  leaves.reserve(host.size());
+  CK(cudaMemcpyAsync(leaves.p, host.data(), sizeof(int) * host.size(), cudaMemcpyHostToDevice, s));
+  leaf_of_pos.reserve(t.n);
+  k_leaf_of_pos<<<(int)host.size(), 64, 0, s>>>(leaves.p, (int)host.size(), t.begin.p, t.count.p,
+                                                leaf_of_pos.p);
+  CK_LAUNCH();
+  CK(cudaStreamSynchronize(s));
+}
+
+void Engine::compute_device(const double* d_queries, size_t nq, double h, double* d_out)
+{
+  if (!(h > 0.0)) throw InvalidArgument("bandwidth must be positive");
+  if (!std::isfinite(h)) throw InvalidArgument("bandwidth must be positive and finite");
+  const DevTree* qt = &rt_;
+  if (d_queries) {
+    if (nq == 0) throw InvalidArgument("PointSet requires N >= 1 and D >= 1");
+    cudaEvent_t a = ev_[0], b = ev_[1];
+    CK(cudaEventRecord(a, s_));
+    build_tree(qt_tmp_, d_queries, (int)nq, D_, cfg_.leaf_threshold, s_);  // engine.cpp:417
+    CK(cudaEventRecord(b, s_));
+    qt = &qt_tmp_;
+    setup_leaves(*qt, leaves_, leaf_of_pos_, qleaves_host_, s_);
+  } else if (leaves_src_ != 0) {
+    setup_leaves(rt_, leaves_, leaf_of_pos_, qleaves_host_, s_);
+  }
+  leaves_src_ = d_queries == nullptr ? 0 : 1;
+  run_phases(*qt, h, d_out);
+}
+
+void Engine::compute_host(const double* h_queries, size_t nq, double h, double* h_out)
+{
+  const size_t n_out = h_queries ? nq : n_;
+  DevBuf<double> out;
+  out.reserve(n_out);
+  if (h_queries) {
+    qx_.reserve(nq * D_);
+    CK(cudaMemcpyAsync(qx_.p, h_queries, sizeof(double) * nq * D_, cudaMemcpyHostToDevice, s_));
+  }
+  compute_device(h_queries ? qx_.p : nullptr, nq, h, out.p);
+  CK(cudaMemcpyAsync(h_out, out.p, sizeof(double) * n_out, cudaMemcpyDeviceToHost, s_));
+  CK(cudaStreamSynchronize(s_));
+}
+
+void Engine::cv_reduce(const double* d_sums, double h, const double* d_conv, double conv_h,
+                       double* lk, int* clamped, double* ls)
+{
+  const size_t n = n_;
+  if (n < 2) throw InvalidArgument("CV requires at least 2 points");
+  const double two_pi = 6.283185307179586476925286766559;
+  const double nh = (double)(n - 1) * std::pow(two_pi * h * h, 0.5 * D_);
+  const double nc = d_conv ? (double)(n - 1) * std::pow(two_pi * conv_h * conv_h, 0.5 * D_) : 1.0;
+  red_.reserve(kRedBlocks * 3);
+  k_cv_partial<<<kRedBlocks, kBlock, 0, s_>>>(d_sums, d_conv, (int)n, nh, nc, red_.p);
+  CK_LAUNCH();
+  std::vector<double> part(kRedBlocks * 3);
+  CK(cudaMemcpyAsync(part.data(), red_.p, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, s_));
+  CK(cudaStreamSynchronize(s_));
+  double a = 0, b = 0, c = 0;
+  for (int k = 0; k < kRedBlocks; ++k) {
+    a += part[k * 3];
+    b += part[k * 3 + 1];
+    c += part[k * 3 + 2];
+  }
+  if (lk) *lk = a / (double)n;
+  if (clamped) *clamped = (int)c;
+  if (ls) *ls = b / (double)n;
+}
+
+void naive_device(const double* d_q, size_t nq, const double* d_r, size_t nr, int D, double h,
+                  double* d_out, cudaStream_t s)
+{
+  const int TR = 256;
+  k_naive<<<ceil_div(nq, 128), 128, TR * D * sizeof(double), s>>>(d_q, (int)nq, d_r, (int)nr, D,
+                                                                 -1.0 / (2.0 * h * h), d_out);
+  CK_LAUNCH();
+}
+
+double measure_dfma_peak(int device)
+{
+  cudaDeviceProp p{};
+  CK(cudaGetDeviceProperties(&p, device));
+  DevBuf<double> o;
+  o.reserve(1);
+  const int blocks = p.multiProcessorCount * 8, threads = 256, iters = 4096;
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  k_dfma_peak<<<blocks, threads>>>(o.p, 64);
+  CK(cudaEventRecord(a));
+  k_dfma_peak<<<blocks, threads>>>(o.p, iters);
+  CK(cudaEventRecord(b));
+  CK(cudaEventSynchronize(b));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return (double)blocks * threads * iters * 8.0 / (ms * 1e-3);
+}
+
+}  // namespace dfgtb

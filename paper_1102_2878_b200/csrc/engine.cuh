@@ -1,0 +1,120 @@
+// DFGT engine: level-synchronous dual-tree traversal + series/base-case kernels.
+#pragma once
+
+#include "series.cuh"
+#include "tree.cuh"
+
+#include <memory>
+
+namespace dfgtb {
+
+struct Config {
+  double epsilon = 0.01;
+  int leaf_threshold = 20;   // reference default (engine.hpp:19)
+  int p_max = 0;             // 0 -> default_p_max(D)
+  int cost_model = 0;        // 0 exponential, 1 term_count (truncation.hpp:216)
+  int mode = 1;              // 0 centroid (DFD), 1 series (DFGT)
+};
+
+// Mirrors TraversalStats (engine.hpp:66-74).
+struct Stats {
+  unsigned long long kernel_evaluations = 0, pairs_visited = 0, base_cases = 0,
+                     prunes_finite_diff = 0, prunes_farfield = 0, prunes_direct_local = 0,
+                     prunes_far_to_local = 0;
+  int levels = 0;
+};
+
+// Device milliseconds of the last compute(), per phase (CUDA events on the engine stream).
+struct Timings {
+  float tree_ms = 0, traverse_ms = 0, moments_ms = 0, local_ms = 0, base_ms = 0, farfield_ms = 0,
+        final_ms = 0, total_ms = 0;
+};
+
+struct Cnt {
+  int e, p, f, dt, t, b, fd;
+};
+
+struct Item {
+  int q, r, code, rank;  // code: order | kind << 8 (kind 1 F, 2 D, 3 T, 4 base)
+};
+
+int default_p_max(int D);
+
+class Engine {
+public:
+  Engine(const double* h_refs, size_t n, size_t d, const Config& cfg, bool refs_on_device = false);
+  ~Engine();
+
+  // Sums for queries (device pointer, nq x D row-major; nullptr -> Q = R) written
+  // to d_out (device, nq, original query order).
+  void compute_device(const double* d_queries, size_t nq, double h, double* d_out);
+  // Host-buffer convenience used by the C-ABI.
+  void compute_host(const double* h_queries, size_t nq, double h, double* h_out);
+
+  // CV reductions of Q = R sums already on device (lk: log LOO mean, clamps; ls).
+  void cv_reduce(const double* d_sums, double h, const double* d_conv, double conv_h,
+                 double* lk, int* clamped, double* ls);
+
+  const Stats& last_stats() const { return stats_; }
+  const Timings& last_timings() const { return tim_; }
+  const DevTree& ref_tree() const { return rt_; }
+  int p_max() const { return ser_.pmax; }
+  int dim() const { return D_; }
+  size_t n() const { return n_; }
+  cudaStream_t stream() const { return s_; }
+  const SeriesTables& series() const { return ser_; }
+  DevSeries dev_series() const;
+  const double* d_refs() const { return x_.p; }
+  // base-case kernel time of the last compute (ms) and its algorithmic pair count
+  float base_kernel_ms() const { return tim_.base_ms; }
+
+private:
+  void traverse(const DevTree& qt, double h);
+  void run_phases(const DevTree& qt, double h, double* d_out);
+
+  Config cfg_;
+  int D_ = 0;
+  size_t n_ = 0;
+  cudaStream_t s_ = nullptr;
+  DevBuf<double> x_;        // reference points (original order)
+  DevTree rt_;              // reference tree
+  DevTree qt_tmp_;          // query tree (Q != R)
+  DevBuf<double> qx_;       // query points (Q != R)
+  SeriesTables ser_;
+  DevBuf<unsigned char> ser_dev_;
+  DevBuf<int> leaves_, leaf_of_pos_;       // per current query tree
+  DevBuf<int> rleaves_;
+  // per-compute state
+  DevBuf<double> L_, M_, s_ex_, s_ff_;
+  DevBuf<int> Lord_, cntF_, cntDT_, cntB_, offF_, offDT_, offB_, mflag_;
+  // frontier (double buffered) and per-level scratch
+  DevBuf<int> fq_[2], foff_[2], flen_[2], fr_[2];
+  DevBuf<double> fbase_[2];
+  DevBuf<double> pkmax_, pkmin_;
+  DevBuf<int> dec_, childlen_;
+  DevBuf<double> newbase_;
+  DevBuf<Cnt> cnt_, cntoff_;
+  DevBuf<Item> itF_, itDT_, itB_, sF_, sDT_, sB_;
+  DevBuf<unsigned char> scan_tmp_;
+  DevBuf<unsigned long long> dstat_;
+  DevBuf<double> red_;
+  cudaEvent_t ev_[10];
+  Stats stats_;
+  Timings tim_;
+  long long nF_ = 0, nDT_ = 0, nB_ = 0;
+  std::vector<int> qleaves_host_;
+  int leaves_src_ = -1;  // 0: leaves_ describe the reference tree, 1: a query tree
+};
+
+// Exhaustive FP64 sums on the device (K12, naive_kde engine.cpp:22-36).
+void naive_device(const double* d_q, size_t nq, const double* d_r, size_t nr, int D, double h,
+                  double* d_out, cudaStream_t s);
+
+// Measured FP64 FMA throughput (instr/s) -- roofline denominator for bench.py.
+double measure_dfma_peak(int device);
+
+// Series term tables -> one device blob, and the device view over it.
+void upload_series(const SeriesTables& t, DevBuf<unsigned char>& dev, cudaStream_t s);
+DevSeries series_view(const SeriesTables& t, const DevBuf<unsigned char>& dev);
+
+}  // namespace dfgtb

@@ -1,0 +1,553 @@
+// Level-synchronous, bit-exact GPU build of the reference kd-tree.
+//
+// Reference: KdTree::build (kdtree.cpp:21-109).  Per level, for every node of the
+// level at once:
+//   1. bounds    : exact min/max per dimension over the node's points (ordered-key
+//                  atomics, order independent);  centroid = 0.5*(lo+hi);
+//                  widest = first dimension of maximal width (kdtree.cpp:49-71)
+//   2. partition : std::partition(x[widest] <= mid) reproduced exactly.  libstdc++'s
+//                  bidirectional __partition swaps the k-th failing element of the
+//                  final left block with the k-th passing element (counted from the
+//                  right) of the final right block; everything else stays.  A
+//                  global prefix scan of the predicate gives both ranks directly.
+//   3. fallback  : one-sided splits run a single-thread device restatement of
+//                  libstdc++ 13's std::nth_element / __introselect (kdtree.cpp:85-94)
+//                  on the node's segment; these nodes are rare (duplicates).
+// Nodes are numbered in BFS order while building and renumbered to the reference's
+// preorder ids at the end.
+#include "tree.cuh"
+
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <numeric>
+
+namespace dfgtb {
+namespace {
+
+constexpr int kTile = 1024;
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ unsigned long long dkey(double v)
+{
+  if (v == 0.0) v = 0.0;  // canonical +0 (reference compares with <, so +-0 tie)
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dkey_inv(unsigned long long k)
+{
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+struct LevelArgs {
+  const double* x;     // original coordinates (row-major)
+  int D;
+  int* perm;
+  const int* nbeg;     // per level node: begin
+  const int* ncnt;     // per level node: count
+  const int* tile_node;   // per tile: level-node index
+  const int* tile_start;  // per tile: first sorted position
+  unsigned long long* kmin;  // per level node * D
+  unsigned long long* kmax;
+};
+
+__global__ void k_bounds_init(unsigned long long* kmin, unsigned long long* kmax, int m)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) {
+    kmin[i] = ~0ull;
+    kmax[i] = 0ull;
+  }
+}
+
+// One CTA per tile of <= kTile points of one node.
+__global__ void k_bounds_tiles(LevelArgs a)
+{
+  const int tile = blockIdx.x;
+  const int j = a.tile_node[tile];
+  const int start = a.tile_start[tile];
+  const int end = min(a.nbeg[j] + a.ncnt[j], start + kTile);
+  const int D = a.D;
+  for (int d = 0; d < D; ++d) {
+    unsigned long long mn = ~0ull, mx = 0ull;
+    for (int i = start + threadIdx.x; i < end; i += blockDim.x) {
+      const unsigned long long k = dkey(a.x[(size_t)a.perm[i] * D + d]);
+      mn = min(mn, k);
+      mx = max(mx, k);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&a.kmin[(size_t)j * D + d], mn);
+      atomicMax(&a.kmax[(size_t)j * D + d], mx);
+    }
+  }
+}
+
+// Per level node: bounds, centroid, widest side, split midpoint (kdtree.cpp:49-78).
+__global__ void k_decide(LevelArgs a, int m, int leaf, int base, double* lo, double* hi,
+                         double* centroid, double* max_side, int* split_dim, double* mid_out,
+                         int* do_split)
+{
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const int D = a.D;
+  const size_t o = (size_t)(base + j) * D;
+  int widest = 0;
+  double width = 0.0;
+  for (int d = 0; d < D; ++d) {
+    const double l = dkey_inv(a.kmin[(size_t)j * D + d]);
+    const double h = dkey_inv(a.kmax[(size_t)j * D + d]);
+    lo[o + d] = l;
+    hi[o + d] = h;
+    centroid[o + d] = __dmul_rn(0.5, __dadd_rn(l, h));
+    const double w = __dadd_rn(h, -l);
+    if (d == 0 || w > width) {
+      width = w;
+      widest = d;
+    }
+  }
+  max_side[base + j] = width;
+  const int split = a.ncnt[j] > leaf;
+  do_split[j] = split;
+  split_dim[base + j] = split ? widest : -1;
+  mid_out[j] = centroid[o + widest];  // 0.5*(lo+hi) of the widest dimension
+}
+
+// Predicate flags for every position of a splitting node.
+__global__ void k_flags(LevelArgs a, const int* do_split, const int* split_dim_lvl,
+                        const double* mid, int* flag)
+{
+  const int tile = blockIdx.x;
+  const int j = a.tile_node[tile];
+  if (!do_split[j]) return;
+  const int start = a.tile_start[tile];
+  const int end = min(a.nbeg[j] + a.ncnt[j], start + kTile);
+  const int w = split_dim_lvl[j];
+  const double m = mid[j];
+  for (int i = start + threadIdx.x; i < end; i += blockDim.x)
+    flag[i] = a.x[(size_t)a.perm[i] * a.D + w] <= m ? 1 : 0;
+}
+
+// Right-block passers register at slot (begin + rank-from-right).
+__global__ void k_slots(LevelArgs a, const int* do_split, const int* flag, const int* P,
+                        int* slot)
+{
+  const int tile = blockIdx.x;
+  const int j = a.tile_node[tile];
+  if (!do_split[j]) return;
+  const int b = a.nbeg[j], e = b + a.ncnt[j];
+  const int start = a.tile_start[tile];
+  const int end = min(e, start + kTile);
+  const int L = P[e] - P[b];
+  for (int i = start + threadIdx.x; i < end; i += blockDim.x)
+    if (i >= b + L && flag[i]) slot[b + (P[e] - P[i] - 1)] = i;
+}
+
+// Left-block failers swap with their partner (disjoint pairs -> race free).
+__global__ void k_swap(LevelArgs a, const int* do_split, const int* flag, const int* P,
+                       const int* slot)
+{
+  const int tile = blockIdx.x;
+  const int j = a.tile_node[tile];
+  if (!do_split[j]) return;
+  const int b = a.nbeg[j], e = b + a.ncnt[j];
+  const int start = a.tile_start[tile];
+  const int end = min(e, start + kTile);
+  const int L = P[e] - P[b];
+  for (int i = start + threadIdx.x; i < end && i < b + L; i += blockDim.x) {
+    if (!flag[i]) {
+      const int k = (i - b) - (P[i] - P[b]);
+      const int partner = slot[b + k];
+      const int t = a.perm[i];
+      a.perm[i] = a.perm[partner];
+      a.perm[partner] = t;
+    }
+  }
+}
+
+// ---- single-thread restatement of libstdc++ 13 nth_element (stl_algo.h) ----
+struct KeyCmp {
+  const double* x;
+  int D, w;
+  __device__ double key(int idx) const { return x[(size_t)idx * D + w]; }
+  __device__ bool operator()(int a, int b) const { return key(a) < key(b); }
+};
+
+__device__ void dswap(int* a, int* b)
+{
+  const int t = *a;
+  *a = *b;
+  *b = t;
+}
+
+__device__ void dev_median_to_first(int* res, int* a, int* b, int* c, const KeyCmp& cmp)
+{
+  if (cmp(*a, *b)) {
+    if (cmp(*b, *c)) dswap(res, b);
+    else if (cmp(*a, *c)) dswap(res, c);
+    else dswap(res, a);
+  } else if (cmp(*a, *c)) dswap(res, a);
+  else if (cmp(*b, *c)) dswap(res, c);
+  else dswap(res, b);
+}
+
+__device__ int* dev_unguarded_partition(int* first, int* last, int* pivot, const KeyCmp& cmp)
+{
+  for (;;) {
+    while (cmp(*first, *pivot)) ++first;
+    --last;
+    while (cmp(*pivot, *last)) --last;
+    if (!(first < last)) return first;
+    dswap(first, last);
+    ++first;
+  }
+}
+
+__device__ void dev_insertion_sort(int* first, int* last, const KeyCmp& cmp)
+{
+  if (first == last) return;
+  for (int* i = first + 1; i != last; ++i) {
+    const int v = *i;
+    if (cmp(v, *first)) {
+      for (int* p = i; p != first; --p) *p = *(p - 1);
+      *first = v;
+    } else {
+      int* l = i;
+      int* nx = i - 1;
+      while (cmp(v, *nx)) {
+        *l = *nx;
+        l = nx;
+        --nx;
+      }
+      *l = v;
+    }
+  }
+}
+
+__device__ void dev_push_heap(int* first, long hole, long top, int v, const KeyCmp& cmp)
+{
+  long parent = (hole - 1) / 2;
+  while (hole > top && cmp(first[parent], v)) {
+    first[hole] = first[parent];
+    hole = parent;
+    parent = (hole - 1) / 2;
+  }
+  first[hole] = v;
+}
+
+__device__ void dev_adjust_heap(int* first, long hole, long len, int v, const KeyCmp& cmp)
+{
+  const long top = hole;
+  long second = hole;
+  while (second < (len - 1) / 2) {
+    second = 2 * (second + 1);
+    if (cmp(first[second], first[second - 1])) second--;
+    first[hole] = first[second];
+    hole = second;
+  }
+  if ((len & 1) == 0 && second == (len - 2) / 2) {
+    second = 2 * (second + 1);
+    first[hole] = first[second - 1];
+    hole = second - 1;
+  }
+  dev_push_heap(first, hole, top, v, cmp);
+}
+
+__device__ void dev_heap_select(int* first, int* middle, int* last, const KeyCmp& cmp)
+{
+  const long len = middle - first;
+  if (len >= 2) {
+    long parent = (len - 2) / 2;
+    for (;;) {
+      dev_adjust_heap(first, parent, len, first[parent], cmp);
+      if (parent == 0) break;
+      parent--;
+    }
+  }
+  for (int* i = middle; i < last; ++i) {
+    if (cmp(*i, *first)) {
+      const int v = *i;
+      *i = *first;
+      dev_adjust_heap(first, 0, len, v, cmp);
+    }
+  }
+}
+
+__device__ void dev_nth_element(int* first, int* nth, int* last, const KeyCmp& cmp)
+{
+  if (first == last || nth == last) return;
+  long n = last - first;
+  int lg = 0;
+  while (n > 1) {
+    n >>= 1;
+    ++lg;
+  }
+  long depth = 2L * lg;
+  while (last - first > 3) {
+    if (depth == 0) {
+      dev_heap_select(first, nth + 1, last, cmp);
+      dswap(first, nth);
+      return;
+    }
+    --depth;
+    int* mid = first + (last - first) / 2;
+    dev_median_to_first(first, first + 1, mid, last - 1, cmp);
+    int* cut = dev_unguarded_partition(first + 1, last, first, cmp);
+    if (cut <= nth) first = cut;
+    else last = cut;
+  }
+  dev_insertion_sort(first, last, cmp);
+}
+
+// One thread per splitting node: final left count / split coordinate, running the
+// median fallback when the midpoint split is one-sided (kdtree.cpp:85-94).
+__global__ void k_finish_split(LevelArgs a, int m, int base, const int* do_split,
+                               const int* split_dim_lvl, const double* mid, const int* P,
+                               int* left_count, double* split_coord)
+{
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  if (!do_split[j]) {
+    left_count[j] = 0;
+    split_coord[base + j] = 0.0;
+    return;
+  }
+  const int b = a.nbeg[j], c = a.ncnt[j];
+  const int L = P[b + c] - P[b];
+  if (L == 0 || L == c) {
+    KeyCmp cmp{ a.x, a.D, split_dim_lvl[j] };
+    int* p0 = a.perm + b;
+    dev_nth_element(p0, p0 + c / 2, p0 + c, cmp);
+    left_count[j] = c / 2;
+    split_coord[base + j] = cmp.key(p0[c / 2]);
+  } else {
+    left_count[j] = L;
+    split_coord[base + j] = mid[j];
+  }
+}
+
+// Scatter BFS-indexed build arrays into preorder-indexed tree arrays.
+__global__ void k_to_preorder(int K, int D, const int* bfs2pre, const double* blo,
+                              const double* bhi, const double* bcen, const double* bside,
+                              const double* bsc, const int* bsd, const int* bleft,
+                              const int* bright, const int* bbeg, const int* bcnt,
+                              const int* bpar, const int* bdep, double* lo, double* hi,
+                              double* cen, double* side, double* sc, int* sd, int* left,
+                              int* right, int* beg, int* cnt, int* par, int* dep, int* by_depth)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= K) return;
+  const int p = bfs2pre[i];
+  for (int d = 0; d < D; ++d) {
+    lo[(size_t)p * D + d] = blo[(size_t)i * D + d];
+    hi[(size_t)p * D + d] = bhi[(size_t)i * D + d];
+    cen[(size_t)p * D + d] = bcen[(size_t)i * D + d];
+  }
+  side[p] = bside[i];
+  sc[p] = bsc[i];
+  sd[p] = bsd[i];
+  left[p] = bleft[i] < 0 ? -1 : bfs2pre[bleft[i]];
+  right[p] = bright[i] < 0 ? -1 : bfs2pre[bright[i]];
+  beg[p] = bbeg[i];
+  cnt[p] = bcnt[i];
+  par[p] = bpar[i] < 0 ? -1 : bfs2pre[bpar[i]];
+  dep[p] = bdep[i];
+  by_depth[i] = p;
+}
+
+__global__ void k_gather_points(const double* x, const int* perm, int n, int D, double* xs)
+{
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (size_t)n * D) return;
+  const size_t r = i / D, d = i % D;
+  xs[i] = x[(size_t)perm[r] * D + d];
+}
+
+__global__ void k_iota(int* p, int n)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = i;
+}
+
+}  // namespace
+
+void build_tree(DevTree& t, const double* d_x, int n, int D, int leaf, cudaStream_t s)
+{
+  if (leaf < 1) throw InvalidArgument("leaf_threshold must be >= 1");
+  if (n < 1 || D < 1) throw InvalidArgument("PointSet requires N >= 1 and D >= 1");
+  t.n = n;
+  t.D = D;
+  t.leaf = leaf;
+  const int maxK = 2 * n;  // nodes <= 2n - 1
+
+  // BFS-indexed build arrays
+  DevBuf<double> blo, bhi, bcen, bside, bsc;
+  DevBuf<int> bsd;
+  blo.reserve((size_t)maxK * D);
+  bhi.reserve((size_t)maxK * D);
+  bcen.reserve((size_t)maxK * D);
+  bside.reserve(maxK);
+  bsc.reserve(maxK);
+  bsd.reserve(maxK);
+
+  t.perm.reserve(n);
+  k_iota<<<ceil_div(n, 256), 256, 0, s>>>(t.perm.p, n);
+  CK_LAUNCH();
+
+  DevBuf<int> flag, P, slot;
+  flag.reserve((size_t)n + 1);
+  P.reserve((size_t)n + 1);
+  slot.reserve(n);
+  CK(cudaMemsetAsync(flag.p, 0, sizeof(int) * ((size_t)n + 1), s));
+
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, flag.p, P.p, n + 1, s);
+  DevBuf<unsigned char> scan_tmp;
+  scan_tmp.reserve(scan_bytes + 16);
+
+  // host bookkeeping (BFS ids)
+  std::vector<int> h_beg{ 0 }, h_cnt{ n }, h_left, h_right, h_par{ -1 }, h_dep{ 0 };
+  std::vector<int> level_off{ 0 };
+  DevBuf<int> d_nbeg, d_ncnt, d_tnode, d_tstart, d_dosplit, d_sd_lvl, d_lc;
+  DevBuf<double> d_mid;
+  DevBuf<unsigned long long> d_kmin, d_kmax;
+
+  int base = 0;
+  while (base < (int)h_beg.size()) {
+    const int m = (int)h_beg.size() - base;
+    // tiles
+    std::vector<int> tnode, tstart;
+    for (int j = 0; j < m; ++j) {
+      const int b = h_beg[base + j], c = h_cnt[base + j];
+      for (int st = b; st < b + c; st += kTile) {
+        tnode.push_back(j);
+        tstart.push_back(st);
+      }
+    }
+    const int ntiles = (int)tnode.size();
+    d_nbeg.reserve(m);
+    d_ncnt.reserve(m);
+    d_tnode.reserve(ntiles);
+    d_tstart.reserve(ntiles);
+    d_dosplit.reserve(m);
+    d_sd_lvl.reserve(m);
+    d_lc.reserve(m);
+    d_mid.reserve(m);
+    d_kmin.reserve((size_t)m * D);
+    d_kmax.reserve((size_t)m * D);
+    CK(cudaMemcpyAsync(d_nbeg.p, h_beg.data() + base, sizeof(int) * m, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_ncnt.p, h_cnt.data() + base, sizeof(int) * m, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_tnode.p, tnode.data(), sizeof(int) * ntiles, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_tstart.p, tstart.data(), sizeof(int) * ntiles, cudaMemcpyHostToDevice, s));
+
+    LevelArgs a{ d_x, D, t.perm.p, d_nbeg.p, d_ncnt.p, d_tnode.p, d_tstart.p, d_kmin.p, d_kmax.p };
+    k_bounds_init<<<ceil_div((long long)m * D, 256), 256, 0, s>>>(d_kmin.p, d_kmax.p, m * D);
+    k_bounds_tiles<<<ntiles, kThreads, 0, s>>>(a);
+    k_decide<<<ceil_div(m, 128), 128, 0, s>>>(a, m, leaf, base, blo.p, bhi.p, bcen.p, bside.p,
+                                              bsd.p, d_mid.p, d_dosplit.p);
+    // split_dim per level node (for flags) = bsd[base + j]
+    CK(cudaMemcpyAsync(d_sd_lvl.p, bsd.p + base, sizeof(int) * m, cudaMemcpyDeviceToDevice, s));
+    k_flags<<<ntiles, kThreads, 0, s>>>(a, d_dosplit.p, d_sd_lvl.p, d_mid.p, flag.p);
+    cub::DeviceScan::ExclusiveSum(scan_tmp.p, scan_bytes, flag.p, P.p, n + 1, s);
+    k_slots<<<ntiles, kThreads, 0, s>>>(a, d_dosplit.p, flag.p, P.p, slot.p);
+    k_swap<<<ntiles, kThreads, 0, s>>>(a, d_dosplit.p, flag.p, P.p, slot.p);
+    k_finish_split<<<ceil_div(m, 64), 64, 0, s>>>(a, m, base, d_dosplit.p, d_sd_lvl.p, d_mid.p,
+                                                  P.p, d_lc.p, bsc.p);
+    CK_LAUNCH();
+    // reset flags of this level's splitting segments (non-split positions stay 0)
+    CK(cudaMemsetAsync(flag.p, 0, sizeof(int) * ((size_t)n + 1), s));
+
+    std::vector<int> lc(m), ds(m);
+    CK(cudaMemcpyAsync(lc.data(), d_lc.p, sizeof(int) * m, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ds.data(), d_dosplit.p, sizeof(int) * m, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+
+    const int next_base = (int)h_beg.size();
+    h_left.resize(h_beg.size(), -1);
+    h_right.resize(h_beg.size(), -1);
+    for (int j = 0; j < m; ++j) {
+      if (!ds[j]) continue;
+      const int id = base + j;
+      const int b = h_beg[id], c = h_cnt[id];
+      h_left[id] = (int)h_beg.size();
+      h_beg.push_back(b);
+      h_cnt.push_back(lc[j]);
+      h_par.push_back(id);
+      h_dep.push_back(h_dep[id] + 1);
+      h_right[id] = (int)h_beg.size();
+      h_beg.push_back(b + lc[j]);
+      h_cnt.push_back(c - lc[j]);
+      h_par.push_back(id);
+      h_dep.push_back(h_dep[id] + 1);
+    }
+    base = next_base;
+    level_off.push_back(base);
+  }
+  const int K = (int)h_beg.size();
+  h_left.resize(K, -1);
+  h_right.resize(K, -1);
+  t.nodes = K;
+  t.height = (int)level_off.size() - 1;
+  t.depth_off = level_off;
+
+  // preorder numbering: left = parent + 1, right = parent + 1 + size(left)
+  std::vector<int> sub(K, 1);
+  for (int i = K - 1; i >= 0; --i)
+    if (h_left[i] >= 0) sub[i] = 1 + sub[h_left[i]] + sub[h_right[i]];
+  std::vector<int> bfs2pre(K);
+  bfs2pre[0] = 0;
+  for (int i = 0; i < K; ++i)
+    if (h_left[i] >= 0) {
+      bfs2pre[h_left[i]] = bfs2pre[i] + 1;
+      bfs2pre[h_right[i]] = bfs2pre[i] + 1 + sub[h_left[i]];
+    }
+
+  DevBuf<int> d_map, d_bleft, d_bright, d_bbeg, d_bcnt, d_bpar, d_bdep;
+  auto up = [&](DevBuf<int>& b, const std::vector<int>& v) {
+    b.reserve(v.size());
+    CK(cudaMemcpyAsync(b.p, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice, s));
+  };
+  up(d_map, bfs2pre);
+  up(d_bleft, h_left);
+  up(d_bright, h_right);
+  up(d_bbeg, h_beg);
+  up(d_bcnt, h_cnt);
+  up(d_bpar, h_par);
+  up(d_bdep, h_dep);
+  t.lo.reserve((size_t)K * D);
+  t.hi.reserve((size_t)K * D);
+  t.centroid.reserve((size_t)K * D);
+  t.max_side.reserve(K);
+  t.split_coord.reserve(K);
+  t.split_dim.reserve(K);
+  t.left.reserve(K);
+  t.right.reserve(K);
+  t.begin.reserve(K);
+  t.count.reserve(K);
+  t.parent.reserve(K);
+  t.depth.reserve(K);
+  t.by_depth.reserve(K);
+  k_to_preorder<<<ceil_div(K, 256), 256, 0, s>>>(
+    K, D, d_map.p, blo.p, bhi.p, bcen.p, bside.p, bsc.p, bsd.p, d_bleft.p, d_bright.p, d_bbeg.p,
+    d_bcnt.p, d_bpar.p, d_bdep.p, t.lo.p, t.hi.p, t.centroid.p, t.max_side.p, t.split_coord.p,
+    t.split_dim.p, t.left.p, t.right.p, t.begin.p, t.count.p, t.parent.p, t.depth.p,
+    t.by_depth.p);
+  CK_LAUNCH();
+  t.xs.reserve((size_t)n * D);
+  k_gather_points<<<ceil_div((long long)n * D, 256), 256, 0, s>>>(d_x, t.perm.p, n, D, t.xs.p);
+  CK_LAUNCH();
+  t.h_count.assign(K, 0);
+  t.h_left.assign(K, -1);
+  for (int i = 0; i < K; ++i) {
+    t.h_count[bfs2pre[i]] = h_cnt[i];
+    t.h_left[bfs2pre[i]] = h_left[i] < 0 ? -1 : bfs2pre[h_left[i]];
+  }
+  CK(cudaStreamSynchronize(s));
+}
+
+}  // namespace dfgtb

@@ -1,0 +1,192 @@
+"""GPU DFGT sums vs the FP64 oracle: the per-query eps guarantee and the
+reference's engine properties (test_engine.cpp, acceptance.cpp criterion 1).
+
+Tolerance: |G_gpu - G_exact| <= eps * G_exact per query (the reference's contract,
+engine.hpp:93), checked with a 1e-12 relative slack for FP64 summation order.
+"""
+import numpy as np
+import pytest
+
+from paper_1102_2878_b200 import datagen
+
+pytestmark = pytest.mark.gpu
+SLACK = 1e-12
+
+
+def _mixture(n, d, seed):
+    g = np.random.default_rng(seed)
+    c = g.random((6, d))
+    comp = g.integers(0, 6, n)
+    return c[comp] + 0.05 * g.standard_normal((n, d))
+
+
+def _check(approx, exact, eps):
+    ok = exact > 0
+    rel = np.abs(approx[ok] - exact[ok]) / exact[ok]
+    assert rel.max(initial=0.0) <= eps * (1 + 1e-9) + SLACK, rel.max()
+    return rel.max(initial=0.0)
+
+
+def test_single_point_is_one(dfgtb):
+    p = np.array([[0.3, -0.7]])
+    assert dfgtb.dfgt_kde(p, p, 0.8).tolist() == [1.0]
+    assert dfgtb.dfd_kde(p, p, 0.8, 0.01).tolist() == [1.0]
+
+
+def test_naive_goldens(dfgtb, orc):
+    p = np.array([[1.0, 2.0]])
+    assert dfgtb.naive_kde(p, p, 0.5).tolist() == [1.0]
+    s = dfgtb.naive_kde(np.array([[0.0]]), np.array([[0.0], [3.0]]), 1.5)
+    assert s[0] == pytest.approx(1.0 + np.exp(-9.0 / (2 * 1.5 * 1.5)), rel=1e-14)
+    x = np.random.default_rng(1).random((700, 3))
+    assert np.allclose(dfgtb.naive_kde(x, x, 0.07), orc.naive_kde(x, x, 0.07), rtol=1e-13, atol=0)
+
+
+def test_dimension_mismatch_raises(dfgtb):
+    with pytest.raises(ValueError):
+        dfgtb.naive_kde(np.zeros((1, 2)), np.zeros((1, 3)), 1.0)
+    with pytest.raises(ValueError):
+        dfgtb.dfgt_kde(np.zeros((1, 2)), np.zeros((1, 3)), 1.0)
+
+
+def test_invalid_arguments(dfgtb):
+    x = np.random.default_rng(0).random((50, 2))
+    with pytest.raises(ValueError):
+        dfgtb.DualTreeEngine(x, config=dfgtb.EngineConfig(epsilon=-1.0))
+    with pytest.raises(ValueError):
+        dfgtb.DualTreeEngine(x, config=dfgtb.EngineConfig(leaf_threshold=0))
+    with pytest.raises(ValueError):
+        dfgtb.DualTreeEngine(x, config=dfgtb.EngineConfig(p_max=16))
+    e = dfgtb.DualTreeEngine(x)
+    with pytest.raises(ValueError):
+        e.compute(None, 0.0)
+    with pytest.raises(ValueError):
+        e.compute(None, -1.0)
+
+
+def test_dfd_zero_tolerance_matches_naive(dfgtb, orc):
+    pts = _mixture(300, 2, 9)
+    exact = orc.naive_kde(pts, pts, 0.05)
+    approx = dfgtb.dfd_kde(pts, pts, 0.05, 0.0, 8)
+    assert dfgtb.verify_relative_error(approx, exact).max_relative_error <= 1e-12
+
+
+@pytest.mark.parametrize("h", [0.001, 0.05, 0.5, 5.0])
+def test_dfd_contract(dfgtb, orc, h):
+    pts = _mixture(1000, 2, 12)
+    _check(dfgtb.dfd_kde(pts, pts, h, 0.01), orc.naive_kde(pts, pts, h), 0.01)
+
+
+def test_dfgt_contract_across_scales(dfgtb, orc):
+    pts = _mixture(500, 2, 21)
+    e = dfgtb.DualTreeEngine(pts, dfgtb.Mode.series, dfgtb.EngineConfig(epsilon=0.01))
+    for scale in (1e-3, 1e-2, 1e-1, 1.0, 10.0, 100.0, 1000.0):
+        h = scale * 0.05
+        _check(e.compute(None, h), orc.naive_kde(pts, pts, h), 0.01)
+
+
+def test_separate_query_and_reference(dfgtb, orc):
+    refs = _mixture(700, 3, 31)
+    q = np.random.default_rng(32).random((350, 3))
+    for h in (0.05, 0.2, 2.0):
+        approx = dfgtb.dfgt_kde(q, refs, h, dfgtb.EngineConfig(epsilon=0.001))
+        _check(approx, orc.naive_kde(q, refs, h), 0.001)
+
+
+def test_global_guarantee_random_instances(dfgtb, orc):
+    rng = np.random.default_rng(123)
+    for inst in range(15):
+        d = 1 + inst % 3
+        n = 200 + 50 * inst
+        pts = _mixture(n, d, 400 + inst)
+        h = 10 ** rng.uniform(-3, 3)
+        exact = orc.naive_kde(pts, pts, h)
+        for eps in (0.1, 0.01, 0.001):
+            _check(dfgtb.dfgt_kde(pts, pts, h, dfgtb.EngineConfig(epsilon=eps)), exact, eps)
+
+
+def test_term_count_cost_model(dfgtb, orc):
+    pts = _mixture(400, 2, 77)
+    cfg = dfgtb.EngineConfig(epsilon=0.01, cost_model=dfgtb.CostModel.term_count)
+    for h in (0.02, 0.2, 2.0):
+        _check(dfgtb.dfgt_kde(pts, pts, h, cfg), orc.naive_kde(pts, pts, h), 0.01)
+
+
+def test_loose_tolerance_single_prune(dfgtb):
+    pts = _mixture(150, 2, 5)
+    e = dfgtb.DualTreeEngine(pts, dfgtb.Mode.series,
+                             dfgtb.EngineConfig(epsilon=1e6, leaf_threshold=10))
+    s = e.compute(None, 1.0)
+    assert e.last_stats().pairs_visited == 1
+    assert np.all(np.isfinite(s))
+
+
+def test_bit_identical_runs(dfgtb):
+    pts = _mixture(800, 2, 55)
+    a = dfgtb.dfgt_kde(pts, pts, 0.02)
+    b = dfgtb.dfgt_kde(pts, pts, 0.02)
+    assert np.array_equal(a, b)
+    w = datagen.config(2, scale_n=0.2)
+    e = dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(leaf_threshold=32))
+    for h in (w.h_s, 3 * w.h_s):
+        assert np.array_equal(e.compute(None, h), e.compute(None, h))
+
+
+def test_kernel_evals_monotone_in_eps(dfgtb):
+    pts = _mixture(1000, 2, 66)
+    prev = None
+    for eps in (1e-3, 1e-2, 1e-1):
+        e = dfgtb.DualTreeEngine(pts, config=dfgtb.EngineConfig(epsilon=eps))
+        e.compute(None, 0.05)
+        ev = e.last_stats().kernel_evaluations
+        assert prev is None or ev <= prev
+        prev = ev
+
+
+def test_series_prunes_engage(dfgtb):
+    pts = _mixture(2000, 2, 99)
+    e = dfgtb.DualTreeEngine(pts, config=dfgtb.EngineConfig(epsilon=0.01))
+    e.compute(None, 0.1)
+    st = e.last_stats()
+    assert st.prunes_farfield + st.prunes_direct_local + st.prunes_far_to_local > 0
+
+
+def test_all_duplicates_exact(dfgtb):
+    pts = np.tile([[0.25, -1.5]], (64, 1))
+    e = dfgtb.DualTreeEngine(pts, config=dfgtb.EngineConfig(epsilon=0.0, leaf_threshold=4))
+    assert np.all(e.compute(None, 0.7) == 64.0)
+
+
+def test_six_dimensional_order_one(dfgtb, orc):
+    pts = _mixture(300, 6, 11)
+    e = dfgtb.DualTreeEngine(pts, config=dfgtb.EngineConfig(epsilon=0.01))
+    assert e.p_max() == 1
+    for h in (0.05, 0.5, 5.0):
+        _check(e.compute(None, h), orc.naive_kde(pts, pts, h), 0.01)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_config_generators_small(dfgtb, orc, k):
+    """Every config's distribution at reduced N, full eps check vs the CPU oracle
+    (acceptance.cpp criterion 1 analogue)."""
+    w = datagen.config(k, scale_n=0.05 if k != 1 else 0.3)
+    for eps in w.epsilons:
+        e = dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(epsilon=eps, leaf_threshold=32,
+                                                                    p_max=w.p_max or None))
+        for s in (w.scales if len(w.scales) > 1 else (0.5, 1.0, 2.0)):
+            h = s * w.h_s
+            exact = orc.naive_kde(w.refs, w.refs, h)
+            _check(e.compute(None, h), exact, eps)
+
+
+def test_dfgt_matches_reference_within_eps(dfgtb, ref):
+    """GPU vs the compiled reference DFGT: both within eps of exact, so within
+    2 eps of each other; prune decisions differ (BFS vs DFS order)."""
+    w = datagen.config(2, scale_n=0.05)
+    re = ref.engine(w.refs, eps=0.01, leaf=32)
+    e = dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(leaf_threshold=32))
+    for s in w.scales:
+        h = s * w.h_s
+        a = e.compute(None, h)
+        b, _ = re.compute(h)
+        assert np.all(np.abs(a - b) <= 0.0201 * np.abs(b) + 1e-300)
