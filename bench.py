@@ -1,0 +1,299 @@
+#!/usr/bin/env python
+"""Benchmark: DFGT kernel-sum queries/sec on BASELINE config 2 (one B200).
+
+Workload (BASELINE.json configs[1]): Q = R = 50,000 points, D = 2,
+16-component clipped Gaussian mixture (seeded synthetic), eps = 0.01, leaf 32,
+p_max = 6.  One STEP = the full CV bandwidth sweep: 9 bandwidths h = h_s 10^k,
+k in {-3,-2,-1,-0.5,0,0.5,1,2,3}, each with kernel sums at h and at 2h (18 sums of
+50k queries) and CV_LK + CV_LS reduced on the device.  Metric = queries/sec per h
+= 18 * 50,000 / step time (whole job over all ranks).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's own CPU implementation (compiled from
+/root/reference into oracle/_ref) on the host cores, same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gaussian KDE kernel-sum queries/sec (Q=R, eps=1e-2) per h; % of exp/FP64 roofline"
+UNIT = "queries/s"
+FP64_INSTR_PER_PAIR = {1: 21, 2: 23, 3: 25, 4: 27, 5: 29}  # 2D+19, see DESIGN.md
+
+
+def workload(rank: int = 0):
+    from paper_1102_2878_b200 import datagen
+    w = datagen.config(2)
+    if rank:  # weak scaling: every rank sweeps its own independent instance
+        x = datagen.gauss_mixture_2d(w.refs.shape[0], 1002 + 1000 * rank)
+        w = datagen.Workload(w.name, x, None, datagen.silverman_h(x), w.scales)
+    return w
+
+
+# --------------------------------------------------------------------- reference
+def _ref_one(args):
+    refs, h, eps, leaf = args
+    from oracle import load_reference
+    ref = load_reference()
+    t0 = time.perf_counter()
+    eng = ref.engine(refs, eps=eps, leaf=leaf)
+    sums, _ = eng.compute(h)
+    eng.close()
+    return sums, time.perf_counter() - t0
+
+
+def reference_sweep(w, cores: int):
+    """The reference's bandwidth sweep for both CV scores: one reference engine per
+    (h | 2h) compute, `cores` processes (the engine is single-threaded, engine.hpp:85)."""
+    import multiprocessing as mp
+    from oracle import load_oracle
+    hs = [s * w.h_s for s in w.scales]
+    jobs = [(w.refs, h, 0.01, 32) for h in hs] + [(w.refs, 2 * h, 0.01, 32) for h in hs]
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(min(cores, len(jobs))) as pool:
+        res = pool.map(_ref_one, jobs, chunksize=1)
+    wall = time.perf_counter() - t0
+    orc = load_oracle()
+    n = len(hs)
+    scores = []
+    for i, h in enumerate(hs):
+        lk, cl = orc.lkcv(2, h, res[i][0])
+        ls = orc.lscv(2, h, res[i][0], 2 * h, res[n + i][0])
+        scores.append((h, lk, cl, ls))
+    return wall, scores, sum(r[1] for r in res)
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    from oracle import load_reference
+    if load_reference() is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libdfgt_ref.so not built (needs /root/reference at build time)"}))
+        return
+    w = workload(0)
+    cores = os.cpu_count() or 1
+    n_q = 2 * len(w.scales) * w.refs.shape[0]
+    for _ in range(a.warmup):
+        reference_sweep(w, cores)
+    times = []
+    for _ in range(a.steps):
+        wall, _, _ = reference_sweep(w, cores)
+        times.append(wall)
+    t = float(np.mean(times))
+    v = n_q / t
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(w, world),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": min(cores, 18), "kind": "reference",
+                         "sample": "full cfg2 sweep per step: 18 reference DualTreeEngine computes "
+                                   "(9 scales x {h, 2h}), one engine per compute, "
+                                   f"{min(cores, 18)} processes on the host cores"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def config_block(w, world):
+    return {"workload": f"{w.name}: CV sweep 9 x (h, 2h) kernel sums + CV_LK/CV_LS",
+            "N": int(w.refs.shape[0]), "D": int(w.refs.shape[1]), "eps": 0.01, "leaf": 32,
+            "p_max": 6, "bandwidths": 18, "global_batch": int(18 * w.refs.shape[0] * world),
+            "l2": "flushed between timed steps (256 MiB device write)",
+            "parallelism": f"replicas{world}" if world > 1 else "single"}
+
+
+# -------------------------------------------------------------------------- ours
+class Clocks:
+    def __init__(self, idx):
+        self.p = None
+        self.idx = idx
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.out = ""
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 6 and f[0].isdigit():
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(int(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def run_ours(a, rank, world, local_rank):
+    import torch
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import paper_1102_2878_b200 as dfgtb
+    from paper_1102_2878_b200 import _capi
+
+    w = workload(rank)
+    n = w.refs.shape[0]
+    cfg = dfgtb.EngineConfig(epsilon=0.01, leaf_threshold=32)
+    eng = dfgtb.DualTreeEngine(w.refs, dfgtb.Mode.series, cfg)
+    stream = torch.cuda.ExternalStream(_capi.lib.dfgtb_stream(eng.handle))
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
+    peak_instr = _capi.lib.dfgtb_dfma_peak()
+
+    def step():
+        return eng.sweep(w.scales, w.h_s)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    l0 = _capi.lib.dfgtb_launch_count(eng.handle)
+    ms, base_ms, base_pairs, rows = [], 0.0, 0, None
+    with Clocks(local_rank) as clk:
+        for _ in range(a.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rows = step()
+            e1.record(stream)
+            e1.synchronize()
+            ms.append(e0.elapsed_time(e1))
+            base_ms += sum(r.base_ms for r in rows)
+            base_pairs += sum(r.base_pairs for r in rows)
+    launches = _capi.lib.dfgtb_launch_count(eng.handle) - l0
+    torch.cuda.synchronize()
+    t_step = float(np.mean(ms))
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t_step], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = float(tt.item())
+    value = 18 * n * world / (t_step * 1e-3)
+
+    # e2e: public API with host buffers (pinned), engine build + sweep + scores back
+    pinned = torch.empty(w.refs.shape, dtype=torch.float64, pin_memory=True)
+    pinned.numpy()[:] = w.refs
+    host = pinned.numpy()
+    e2e_t = []
+    for i in range(max(2, min(a.steps, 5)) + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with dfgtb.DualTreeEngine(host, dfgtb.Mode.series, cfg) as e2:
+            r2 = e2.sweep(w.scales, w.h_s)
+        t1 = time.perf_counter()
+        if i:  # first iteration is warm-up
+            e2e_t.append(t1 - t0)
+    e2e_s = float(np.mean(e2e_t))
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_v = 18 * n * world / e2e_s
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return
+    instr = FP64_INSTR_PER_PAIR.get(w.refs.shape[1], 2 * w.refs.shape[1] + 19)
+    achieved = base_pairs * instr / (base_ms * 1e-3) if base_ms > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "base_case_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg2 generator, SURVEY 8(d))",
+        "config": config_block(w, world),
+        "roofline": {"bound": "fp64", "kernel": "k_base_case (K10 exhaustive base case)",
+                     "achieved": achieved / 1e12, "peak": peak_instr / 1e12,
+                     "unit": "T FP64-pipe instr/s", "frac": achieved / peak_instr if peak_instr > 0 else None,
+                     "traffic": traffic, "instr_per_pair": instr,
+                     "base_pairs_per_step": base_pairs // max(a.steps, 1),
+                     "base_ms_per_step": base_ms / max(a.steps, 1),
+                     "peak_source": "measured DFMA throughput (dfgtb_dfma_peak) on this GPU"},
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+        "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": int(w.refs.nbytes),
+                "d2h_bytes_per_step": int(len(w.scales) * 148 * 3 * 8)},
+        "scores": [{"h": r.h, "lk": r.lk_score, "lk_clamped": r.lk_clamped, "ls": r.ls_score}
+                   for r in rows],
+    }
+    if world == 1 and not a.no_cpu_baseline:
+        from oracle import load_reference
+        if load_reference() is not None:
+            cores = os.cpu_count() or 1
+            wall, _, cpu_sum = reference_sweep(w, cores)
+            line["cpu_baseline"] = {
+                "value": 18 * n / wall, "unit": UNIT, "cores": min(cores, 18), "kind": "reference",
+                "sample": "one full cfg2 sweep: 18 reference DualTreeEngine computes (9 scales x "
+                          f"{{h, 2h}}), one engine per process, {min(cores, 18)} processes; "
+                          f"sum of single-core compute time {cpu_sum:.1f} s"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    a = p.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+    else:
+        run_ours(a, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

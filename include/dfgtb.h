@@ -59,6 +59,10 @@ typedef struct dfgtb_cv_row {
   int lk_clamped;
   double ls_score;  /* lscv_from_sums  (cv.cpp:78-97) */
   double seconds;   /* device time of this row's computes */
+  double base_ms;   /* device time of the base-case kernel launches of this row */
+  uint64_t base_pairs;          /* (q, r) kernel evaluations in those base cases */
+  uint64_t kernel_evaluations;  /* TraversalStats::kernel_evaluations, summed */
+  uint64_t pairs_visited;       /* TraversalStats::pairs_visited, summed */
 } dfgtb_cv_row;
 
 typedef struct dfgtb_handle dfgtb_handle;
@@ -133,6 +137,12 @@ double dfgtb_dfma_peak(void);
 
 /* Number of visible CUDA devices (0 when none; never raises). */
 int dfgtb_device_count(void);
+
+/* The handle's CUDA stream (cudaStream_t as an integer) -- for timing with CUDA
+ * events on the stream the kernels run on -- and the number of this library's
+ * kernels launched on it since creation. */
+uintptr_t dfgtb_stream(dfgtb_handle* h);
+uint64_t dfgtb_launch_count(dfgtb_handle* h);
 
 const char* dfgtb_last_error(void);
 

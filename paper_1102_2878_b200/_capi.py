@@ -44,7 +44,8 @@ class Timings(C.Structure):
 class CvRow(C.Structure):
     _fields_ = [("scale", C.c_double), ("h", C.c_double), ("conv_h", C.c_double),
                 ("lk_score", C.c_double), ("lk_clamped", C.c_int), ("ls_score", C.c_double),
-                ("seconds", C.c_double)]
+                ("seconds", C.c_double), ("base_ms", C.c_double), ("base_pairs", C.c_uint64),
+                ("kernel_evaluations", C.c_uint64), ("pairs_visited", C.c_uint64)]
 
 
 # every symbol include/dfgtb.h declares (tests check the .so exports all of them)
@@ -53,7 +54,8 @@ EXPORTS = (
     "dfgtb_compute", "dfgtb_compute_device", "dfgtb_last_stats", "dfgtb_last_timings",
     "dfgtb_p_max", "dfgtb_cv", "dfgtb_sweep", "dfgtb_lkcv_from_sums", "dfgtb_lscv_from_sums",
     "dfgtb_tree_nodes", "dfgtb_tree_height", "dfgtb_export_tree", "dfgtb_naive",
-    "dfgtb_series_op", "dfgtb_dfma_peak", "dfgtb_device_count", "dfgtb_last_error",
+    "dfgtb_series_op", "dfgtb_dfma_peak", "dfgtb_device_count", "dfgtb_stream",
+    "dfgtb_launch_count", "dfgtb_last_error",
 )
 
 
@@ -86,6 +88,8 @@ def _load():
                                       _D]),
         "dfgtb_dfma_peak": (C.c_double, []),
         "dfgtb_device_count": (C.c_int, []),
+        "dfgtb_stream": (C.c_size_t, [V]),
+        "dfgtb_launch_count": (C.c_uint64, [V]),
         "dfgtb_last_error": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():

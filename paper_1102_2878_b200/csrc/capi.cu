@@ -206,16 +206,29 @@ int dfgtb_cv(dfgtb_handle* h, double bw, double conv_h, dfgtb_cv_row* row)
     const size_t n = e.n();
     if (n < 2) throw InvalidArgument("likelihood CV requires at least 2 points");
     h->s1.reserve(n);
-    float ms = 0;
+    float ms = 0, bms = 0;
+    uint64_t bp = 0, kev = 0, pv = 0;
+    auto acc = [&] {
+      const Stats& st = e.last_stats();
+      ms += e.last_timings().total_ms;
+      bms += e.last_timings().base_ms;
+      bp += st.kernel_evaluations - 2ull * st.pairs_visited;
+      kev += st.kernel_evaluations;
+      pv += st.pairs_visited;
+    };
     e.compute_device(nullptr, n, bw, h->s1.p);
-    ms += e.last_timings().total_ms;
+    acc();
     const double* conv = nullptr;
     if (conv_h > 0.0) {
       h->s2.reserve(n);
       e.compute_device(nullptr, n, conv_h, h->s2.p);
-      ms += e.last_timings().total_ms;
+      acc();
       conv = h->s2.p;
     }
+    row->base_ms = bms;
+    row->base_pairs = bp;
+    row->kernel_evaluations = kev;
+    row->pairs_visited = pv;
     double lk = 0, ls = 0;
     int cl = 0;
     e.cv_reduce(h->s1.p, bw, conv, conv_h, &lk, &cl, &ls);
@@ -369,6 +382,17 @@ int dfgtb_series_op(int op, size_t d, int p_max, const double* in, size_t n, con
     else
       for (size_t i = 0; i < T; ++i) out[t.pos[i]] = hout[i];
   });
+}
+
+uintptr_t dfgtb_stream(dfgtb_handle* h)
+{
+  return h && h->eng ? (uintptr_t)h->eng->stream() : 0;
+}
+
+uint64_t dfgtb_launch_count(dfgtb_handle* h)
+{
+  (void)h;
+  return launch_counter();
 }
 
 int dfgtb_device_count(void)

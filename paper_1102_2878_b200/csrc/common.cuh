@@ -33,7 +33,14 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
   throw CudaError(msg);
 }
 #define CK(x) ::dfgtb::cuda_check((x), #x, __FILE__, __LINE__)
-#define CK_LAUNCH() ::dfgtb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+// Every kernel launch of this library is followed by CK_LAUNCH(): it checks the
+// launch and counts it (dfgtb_launch_count reports the process-wide total).
+uint64_t& launch_counter();
+#define CK_LAUNCH()                                                                    \
+  do {                                                                                 \
+    ::dfgtb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__);      \
+    ++::dfgtb::launch_counter();                                                       \
+  } while (0)
 
 // Growable device buffer (capacity only ever grows; contents not preserved on growth).
 template <class T>

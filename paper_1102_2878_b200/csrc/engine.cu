@@ -33,6 +33,12 @@
 
 namespace dfgtb {
 
+uint64_t& launch_counter()
+{
+  static uint64_t n = 0;
+  return n;
+}
+
 int default_p_max(int D)
 {  // truncation.cpp:168-186
   switch (D) {
@@ -400,44 +406,178 @@ __global__ void k_mark_moments(const Item* it, int n, int* flag)
   }
 }
 
-// K2/K3: moments of every reference node some F/T item uses, directly from its
-// contiguous sorted points (equivalent to leaf moments + F2F, engine.cpp:384-399).
-__global__ void k_moments(DevSeries g, TreeView R, int nodes, const int* flag, double s, double* M)
+// K2/K3 (large tables, lazy): UNSCALED moments of the reference nodes an F/T item
+// uses and that are not cached yet, one block per node over its contiguous points.
+__global__ void k_moments(DevSeries g, TreeView R, int nodes, const int* flag, int* done, double* M)
 {
   extern __shared__ double sm[];
   for (int n = blockIdx.x; n < nodes; n += gridDim.x) {
-    if (!flag[n]) continue;
-    dev_moments_block(g, R.xs + (size_t)R.begin[n] * g.D, R.count[n], R.cen + (size_t)n * g.D, s,
+    if (!flag[n] || done[n]) continue;
+    dev_moments_block(g, R.xs + (size_t)R.begin[n] * g.D, R.count[n], R.cen + (size_t)n * g.D, 1.0,
                       M + (size_t)n * g.T, sm);
     __syncthreads();
+    if (threadIdx.x == 0) done[n] = 1;
   }
 }
 
-// D and T items of one query node, in sorted order (summarize, engine.cpp:212-232).
-__global__ void k_local_items(DevSeries g, TreeView Q, TreeView R, int nodes, const int* cnt,
-                              const int* off, const Item* items, const double* M, double s,
-                              double* L, int* Lord)
+// K2/K3 (eager, tables <= 4096 terms): unscaled moments of EVERY reference node,
+// computed once per tree.  M~_a(node) = (1/a!) sum_r prod_d (r - c)_d^{a_d}; the
+// reference's per-h moment is s^|a| M~_a with s = 1/(h sqrt 2) (engine.cpp:368-403
+// recomputes per h; one pass serves the whole sweep).  Pass 1: partial sums over
+// 64-point chunks of each node; pass 2: per node, chunks summed in order.
+constexpr int kMomChunk = 64;
+__global__ void k_moment_chunks(DevSeries g, TreeView R, const int* cnode, const int* cstart,
+                                int nchunks, double* part)
 {
   extern __shared__ double sm[];
+  const int D = g.D, pm = g.pmax, per = D * pm;
+  for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const int n = cnode[c], st = cstart[c];
+    const int m = min(kMomChunk, R.begin[n] + R.count[n] - st);
+    const double* cen = R.cen + (size_t)n * D;
+    __syncthreads();
+    for (int w = threadIdx.x; w < m * D; w += blockDim.x) {
+      const int pt = w / D, d = w % D;
+      const double u = R.xs[(size_t)(st + pt) * D + d] - cen[d];
+      double* P = sm + pt * per + d * pm;
+      P[0] = 1.0;
+      for (int k = 1; k < pm; ++k) P[k] = P[k - 1] * u;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < g.T; i += blockDim.x) {
+      const uint64_t a = g.dig[i];
+      double sum = 0.0;
+      for (int pt = 0; pt < m; ++pt) sum += mono(sm + pt * per, pm, D, a);
+      part[(size_t)c * g.T + i] = sum;
+    }
+  }
+}
+
+__global__ void k_moment_reduce(DevSeries g, int nodes, const int* coff, const double* part,
+                                double* M)
+{
+  for (int n = blockIdx.x; n < nodes; n += gridDim.x)
+    for (int i = threadIdx.x; i < g.T; i += blockDim.x) {
+      double acc = 0.0;
+      for (int c = coff[n]; c < coff[n + 1]; ++c) acc += part[(size_t)c * g.T + i];
+      M[(size_t)n * g.T + i] = acc * g.invf[i];
+    }
+}
+
+// s^k, k <= D(p_max-1), for scaling unscaled moments inside F / T kernels.
+struct SPow {
+  double v[128];
+};
+
+// D/T work split into chunks: a D item over <= kLocChunk reference points or one
+// T item.  Each chunk writes an unsigned partial table; k_local_reduce sums a query
+// node's chunks in item order and applies (-1)^|b|/b! (summarize, engine.cpp:212-232).
+constexpr int kLocChunk = 64;
+struct LChunk {
+  int item, start, n;
+};
+
+__global__ void k_local_count(const Item* items, int n, TreeView R, int* nch)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int kind = items[i].code >> 8;
+  nch[i] = kind == kD ? (R.count[items[i].r] + kLocChunk - 1) / kLocChunk : 1;
+}
+
+__global__ void k_local_fill(const Item* items, int n, TreeView R, const int* choff, LChunk* ch)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int kind = items[i].code >> 8;
+  const int r = items[i].r;
+  if (kind == kD) {
+    const int b = R.begin[r], c = R.count[r];
+    for (int k = 0, st = 0; st < c; ++k, st += kLocChunk)
+      ch[choff[i] + k] = LChunk{ i, b + st, min(kLocChunk, c - st) };
+  } else {
+    ch[choff[i]] = LChunk{ i, -1, 0 };
+  }
+}
+
+__global__ void k_local_chunks(DevSeries g, TreeView Q, TreeView R, const Item* items,
+                               const LChunk* ch, int nch, const double* Mt, SPow sp, double s,
+                               double* part)
+{
+  extern __shared__ double sm[];
+  __shared__ double spw[128];
+  for (int k = threadIdx.x; k < 128; k += blockDim.x) spw[k] = sp.v[k];
+  for (int c = blockIdx.x; c < nch; c += gridDim.x) {
+    const LChunk lc = ch[c];
+    const Item it = items[lc.item];
+    const int kind = it.code >> 8, order = it.code & 0xff;
+    double* P = part + (size_t)c * g.T;
+    const double* qc = Q.cen + (size_t)it.q * g.D;
+    if (kind == kD)
+      dev_direct_local_partial(g, R.xs + (size_t)lc.start * g.D, lc.n, qc, s, order, P, sm);
+    else
+      dev_f2l_block(g, Mt + (size_t)it.r * g.T, R.cen + (size_t)it.r * g.D, qc, s, order, P, sm,
+                    spw, 1);
+  }
+}
+
+__global__ void k_local_reduce(DevSeries g, int nodes, const int* cnt, const int* off,
+                               const Item* items, const int* choff, const double* part, double* L,
+                               int* Lord)
+{
   for (int n = blockIdx.x; n < nodes; n += gridDim.x) {
     const int c = cnt[n];
     if (!c) continue;
-    const Item* it = items + off[n];
-    int ord = Lord[n];
-    for (int k = 0; k < c; ++k) {
-      const int kind = it[k].code >> 8, order = it[k].code & 0xff;
-      const int r = it[k].r;
-      if (kind == kD)
-        dev_direct_local_block(g, R.xs + (size_t)R.begin[r] * g.D, R.count[r],
-                               Q.cen + (size_t)n * g.D, s, order, L + (size_t)n * g.T, sm);
-      else
-        dev_f2l_block(g, M + (size_t)r * g.T, R.cen + (size_t)r * g.D, Q.cen + (size_t)n * g.D, s,
-                      order, L + (size_t)n * g.T, sm);
-      ord = max(ord, order);
-      __syncthreads();
+    const int i0 = off[n], i1 = i0 + c;
+    int ord = 0;
+    for (int k = i0; k < i1; ++k) ord = max(ord, items[k].code & 0xff);
+    const int nt = ipow_i(ord, g.D);
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+      const uint64_t a = g.dig[t];
+      int mx = 0;
+      for (int d = 0; d < g.D; ++d) mx = max(mx, digit_of(a, d));
+      double acc = 0.0;
+      for (int k = i0; k < i1; ++k) {
+        if (mx >= (items[k].code & 0xff)) continue;  // term beyond this item's order
+        for (int q = choff[k]; q < choff[k + 1]; ++q) acc += part[(size_t)q * g.T + t];
+      }
+      const double sg = (g.degree[t] & 1) ? -1.0 : 1.0;
+      L[(size_t)n * g.T + t] += sg * g.invf[t] * acc;
     }
-    if (threadIdx.x == 0) Lord[n] = ord;
+    if (threadIdx.x == 0 && Lord[n] < ord) Lord[n] = ord;
   }
+}
+
+// Base-case tasks: a query leaf's (sorted) base items cut into runs of <= kTaskItems
+// reference leaves, times 32-query chunks of the leaf.  One warp per task writes
+// per-query partial sums; k_finalize adds a query's partials in task order.
+constexpr int kTaskItems = 8;
+struct BTask {
+  int leaf, item0, item1, q0;
+};
+
+__global__ void k_task_count(const int* leaves, int nleaves, const int* cntB, TreeView Q, int* nt)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nleaves) return;
+  const int leaf = leaves[i];
+  const int ic = (cntB[leaf] + kTaskItems - 1) / kTaskItems;
+  nt[i] = ic * ((Q.count[leaf] + 31) / 32);
+}
+
+__global__ void k_task_fill(const int* leaves, int nleaves, const int* cntB, const int* offB,
+                            TreeView Q, const int* toff, BTask* tasks, int* leaf_task)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nleaves) return;
+  const int leaf = leaves[i];
+  const int c = cntB[leaf], o = offB[leaf];
+  const int ic = (c + kTaskItems - 1) / kTaskItems;
+  int t = toff[i];
+  leaf_task[leaf] = t;
+  for (int q0 = 0; q0 < Q.count[leaf]; q0 += 32)
+    for (int k = 0; k < ic; ++k)
+      tasks[t++] = BTask{ leaf, o + k * kTaskItems, o + min(c, (k + 1) * kTaskItems), q0 };
 }
 
 // Top-down L2L of one depth level (post_process, engine.cpp:294-304).
@@ -459,62 +599,76 @@ __global__ void k_l2l(DevSeries g, TreeView Q, const int* nodes_at, int m, doubl
   }
 }
 
-// K10: exhaustive base case.  One warp per query leaf, lanes = its queries; the
-// leaf's (query leaf, reference leaf) items stream their reference points as
-// warp-uniform (broadcast) loads.  FP64 libdevice exp (exact to ~1 ulp).
+// K10: exhaustive base case (Traversal::base_case, engine.cpp:239-269).  One warp
+// per task = (query leaf, 32-query chunk, run of <= kTaskItems reference leaves):
+// lanes own queries, reference points stream as warp-uniform (broadcast) loads,
+// two independent accumulators for ILP.  FP64 libdevice exp (~1 ulp).
 template <int DT>
 __global__ void __launch_bounds__(kBlock) k_base_case(TreeView Q, TreeView R, int Drt,
-                                                      const int* leaves, int nleaves,
-                                                      const int* cnt, const int* off,
+                                                      const BTask* tasks, int ntasks,
                                                       const Item* items, double scale,
-                                                      double* s_ex)
+                                                      double* part)
 {
   const int lane = threadIdx.x & 31;
   const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const int D = DT ? DT : Drt;
-  for (int li = w0; li < nleaves; li += nw) {
-    const int leaf = leaves[li];
-    const int qb = Q.begin[leaf], qc = Q.count[leaf];
-    const int c = cnt[leaf];
-    const Item* it = items + off[leaf];
-    for (int q0 = 0; q0 < qc; q0 += 32) {
-      const int qi = q0 + lane;
-      const bool act = qi < qc;
-      double q[DT ? DT : kMaxDim];
+  constexpr int DM = DT ? DT : kMaxDim;
+  for (int w = w0; w < ntasks; w += nw) {
+    const BTask t = tasks[w];
+    const int qb = Q.begin[t.leaf] + t.q0;
+    const bool act = lane < Q.count[t.leaf] - t.q0;
+    double q[DM];
 #pragma unroll
-      for (int d = 0; d < (DT ? DT : kMaxDim); ++d)
-        if (DT || d < D) q[d] = act ? Q.xs[(size_t)(qb + qi) * D + d] : 0.0;
-      double acc = 0.0;
-      for (int k = 0; k < c; ++k) {
-        const int r = it[k].r;
-        const double* rp = R.xs + (size_t)R.begin[r] * D;
-        const int rc = R.count[r];
-        for (int j = 0; j < rc; ++j) {
-          double d2 = 0.0;
+    for (int d = 0; d < DM; ++d)
+      if (DT || d < D) q[d] = act ? Q.xs[(size_t)(qb + lane) * D + d] : 0.0;
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int k = t.item0; k < t.item1; ++k) {
+      const int r = items[k].r;
+      const double* rp = R.xs + (size_t)R.begin[r] * D;
+      const int rc = R.count[r];
+      int j = 0;
+      for (; j + 1 < rc; j += 2) {
+        double da = 0.0, db = 0.0;
 #pragma unroll
-          for (int d = 0; d < (DT ? DT : kMaxDim); ++d) {
-            if (DT || d < D) {
-              const double t = q[d] - rp[(size_t)j * D + d];
-              d2 += t * t;
-            }
+        for (int d = 0; d < DM; ++d) {
+          if (DT || d < D) {
+            const double ta = q[d] - rp[(size_t)j * D + d];
+            const double tb = q[d] - rp[(size_t)(j + 1) * D + d];
+            da += ta * ta;
+            db += tb * tb;
           }
-          acc += exp(scale * d2);
         }
+        acc0 += exp(scale * da);
+        acc1 += exp(scale * db);
       }
-      if (act) s_ex[qb + qi] = acc;
+      if (j < rc) {
+        double da = 0.0;
+#pragma unroll
+        for (int d = 0; d < DM; ++d) {
+          if (DT || d < D) {
+            const double ta = q[d] - rp[(size_t)j * D + d];
+            da += ta * ta;
+          }
+        }
+        acc0 += exp(scale * da);
+      }
     }
+    part[(size_t)w * 32 + lane] = acc0 + acc1;
   }
 }
 
 // F items: every query of a leaf evaluates the far-field expansions attached to the
-// leaf or any ancestor (eval_farfield per query, engine.cpp:200-211).
+// leaf or any ancestor, root first (eval_farfield per query, engine.cpp:200-211).
 __global__ void __launch_bounds__(kBlock) k_farfield(DevSeries g, TreeView Q, TreeView R,
                                                      const int* leaves, int nleaves,
                                                      const int* cnt, const int* off,
-                                                     const Item* items, const double* M, double s,
-                                                     double* s_ff)
+                                                     const Item* items, const double* Mt, SPow sp,
+                                                     double s, double* s_ff)
 {
+  __shared__ double spw[128];
+  for (int k = threadIdx.x; k < 128; k += blockDim.x) spw[k] = sp.v[k];
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -522,22 +676,22 @@ __global__ void __launch_bounds__(kBlock) k_farfield(DevSeries g, TreeView Q, Tr
   for (int li = w0; li < nleaves; li += nw) {
     const int leaf = leaves[li];
     const int qb = Q.begin[leaf], qc = Q.count[leaf];
+    int chain[64];
+    int depth = 0;
+    for (int n = leaf; n >= 0 && depth < 64; n = Q.parent[n]) chain[depth++] = n;
     for (int q0 = 0; q0 < qc; q0 += 32) {
       const int qi = q0 + lane;
       const bool act = qi < qc;
       const double* qp = Q.xs + (size_t)(qb + (act ? qi : 0)) * D;
       double acc = 0.0;
-      // root-to-leaf order: collect the ancestor chain (depth <= 64)
-      int chain[64];
-      int depth = 0;
-      for (int n = leaf; n >= 0 && depth < 64; n = Q.parent[n]) chain[depth++] = n;
       for (int k = depth - 1; k >= 0; --k) {
         const int n = chain[k];
         const int c = cnt[n];
         const Item* it = items + off[n];
         for (int t = 0; t < c; ++t) {
           const int r = it[t].r, order = it[t].code & 0xff;
-          acc += dev_eval_farfield(g, M + (size_t)r * g.T, R.cen + (size_t)r * D, qp, s, order);
+          acc += dev_eval_farfield(g, Mt + (size_t)r * g.T, R.cen + (size_t)r * D, qp, s, order,
+                                   spw);
         }
       }
       if (act) s_ff[qb + qi] = acc;
@@ -545,11 +699,13 @@ __global__ void __launch_bounds__(kBlock) k_farfield(DevSeries g, TreeView Q, Tr
   }
 }
 
-// Local evaluation at the leaves and the final sum (post_process leaf branch and
-// Traversal::run, engine.cpp:273-291, 85-89); results scattered to input order.
+// Local evaluation at the leaves, the base-case partials in task order, and the final
+// sum (post_process leaf branch and Traversal::run, engine.cpp:273-291, 85-89);
+// results scattered to input order.
 __global__ void k_finalize(DevSeries g, TreeView Q, const int* leaf_of_pos, const int* perm, int n,
-                           const double* L, const int* Lord, const double* s_ex,
-                           const double* s_ff, double s, double* out)
+                           const double* L, const int* Lord, const int* cntB,
+                           const int* leaf_task, const double* part, const double* s_ff,
+                           double s, double* out)
 {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -559,7 +715,14 @@ __global__ void k_finalize(DevSeries g, TreeView Q, const int* leaf_of_pos, cons
   if (order > 0)
     loc = dev_eval_local(g, L + (size_t)leaf * g.T, Q.cen + (size_t)leaf * g.D,
                          Q.xs + (size_t)i * g.D, s, order);
-  out[perm[i]] = loc + s_ff[i] + s_ex[i];
+  const int li = i - Q.begin[leaf];
+  const int nic = (cntB[leaf] + kTaskItems - 1) / kTaskItems;
+  double ex = 0.0;
+  if (nic) {
+    const int t0 = leaf_task[leaf] + (li >> 5) * nic;
+    for (int k = 0; k < nic; ++k) ex += part[(size_t)(t0 + k) * 32 + (li & 31)];
+  }
+  out[perm[i]] = loc + s_ff[i] + ex;
 }
 
 __global__ void k_leaf_of_pos(const int* leaves, int nleaves, const int* begin, const int* count,
@@ -675,17 +838,16 @@ void launch_classify(int D, int grid, cudaStream_t s, const TravArgs& a)
   CK_LAUNCH();
 }
 
-void launch_base(int D, int grid, cudaStream_t s, TreeView Q, TreeView R, const int* leaves,
-                 int nleaves, const int* cnt, const int* off, const Item* items, double scale,
-                 double* s_ex)
+void launch_base(int D, int grid, cudaStream_t s, TreeView Q, TreeView R, const BTask* tasks,
+                 int ntasks, const Item* items, double scale, double* part)
 {
   switch (D) {
-  case 1: k_base_case<1><<<grid, kBlock, 0, s>>>(Q, R, D, leaves, nleaves, cnt, off, items, scale, s_ex); break;
-  case 2: k_base_case<2><<<grid, kBlock, 0, s>>>(Q, R, D, leaves, nleaves, cnt, off, items, scale, s_ex); break;
-  case 3: k_base_case<3><<<grid, kBlock, 0, s>>>(Q, R, D, leaves, nleaves, cnt, off, items, scale, s_ex); break;
-  case 4: k_base_case<4><<<grid, kBlock, 0, s>>>(Q, R, D, leaves, nleaves, cnt, off, items, scale, s_ex); break;
-  case 5: k_base_case<5><<<grid, kBlock, 0, s>>>(Q, R, D, leaves, nleaves, cnt, off, items, scale, s_ex); break;
-  default: k_base_case<0><<<grid, kBlock, 0, s>>>(Q, R, D, leaves, nleaves, cnt, off, items, scale, s_ex); break;
+  case 1: k_base_case<1><<<grid, kBlock, 0, s>>>(Q, R, D, tasks, ntasks, items, scale, part); break;
+  case 2: k_base_case<2><<<grid, kBlock, 0, s>>>(Q, R, D, tasks, ntasks, items, scale, part); break;
+  case 3: k_base_case<3><<<grid, kBlock, 0, s>>>(Q, R, D, tasks, ntasks, items, scale, part); break;
+  case 4: k_base_case<4><<<grid, kBlock, 0, s>>>(Q, R, D, tasks, ntasks, items, scale, part); break;
+  case 5: k_base_case<5><<<grid, kBlock, 0, s>>>(Q, R, D, tasks, ntasks, items, scale, part); break;
+  default: k_base_case<0><<<grid, kBlock, 0, s>>>(Q, R, D, tasks, ntasks, items, scale, part); break;
   }
   CK_LAUNCH();
 }
@@ -706,6 +868,7 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
   const int pm = cfg.mode == 0 ? 1 : (cfg.p_max > 0 ? cfg.p_max : default_p_max(D_));
   if (cfg.p_max < 0 || (cfg.mode == 1 && cfg.p_max > 15)) throw InvalidArgument("SeriesGeometry requires dim >= 1 and 1 <= p_max <= 15");
   ser_ = SeriesTables(D_, pm);
+  if (D_ * (pm - 1) >= 128) throw InvalidArgument("D * (p_max - 1) must be < 128");
   if (D_ > kMaxDim) throw InvalidArgument("dimension > 16 is not supported by the device engine");
   CK(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
   for (auto& e : ev_) CK(cudaEventCreate(&e));
@@ -715,6 +878,16 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
   upload_series(ser_, ser_dev_, s_);
   CK(cudaEventRecord(ev_[0], s_));
   build_tree(rt_, x_.p, (int)n, D_, cfg.leaf_threshold, s_);
+  if (cfg.mode == 1) {
+    if (ser_.T <= 4096) {
+      eager_ = true;
+      eager_moments();
+    } else {
+      Mt_.reserve((size_t)rt_.nodes * ser_.T);
+      mdone_.reserve(rt_.nodes);
+      CK(cudaMemsetAsync(mdone_.p, 0, sizeof(int) * rt_.nodes, s_));
+    }
+  }
   CK(cudaEventRecord(ev_[1], s_));
   CK(cudaStreamSynchronize(s_));
   CK(cudaEventElapsedTime(&tim_.tree_ms, ev_[0], ev_[1]));
@@ -914,34 +1087,100 @@ void Engine::traverse(const DevTree& qt, double h)
   sort_items(itB_, nB_, cntB_, offB_, sB_);
 }
 
+// Unscaled moments of every reference node, once per tree (tables <= 4096 terms).
+void Engine::eager_moments()
+{
+  const DevTree& t = rt_;
+  const int K = t.nodes, T = ser_.T;
+  std::vector<int> cnode, cstart, coff(K + 1, 0);
+  for (int n = 0; n < K; ++n) {
+    coff[n] = (int)cnode.size();
+    for (int st = 0; st < t.h_count[n]; st += kMomChunk) {
+      cnode.push_back(n);
+      cstart.push_back(t.h_begin[n] + st);
+    }
+  }
+  coff[K] = (int)cnode.size();
+  const int nch = (int)cnode.size();
+  DevBuf<int> dn, ds, dof;
+  DevBuf<double> part;
+  dn.reserve(nch);
+  ds.reserve(nch);
+  dof.reserve(K + 1);
+  part.reserve((size_t)nch * T);
+  CK(cudaMemcpyAsync(dn.p, cnode.data(), sizeof(int) * nch, cudaMemcpyHostToDevice, s_));
+  CK(cudaMemcpyAsync(ds.p, cstart.data(), sizeof(int) * nch, cudaMemcpyHostToDevice, s_));
+  CK(cudaMemcpyAsync(dof.p, coff.data(), sizeof(int) * (K + 1), cudaMemcpyHostToDevice, s_));
+  Mt_.reserve((size_t)K * T);
+  const DevSeries g = dev_series();
+  const int smem = kMomChunk * D_ * ser_.pmax * (int)sizeof(double);
+  k_moment_chunks<<<std::min(nch, 148 * 16), 128, smem, s_>>>(g, view_of(t), dn.p, ds.p, nch,
+                                                               part.p);
+  CK_LAUNCH();
+  k_moment_reduce<<<std::min(K, 148 * 16), 128, 0, s_>>>(g, K, dof.p, part.p, Mt_.p);
+  CK_LAUNCH();
+  CK(cudaStreamSynchronize(s_));
+}
+
 void Engine::run_phases(const DevTree& qt, double h, double* d_out)
 {
   cudaStream_t s = s_;
   const DevSeries g = dev_series();
   const double sc = inv_scale(h);
   const TreeView Q = view_of(qt), R = view_of(rt_);
-  const int K = qt.nodes;
+  const int K = qt.nodes, T = ser_.T;
   CK(cudaEventRecord(ev_[2], s));
   traverse(qt, h);
   CK(cudaEventRecord(ev_[3], s));
-  // moments of the reference nodes used by F/T items
+  SPow sp;
+  sp.v[0] = 1.0;
+  for (int k = 1; k < 128; ++k) sp.v[k] = sp.v[k - 1] * sc;
+  // moments of the reference nodes used by F/T items (large tables only; small
+  // tables were computed for every node when the engine was built)
   const bool need_m = stats_.prunes_farfield + stats_.prunes_far_to_local > 0;
-  if (need_m) {
+  if (need_m && !eager_) {
     mflag_.reserve(rt_.nodes);
     CK(cudaMemsetAsync(mflag_.p, 0, sizeof(int) * rt_.nodes, s));
-    if (nF_) k_mark_moments<<<ceil_div(nF_, 256), 256, 0, s>>>(sF_.p, (int)nF_, mflag_.p);
-    if (nDT_) k_mark_moments<<<ceil_div(nDT_, 256), 256, 0, s>>>(sDT_.p, (int)nDT_, mflag_.p);
-    M_.reserve((size_t)rt_.nodes * ser_.T);
+    if (nF_) {
+      k_mark_moments<<<ceil_div(nF_, 256), 256, 0, s>>>(sF_.p, (int)nF_, mflag_.p);
+      CK_LAUNCH();
+    }
+    if (nDT_) {
+      k_mark_moments<<<ceil_div(nDT_, 256), 256, 0, s>>>(sDT_.p, (int)nDT_, mflag_.p);
+      CK_LAUNCH();
+    }
     const int smem = 32 * D_ * ser_.pmax * (int)sizeof(double);
-    k_moments<<<std::min(rt_.nodes, 148 * 8), 128, smem, s>>>(g, R, rt_.nodes, mflag_.p, sc, M_.p);
+    k_moments<<<std::min(rt_.nodes, 148 * 8), 128, smem, s>>>(g, R, rt_.nodes, mflag_.p, mdone_.p,
+                                                             Mt_.p);
     CK_LAUNCH();
   }
   CK(cudaEventRecord(ev_[4], s));
-  // D/T items, then L2L down the query tree
+  // D/T items -> chunked partial tables -> per-query-node reduction
   if (nDT_) {
-    const int smem = std::max(32 * D_ * ser_.pmax, D_ * (2 * ser_.pmax)) * (int)sizeof(double);
-    k_local_items<<<std::min(K, 148 * 8), 128, smem, s>>>(g, Q, R, K, cntDT_.p, offDT_.p, sDT_.p,
-                                                           M_.p, sc, L_.p, Lord_.p);
+    lnch_.reserve(nDT_ + 1);
+    lchoff_.reserve(nDT_ + 1);
+    k_local_count<<<ceil_div(nDT_, 256), 256, 0, s>>>(sDT_.p, (int)nDT_, R, lnch_.p);
+    CK_LAUNCH();
+    CK(cudaMemsetAsync(lnch_.p + nDT_, 0, sizeof(int), s));
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, lnch_.p, lchoff_.p, (int)nDT_ + 1, s);
+    scan_tmp_.reserve(need + 256);
+    size_t have = scan_tmp_.cap;
+    cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, lnch_.p, lchoff_.p, (int)nDT_ + 1, s);
+    int nch = 0;
+    CK(cudaMemcpyAsync(&nch, lchoff_.p + nDT_, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    lchunk_.reserve((size_t)nch * 3);
+    LChunk* ch = reinterpret_cast<LChunk*>(lchunk_.p);
+    k_local_fill<<<ceil_div(nDT_, 256), 256, 0, s>>>(sDT_.p, (int)nDT_, R, lchoff_.p, ch);
+    CK_LAUNCH();
+    lpart_.reserve((size_t)nch * T);
+    const int smem = std::max(kLocChunk * D_ * ser_.pmax, D_ * (2 * ser_.pmax)) * (int)sizeof(double);
+    k_local_chunks<<<std::min(nch, 148 * 16), 64, smem, s>>>(g, Q, R, sDT_.p, ch, nch, Mt_.p, sp, sc,
+                                                             lpart_.p);
+    CK_LAUNCH();
+    k_local_reduce<<<std::min(K, 148 * 16), 64, 0, s>>>(g, K, cntDT_.p, offDT_.p, sDT_.p,
+                                                        lchoff_.p, lpart_.p, L_.p, Lord_.p);
     CK_LAUNCH();
   }
   if (stats_.prunes_finite_diff + stats_.prunes_direct_local + stats_.prunes_far_to_local > 0) {
@@ -950,34 +1189,61 @@ void Engine::run_phases(const DevTree& qt, double h, double* d_out)
       const int b = qt.depth_off[d], e = qt.depth_off[d + 1];
       k_l2l<<<std::min(e - b, 148 * 8), 64, smem, s>>>(g, Q, qt.by_depth.p + b, e - b, sc, L_.p,
                                                        Lord_.p);
+      CK_LAUNCH();
     }
-    CK_LAUNCH();
   }
   CK(cudaEventRecord(ev_[5], s));
-  // base cases (dominant kernel)
-  s_ex_.reserve(qt.n);
-  s_ff_.reserve(qt.n);
+  // base-case tasks
   const int nleaves = (int)qleaves_host_.size();
-  launch_base(D_, grid_warps(nleaves), s, Q, R, leaves_.p, nleaves, cntB_.p, offB_.p, sB_.p,
-              -1.0 / (2.0 * h * h), s_ex_.p);
+  int ntasks = 0;
+  if (nB_) {
+    ntask_.reserve(nleaves + 1);
+    toff_.reserve(nleaves + 1);
+    k_task_count<<<ceil_div(nleaves, 256), 256, 0, s>>>(leaves_.p, nleaves, cntB_.p, Q, ntask_.p);
+    CK_LAUNCH();
+    CK(cudaMemsetAsync(ntask_.p + nleaves, 0, sizeof(int), s));
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, ntask_.p, toff_.p, nleaves + 1, s);
+    scan_tmp_.reserve(need + 256);
+    size_t have = scan_tmp_.cap;
+    cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, ntask_.p, toff_.p, nleaves + 1, s);
+    CK(cudaMemcpyAsync(&ntasks, toff_.p + nleaves, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    tasks_.reserve((size_t)ntasks * 4);
+    leaf_task_.reserve(K);
+    k_task_fill<<<ceil_div(nleaves, 256), 256, 0, s>>>(leaves_.p, nleaves, cntB_.p, offB_.p, Q,
+                                                       toff_.p, reinterpret_cast<BTask*>(tasks_.p),
+                                                       leaf_task_.p);
+    CK_LAUNCH();
+    bpart_.reserve((size_t)ntasks * 32);
+  } else {
+    leaf_task_.reserve(K);
+    bpart_.reserve(32);
+  }
+  CK(cudaEventRecord(ev_[9], s));
+  if (ntasks)
+    launch_base(D_, grid_warps(ntasks), s, Q, R, reinterpret_cast<const BTask*>(tasks_.p), ntasks,
+                sB_.p, -1.0 / (2.0 * h * h), bpart_.p);
   CK(cudaEventRecord(ev_[6], s));
+  s_ff_.reserve(qt.n);
   if (nF_) {
     k_farfield<<<grid_warps(nleaves), kBlock, 0, s>>>(g, Q, R, leaves_.p, nleaves, cntF_.p, offF_.p,
-                                                     sF_.p, M_.p, sc, s_ff_.p);
+                                                     sF_.p, Mt_.p, sp, sc, s_ff_.p);
     CK_LAUNCH();
   } else {
     CK(cudaMemsetAsync(s_ff_.p, 0, sizeof(double) * qt.n, s));
   }
   CK(cudaEventRecord(ev_[7], s));
   k_finalize<<<ceil_div(qt.n, 128), 128, 0, s>>>(g, Q, leaf_of_pos_.p, qt.perm.p, qt.n, L_.p,
-                                                 Lord_.p, s_ex_.p, s_ff_.p, sc, d_out);
+                                                 Lord_.p, cntB_.p, leaf_task_.p, bpart_.p, s_ff_.p,
+                                                 sc, d_out);
   CK_LAUNCH();
   CK(cudaEventRecord(ev_[8], s));
   CK(cudaStreamSynchronize(s));
   CK(cudaEventElapsedTime(&tim_.traverse_ms, ev_[2], ev_[3]));
   CK(cudaEventElapsedTime(&tim_.moments_ms, ev_[3], ev_[4]));
   CK(cudaEventElapsedTime(&tim_.local_ms, ev_[4], ev_[5]));
-  CK(cudaEventElapsedTime(&tim_.base_ms, ev_[5], ev_[6]));
+  CK(cudaEventElapsedTime(&tim_.base_ms, ev_[9], ev_[6]));
   CK(cudaEventElapsedTime(&tim_.farfield_ms, ev_[6], ev_[7]));
   CK(cudaEventElapsedTime(&tim_.final_ms, ev_[7], ev_[8]));
   CK(cudaEventElapsedTime(&tim_.total_ms, ev_[2], ev_[8]));

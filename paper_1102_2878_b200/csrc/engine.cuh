@@ -71,6 +71,7 @@ public:
 private:
   void traverse(const DevTree& qt, double h);
   void run_phases(const DevTree& qt, double h, double* d_out);
+  void eager_moments();
 
   Config cfg_;
   int D_ = 0;
@@ -85,8 +86,11 @@ private:
   DevBuf<int> leaves_, leaf_of_pos_;       // per current query tree
   DevBuf<int> rleaves_;
   // per-compute state
-  DevBuf<double> L_, M_, s_ex_, s_ff_;
-  DevBuf<int> Lord_, cntF_, cntDT_, cntB_, offF_, offDT_, offB_, mflag_;
+  DevBuf<double> L_, Mt_, s_ff_;      // Mt_: UNSCALED reference moments (h-independent)
+  DevBuf<int> Lord_, cntF_, cntDT_, cntB_, offF_, offDT_, offB_, mflag_, mdone_;
+  bool eager_ = false;                // Mt_ holds every node (tables <= 4096 terms)
+  DevBuf<int> lnch_, lchoff_, lchunk_, ntask_, toff_, tasks_, leaf_task_;
+  DevBuf<double> lpart_, bpart_;
   // frontier (double buffered) and per-level scratch
   DevBuf<int> fq_[2], foff_[2], flen_[2], fr_[2];
   DevBuf<double> fbase_[2];

@@ -50,15 +50,21 @@ __device__ inline void dev_moments_block(const DevSeries& g, const double* pts, 
 }
 
 // Per thread: sum_{i < order^D} M[i] h_alpha_i((q - c)*s)   (eval_farfield, series.cpp:289-303)
+// spow != nullptr: M holds UNSCALED moments (h-independent) and M[i] * s^|alpha_i|
+// is the reference's scaled moment.
 __device__ inline double dev_eval_farfield(const DevSeries& g, const double* M, const double* c,
-                                           const double* q, double s, int order)
+                                           const double* q, double s, int order,
+                                           const double* spow = nullptr)
 {
   const int D = g.D;
   double H[kMaxDim * kPMaxDev];
   for (int d = 0; d < D; ++d) hermite_row((q[d] - c[d]) * s, order, H + d * kPMaxDev);
   const int n = ipow_i(order, D);
   double sum = 0.0;
-  for (int i = 0; i < n; ++i) sum += M[i] * herm_prod(H, kPMaxDev, D, g.dig[i]);
+  for (int i = 0; i < n; ++i) {
+    const double m = spow ? M[i] * spow[g.degree[i]] : M[i];
+    sum += m * herm_prod(H, kPMaxDev, D, g.dig[i]);
+  }
   return sum;
 }
 
@@ -102,9 +108,11 @@ __device__ inline void dev_direct_local_block(const DevSeries& g, const double* 
 
 // Block-cooperative F2L: L[b] += (-1)^|b|/b! sum_a M[a] h_{a+b}((c_dst - c_src)*s)
 // (trans_far_to_local, series.cpp:328-353).  smem: D*(2*order-1) doubles.
+// With raw != 0 the unsigned sum is written to L[i] instead (partial tables that
+// are reduced and signed later); spow as in dev_eval_farfield.
 __device__ inline void dev_f2l_block(const DevSeries& g, const double* M, const double* src_c,
                                      const double* dst_c, double s, int order, double* L,
-                                     double* smem)
+                                     double* smem, const double* spow = nullptr, int raw = 0)
 {
   const int D = g.D;
   const int n = ipow_i(order, D);
@@ -116,9 +124,40 @@ __device__ inline void dev_f2l_block(const DevSeries& g, const double* M, const 
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const uint64_t b = g.dig[i];
     double acc = 0.0;
-    for (int j = 0; j < n; ++j) acc += M[j] * herm_prod2(smem, ho, D, g.dig[j], b);
-    const double sg = (g.degree[i] & 1) ? -1.0 : 1.0;
-    L[i] += sg * g.invf[i] * acc;
+    for (int j = 0; j < n; ++j) {
+      const double m = spow ? M[j] * spow[g.degree[j]] : M[j];
+      acc += m * herm_prod2(smem, ho, D, g.dig[j], b);
+    }
+    if (raw) {
+      L[i] = acc;
+    } else {
+      const double sg = (g.degree[i] & 1) ? -1.0 : 1.0;
+      L[i] += sg * g.invf[i] * acc;
+    }
+  }
+}
+
+// Unsigned direct-local partial: P[i] = sum_{r in pts} prod_d h_{alpha_i,d}((c - r)*s)
+// for i < order^D (one chunk of a D item; sign and 1/alpha! applied at reduction).
+// smem: npts*D*order doubles (npts <= blockDim-sized chunk).
+__device__ inline void dev_direct_local_partial(const DevSeries& g, const double* pts, int npts,
+                                                const double* c, double s, int order, double* P,
+                                                double* smem)
+{
+  const int D = g.D;
+  const int n = ipow_i(order, D);
+  const int per = D * order;
+  __syncthreads();
+  for (int w = threadIdx.x; w < npts * D; w += blockDim.x) {
+    const int pt = w / D, d = w % D;
+    hermite_row((c[d] - pts[(size_t)pt * D + d]) * s, order, smem + pt * per + d * order);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t a = g.dig[i];
+    double sum = 0.0;
+    for (int pt = 0; pt < npts; ++pt) sum += herm_prod(smem + pt * per, order, D, a);
+    P[i] = sum;
   }
 }
 

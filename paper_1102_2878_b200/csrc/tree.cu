@@ -397,7 +397,7 @@ void build_tree(DevTree& t, const double* d_x, int n, int D, int leaf, cudaStrea
 
   t.perm.reserve(n);
   k_iota<<<ceil_div(n, 256), 256, 0, s>>>(t.perm.p, n);
-  CK_LAUNCH();
+  CK_LAUNCH();  // (counts every launch below too)
 
   DevBuf<int> flag, P, slot;
   flag.reserve((size_t)n + 1);
@@ -447,15 +447,21 @@ void build_tree(DevTree& t, const double* d_x, int n, int D, int leaf, cudaStrea
 
     LevelArgs a{ d_x, D, t.perm.p, d_nbeg.p, d_ncnt.p, d_tnode.p, d_tstart.p, d_kmin.p, d_kmax.p };
     k_bounds_init<<<ceil_div((long long)m * D, 256), 256, 0, s>>>(d_kmin.p, d_kmax.p, m * D);
+    CK_LAUNCH();
     k_bounds_tiles<<<ntiles, kThreads, 0, s>>>(a);
+    CK_LAUNCH();
     k_decide<<<ceil_div(m, 128), 128, 0, s>>>(a, m, leaf, base, blo.p, bhi.p, bcen.p, bside.p,
                                               bsd.p, d_mid.p, d_dosplit.p);
+    CK_LAUNCH();
     // split_dim per level node (for flags) = bsd[base + j]
     CK(cudaMemcpyAsync(d_sd_lvl.p, bsd.p + base, sizeof(int) * m, cudaMemcpyDeviceToDevice, s));
     k_flags<<<ntiles, kThreads, 0, s>>>(a, d_dosplit.p, d_sd_lvl.p, d_mid.p, flag.p);
+    CK_LAUNCH();
     cub::DeviceScan::ExclusiveSum(scan_tmp.p, scan_bytes, flag.p, P.p, n + 1, s);
     k_slots<<<ntiles, kThreads, 0, s>>>(a, d_dosplit.p, flag.p, P.p, slot.p);
+    CK_LAUNCH();
     k_swap<<<ntiles, kThreads, 0, s>>>(a, d_dosplit.p, flag.p, P.p, slot.p);
+    CK_LAUNCH();
     k_finish_split<<<ceil_div(m, 64), 64, 0, s>>>(a, m, base, d_dosplit.p, d_sd_lvl.p, d_mid.p,
                                                   P.p, d_lc.p, bsc.p);
     CK_LAUNCH();
@@ -543,8 +549,10 @@ void build_tree(DevTree& t, const double* d_x, int n, int D, int leaf, cudaStrea
   CK_LAUNCH();
   t.h_count.assign(K, 0);
   t.h_left.assign(K, -1);
+  t.h_begin.assign(K, 0);
   for (int i = 0; i < K; ++i) {
     t.h_count[bfs2pre[i]] = h_cnt[i];
+    t.h_begin[bfs2pre[i]] = h_beg[i];
     t.h_left[bfs2pre[i]] = h_left[i] < 0 ? -1 : bfs2pre[h_left[i]];
   }
   CK(cudaStreamSynchronize(s));

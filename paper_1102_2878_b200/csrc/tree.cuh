@@ -19,6 +19,7 @@ struct DevTree {
   std::vector<int> depth_off; // height+1 offsets into by_depth
   std::vector<int> h_count;   // host copy of count (preorder)
   std::vector<int> h_left;    // host copy of left (preorder)
+  std::vector<int> h_begin;   // host copy of begin (preorder)
 };
 
 // Builds the tree of the n x D row-major device points `d_x` (reference
