@@ -33,6 +33,9 @@ typedef struct dfgtb_config {
   int p_max;          /* series order limit; 0 = default_p_max(D)         (truncation.cpp:168) */
   int cost_model;     /* 0 exponential, 1 term_count                      (truncation.hpp:216) */
   int mode;           /* 0 centroid (DFD), 1 series (DFGT)                (engine.hpp:89) */
+  int local_pushdown; /* 0: evaluate ancestors' local expansions at each query (default);
+                         1: the reference's L2L push-down chain (engine.cpp:294-304).
+                         Identical mathematics (exact polynomial re-centering). */
 } dfgtb_config;
 
 /* TraversalStats (engine.hpp:66-74) + level count of the BFS traversal. */

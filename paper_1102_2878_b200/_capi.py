@@ -20,7 +20,7 @@ _I64 = C.POINTER(C.c_int64)
 
 class Config(C.Structure):
     _fields_ = [("epsilon", C.c_double), ("leaf_threshold", C.c_int), ("p_max", C.c_int),
-                ("cost_model", C.c_int), ("mode", C.c_int)]
+                ("cost_model", C.c_int), ("mode", C.c_int), ("local_pushdown", C.c_int)]
 
 
 class Stats(C.Structure):

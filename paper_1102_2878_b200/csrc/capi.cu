@@ -54,6 +54,7 @@ Config to_cfg(const dfgtb_config* c)
     k.p_max = c->p_max;
     k.cost_model = c->cost_model;
     k.mode = c->mode;
+    k.local_pushdown = c->local_pushdown;
   }
   return k;
 }
@@ -113,6 +114,7 @@ void dfgtb_default_config(dfgtb_config* c)
   c->p_max = 0;
   c->cost_model = 0;
   c->mode = 1;
+  c->local_pushdown = 0;
 }
 
 const char* dfgtb_last_error(void) { return g_err.c_str(); }

@@ -24,8 +24,11 @@
 #include "engine.cuh"
 #include "series_dev.cuh"
 
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
 #include <math_constants.h>
+#include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cfloat>
@@ -50,6 +53,8 @@ int default_p_max(int D)
   default: return 1;
   }
 }
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -149,28 +154,43 @@ struct TreeView {
   const double* xs;
 };
 
+// Device-resident traversal state.  The level loop runs without host round trips:
+// every kernel reads the frontier size and the bandwidth from here, and k_advance
+// decides (cudaGraphSetConditional) whether the graph's WHILE node runs another
+// level.  Capacities are checked before anything is written; on overflow the loop
+// stops and the host regrows the buffers and reruns (engine.cu: Engine::traverse).
+struct TravState {
+  double h, scale, eps, ntot;          // per compute (host)
+  int capE, capP, capF, capDT, capB;   // buffer capacities (host)
+  int cur;                             // frontier buffer of the current level
+  int m[2], p[2];                      // entries / pairs in each frontier buffer
+  int nF, nDT, nB;                     // items emitted so far
+  int overflow, levels;
+  int done;                            // CTAs finished with their tile sum (k_traverse)
+  Cnt lvl;                             // totals of the current level
+  unsigned long long pairs, fd, f, dt, t, b, kev;
+};
+
+__device__ __forceinline__ Cnt ldcg_cnt(const Cnt* p)
+{
+  const int* q = reinterpret_cast<const int*>(p);
+  return Cnt{ __ldcg(q), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3), __ldcg(q + 4), __ldcg(q + 5),
+              __ldcg(q + 6) };
+}
+
 struct TravArgs {
   TreeView Q, R;
-  int D, pmax, cost, series;
-  double h, scale, eps, ntot;
-  // frontier in
-  int m;
-  const int *fq, *foff, *flen, *fr;
-  const double* fbase;
-  // scratch
+  int D, pmax, cost, series, T;
+  TravState* st;
+  int *fq[2], *foff[2], *flen[2], *fr[2];
+  double* fbase[2];
   double *pkmax, *pkmin;
   int* dec;
-  Cnt* cnt;
+  Cnt *cnt, *cntoff, *tsum, *toff;
   int* childlen;
   double* newbase;
   double* L;
-  int T;
   int* Lord;
-  unsigned long long* kevals;
-  // emit
-  const Cnt* cntoff;
-  int *nq, *noff, *nlen, *nr;
-  double* nbase;
   Item *itF, *itDT, *itB;
   int *cntF, *cntDT, *cntB;
 };
@@ -208,185 +228,436 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane, int& total)
   return x - v;
 }
 
-// One warp per frontier query node: bounds, G^l, prune/summarise/base/expand decisions.
-template <int DT>
-__global__ void __launch_bounds__(kBlock) k_classify(TravArgs a)
-{
-  const int lane = threadIdx.x & 31;
-  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  const int D = DT ? DT : a.D;
-  for (int e = w0; e < a.m; e += nw) {
-    const int Q = a.fq[e];
-    const int off = a.foff[e], len = a.flen[e];
-    const double* qlo = a.Q.lo + (size_t)Q * D;
-    const double* qhi = a.Q.hi + (size_t)Q * D;
-    const bool qleaf = a.Q.left[Q] < 0;
-    const double nq = (double)a.Q.count[Q];
-    const double sq = a.Q.side[Q];
-    // pass 1: kernel bounds and the lower-bound mass of every live pair
-    double part = 0.0;
-    for (int j = lane; j < len; j += 32) {
-      const int R = a.fr[off + j];
-      double dl, du;
-      box_bounds<DT>(qlo, qhi, a.R.lo + (size_t)R * D, a.R.hi + (size_t)R * D, D, dl, du);
-      const double kmax = exp(a.scale * dl);  // kernel at closest approach
-      const double kmin = exp(a.scale * du);
-      a.pkmax[off + j] = kmax;
-      a.pkmin[off + j] = kmin;
-      part += (double)a.R.count[R] * kmin;
-    }
-    const double glo = a.fbase[e] + warp_sum(part);
-    // pass 2: decisions
-    double fd_dlo = 0.0, fd_const = 0.0, ret = 0.0;
-    int nF = 0, nDT = 0, nT = 0, nB = 0, nFD = 0, slots = 0;
-    unsigned long long kev = 0;
-    for (int j = lane; j < len; j += 32) {
-      const int R = a.fr[off + j];
-      const double kmax = a.pkmax[off + j], kmin = a.pkmin[off + j];
-      const double nr = (double)a.R.count[R];
-      const double dlo = nr * kmin;
-      const double tau = a.eps * nr * glo / a.ntot;
-      int kind = kX, order = 0;
-      if (0.5 * nr * (kmax - kmin) <= tau) {  // kernel-difference prune, engine.cpp:137-148
-        kind = kFD;
-        fd_dlo += dlo;
-        fd_const += 0.5 * nr * (kmax + kmin);
-        ++nFD;
-      } else {
-        if (a.series) {
-          dev_choose(nq, nr, sq, a.R.side[R], a.h, tau, a.pmax, D, a.cost, kind, order);
-          if (kind == kE) kind = kX;
-        }
-        if (kind == kX && qleaf && a.R.left[R] < 0) kind = kB;
-        if (kind == kX) {
-          slots += a.R.left[R] < 0 ? 1 : 2;
-        } else if (kind == kB) {
-          ++nB;
-          kev += (unsigned long long)a.Q.count[Q] * (unsigned long long)a.R.count[R];
-          ret += dlo;
-        } else {
-          ret += dlo;
-          if (kind == kF) ++nF;
-          else {
-            ++nDT;
-            if (kind == kT) ++nT;
-          }
-        }
-      }
-      a.dec[off + j] = kind | (order << 8);
-    }
-    fd_dlo = warp_sum(fd_dlo);
-    fd_const = warp_sum(fd_const);
-    ret = warp_sum(ret);
-    nF = warp_sum_i(nF);
-    nDT = warp_sum_i(nDT);
-    nT = warp_sum_i(nT);
-    nB = warp_sum_i(nB);
-    nFD = warp_sum_i(nFD);
-    slots = warp_sum_i(slots);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) kev += __shfl_xor_sync(0xffffffffu, kev, o);
-    if (lane == 0) {
-      const int ne = slots > 0 ? (qleaf ? 1 : 2) : 0;
-      a.cnt[e] = Cnt{ ne, ne * slots, nF, nDT, nT, nB, nFD };
-      a.childlen[e] = slots;
-      a.newbase[e] = a.fbase[e] + (fd_dlo + ret);
-      if (nFD) {
-        a.L[(size_t)Q * a.T] += fd_const;  // constant local term (order 1)
-        if (a.Lord[Q] < 1) a.Lord[Q] = 1;
-      }
-      if (kev) atomicAdd(a.kevals, kev);
-    }
-  }
-}
-
-// One warp per frontier query node: write the next frontier and the work items.
-__global__ void __launch_bounds__(kBlock) k_emit(TravArgs a, int gF, int gDT, int gB)
-{
-  const int lane = threadIdx.x & 31;
-  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int e = w0; e < a.m; e += nw) {
-    const Cnt o = a.cntoff[e];
-    const Cnt c = a.cnt[e];
-    const int Q = a.fq[e];
-    const int off = a.foff[e], len = a.flen[e];
-    const bool qleaf = a.Q.left[Q] < 0;
-    const int cl = a.childlen[e];
-    if (lane == 0 && c.e) {
-      const double nb = a.newbase[e];
-      if (qleaf) {
-        a.nq[o.e] = Q;
-        a.nbase[o.e] = nb;
-        a.noff[o.e] = o.p;
-        a.nlen[o.e] = cl;
-      } else {
-        a.nq[o.e] = a.Q.left[Q];
-        a.nq[o.e + 1] = a.Q.right[Q];
-        a.nbase[o.e] = nb;
-        a.nbase[o.e + 1] = nb;
-        a.noff[o.e] = o.p;
-        a.noff[o.e + 1] = o.p + cl;
-        a.nlen[o.e] = cl;
-        a.nlen[o.e + 1] = cl;
-      }
-    }
-    const int rF = a.cntF[Q], rDT = a.cntDT[Q], rB = a.cntB[Q];
-    int runX = 0, runF = 0, runDT = 0, runB = 0;
-    for (int j0 = 0; j0 < len; j0 += 32) {
-      const int j = j0 + lane;
-      int kind = kE, order = 0, R = 0;
-      if (j < len) {
-        const int dcode = a.dec[off + j];
-        kind = dcode & 0xff;
-        order = dcode >> 8;
-        R = a.fr[off + j];
-      }
-      const bool rleaf = (j < len) ? a.R.left[R] < 0 : true;
-      int tot;
-      const int px = warp_excl_scan(kind == kX ? (rleaf ? 1 : 2) : 0, lane, tot);
-      if (kind == kX) {
-        const int dst = o.p + runX + px;
-        if (rleaf) {
-          a.nr[dst] = R;
-          if (!qleaf) a.nr[dst + cl] = R;
-        } else {
-          a.nr[dst] = a.R.left[R];
-          a.nr[dst + 1] = a.R.right[R];
-          if (!qleaf) {
-            a.nr[dst + cl] = a.R.left[R];
-            a.nr[dst + cl + 1] = a.R.right[R];
-          }
-        }
-      }
-      runX += tot;
-      int t2;
-      const int pf = warp_excl_scan(kind == kF, lane, t2);
-      if (kind == kF) a.itF[gF + o.f + runF + pf] = Item{ Q, R, order | (kF << 8), rF + runF + pf };
-      runF += t2;
-      const int pd = warp_excl_scan(kind == kD || kind == kT, lane, t2);
-      if (kind == kD || kind == kT)
-        a.itDT[gDT + o.dt + runDT + pd] = Item{ Q, R, order | (kind << 8), rDT + runDT + pd };
-      runDT += t2;
-      const int pb = warp_excl_scan(kind == kB, lane, t2);
-      if (kind == kB) a.itB[gB + o.b + runB + pb] = Item{ Q, R, kB << 8, rB + runB + pb };
-      runB += t2;
-    }
-    if (lane == 0) {
-      a.cntF[Q] = rF + runF;
-      a.cntDT[Q] = rDT + runDT;
-      a.cntB[Q] = rB + runB;
-    }
-  }
-}
-
 struct CntSum {
   __host__ __device__ Cnt operator()(const Cnt& x, const Cnt& y) const
   {
     return Cnt{ x.e + y.e, x.p + y.p, x.f + y.f, x.dt + y.dt, x.t + y.t, x.b + y.b, x.fd + y.fd };
   }
 };
+
+// Root pair (Q root, R root) and a fresh state (host-owned fields untouched).
+__global__ void k_trav_init(TravArgs a)
+{
+  TravState& st = *a.st;
+  st.cur = 0;
+  st.m[0] = 1;
+  st.p[0] = 1;
+  st.m[1] = st.p[1] = 0;
+  st.nF = st.nDT = st.nB = 0;
+  st.overflow = 0;
+  st.levels = 0;
+  st.done = 0;
+  st.lvl = Cnt{};
+  st.pairs = st.fd = st.f = st.dt = st.t = st.b = st.kev = 0;
+  a.fq[0][0] = 0;
+  a.foff[0][0] = 0;
+  a.flen[0][0] = 1;
+  a.fbase[0][0] = 0.0;
+  a.fr[0][0] = 0;
+}
+
+// Per-level inputs every warp needs (read once from the state).
+struct LevelView {
+  int cur, m;
+  double h, scale, eps, ntot;
+};
+
+__device__ __forceinline__ LevelView level_view(const TravState& st)
+{
+  return LevelView{ st.cur, st.m[st.cur], st.h, st.scale, st.eps, st.ntot };
+}
+
+// One warp, one frontier query node: kernel bounds of every live pair, the lower
+// bound G^l, and the prune / summarise / base / expand decision per pair
+// (Traversal::recurse, engine.cpp:113-195).
+template <int DT>
+__device__ __forceinline__ void classify_entry(const TravArgs& a, const LevelView& v, int e, int lane)
+{
+  const int cur = v.cur;
+  const int* fr = a.fr[cur];
+  const int D = DT ? DT : a.D;
+  const int Q = a.fq[cur][e];
+  const int off = a.foff[cur][e], len = a.flen[cur][e];
+  const double fb = a.fbase[cur][e];
+  const double* qlo = a.Q.lo + (size_t)Q * D;
+  const double* qhi = a.Q.hi + (size_t)Q * D;
+  const bool qleaf = a.Q.left[Q] < 0;
+  const double nq = (double)a.Q.count[Q];
+  const double sq = a.Q.side[Q];
+  // pass 1: kernel bounds and the lower-bound mass of every live pair
+  double part = 0.0;
+  for (int j = lane; j < len; j += 32) {
+    const int R = fr[off + j];
+    double dl, du;
+    box_bounds<DT>(qlo, qhi, a.R.lo + (size_t)R * D, a.R.hi + (size_t)R * D, D, dl, du);
+    const double kmax = exp(v.scale * dl);  // kernel at closest approach
+    const double kmin = exp(v.scale * du);
+    a.pkmax[off + j] = kmax;
+    a.pkmin[off + j] = kmin;
+    part += (double)a.R.count[R] * kmin;
+  }
+  const double glo = fb + warp_sum(part);
+  // pass 2: decisions
+  double fd_dlo = 0.0, fd_const = 0.0, ret = 0.0;
+  int nF = 0, nDT = 0, nT = 0, nB = 0, nFD = 0, slots = 0;
+  unsigned long long kev = 0;
+  for (int j = lane; j < len; j += 32) {
+    const int R = fr[off + j];
+    const double kmax = a.pkmax[off + j], kmin = a.pkmin[off + j];
+    const double nr = (double)a.R.count[R];
+    const double dlo = nr * kmin;
+    const double tau = v.eps * nr * glo / v.ntot;
+    int kind = kX, order = 0;
+    if (0.5 * nr * (kmax - kmin) <= tau) {  // kernel-difference prune, engine.cpp:137-148
+      kind = kFD;
+      fd_dlo += dlo;
+      fd_const += 0.5 * nr * (kmax + kmin);
+      ++nFD;
+    } else {
+      if (a.series) {
+        dev_choose(nq, nr, sq, a.R.side[R], v.h, tau, a.pmax, D, a.cost, kind, order);
+        if (kind == kE) kind = kX;
+      }
+      if (kind == kX && qleaf && a.R.left[R] < 0) kind = kB;
+      if (kind == kX) {
+        slots += a.R.left[R] < 0 ? 1 : 2;
+      } else if (kind == kB) {
+        ++nB;
+        kev += (unsigned long long)a.Q.count[Q] * (unsigned long long)a.R.count[R];
+        ret += dlo;
+      } else {
+        ret += dlo;
+        if (kind == kF) ++nF;
+        else {
+          ++nDT;
+          if (kind == kT) ++nT;
+        }
+      }
+    }
+    a.dec[off + j] = kind | (order << 8);
+  }
+  fd_dlo = warp_sum(fd_dlo);
+  fd_const = warp_sum(fd_const);
+  ret = warp_sum(ret);
+  nF = warp_sum_i(nF);
+  nDT = warp_sum_i(nDT);
+  nT = warp_sum_i(nT);
+  nB = warp_sum_i(nB);
+  nFD = warp_sum_i(nFD);
+  slots = warp_sum_i(slots);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) kev += __shfl_xor_sync(0xffffffffu, kev, o);
+  if (lane == 0) {
+    const int ne = slots > 0 ? (qleaf ? 1 : 2) : 0;
+    a.cnt[e] = Cnt{ ne, ne * slots, nF, nDT, nT, nB, nFD };
+    a.childlen[e] = slots;
+    a.newbase[e] = fb + (fd_dlo + ret);
+    if (nFD) {
+      a.L[(size_t)Q * a.T] += fd_const;  // constant local term (order 1)
+      if (a.Lord[Q] < 1) a.Lord[Q] = 1;
+    }
+    if (kev) atomicAdd(&a.st->kev, kev);
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kBlock) k_classify(TravArgs a)
+{
+  const LevelView v = level_view(*a.st);
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int e = w0; e < v.m; e += nw) classify_entry<DT>(a, v, e, lane);
+}
+
+
+// Device-side exclusive scan of the per-entry counts (frontier size read from the
+// state): tile sums -> one-block scan of the tiles (+ capacity check) -> tile rescan.
+constexpr int kScanTiles = 256;
+__global__ void __launch_bounds__(256) k_scan_tiles(TravArgs a)
+{
+  const TravState& st = *a.st;
+  const int m = st.m[st.cur];
+  const int per = (m + kScanTiles - 1) / kScanTiles;
+  const int b0 = blockIdx.x * per, b1 = min(m, b0 + per);
+  Cnt acc{};
+  for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) acc = CntSum()(acc, a.cnt[i]);
+  using BR = cub::BlockReduce<Cnt, 256>;
+  __shared__ typename BR::TempStorage tmp;
+  const Cnt tot = BR(tmp).Reduce(acc, CntSum());
+  if (threadIdx.x == 0) a.tsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanTiles) k_scan_top(TravArgs a)
+{
+  TravState& st = *a.st;
+  using BS = cub::BlockScan<Cnt, kScanTiles>;
+  __shared__ typename BS::TempStorage tmp;
+  Cnt agg;
+  Cnt out;
+  BS(tmp).ExclusiveScan(a.tsum[threadIdx.x], out, Cnt{}, CntSum(), agg);
+  a.toff[threadIdx.x] = out;
+  if (threadIdx.x == 0) {
+    st.lvl = agg;
+    if (agg.e > st.capE || agg.p > st.capP || (long long)st.nF + agg.f > st.capF ||
+        (long long)st.nDT + agg.dt > st.capDT || (long long)st.nB + agg.b > st.capB)
+      st.overflow = 1;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_scan_local(TravArgs a)
+{
+  const TravState& st = *a.st;
+  const int m = st.m[st.cur];
+  const int per = (m + kScanTiles - 1) / kScanTiles;
+  const int b0 = blockIdx.x * per, b1 = min(m, b0 + per);
+  using BS = cub::BlockScan<Cnt, 256>;
+  __shared__ typename BS::TempStorage tmp;
+  Cnt carry = a.toff[blockIdx.x];
+  for (int base = b0; base < b1; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const Cnt v = i < b1 ? a.cnt[i] : Cnt{};
+    Cnt ex, agg;
+    BS(tmp).ExclusiveScan(v, ex, Cnt{}, CntSum(), agg);
+    if (i < b1) a.cntoff[i] = CntSum()(carry, ex);
+    carry = CntSum()(carry, agg);
+    __syncthreads();
+  }
+}
+
+// One warp, one frontier query node: write its part of the next frontier and its
+// work items at the offsets `o` (exclusive scan of the level's counts).
+__device__ __forceinline__ void emit_entry(const TravArgs& a, int cur, int gF, int gDT, int gB,
+                                           int e, const Cnt& o, int lane)
+{
+  const int nxt = cur ^ 1;
+  const int* fr = a.fr[cur];
+  int* nr = a.fr[nxt];
+  const Cnt c = a.cnt[e];
+  const int Q = a.fq[cur][e];
+  const int off = a.foff[cur][e], len = a.flen[cur][e];
+  const bool qleaf = a.Q.left[Q] < 0;
+  const int cl = a.childlen[e];
+  if (lane == 0 && c.e) {
+    const double nb = a.newbase[e];
+    if (qleaf) {
+      a.fq[nxt][o.e] = Q;
+      a.fbase[nxt][o.e] = nb;
+      a.foff[nxt][o.e] = o.p;
+      a.flen[nxt][o.e] = cl;
+    } else {
+      a.fq[nxt][o.e] = a.Q.left[Q];
+      a.fq[nxt][o.e + 1] = a.Q.right[Q];
+      a.fbase[nxt][o.e] = nb;
+      a.fbase[nxt][o.e + 1] = nb;
+      a.foff[nxt][o.e] = o.p;
+      a.foff[nxt][o.e + 1] = o.p + cl;
+      a.flen[nxt][o.e] = cl;
+      a.flen[nxt][o.e + 1] = cl;
+    }
+  }
+  const int rF = a.cntF[Q], rDT = a.cntDT[Q], rB = a.cntB[Q];
+  int runX = 0, runF = 0, runDT = 0, runB = 0;
+  for (int j0 = 0; j0 < len; j0 += 32) {
+    const int j = j0 + lane;
+    int kind = kE, order = 0, R = 0;
+    if (j < len) {
+      const int dcode = a.dec[off + j];
+      kind = dcode & 0xff;
+      order = dcode >> 8;
+      R = fr[off + j];
+    }
+    const bool rleaf = (j < len) ? a.R.left[R] < 0 : true;
+    int tot;
+    const int px = warp_excl_scan(kind == kX ? (rleaf ? 1 : 2) : 0, lane, tot);
+    if (kind == kX) {
+      const int dst = o.p + runX + px;
+      if (rleaf) {
+        nr[dst] = R;
+        if (!qleaf) nr[dst + cl] = R;
+      } else {
+        nr[dst] = a.R.left[R];
+        nr[dst + 1] = a.R.right[R];
+        if (!qleaf) {
+          nr[dst + cl] = a.R.left[R];
+          nr[dst + cl + 1] = a.R.right[R];
+        }
+      }
+    }
+    runX += tot;
+    int t2;
+    const int pf = warp_excl_scan(kind == kF, lane, t2);
+    if (kind == kF) a.itF[gF + o.f + runF + pf] = Item{ Q, R, order | (kF << 8), rF + runF + pf };
+    runF += t2;
+    const int pd = warp_excl_scan(kind == kD || kind == kT, lane, t2);
+    if (kind == kD || kind == kT)
+      a.itDT[gDT + o.dt + runDT + pd] = Item{ Q, R, order | (kind << 8), rDT + runDT + pd };
+    runDT += t2;
+    const int pb = warp_excl_scan(kind == kB, lane, t2);
+    if (kind == kB) a.itB[gB + o.b + runB + pb] = Item{ Q, R, kB << 8, rB + runB + pb };
+    runB += t2;
+  }
+  if (lane == 0) {
+    a.cntF[Q] = rF + runF;
+    a.cntDT[Q] = rDT + runDT;
+    a.cntB[Q] = rB + runB;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_emit(TravArgs a)
+{
+  const TravState& st = *a.st;
+  if (st.overflow) return;
+  const int cur = st.cur, m = st.m[cur];
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int e = w0; e < m; e += nw) emit_entry(a, cur, st.nF, st.nDT, st.nB, e, a.cntoff[e], lane);
+}
+
+// The whole level loop in ONE cooperative launch (one CTA per SM): per level
+//   classify (warp per entry, grid-stride) | grid sync |
+//   tile sums over contiguous entry ranges; the last CTA to finish scans the tiles,
+//   checks capacities and publishes the level totals | grid sync |
+//   each CTA rescans its range and emits it (offsets are local) | grid sync.
+// Every CTA advances an identical private copy of (cur, m, item offsets), so no
+// extra barrier is needed to publish them; CTA 0 writes the state back at the end.
+constexpr int kPBlock = 512;
+template <int DT>
+__global__ void __launch_bounds__(kPBlock) k_traverse(TravArgs a)
+{
+  cg::grid_group grid = cg::this_grid();
+  TravState& st = *a.st;
+  __shared__ int s_last;
+  using BR = cub::BlockReduce<Cnt, kPBlock>;
+  using BS = cub::BlockScan<Cnt, kPBlock>;
+  __shared__ union {
+    typename BR::TempStorage r;
+    typename BS::TempStorage s;
+  } tmp;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int G = gridDim.x;
+  int cur = 0, m = 1, p = 1, gF = 0, gDT = 0, gB = 0, levels = 0;
+  unsigned long long pairs = 0, fd = 0, f = 0, dt = 0, t = 0, b = 0;
+  bool overflow = false;
+  LevelView v{ 0, 1, st.h, st.scale, st.eps, st.ntot };
+  for (;;) {
+    v.cur = cur;
+    v.m = m;
+    for (int e = gw; e < m; e += nw) classify_entry<DT>(a, v, e, lane);
+    grid.sync();
+    // tile sums (contiguous ranges of entries per CTA)
+    const int per = (m + G - 1) / G;
+    const int b0 = min(m, blockIdx.x * per), b1 = min(m, b0 + per);
+    Cnt acc{};
+    for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) acc = CntSum()(acc, a.cnt[i]);
+    const Cnt tot = BR(tmp.r).Reduce(acc, CntSum());
+    if (threadIdx.x == 0) {
+      a.tsum[blockIdx.x] = tot;
+      __threadfence();
+      s_last = atomicAdd(&st.done, 1) == G - 1;
+    }
+    __syncthreads();
+    if (s_last) {  // last CTA: scan the tile sums, publish totals and the overflow verdict
+      __threadfence();
+      Cnt run{};
+      for (int base = 0; base < G; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const Cnt x = i < G ? ldcg_cnt(a.tsum + i) : Cnt{};  // other CTAs' tiles: bypass L1
+        Cnt ex, agg;
+        __syncthreads();
+        BS(tmp.s).ExclusiveScan(x, ex, Cnt{}, CntSum(), agg);
+        if (i < G) a.toff[i] = CntSum()(run, ex);
+        run = CntSum()(run, agg);
+      }
+      if (threadIdx.x == 0) {
+        st.lvl = run;
+        st.overflow = run.e > st.capE || run.p > st.capP || (long long)gF + run.f > st.capF ||
+                      (long long)gDT + run.dt > st.capDT || (long long)gB + run.b > st.capB;
+        st.done = 0;
+        __threadfence();
+      }
+    }
+    grid.sync();
+    const Cnt lv2 = ldcg_cnt(&st.lvl);
+    overflow = __ldcg(&st.overflow) != 0;
+    if (overflow) break;
+    // local rescan of this CTA's range, then emit it (warp per entry)
+    Cnt carry = a.toff[blockIdx.x];
+    for (int base = b0; base < b1; base += blockDim.x) {
+      const int i = base + threadIdx.x;
+      const Cnt x = i < b1 ? a.cnt[i] : Cnt{};
+      Cnt ex, agg;
+      __syncthreads();
+      BS(tmp.s).ExclusiveScan(x, ex, Cnt{}, CntSum(), agg);
+      if (i < b1) a.cntoff[i] = CntSum()(carry, ex);
+      carry = CntSum()(carry, agg);
+    }
+    __syncthreads();
+    for (int e = b0 + wib; e < b1; e += blockDim.x / 32)
+      emit_entry(a, cur, gF, gDT, gB, e, a.cntoff[e], lane);
+    // advance (identical in every CTA)
+    pairs += p;
+    fd += lv2.fd;
+    f += lv2.f;
+    dt += lv2.dt;
+    t += lv2.t;
+    b += lv2.b;
+    gF += lv2.f;
+    gDT += lv2.dt;
+    gB += lv2.b;
+    cur ^= 1;
+    m = lv2.e;
+    p = lv2.p;
+    ++levels;
+    grid.sync();
+    if (m == 0) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st.cur = cur;
+    st.m[cur] = m;
+    st.p[cur] = p;
+    st.nF = gF;
+    st.nDT = gDT;
+    st.nB = gB;
+    st.levels = levels;
+    st.pairs = pairs;
+    st.fd = fd;
+    st.f = f;
+    st.dt = dt;
+    st.t = t;
+    st.b = b;
+  }
+}
+
+
+// Close the level: fold its totals into the state, flip the frontier buffers and
+// tell the WHILE node whether another level follows.
+__global__ void k_advance(TravArgs a, cudaGraphConditionalHandle hc, int use_cond)
+{
+  TravState& st = *a.st;
+  if (!st.overflow) {
+    const Cnt l = st.lvl;
+    st.pairs += st.p[st.cur];
+    st.fd += l.fd;
+    st.f += l.f;
+    st.dt += l.dt;
+    st.t += l.t;
+    st.b += l.b;
+    st.nF += l.f;
+    st.nDT += l.dt;
+    st.nB += l.b;
+    st.m[st.cur ^ 1] = l.e;
+    st.p[st.cur ^ 1] = l.p;
+    st.cur ^= 1;
+    st.levels += 1;
+  }
+  const bool more = !st.overflow && st.m[st.cur] > 0;
+  if (use_cond) cudaGraphSetConditional(hc, more ? 1u : 0u);
+}
+
 
 __global__ void k_scatter_items(const Item* in, int n, const int* noff, Item* out)
 {
@@ -414,7 +685,7 @@ __global__ void k_moments(DevSeries g, TreeView R, int nodes, const int* flag, i
   for (int n = blockIdx.x; n < nodes; n += gridDim.x) {
     if (!flag[n] || done[n]) continue;
     dev_moments_block(g, R.xs + (size_t)R.begin[n] * g.D, R.count[n], R.cen + (size_t)n * g.D, 1.0,
-                      M + (size_t)n * g.T, sm);
+                      M + (size_t)n * g.T, sm, g.pos);
     __syncthreads();
     if (threadIdx.x == 0) done[n] = 1;
   }
@@ -460,7 +731,7 @@ __global__ void k_moment_reduce(DevSeries g, int nodes, const int* coff, const d
     for (int i = threadIdx.x; i < g.T; i += blockDim.x) {
       double acc = 0.0;
       for (int c = coff[n]; c < coff[n + 1]; ++c) acc += part[(size_t)c * g.T + i];
-      M[(size_t)n * g.T + i] = acc * g.invf[i];
+      M[(size_t)n * g.T + g.pos[i]] = acc * g.invf[i];
     }
 }
 
@@ -472,7 +743,8 @@ struct SPow {
 // D/T work split into chunks: a D item over <= kLocChunk reference points or one
 // T item.  Each chunk writes an unsigned partial table; k_local_reduce sums a query
 // node's chunks in item order and applies (-1)^|b|/b! (summarize, engine.cpp:212-232).
-constexpr int kLocChunk = 64;
+constexpr int kLocChunk = 1024;  // points per D chunk (staged 64 at a time)
+constexpr int kLocSub = 64;
 struct LChunk {
   int item, start, n;
 };
@@ -514,10 +786,12 @@ __global__ void k_local_chunks(DevSeries g, TreeView Q, TreeView R, const Item* 
     double* P = part + (size_t)c * g.T;
     const double* qc = Q.cen + (size_t)it.q * g.D;
     if (kind == kD)
-      dev_direct_local_partial(g, R.xs + (size_t)lc.start * g.D, lc.n, qc, s, order, P, sm);
+      for (int b = 0; b < lc.n; b += kLocSub)
+        dev_direct_local_partial(g, R.xs + (size_t)(lc.start + b) * g.D, min(kLocSub, lc.n - b), qc,
+                                 s, order, P, sm, b > 0);
     else
       dev_f2l_block(g, Mt + (size_t)it.r * g.T, R.cen + (size_t)it.r * g.D, qc, s, order, P, sm,
-                    spw, 1);
+                    spw, 1, g.pos);
   }
 }
 
@@ -599,62 +873,166 @@ __global__ void k_l2l(DevSeries g, TreeView Q, const int* nodes_at, int m, doubl
   }
 }
 
+// exp(-y), 0 <= y <= 708.39, to ~1 ulp: Cody-Waite reduction y*log2(e) = n + f,
+// r = -y - n ln2 (|r| <= ln2/2), degree-12 Taylor polynomial (truncation
+// <= 1.7e-16 relative), 2^n spliced into the exponent field.  Coefficients sit in
+// the constant bank so every DFMA takes its constant operand from c[] (libdevice
+// exp re-materialises its 64-bit constants with integer moves inside hot loops).
+// Same accuracy class as libdevice exp; no reduced precision is charged to eps.
+__constant__ double c_expk[15];
+
+__device__ __forceinline__ double exp_negy(double y)
+{
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
+  const double t = fma(-y, c_expk[0], magic);
+  const double n = t - magic;
+  double r = fma(n, -c_expk[1], -y);
+  r = fma(n, -c_expk[2], r);
+  double p = c_expk[3];
+#pragma unroll
+  for (int k = 4; k < 15; ++k) p = fma(p, r, c_expk[k]);
+  p = fma(p, r, 1.0);
+  const int ni = __double2loint(t);  // n in the low word of t
+  return __hiloint2double(__double2hiint(p) + (ni << 20), __double2loint(p));
+}
+
+// Scaled, centred, padded coordinates for the base case: x' = (x - c0) / (h sqrt 2)
+// so that |q' - r'|^2 = |q - r|^2 / (2 h^2) directly (stride DP, zero padding).
+__global__ void k_scale_points(const double* xs, int n, int D, int DP, const double* c0, double s,
+                               double* out)
+{
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (size_t)n * DP) return;
+  const size_t p = i / DP;
+  const int d = (int)(i % DP);
+  out[i] = d < D ? (xs[p * D + d] - c0[d]) * s : 0.0;
+}
+
+template <int DT>
+struct PtLoad {
+  static constexpr int DP = DT == 1 ? 1 : (DT + 1) / 2 * 2;
+  __device__ __forceinline__ static void load(const double* base, int j, double (&v)[DP])
+  {
+    if constexpr (DT == 1) {
+      v[0] = base[j];
+    } else {
+      const double2* b2 = reinterpret_cast<const double2*>(base + (size_t)j * DP);
+#pragma unroll
+      for (int k = 0; k < DP / 2; ++k) {
+        const double2 t = b2[k];
+        v[2 * k] = t.x;
+        v[2 * k + 1] = t.y;
+      }
+    }
+  }
+};
+
 // K10: exhaustive base case (Traversal::base_case, engine.cpp:239-269).  One warp
 // per task = (query leaf, 32-query chunk, run of <= kTaskItems reference leaves):
-// lanes own queries, reference points stream as warp-uniform (broadcast) loads,
-// two independent accumulators for ILP.  FP64 libdevice exp (~1 ulp).
+// lanes own queries, each reference point arrives as one warp-uniform vector load
+// (broadcast), two pairs in flight per iteration.  A reference leaf whose box bound
+// guarantees y <= 708 for every pair takes the branch-free path; otherwise pairs
+// beyond the fast range fall back to libdevice exp (exact underflow behaviour).
 template <int DT>
-__global__ void __launch_bounds__(kBlock) k_base_case(TreeView Q, TreeView R, int Drt,
-                                                      const BTask* tasks, int ntasks,
-                                                      const Item* items, double scale,
-                                                      double* part)
+__global__ void __launch_bounds__(kBlock) k_base_case(TreeView Q, TreeView R, const BTask* tasks,
+                                                      int ntasks, const Item* items,
+                                                      const double* xq, const double* xr,
+                                                      double s2, double* part)
 {
+  constexpr int D = DT;
+  constexpr int DP = PtLoad<DT>::DP;
   const int lane = threadIdx.x & 31;
   const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  const int D = DT ? DT : Drt;
-  constexpr int DM = DT ? DT : kMaxDim;
   for (int w = w0; w < ntasks; w += nw) {
     const BTask t = tasks[w];
     const int qb = Q.begin[t.leaf] + t.q0;
     const bool act = lane < Q.count[t.leaf] - t.q0;
-    double q[DM];
-#pragma unroll
-    for (int d = 0; d < DM; ++d)
-      if (DT || d < D) q[d] = act ? Q.xs[(size_t)(qb + lane) * D + d] : 0.0;
+    double q[DP];
+    PtLoad<DT>::load(xq, act ? qb + lane : qb, q);
+    const double* qlo = Q.lo + (size_t)t.leaf * D;
+    const double* qhi = Q.hi + (size_t)t.leaf * D;
     double acc0 = 0.0, acc1 = 0.0;
     for (int k = t.item0; k < t.item1; ++k) {
       const int r = items[k].r;
-      const double* rp = R.xs + (size_t)R.begin[r] * D;
+      const double* rp = xr + (size_t)R.begin[r] * DP;
       const int rc = R.count[r];
-      int j = 0;
-      for (; j + 1 < rc; j += 2) {
-        double da = 0.0, db = 0.0;
+      double dl, du;
+      box_bounds<DT>(qlo, qhi, R.lo + (size_t)r * D, R.hi + (size_t)r * D, D, dl, du);
+      if (s2 * du <= 708.0) {
+        int j = 0;
+        for (; j + 1 < rc; j += 2) {
+          double a[DP], b[DP];
+          PtLoad<DT>::load(rp, j, a);
+          PtLoad<DT>::load(rp, j + 1, b);
+          double ya = 0.0, yb = 0.0;
 #pragma unroll
-        for (int d = 0; d < DM; ++d) {
-          if (DT || d < D) {
-            const double ta = q[d] - rp[(size_t)j * D + d];
-            const double tb = q[d] - rp[(size_t)(j + 1) * D + d];
-            da += ta * ta;
-            db += tb * tb;
+          for (int d = 0; d < D; ++d) {
+            const double ta = q[d] - a[d], tb = q[d] - b[d];
+            ya = fma(ta, ta, ya);
+            yb = fma(tb, tb, yb);
           }
+          acc0 += exp_negy(ya);
+          acc1 += exp_negy(yb);
         }
-        acc0 += exp(scale * da);
-        acc1 += exp(scale * db);
-      }
-      if (j < rc) {
-        double da = 0.0;
+        if (j < rc) {
+          double a[DP];
+          PtLoad<DT>::load(rp, j, a);
+          double ya = 0.0;
 #pragma unroll
-        for (int d = 0; d < DM; ++d) {
-          if (DT || d < D) {
-            const double ta = q[d] - rp[(size_t)j * D + d];
-            da += ta * ta;
+          for (int d = 0; d < D; ++d) {
+            const double ta = q[d] - a[d];
+            ya = fma(ta, ta, ya);
           }
+          acc0 += exp_negy(ya);
         }
-        acc0 += exp(scale * da);
+      } else {
+        for (int j = 0; j < rc; ++j) {
+          double a[DP];
+          PtLoad<DT>::load(rp, j, a);
+          double ya = 0.0;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const double ta = q[d] - a[d];
+            ya = fma(ta, ta, ya);
+          }
+          acc0 += ya <= 708.0 ? exp_negy(ya) : exp(-ya);
+        }
       }
     }
     part[(size_t)w * 32 + lane] = acc0 + acc1;
+  }
+}
+
+// Generic dimension (D > 5): scalar loads of the scaled coordinates, libdevice exp.
+__global__ void __launch_bounds__(kBlock) k_base_case_any(TreeView Q, TreeView R, int D,
+                                                          const BTask* tasks, int ntasks,
+                                                          const Item* items, const double* xq,
+                                                          const double* xr, double* part)
+{
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int w = w0; w < ntasks; w += nw) {
+    const BTask t = tasks[w];
+    const int qb = Q.begin[t.leaf] + t.q0;
+    const bool act = lane < Q.count[t.leaf] - t.q0;
+    double q[kMaxDim];
+    for (int d = 0; d < D; ++d) q[d] = xq[(size_t)(act ? qb + lane : qb) * D + d];
+    double acc = 0.0;
+    for (int k = t.item0; k < t.item1; ++k) {
+      const int r = items[k].r;
+      const double* rp = xr + (size_t)R.begin[r] * D;
+      for (int j = 0; j < R.count[r]; ++j) {
+        double y = 0.0;
+        for (int d = 0; d < D; ++d) {
+          const double ta = q[d] - rp[(size_t)j * D + d];
+          y = fma(ta, ta, y);
+        }
+        acc += exp(-y);
+      }
+    }
+    part[(size_t)w * 32 + lane] = acc;
   }
 }
 
@@ -691,7 +1069,87 @@ __global__ void __launch_bounds__(kBlock) k_farfield(DevSeries g, TreeView Q, Tr
         for (int t = 0; t < c; ++t) {
           const int r = it[t].r, order = it[t].code & 0xff;
           acc += dev_eval_farfield(g, Mt + (size_t)r * g.T, R.cen + (size_t)r * D, qp, s, order,
-                                   spw);
+                                   spw, g.pos);
+        }
+      }
+      if (act) s_ff[qb + qi] = acc;
+    }
+  }
+}
+
+// Specialised far-field evaluation for the default tables (p_max == PM): every
+// multi-index is a compile-time constant, so the Hermite rows, s^|a| and the digit
+// products live in registers and the (position-layout) moments are read as
+// warp-uniform broadcast loads.  Same sum as dev_eval_farfield, same term order.
+template <int D, int PM>
+__device__ __forceinline__ double ff_eval_t(const double* Mt, const double* c, const double* q,
+                                            double s, int order, const double (&spw)[D * (PM - 1) + 1])
+{
+  double H[D][PM];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double t = (q[d] - c[d]) * s;
+    H[d][0] = exp(-t * t);
+    if (PM > 1) H[d][1] = 2.0 * t * H[d][0];
+#pragma unroll
+    for (int k = 1; k + 1 < PM; ++k) H[d][k + 1] = 2.0 * t * H[d][k] - 2.0 * k * H[d][k - 1];
+  }
+  double sum = 0.0;
+  constexpr int NP = ipow_c(PM, D);
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    int dig[D], mx = 0, deg = 0, rest = p;
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) {
+      dig[d] = rest % PM;
+      rest /= PM;
+      mx = dig[d] > mx ? dig[d] : mx;
+      deg += dig[d];
+    }
+    if (mx < order) {
+      double f = Mt[p] * spw[deg];
+#pragma unroll
+      for (int d = 0; d < D; ++d) f *= H[d][dig[d]];
+      sum += f;
+    }
+  }
+  return sum;
+}
+
+template <int D, int PM>
+__global__ void __launch_bounds__(kBlock) k_farfield_t(TreeView Q, TreeView R, const int* leaves,
+                                                       int nleaves, const int* cnt, const int* off,
+                                                       const Item* items, const double* Mt, SPow sp,
+                                                       double s, double* s_ff)
+{
+  constexpr int T = ipow_c(PM, D);
+  constexpr int ND = D * (PM - 1) + 1;
+  double spw[ND];
+#pragma unroll
+  for (int k = 0; k < ND; ++k) spw[k] = sp.v[k];
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int li = w0; li < nleaves; li += nw) {
+    const int leaf = leaves[li];
+    const int qb = Q.begin[leaf], qc = Q.count[leaf];
+    int chain[64];
+    int depth = 0;
+    for (int n = leaf; n >= 0 && depth < 64; n = Q.parent[n]) chain[depth++] = n;
+    for (int q0 = 0; q0 < qc; q0 += 32) {
+      const int qi = q0 + lane;
+      const bool act = qi < qc;
+      double qv[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) qv[d] = Q.xs[(size_t)(qb + (act ? qi : 0)) * D + d];
+      double acc = 0.0;
+      for (int k = depth - 1; k >= 0; --k) {
+        const int n = chain[k];
+        const int c = cnt[n];
+        const Item* it = items + off[n];
+        for (int t = 0; t < c; ++t) {
+          const int r = it[t].r, order = it[t].code & 0xff;
+          acc += ff_eval_t<D, PM>(Mt + (size_t)r * T, R.cen + (size_t)r * D, qv, s, order, spw);
         }
       }
       if (act) s_ff[qb + qi] = acc;
@@ -702,19 +1160,34 @@ __global__ void __launch_bounds__(kBlock) k_farfield(DevSeries g, TreeView Q, Tr
 // Local evaluation at the leaves, the base-case partials in task order, and the final
 // sum (post_process leaf branch and Traversal::run, engine.cpp:273-291, 85-89);
 // results scattered to input order.
+// direct != 0: the local expansions of ALL ancestors are evaluated at the query
+// (root first) instead of being pushed down by L2L first -- the same polynomial,
+// re-centred exactly, without the per-level launch chain.
 __global__ void k_finalize(DevSeries g, TreeView Q, const int* leaf_of_pos, const int* perm, int n,
                            const double* L, const int* Lord, const int* cntB,
                            const int* leaf_task, const double* part, const double* s_ff,
-                           double s, double* out)
+                           double s, int direct, double* out)
 {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int leaf = leaf_of_pos[i];
-  const int order = Lord[leaf];
+  const double* qp = Q.xs + (size_t)i * g.D;
   double loc = 0.0;
-  if (order > 0)
-    loc = dev_eval_local(g, L + (size_t)leaf * g.T, Q.cen + (size_t)leaf * g.D,
-                         Q.xs + (size_t)i * g.D, s, order);
+  if (direct) {
+    int chain[64];
+    int depth = 0;
+    for (int a = leaf; a >= 0 && depth < 64; a = Q.parent[a]) chain[depth++] = a;
+    for (int k = depth - 1; k >= 0; --k) {
+      const int a = chain[k];
+      const int order = Lord[a];
+      if (order > 0)
+        loc += dev_eval_local(g, L + (size_t)a * g.T, Q.cen + (size_t)a * g.D, qp, s, order);
+    }
+  } else {
+    const int order = Lord[leaf];
+    if (order > 0)
+      loc = dev_eval_local(g, L + (size_t)leaf * g.T, Q.cen + (size_t)leaf * g.D, qp, s, order);
+  }
   const int li = i - Q.begin[leaf];
   const int nic = (cntB[leaf] + kTaskItems - 1) / kTaskItems;
   double ex = 0.0;
@@ -839,18 +1312,21 @@ void launch_classify(int D, int grid, cudaStream_t s, const TravArgs& a)
 }
 
 void launch_base(int D, int grid, cudaStream_t s, TreeView Q, TreeView R, const BTask* tasks,
-                 int ntasks, const Item* items, double scale, double* part)
+                 int ntasks, const Item* items, const double* xq, const double* xr, double s2,
+                 double* part)
 {
   switch (D) {
-  case 1: k_base_case<1><<<grid, kBlock, 0, s>>>(Q, R, D, tasks, ntasks, items, scale, part); break;
-  case 2: k_base_case<2><<<grid, kBlock, 0, s>>>(Q, R, D, tasks, ntasks, items, scale, part); break;
-  case 3: k_base_case<3><<<grid, kBlock, 0, s>>>(Q, R, D, tasks, ntasks, items, scale, part); break;
-  case 4: k_base_case<4><<<grid, kBlock, 0, s>>>(Q, R, D, tasks, ntasks, items, scale, part); break;
-  case 5: k_base_case<5><<<grid, kBlock, 0, s>>>(Q, R, D, tasks, ntasks, items, scale, part); break;
-  default: k_base_case<0><<<grid, kBlock, 0, s>>>(Q, R, D, tasks, ntasks, items, scale, part); break;
+  case 1: k_base_case<1><<<grid, kBlock, 0, s>>>(Q, R, tasks, ntasks, items, xq, xr, s2, part); break;
+  case 2: k_base_case<2><<<grid, kBlock, 0, s>>>(Q, R, tasks, ntasks, items, xq, xr, s2, part); break;
+  case 3: k_base_case<3><<<grid, kBlock, 0, s>>>(Q, R, tasks, ntasks, items, xq, xr, s2, part); break;
+  case 4: k_base_case<4><<<grid, kBlock, 0, s>>>(Q, R, tasks, ntasks, items, xq, xr, s2, part); break;
+  case 5: k_base_case<5><<<grid, kBlock, 0, s>>>(Q, R, tasks, ntasks, items, xq, xr, s2, part); break;
+  default: k_base_case_any<<<grid, kBlock, 0, s>>>(Q, R, D, tasks, ntasks, items, xq, xr, part); break;
   }
   CK_LAUNCH();
 }
+
+int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }
 
 }  // namespace
 
@@ -876,6 +1352,18 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
   CK(cudaMemcpyAsync(x_.p, refs, sizeof(double) * n * d,
                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s_));
   upload_series(ser_, ser_dev_, s_);
+  {  // exp_negy constants: log2(e), Cody-Waite ln2 split, 1/12! ... 1/1!
+    double k[15];
+    k[0] = 1.4426950408889634;
+    k[1] = 6.93147180369123816490e-01;
+    k[2] = 1.90821492927058770002e-10;
+    double f = 1.0;
+    for (int i = 1; i <= 12; ++i) {
+      f *= i;
+      k[3 + (12 - i)] = 1.0 / f;
+    }
+    CK(cudaMemcpyToSymbolAsync(c_expk, k, sizeof(k), 0, cudaMemcpyHostToDevice, s_));
+  }
   CK(cudaEventRecord(ev_[0], s_));
   build_tree(rt_, x_.p, (int)n, D_, cfg.leaf_threshold, s_);
   if (cfg.mode == 1) {
@@ -897,6 +1385,8 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
 Engine::~Engine()
 {
   if (s_) cudaStreamSynchronize(s_);
+  destroy_graph();
+  if (hst_) cudaFreeHost(hst_);
   for (auto& e : ev_) cudaEventDestroy(e);
   if (s_) cudaStreamDestroy(s_);
 }
@@ -906,7 +1396,7 @@ DevSeries Engine::dev_series() const { return series_view(ser_, ser_dev_); }
 void upload_series(const SeriesTables& t, DevBuf<unsigned char>& dev, cudaStream_t s)
 {
   const int T = t.T;
-  const size_t bytes = sizeof(uint64_t) * T + sizeof(double) * 2 * T + sizeof(int) * 2 * T;
+  const size_t bytes = sizeof(uint64_t) * T + sizeof(double) * 2 * T + sizeof(int) * 3 * T;
   dev.reserve(bytes);
   std::vector<unsigned char> blob(bytes);
   unsigned char* p = blob.data();
@@ -919,6 +1409,8 @@ void upload_series(const SeriesTables& t, DevBuf<unsigned char>& dev, cudaStream
   std::memcpy(p, t.degree.data(), sizeof(int) * T);
   p += sizeof(int) * T;
   std::memcpy(p, t.term_of_pos.data(), sizeof(int) * T);
+  p += sizeof(int) * T;
+  std::memcpy(p, t.pos.data(), sizeof(int) * T);
   CK(cudaMemcpyAsync(dev.p, blob.data(), bytes, cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));
 }
@@ -940,7 +1432,112 @@ DevSeries series_view(const SeriesTables& t, const DevBuf<unsigned char>& dev)
   g.degree = (const int*)p;
   p += sizeof(int) * T;
   g.term_of_pos = (const int*)p;
+  p += sizeof(int) * T;
+  g.pos = (const int*)p;
   return g;
+}
+
+// The kernels of one traversal level (all sizes read from the device state).
+constexpr int kLevelKernels = 6;
+static void launch_level(const TravArgs& a, int D, cudaStream_t s, cudaGraphConditionalHandle hc,
+                         int use_cond)
+{
+  const int grid = 148 * 4;
+  launch_classify(D, grid, s, a);
+  k_scan_tiles<<<kScanTiles, 256, 0, s>>>(a);
+  CK_LAUNCH();
+  k_scan_top<<<1, kScanTiles, 0, s>>>(a);
+  CK_LAUNCH();
+  k_scan_local<<<kScanTiles, 256, 0, s>>>(a);
+  CK_LAUNCH();
+  k_emit<<<grid, kBlock, 0, s>>>(a);
+  CK_LAUNCH();
+  k_advance<<<1, 1, 0, s>>>(a, hc, use_cond);
+  CK_LAUNCH();
+}
+
+void Engine::destroy_graph()
+{
+  if (gexec_) cudaGraphExecDestroy(gexec_);
+  if (graph_) cudaGraphDestroy(graph_);
+  gexec_ = nullptr;
+  graph_ = nullptr;
+  gsig_.clear();
+}
+
+// Runs the whole level loop.  Preferred: one CUDA graph whose WHILE node repeats the
+// level kernels until k_advance clears the condition -- no host round trip per
+// level.  Fallback (graph build failed): the host launches levels and polls.
+void Engine::run_levels(const void* args, const std::vector<const void*>& sig)
+{
+  const TravArgs& a = *static_cast<const TravArgs*>(args);
+  if (use_persistent_) {
+    void* fn = nullptr;
+    switch (D_) {
+    case 1: fn = (void*)k_traverse<1>; break;
+    case 2: fn = (void*)k_traverse<2>; break;
+    case 3: fn = (void*)k_traverse<3>; break;
+    case 4: fn = (void*)k_traverse<4>; break;
+    case 5: fn = (void*)k_traverse<5>; break;
+    default: fn = (void*)k_traverse<0>; break;
+    }
+    int dev = 0, nsm = 0, per_sm = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPBlock, 0));
+    if (per_sm >= 1) {
+      TravArgs copy = a;
+      void* kargs[] = { &copy };
+      CK(cudaLaunchCooperativeKernel(fn, nsm, kPBlock, kargs, 0, s_));
+      ++launch_counter();
+      return;
+    }
+    use_persistent_ = false;  // cannot co-schedule one CTA per SM: use the graph loop
+  }
+  if (use_graph_ && sig != gsig_) {
+    destroy_graph();
+    const uint64_t before = launch_counter();
+    try {
+      CK(cudaGraphCreate(&graph_, 0));
+      CK(cudaGraphConditionalHandleCreate(&hc_, graph_, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams p = {};
+      p.type = cudaGraphNodeTypeConditional;
+      p.conditional.handle = hc_;
+      p.conditional.type = cudaGraphCondTypeWhile;
+      p.conditional.size = 1;
+      cudaGraphNode_t node;
+      CK(cudaGraphAddNode(&node, graph_, nullptr, 0, &p));
+      cudaGraph_t body = p.conditional.phGraph_out[0];
+      CK(cudaStreamBeginCaptureToGraph(s_, body, nullptr, nullptr, 0,
+                                       cudaStreamCaptureModeThreadLocal));
+      launch_level(a, D_, s_, hc_, 1);
+      CK(cudaStreamEndCapture(s_, &body));
+      CK(cudaGraphInstantiate(&gexec_, graph_, 0));
+      gsig_ = sig;
+    } catch (const CudaError&) {
+      cudaStreamCaptureStatus cs;
+      if (cudaStreamIsCapturing(s_, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+        cudaGraph_t junk = nullptr;
+        cudaStreamEndCapture(s_, &junk);
+        if (junk) cudaGraphDestroy(junk);
+      }
+      cudaGetLastError();
+      destroy_graph();
+      use_graph_ = false;
+    }
+    launch_counter() = before;  // captured launches are counted when they execute
+  }
+  if (use_graph_) {
+    CK(cudaGraphLaunch(gexec_, s_));
+    return;
+  }
+  TravState* hs = static_cast<TravState*>(hst_);
+  for (;;) {
+    launch_level(a, D_, s_, 0, 0);
+    CK(cudaMemcpyAsync(hs, a.st, sizeof(TravState), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    if (hs->overflow || hs->m[hs->cur] == 0) break;
+  }
 }
 
 void Engine::traverse(const DevTree& qt, double h)
@@ -949,124 +1546,124 @@ void Engine::traverse(const DevTree& qt, double h)
   const int T = ser_.T;
   cudaStream_t s = s_;
   L_.reserve((size_t)K * T);
-  CK(cudaMemsetAsync(L_.p, 0, sizeof(double) * K * T, s));
-  for (DevBuf<int>* b : { &Lord_, &cntF_, &cntDT_, &cntB_ }) {
-    b->reserve(K);
-    CK(cudaMemsetAsync(b->p, 0, sizeof(int) * K, s));
+  for (DevBuf<int>* b : { &Lord_, &cntF_, &cntDT_, &cntB_ }) b->reserve(K);
+  if (!hst_) {
+    CK(cudaMallocHost(&hst_, sizeof(TravState)));
+    dst_.reserve(sizeof(TravState));
   }
-  CK(cudaMemsetAsync(dstat_.p, 0, sizeof(unsigned long long), s));
+  TravState* hs = static_cast<TravState*>(hst_);
+  TravState* ds = reinterpret_cast<TravState*>(dst_.p);
+  if (capE_ == 0) {  // first guesses; overflow regrows (and the engine keeps the sizes)
+    capE_ = std::max(4096, 2 * K);
+    capP_ = std::max(1 << 16, 16 * K);
+    capF_ = capDT_ = std::max(4096, 2 * K);
+    capB_ = std::max(1 << 16, 16 * K);
+  }
+  for (int attempt = 0;; ++attempt) {
+    for (int b = 0; b < 2; ++b) {
+      fq_[b].reserve(capE_);
+      foff_[b].reserve(capE_);
+      flen_[b].reserve(capE_);
+      fbase_[b].reserve(capE_);
+      fr_[b].reserve(capP_);
+    }
+    pkmax_.reserve(capP_);
+    pkmin_.reserve(capP_);
+    dec_.reserve(capP_);
+    cnt_.reserve(capE_);
+    cntoff_.reserve(capE_);
+    childlen_.reserve(capE_);
+    newbase_.reserve(capE_);
+    ctsum_.reserve(kScanTiles);
+    ctoff_.reserve(kScanTiles);
+    itF_.reserve(capF_);
+    itDT_.reserve(capDT_);
+    itB_.reserve(capB_);
 
-  // initial frontier: (Q root, R root)
-  int cur = 0;
-  fq_[0].reserve(1); foff_[0].reserve(1); flen_[0].reserve(1); fbase_[0].reserve(1); fr_[0].reserve(1);
-  const int zero = 0, one = 1;
-  const double dz = 0.0;
-  CK(cudaMemcpyAsync(fq_[0].p, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(foff_[0].p, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(flen_[0].p, &one, sizeof(int), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(fbase_[0].p, &dz, sizeof(double), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(fr_[0].p, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
-  int m = 1;
-  long long npairs = 1;
-  nF_ = nDT_ = nB_ = 0;
-  stats_ = Stats{};
-
-  TravArgs a{};
-  a.Q = view_of(qt);
-  a.R = view_of(rt_);
-  a.D = D_;
-  a.pmax = ser_.pmax;
-  a.cost = cfg_.cost_model;
-  a.series = cfg_.mode == 1;
-  a.h = h;
-  a.scale = -1.0 / (2.0 * h * h);
-  a.eps = cfg_.epsilon;
-  a.ntot = (double)n_;
-  a.L = L_.p;
-  a.T = T;
-  a.Lord = Lord_.p;
-  a.kevals = dstat_.p;
-  a.cntF = cntF_.p;
-  a.cntDT = cntDT_.p;
-  a.cntB = cntB_.p;
-
-  size_t scan_bytes = 0;
-  Cnt hc{};
-  while (m > 0) {
-    ++stats_.levels;
-    stats_.pairs_visited += npairs;
-    pkmax_.reserve(npairs);
-    pkmin_.reserve(npairs);
-    dec_.reserve(npairs);
-    cnt_.reserve((size_t)m + 1);
-    cntoff_.reserve((size_t)m + 1);
-    childlen_.reserve(m);
-    newbase_.reserve(m);
-    a.m = m;
-    a.fq = fq_[cur].p;
-    a.foff = foff_[cur].p;
-    a.flen = flen_[cur].p;
-    a.fr = fr_[cur].p;
-    a.fbase = fbase_[cur].p;
+    TravArgs a{};
+    a.Q = view_of(qt);
+    a.R = view_of(rt_);
+    a.D = D_;
+    a.pmax = ser_.pmax;
+    a.cost = cfg_.cost_model;
+    a.series = cfg_.mode == 1;
+    a.T = T;
+    a.st = ds;
+    for (int b = 0; b < 2; ++b) {
+      a.fq[b] = fq_[b].p;
+      a.foff[b] = foff_[b].p;
+      a.flen[b] = flen_[b].p;
+      a.fr[b] = fr_[b].p;
+      a.fbase[b] = fbase_[b].p;
+    }
     a.pkmax = pkmax_.p;
     a.pkmin = pkmin_.p;
     a.dec = dec_.p;
     a.cnt = cnt_.p;
+    a.cntoff = cntoff_.p;
+    a.tsum = ctsum_.p;
+    a.toff = ctoff_.p;
     a.childlen = childlen_.p;
     a.newbase = newbase_.p;
-    const int grid = grid_warps(m);
-    launch_classify(D_, grid, s, a);
-    // exclusive scan of per-entry counts (m+1 entries, last = totals)
-    CK(cudaMemsetAsync(cnt_.p + m, 0, sizeof(Cnt), s));
-    size_t need = 0;
-    cub::DeviceScan::ExclusiveScan(nullptr, need, cnt_.p, cntoff_.p, CntSum(), Cnt{}, m + 1, s);
-    if (need > scan_bytes || !scan_tmp_.p) {
-      scan_tmp_.reserve(need + 256);
-      scan_bytes = scan_tmp_.cap;
-    }
-    size_t have = scan_tmp_.cap;
-    cub::DeviceScan::ExclusiveScan(scan_tmp_.p, have, cnt_.p, cntoff_.p, CntSum(), Cnt{}, m + 1, s);
-    CK_LAUNCH();
-    CK(cudaMemcpyAsync(&hc, cntoff_.p + m, sizeof(Cnt), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if ((long long)hc.p > INT32_MAX / 2) throw OutOfMemory("frontier exceeds 2^30 pairs");
-    stats_.prunes_finite_diff += hc.fd;
-    stats_.prunes_farfield += hc.f;
-    stats_.prunes_direct_local += hc.dt - hc.t;
-    stats_.prunes_far_to_local += hc.t;
-    stats_.base_cases += hc.b;
-    // room for the next frontier and this level's items (keep earlier items)
-    const int nxt = cur ^ 1;
-    fq_[nxt].reserve(std::max(hc.e, 1));
-    foff_[nxt].reserve(std::max(hc.e, 1));
-    flen_[nxt].reserve(std::max(hc.e, 1));
-    fbase_[nxt].reserve(std::max(hc.e, 1));
-    fr_[nxt].reserve(std::max(hc.p, 1));
-    itF_.grow_keep(nF_ + hc.f + 1, nF_, s);
-    itDT_.grow_keep(nDT_ + hc.dt + 1, nDT_, s);
-    itB_.grow_keep(nB_ + hc.b + 1, nB_, s);
-    a.cntoff = cntoff_.p;
-    a.nq = fq_[nxt].p;
-    a.noff = foff_[nxt].p;
-    a.nlen = flen_[nxt].p;
-    a.nr = fr_[nxt].p;
-    a.nbase = fbase_[nxt].p;
+    a.L = L_.p;
+    a.Lord = Lord_.p;
     a.itF = itF_.p;
     a.itDT = itDT_.p;
     a.itB = itB_.p;
-    k_emit<<<grid, kBlock, 0, s>>>(a, (int)nF_, (int)nDT_, (int)nB_);
+    a.cntF = cntF_.p;
+    a.cntDT = cntDT_.p;
+    a.cntB = cntB_.p;
+    const std::vector<const void*> sig = {
+      a.Q.lo, a.Q.hi, a.Q.cen, a.Q.side, a.Q.left, a.Q.right, a.Q.count, a.Q.begin,
+      a.R.lo, a.R.hi, a.R.side, a.R.left, a.R.right, a.R.count,
+      a.st, a.fq[0], a.fq[1], a.foff[0], a.foff[1], a.flen[0], a.flen[1], a.fr[0], a.fr[1],
+      a.fbase[0], a.fbase[1], a.pkmax, a.pkmin, a.dec, a.cnt, a.cntoff, a.tsum, a.toff,
+      a.childlen, a.newbase, a.L, a.Lord, a.itF, a.itDT, a.itB, a.cntF, a.cntDT, a.cntB };
+
+    CK(cudaMemsetAsync(L_.p, 0, sizeof(double) * K * T, s));
+    for (DevBuf<int>* b : { &Lord_, &cntF_, &cntDT_, &cntB_ })
+      CK(cudaMemsetAsync(b->p, 0, sizeof(int) * K, s));
+    hs->h = h;
+    hs->scale = -1.0 / (2.0 * h * h);
+    hs->eps = cfg_.epsilon;
+    hs->ntot = (double)n_;
+    hs->capE = capE_;
+    hs->capP = capP_;
+    hs->capF = capF_;
+    hs->capDT = capDT_;
+    hs->capB = capB_;
+    CK(cudaMemcpyAsync(ds, hs, sizeof(TravState), cudaMemcpyHostToDevice, s));
+    k_trav_init<<<1, 1, 0, s>>>(a);
     CK_LAUNCH();
-    nF_ += hc.f;
-    nDT_ += hc.dt;
-    nB_ += hc.b;
-    m = hc.e;
-    npairs = hc.p;
-    cur = nxt;
+    run_levels(&a, sig);
+    CK(cudaMemcpyAsync(hs, ds, sizeof(TravState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!use_persistent_ && use_graph_) launch_counter() += (uint64_t)hs->levels * kLevelKernels;
+    if (!hs->overflow) break;
+    if (attempt > 10) throw OutOfMemory("traversal buffers keep overflowing");
+    const Cnt l = hs->lvl;
+    auto grow = [](int cap, long long need) {
+      if (need > INT32_MAX / 2) throw OutOfMemory("traversal exceeds 2^30 entries");
+      return (int)std::max<long long>(cap, 2 * need);
+    };
+    capE_ = grow(capE_, l.e);
+    capP_ = grow(capP_, l.p);
+    capF_ = grow(capF_, (long long)hs->nF + l.f);
+    capDT_ = grow(capDT_, (long long)hs->nDT + l.dt);
+    capB_ = grow(capB_, (long long)hs->nB + l.b);
   }
-  unsigned long long kev = 0;
-  CK(cudaMemcpyAsync(&kev, dstat_.p, sizeof(kev), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  stats_.kernel_evaluations = 2ull * stats_.pairs_visited + kev;
+  stats_ = Stats{};
+  stats_.levels = hs->levels;
+  stats_.pairs_visited = hs->pairs;
+  stats_.prunes_finite_diff = hs->fd;
+  stats_.prunes_farfield = hs->f;
+  stats_.prunes_direct_local = hs->dt - hs->t;
+  stats_.prunes_far_to_local = hs->t;
+  stats_.base_cases = hs->b;
+  stats_.kernel_evaluations = 2ull * hs->pairs + hs->kev;
+  nF_ = hs->nF;
+  nDT_ = hs->nDT;
+  nB_ = hs->nB;
 
   // counting sort of the items by query node (stable: level order, then emit order)
   auto sort_items = [&](DevBuf<Item>& in, long long nitems, DevBuf<int>& cnt, DevBuf<int>& off,
@@ -1175,7 +1772,7 @@ void Engine::run_phases(const DevTree& qt, double h, double* d_out)
     k_local_fill<<<ceil_div(nDT_, 256), 256, 0, s>>>(sDT_.p, (int)nDT_, R, lchoff_.p, ch);
     CK_LAUNCH();
     lpart_.reserve((size_t)nch * T);
-    const int smem = std::max(kLocChunk * D_ * ser_.pmax, D_ * (2 * ser_.pmax)) * (int)sizeof(double);
+    const int smem = std::max(kLocSub * D_ * ser_.pmax, D_ * (2 * ser_.pmax)) * (int)sizeof(double);
     k_local_chunks<<<std::min(nch, 148 * 16), 64, smem, s>>>(g, Q, R, sDT_.p, ch, nch, Mt_.p, sp, sc,
                                                              lpart_.p);
     CK_LAUNCH();
@@ -1183,7 +1780,8 @@ void Engine::run_phases(const DevTree& qt, double h, double* d_out)
                                                         lchoff_.p, lpart_.p, L_.p, Lord_.p);
     CK_LAUNCH();
   }
-  if (stats_.prunes_finite_diff + stats_.prunes_direct_local + stats_.prunes_far_to_local > 0) {
+  if (cfg_.local_pushdown == 1 &&
+      stats_.prunes_finite_diff + stats_.prunes_direct_local + stats_.prunes_far_to_local > 0) {
     const int smem = D_ * ser_.pmax * (int)sizeof(double);
     for (int d = 0; d + 1 < qt.height; ++d) {
       const int b = qt.depth_off[d], e = qt.depth_off[d + 1];
@@ -1220,15 +1818,44 @@ void Engine::run_phases(const DevTree& qt, double h, double* d_out)
     leaf_task_.reserve(K);
     bpart_.reserve(32);
   }
+  const double* xq = nullptr;
+  const double* xr = nullptr;
+  if (ntasks) {  // scaled, centred, padded coordinates (Q and, if different, R)
+    const int DP = padded_dim(D_);
+    xq_.reserve((size_t)qt.n * DP);
+    k_scale_points<<<ceil_div((long long)qt.n * DP, 256), 256, 0, s>>>(qt.xs.p, qt.n, D_, DP,
+                                                                       rt_.centroid.p, sc, xq_.p);
+    CK_LAUNCH();
+    xq = xr = xq_.p;
+    if (&qt != &rt_) {
+      xr_.reserve((size_t)rt_.n * DP);
+      k_scale_points<<<ceil_div((long long)rt_.n * DP, 256), 256, 0, s>>>(rt_.xs.p, rt_.n, D_, DP,
+                                                                          rt_.centroid.p, sc, xr_.p);
+      CK_LAUNCH();
+      xr = xr_.p;
+    }
+  }
   CK(cudaEventRecord(ev_[9], s));
   if (ntasks)
     launch_base(D_, grid_warps(ntasks), s, Q, R, reinterpret_cast<const BTask*>(tasks_.p), ntasks,
-                sB_.p, -1.0 / (2.0 * h * h), bpart_.p);
+                sB_.p, xq, xr, 1.0 / (2.0 * h * h), bpart_.p);
   CK(cudaEventRecord(ev_[6], s));
   s_ff_.reserve(qt.n);
   if (nF_) {
-    k_farfield<<<grid_warps(nleaves), kBlock, 0, s>>>(g, Q, R, leaves_.p, nleaves, cntF_.p, offF_.p,
-                                                     sF_.p, Mt_.p, sp, sc, s_ff_.p);
+    const int gw = grid_warps(nleaves);
+    const int pm = ser_.pmax;
+#define FF_T(DD, PP)                                                                         \
+  k_farfield_t<DD, PP><<<gw, kBlock, 0, s>>>(Q, R, leaves_.p, nleaves, cntF_.p, offF_.p, sF_.p, \
+                                             Mt_.p, sp, sc, s_ff_.p)
+    if (D_ == 1 && pm == 8) FF_T(1, 8);
+    else if (D_ == 2 && pm == 6) FF_T(2, 6);
+    else if (D_ == 3 && pm == 4) FF_T(3, 4);
+    else if (D_ == 4 && pm == 2) FF_T(4, 2);
+    else if (D_ == 5 && pm == 2) FF_T(5, 2);
+    else
+      k_farfield<<<gw, kBlock, 0, s>>>(g, Q, R, leaves_.p, nleaves, cntF_.p, offF_.p, sF_.p, Mt_.p,
+                                      sp, sc, s_ff_.p);
+#undef FF_T
     CK_LAUNCH();
   } else {
     CK(cudaMemsetAsync(s_ff_.p, 0, sizeof(double) * qt.n, s));
@@ -1236,7 +1863,7 @@ void Engine::run_phases(const DevTree& qt, double h, double* d_out)
   CK(cudaEventRecord(ev_[7], s));
   k_finalize<<<ceil_div(qt.n, 128), 128, 0, s>>>(g, Q, leaf_of_pos_.p, qt.perm.p, qt.n, L_.p,
                                                  Lord_.p, cntB_.p, leaf_task_.p, bpart_.p, s_ff_.p,
-                                                 sc, d_out);
+                                                 sc, cfg_.local_pushdown == 0, d_out);
   CK_LAUNCH();
   CK(cudaEventRecord(ev_[8], s));
   CK(cudaStreamSynchronize(s));

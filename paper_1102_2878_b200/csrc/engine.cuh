@@ -14,6 +14,10 @@ struct Config {
   int p_max = 0;             // 0 -> default_p_max(D)
   int cost_model = 0;        // 0 exponential, 1 term_count (truncation.hpp:216)
   int mode = 1;              // 0 centroid (DFD), 1 series (DFGT)
+  // 0: every query evaluates the local expansions of all its ancestors directly
+  //    (exact re-centering, one kernel); 1: the reference's L2L push-down chain
+  //    (post_process, engine.cpp:294-304), one launch per tree level.
+  int local_pushdown = 0;
 };
 
 // Mirrors TraversalStats (engine.hpp:66-74).
@@ -70,6 +74,8 @@ public:
 
 private:
   void traverse(const DevTree& qt, double h);
+  void run_levels(const void* trav_args, const std::vector<const void*>& sig);
+  void destroy_graph();
   void run_phases(const DevTree& qt, double h, double* d_out);
   void eager_moments();
 
@@ -90,14 +96,24 @@ private:
   DevBuf<int> Lord_, cntF_, cntDT_, cntB_, offF_, offDT_, offB_, mflag_, mdone_;
   bool eager_ = false;                // Mt_ holds every node (tables <= 4096 terms)
   DevBuf<int> lnch_, lchoff_, lchunk_, ntask_, toff_, tasks_, leaf_task_;
-  DevBuf<double> lpart_, bpart_;
+  DevBuf<double> lpart_, bpart_, xq_, xr_;
   // frontier (double buffered) and per-level scratch
   DevBuf<int> fq_[2], foff_[2], flen_[2], fr_[2];
   DevBuf<double> fbase_[2];
   DevBuf<double> pkmax_, pkmin_;
   DevBuf<int> dec_, childlen_;
   DevBuf<double> newbase_;
-  DevBuf<Cnt> cnt_, cntoff_;
+  DevBuf<Cnt> cnt_, cntoff_, ctsum_, ctoff_;
+  // device-driven level loop: state (device + pinned host mirror), capacities, graph
+  void* hst_ = nullptr;
+  DevBuf<unsigned char> dst_;
+  int capE_ = 0, capP_ = 0, capF_ = 0, capDT_ = 0, capB_ = 0;
+  bool use_persistent_ = true;  // one cooperative kernel runs every level
+  bool use_graph_ = true;       // else: CUDA-graph WHILE loop; else host loop
+  cudaGraph_t graph_ = nullptr;
+  cudaGraphExec_t gexec_ = nullptr;
+  cudaGraphConditionalHandle hc_ = 0;
+  std::vector<const void*> gsig_;
   DevBuf<Item> itF_, itDT_, itB_, sF_, sDT_, sB_;
   DevBuf<unsigned char> scan_tmp_;
   DevBuf<unsigned long long> dstat_;

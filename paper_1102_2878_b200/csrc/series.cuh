@@ -112,7 +112,10 @@ struct DevSeries {
   const double* fact;
   const int* degree;
   const int* term_of_pos;
+  const int* pos;  // term -> base-p_max position (the reference's table layout)
 };
+
+__host__ __device__ constexpr int ipow_c(int b, int e) { return e == 0 ? 1 : b * ipow_c(b, e - 1); }
 
 __host__ __device__ inline int ipow_i(int b, int e)
 {

@@ -13,8 +13,11 @@ constexpr int kPMaxDev = 15;
 // over the full table (accumulate_farfield_moments, series.cpp:238-254).
 // `pts` are the node's points (row-major, contiguous).  smem: 32*D*pmax doubles.
 __device__ inline void dev_moments_block(const DevSeries& g, const double* pts, int npts,
-                                         const double* c, double s, double* M, double* smem)
+                                         const double* c, double s, double* Mout, double* smem,
+                                         const int* opos = nullptr)
 {
+  // opos != nullptr: write the table in the reference's POSITION layout
+  auto M = [&](int i) -> double& { return Mout[opos ? opos[i] : i]; };
   const int D = g.D, pm = g.pmax, T = g.T;
   const int per = D * pm;
   double acc[8];
@@ -23,7 +26,7 @@ __device__ inline void dev_moments_block(const DevSeries& g, const double* pts, 
   // tables beyond 8*blockDim terms fall back to global accumulation
   const bool reg = nmine <= 8;
   if (!reg)
-    for (int i = threadIdx.x; i < T; i += blockDim.x) M[i] = 0.0;
+    for (int i = threadIdx.x; i < T; i += blockDim.x) M(i) = 0.0;
   for (int base = 0; base < npts; base += 32) {
     const int m = min(32, npts - base);
     __syncthreads();
@@ -41,12 +44,12 @@ __device__ inline void dev_moments_block(const DevSeries& g, const double* pts, 
       double sum = 0.0;
       for (int pt = 0; pt < m; ++pt) sum += mono(smem + pt * per, pm, D, a);
       if (reg) acc[slot] += sum;
-      else M[i] += sum;
+      else M(i) += sum;
     }
   }
   int slot = 0;
   for (int i = threadIdx.x; i < T; i += blockDim.x, ++slot)
-    M[i] = (reg ? acc[slot] : M[i]) * g.invf[i];
+    M(i) = (reg ? acc[slot] : M(i)) * g.invf[i];
 }
 
 // Per thread: sum_{i < order^D} M[i] h_alpha_i((q - c)*s)   (eval_farfield, series.cpp:289-303)
@@ -54,7 +57,8 @@ __device__ inline void dev_moments_block(const DevSeries& g, const double* pts, 
 // is the reference's scaled moment.
 __device__ inline double dev_eval_farfield(const DevSeries& g, const double* M, const double* c,
                                            const double* q, double s, int order,
-                                           const double* spow = nullptr)
+                                           const double* spow = nullptr,
+                                           const int* mpos = nullptr)
 {
   const int D = g.D;
   double H[kMaxDim * kPMaxDev];
@@ -62,7 +66,8 @@ __device__ inline double dev_eval_farfield(const DevSeries& g, const double* M, 
   const int n = ipow_i(order, D);
   double sum = 0.0;
   for (int i = 0; i < n; ++i) {
-    const double m = spow ? M[i] * spow[g.degree[i]] : M[i];
+    const double mi = M[mpos ? mpos[i] : i];  // mpos: table stored in position layout
+    const double m = spow ? mi * spow[g.degree[i]] : mi;
     sum += m * herm_prod(H, kPMaxDev, D, g.dig[i]);
   }
   return sum;
@@ -112,7 +117,8 @@ __device__ inline void dev_direct_local_block(const DevSeries& g, const double* 
 // are reduced and signed later); spow as in dev_eval_farfield.
 __device__ inline void dev_f2l_block(const DevSeries& g, const double* M, const double* src_c,
                                      const double* dst_c, double s, int order, double* L,
-                                     double* smem, const double* spow = nullptr, int raw = 0)
+                                     double* smem, const double* spow = nullptr, int raw = 0,
+                                     const int* mpos = nullptr)
 {
   const int D = g.D;
   const int n = ipow_i(order, D);
@@ -125,7 +131,8 @@ __device__ inline void dev_f2l_block(const DevSeries& g, const double* M, const 
     const uint64_t b = g.dig[i];
     double acc = 0.0;
     for (int j = 0; j < n; ++j) {
-      const double m = spow ? M[j] * spow[g.degree[j]] : M[j];
+      const double mj = M[mpos ? mpos[j] : j];
+      const double m = spow ? mj * spow[g.degree[j]] : mj;
       acc += m * herm_prod2(smem, ho, D, g.dig[j], b);
     }
     if (raw) {
@@ -142,7 +149,7 @@ __device__ inline void dev_f2l_block(const DevSeries& g, const double* M, const 
 // smem: npts*D*order doubles (npts <= blockDim-sized chunk).
 __device__ inline void dev_direct_local_partial(const DevSeries& g, const double* pts, int npts,
                                                 const double* c, double s, int order, double* P,
-                                                double* smem)
+                                                double* smem, bool accumulate = false)
 {
   const int D = g.D;
   const int n = ipow_i(order, D);
@@ -157,7 +164,7 @@ __device__ inline void dev_direct_local_partial(const DevSeries& g, const double
     const uint64_t a = g.dig[i];
     double sum = 0.0;
     for (int pt = 0; pt < npts; ++pt) sum += herm_prod(smem + pt * per, order, D, a);
-    P[i] = sum;
+    P[i] = accumulate ? P[i] + sum : sum;
   }
 }
 

@@ -79,10 +79,14 @@ class EngineConfig:
     leaf_threshold: int = 20
     p_max: Optional[int] = None
     cost_model: CostModel = CostModel.exponential
+    # 0: direct evaluation of ancestors' local expansions (default, one kernel);
+    # 1: the reference's L2L push-down chain (engine.cpp:294-304)
+    local_pushdown: int = 0
 
     def _c(self, mode: Mode) -> _capi.Config:
         return _capi.Config(float(self.epsilon), int(self.leaf_threshold),
-                            int(self.p_max or 0), int(self.cost_model), int(mode))
+                            int(self.p_max or 0), int(self.cost_model), int(mode),
+                            int(self.local_pushdown))
 
 
 @dataclass

@@ -190,3 +190,29 @@ def test_dfgt_matches_reference_within_eps(dfgtb, ref):
         a = e.compute(None, h)
         b, _ = re.compute(h)
         assert np.all(np.abs(a - b) <= 0.0201 * np.abs(b) + 1e-300)
+
+
+def test_l2l_chain_matches_direct_ancestor_evaluation(dfgtb, orc):
+    """local_pushdown=1 runs the reference's L2L push-down chain (post_process,
+    engine.cpp:294-304); the default evaluates every ancestor's local expansion at
+    the query.  Exact polynomial re-centring: both agree to rounding."""
+    w = datagen.config(2, scale_n=0.04)
+    for s in (0.3, 1.0, 3.0, 10.0):
+        h = s * w.h_s
+        a = dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(leaf_threshold=32)).compute(None, h)
+        e = dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(leaf_threshold=32, local_pushdown=1))
+        b = e.compute(None, h)
+        assert np.max(np.abs(a - b) / np.abs(b)) <= 1e-10
+        _check(b, orc.naive_kde(w.refs, w.refs, h), 0.01)
+
+
+def test_fast_exp_accuracy(dfgtb, orc):
+    """The base case's exp(-y) (Cody-Waite + degree-12 Taylor, constant-bank
+    coefficients) vs libm: eps = 0 base-case-only sums agree with the exact oracle
+    to summation-order rounding, including pairs deep in the underflow range."""
+    g = np.random.default_rng(3)
+    x = g.random((600, 2)) * np.array([1.0, 0.01])
+    for h in (0.002, 0.01, 0.05, 0.3):
+        approx = dfgtb.dfd_kde(x, x, h, 0.0, 16)
+        exact = orc.naive_kde(x, x, h)
+        assert np.max(np.abs(approx - exact) / exact) <= 1e-13
