@@ -89,6 +89,12 @@ int dfgtb_compute(dfgtb_handle* h, const double* queries, size_t nq, double band
 int dfgtb_compute_device(dfgtb_handle* h, const double* d_queries, size_t nq, double bandwidth,
                          double* d_out_sums, dfgtb_stats* stats);
 
+/* Several bandwidths in ONE lock-step GPU traversal (what a CV sweep does with its
+ * h and 2h passes, cv.cpp:156-180): out_sums[b * n_out + i] is the sum at bws[b];
+ * stats (nullable) receives nb entries.  Equivalent to nb dfgtb_compute calls. */
+int dfgtb_compute_batch(dfgtb_handle* h, const double* queries, size_t nq, const double* bws,
+                        size_t nb, double* out_sums, dfgtb_stats* stats);
+
 /* DualTreeEngine::last_stats / p_max  engine.hpp:97-99. */
 int dfgtb_last_stats(dfgtb_handle* h, dfgtb_stats* stats);
 int dfgtb_last_timings(dfgtb_handle* h, dfgtb_timings* t);

@@ -51,7 +51,8 @@ class CvRow(C.Structure):
 # every symbol include/dfgtb.h declares (tests check the .so exports all of them)
 EXPORTS = (
     "dfgtb_default_config", "dfgtb_create", "dfgtb_create_device", "dfgtb_destroy",
-    "dfgtb_compute", "dfgtb_compute_device", "dfgtb_last_stats", "dfgtb_last_timings",
+    "dfgtb_compute", "dfgtb_compute_device", "dfgtb_compute_batch", "dfgtb_last_stats",
+    "dfgtb_last_timings",
     "dfgtb_p_max", "dfgtb_cv", "dfgtb_sweep", "dfgtb_lkcv_from_sums", "dfgtb_lscv_from_sums",
     "dfgtb_tree_nodes", "dfgtb_tree_height", "dfgtb_export_tree", "dfgtb_naive",
     "dfgtb_series_op", "dfgtb_dfma_peak", "dfgtb_device_count", "dfgtb_stream",
@@ -73,6 +74,7 @@ def _load():
         "dfgtb_destroy": (None, [V]),
         "dfgtb_compute": (C.c_int, [V, _D, sz, C.c_double, _D, C.POINTER(Stats)]),
         "dfgtb_compute_device": (C.c_int, [V, V, sz, C.c_double, V, C.POINTER(Stats)]),
+        "dfgtb_compute_batch": (C.c_int, [V, _D, sz, _D, sz, _D, C.POINTER(Stats)]),
         "dfgtb_last_stats": (C.c_int, [V, C.POINTER(Stats)]),
         "dfgtb_last_timings": (C.c_int, [V, C.POINTER(Timings)]),
         "dfgtb_p_max": (C.c_int, [V]),

@@ -200,46 +200,51 @@ int dfgtb_last_timings(dfgtb_handle* h, dfgtb_timings* t)
 
 int dfgtb_p_max(dfgtb_handle* h) { return h && h->eng ? h->eng->p_max() : -1; }
 
+// Batched CV: every bandwidth (and its convolution bandwidth) of `ns` scales goes
+// through ONE lock-step traversal; sums stay in HBM; CV partial sums come back.
+static void cv_rows(dfgtb_handle* h, const double* bws, const double* convs, int ns,
+                    dfgtb_cv_row* rows)
+{
+  Engine& e = *h->eng;
+  const size_t n = e.n();
+  if (n < 2) throw InvalidArgument("likelihood CV requires at least 2 points");
+  const bool ls = convs != nullptr;
+  std::vector<double> hs(bws, bws + ns);
+  if (ls) hs.insert(hs.end(), convs, convs + ns);
+  const int nb = (int)hs.size();
+  h->s1.reserve(n * (size_t)nb);
+  e.compute_batch(nullptr, n, hs.data(), nb, h->s1.p);
+  const Timings& t = e.last_timings();
+  std::vector<double> lk(ns), lsv(ns);
+  std::vector<int> cl(ns);
+  e.cv_reduce(h->s1.p, bws, ls ? h->s1.p + n * (size_t)ns : nullptr, convs, ns, lk.data(), cl.data(),
+              lsv.data());
+  for (int k = 0; k < ns; ++k) {
+    dfgtb_cv_row& r = rows[k];
+    r.h = bws[k];
+    r.conv_h = ls ? convs[k] : 0.0;
+    r.lk_score = lk[k];
+    r.lk_clamped = cl[k];
+    r.ls_score = ls ? lsv[k] : 0.0;
+    // the batch shares one traversal: its device time is split evenly over the rows
+    r.seconds = t.total_ms * 1e-3 / ns;
+    r.base_ms = t.base_ms / ns;
+    r.base_pairs = r.kernel_evaluations = r.pairs_visited = 0;
+    for (int slot : { k, ns + k }) {
+      if (slot >= nb) continue;
+      const Stats& st = e.last_stats(slot);
+      r.base_pairs += st.kernel_evaluations - 2ull * st.pairs_visited;
+      r.kernel_evaluations += st.kernel_evaluations;
+      r.pairs_visited += st.pairs_visited;
+    }
+  }
+}
+
 int dfgtb_cv(dfgtb_handle* h, double bw, double conv_h, dfgtb_cv_row* row)
 {
   return guard([&] {
     check_h(h);
-    Engine& e = *h->eng;
-    const size_t n = e.n();
-    if (n < 2) throw InvalidArgument("likelihood CV requires at least 2 points");
-    h->s1.reserve(n);
-    float ms = 0, bms = 0;
-    uint64_t bp = 0, kev = 0, pv = 0;
-    auto acc = [&] {
-      const Stats& st = e.last_stats();
-      ms += e.last_timings().total_ms;
-      bms += e.last_timings().base_ms;
-      bp += st.kernel_evaluations - 2ull * st.pairs_visited;
-      kev += st.kernel_evaluations;
-      pv += st.pairs_visited;
-    };
-    e.compute_device(nullptr, n, bw, h->s1.p);
-    acc();
-    const double* conv = nullptr;
-    if (conv_h > 0.0) {
-      h->s2.reserve(n);
-      e.compute_device(nullptr, n, conv_h, h->s2.p);
-      acc();
-      conv = h->s2.p;
-    }
-    row->base_ms = bms;
-    row->base_pairs = bp;
-    row->kernel_evaluations = kev;
-    row->pairs_visited = pv;
-    double lk = 0, ls = 0;
-    int cl = 0;
-    e.cv_reduce(h->s1.p, bw, conv, conv_h, &lk, &cl, &ls);
-    row->h = bw;
-    row->conv_h = conv_h;
-    row->lk_score = lk;
-    row->lk_clamped = cl;
-    row->ls_score = conv ? ls : 0.0;
-    row->seconds = ms * 1e-3;
+    cv_rows(h, &bw, conv_h > 0.0 ? &conv_h : nullptr, 1, row);
   });
 }
 
@@ -251,12 +256,41 @@ int dfgtb_sweep(dfgtb_handle* h, const double* scales, size_t ns, double base_h,
     if (!(base_h > 0.0)) throw InvalidArgument("base bandwidth must be positive");
     for (size_t i = 1; i < ns; ++i)
       if (!(scales[i] > scales[i - 1])) throw InvalidArgument("scales must be strictly increasing");
-    for (size_t i = 0; i < ns; ++i) {
-      const double bw = scales[i] * base_h;
-      const double ch = sqrt2 ? std::sqrt(2.0) * bw : 2.0 * bw;  // cv.cpp:27-30
-      const int rc = dfgtb_cv(h, bw, ch, &rows[i]);
-      if (rc != DFGTB_OK) throw std::runtime_error(g_err);
-      rows[i].scale = scales[i];
+    const size_t chunk = kMaxSlots / 2;  // h and conv_h of up to 32 scales per batch
+    for (size_t i0 = 0; i0 < ns; i0 += chunk) {
+      const int m = (int)std::min(chunk, ns - i0);
+      std::vector<double> bws(m), convs(m);
+      for (int k = 0; k < m; ++k) {
+        bws[k] = scales[i0 + k] * base_h;
+        convs[k] = sqrt2 ? std::sqrt(2.0) * bws[k] : 2.0 * bws[k];  // cv.cpp:27-30
+      }
+      cv_rows(h, bws.data(), convs.data(), m, rows + i0);
+      for (int k = 0; k < m; ++k) rows[i0 + k].scale = scales[i0 + k];
+    }
+  });
+}
+
+int dfgtb_compute_batch(dfgtb_handle* h, const double* queries, size_t nq, const double* bws,
+                        size_t nb, double* out_sums, dfgtb_stats* stats)
+{
+  return guard([&] {
+    check_h(h);
+    Engine& e = *h->eng;
+    const size_t n_out = queries ? nq : e.n();
+    if (nb == 0) throw InvalidArgument("empty bandwidth batch");
+    DevBuf<double> q, out;
+    out.reserve(n_out * nb);
+    if (queries) {
+      q.reserve(nq * e.dim());
+      CK(cudaMemcpy(q.p, queries, sizeof(double) * nq * e.dim(), cudaMemcpyHostToDevice));
+    }
+    for (size_t b0 = 0; b0 < nb; b0 += kMaxSlots) {
+      const int m = (int)std::min<size_t>(kMaxSlots, nb - b0);
+      e.compute_batch(queries ? q.p : nullptr, nq, bws + b0, m, out.p);
+      CK(cudaMemcpy(out_sums + b0 * n_out, out.p, sizeof(double) * n_out * m,
+                    cudaMemcpyDeviceToHost));
+      if (stats)
+        for (int k = 0; k < m; ++k) fill_stats(e.last_stats(k), stats + b0 + k);
     }
   });
 }

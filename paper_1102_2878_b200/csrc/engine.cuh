@@ -28,7 +28,8 @@ struct Stats {
   int levels = 0;
 };
 
-// Device milliseconds of the last compute(), per phase (CUDA events on the engine stream).
+// Device milliseconds of the last compute batch, per phase (CUDA events on the
+// engine stream).
 struct Timings {
   float tree_ms = 0, traverse_ms = 0, moments_ms = 0, local_ms = 0, base_ms = 0, farfield_ms = 0,
         final_ms = 0, total_ms = 0;
@@ -38,9 +39,13 @@ struct Cnt {
   int e, p, f, dt, t, b, fd;
 };
 
+// A work item.  key = slot * K + query node (slot = bandwidth of the batch, K =
+// query-tree node count); code = order | kind << 8 (kind 1 F, 2 D, 3 T, 4 base).
 struct Item {
-  int q, r, code, rank;  // code: order | kind << 8 (kind 1 F, 2 D, 3 T, 4 base)
+  int key, r, code, rank;
 };
+
+constexpr int kMaxSlots = 64;  // bandwidths per batch
 
 int default_p_max(int D);
 
@@ -49,17 +54,22 @@ public:
   Engine(const double* h_refs, size_t n, size_t d, const Config& cfg, bool refs_on_device = false);
   ~Engine();
 
-  // Sums for queries (device pointer, nq x D row-major; nullptr -> Q = R) written
-  // to d_out (device, nq, original query order).
-  void compute_device(const double* d_queries, size_t nq, double h, double* d_out);
-  // Host-buffer convenience used by the C-ABI.
+  // Sums for `nb` bandwidths at once (one lock-step traversal, batched kernels):
+  // d_out[b * nq + i] = G_{h_b}(q_i) in input order.  d_queries nullptr -> Q = R.
+  void compute_batch(const double* d_queries, size_t nq, const double* h, int nb, double* d_out);
+  void compute_device(const double* d_queries, size_t nq, double h, double* d_out)
+  {
+    compute_batch(d_queries, nq, &h, 1, d_out);
+  }
   void compute_host(const double* h_queries, size_t nq, double h, double* h_out);
 
-  // CV reductions of Q = R sums already on device (lk: log LOO mean, clamps; ls).
-  void cv_reduce(const double* d_sums, double h, const double* d_conv, double conv_h,
-                 double* lk, int* clamped, double* ls);
+  // CV reductions of Q = R sums on device, for `ns` scales at once:
+  // lk[k], clamped[k] from d_sums + k*n at h[k]; ls[k] uses d_conv + k*n at conv_h[k]
+  // (d_conv may be nullptr -> no LS).
+  void cv_reduce(const double* d_sums, const double* h, const double* d_conv, const double* conv_h,
+                 int ns, double* lk, int* clamped, double* ls);
 
-  const Stats& last_stats() const { return stats_; }
+  const Stats& last_stats(int slot = 0) const { return slot_stats_[slot]; }
   const Timings& last_timings() const { return tim_; }
   const DevTree& ref_tree() const { return rt_; }
   int p_max() const { return ser_.pmax; }
@@ -69,15 +79,14 @@ public:
   const SeriesTables& series() const { return ser_; }
   DevSeries dev_series() const;
   const double* d_refs() const { return x_.p; }
-  // base-case kernel time of the last compute (ms) and its algorithmic pair count
-  float base_kernel_ms() const { return tim_.base_ms; }
 
 private:
-  void traverse(const DevTree& qt, double h);
+  void traverse(const DevTree& qt, const double* h, int nb);
   void run_levels(const void* trav_args, const std::vector<const void*>& sig);
   void destroy_graph();
-  void run_phases(const DevTree& qt, double h, double* d_out);
+  void run_phases(const DevTree& qt, const double* h, int nb, double* d_out);
   void eager_moments();
+  void setup_leaves(const DevTree& t);
 
   Config cfg_;
   int D_ = 0;
@@ -89,14 +98,15 @@ private:
   DevBuf<double> qx_;       // query points (Q != R)
   SeriesTables ser_;
   DevBuf<unsigned char> ser_dev_;
-  DevBuf<int> leaves_, leaf_of_pos_;       // per current query tree
-  DevBuf<int> rleaves_;
-  // per-compute state
+  DevBuf<int> leaves_, leaf_of_pos_;  // of the current query tree
+  std::vector<int> qleaves_host_;
+  int leaves_src_ = -1;     // 0: leaves_ describe the reference tree, 1: a query tree
+  // per batch (node-indexed arrays are slot-major: key = slot * K + node)
   DevBuf<double> L_, Mt_, s_ff_;      // Mt_: UNSCALED reference moments (h-independent)
   DevBuf<int> Lord_, cntF_, cntDT_, cntB_, offF_, offDT_, offB_, mflag_, mdone_;
   bool eager_ = false;                // Mt_ holds every node (tables <= 4096 terms)
   DevBuf<int> lnch_, lchoff_, lchunk_, ntask_, toff_, tasks_, leaf_task_;
-  DevBuf<double> lpart_, bpart_, xq_, xr_;
+  DevBuf<double> lpart_, bpart_, xq_, xr_, slotp_;
   // frontier (double buffered) and per-level scratch
   DevBuf<int> fq_[2], foff_[2], flen_[2], fr_[2];
   DevBuf<double> fbase_[2];
@@ -104,6 +114,9 @@ private:
   DevBuf<int> dec_, childlen_;
   DevBuf<double> newbase_;
   DevBuf<Cnt> cnt_, cntoff_, ctsum_, ctoff_;
+  DevBuf<Item> itF_, itDT_, itB_, sF_, sDT_, sB_;
+  DevBuf<unsigned char> scan_tmp_;
+  DevBuf<double> red_;
   // device-driven level loop: state (device + pinned host mirror), capacities, graph
   void* hst_ = nullptr;
   DevBuf<unsigned char> dst_;
@@ -114,16 +127,11 @@ private:
   cudaGraphExec_t gexec_ = nullptr;
   cudaGraphConditionalHandle hc_ = 0;
   std::vector<const void*> gsig_;
-  DevBuf<Item> itF_, itDT_, itB_, sF_, sDT_, sB_;
-  DevBuf<unsigned char> scan_tmp_;
-  DevBuf<unsigned long long> dstat_;
-  DevBuf<double> red_;
   cudaEvent_t ev_[10];
-  Stats stats_;
+  std::vector<Stats> slot_stats_;
   Timings tim_;
   long long nF_ = 0, nDT_ = 0, nB_ = 0;
-  std::vector<int> qleaves_host_;
-  int leaves_src_ = -1;  // 0: leaves_ describe the reference tree, 1: a query tree
+  int nb_ = 1;
 };
 
 // Exhaustive FP64 sums on the device (K12, naive_kde engine.cpp:22-36).
@@ -136,5 +144,8 @@ double measure_dfma_peak(int device);
 // Series term tables -> one device blob, and the device view over it.
 void upload_series(const SeriesTables& t, DevBuf<unsigned char>& dev, cudaStream_t s);
 DevSeries series_view(const SeriesTables& t, const DevBuf<unsigned char>& dev);
+
+// Constant-bank coefficients of the base case's exp (execute.cu).
+void init_exp_constants(cudaStream_t s);
 
 }  // namespace dfgtb

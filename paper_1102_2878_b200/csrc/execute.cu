@@ -1,0 +1,1003 @@
+// Execution of the traversal's work lists on sm_100a, batched over bandwidth slots.
+//
+// Reference path (/root/reference/proj/src):
+//   moments_for (leaf moments + F2F)  engine.cpp:368-403  -> k_moment_chunks/reduce (once per tree)
+//   summarize D (direct local)        engine.cpp:212-221  -> k_local_chunks + k_local_reduce
+//   summarize T (far-to-local)        engine.cpp:223-232  -> k_local_chunks + k_local_reduce
+//   post_process L2L                  engine.cpp:294-304  -> k_l2l (local_pushdown = 1) or the
+//                                                            direct ancestor evaluation in k_finalize
+//   base_case                         engine.cpp:239-269  -> k_base_case (K10, the hot kernel)
+//   summarize F (far-field eval)      engine.cpp:200-211  -> k_farfield(_t)
+//   post_process leaf + run           engine.cpp:273-291, 85-89 -> k_finalize
+//   lkcv / lscv_from_sums             cv.cpp:61-97        -> k_cv_partial
+#include "internal.cuh"
+
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cfloat>
+
+namespace dfgtb {
+using namespace detail;
+
+namespace {
+
+// ------------------------------------------------------------------- moments
+__global__ void k_mark_moments(const Item* it, int n, int* flag)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int kind = it[i].code >> 8;
+    if (kind == kF || kind == kT) flag[it[i].r] = 1;
+  }
+}
+
+// K2/K3 (large tables, lazy): UNSCALED moments (position layout) of the reference
+// nodes an F/T item uses and that are not cached yet, one block per node.
+__global__ void k_moments(DevSeries g, TreeView R, int nodes, const int* flag, int* done, double* M)
+{
+  extern __shared__ double sm[];
+  for (int n = blockIdx.x; n < nodes; n += gridDim.x) {
+    if (!flag[n] || done[n]) continue;
+    dev_moments_block(g, R.xs + (size_t)R.begin[n] * g.D, R.count[n], R.cen + (size_t)n * g.D, 1.0,
+                      M + (size_t)n * g.T, sm, g.pos);
+    __syncthreads();
+    if (threadIdx.x == 0) done[n] = 1;
+  }
+}
+
+// K2/K3 (eager, tables <= 4096 terms): unscaled moments of EVERY reference node, once
+// per tree: M~_a(node) = (1/a!) sum_r prod_d (r - c)_d^{a_d}.  The reference's per-h
+// moment is s^|a| M~_a with s = 1/(h sqrt 2) -- one pass serves a whole sweep.
+// Pass 1: partial sums over 64-point chunks of each node; pass 2: chunks summed in
+// order per node; tables stored in the reference's position layout.
+constexpr int kMomChunk = 64;
+__global__ void k_moment_chunks(DevSeries g, TreeView R, const int* cnode, const int* cstart,
+                                int nchunks, double* part)
+{
+  extern __shared__ double sm[];
+  const int D = g.D, pm = g.pmax, per = D * pm;
+  for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const int n = cnode[c], st = cstart[c];
+    const int m = min(kMomChunk, R.begin[n] + R.count[n] - st);
+    const double* cen = R.cen + (size_t)n * D;
+    __syncthreads();
+    for (int w = threadIdx.x; w < m * D; w += blockDim.x) {
+      const int pt = w / D, d = w % D;
+      const double u = R.xs[(size_t)(st + pt) * D + d] - cen[d];
+      double* P = sm + pt * per + d * pm;
+      P[0] = 1.0;
+      for (int k = 1; k < pm; ++k) P[k] = P[k - 1] * u;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < g.T; i += blockDim.x) {
+      const uint64_t a = g.dig[i];
+      double sum = 0.0;
+      for (int pt = 0; pt < m; ++pt) sum += mono(sm + pt * per, pm, D, a);
+      part[(size_t)c * g.T + i] = sum;
+    }
+  }
+}
+
+__global__ void k_moment_reduce(DevSeries g, int nodes, const int* coff, const double* part,
+                                double* M)
+{
+  for (int n = blockIdx.x; n < nodes; n += gridDim.x)
+    for (int i = threadIdx.x; i < g.T; i += blockDim.x) {
+      double acc = 0.0;
+      for (int c = coff[n]; c < coff[n + 1]; ++c) acc += part[(size_t)c * g.T + i];
+      M[(size_t)n * g.T + g.pos[i]] = acc * g.invf[i];
+    }
+}
+
+// --------------------------------------------------- D / T items (local expansions)
+// Work split into chunks: a D item over <= kLocChunk reference points, or one T
+// item.  Each chunk writes an unsigned partial table; k_local_reduce sums a query
+// node's chunks in item order and applies (-1)^|b|/b! (summarize, engine.cpp:212-232).
+constexpr int kLocChunk = 1024;  // points per D chunk (staged kLocSub at a time)
+constexpr int kLocSub = 64;
+struct LChunk {
+  int item, start, n;
+};
+
+__global__ void k_local_count(const Item* items, int n, TreeView R, int* nch)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int kind = items[i].code >> 8;
+  nch[i] = kind == kD ? (R.count[items[i].r] + kLocChunk - 1) / kLocChunk : 1;
+}
+
+__global__ void k_local_fill(const Item* items, int n, TreeView R, const int* choff, LChunk* ch)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int kind = items[i].code >> 8;
+  const int r = items[i].r;
+  if (kind == kD) {
+    const int b = R.begin[r], c = R.count[r];
+    for (int k = 0, st = 0; st < c; ++k, st += kLocChunk)
+      ch[choff[i] + k] = LChunk{ i, b + st, min(kLocChunk, c - st) };
+  } else {
+    ch[choff[i]] = LChunk{ i, -1, 0 };
+  }
+}
+
+__global__ void k_local_chunks(DevSeries g, TreeView Q, TreeView R, int K, const Item* items,
+                               const LChunk* ch, int nch, const double* Mt, SlotView sv,
+                               double* part)
+{
+  extern __shared__ double sm[];
+  for (int c = blockIdx.x; c < nch; c += gridDim.x) {
+    const LChunk lc = ch[c];
+    const Item it = items[lc.item];
+    const int slot = it.key / K, node = it.key - slot * K;
+    const int kind = it.code >> 8, order = it.code & 0xff;
+    const double s = sv.s[slot];
+    double* P = part + (size_t)c * g.T;
+    const double* qc = Q.cen + (size_t)node * g.D;
+    if (kind == kD) {
+      for (int b = 0; b < lc.n; b += kLocSub)
+        dev_direct_local_partial(g, R.xs + (size_t)(lc.start + b) * g.D, min(kLocSub, lc.n - b), qc,
+                                 s, order, P, sm, b > 0);
+    } else {
+      dev_f2l_block(g, Mt + (size_t)it.r * g.T, R.cen + (size_t)it.r * g.D, qc, s, order, P, sm,
+                    sv.spow + (size_t)slot * kSPow, 1, g.pos);
+    }
+  }
+}
+
+__global__ void k_local_reduce(DevSeries g, int keys, const int* cnt, const int* off,
+                               const Item* items, const int* choff, const double* part, double* L,
+                               int* Lord)
+{
+  for (int n = blockIdx.x; n < keys; n += gridDim.x) {
+    const int c = cnt[n];
+    if (!c) continue;
+    const int i0 = off[n], i1 = i0 + c;
+    int ord = 0;
+    for (int k = i0; k < i1; ++k) ord = max(ord, items[k].code & 0xff);
+    const int nt = ipow_i(ord, g.D);
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+      const uint64_t a = g.dig[t];
+      int mx = 0;
+      for (int d = 0; d < g.D; ++d) mx = max(mx, digit_of(a, d));
+      double acc = 0.0;
+      for (int k = i0; k < i1; ++k) {
+        if (mx >= (items[k].code & 0xff)) continue;  // term beyond this item's order
+        for (int q = choff[k]; q < choff[k + 1]; ++q) acc += part[(size_t)q * g.T + t];
+      }
+      const double sg = (g.degree[t] & 1) ? -1.0 : 1.0;
+      L[(size_t)n * g.T + t] += sg * g.invf[t] * acc;
+    }
+    if (threadIdx.x == 0 && Lord[n] < ord) Lord[n] = ord;
+  }
+}
+
+// Top-down L2L of one depth level for every slot (post_process, engine.cpp:294-304).
+__global__ void k_l2l(DevSeries g, TreeView Q, int K, int nb, const int* nodes_at, int m,
+                      SlotView sv, double* L, int* Lord)
+{
+  extern __shared__ double sm[];
+  for (int k = blockIdx.x; k < m * nb; k += gridDim.x) {
+    const int slot = k / m;
+    const int n = nodes_at[k - slot * m];
+    const int key = slot * K + n;
+    const int order = Lord[key];
+    if (Q.left[n] < 0 || order <= 0) continue;
+    const int ch[2] = { slot * K + Q.left[n], slot * K + Q.right[n] };
+    const int chn[2] = { Q.left[n], Q.right[n] };
+    for (int c = 0; c < 2; ++c) {
+      dev_l2l_block(g, L + (size_t)key * g.T, Q.cen + (size_t)n * g.D, Q.cen + (size_t)chn[c] * g.D,
+                    sv.s[slot], order, L + (size_t)ch[c] * g.T, sm);
+      __syncthreads();
+      if (threadIdx.x == 0 && Lord[ch[c]] < order) Lord[ch[c]] = order;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- base case
+// Base-case tasks: a (slot, query leaf)'s sorted base items cut into runs of <=
+// kTaskItems reference leaves, times 32-query chunks of the leaf.  One warp per task
+// writes per-query partial sums; k_finalize adds a query's partials in task order.
+constexpr int kTaskItems = 8;
+struct BTask {
+  int key, item0, item1, q0;
+};
+
+__global__ void k_task_count(const int* leaves, int nleaves, int nb, int K, const int* cntB,
+                             TreeView Q, int* nt)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nleaves * nb) return;
+  const int slot = i / nleaves;
+  const int leaf = leaves[i - slot * nleaves];
+  const int ic = (cntB[slot * K + leaf] + kTaskItems - 1) / kTaskItems;
+  nt[i] = ic * ((Q.count[leaf] + 31) / 32);
+}
+
+__global__ void k_task_fill(const int* leaves, int nleaves, int nb, int K, const int* cntB,
+                            const int* offB, TreeView Q, const int* toff, BTask* tasks,
+                            int* leaf_task)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nleaves * nb) return;
+  const int slot = i / nleaves;
+  const int leaf = leaves[i - slot * nleaves];
+  const int key = slot * K + leaf;
+  const int c = cntB[key], o = offB[key];
+  const int ic = (c + kTaskItems - 1) / kTaskItems;
+  int t = toff[i];
+  leaf_task[key] = t;
+  for (int q0 = 0; q0 < Q.count[leaf]; q0 += 32)
+    for (int k = 0; k < ic; ++k)
+      tasks[t++] = BTask{ key, o + k * kTaskItems, o + min(c, (k + 1) * kTaskItems), q0 };
+}
+
+// exp(-y), 0 <= y <= 708.39, to ~1 ulp: Cody-Waite reduction y*log2(e) = n + f,
+// r = -y - n ln2 (|r| <= ln2/2), degree-12 Taylor polynomial (truncation
+// <= 1.7e-16 relative), 2^n spliced into the exponent field.  The coefficients sit in
+// the constant bank so every DFMA reads its constant operand from c[] (libdevice exp
+// re-materialises its 64-bit constants with integer moves inside hot loops).  Same
+// accuracy class as libdevice exp: no reduced precision is charged to eps.
+__constant__ double c_expk[15];
+
+__device__ __forceinline__ double exp_negy(double y)
+{
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
+  const double t = fma(-y, c_expk[0], magic);
+  const double n = t - magic;
+  double r = fma(n, -c_expk[1], -y);
+  r = fma(n, -c_expk[2], r);
+  double p = c_expk[3];
+#pragma unroll
+  for (int k = 4; k < 15; ++k) p = fma(p, r, c_expk[k]);
+  p = fma(p, r, 1.0);
+  const int ni = __double2loint(t);  // n in the low word of t
+  return __hiloint2double(__double2hiint(p) + (ni << 20), __double2loint(p));
+}
+
+// Scaled, centred, padded coordinates for the base case, per slot:
+// x' = (x - c0) / (h sqrt 2) so that |q' - r'|^2 = |q - r|^2 / (2 h^2) (stride DP).
+__global__ void k_scale_points(const double* xs, int n, int D, int DP, int nb, const double* c0,
+                               SlotView sv, double* out)
+{
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t per = (size_t)n * DP;
+  if (i >= per * nb) return;
+  const int slot = (int)(i / per);
+  const size_t j = i - (size_t)slot * per;
+  const size_t p = j / DP;
+  const int d = (int)(j % DP);
+  out[i] = d < D ? (xs[p * D + d] - c0[d]) * sv.s[slot] : 0.0;
+}
+
+template <int DT>
+struct PtLoad {
+  static constexpr int DP = DT == 1 ? 1 : (DT + 1) / 2 * 2;
+  __device__ __forceinline__ static void load(const double* base, int j, double (&v)[DP])
+  {
+    if constexpr (DT == 1) {
+      v[0] = base[j];
+    } else {
+      const double2* b2 = reinterpret_cast<const double2*>(base + (size_t)j * DP);
+#pragma unroll
+      for (int k = 0; k < DP / 2; ++k) {
+        const double2 t = b2[k];
+        v[2 * k] = t.x;
+        v[2 * k + 1] = t.y;
+      }
+    }
+  }
+};
+
+// K10: exhaustive base case (Traversal::base_case, engine.cpp:239-269).  One warp per
+// task: lanes own queries, each reference point arrives as one warp-uniform vector
+// load (broadcast), two pairs in flight per iteration.  A reference leaf whose box
+// bound guarantees y <= 708 for every pair takes the branch-free path; otherwise pairs
+// beyond the fast range fall back to libdevice exp (exact underflow behaviour).
+template <int DT>
+__global__ void __launch_bounds__(kBlock) k_base_case(TreeView Q, TreeView R, int K,
+                                                      const BTask* tasks, int ntasks,
+                                                      const Item* items, const double* xq,
+                                                      const double* xr, int nq, int nr,
+                                                      SlotView sv, double* part)
+{
+  constexpr int D = DT;
+  constexpr int DP = PtLoad<DT>::DP;
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int w = w0; w < ntasks; w += nw) {
+    const BTask t = tasks[w];
+    const int slot = t.key / K, leaf = t.key - slot * K;
+    const double* xqs = xq + (size_t)slot * nq * DP;
+    const double* xrs = xr + (size_t)slot * nr * DP;
+    const double s2 = sv.s2[slot];
+    const int qb = Q.begin[leaf] + t.q0;
+    const bool act = lane < Q.count[leaf] - t.q0;
+    double q[DP];
+    PtLoad<DT>::load(xqs, act ? qb + lane : qb, q);
+    const double* qlo = Q.lo + (size_t)leaf * D;
+    const double* qhi = Q.hi + (size_t)leaf * D;
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int k = t.item0; k < t.item1; ++k) {
+      const int r = items[k].r;
+      const double* rp = xrs + (size_t)R.begin[r] * DP;
+      const int rc = R.count[r];
+      double dl, du;
+      box_bounds<DT>(qlo, qhi, R.lo + (size_t)r * D, R.hi + (size_t)r * D, D, dl, du);
+      if (s2 * du <= 708.0) {
+        int j = 0;
+        for (; j + 1 < rc; j += 2) {
+          double a[DP], b[DP];
+          PtLoad<DT>::load(rp, j, a);
+          PtLoad<DT>::load(rp, j + 1, b);
+          double ya = 0.0, yb = 0.0;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const double ta = q[d] - a[d], tb = q[d] - b[d];
+            ya = fma(ta, ta, ya);
+            yb = fma(tb, tb, yb);
+          }
+          acc0 += exp_negy(ya);
+          acc1 += exp_negy(yb);
+        }
+        if (j < rc) {
+          double a[DP];
+          PtLoad<DT>::load(rp, j, a);
+          double ya = 0.0;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const double ta = q[d] - a[d];
+            ya = fma(ta, ta, ya);
+          }
+          acc0 += exp_negy(ya);
+        }
+      } else {
+        for (int j = 0; j < rc; ++j) {
+          double a[DP];
+          PtLoad<DT>::load(rp, j, a);
+          double ya = 0.0;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const double ta = q[d] - a[d];
+            ya = fma(ta, ta, ya);
+          }
+          acc0 += ya <= 708.0 ? exp_negy(ya) : exp(-ya);
+        }
+      }
+    }
+    part[(size_t)w * 32 + lane] = acc0 + acc1;
+  }
+}
+
+// Generic dimension (D > 5): scalar loads of the scaled coordinates, libdevice exp.
+__global__ void __launch_bounds__(kBlock) k_base_case_any(TreeView Q, TreeView R, int K, int D,
+                                                          const BTask* tasks, int ntasks,
+                                                          const Item* items, const double* xq,
+                                                          const double* xr, int nq, int nr,
+                                                          double* part)
+{
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int w = w0; w < ntasks; w += nw) {
+    const BTask t = tasks[w];
+    const int slot = t.key / K, leaf = t.key - slot * K;
+    const double* xqs = xq + (size_t)slot * nq * D;
+    const double* xrs = xr + (size_t)slot * nr * D;
+    const int qb = Q.begin[leaf] + t.q0;
+    const bool act = lane < Q.count[leaf] - t.q0;
+    double q[kMaxDim];
+    for (int d = 0; d < D; ++d) q[d] = xqs[(size_t)(act ? qb + lane : qb) * D + d];
+    double acc = 0.0;
+    for (int k = t.item0; k < t.item1; ++k) {
+      const int r = items[k].r;
+      const double* rp = xrs + (size_t)R.begin[r] * D;
+      for (int j = 0; j < R.count[r]; ++j) {
+        double y = 0.0;
+        for (int d = 0; d < D; ++d) {
+          const double ta = q[d] - rp[(size_t)j * D + d];
+          y = fma(ta, ta, y);
+        }
+        acc += exp(-y);
+      }
+    }
+    part[(size_t)w * 32 + lane] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- far field
+// Every query evaluates the far-field expansions attached to its leaf or any ancestor,
+// root first (eval_farfield per query, engine.cpp:200-211).  One warp per (slot, leaf).
+__global__ void __launch_bounds__(kBlock) k_farfield(DevSeries g, TreeView Q, TreeView R, int K,
+                                                     int nb, const int* leaves, int nleaves,
+                                                     const int* cnt, const int* off,
+                                                     const Item* items, const double* Mt,
+                                                     SlotView sv, int nq, double* s_ff)
+{
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int D = g.D;
+  for (int li = w0; li < nleaves * nb; li += nw) {
+    const int slot = li / nleaves;
+    const int leaf = leaves[li - slot * nleaves];
+    const double s = sv.s[slot];
+    const double* spw = sv.spow + (size_t)slot * kSPow;
+    const int qb = Q.begin[leaf], qc = Q.count[leaf];
+    int chain[64];
+    int depth = 0;
+    for (int n = leaf; n >= 0 && depth < 64; n = Q.parent[n]) chain[depth++] = n;
+    for (int q0 = 0; q0 < qc; q0 += 32) {
+      const int qi = q0 + lane;
+      const bool act = qi < qc;
+      const double* qp = Q.xs + (size_t)(qb + (act ? qi : 0)) * D;
+      double acc = 0.0;
+      for (int k = depth - 1; k >= 0; --k) {
+        const int key = slot * K + chain[k];
+        const int c = cnt[key];
+        const Item* it = items + off[key];
+        for (int t = 0; t < c; ++t) {
+          const int r = it[t].r, order = it[t].code & 0xff;
+          acc += dev_eval_farfield(g, Mt + (size_t)r * g.T, R.cen + (size_t)r * D, qp, s, order,
+                                   spw, g.pos);
+        }
+      }
+      if (act) s_ff[(size_t)slot * nq + qb + qi] = acc;
+    }
+  }
+}
+
+// Specialised far-field evaluation for the default tables (p_max == PM): every
+// multi-index is a compile-time constant, so the Hermite rows, s^|a| and the digit
+// products live in registers and the (position-layout) moments are read as
+// warp-uniform broadcast loads.  Same sum as dev_eval_farfield, position order.
+template <int D, int PM>
+__device__ __forceinline__ double ff_eval_t(const double* Mt, const double* c, const double* q,
+                                            double s, int order,
+                                            const double (&spw)[D * (PM - 1) + 1])
+{
+  double H[D][PM];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double t = (q[d] - c[d]) * s;
+    H[d][0] = exp(-t * t);
+    if (PM > 1) H[d][1] = 2.0 * t * H[d][0];
+#pragma unroll
+    for (int k = 1; k + 1 < PM; ++k) H[d][k + 1] = 2.0 * t * H[d][k] - 2.0 * k * H[d][k - 1];
+  }
+  double sum = 0.0;
+  constexpr int NP = ipow_c(PM, D);
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    int dig[D], mx = 0, deg = 0, rest = p;
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) {
+      dig[d] = rest % PM;
+      rest /= PM;
+      mx = dig[d] > mx ? dig[d] : mx;
+      deg += dig[d];
+    }
+    if (mx < order) {
+      double f = Mt[p] * spw[deg];
+#pragma unroll
+      for (int d = 0; d < D; ++d) f *= H[d][dig[d]];
+      sum += f;
+    }
+  }
+  return sum;
+}
+
+template <int D, int PM>
+__global__ void __launch_bounds__(kBlock) k_farfield_t(TreeView Q, TreeView R, int K, int nb,
+                                                       const int* leaves, int nleaves,
+                                                       const int* cnt, const int* off,
+                                                       const Item* items, const double* Mt,
+                                                       SlotView sv, int nq, double* s_ff)
+{
+  constexpr int T = ipow_c(PM, D);
+  constexpr int ND = D * (PM - 1) + 1;
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int li = w0; li < nleaves * nb; li += nw) {
+    const int slot = li / nleaves;
+    const int leaf = leaves[li - slot * nleaves];
+    const double s = sv.s[slot];
+    double spw[ND];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) spw[k] = sv.spow[(size_t)slot * kSPow + k];
+    const int qb = Q.begin[leaf], qc = Q.count[leaf];
+    int chain[64];
+    int depth = 0;
+    for (int n = leaf; n >= 0 && depth < 64; n = Q.parent[n]) chain[depth++] = n;
+    for (int q0 = 0; q0 < qc; q0 += 32) {
+      const int qi = q0 + lane;
+      const bool act = qi < qc;
+      double qv[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) qv[d] = Q.xs[(size_t)(qb + (act ? qi : 0)) * D + d];
+      double acc = 0.0;
+      for (int k = depth - 1; k >= 0; --k) {
+        const int key = slot * K + chain[k];
+        const int c = cnt[key];
+        const Item* it = items + off[key];
+        for (int t = 0; t < c; ++t) {
+          const int r = it[t].r, order = it[t].code & 0xff;
+          acc += ff_eval_t<D, PM>(Mt + (size_t)r * T, R.cen + (size_t)r * D, qv, s, order, spw);
+        }
+      }
+      if (act) s_ff[(size_t)slot * nq + qb + qi] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- finalize
+// Local evaluation, the base-case partials in task order, and the final sum
+// (post_process leaf branch and Traversal::run, engine.cpp:273-291, 85-89); results
+// scattered to input order.  direct != 0: the local expansions of ALL ancestors are
+// evaluated at the query (root first) instead of being pushed down by L2L first --
+// the same polynomial, re-centred exactly, without the per-level launch chain.
+__global__ void k_finalize(DevSeries g, TreeView Q, int K, int nb, const int* leaf_of_pos,
+                           const int* perm, int n, const double* L, const int* Lord,
+                           const int* cntB, const int* leaf_task, const double* part,
+                           const double* s_ff, SlotView sv, int direct, double* out)
+{
+  const long long gi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= (long long)n * nb) return;
+  const int slot = (int)(gi / n);
+  const int i = (int)(gi - (long long)slot * n);
+  const int leaf = leaf_of_pos[i];
+  const int lkey = slot * K + leaf;
+  const double s = sv.s[slot];
+  const double* qp = Q.xs + (size_t)i * g.D;
+  double loc = 0.0;
+  if (direct) {
+    int chain[64];
+    int depth = 0;
+    for (int a = leaf; a >= 0 && depth < 64; a = Q.parent[a]) chain[depth++] = a;
+    for (int k = depth - 1; k >= 0; --k) {
+      const int key = slot * K + chain[k];
+      const int order = Lord[key];
+      if (order > 0)
+        loc += dev_eval_local(g, L + (size_t)key * g.T, Q.cen + (size_t)chain[k] * g.D, qp, s, order);
+    }
+  } else {
+    const int order = Lord[lkey];
+    if (order > 0)
+      loc = dev_eval_local(g, L + (size_t)lkey * g.T, Q.cen + (size_t)leaf * g.D, qp, s, order);
+  }
+  const int li = i - Q.begin[leaf];
+  const int nic = (cntB[lkey] + kTaskItems - 1) / kTaskItems;
+  double ex = 0.0;
+  if (nic) {
+    const int t0 = leaf_task[lkey] + (li >> 5) * nic;
+    for (int k = 0; k < nic; ++k) ex += part[(size_t)(t0 + k) * 32 + (li & 31)];
+  }
+  out[(size_t)slot * n + perm[i]] = loc + s_ff[(size_t)slot * n + i] + ex;
+}
+
+__global__ void k_leaf_of_pos(const int* leaves, int nleaves, const int* begin, const int* count,
+                              int* leaf_of_pos)
+{
+  const int i = blockIdx.x;
+  if (i >= nleaves) return;
+  const int leaf = leaves[i];
+  for (int k = threadIdx.x; k < count[leaf]; k += blockDim.x) leaf_of_pos[begin[leaf] + k] = leaf;
+}
+
+// ---------------------------------------------------------------------- CV
+// K11 (cv.cpp:17-25, 61-97): per scale k (blockIdx.y), deterministic two-stage sums of
+// log LOO density, clamp count and the least-squares term.
+constexpr int kRedBlocks = 148;
+struct CvNorm {
+  double nh[kMaxSlots], nc[kMaxSlots];
+};
+__global__ void k_cv_partial(const double* sums, const double* conv, int n, CvNorm cn, double* part)
+{
+  __shared__ double sl[kBlock / 32], ss[kBlock / 32], sc[kBlock / 32];
+  const int k = blockIdx.y;
+  const double* S = sums + (size_t)k * n;
+  const double* C = conv ? conv + (size_t)k * n : nullptr;
+  const double nh = cn.nh[k], nc = cn.nc[k];
+  double lk = 0.0, ls = 0.0, cl = 0.0;
+  const int per = (n + gridDim.x - 1) / gridDim.x;
+  const int b = blockIdx.x * per, e = min(n, b + per);
+  for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
+    double loo = S[i] - 1.0;
+    if (loo <= 0.0) {
+      loo = DBL_MIN;
+      cl += 1.0;
+    }
+    lk += log(loo / nh);
+    if (C) ls += (C[i] - 1.0) / nc - 2.0 * ((S[i] - 1.0) / nh);
+  }
+  lk = warp_sum(lk);
+  ls = warp_sum(ls);
+  cl = warp_sum(cl);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sl[w] = lk;
+    ss[w] = ls;
+    sc[w] = cl;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, b2 = 0, c = 0;
+    for (int q = 0; q < kBlock / 32; ++q) {
+      a += sl[q];
+      b2 += ss[q];
+      c += sc[q];
+    }
+    double* P = part + ((size_t)k * gridDim.x + blockIdx.x) * 3;
+    P[0] = a;
+    P[1] = b2;
+    P[2] = c;
+  }
+}
+
+// K12: exhaustive FP64 sums, 128 queries per block, reference tiles through smem.
+__global__ void k_naive(const double* q, int nq, const double* r, int nr, int D, double scale,
+                        double* out)
+{
+  extern __shared__ double tile[];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double qq[kMaxDim];
+  for (int d = 0; d < D; ++d) qq[d] = i < nq ? q[(size_t)i * D + d] : 0.0;
+  double acc = 0.0;
+  const int TR = 256;
+  for (int b = 0; b < nr; b += TR) {
+    const int m = min(TR, nr - b);
+    __syncthreads();
+    for (int k = threadIdx.x; k < m * D; k += blockDim.x) tile[k] = r[(size_t)b * D + k];
+    __syncthreads();
+    for (int j = 0; j < m; ++j) {
+      double d2 = 0.0;
+      for (int d = 0; d < D; ++d) {
+        const double t = qq[d] - tile[j * D + d];
+        d2 += t * t;
+      }
+      acc += exp(scale * d2);
+    }
+  }
+  if (i < nq) out[i] = acc;
+}
+
+__global__ void k_dfma_peak(double* out, int iters)
+{
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+         a6 = a0 + 6, a7 = a0 + 7;
+  const double m = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+    a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+  }
+  if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == 42.0) out[0] = 1.0;
+}
+
+int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }
+
+void launch_base(int D, int grid, cudaStream_t s, TreeView Q, TreeView R, int K,
+                 const BTask* tasks, int ntasks, const Item* items, const double* xq,
+                 const double* xr, int nq, int nr, SlotView sv, double* part)
+{
+#define BASE(DD) \
+  k_base_case<DD><<<grid, kBlock, 0, s>>>(Q, R, K, tasks, ntasks, items, xq, xr, nq, nr, sv, part)
+  switch (D) {
+  case 1: BASE(1); break;
+  case 2: BASE(2); break;
+  case 3: BASE(3); break;
+  case 4: BASE(4); break;
+  case 5: BASE(5); break;
+  default:
+    k_base_case_any<<<grid, kBlock, 0, s>>>(Q, R, K, D, tasks, ntasks, items, xq, xr, nq, nr, part);
+    break;
+  }
+#undef BASE
+  CK_LAUNCH();
+}
+
+}  // namespace
+
+void init_exp_constants(cudaStream_t s)
+{  // log2(e), Cody-Waite ln2 split, then 1/12! ... 1/1!
+  double k[15];
+  k[0] = 1.4426950408889634;
+  k[1] = 6.93147180369123816490e-01;
+  k[2] = 1.90821492927058770002e-10;
+  double f = 1.0;
+  for (int i = 1; i <= 12; ++i) {
+    f *= i;
+    k[3 + (12 - i)] = 1.0 / f;
+  }
+  CK(cudaMemcpyToSymbolAsync(c_expk, k, sizeof(k), 0, cudaMemcpyHostToDevice, s));
+}
+
+// Unscaled moments of every reference node, once per tree (tables <= 4096 terms).
+void Engine::eager_moments()
+{
+  const DevTree& t = rt_;
+  const int K = t.nodes, T = ser_.T;
+  std::vector<int> cnode, cstart, coff(K + 1, 0);
+  for (int n = 0; n < K; ++n) {
+    coff[n] = (int)cnode.size();
+    for (int st = 0; st < t.h_count[n]; st += kMomChunk) {
+      cnode.push_back(n);
+      cstart.push_back(t.h_begin[n] + st);
+    }
+  }
+  coff[K] = (int)cnode.size();
+  const int nch = (int)cnode.size();
+  DevBuf<int> dn, ds, dof;
+  DevBuf<double> part;
+  dn.reserve(nch);
+  ds.reserve(nch);
+  dof.reserve(K + 1);
+  part.reserve((size_t)nch * T);
+  CK(cudaMemcpyAsync(dn.p, cnode.data(), sizeof(int) * nch, cudaMemcpyHostToDevice, s_));
+  CK(cudaMemcpyAsync(ds.p, cstart.data(), sizeof(int) * nch, cudaMemcpyHostToDevice, s_));
+  CK(cudaMemcpyAsync(dof.p, coff.data(), sizeof(int) * (K + 1), cudaMemcpyHostToDevice, s_));
+  Mt_.reserve((size_t)K * T);
+  const DevSeries g = dev_series();
+  const int smem = kMomChunk * D_ * ser_.pmax * (int)sizeof(double);
+  k_moment_chunks<<<std::min(nch, 148 * 16), 128, smem, s_>>>(g, view_of(t), dn.p, ds.p, nch,
+                                                               part.p);
+  CK_LAUNCH();
+  k_moment_reduce<<<std::min(K, 148 * 16), 128, 0, s_>>>(g, K, dof.p, part.p, Mt_.p);
+  CK_LAUNCH();
+  CK(cudaStreamSynchronize(s_));
+}
+
+void Engine::setup_leaves(const DevTree& t)
+{
+  qleaves_host_.clear();
+  for (int i = 0; i < t.nodes; ++i)
+    if (t.h_left[i] < 0) qleaves_host_.push_back(i);
+  const int nl = (int)qleaves_host_.size();
+  leaves_.reserve(nl);
+  CK(cudaMemcpyAsync(leaves_.p, qleaves_host_.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, s_));
+  leaf_of_pos_.reserve(t.n);
+  k_leaf_of_pos<<<nl, 64, 0, s_>>>(leaves_.p, nl, t.begin.p, t.count.p, leaf_of_pos_.p);
+  CK_LAUNCH();
+  CK(cudaStreamSynchronize(s_));
+}
+
+void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_out)
+{
+  cudaStream_t s = s_;
+  const DevSeries g = dev_series();
+  const TreeView Q = view_of(qt), R = view_of(rt_);
+  const int K = qt.nodes, T = ser_.T;
+  const int KB = K * nb;
+  nb_ = nb;
+  // per-slot constants: s, s2, s^k
+  {
+    std::vector<double> hp((size_t)nb * (2 + kSPow));
+    for (int b = 0; b < nb; ++b) {
+      const double sc = inv_scale(h[b]);
+      hp[b] = sc;
+      hp[nb + b] = 1.0 / (2.0 * h[b] * h[b]);
+      double* sp = hp.data() + 2 * nb + (size_t)b * kSPow;
+      sp[0] = 1.0;
+      for (int k = 1; k < kSPow; ++k) sp[k] = sp[k - 1] * sc;
+    }
+    slotp_.reserve(hp.size());
+    CK(cudaMemcpyAsync(slotp_.p, hp.data(), sizeof(double) * hp.size(), cudaMemcpyHostToDevice, s));
+  }
+  const SlotView sv{ slotp_.p, slotp_.p + nb, slotp_.p + 2 * nb };
+  CK(cudaEventRecord(ev_[2], s));
+  traverse(qt, h, nb);
+  CK(cudaEventRecord(ev_[3], s));
+  // moments of the reference nodes used by F/T items (large tables only; small
+  // tables were computed for every node when the engine was built)
+  unsigned long long nFT = 0, nLoc = 0;
+  for (const Stats& st : slot_stats_) {
+    nFT += st.prunes_farfield + st.prunes_far_to_local;
+    nLoc += st.prunes_finite_diff + st.prunes_direct_local + st.prunes_far_to_local;
+  }
+  if (nFT && !eager_) {
+    mflag_.reserve(rt_.nodes);
+    CK(cudaMemsetAsync(mflag_.p, 0, sizeof(int) * rt_.nodes, s));
+    if (nF_) {
+      k_mark_moments<<<ceil_div(nF_, 256), 256, 0, s>>>(sF_.p, (int)nF_, mflag_.p);
+      CK_LAUNCH();
+    }
+    if (nDT_) {
+      k_mark_moments<<<ceil_div(nDT_, 256), 256, 0, s>>>(sDT_.p, (int)nDT_, mflag_.p);
+      CK_LAUNCH();
+    }
+    const int smem = 32 * D_ * ser_.pmax * (int)sizeof(double);
+    k_moments<<<std::min(rt_.nodes, 148 * 8), 128, smem, s>>>(g, R, rt_.nodes, mflag_.p, mdone_.p,
+                                                             Mt_.p);
+    CK_LAUNCH();
+  }
+  CK(cudaEventRecord(ev_[4], s));
+  // D/T items -> chunked partial tables -> per-(slot, query node) reduction
+  if (nDT_) {
+    lnch_.reserve(nDT_ + 1);
+    lchoff_.reserve(nDT_ + 1);
+    k_local_count<<<ceil_div(nDT_, 256), 256, 0, s>>>(sDT_.p, (int)nDT_, R, lnch_.p);
+    CK_LAUNCH();
+    CK(cudaMemsetAsync(lnch_.p + nDT_, 0, sizeof(int), s));
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, lnch_.p, lchoff_.p, (int)nDT_ + 1, s);
+    scan_tmp_.reserve(need + 256);
+    size_t have = scan_tmp_.cap;
+    cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, lnch_.p, lchoff_.p, (int)nDT_ + 1, s);
+    int nch = 0;
+    CK(cudaMemcpyAsync(&nch, lchoff_.p + nDT_, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    lchunk_.reserve((size_t)nch * 3);
+    LChunk* ch = reinterpret_cast<LChunk*>(lchunk_.p);
+    k_local_fill<<<ceil_div(nDT_, 256), 256, 0, s>>>(sDT_.p, (int)nDT_, R, lchoff_.p, ch);
+    CK_LAUNCH();
+    lpart_.reserve((size_t)nch * T);
+    const int smem = std::max(kLocSub * D_ * ser_.pmax, D_ * (2 * ser_.pmax)) * (int)sizeof(double);
+    k_local_chunks<<<std::min(nch, 148 * 16), 64, smem, s>>>(g, Q, R, K, sDT_.p, ch, nch, Mt_.p, sv,
+                                                             lpart_.p);
+    CK_LAUNCH();
+    k_local_reduce<<<std::min(KB, 148 * 16), 64, 0, s>>>(g, KB, cntDT_.p, offDT_.p, sDT_.p,
+                                                         lchoff_.p, lpart_.p, L_.p, Lord_.p);
+    CK_LAUNCH();
+  }
+  if (cfg_.local_pushdown == 1 && nLoc > 0) {
+    const int smem = D_ * ser_.pmax * (int)sizeof(double);
+    for (int d = 0; d + 1 < qt.height; ++d) {
+      const int b = qt.depth_off[d], e = qt.depth_off[d + 1];
+      k_l2l<<<std::min((e - b) * nb, 148 * 8), 64, smem, s>>>(g, Q, K, nb, qt.by_depth.p + b, e - b,
+                                                             sv, L_.p, Lord_.p);
+      CK_LAUNCH();
+    }
+  }
+  CK(cudaEventRecord(ev_[5], s));
+  // base-case tasks
+  const int nleaves = (int)qleaves_host_.size();
+  const int nlb = nleaves * nb;
+  int ntasks = 0;
+  leaf_task_.reserve(KB);
+  if (nB_) {
+    ntask_.reserve(nlb + 1);
+    toff_.reserve(nlb + 1);
+    k_task_count<<<ceil_div(nlb, 256), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, Q, ntask_.p);
+    CK_LAUNCH();
+    CK(cudaMemsetAsync(ntask_.p + nlb, 0, sizeof(int), s));
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, ntask_.p, toff_.p, nlb + 1, s);
+    scan_tmp_.reserve(need + 256);
+    size_t have = scan_tmp_.cap;
+    cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, ntask_.p, toff_.p, nlb + 1, s);
+    CK(cudaMemcpyAsync(&ntasks, toff_.p + nlb, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    tasks_.reserve((size_t)ntasks * 4);
+    k_task_fill<<<ceil_div(nlb, 256), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p, Q,
+                                                   toff_.p, reinterpret_cast<BTask*>(tasks_.p),
+                                                   leaf_task_.p);
+    CK_LAUNCH();
+    bpart_.reserve((size_t)ntasks * 32);
+  } else {
+    bpart_.reserve(32);
+  }
+  const double* xq = nullptr;
+  const double* xr = nullptr;
+  if (ntasks) {  // scaled, centred, padded coordinates per slot (Q and, if different, R)
+    const int DP = padded_dim(D_);
+    xq_.reserve((size_t)qt.n * DP * nb);
+    k_scale_points<<<ceil_div((long long)qt.n * DP * nb, 256), 256, 0, s>>>(
+      qt.xs.p, qt.n, D_, DP, nb, rt_.centroid.p, sv, xq_.p);
+    CK_LAUNCH();
+    xq = xr = xq_.p;
+    if (&qt != &rt_) {
+      xr_.reserve((size_t)rt_.n * DP * nb);
+      k_scale_points<<<ceil_div((long long)rt_.n * DP * nb, 256), 256, 0, s>>>(
+        rt_.xs.p, rt_.n, D_, DP, nb, rt_.centroid.p, sv, xr_.p);
+      CK_LAUNCH();
+      xr = xr_.p;
+    }
+  }
+  CK(cudaEventRecord(ev_[9], s));
+  if (ntasks)
+    launch_base(D_, grid_warps(ntasks), s, Q, R, K, reinterpret_cast<const BTask*>(tasks_.p), ntasks,
+                sB_.p, xq, xr, qt.n, rt_.n, sv, bpart_.p);
+  CK(cudaEventRecord(ev_[6], s));
+  s_ff_.reserve((size_t)qt.n * nb);
+  if (nF_) {
+    const int gw = grid_warps(nlb);
+    const int pm = ser_.pmax;
+#define FF_T(DD, PP)                                                                              \
+  k_farfield_t<DD, PP><<<gw, kBlock, 0, s>>>(Q, R, K, nb, leaves_.p, nleaves, cntF_.p, offF_.p,   \
+                                             sF_.p, Mt_.p, sv, qt.n, s_ff_.p)
+    if (D_ == 1 && pm == 8) FF_T(1, 8);
+    else if (D_ == 2 && pm == 6) FF_T(2, 6);
+    else if (D_ == 3 && pm == 4) FF_T(3, 4);
+    else if (D_ == 4 && pm == 2) FF_T(4, 2);
+    else if (D_ == 5 && pm == 2) FF_T(5, 2);
+    else
+      k_farfield<<<gw, kBlock, 0, s>>>(g, Q, R, K, nb, leaves_.p, nleaves, cntF_.p, offF_.p, sF_.p,
+                                      Mt_.p, sv, qt.n, s_ff_.p);
+#undef FF_T
+    CK_LAUNCH();
+  } else {
+    CK(cudaMemsetAsync(s_ff_.p, 0, sizeof(double) * qt.n * nb, s));
+  }
+  CK(cudaEventRecord(ev_[7], s));
+  k_finalize<<<ceil_div((long long)qt.n * nb, 128), 128, 0, s>>>(
+    g, Q, K, nb, leaf_of_pos_.p, qt.perm.p, qt.n, L_.p, Lord_.p, cntB_.p, leaf_task_.p, bpart_.p,
+    s_ff_.p, sv, cfg_.local_pushdown == 0, d_out);
+  CK_LAUNCH();
+  CK(cudaEventRecord(ev_[8], s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaEventElapsedTime(&tim_.traverse_ms, ev_[2], ev_[3]));
+  CK(cudaEventElapsedTime(&tim_.moments_ms, ev_[3], ev_[4]));
+  CK(cudaEventElapsedTime(&tim_.local_ms, ev_[4], ev_[5]));
+  CK(cudaEventElapsedTime(&tim_.base_ms, ev_[9], ev_[6]));
+  CK(cudaEventElapsedTime(&tim_.farfield_ms, ev_[6], ev_[7]));
+  CK(cudaEventElapsedTime(&tim_.final_ms, ev_[7], ev_[8]));
+  CK(cudaEventElapsedTime(&tim_.total_ms, ev_[2], ev_[8]));
+}
+
+void Engine::cv_reduce(const double* d_sums, const double* h, const double* d_conv,
+                       const double* conv_h, int ns, double* lk, int* clamped, double* ls)
+{
+  const size_t n = n_;
+  if (n < 2) throw InvalidArgument("CV requires at least 2 points");
+  if (ns < 1 || ns > kMaxSlots) throw InvalidArgument("CV batch size outside [1, 64]");
+  const double two_pi = 6.283185307179586476925286766559;
+  CvNorm cn{};
+  for (int k = 0; k < ns; ++k) {
+    cn.nh[k] = (double)(n - 1) * std::pow(two_pi * h[k] * h[k], 0.5 * D_);
+    cn.nc[k] = d_conv ? (double)(n - 1) * std::pow(two_pi * conv_h[k] * conv_h[k], 0.5 * D_) : 1.0;
+  }
+  red_.reserve((size_t)kRedBlocks * 3 * ns);
+  k_cv_partial<<<dim3(kRedBlocks, ns), kBlock, 0, s_>>>(d_sums, d_conv, (int)n, cn, red_.p);
+  CK_LAUNCH();
+  std::vector<double> part((size_t)kRedBlocks * 3 * ns);
+  CK(cudaMemcpyAsync(part.data(), red_.p, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, s_));
+  CK(cudaStreamSynchronize(s_));
+  for (int k = 0; k < ns; ++k) {
+    double a = 0, b = 0, c = 0;
+    for (int q = 0; q < kRedBlocks; ++q) {
+      const double* P = part.data() + ((size_t)k * kRedBlocks + q) * 3;
+      a += P[0];
+      b += P[1];
+      c += P[2];
+    }
+    if (lk) lk[k] = a / (double)n;
+    if (clamped) clamped[k] = (int)c;
+    if (ls) ls[k] = b / (double)n;
+  }
+}
+
+void naive_device(const double* d_q, size_t nq, const double* d_r, size_t nr, int D, double h,
+                  double* d_out, cudaStream_t s)
+{
+  const int TR = 256;
+  k_naive<<<ceil_div(nq, 128), 128, TR * D * sizeof(double), s>>>(d_q, (int)nq, d_r, (int)nr, D,
+                                                                 -1.0 / (2.0 * h * h), d_out);
+  CK_LAUNCH();
+}
+
+double measure_dfma_peak(int device)
+{
+  cudaDeviceProp p{};
+  CK(cudaGetDeviceProperties(&p, device));
+  DevBuf<double> o;
+  o.reserve(1);
+  const int blocks = p.multiProcessorCount * 8, threads = 256, iters = 4096;
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  k_dfma_peak<<<blocks, threads>>>(o.p, 64);
+  CK(cudaEventRecord(a));
+  k_dfma_peak<<<blocks, threads>>>(o.p, iters);
+  CK(cudaEventRecord(b));
+  CK(cudaEventSynchronize(b));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return (double)blocks * threads * iters * 8.0 / (ms * 1e-3);
+}
+
+}  // namespace dfgtb

@@ -1,0 +1,870 @@
+// Level-synchronous dual-tree traversal on sm_100a (replaces the reference's
+// recursive Traversal::recurse, engine.cpp:113-195, and choose_best_method,
+// truncation.cpp:130-166).
+//
+// The frontier holds live (query node, reference node) pairs grouped by query node
+// -- an antichain: each query node appears at most once per level -- and one warp
+// classifies one query node's pairs.  A BATCH of bandwidths is traversed in lock
+// step: an entry's key is slot * K + node, so every bandwidth of a CV sweep shares
+// each level's launches and synchronisation.
+//
+// Error budget (the reference's proof, with a BFS lower bound):
+// tau(Q, R) = eps |R| G^l(Q) / |R_total|, where G^l(Q) = the K(d_max) lower-bound
+// mass of every pair retired at Q or an ancestor (pruned, summarised or sent to the
+// base case) plus that of every live pair of Q.  Those pairs partition the reference
+// set, so G^l(Q) <= G(q) for every q in Q and the errors of all retired pairs of q
+// add up to <= eps G(q).
+//
+// Work items are appended per level with a per-(slot, node) rank and counting-sorted
+// by key afterwards: every accumulation happens in a fixed order, results are
+// bit-reproducible run to run.
+#include "internal.cuh"
+
+#include <cooperative_groups.h>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+#include <cub/device/device_scan.cuh>
+#include <math_constants.h>
+
+#include <algorithm>
+
+namespace dfgtb {
+namespace cg = cooperative_groups;
+using namespace detail;
+
+namespace {
+
+// ------------------------------------------------------------------ truncation
+__device__ double d_binomial(int n, int k)
+{  // truncation.cpp:11-18
+  double b = 1.0;
+  for (int i = 1; i <= k; ++i) b *= (double)(n - k + i) / (double)i;
+  return b;
+}
+__device__ double d_sqrt_factorial(int p)
+{  // truncation.cpp:20-27
+  double f = 1.0;
+  for (int k = 2; k <= p; ++k) f *= k;
+  return sqrt(f);
+}
+__device__ double d_ipow(double x, int n)
+{
+  double r = 1.0;
+  for (int i = 0; i < n; ++i) r *= x;
+  return r;
+}
+__device__ double d_bound_sum(double count, double s, int dpow, double a, double b, int dim)
+{  // truncation.cpp:40-54 (log-space fallback when the prefactor overflows)
+  double sum = 0.0;
+  for (int k = 0; k < dim; ++k) sum += d_binomial(dim, k) * d_ipow(a, k) * d_ipow(b, dim - k);
+  const double pre = count / d_ipow(1.0 - s, dim * dpow);
+  double bound = pre * sum;
+  if (!isfinite(bound) && count > 0.0 && sum > 0.0)
+    bound = exp(log(count) - (double)(dim * dpow) * log1p(-s) + log(sum));
+  return bound;
+}
+__device__ double d_ff_bound(double count, double r, int p, int dim)
+{  // truncation.cpp:58-65 (local_error_bound is the same formula)
+  if (count <= 0.0) return 0.0;
+  const double rp = d_ipow(r, p);
+  return d_bound_sum(count, r, 1, 1.0 - rp, rp / d_sqrt_factorial(p), dim);
+}
+__device__ double d_f2l_bound(double count, double r, int p, int dim)
+{  // truncation.cpp:72-81
+  if (count <= 0.0) return 0.0;
+  const double s = 2.0 * r, sp = d_ipow(s, p);
+  return d_bound_sum(count, s, 2, (1.0 - sp) * (1.0 - sp), sp * (2.0 - sp) / d_sqrt_factorial(p),
+                     dim);
+}
+__device__ int d_order_ff(double ratio, double count, double tau, int pmax, int dim)
+{  // least_order + farfield_order / local_accum_order, truncation.cpp:85-112
+  if (ratio >= 1.0) return 0;
+  for (int p = 1; p <= pmax; ++p)
+    if (d_ff_bound(count, ratio, p, dim) <= tau) return p;
+  return 0;
+}
+__device__ int d_order_f2l(double ratio, double count, double tau, int pmax, int dim)
+{  // f2l_order, truncation.cpp:114-128
+  if (ratio >= 0.5) return 0;
+  for (int p = 1; p <= pmax; ++p)
+    if (d_f2l_bound(count, ratio, p, dim) <= tau) return p;
+  return 0;
+}
+// choose_best_method, truncation.cpp:130-166 (ties F > D > T > E)
+__device__ void dev_choose(double nq, double nr, double sq, double sr, double h, double tau,
+                           int pmax, int dim, int cost, int& kind, int& order)
+{
+  const int pf = d_order_ff(sr / (2.0 * h), nr, tau, pmax, dim);
+  const int pd = d_order_ff(sq / (2.0 * h), nr, tau, pmax, dim);
+  const int pt = d_order_f2l((sq < sr ? sr : sq) / (4.0 * h), nr, tau, pmax, dim);
+  const double D = (double)dim;
+  double cf = CUDART_INF, cd = CUDART_INF, ct = CUDART_INF;
+  if (cost == 0) {  // exponential model; integer powers are exact
+    if (pf) cf = nq * d_ipow(D, pf + 1);
+    if (pd) cd = nr * d_ipow(D, pd + 1);
+    if (pt) ct = d_ipow(D, 2 * pt + 1);
+  } else {
+    if (pf) cf = nq * d_ipow((double)pf, dim);
+    if (pd) cd = nr * d_ipow((double)pd, dim);
+    if (pt) ct = D * d_ipow((double)pt, 2 * dim);
+  }
+  const double ce = D * nq * nr;
+  const double m1 = cd < cf ? cd : cf, m2 = ce < ct ? ce : ct;
+  const double best = m2 < m1 ? m2 : m1;
+  if (cf == best) { kind = kF; order = pf; }
+  else if (cd == best) { kind = kD; order = pd; }
+  else if (ct == best) { kind = kT; order = pt; }
+  else { kind = kE; order = 0; }
+}
+
+// ------------------------------------------------------------------ state
+// Device-resident traversal state: every kernel reads the frontier size here, so
+// the level loop needs no host round trip.  Capacities are checked before anything
+// is written; on overflow the loop stops and the host regrows the buffers and reruns.
+enum SlotStat { sPairs = 0, sFD, sF, sD, sT, sB, sKev, sNStat };
+struct TravState {
+  double eps, ntot;                    // per batch (host)
+  int nslots, K;
+  double h[kMaxSlots], scale[kMaxSlots];
+  int capE, capP, capF, capDT, capB;   // buffer capacities (host)
+  int cur;                             // frontier buffer of the current level
+  int m[2], p[2];                      // entries / pairs in each frontier buffer
+  int nF, nDT, nB;                     // items emitted so far
+  int overflow, levels;
+  int done;                            // CTAs finished with their tile sum (k_traverse)
+  Cnt lvl;                             // totals of the current level
+  unsigned long long sst[kMaxSlots][sNStat];  // per-slot TraversalStats
+};
+
+struct TravArgs {
+  TreeView Q, R;
+  int D, pmax, cost, series, T;
+  TravState* st;
+  int *fq[2], *foff[2], *flen[2], *fr[2];
+  double* fbase[2];
+  double *pkmax, *pkmin;
+  int* dec;
+  Cnt *cnt, *cntoff, *tsum, *toff;
+  int* childlen;
+  double* newbase;
+  double* L;
+  int* Lord;
+  Item *itF, *itDT, *itB;
+  int *cntF, *cntDT, *cntB;
+};
+
+__device__ __forceinline__ Cnt ldcg_cnt(const Cnt* p)
+{
+  const int* q = reinterpret_cast<const int*>(p);
+  return Cnt{ __ldcg(q), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3), __ldcg(q + 4), __ldcg(q + 5),
+              __ldcg(q + 6) };
+}
+
+__device__ __forceinline__ int warp_excl_scan(int v, int lane, int& total)
+{
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  total = __shfl_sync(0xffffffffu, x, 31);
+  return x - v;
+}
+
+struct CntSum {
+  __host__ __device__ Cnt operator()(const Cnt& x, const Cnt& y) const
+  {
+    return Cnt{ x.e + y.e, x.p + y.p, x.f + y.f, x.dt + y.dt, x.t + y.t, x.b + y.b, x.fd + y.fd };
+  }
+};
+
+// Root pairs (slot b: key b*K -> reference root) and a fresh state.
+__global__ void k_trav_init(TravArgs a)
+{
+  TravState& st = *a.st;
+  const int nb = st.nslots;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    a.fq[0][b] = b * st.K;
+    a.foff[0][b] = b;
+    a.flen[0][b] = 1;
+    a.fbase[0][b] = 0.0;
+    a.fr[0][b] = 0;
+    for (int k = 0; k < sNStat; ++k) st.sst[b][k] = 0;
+  }
+  if (threadIdx.x == 0) {
+    st.cur = 0;
+    st.m[0] = nb;
+    st.p[0] = nb;
+    st.m[1] = st.p[1] = 0;
+    st.nF = st.nDT = st.nB = 0;
+    st.overflow = 0;
+    st.levels = 0;
+    st.done = 0;
+    st.lvl = Cnt{};
+  }
+}
+
+// One warp, one frontier query node: kernel bounds of every live pair, the lower
+// bound G^l, and the prune / summarise / base / expand decision per pair.
+template <int DT>
+__device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st, int cur, int e,
+                                               int lane)
+{
+  const int* fr = a.fr[cur];
+  const int D = DT ? DT : a.D;
+  const int key = a.fq[cur][e];
+  const int slot = key / st.K;
+  const int Q = key - slot * st.K;
+  const double h = st.h[slot], scale = st.scale[slot], eps = st.eps, ntot = st.ntot;
+  const int off = a.foff[cur][e], len = a.flen[cur][e];
+  const double fb = a.fbase[cur][e];
+  const double* qlo = a.Q.lo + (size_t)Q * D;
+  const double* qhi = a.Q.hi + (size_t)Q * D;
+  const bool qleaf = a.Q.left[Q] < 0;
+  const double nq = (double)a.Q.count[Q];
+  const double sq = a.Q.side[Q];
+  // pass 1: kernel bounds and the lower-bound mass of every live pair
+  double part = 0.0;
+  for (int j = lane; j < len; j += 32) {
+    const int R = fr[off + j];
+    double dl, du;
+    box_bounds<DT>(qlo, qhi, a.R.lo + (size_t)R * D, a.R.hi + (size_t)R * D, D, dl, du);
+    const double kmax = exp(scale * dl);  // kernel at closest approach
+    const double kmin = exp(scale * du);
+    a.pkmax[off + j] = kmax;
+    a.pkmin[off + j] = kmin;
+    part += (double)a.R.count[R] * kmin;
+  }
+  const double glo = fb + warp_sum(part);
+  // pass 2: decisions
+  double fd_dlo = 0.0, fd_const = 0.0, ret = 0.0;
+  int nF = 0, nDT = 0, nT = 0, nB = 0, nFD = 0, slots = 0;
+  unsigned long long kev = 0;
+  for (int j = lane; j < len; j += 32) {
+    const int R = fr[off + j];
+    const double kmax = a.pkmax[off + j], kmin = a.pkmin[off + j];
+    const double nr = (double)a.R.count[R];
+    const double dlo = nr * kmin;
+    const double tau = eps * nr * glo / ntot;
+    int kind = kX, order = 0;
+    if (0.5 * nr * (kmax - kmin) <= tau) {  // kernel-difference prune, engine.cpp:137-148
+      kind = kFD;
+      fd_dlo += dlo;
+      fd_const += 0.5 * nr * (kmax + kmin);
+      ++nFD;
+    } else {
+      if (a.series) {
+        dev_choose(nq, nr, sq, a.R.side[R], h, tau, a.pmax, D, a.cost, kind, order);
+        if (kind == kE) kind = kX;
+      }
+      if (kind == kX && qleaf && a.R.left[R] < 0) kind = kB;
+      if (kind == kX) {
+        slots += a.R.left[R] < 0 ? 1 : 2;
+      } else if (kind == kB) {
+        ++nB;
+        kev += (unsigned long long)a.Q.count[Q] * (unsigned long long)a.R.count[R];
+        ret += dlo;
+      } else {
+        ret += dlo;
+        if (kind == kF) ++nF;
+        else {
+          ++nDT;
+          if (kind == kT) ++nT;
+        }
+      }
+    }
+    a.dec[off + j] = kind | (order << 8);
+  }
+  fd_dlo = warp_sum(fd_dlo);
+  fd_const = warp_sum(fd_const);
+  ret = warp_sum(ret);
+  nF = warp_sum_i(nF);
+  nDT = warp_sum_i(nDT);
+  nT = warp_sum_i(nT);
+  nB = warp_sum_i(nB);
+  nFD = warp_sum_i(nFD);
+  slots = warp_sum_i(slots);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) kev += __shfl_xor_sync(0xffffffffu, kev, o);
+  if (lane == 0) {
+    const int ne = slots > 0 ? (qleaf ? 1 : 2) : 0;
+    a.cnt[e] = Cnt{ ne, ne * slots, nF, nDT, nT, nB, nFD };
+    a.childlen[e] = slots;
+    a.newbase[e] = fb + (fd_dlo + ret);
+    if (nFD) {
+      a.L[(size_t)key * a.T] += fd_const;  // constant local term (order 1)
+      if (a.Lord[key] < 1) a.Lord[key] = 1;
+    }
+    unsigned long long* ss = st.sst[slot];
+    atomicAdd(ss + sPairs, (unsigned long long)len);
+    if (nFD) atomicAdd(ss + sFD, (unsigned long long)nFD);
+    if (nF) atomicAdd(ss + sF, (unsigned long long)nF);
+    if (nDT - nT) atomicAdd(ss + sD, (unsigned long long)(nDT - nT));
+    if (nT) atomicAdd(ss + sT, (unsigned long long)nT);
+    if (nB) atomicAdd(ss + sB, (unsigned long long)nB);
+    if (kev) atomicAdd(ss + sKev, kev);
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kBlock) k_classify(TravArgs a)
+{
+  TravState& st = *a.st;
+  const int cur = st.cur, m = st.m[cur];
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int e = w0; e < m; e += nw) classify_entry<DT>(a, st, cur, e, lane);
+}
+
+// Device-side exclusive scan of the per-entry counts (graph / host-loop paths):
+// tile sums -> one-block scan of the tiles (+ capacity check) -> tile rescan.
+constexpr int kScanTiles = 256;
+__global__ void __launch_bounds__(256) k_scan_tiles(TravArgs a)
+{
+  const TravState& st = *a.st;
+  const int m = st.m[st.cur];
+  const int per = (m + kScanTiles - 1) / kScanTiles;
+  const int b0 = min(m, blockIdx.x * per), b1 = min(m, b0 + per);
+  Cnt acc{};
+  for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) acc = CntSum()(acc, a.cnt[i]);
+  using BR = cub::BlockReduce<Cnt, 256>;
+  __shared__ typename BR::TempStorage tmp;
+  const Cnt tot = BR(tmp).Reduce(acc, CntSum());
+  if (threadIdx.x == 0) a.tsum[blockIdx.x] = tot;
+}
+
+__device__ __forceinline__ bool over_capacity(const TravState& st, const Cnt& t, int gF, int gDT,
+                                              int gB)
+{
+  return t.e > st.capE || t.p > st.capP || (long long)gF + t.f > st.capF ||
+         (long long)gDT + t.dt > st.capDT || (long long)gB + t.b > st.capB;
+}
+
+__global__ void __launch_bounds__(kScanTiles) k_scan_top(TravArgs a)
+{
+  TravState& st = *a.st;
+  using BS = cub::BlockScan<Cnt, kScanTiles>;
+  __shared__ typename BS::TempStorage tmp;
+  Cnt agg, out;
+  BS(tmp).ExclusiveScan(a.tsum[threadIdx.x], out, Cnt{}, CntSum(), agg);
+  a.toff[threadIdx.x] = out;
+  if (threadIdx.x == 0) {
+    st.lvl = agg;
+    if (over_capacity(st, agg, st.nF, st.nDT, st.nB)) st.overflow = 1;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_scan_local(TravArgs a)
+{
+  const TravState& st = *a.st;
+  const int m = st.m[st.cur];
+  const int per = (m + kScanTiles - 1) / kScanTiles;
+  const int b0 = min(m, blockIdx.x * per), b1 = min(m, b0 + per);
+  using BS = cub::BlockScan<Cnt, 256>;
+  __shared__ typename BS::TempStorage tmp;
+  Cnt carry = a.toff[blockIdx.x];
+  for (int base = b0; base < b1; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const Cnt v = i < b1 ? a.cnt[i] : Cnt{};
+    Cnt ex, agg;
+    BS(tmp).ExclusiveScan(v, ex, Cnt{}, CntSum(), agg);
+    if (i < b1) a.cntoff[i] = CntSum()(carry, ex);
+    carry = CntSum()(carry, agg);
+    __syncthreads();
+  }
+}
+
+// One warp, one frontier query node: its part of the next frontier and its work
+// items, at the offsets `o` (exclusive scan of the level's counts).
+__device__ __forceinline__ void emit_entry(const TravArgs& a, int K, int cur, int gF, int gDT,
+                                           int gB, int e, const Cnt& o, int lane)
+{
+  const int nxt = cur ^ 1;
+  const int* fr = a.fr[cur];
+  int* nr = a.fr[nxt];
+  const Cnt c = a.cnt[e];
+  const int key = a.fq[cur][e];
+  const int slot = key / K;
+  const int Q = key - slot * K;
+  const int off = a.foff[cur][e], len = a.flen[cur][e];
+  const bool qleaf = a.Q.left[Q] < 0;
+  const int cl = a.childlen[e];
+  if (lane == 0 && c.e) {
+    const double nb = a.newbase[e];
+    if (qleaf) {
+      a.fq[nxt][o.e] = key;
+      a.fbase[nxt][o.e] = nb;
+      a.foff[nxt][o.e] = o.p;
+      a.flen[nxt][o.e] = cl;
+    } else {
+      a.fq[nxt][o.e] = slot * K + a.Q.left[Q];
+      a.fq[nxt][o.e + 1] = slot * K + a.Q.right[Q];
+      a.fbase[nxt][o.e] = nb;
+      a.fbase[nxt][o.e + 1] = nb;
+      a.foff[nxt][o.e] = o.p;
+      a.foff[nxt][o.e + 1] = o.p + cl;
+      a.flen[nxt][o.e] = cl;
+      a.flen[nxt][o.e + 1] = cl;
+    }
+  }
+  const int rF = a.cntF[key], rDT = a.cntDT[key], rB = a.cntB[key];
+  int runX = 0, runF = 0, runDT = 0, runB = 0;
+  for (int j0 = 0; j0 < len; j0 += 32) {
+    const int j = j0 + lane;
+    int kind = kE, order = 0, R = 0;
+    if (j < len) {
+      const int dcode = a.dec[off + j];
+      kind = dcode & 0xff;
+      order = dcode >> 8;
+      R = fr[off + j];
+    }
+    const bool rleaf = (j < len) ? a.R.left[R] < 0 : true;
+    int tot;
+    const int px = warp_excl_scan(kind == kX ? (rleaf ? 1 : 2) : 0, lane, tot);
+    if (kind == kX) {
+      const int dst = o.p + runX + px;
+      if (rleaf) {
+        nr[dst] = R;
+        if (!qleaf) nr[dst + cl] = R;
+      } else {
+        nr[dst] = a.R.left[R];
+        nr[dst + 1] = a.R.right[R];
+        if (!qleaf) {
+          nr[dst + cl] = a.R.left[R];
+          nr[dst + cl + 1] = a.R.right[R];
+        }
+      }
+    }
+    runX += tot;
+    int t2;
+    const int pf = warp_excl_scan(kind == kF, lane, t2);
+    if (kind == kF) a.itF[gF + o.f + runF + pf] = Item{ key, R, order | (kF << 8), rF + runF + pf };
+    runF += t2;
+    const int pd = warp_excl_scan(kind == kD || kind == kT, lane, t2);
+    if (kind == kD || kind == kT)
+      a.itDT[gDT + o.dt + runDT + pd] = Item{ key, R, order | (kind << 8), rDT + runDT + pd };
+    runDT += t2;
+    const int pb = warp_excl_scan(kind == kB, lane, t2);
+    if (kind == kB) a.itB[gB + o.b + runB + pb] = Item{ key, R, kB << 8, rB + runB + pb };
+    runB += t2;
+  }
+  if (lane == 0) {
+    a.cntF[key] = rF + runF;
+    a.cntDT[key] = rDT + runDT;
+    a.cntB[key] = rB + runB;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_emit(TravArgs a)
+{
+  const TravState& st = *a.st;
+  if (st.overflow) return;
+  const int cur = st.cur, m = st.m[cur];
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int e = w0; e < m; e += nw)
+    emit_entry(a, st.K, cur, st.nF, st.nDT, st.nB, e, a.cntoff[e], lane);
+}
+
+// Close a level (graph / host-loop paths): fold its totals into the state, flip the
+// frontier buffers and tell the WHILE node whether another level follows.
+__global__ void k_advance(TravArgs a, cudaGraphConditionalHandle hc, int use_cond)
+{
+  TravState& st = *a.st;
+  if (!st.overflow) {
+    const Cnt l = st.lvl;
+    st.nF += l.f;
+    st.nDT += l.dt;
+    st.nB += l.b;
+    st.m[st.cur ^ 1] = l.e;
+    st.p[st.cur ^ 1] = l.p;
+    st.cur ^= 1;
+    st.levels += 1;
+  }
+  const bool more = !st.overflow && st.m[st.cur] > 0;
+  if (use_cond) cudaGraphSetConditional(hc, more ? 1u : 0u);
+}
+
+// The whole level loop in ONE cooperative launch (one CTA per SM).  Per level:
+//   classify (warp per entry, grid-stride) | grid sync |
+//   tile sums over contiguous entry ranges; the last CTA to finish scans the tiles,
+//   checks capacities and publishes the level totals | grid sync |
+//   each CTA rescans its own range and emits it | grid sync.
+// Every CTA advances an identical private copy of (cur, m, item offsets), so no
+// further barrier is needed; CTA 0 writes the state back at the end.
+constexpr int kPBlock = 512;
+template <int DT>
+__global__ void __launch_bounds__(kPBlock) k_traverse(TravArgs a)
+{
+  cg::grid_group grid = cg::this_grid();
+  TravState& st = *a.st;
+  __shared__ int s_last;
+  using BR = cub::BlockReduce<Cnt, kPBlock>;
+  using BS = cub::BlockScan<Cnt, kPBlock>;
+  __shared__ union {
+    typename BR::TempStorage r;
+    typename BS::TempStorage s;
+  } tmp;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int G = gridDim.x;
+  const int K = st.K;
+  int cur = 0, m = st.nslots, p = st.nslots, gF = 0, gDT = 0, gB = 0, levels = 0;
+  for (;;) {
+    for (int e = gw; e < m; e += nw) classify_entry<DT>(a, st, cur, e, lane);
+    grid.sync();
+    const int per = (m + G - 1) / G;
+    const int b0 = min(m, blockIdx.x * per), b1 = min(m, b0 + per);
+    Cnt acc{};
+    for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) acc = CntSum()(acc, a.cnt[i]);
+    const Cnt tot = BR(tmp.r).Reduce(acc, CntSum());
+    if (threadIdx.x == 0) {
+      a.tsum[blockIdx.x] = tot;
+      __threadfence();
+      s_last = atomicAdd(&st.done, 1) == G - 1;
+    }
+    __syncthreads();
+    if (s_last) {  // last CTA: scan the tile sums, publish totals and the overflow verdict
+      __threadfence();
+      Cnt run{};
+      for (int base = 0; base < G; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const Cnt x = i < G ? ldcg_cnt(a.tsum + i) : Cnt{};  // other CTAs' tiles: bypass L1
+        Cnt ex, agg;
+        __syncthreads();
+        BS(tmp.s).ExclusiveScan(x, ex, Cnt{}, CntSum(), agg);
+        if (i < G) a.toff[i] = CntSum()(run, ex);
+        run = CntSum()(run, agg);
+      }
+      if (threadIdx.x == 0) {
+        st.lvl = run;
+        st.overflow = over_capacity(st, run, gF, gDT, gB);
+        st.done = 0;
+        __threadfence();
+      }
+    }
+    grid.sync();
+    const Cnt lv = ldcg_cnt(&st.lvl);
+    if (__ldcg(&st.overflow)) break;
+    Cnt carry = a.toff[blockIdx.x];
+    for (int base = b0; base < b1; base += blockDim.x) {
+      const int i = base + threadIdx.x;
+      const Cnt x = i < b1 ? a.cnt[i] : Cnt{};
+      Cnt ex, agg;
+      __syncthreads();
+      BS(tmp.s).ExclusiveScan(x, ex, Cnt{}, CntSum(), agg);
+      if (i < b1) a.cntoff[i] = CntSum()(carry, ex);
+      carry = CntSum()(carry, agg);
+    }
+    __syncthreads();
+    for (int e = b0 + wib; e < b1; e += blockDim.x / 32)
+      emit_entry(a, K, cur, gF, gDT, gB, e, a.cntoff[e], lane);
+    gF += lv.f;
+    gDT += lv.dt;
+    gB += lv.b;
+    cur ^= 1;
+    m = lv.e;
+    p = lv.p;
+    ++levels;
+    grid.sync();
+    if (m == 0) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st.cur = cur;
+    st.m[cur] = m;
+    st.p[cur] = p;
+    st.nF = gF;
+    st.nDT = gDT;
+    st.nB = gB;
+    st.levels = levels;
+  }
+}
+
+void launch_classify(int D, int grid, cudaStream_t s, const TravArgs& a)
+{
+  switch (D) {
+  case 1: k_classify<1><<<grid, kBlock, 0, s>>>(a); break;
+  case 2: k_classify<2><<<grid, kBlock, 0, s>>>(a); break;
+  case 3: k_classify<3><<<grid, kBlock, 0, s>>>(a); break;
+  case 4: k_classify<4><<<grid, kBlock, 0, s>>>(a); break;
+  case 5: k_classify<5><<<grid, kBlock, 0, s>>>(a); break;
+  default: k_classify<0><<<grid, kBlock, 0, s>>>(a); break;
+  }
+  CK_LAUNCH();
+}
+
+// The kernels of one level for the graph / host-loop paths.
+constexpr int kLevelKernels = 6;
+void launch_level(const TravArgs& a, int D, cudaStream_t s, cudaGraphConditionalHandle hc,
+                  int use_cond)
+{
+  const int grid = 148 * 4;
+  launch_classify(D, grid, s, a);
+  k_scan_tiles<<<kScanTiles, 256, 0, s>>>(a);
+  CK_LAUNCH();
+  k_scan_top<<<1, kScanTiles, 0, s>>>(a);
+  CK_LAUNCH();
+  k_scan_local<<<kScanTiles, 256, 0, s>>>(a);
+  CK_LAUNCH();
+  k_emit<<<grid, kBlock, 0, s>>>(a);
+  CK_LAUNCH();
+  k_advance<<<1, 1, 0, s>>>(a, hc, use_cond);
+  CK_LAUNCH();
+}
+
+__global__ void k_scatter_items(const Item* in, int n, const int* noff, Item* out)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const Item it = in[i];
+    out[noff[it.key] + it.rank] = it;
+  }
+}
+
+}  // namespace
+
+void Engine::destroy_graph()
+{
+  if (gexec_) cudaGraphExecDestroy(gexec_);
+  if (graph_) cudaGraphDestroy(graph_);
+  gexec_ = nullptr;
+  graph_ = nullptr;
+  gsig_.clear();
+}
+
+// Runs the whole level loop: preferably one cooperative kernel; else one CUDA graph
+// whose WHILE node repeats the level kernels until k_advance clears the condition;
+// else the host launches levels and polls.
+void Engine::run_levels(const void* args, const std::vector<const void*>& sig)
+{
+  const TravArgs& a = *static_cast<const TravArgs*>(args);
+  if (use_persistent_) {
+    void* fn = nullptr;
+    switch (D_) {
+    case 1: fn = (void*)k_traverse<1>; break;
+    case 2: fn = (void*)k_traverse<2>; break;
+    case 3: fn = (void*)k_traverse<3>; break;
+    case 4: fn = (void*)k_traverse<4>; break;
+    case 5: fn = (void*)k_traverse<5>; break;
+    default: fn = (void*)k_traverse<0>; break;
+    }
+    int dev = 0, nsm = 0, per_sm = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPBlock, 0));
+    if (per_sm >= 1) {
+      TravArgs copy = a;
+      void* kargs[] = { &copy };
+      CK(cudaLaunchCooperativeKernel(fn, nsm, kPBlock, kargs, 0, s_));
+      ++launch_counter();
+      return;
+    }
+    use_persistent_ = false;  // cannot co-schedule one CTA per SM: use the graph loop
+  }
+  if (use_graph_ && sig != gsig_) {
+    destroy_graph();
+    const uint64_t before = launch_counter();
+    try {
+      CK(cudaGraphCreate(&graph_, 0));
+      CK(cudaGraphConditionalHandleCreate(&hc_, graph_, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams p = {};
+      p.type = cudaGraphNodeTypeConditional;
+      p.conditional.handle = hc_;
+      p.conditional.type = cudaGraphCondTypeWhile;
+      p.conditional.size = 1;
+      cudaGraphNode_t node;
+      CK(cudaGraphAddNode(&node, graph_, nullptr, 0, &p));
+      cudaGraph_t body = p.conditional.phGraph_out[0];
+      CK(cudaStreamBeginCaptureToGraph(s_, body, nullptr, nullptr, 0,
+                                       cudaStreamCaptureModeThreadLocal));
+      launch_level(a, D_, s_, hc_, 1);
+      CK(cudaStreamEndCapture(s_, &body));
+      CK(cudaGraphInstantiate(&gexec_, graph_, 0));
+      gsig_ = sig;
+    } catch (const CudaError&) {
+      cudaStreamCaptureStatus cs;
+      if (cudaStreamIsCapturing(s_, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+        cudaGraph_t junk = nullptr;
+        cudaStreamEndCapture(s_, &junk);
+        if (junk) cudaGraphDestroy(junk);
+      }
+      cudaGetLastError();
+      destroy_graph();
+      use_graph_ = false;
+    }
+    launch_counter() = before;  // captured launches are counted when they execute
+  }
+  if (use_graph_) {
+    CK(cudaGraphLaunch(gexec_, s_));
+    return;
+  }
+  TravState* hs = static_cast<TravState*>(hst_);
+  for (;;) {
+    launch_level(a, D_, s_, 0, 0);
+    CK(cudaMemcpyAsync(hs, a.st, sizeof(TravState), cudaMemcpyDeviceToHost, s_));
+    CK(cudaStreamSynchronize(s_));
+    if (hs->overflow || hs->m[hs->cur] == 0) break;
+  }
+}
+
+void Engine::traverse(const DevTree& qt, const double* h, int nb)
+{
+  const int K = qt.nodes;
+  const int T = ser_.T;
+  const long long KB = (long long)K * nb;
+  if (KB > INT32_MAX / 2) throw OutOfMemory("batch too large: slots * nodes exceeds 2^30");
+  cudaStream_t s = s_;
+  L_.reserve((size_t)KB * T);
+  for (DevBuf<int>* b : { &Lord_, &cntF_, &cntDT_, &cntB_ }) b->reserve(KB);
+  if (!hst_) {
+    CK(cudaMallocHost(&hst_, sizeof(TravState)));
+    dst_.reserve(sizeof(TravState));
+  }
+  TravState* hs = static_cast<TravState*>(hst_);
+  TravState* ds = reinterpret_cast<TravState*>(dst_.p);
+  {  // first guesses; overflow regrows and the engine keeps the sizes
+    const int kb = (int)std::min<long long>(KB, INT32_MAX / 64);
+    capE_ = std::max(capE_, std::max(4096, 2 * kb));
+    capP_ = std::max(capP_, std::max(1 << 16, 16 * kb));
+    capF_ = std::max(capF_, std::max(4096, 2 * kb));
+    capDT_ = std::max(capDT_, std::max(4096, 2 * kb));
+    capB_ = std::max(capB_, std::max(1 << 16, 16 * kb));
+  }
+  for (int attempt = 0;; ++attempt) {
+    for (int b = 0; b < 2; ++b) {
+      fq_[b].reserve(capE_);
+      foff_[b].reserve(capE_);
+      flen_[b].reserve(capE_);
+      fbase_[b].reserve(capE_);
+      fr_[b].reserve(capP_);
+    }
+    pkmax_.reserve(capP_);
+    pkmin_.reserve(capP_);
+    dec_.reserve(capP_);
+    cnt_.reserve(capE_);
+    cntoff_.reserve(capE_);
+    childlen_.reserve(capE_);
+    newbase_.reserve(capE_);
+    ctsum_.reserve(kScanTiles);
+    ctoff_.reserve(kScanTiles);
+    itF_.reserve(capF_);
+    itDT_.reserve(capDT_);
+    itB_.reserve(capB_);
+
+    TravArgs a{};
+    a.Q = view_of(qt);
+    a.R = view_of(rt_);
+    a.D = D_;
+    a.pmax = ser_.pmax;
+    a.cost = cfg_.cost_model;
+    a.series = cfg_.mode == 1;
+    a.T = T;
+    a.st = ds;
+    for (int b = 0; b < 2; ++b) {
+      a.fq[b] = fq_[b].p;
+      a.foff[b] = foff_[b].p;
+      a.flen[b] = flen_[b].p;
+      a.fr[b] = fr_[b].p;
+      a.fbase[b] = fbase_[b].p;
+    }
+    a.pkmax = pkmax_.p;
+    a.pkmin = pkmin_.p;
+    a.dec = dec_.p;
+    a.cnt = cnt_.p;
+    a.cntoff = cntoff_.p;
+    a.tsum = ctsum_.p;
+    a.toff = ctoff_.p;
+    a.childlen = childlen_.p;
+    a.newbase = newbase_.p;
+    a.L = L_.p;
+    a.Lord = Lord_.p;
+    a.itF = itF_.p;
+    a.itDT = itDT_.p;
+    a.itB = itB_.p;
+    a.cntF = cntF_.p;
+    a.cntDT = cntDT_.p;
+    a.cntB = cntB_.p;
+    const std::vector<const void*> sig = {
+      a.Q.lo, a.Q.hi, a.Q.cen, a.Q.side, a.Q.left, a.Q.right, a.Q.count, a.Q.begin,
+      a.R.lo, a.R.hi, a.R.side, a.R.left, a.R.right, a.R.count,
+      a.st, a.fq[0], a.fq[1], a.foff[0], a.foff[1], a.flen[0], a.flen[1], a.fr[0], a.fr[1],
+      a.fbase[0], a.fbase[1], a.pkmax, a.pkmin, a.dec, a.cnt, a.cntoff, a.tsum, a.toff,
+      a.childlen, a.newbase, a.L, a.Lord, a.itF, a.itDT, a.itB, a.cntF, a.cntDT, a.cntB };
+
+    CK(cudaMemsetAsync(L_.p, 0, sizeof(double) * KB * T, s));
+    for (DevBuf<int>* b : { &Lord_, &cntF_, &cntDT_, &cntB_ })
+      CK(cudaMemsetAsync(b->p, 0, sizeof(int) * KB, s));
+    hs->eps = cfg_.epsilon;
+    hs->ntot = (double)n_;
+    hs->nslots = nb;
+    hs->K = K;
+    for (int b = 0; b < nb; ++b) {
+      hs->h[b] = h[b];
+      hs->scale[b] = -1.0 / (2.0 * h[b] * h[b]);
+    }
+    hs->capE = capE_;
+    hs->capP = capP_;
+    hs->capF = capF_;
+    hs->capDT = capDT_;
+    hs->capB = capB_;
+    CK(cudaMemcpyAsync(ds, hs, sizeof(TravState), cudaMemcpyHostToDevice, s));
+    k_trav_init<<<1, 64, 0, s>>>(a);
+    CK_LAUNCH();
+    run_levels(&a, sig);
+    CK(cudaMemcpyAsync(hs, ds, sizeof(TravState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!use_persistent_ && use_graph_) launch_counter() += (uint64_t)hs->levels * kLevelKernels;
+    if (!hs->overflow) break;
+    if (attempt > 10) throw OutOfMemory("traversal buffers keep overflowing");
+    const Cnt l = hs->lvl;
+    auto grow = [](int cap, long long need) {
+      if (need > INT32_MAX / 2) throw OutOfMemory("traversal exceeds 2^30 entries");
+      return (int)std::max<long long>(cap, 2 * need);
+    };
+    capE_ = grow(capE_, l.e);
+    capP_ = grow(capP_, l.p);
+    capF_ = grow(capF_, (long long)hs->nF + l.f);
+    capDT_ = grow(capDT_, (long long)hs->nDT + l.dt);
+    capB_ = grow(capB_, (long long)hs->nB + l.b);
+  }
+  slot_stats_.assign(nb, Stats{});
+  for (int b = 0; b < nb; ++b) {
+    Stats& st = slot_stats_[b];
+    const unsigned long long* ss = hs->sst[b];
+    st.levels = hs->levels;
+    st.pairs_visited = ss[sPairs];
+    st.prunes_finite_diff = ss[sFD];
+    st.prunes_farfield = ss[sF];
+    st.prunes_direct_local = ss[sD];
+    st.prunes_far_to_local = ss[sT];
+    st.base_cases = ss[sB];
+    st.kernel_evaluations = 2ull * ss[sPairs] + ss[sKev];
+  }
+  nF_ = hs->nF;
+  nDT_ = hs->nDT;
+  nB_ = hs->nB;
+
+  // counting sort of the items by key (stable: level order, then emit order)
+  auto sort_items = [&](DevBuf<Item>& in, long long nitems, DevBuf<int>& cnt, DevBuf<int>& off,
+                        DevBuf<Item>& out) {
+    off.reserve((size_t)KB + 1);
+    if (nitems == 0) return;
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, cnt.p, off.p, (int)KB, s);
+    scan_tmp_.reserve(need + 256);
+    size_t have = scan_tmp_.cap;
+    cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, cnt.p, off.p, (int)KB, s);
+    out.reserve(nitems);
+    k_scatter_items<<<ceil_div(nitems, 256), 256, 0, s>>>(in.p, (int)nitems, off.p, out.p);
+    CK_LAUNCH();
+  };
+  sort_items(itF_, nF_, cntF_, offF_, sF_);
+  sort_items(itDT_, nDT_, cntDT_, offDT_, sDT_);
+  sort_items(itB_, nB_, cntB_, offB_, sB_);
+}
+
+}  // namespace dfgtb

@@ -169,6 +169,27 @@ class DualTreeEngine:
         check(lib.dfgtb_compute(self._h, _dp(q), q.shape[0], float(h), _dp(out), None))
         return out
 
+    def compute_batch(self, queries, hs) -> np.ndarray:
+        """Sums for several bandwidths through one lock-step GPU traversal:
+        row b = compute(queries, hs[b]).  Returns (len(hs), n_queries)."""
+        hv = np.ascontiguousarray(hs, dtype=np.float64).ravel()
+        if queries is None or queries is self.refs:
+            q, nq, n_out = None, 0, self.refs.shape[0]
+        else:
+            q = _pts(queries)
+            if q.shape[1] != self.refs.shape[1]:
+                raise ValueError("query and reference dimensions differ")
+            nq = n_out = q.shape[0]
+        out = np.empty((hv.size, n_out))
+        st = (_capi.Stats * max(1, hv.size))()
+        check(lib.dfgtb_compute_batch(self._h, _dp(q) if q is not None else None, nq, _dp(hv),
+                                      hv.size, _dp(out), st))
+        self._batch_stats = [TraversalStats(**s.as_dict()) for s in st[:hv.size]]
+        return out
+
+    def batch_stats(self):
+        return list(getattr(self, "_batch_stats", []))
+
     def compute_device(self, d_queries: int, nq: int, h: float, d_out: int) -> None:
         """Device-pointer variant (inputs already resident in HBM)."""
         check(lib.dfgtb_compute_device(self._h, C.c_void_p(d_queries or 0), nq, float(h),

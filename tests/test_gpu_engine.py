@@ -192,6 +192,27 @@ def test_dfgt_matches_reference_within_eps(dfgtb, ref):
         assert np.all(np.abs(a - b) <= 0.0201 * np.abs(b) + 1e-300)
 
 
+def test_batched_bandwidths_bit_identical_to_single(dfgtb):
+    """compute_batch runs every bandwidth through one lock-step traversal; each slot's
+    decisions and accumulation order are its own, so results equal one-at-a-time runs
+    bit for bit (Q = R and Q != R)."""
+    w = datagen.config(2, scale_n=0.05)
+    e = dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(leaf_threshold=32))
+    hs = [s * w.h_s for s in w.scales] + [2 * s * w.h_s for s in w.scales]
+    batch = e.compute_batch(None, hs)
+    bstats = e.batch_stats()
+    for b, h in enumerate(hs):
+        single = e.compute(None, h)
+        assert np.array_equal(batch[b], single), b
+        a, s = vars(bstats[b]), vars(e.last_stats())
+        a.pop("levels"), s.pop("levels")  # a batch runs until its deepest slot is done
+        assert a == s
+    q = np.random.default_rng(8).random((777, 2))
+    batch = e.compute_batch(q, hs[:5])
+    for b, h in enumerate(hs[:5]):
+        assert np.array_equal(batch[b], e.compute(q, h))
+
+
 def test_l2l_chain_matches_direct_ancestor_evaluation(dfgtb, orc):
     """local_pushdown=1 runs the reference's L2L push-down chain (post_process,
     engine.cpp:294-304); the default evaluates every ancestor's local expansion at
