@@ -53,6 +53,7 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s_));
   upload_series(ser_, ser_dev_, s_);
   init_exp_constants(s_);
+  init_truncation_tables(s_);
   CK(cudaEventRecord(ev_[0], s_));
   build_tree(rt_, x_.p, (int)n, D_, cfg.leaf_threshold, s_);
   if (cfg.mode == 1) {

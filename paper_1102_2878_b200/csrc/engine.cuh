@@ -147,5 +147,7 @@ DevSeries series_view(const SeriesTables& t, const DevBuf<unsigned char>& dev);
 
 // Constant-bank coefficients of the base case's exp (execute.cu).
 void init_exp_constants(cudaStream_t s);
+// Constant tables of the error bounds (traverse.cu).
+void init_truncation_tables(cudaStream_t s);
 
 }  // namespace dfgtb

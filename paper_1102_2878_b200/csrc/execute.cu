@@ -147,6 +147,81 @@ __global__ void k_local_chunks(DevSeries g, TreeView Q, TreeView R, int K, const
   }
 }
 
+// Specialised D chunks for the default tables (p_max == PM, <= 64 terms): each thread
+// accumulates its points' Hermite products for every multi-index in registers
+// (compile-time digits), then the block reduces over threads in a fixed order.  T
+// chunks use the generic F2L.  Same partial table as dev_direct_local_partial.
+constexpr int kLocThreads = 64;
+template <int D, int PM>
+__global__ void __launch_bounds__(kLocThreads) k_local_chunks_t(DevSeries g, TreeView Q, TreeView R,
+                                                               int K, const Item* items,
+                                                               const LChunk* ch, int nch,
+                                                               const double* Mt, SlotView sv,
+                                                               double* part)
+{
+  constexpr int NP = ipow_c(PM, D);
+  __shared__ double red[NP][kLocThreads + 1];
+  extern __shared__ double sm[];
+  for (int c = blockIdx.x; c < nch; c += gridDim.x) {
+    const LChunk lc = ch[c];
+    const Item it = items[lc.item];
+    const int slot = it.key / K, node = it.key - slot * K;
+    const int kind = it.code >> 8, order = it.code & 0xff;
+    const double s = sv.s[slot];
+    double* P = part + (size_t)c * g.T;
+    const double* qc = Q.cen + (size_t)node * D;
+    if (kind != kD) {
+      dev_f2l_block(g, Mt + (size_t)it.r * g.T, R.cen + (size_t)it.r * D, qc, s, order, P, sm,
+                    sv.spow + (size_t)slot * kSPow, 1, g.pos);
+      __syncthreads();
+      continue;
+    }
+    double acc[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) acc[p] = 0.0;
+    double cq[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) cq[d] = qc[d];
+    for (int j = threadIdx.x; j < lc.n; j += kLocThreads) {
+      const double* rp = R.xs + (size_t)(lc.start + j) * D;
+      double H[D][PM];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const double t = (cq[d] - rp[d]) * s;
+        H[d][0] = exp(-t * t);
+        if (PM > 1) H[d][1] = 2.0 * t * H[d][0];
+#pragma unroll
+        for (int k = 1; k + 1 < PM; ++k) H[d][k + 1] = 2.0 * t * H[d][k] - 2.0 * k * H[d][k - 1];
+      }
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        double f = 1.0;
+        int rest = p;
+#pragma unroll
+        for (int d = D - 1; d >= 0; --d) {
+          f *= H[d][rest % PM];
+          rest /= PM;
+        }
+        acc[p] += f;
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) red[p][threadIdx.x] = acc[p];
+    __syncthreads();
+    for (int p = threadIdx.x; p < NP; p += kLocThreads) {
+      int rest = p, mx = 0;
+      for (int d = 0; d < D; ++d) {
+        mx = max(mx, rest % PM);
+        rest /= PM;
+      }
+      double sum = 0.0;
+      for (int k = 0; k < kLocThreads; ++k) sum += red[p][k];
+      if (mx < order) P[g.term_of_pos[p]] = sum;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void k_local_reduce(DevSeries g, int keys, const int* cnt, const int* off,
                                const Item* items, const int* choff, const double* part, double* L,
                                int* Lord)
@@ -835,8 +910,19 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
     CK_LAUNCH();
     lpart_.reserve((size_t)nch * T);
     const int smem = std::max(kLocSub * D_ * ser_.pmax, D_ * (2 * ser_.pmax)) * (int)sizeof(double);
-    k_local_chunks<<<std::min(nch, 148 * 16), 64, smem, s>>>(g, Q, R, K, sDT_.p, ch, nch, Mt_.p, sv,
-                                                             lpart_.p);
+    const int gl = std::min(nch, 148 * 16);
+    const int pm = ser_.pmax;
+#define LOC_T(DD, PP)                                                                            \
+  k_local_chunks_t<DD, PP><<<gl, kLocThreads, D_ * (2 * PP) * (int)sizeof(double), s>>>(          \
+    g, Q, R, K, sDT_.p, ch, nch, Mt_.p, sv, lpart_.p)
+    if (D_ == 1 && pm == 8) LOC_T(1, 8);
+    else if (D_ == 2 && pm == 6) LOC_T(2, 6);
+    else if (D_ == 3 && pm == 4) LOC_T(3, 4);
+    else if (D_ == 4 && pm == 2) LOC_T(4, 2);
+    else if (D_ == 5 && pm == 2) LOC_T(5, 2);
+    else
+      k_local_chunks<<<gl, 64, smem, s>>>(g, Q, R, K, sDT_.p, ch, nch, Mt_.p, sv, lpart_.p);
+#undef LOC_T
     CK_LAUNCH();
     k_local_reduce<<<std::min(KB, 148 * 16), 64, 0, s>>>(g, KB, cntDT_.p, offDT_.p, sDT_.p,
                                                          lchoff_.p, lpart_.p, L_.p, Lord_.p);

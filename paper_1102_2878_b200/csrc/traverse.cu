@@ -35,61 +35,66 @@ using namespace detail;
 namespace {
 
 // ------------------------------------------------------------------ truncation
-__device__ double d_binomial(int n, int k)
-{  // truncation.cpp:11-18
-  double b = 1.0;
-  for (int i = 1; i <= k; ++i) b *= (double)(n - k + i) / (double)i;
-  return b;
-}
-__device__ double d_sqrt_factorial(int p)
-{  // truncation.cpp:20-27
-  double f = 1.0;
-  for (int k = 2; k <= p; ++k) f *= k;
-  return sqrt(f);
-}
-__device__ double d_ipow(double x, int n)
+// Error bounds of truncation.cpp:40-81 in division-free form.  The reference tests
+//   bound(p) = count / (1-s)^(D*dpow) * S(p) <= tau,
+//   S(p) = sum_{k<D} C(D,k) a^k b^(D-k),
+// in increasing p (least_order, truncation.cpp:85-94).  (1-s) > 0 wherever a bound is
+// evaluated, so the test is count * S(p) <= tau * (1-s)^(D*dpow): the same decision
+// without the overflow of the prefactor (the reference's log-space fallback exists
+// only for that, truncation.cpp:46-52) and without one FP64 divide and square root
+// per candidate order.  1/sqrt(p!) and C(D,k) come from constant tables.
+__constant__ double c_isf[16];        // 1 / sqrt(p!)
+__constant__ double c_binom[17][17];  // C(n, k)
+
+__device__ __forceinline__ double d_ipow(double x, int n)
 {
   double r = 1.0;
   for (int i = 0; i < n; ++i) r *= x;
   return r;
 }
-__device__ double d_bound_sum(double count, double s, int dpow, double a, double b, int dim)
-{  // truncation.cpp:40-54 (log-space fallback when the prefactor overflows)
-  double sum = 0.0;
-  for (int k = 0; k < dim; ++k) sum += d_binomial(dim, k) * d_ipow(a, k) * d_ipow(b, dim - k);
-  const double pre = count / d_ipow(1.0 - s, dim * dpow);
-  double bound = pre * sum;
-  if (!isfinite(bound) && count > 0.0 && sum > 0.0)
-    bound = exp(log(count) - (double)(dim * dpow) * log1p(-s) + log(sum));
-  return bound;
+
+__device__ __forceinline__ double bound_sum_S(double a, double b, int dim)
+{  // sum_{k<dim} C(dim,k) a^k b^(dim-k)
+  double bp[kMaxDim + 1];
+  bp[0] = 1.0;
+  for (int k = 1; k <= dim; ++k) bp[k] = bp[k - 1] * b;
+  double sum = 0.0, ak = 1.0;
+  for (int k = 0; k < dim; ++k) {
+    sum += c_binom[dim][k] * ak * bp[dim - k];
+    ak *= a;
+  }
+  return sum;
 }
-__device__ double d_ff_bound(double count, double r, int p, int dim)
-{  // truncation.cpp:58-65 (local_error_bound is the same formula)
-  if (count <= 0.0) return 0.0;
-  const double rp = d_ipow(r, p);
-  return d_bound_sum(count, r, 1, 1.0 - rp, rp / d_sqrt_factorial(p), dim);
-}
-__device__ double d_f2l_bound(double count, double r, int p, int dim)
-{  // truncation.cpp:72-81
-  if (count <= 0.0) return 0.0;
-  const double s = 2.0 * r, sp = d_ipow(s, p);
-  return d_bound_sum(count, s, 2, (1.0 - sp) * (1.0 - sp), sp * (2.0 - sp) / d_sqrt_factorial(p),
-                     dim);
-}
+
+// farfield_order / local_accum_order (truncation.cpp:98-112): least p <= pmax with
+// the Lemma 3/4 bound <= tau, 0 if none or ratio >= 1.
 __device__ int d_order_ff(double ratio, double count, double tau, int pmax, int dim)
-{  // least_order + farfield_order / local_accum_order, truncation.cpp:85-112
+{
   if (ratio >= 1.0) return 0;
-  for (int p = 1; p <= pmax; ++p)
-    if (d_ff_bound(count, ratio, p, dim) <= tau) return p;
+  const double thr = tau * d_ipow(1.0 - ratio, dim);
+  double rp = 1.0;
+  for (int p = 1; p <= pmax; ++p) {
+    rp *= ratio;
+    if (count * bound_sum_S(1.0 - rp, rp * c_isf[p], dim) <= thr) return p;
+  }
   return 0;
 }
+
+// f2l_order (truncation.cpp:114-128): Lemma 5 with s = 2r, power 2D; 0 if r >= 1/2.
 __device__ int d_order_f2l(double ratio, double count, double tau, int pmax, int dim)
-{  // f2l_order, truncation.cpp:114-128
+{
   if (ratio >= 0.5) return 0;
-  for (int p = 1; p <= pmax; ++p)
-    if (d_f2l_bound(count, ratio, p, dim) <= tau) return p;
+  const double s = 2.0 * ratio;
+  const double thr = tau * d_ipow(1.0 - s, 2 * dim);
+  double sp = 1.0;
+  for (int p = 1; p <= pmax; ++p) {
+    sp *= s;
+    const double a = (1.0 - sp) * (1.0 - sp);
+    if (count * bound_sum_S(a, sp * (2.0 - sp) * c_isf[p], dim) <= thr) return p;
+  }
   return 0;
 }
+
 // choose_best_method, truncation.cpp:130-166 (ties F > D > T > E)
 __device__ void dev_choose(double nq, double nr, double sq, double sr, double h, double tau,
                            int pmax, int dim, int cost, int& kind, int& order)
@@ -626,6 +631,24 @@ __global__ void k_scatter_items(const Item* in, int n, const int* noff, Item* ou
 }
 
 }  // namespace
+
+void init_truncation_tables(cudaStream_t s)
+{
+  double isf[16], bin[17][17];
+  double f = 1.0;
+  for (int p = 0; p < 16; ++p) {
+    if (p > 1) f *= p;
+    isf[p] = 1.0 / std::sqrt(f);
+  }
+  for (int n = 0; n <= 16; ++n)
+    for (int k = 0; k <= 16; ++k) {
+      double b = k > n ? 0.0 : 1.0;
+      for (int i = 1; i <= k && k <= n; ++i) b *= (double)(n - k + i) / (double)i;  // truncation.cpp:11-18
+      bin[n][k] = b;
+    }
+  CK(cudaMemcpyToSymbolAsync(c_isf, isf, sizeof(isf), 0, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyToSymbolAsync(c_binom, bin, sizeof(bin), 0, cudaMemcpyHostToDevice, s));
+}
 
 void Engine::destroy_graph()
 {
