@@ -117,6 +117,9 @@ private:
   DevBuf<Item> itF_, itDT_, itB_, sF_, sDT_, sB_;
   DevBuf<unsigned char> scan_tmp_;
   DevBuf<double> red_;
+  DevBuf<unsigned long long> trace_;  // DFGTB_TRACE=1: per-level phase timestamps
+  DevBuf<unsigned long long> tflag_;  // look-back status words of the persistent traversal
+  unsigned int epoch_ = 0;
   // device-driven level loop: state (device + pinned host mirror), capacities, graph
   void* hst_ = nullptr;
   DevBuf<unsigned char> dst_;

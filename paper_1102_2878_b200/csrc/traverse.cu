@@ -27,6 +27,8 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 namespace dfgtb {
 namespace cg = cooperative_groups;
@@ -136,7 +138,8 @@ struct TravState {
   int m[2], p[2];                      // entries / pairs in each frontier buffer
   int nF, nDT, nB;                     // items emitted so far
   int overflow, levels;
-  int done;                            // CTAs finished with their tile sum (k_traverse)
+  int done;                            // CTAs finished with their tile sum (unused)
+  unsigned int epoch;                  // per launch: tags the look-back status words
   Cnt lvl;                             // totals of the current level
   unsigned long long sst[kMaxSlots][sNStat];  // per-slot TraversalStats
 };
@@ -156,6 +159,8 @@ struct TravArgs {
   int* Lord;
   Item *itF, *itDT, *itB;
   int *cntF, *cntDT, *cntB;
+  unsigned long long* trace;  // optional per-phase %globaltimer stamps (DFGTB_TRACE)
+  unsigned long long* tflag;  // look-back status words, one per CTA of k_traverse
 };
 
 __device__ __forceinline__ Cnt ldcg_cnt(const Cnt* p)
@@ -493,81 +498,165 @@ __global__ void k_advance(TravArgs a, cudaGraphConditionalHandle hc, int use_con
   if (use_cond) cudaGraphSetConditional(hc, more ? 1u : 0u);
 }
 
-// The whole level loop in ONE cooperative launch (one CTA per SM).  Per level:
-//   classify (warp per entry, grid-stride) | grid sync |
-//   tile sums over contiguous entry ranges; the last CTA to finish scans the tiles,
-//   checks capacities and publishes the level totals | grid sync |
-//   each CTA rescans its own range and emits it | grid sync.
-// Every CTA advances an identical private copy of (cur, m, item offsets), so no
-// further barrier is needed; CTA 0 writes the state back at the end.
+// Decoupled look-back over the CTAs of k_traverse (single-pass scan of the per-CTA
+// level counts).  Status words carry (epoch, level) so stale words of earlier levels
+// or launches read as "not yet published"; flag 1 = aggregate, 2 = inclusive prefix.
+__device__ __forceinline__ void st_flag(unsigned long long* p, unsigned long long v)
+{
+  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_flag(const unsigned long long* p)
+{
+  unsigned long long v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ Cnt warp_sum_cnt(Cnt v)
+{
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.e += __shfl_xor_sync(0xffffffffu, v.e, o);
+    v.p += __shfl_xor_sync(0xffffffffu, v.p, o);
+    v.f += __shfl_xor_sync(0xffffffffu, v.f, o);
+    v.dt += __shfl_xor_sync(0xffffffffu, v.dt, o);
+    v.t += __shfl_xor_sync(0xffffffffu, v.t, o);
+    v.b += __shfl_xor_sync(0xffffffffu, v.b, o);
+    v.fd += __shfl_xor_sync(0xffffffffu, v.fd, o);
+  }
+  return v;
+}
+
+// Called by one whole warp; returns the exclusive prefix of tile b (valid in all
+// lanes).  The warp inspects 32 predecessors at a time: it waits until all of them
+// have published, then sums aggregates down to the nearest inclusive prefix.
+__device__ Cnt lookback(const TravArgs& a, int b, const Cnt& agg, unsigned long long tag, int lane)
+{
+  if (b == 0) {
+    if (lane == 0) {
+      a.toff[0] = agg;  // inclusive prefix of tile 0
+      __threadfence();
+      st_flag(a.tflag, tag | 2);
+    }
+    return Cnt{};
+  }
+  if (lane == 0) {
+    a.tsum[b] = agg;
+    __threadfence();
+    st_flag(a.tflag + b, tag | 1);
+  }
+  Cnt excl{};
+  for (int top = b - 1;; top -= 32) {
+    const int j = top - lane;  // lane 0 = nearest predecessor
+    unsigned long long f = 0;
+    if (j >= 0) {
+      do {
+        f = ld_flag(a.tflag + j);
+      } while ((f & ~3ull) != tag);
+    }
+    __threadfence();
+    const unsigned inc = __ballot_sync(0xffffffffu, j >= 0 && (f & 3) == 2);
+    const int stop = inc ? __ffs(inc) - 1 : 32;  // nearest inclusive predecessor
+    Cnt v{};
+    if (j >= 0 && lane < stop) v = ldcg_cnt(a.tsum + j);
+    if (lane == stop) v = ldcg_cnt(a.toff + j);
+    excl = CntSum()(excl, warp_sum_cnt(v));
+    if (inc) break;
+  }
+  if (lane == 0) {
+    a.toff[b] = CntSum()(excl, agg);
+    __threadfence();
+    st_flag(a.tflag + b, tag | 2);
+  }
+  return excl;
+}
+
+// The whole level loop in ONE cooperative launch (one CTA per SM).  Each level is a
+// single phase: CTA b owns a contiguous range of frontier entries; its warps classify
+// them, the CTA scans its counts, learns its global offset by a decoupled look-back
+// over the preceding CTAs, and emits its entries -- then ONE grid-wide barrier makes
+// the next frontier visible.  The last CTA publishes the level totals and the
+// capacity verdict.  Every CTA advances an identical private copy of (cur, m, item
+// offsets); CTA 0 writes the state back at the end.
 constexpr int kPBlock = 512;
 template <int DT>
 __global__ void __launch_bounds__(kPBlock) k_traverse(TravArgs a)
 {
   cg::grid_group grid = cg::this_grid();
   TravState& st = *a.st;
-  __shared__ int s_last;
   using BR = cub::BlockReduce<Cnt, kPBlock>;
   using BS = cub::BlockScan<Cnt, kPBlock>;
   __shared__ union {
     typename BR::TempStorage r;
     typename BS::TempStorage s;
   } tmp;
+  __shared__ Cnt s_agg, s_excl;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
+  constexpr int kWarps = kPBlock / 32;
   const int G = gridDim.x;
   const int K = st.K;
+  const unsigned long long epoch = (unsigned long long)st.epoch << 32;
   int cur = 0, m = st.nslots, p = st.nslots, gF = 0, gDT = 0, gB = 0, levels = 0;
   for (;;) {
-    for (int e = gw; e < m; e += nw) classify_entry<DT>(a, st, cur, e, lane);
-    grid.sync();
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && levels < 512) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[levels * 4] = t;
+    }
     const int per = (m + G - 1) / G;
     const int b0 = min(m, blockIdx.x * per), b1 = min(m, b0 + per);
+    for (int e = b0 + wib; e < b1; e += kWarps) classify_entry<DT>(a, st, cur, e, lane);
+    __syncthreads();
     Cnt acc{};
     for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) acc = CntSum()(acc, a.cnt[i]);
-    const Cnt tot = BR(tmp.r).Reduce(acc, CntSum());
-    if (threadIdx.x == 0) {
-      a.tsum[blockIdx.x] = tot;
-      __threadfence();
-      s_last = atomicAdd(&st.done, 1) == G - 1;
+    const Cnt agg0 = BR(tmp.r).Reduce(acc, CntSum());
+    if (threadIdx.x == 0) s_agg = agg0;
+    __syncthreads();
+    if (wib == 0) {
+      const Cnt agg = s_agg;
+      const Cnt ex = lookback(a, blockIdx.x, agg, epoch | ((unsigned long long)levels << 2), lane);
+      if (lane == 0) {
+        s_excl = ex;
+        if (blockIdx.x == G - 1) {
+          const Cnt tot = CntSum()(ex, agg);
+          st.lvl = tot;
+          st.overflow = over_capacity(st, tot, gF, gDT, gB);
+        }
+      }
     }
     __syncthreads();
-    if (s_last) {  // last CTA: scan the tile sums, publish totals and the overflow verdict
-      __threadfence();
-      Cnt run{};
-      for (int base = 0; base < G; base += blockDim.x) {
+    if (a.trace && blockIdx.x == G - 1 && threadIdx.x == 0 && levels < 512) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[levels * 4 + 1] = t;
+    }
+    const Cnt excl = s_excl;
+    // everything this CTA writes ends below excl + agg: emit only if that fits (on
+    // overflow the level is abandoned and the host reruns with larger buffers)
+    if (!over_capacity(st, CntSum()(excl, s_agg), gF, gDT, gB)) {
+      Cnt carry = excl;
+      for (int base = b0; base < b1; base += blockDim.x) {
         const int i = base + threadIdx.x;
-        const Cnt x = i < G ? ldcg_cnt(a.tsum + i) : Cnt{};  // other CTAs' tiles: bypass L1
-        Cnt ex, agg;
+        const Cnt x = i < b1 ? a.cnt[i] : Cnt{};
+        Cnt ex, ag;
         __syncthreads();
-        BS(tmp.s).ExclusiveScan(x, ex, Cnt{}, CntSum(), agg);
-        if (i < G) a.toff[i] = CntSum()(run, ex);
-        run = CntSum()(run, agg);
+        BS(tmp.s).ExclusiveScan(x, ex, Cnt{}, CntSum(), ag);
+        if (i < b1) a.cntoff[i] = CntSum()(carry, ex);
+        carry = CntSum()(carry, ag);
       }
-      if (threadIdx.x == 0) {
-        st.lvl = run;
-        st.overflow = over_capacity(st, run, gF, gDT, gB);
-        st.done = 0;
-        __threadfence();
-      }
+      __syncthreads();
+      for (int e = b0 + wib; e < b1; e += kWarps)
+        emit_entry(a, K, cur, gF, gDT, gB, e, a.cntoff[e], lane);
     }
     grid.sync();
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && levels < 512) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[levels * 4 + 2] = t;
+      a.trace[(levels + 1) * 4 + 3] = t;
+    }
     const Cnt lv = ldcg_cnt(&st.lvl);
     if (__ldcg(&st.overflow)) break;
-    Cnt carry = a.toff[blockIdx.x];
-    for (int base = b0; base < b1; base += blockDim.x) {
-      const int i = base + threadIdx.x;
-      const Cnt x = i < b1 ? a.cnt[i] : Cnt{};
-      Cnt ex, agg;
-      __syncthreads();
-      BS(tmp.s).ExclusiveScan(x, ex, Cnt{}, CntSum(), agg);
-      if (i < b1) a.cntoff[i] = CntSum()(carry, ex);
-      carry = CntSum()(carry, agg);
-    }
-    __syncthreads();
-    for (int e = b0 + wib; e < b1; e += blockDim.x / 32)
-      emit_entry(a, K, cur, gF, gDT, gB, e, a.cntoff[e], lane);
     gF += lv.f;
     gDT += lv.dt;
     gB += lv.b;
@@ -575,7 +664,6 @@ __global__ void __launch_bounds__(kPBlock) k_traverse(TravArgs a)
     m = lv.e;
     p = lv.p;
     ++levels;
-    grid.sync();
     if (m == 0) break;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -588,6 +676,7 @@ __global__ void __launch_bounds__(kPBlock) k_traverse(TravArgs a)
     st.levels = levels;
   }
 }
+
 
 void launch_classify(int D, int grid, cudaStream_t s, const TravArgs& a)
 {
@@ -811,6 +900,17 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     a.cntF = cntF_.p;
     a.cntDT = cntDT_.p;
     a.cntB = cntB_.p;
+    if (!tflag_.p) {
+      tflag_.reserve(kScanTiles);
+      CK(cudaMemsetAsync(tflag_.p, 0, sizeof(unsigned long long) * kScanTiles, s));
+    }
+    a.tflag = tflag_.p;
+    static const bool tracing = std::getenv("DFGTB_TRACE") != nullptr;
+    if (tracing) {
+      trace_.reserve(512 * 4);
+      CK(cudaMemsetAsync(trace_.p, 0, sizeof(unsigned long long) * 512 * 4, s));
+      a.trace = trace_.p;
+    }
     const std::vector<const void*> sig = {
       a.Q.lo, a.Q.hi, a.Q.cen, a.Q.side, a.Q.left, a.Q.right, a.Q.count, a.Q.begin,
       a.R.lo, a.R.hi, a.R.side, a.R.left, a.R.right, a.R.count,
@@ -834,6 +934,7 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     hs->capF = capF_;
     hs->capDT = capDT_;
     hs->capB = capB_;
+    hs->epoch = ++epoch_;  // never 0: zeroed status words read as unpublished
     CK(cudaMemcpyAsync(ds, hs, sizeof(TravState), cudaMemcpyHostToDevice, s));
     k_trav_init<<<1, 64, 0, s>>>(a);
     CK_LAUNCH();
@@ -841,6 +942,15 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     CK(cudaMemcpyAsync(hs, ds, sizeof(TravState), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (!use_persistent_ && use_graph_) launch_counter() += (uint64_t)hs->levels * kLevelKernels;
+    if (a.trace) {  // per level: classify | scan | emit (microseconds)
+      std::vector<unsigned long long> tr(512 * 4);
+      CK(cudaMemcpy(tr.data(), a.trace, sizeof(unsigned long long) * tr.size(),
+                    cudaMemcpyDeviceToHost));
+      for (int L = 0; L < std::min(hs->levels, 511); ++L)
+        std::fprintf(stderr, "DFGTB_TRACE level %d: classify+lookback %.1f us, emit+sync %.1f us (%.1f)\n", L,
+                     (tr[L * 4 + 1] - tr[L * 4]) * 1e-3, (tr[L * 4 + 2] - tr[L * 4 + 1]) * 1e-3,
+                     (tr[(L + 1) * 4 + 3] - tr[L * 4 + 2]) * 1e-3);
+    }
     if (!hs->overflow) break;
     if (attempt > 10) throw OutOfMemory("traversal buffers keep overflowing");
     const Cnt l = hs->lvl;
