@@ -332,6 +332,31 @@ __device__ __forceinline__ double exp_negy(double y)
   return __hiloint2double(__double2hiint(p) + (ni << 20), __double2loint(p));
 }
 
+// Table-driven exp(-y), 0 <= y <= 708: -y = (64 m + j) ln2/64 + r, |r| <= ln2/128,
+// exp(-y) = 2^m * 2^(j/64) * e^r with 2^(j/64) from a 64-entry shared-memory table and
+// e^r by a degree-5 Taylor polynomial (truncation r^6/6! < 3.5e-17 relative).  11 FP64
+// instructions instead of 16, still ~1.5 ulp: no reduced precision, nothing charged
+// to eps.  c_exp64 = {64 log2 e, ln2_hi/64, ln2_lo/64, 1/5!, 1/4!, 1/3!, 1/2!}.
+__constant__ double c_exp64[7];
+__constant__ double c_exp2tab[64];  // 2^(j/64)
+
+__device__ __forceinline__ double exp_negy_t(double y, const double* tab)
+{
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
+  const double t = fma(-y, c_exp64[0], magic);
+  const double n = t - magic;  // = 64 m + j
+  double r = fma(n, -c_exp64[1], -y);
+  r = fma(n, -c_exp64[2], r);
+  double p = fma(c_exp64[3], r, c_exp64[4]);
+  p = fma(p, r, c_exp64[5]);
+  p = fma(p, r, c_exp64[6]);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int k = __double2loint(t);
+  const double v = p * tab[k & 63];
+  return __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));
+}
+
 // Scaled, centred, padded coordinates for the base case, per slot:
 // x' = (x - c0) / (h sqrt 2) so that |q' - r'|^2 = |q - r|^2 / (2 h^2) (stride DP).
 __global__ void k_scale_points(const double* xs, int n, int D, int DP, int nb, const double* c0,
@@ -366,20 +391,38 @@ struct PtLoad {
   }
 };
 
+// Compact reference-leaf records for the base case, in sorted item order:
+// {first sorted position, count}, count negated when the traversal could not prove
+// y <= 708 for every pair (then the careful exp path runs).
+__global__ void k_base_records(const Item* items, int n, TreeView R, int2* rec)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Item it = items[i];
+  const int c = R.count[it.r];
+  rec[i] = make_int2(R.begin[it.r], (it.code & 1) ? c : -c);
+}
+
 // K10: exhaustive base case (Traversal::base_case, engine.cpp:239-269).  One warp per
-// task: lanes own queries, each reference point arrives as one warp-uniform vector
-// load (broadcast), two pairs in flight per iteration.  A reference leaf whose box
-// bound guarantees y <= 708 for every pair takes the branch-free path; otherwise pairs
-// beyond the fast range fall back to libdevice exp (exact underflow behaviour).
+// task = (slot, query leaf, 32-query chunk, run of <= kTaskItems reference leaves).
+// A chunk of qc queries gets k = 32/qc lanes per query (lane -> query lane % qc,
+// reference points j = lane/qc, +k, ...), combined by shuffles at the end in a fixed
+// order, so small leaves still fill the warp.  Reference points arrive as warp-
+// broadcast 16-byte loads of scaled, centred coordinates (|q'-r'|^2 is the exponent
+// directly), four pairs in flight per lane, the next leaf record prefetched.  Leaves
+// whose box bound proves y <= 708 run the branch-free fast exp; others fall back to
+// libdevice exp beyond the fast range (exact underflow behaviour).
 template <int DT>
-__global__ void __launch_bounds__(kBlock) k_base_case(TreeView Q, TreeView R, int K,
-                                                      const BTask* tasks, int ntasks,
-                                                      const Item* items, const double* xq,
-                                                      const double* xr, int nq, int nr,
-                                                      SlotView sv, double* part)
+__global__ void __launch_bounds__(kBlock, 6) k_base_case(TreeView Q, int K, const BTask* tasks,
+                                                      int ntasks, const int2* rec,
+                                                      const double* xq, const double* xr, int nq,
+                                                      int nr, double* part)
 {
   constexpr int D = DT;
   constexpr int DP = PtLoad<DT>::DP;
+  __shared__ double tab[64];
+  if (threadIdx.x < 64) tab[threadIdx.x] = c_exp2tab[threadIdx.x];
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -388,26 +431,27 @@ __global__ void __launch_bounds__(kBlock) k_base_case(TreeView Q, TreeView R, in
     const int slot = t.key / K, leaf = t.key - slot * K;
     const double* xqs = xq + (size_t)slot * nq * DP;
     const double* xrs = xr + (size_t)slot * nr * DP;
-    const double s2 = sv.s2[slot];
-    const int qb = Q.begin[leaf] + t.q0;
-    const bool act = lane < Q.count[leaf] - t.q0;
+    const int qc = min(32, Q.count[leaf] - t.q0);
+    const int kq = 32 / qc;  // lanes per query
+    const int qi = lane % qc, sub = lane / qc;
+    const bool act = sub < kq;
     double q[DP];
-    PtLoad<DT>::load(xqs, act ? qb + lane : qb, q);
-    const double* qlo = Q.lo + (size_t)leaf * D;
-    const double* qhi = Q.hi + (size_t)leaf * D;
-    double acc0 = 0.0, acc1 = 0.0;
+    PtLoad<DT>::load(xqs, Q.begin[leaf] + t.q0 + qi, q);
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    int2 nxt = rec[t.item0];
     for (int k = t.item0; k < t.item1; ++k) {
-      const int r = items[k].r;
-      const double* rp = xrs + (size_t)R.begin[r] * DP;
-      const int rc = R.count[r];
-      double dl, du;
-      box_bounds<DT>(qlo, qhi, R.lo + (size_t)r * D, R.hi + (size_t)r * D, D, dl, du);
-      if (s2 * du <= 708.0) {
-        int j = 0;
-        for (; j + 1 < rc; j += 2) {
+      const int2 cur = nxt;
+      if (k + 1 < t.item1) nxt = rec[k + 1];
+      const double* rp = xrs + (size_t)cur.x * DP;
+      const bool fast = cur.y > 0;
+      const int rc = fast ? cur.y : -cur.y;
+      if (!act) continue;
+      int j = sub;
+      if (fast) {
+        for (; j + kq < rc; j += 2 * kq) {
           double a[DP], b[DP];
           PtLoad<DT>::load(rp, j, a);
-          PtLoad<DT>::load(rp, j + 1, b);
+          PtLoad<DT>::load(rp, j + kq, b);
           double ya = 0.0, yb = 0.0;
 #pragma unroll
           for (int d = 0; d < D; ++d) {
@@ -415,10 +459,10 @@ __global__ void __launch_bounds__(kBlock) k_base_case(TreeView Q, TreeView R, in
             ya = fma(ta, ta, ya);
             yb = fma(tb, tb, yb);
           }
-          acc0 += exp_negy(ya);
-          acc1 += exp_negy(yb);
+          acc0 += exp_negy_t(ya, tab);  // two chains: ptxas interleaves them
+          acc1 += exp_negy_t(yb, tab);
         }
-        if (j < rc) {
+        for (; j < rc; j += kq) {
           double a[DP];
           PtLoad<DT>::load(rp, j, a);
           double ya = 0.0;
@@ -427,10 +471,10 @@ __global__ void __launch_bounds__(kBlock) k_base_case(TreeView Q, TreeView R, in
             const double ta = q[d] - a[d];
             ya = fma(ta, ta, ya);
           }
-          acc0 += exp_negy(ya);
+          acc0 += exp_negy_t(ya, tab);
         }
       } else {
-        for (int j = 0; j < rc; ++j) {
+        for (; j < rc; j += kq) {
           double a[DP];
           PtLoad<DT>::load(rp, j, a);
           double ya = 0.0;
@@ -443,9 +487,17 @@ __global__ void __launch_bounds__(kBlock) k_base_case(TreeView Q, TreeView R, in
         }
       }
     }
-    part[(size_t)w * 32 + lane] = acc0 + acc1;
+    double acc = (acc0 + acc1) + (acc2 + acc3);
+    if (!act) acc = 0.0;
+    double tot = acc;
+    for (int s2 = 1; s2 < kq; ++s2) {  // lanes of the same query, fixed order
+      const double v = __shfl_sync(0xffffffffu, acc, (lane + s2 * qc) & 31);
+      tot += v;
+    }
+    if (sub == 0) part[(size_t)w * 32 + qi] = tot;
   }
 }
+
 
 // Generic dimension (D > 5): scalar loads of the scaled coordinates, libdevice exp.
 __global__ void __launch_bounds__(kBlock) k_base_case_any(TreeView Q, TreeView R, int K, int D,
@@ -755,11 +807,11 @@ __global__ void k_dfma_peak(double* out, int iters)
 int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }
 
 void launch_base(int D, int grid, cudaStream_t s, TreeView Q, TreeView R, int K,
-                 const BTask* tasks, int ntasks, const Item* items, const double* xq,
-                 const double* xr, int nq, int nr, SlotView sv, double* part)
+                 const BTask* tasks, int ntasks, const Item* items, const int2* rec,
+                 const double* xq, const double* xr, int nq, int nr, double* part)
 {
 #define BASE(DD) \
-  k_base_case<DD><<<grid, kBlock, 0, s>>>(Q, R, K, tasks, ntasks, items, xq, xr, nq, nr, sv, part)
+  k_base_case<DD><<<grid, kBlock, 0, s>>>(Q, K, tasks, ntasks, rec, xq, xr, nq, nr, part)
   switch (D) {
   case 1: BASE(1); break;
   case 2: BASE(2); break;
@@ -788,6 +840,13 @@ void init_exp_constants(cudaStream_t s)
     k[3 + (12 - i)] = 1.0 / f;
   }
   CK(cudaMemcpyToSymbolAsync(c_expk, k, sizeof(k), 0, cudaMemcpyHostToDevice, s));
+  // table-driven variant: 64 log2(e), Cody-Waite ln2/64 split, 1/5! .. 1/2!
+  double k64[7] = { 64.0 * 1.4426950408889634, 6.93147180369123816490e-01 / 64.0,
+                    1.90821492927058770002e-10 / 64.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5 };
+  double tab[64];
+  for (int j = 0; j < 64; ++j) tab[j] = std::exp2((double)j / 64.0);  // correctly rounded in glibc
+  CK(cudaMemcpyToSymbolAsync(c_exp64, k64, sizeof(k64), 0, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyToSymbolAsync(c_exp2tab, tab, sizeof(tab), 0, cudaMemcpyHostToDevice, s));
 }
 
 // Unscaled moments of every reference node, once per tree (tables <= 4096 terms).
@@ -962,6 +1021,10 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
                                                    leaf_task_.p);
     CK_LAUNCH();
     bpart_.reserve((size_t)ntasks * 32);
+    brec_.reserve((size_t)nB_ * 2 + 2);
+    k_base_records<<<ceil_div(nB_, 256), 256, 0, s>>>(sB_.p, (int)nB_, R,
+                                                      reinterpret_cast<int2*>(brec_.p));
+    CK_LAUNCH();
   } else {
     bpart_.reserve(32);
   }
@@ -985,7 +1048,7 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
   CK(cudaEventRecord(ev_[9], s));
   if (ntasks)
     launch_base(D_, grid_warps(ntasks), s, Q, R, K, reinterpret_cast<const BTask*>(tasks_.p), ntasks,
-                sB_.p, xq, xr, qt.n, rt_.n, sv, bpart_.p);
+                sB_.p, reinterpret_cast<const int2*>(brec_.p), xq, xr, qt.n, rt_.n, bpart_.p);
   CK(cudaEventRecord(ev_[6], s));
   s_ff_.reserve((size_t)qt.n * nb);
   if (nF_) {

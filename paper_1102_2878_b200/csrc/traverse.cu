@@ -268,7 +268,12 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
         dev_choose(nq, nr, sq, a.R.side[R], h, tau, a.pmax, D, a.cost, kind, order);
         if (kind == kE) kind = kX;
       }
-      if (kind == kX && qleaf && a.R.left[R] < 0) kind = kB;
+      if (kind == kX && qleaf && a.R.left[R] < 0) {
+        kind = kB;
+        // every pair of this leaf pair has y = d^2/2h^2 <= 708 (K(d_max) >= e^-707.97):
+        // the base case may use its fast exp without underflow handling
+        order = kmin >= 3.4e-308 ? 1 : 0;
+      }
       if (kind == kX) {
         slots += a.R.left[R] < 0 ? 1 : 2;
       } else if (kind == kB) {
@@ -457,7 +462,7 @@ __device__ __forceinline__ void emit_entry(const TravArgs& a, int K, int cur, in
       a.itDT[gDT + o.dt + runDT + pd] = Item{ key, R, order | (kind << 8), rDT + runDT + pd };
     runDT += t2;
     const int pb = warp_excl_scan(kind == kB, lane, t2);
-    if (kind == kB) a.itB[gB + o.b + runB + pb] = Item{ key, R, kB << 8, rB + runB + pb };
+    if (kind == kB) a.itB[gB + o.b + runB + pb] = Item{ key, R, (kB << 8) | order, rB + runB + pb };
     runB += t2;
   }
   if (lane == 0) {
