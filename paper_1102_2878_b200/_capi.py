@@ -55,7 +55,8 @@ EXPORTS = (
     "dfgtb_last_timings",
     "dfgtb_p_max", "dfgtb_cv", "dfgtb_sweep", "dfgtb_lkcv_from_sums", "dfgtb_lscv_from_sums",
     "dfgtb_tree_nodes", "dfgtb_tree_height", "dfgtb_export_tree", "dfgtb_naive",
-    "dfgtb_series_op", "dfgtb_dfma_peak", "dfgtb_device_count", "dfgtb_stream",
+    "dfgtb_series_op", "dfgtb_dfma_peak", "dfgtb_device_count", "dfgtb_release_cached_memory",
+    "dfgtb_stream",
     "dfgtb_launch_count", "dfgtb_last_error",
 )
 
@@ -90,6 +91,7 @@ def _load():
                                       _D]),
         "dfgtb_dfma_peak": (C.c_double, []),
         "dfgtb_device_count": (C.c_int, []),
+        "dfgtb_release_cached_memory": (None, []),
         "dfgtb_stream": (C.c_size_t, [V]),
         "dfgtb_launch_count": (C.c_uint64, [V]),
         "dfgtb_last_error": (C.c_char_p, []),

@@ -441,6 +441,8 @@ int dfgtb_device_count(void)
   return n;
 }
 
+void dfgtb_release_cached_memory(void) { cache_release_all(); }
+
 double dfgtb_dfma_peak(void)
 {
   double v = -1.0;

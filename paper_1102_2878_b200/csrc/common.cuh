@@ -42,6 +42,15 @@ uint64_t& launch_counter();
     ++::dfgtb::launch_counter();                                                       \
   } while (0)
 
+// Process-wide caching device allocator (power-of-two size classes, like PyTorch's
+// caching allocator): engines created and destroyed in a loop reuse their memory
+// instead of paying cudaMalloc/cudaFree each time.  A block returned to the cache
+// may still be read by queued kernels, so returning synchronises the device first
+// (the guarantee cudaFree gave).  dfgtb_release_cached_memory() empties the cache.
+void* cache_alloc(size_t bytes);
+void cache_free(void* p, size_t bytes);
+void cache_release_all();
+
 // Growable device buffer (capacity only ever grows; contents not preserved on growth).
 template <class T>
 struct DevBuf {
@@ -53,11 +62,11 @@ struct DevBuf {
   ~DevBuf() { release(); }
   void release()
   {
-    if (p) cudaFree(p);
+    if (p) cache_free(p, cap * sizeof(T));
     p = nullptr;
     cap = 0;
   }
-  // ensure room for n elements; growth is geometric to amortise cudaMalloc
+  // ensure room for n elements; growth is geometric
   T* reserve(size_t n)
   {
     if (n <= cap && p) return p;
@@ -65,24 +74,7 @@ struct DevBuf {
     while (c < n) c *= 2;
     if (c < 256) c = 256;
     release();
-    CK(cudaMalloc(&p, c * sizeof(T)));
-    cap = c;
-    return p;
-  }
-  // ensure room, preserving the first `keep` elements
-  T* grow_keep(size_t n, size_t keep, cudaStream_t s)
-  {
-    if (n <= cap && p) return p;
-    size_t c = cap ? cap : 256;
-    while (c < n) c *= 2;
-    T* q = nullptr;
-    CK(cudaMalloc(&q, c * sizeof(T)));
-    if (p && keep) CK(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
-    if (p) {
-      CK(cudaStreamSynchronize(s));
-      cudaFree(p);
-    }
-    p = q;
+    p = static_cast<T*>(cache_alloc(c * sizeof(T)));
     cap = c;
     return p;
   }

@@ -9,6 +9,8 @@
 #include "internal.cuh"
 
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 
 namespace dfgtb {
 
@@ -16,6 +18,87 @@ uint64_t& launch_counter()
 {
   static uint64_t n = 0;
   return n;
+}
+
+// ---------------------------------------------------------- caching allocators
+namespace {
+std::mutex g_cache_mu;
+std::unordered_map<size_t, std::vector<void*>>& dev_cache()
+{
+  static auto* c = new std::unordered_map<size_t, std::vector<void*>>();  // never destroyed
+  return *c;
+}
+std::unordered_map<size_t, std::vector<void*>>& host_cache()
+{
+  static auto* c = new std::unordered_map<size_t, std::vector<void*>>();
+  return *c;
+}
+}  // namespace
+
+void* cache_alloc(size_t bytes)
+{
+  {
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    auto it = dev_cache().find(bytes);
+    if (it != dev_cache().end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {  // give the cache back and retry once
+    cudaGetLastError();
+    cache_release_all();
+    e = cudaMalloc(&p, bytes);
+  }
+  CK(e);
+  return p;
+}
+
+void cache_free(void* p, size_t bytes)
+{
+  if (cudaDeviceSynchronize() != cudaSuccess) {  // context gone (process exit) or faulted
+    cudaGetLastError();
+    return;
+  }
+  std::lock_guard<std::mutex> g(g_cache_mu);
+  dev_cache()[bytes].push_back(p);
+}
+
+void cache_release_all()
+{
+  cudaDeviceSynchronize();
+  std::lock_guard<std::mutex> g(g_cache_mu);
+  for (auto& kv : dev_cache())
+    for (void* p : kv.second) cudaFree(p);
+  dev_cache().clear();
+  for (auto& kv : host_cache())
+    for (void* p : kv.second) cudaFreeHost(p);
+  host_cache().clear();
+}
+
+void* pinned_alloc(size_t bytes)
+{
+  {
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    auto it = host_cache().find(bytes);
+    if (it != host_cache().end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      return p;
+    }
+  }
+  void* p = nullptr;
+  CK(cudaMallocHost(&p, bytes));
+  return p;
+}
+
+void pinned_free(void* p, size_t bytes)
+{
+  std::lock_guard<std::mutex> g(g_cache_mu);
+  host_cache()[bytes].push_back(p);
 }
 
 int default_p_max(int D)
@@ -76,7 +159,7 @@ Engine::~Engine()
 {
   if (s_) cudaStreamSynchronize(s_);
   destroy_graph();
-  if (hst_) cudaFreeHost(hst_);
+  if (hst_) pinned_free(hst_, hst_bytes_);
   for (auto& e : ev_) cudaEventDestroy(e);
   if (s_) cudaStreamDestroy(s_);
 }

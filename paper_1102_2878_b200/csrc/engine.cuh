@@ -122,6 +122,7 @@ private:
   unsigned int epoch_ = 0;
   // device-driven level loop: state (device + pinned host mirror), capacities, graph
   void* hst_ = nullptr;
+  size_t hst_bytes_ = 0;
   DevBuf<unsigned char> dst_;
   int capE_ = 0, capP_ = 0, capF_ = 0, capDT_ = 0, capB_ = 0;
   bool use_persistent_ = true;  // one cooperative kernel runs every level
@@ -147,6 +148,10 @@ double measure_dfma_peak(int device);
 // Series term tables -> one device blob, and the device view over it.
 void upload_series(const SeriesTables& t, DevBuf<unsigned char>& dev, cudaStream_t s);
 DevSeries series_view(const SeriesTables& t, const DevBuf<unsigned char>& dev);
+
+// Pinned host blocks (cached like device memory; engine.cu).
+void* pinned_alloc(size_t bytes);
+void pinned_free(void* p, size_t bytes);
 
 // Constant-bank coefficients of the base case's exp (execute.cu).
 void init_exp_constants(cudaStream_t s);

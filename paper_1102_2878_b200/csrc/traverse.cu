@@ -838,7 +838,8 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   L_.reserve((size_t)KB * T);
   for (DevBuf<int>* b : { &Lord_, &cntF_, &cntDT_, &cntB_ }) b->reserve(KB);
   if (!hst_) {
-    CK(cudaMallocHost(&hst_, sizeof(TravState)));
+    hst_ = pinned_alloc(sizeof(TravState));
+    hst_bytes_ = sizeof(TravState);
     dst_.reserve(sizeof(TravState));
   }
   TravState* hs = static_cast<TravState*>(hst_);
