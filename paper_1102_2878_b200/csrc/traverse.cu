@@ -170,16 +170,33 @@ __device__ __forceinline__ Cnt ldcg_cnt(const Cnt* p)
               __ldcg(q + 6) };
 }
 
+// Collectives over aligned groups of W lanes (W = 32: the whole warp).  Every lane
+// of the warp must call them (groups are segments of the shuffles' width).
+template <int W>
 __device__ __forceinline__ int warp_excl_scan(int v, int lane, int& total)
 {
   int x = v;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
+  for (int o = 1; o < W; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o, W);
     if (lane >= o) x += y;
   }
-  total = __shfl_sync(0xffffffffu, x, 31);
+  total = __shfl_sync(0xffffffffu, x, W - 1, W);
   return x - v;
+}
+template <int W>
+__device__ __forceinline__ double group_sum(double v)
+{
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, W);
+  return v;
+}
+template <int W, class I>
+__device__ __forceinline__ I group_sum_i(I v)
+{
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, W);
+  return v;
 }
 
 struct CntSum {
@@ -215,20 +232,21 @@ __global__ void k_trav_init(TravArgs a)
   }
 }
 
-// One warp, one frontier query node: kernel bounds of every live pair, the lower
-// bound G^l, and the prune / summarise / base / expand decision per pair.
-template <int DT>
+// A group of W lanes, one frontier query node: kernel bounds of every live pair, the
+// lower bound G^l, and the prune / summarise / base / expand decision per pair.  The
+// whole warp calls it (valid = false: a group without an entry this round).
+template <int DT, int W>
 __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st, int cur, int e,
-                                               int lane)
+                                               int lane, bool valid)
 {
   const int* fr = a.fr[cur];
   const int D = DT ? DT : a.D;
-  const int key = a.fq[cur][e];
+  const int key = valid ? a.fq[cur][e] : 0;
   const int slot = key / st.K;
   const int Q = key - slot * st.K;
   const double h = st.h[slot], scale = st.scale[slot], eps = st.eps, ntot = st.ntot;
-  const int off = a.foff[cur][e], len = a.flen[cur][e];
-  const double fb = a.fbase[cur][e];
+  const int off = valid ? a.foff[cur][e] : 0, len = valid ? a.flen[cur][e] : 0;
+  const double fb = valid ? a.fbase[cur][e] : 0.0;
   const double* qlo = a.Q.lo + (size_t)Q * D;
   const double* qhi = a.Q.hi + (size_t)Q * D;
   const bool qleaf = a.Q.left[Q] < 0;
@@ -236,7 +254,7 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
   const double sq = a.Q.side[Q];
   // pass 1: kernel bounds and the lower-bound mass of every live pair
   double part = 0.0;
-  for (int j = lane; j < len; j += 32) {
+  for (int j = lane; j < len; j += W) {
     const int R = fr[off + j];
     double dl, du;
     box_bounds<DT>(qlo, qhi, a.R.lo + (size_t)R * D, a.R.hi + (size_t)R * D, D, dl, du);
@@ -246,12 +264,12 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
     a.pkmin[off + j] = kmin;
     part += (double)a.R.count[R] * kmin;
   }
-  const double glo = fb + warp_sum(part);
+  const double glo = fb + group_sum<W>(part);
   // pass 2: decisions
   double fd_dlo = 0.0, fd_const = 0.0, ret = 0.0;
   int nF = 0, nDT = 0, nT = 0, nB = 0, nFD = 0, slots = 0;
   unsigned long long kev = 0;
-  for (int j = lane; j < len; j += 32) {
+  for (int j = lane; j < len; j += W) {
     const int R = fr[off + j];
     const double kmax = a.pkmax[off + j], kmin = a.pkmin[off + j];
     const double nr = (double)a.R.count[R];
@@ -291,18 +309,17 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
     }
     a.dec[off + j] = kind | (order << 8);
   }
-  fd_dlo = warp_sum(fd_dlo);
-  fd_const = warp_sum(fd_const);
-  ret = warp_sum(ret);
-  nF = warp_sum_i(nF);
-  nDT = warp_sum_i(nDT);
-  nT = warp_sum_i(nT);
-  nB = warp_sum_i(nB);
-  nFD = warp_sum_i(nFD);
-  slots = warp_sum_i(slots);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) kev += __shfl_xor_sync(0xffffffffu, kev, o);
-  if (lane == 0) {
+  fd_dlo = group_sum<W>(fd_dlo);
+  fd_const = group_sum<W>(fd_const);
+  ret = group_sum<W>(ret);
+  nF = group_sum_i<W>(nF);
+  nDT = group_sum_i<W>(nDT);
+  nT = group_sum_i<W>(nT);
+  nB = group_sum_i<W>(nB);
+  nFD = group_sum_i<W>(nFD);
+  slots = group_sum_i<W>(slots);
+  kev = group_sum_i<W>(kev);
+  if (lane == 0 && valid) {
     const int ne = slots > 0 ? (qleaf ? 1 : 2) : 0;
     a.cnt[e] = Cnt{ ne, ne * slots, nF, nDT, nT, nB, nFD };
     a.childlen[e] = slots;
@@ -330,7 +347,7 @@ __global__ void __launch_bounds__(kBlock) k_classify(TravArgs a)
   const int lane = threadIdx.x & 31;
   const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int e = w0; e < m; e += nw) classify_entry<DT>(a, st, cur, e, lane);
+  for (int e = w0; e < m; e += nw) classify_entry<DT, 32>(a, st, cur, e, lane, true);
 }
 
 // Device-side exclusive scan of the per-entry counts (graph / host-loop paths):
@@ -391,21 +408,25 @@ __global__ void __launch_bounds__(256) k_scan_local(TravArgs a)
   }
 }
 
-// One warp, one frontier query node: its part of the next frontier and its work
-// items, at the offsets `o` (exclusive scan of the level's counts).
+// A group of W lanes, one frontier query node: its part of the next frontier and its
+// work items, at the offsets `o` (exclusive scan of the level's counts).  The whole
+// warp calls it (valid = false: no entry for this group).
+template <int W>
 __device__ __forceinline__ void emit_entry(const TravArgs& a, int K, int cur, int gF, int gDT,
-                                           int gB, int e, const Cnt& o, int lane)
+                                           int gB, int e, const Cnt& o, int lane, bool valid)
 {
   const int nxt = cur ^ 1;
   const int* fr = a.fr[cur];
   int* nr = a.fr[nxt];
-  const Cnt c = a.cnt[e];
-  const int key = a.fq[cur][e];
+  const Cnt c = valid ? a.cnt[e] : Cnt{};
+  const int key = valid ? a.fq[cur][e] : 0;
   const int slot = key / K;
   const int Q = key - slot * K;
-  const int off = a.foff[cur][e], len = a.flen[cur][e];
+  const int off = valid ? a.foff[cur][e] : 0, len = valid ? a.flen[cur][e] : 0;
   const bool qleaf = a.Q.left[Q] < 0;
-  const int cl = a.childlen[e];
+  const int cl = valid ? a.childlen[e] : 0;
+  // every group of the warp runs the same number of rounds (shuffles inside)
+  const int rounds = W == 32 ? len : __reduce_max_sync(0xffffffffu, (unsigned)len);
   if (lane == 0 && c.e) {
     const double nb = a.newbase[e];
     if (qleaf) {
@@ -424,9 +445,10 @@ __device__ __forceinline__ void emit_entry(const TravArgs& a, int K, int cur, in
       a.flen[nxt][o.e + 1] = cl;
     }
   }
-  const int rF = a.cntF[key], rDT = a.cntDT[key], rB = a.cntB[key];
+  const int rF = valid ? a.cntF[key] : 0, rDT = valid ? a.cntDT[key] : 0,
+            rB = valid ? a.cntB[key] : 0;
   int runX = 0, runF = 0, runDT = 0, runB = 0;
-  for (int j0 = 0; j0 < len; j0 += 32) {
+  for (int j0 = 0; j0 < rounds; j0 += W) {
     const int j = j0 + lane;
     int kind = kE, order = 0, R = 0;
     if (j < len) {
@@ -437,7 +459,7 @@ __device__ __forceinline__ void emit_entry(const TravArgs& a, int K, int cur, in
     }
     const bool rleaf = (j < len) ? a.R.left[R] < 0 : true;
     int tot;
-    const int px = warp_excl_scan(kind == kX ? (rleaf ? 1 : 2) : 0, lane, tot);
+    const int px = warp_excl_scan<W>(kind == kX ? (rleaf ? 1 : 2) : 0, lane, tot);
     if (kind == kX) {
       const int dst = o.p + runX + px;
       if (rleaf) {
@@ -454,18 +476,18 @@ __device__ __forceinline__ void emit_entry(const TravArgs& a, int K, int cur, in
     }
     runX += tot;
     int t2;
-    const int pf = warp_excl_scan(kind == kF, lane, t2);
+    const int pf = warp_excl_scan<W>(kind == kF, lane, t2);
     if (kind == kF) a.itF[gF + o.f + runF + pf] = Item{ key, R, order | (kF << 8), rF + runF + pf };
     runF += t2;
-    const int pd = warp_excl_scan(kind == kD || kind == kT, lane, t2);
+    const int pd = warp_excl_scan<W>(kind == kD || kind == kT, lane, t2);
     if (kind == kD || kind == kT)
       a.itDT[gDT + o.dt + runDT + pd] = Item{ key, R, order | (kind << 8), rDT + runDT + pd };
     runDT += t2;
-    const int pb = warp_excl_scan(kind == kB, lane, t2);
+    const int pb = warp_excl_scan<W>(kind == kB, lane, t2);
     if (kind == kB) a.itB[gB + o.b + runB + pb] = Item{ key, R, (kB << 8) | order, rB + runB + pb };
     runB += t2;
   }
-  if (lane == 0) {
+  if (lane == 0 && valid) {
     a.cntF[key] = rF + runF;
     a.cntDT[key] = rDT + runDT;
     a.cntB[key] = rB + runB;
@@ -481,7 +503,7 @@ __global__ void __launch_bounds__(kBlock) k_emit(TravArgs a)
   const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int e = w0; e < m; e += nw)
-    emit_entry(a, st.K, cur, st.nF, st.nDT, st.nB, e, a.cntoff[e], lane);
+    emit_entry<32>(a, st.K, cur, st.nF, st.nDT, st.nB, e, a.cntoff[e], lane, true);
 }
 
 // Close a level (graph / host-loop paths): fold its totals into the state, flip the
@@ -583,7 +605,37 @@ __device__ Cnt lookback(const TravArgs& a, int b, const Cnt& agg, unsigned long 
 // the next frontier visible.  The last CTA publishes the level totals and the
 // capacity verdict.  Every CTA advances an identical private copy of (cur, m, item
 // offsets); CTA 0 writes the state back at the end.
-constexpr int kPBlock = 512;
+#ifndef KPBLOCK
+#define KPBLOCK 1024
+#endif
+constexpr int kPBlock = KPBLOCK;  // one CTA per SM: 32 warps to hide classify latency
+
+// A CTA's contiguous entry range [b0, b1), W lanes per entry.  All lanes of a warp
+// run the same number of rounds (the group collectives need the full warp).
+template <int DT, int W>
+__device__ __forceinline__ void classify_range(const TravArgs& a, TravState& st, int cur, int b0,
+                                               int b1)
+{
+  const int g = threadIdx.x / W, lane = threadIdx.x % W;
+  constexpr int ng = kPBlock / W;
+  for (int base = b0; base < b1; base += ng) {
+    const int e = base + g;
+    if (__any_sync(0xffffffffu, e < b1)) classify_entry<DT, W>(a, st, cur, e, lane, e < b1);
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void emit_range(const TravArgs& a, int K, int cur, int gF, int gDT, int gB,
+                                           int b0, int b1)
+{
+  const int g = threadIdx.x / W, lane = threadIdx.x % W;
+  constexpr int ng = kPBlock / W;
+  for (int base = b0; base < b1; base += ng) {
+    const int e = base + g;
+    if (__any_sync(0xffffffffu, e < b1))
+      emit_entry<W>(a, K, cur, gF, gDT, gB, e, e < b1 ? a.cntoff[e] : Cnt{}, lane, e < b1);
+  }
+}
 template <int DT>
 __global__ void __launch_bounds__(kPBlock) k_traverse(TravArgs a)
 {
@@ -597,7 +649,6 @@ __global__ void __launch_bounds__(kPBlock) k_traverse(TravArgs a)
   } tmp;
   __shared__ Cnt s_agg, s_excl;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  constexpr int kWarps = kPBlock / 32;
   const int G = gridDim.x;
   const int K = st.K;
   const unsigned long long epoch = (unsigned long long)st.epoch << 32;
@@ -610,7 +661,9 @@ __global__ void __launch_bounds__(kPBlock) k_traverse(TravArgs a)
     }
     const int per = (m + G - 1) / G;
     const int b0 = min(m, blockIdx.x * per), b1 = min(m, b0 + per);
-    for (int e = b0 + wib; e < b1; e += kWarps) classify_entry<DT>(a, st, cur, e, lane);
+    // one warp per entry (narrower lane groups for short lists were measured: no gain,
+    // more register spills -- classify is latency- not lane-bound)
+    classify_range<DT, 32>(a, st, cur, b0, b1);
     __syncthreads();
     Cnt acc{};
     for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) acc = CntSum()(acc, a.cnt[i]);
@@ -650,8 +703,7 @@ __global__ void __launch_bounds__(kPBlock) k_traverse(TravArgs a)
         carry = CntSum()(carry, ag);
       }
       __syncthreads();
-      for (int e = b0 + wib; e < b1; e += kWarps)
-        emit_entry(a, K, cur, gF, gDT, gB, e, a.cntoff[e], lane);
+      emit_range<32>(a, K, cur, gF, gDT, gB, b0, b1);
     }
     grid.sync();
     if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && levels < 512) {
