@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <climits>
 
 namespace dfgtb {
 using namespace detail;
@@ -276,6 +277,7 @@ __global__ void k_l2l(DevSeries g, TreeView Q, int K, int nb, const int* nodes_a
 // kTaskItems reference leaves, times 32-query chunks of the leaf.  One warp per task
 // writes per-query partial sums; k_finalize adds a query's partials in task order.
 constexpr int kTaskItems = 8;
+static_assert(kTaskItems <= 32 && (kTaskItems & (kTaskItems - 1)) == 0, "one item per lane");
 struct BTask {
   int key, item0, item1, q0;
 };
@@ -309,52 +311,54 @@ __global__ void k_task_fill(const int* leaves, int nleaves, int nb, int K, const
       tasks[t++] = BTask{ key, o + k * kTaskItems, o + min(c, (k + 1) * kTaskItems), q0 };
 }
 
-// exp(-y), 0 <= y <= 708.39, to ~1 ulp: Cody-Waite reduction y*log2(e) = n + f,
-// r = -y - n ln2 (|r| <= ln2/2), degree-12 Taylor polynomial (truncation
-// <= 1.7e-16 relative), 2^n spliced into the exponent field.  The coefficients sit in
-// the constant bank so every DFMA reads its constant operand from c[] (libdevice exp
-// re-materialises its 64-bit constants with integer moves inside hot loops).  Same
-// accuracy class as libdevice exp: no reduced precision is charged to eps.
-__constant__ double c_expk[15];
-
-__device__ __forceinline__ double exp_negy(double y)
-{
-  const double magic = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
-  const double t = fma(-y, c_expk[0], magic);
-  const double n = t - magic;
-  double r = fma(n, -c_expk[1], -y);
-  r = fma(n, -c_expk[2], r);
-  double p = c_expk[3];
-#pragma unroll
-  for (int k = 4; k < 15; ++k) p = fma(p, r, c_expk[k]);
-  p = fma(p, r, 1.0);
-  const int ni = __double2loint(t);  // n in the low word of t
-  return __hiloint2double(__double2hiint(p) + (ni << 20), __double2loint(p));
-}
-
 // Table-driven exp(-y), 0 <= y <= 708: -y = (64 m + j) ln2/64 + r, |r| <= ln2/128,
 // exp(-y) = 2^m * 2^(j/64) * e^r with 2^(j/64) from a 64-entry shared-memory table and
-// e^r by a degree-5 Taylor polynomial (truncation r^6/6! < 3.5e-17 relative).  11 FP64
-// instructions instead of 16, still ~1.5 ulp: no reduced precision, nothing charged
-// to eps.  c_exp64 = {64 log2 e, ln2_hi/64, ln2_lo/64, 1/5!, 1/4!, 1/3!, 1/2!}.
-__constant__ double c_exp64[7];
+// e^r by a degree-5 Taylor polynomial (truncation r^6/6! < 3.5e-17 relative).  The
+// reduction uses ONE rounded constant C = RN(ln2/64) in a single FMA: its error,
+// |n| |C - ln2/64| <= y * 1.1e-16 absolute in r, is of the same size as the rounding
+// already present in y = |q'-r'|^2 itself (y * 2-3 ulp), so the pair's relative error
+// stays y * O(1e-16) as with libdevice exp of the same y: nothing is charged to eps.
+// 10 FP64 instructions (libdevice exp: ~16 plus integer work).
+// c_exp64 = {64 log2 e, RN(ln2/64), 1/5!, 1/4!, 1/3!, 1/2!}.
+__constant__ double c_exp64[6];
 __constant__ double c_exp2tab[64];  // 2^(j/64)
 
-__device__ __forceinline__ double exp_negy_t(double y, const double* tab)
+// The table is addressed by its shared-window address `tabs` (512-byte aligned): the
+// entry address is one shift and one AND-OR, the exponent increment (m << 20, taken
+// from the low word k of t as (k & ~63) << 14) one AND and one multiply-add.
+__device__ __forceinline__ double exp_negy_s(double y, unsigned tabs)
 {
-  const double magic = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
+  const double magic = 6755399441055744.0;
   const double t = fma(-y, c_exp64[0], magic);
-  const double n = t - magic;  // = 64 m + j
-  double r = fma(n, -c_exp64[1], -y);
-  r = fma(n, -c_exp64[2], r);
-  double p = fma(c_exp64[3], r, c_exp64[4]);
+  const double n = t - magic;
+  const double r = fma(n, -c_exp64[1], -y);
+  double p = fma(c_exp64[2], r, c_exp64[3]);
+  p = fma(p, r, c_exp64[4]);
   p = fma(p, r, c_exp64[5]);
-  p = fma(p, r, c_exp64[6]);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
   const int k = __double2loint(t);
-  const double v = p * tab[k & 63];
-  return __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));
+  double c;
+  asm volatile("{\n\t.reg .b32 a;\n\tshl.b32 a, %1, 3;\n\tlop3.b32 a, a, 504, %2, 0xea;\n\t"
+               "ld.shared.f64 %0, [a];\n\t}"
+               : "=d"(c) : "r"(k), "r"(tabs));
+  const double v = p * c;
+  int hi;
+  asm("{\n\t.reg .b32 m;\n\tand.b32 m, %1, -64;\n\tmad.lo.s32 %0, m, 16384, %2;\n\t}"
+      : "=r"(hi) : "r"(k), "r"(__double2hiint(v)));
+  return __hiloint2double(hi, __double2loint(v));
+}
+
+// exp(-y) for any y >= 0, branch-free, with the underflow range: beyond y = 708 the
+// argument is shifted by 64 ln2 into the fast range and the result scaled by 2^-64
+// (one rounding into the subnormals, as libm's exp rounds there); y > 752 gives
+// exp(-708) 2^-64, which rounds to 0 like exp(-y) itself.
+__device__ __forceinline__ double exp_negy_c(double y, unsigned tabs)
+{
+  const bool big = y > 708.0;
+  const double yy = big ? y - 44.3614195558365 : y;  // 64 ln 2
+  const double e = exp_negy_s(fmin(yy, 708.0), tabs);
+  return big ? e * 0x1p-64 : e;
 }
 
 // Scaled, centred, padded coordinates for the base case, per slot:
@@ -389,6 +393,30 @@ struct PtLoad {
       }
     }
   }
+  // point j of src -> point j2 of dst (16-byte vectors)
+  __device__ __forceinline__ static void copy2(const double* src, int j, double* dst, int j2)
+  {
+    if constexpr (DT == 1) {
+      dst[j2] = src[j];
+    } else {
+      const double2* s2 = reinterpret_cast<const double2*>(src + (size_t)j * DP);
+      double2* d2 = reinterpret_cast<double2*>(dst + (size_t)j2 * DP);
+#pragma unroll
+      for (int k = 0; k < DP / 2; ++k) d2[k] = s2[k];
+    }
+  }
+  // point j of src -> point j of dst (16-byte vectors)
+  __device__ __forceinline__ static void copy(const double* src, int j, double* dst)
+  {
+    if constexpr (DT == 1) {
+      dst[j] = src[j];
+    } else {
+      const double2* s2 = reinterpret_cast<const double2*>(src + (size_t)j * DP);
+      double2* d2 = reinterpret_cast<double2*>(dst + (size_t)j * DP);
+#pragma unroll
+      for (int k = 0; k < DP / 2; ++k) d2[k] = s2[k];
+    }
+  }
 };
 
 // Compact reference-leaf records for the base case, in sorted item order:
@@ -404,100 +432,186 @@ __global__ void k_base_records(const Item* items, int n, TreeView R, int2* rec)
 }
 
 // K10: exhaustive base case (Traversal::base_case, engine.cpp:239-269).  One warp per
-// task = (slot, query leaf, 32-query chunk, run of <= kTaskItems reference leaves).
-// A chunk of qc queries gets k = 32/qc lanes per query (lane -> query lane % qc,
-// reference points j = lane/qc, +k, ...), combined by shuffles at the end in a fixed
-// order, so small leaves still fill the warp.  Reference points arrive as warp-
-// broadcast 16-byte loads of scaled, centred coordinates (|q'-r'|^2 is the exponent
-// directly), four pairs in flight per lane, the next leaf record prefetched.  Leaves
-// whose box bound proves y <= 708 run the branch-free fast exp; others fall back to
-// libdevice exp beyond the fast range (exact underflow behaviour).
+// task = (slot, query leaf, 32-query chunk, run of <= kTaskItems reference leaves),
+// tasks handed out by an atomic counter (results are written per task, so the order
+// of execution does not change a bit).  The task's reference points are staged, as
+// one contiguous stream, into the warp's shared-memory tile; LANES RUN OVER REFERENCE
+// POINTS and each lane holds a group of G queries in registers, so all 32 lanes are
+// busy whatever the leaf sizes (only the stream's last 32-block is partial) and each
+// reference point is read once per G pairs.  The G partial sums are combined across
+// the warp by a transpose-reduction (G values in log2(32) exchange steps) in a fixed
+// order: bit-reproducible.  Chunks whose leaves the traversal proved to have y <= 708
+// for every pair run the branch-free table exp; others the careful path (libdevice
+// exp beyond the fast range: exact underflow behaviour).
 template <int DT>
-__global__ void __launch_bounds__(kBlock, 6) k_base_case(TreeView Q, int K, const BTask* tasks,
-                                                      int ntasks, const int2* rec,
-                                                      const double* xq, const double* xr, int nq,
-                                                      int nr, double* part)
+struct BaseGeo {
+  static constexpr int DP = PtLoad<DT>::DP;
+#ifndef DFGTB_BASE_G
+#define DFGTB_BASE_G 8
+#endif
+  static constexpr int G = DT <= 2 ? DFGTB_BASE_G : 4;            // queries per lane
+  static constexpr int RMAX = DT == 1 ? 512 : DT == 2 ? 256 : DT <= 4 ? 128 : 64;  // stream tile
+  static constexpr int WARPS = 4;                                 // per CTA
+  static constexpr int WORDS = RMAX * DP + 32 * DP + 32;          // refs | queries | sums
+};
+
+template <int DT, int GG, bool FAST>
+__device__ __forceinline__ void base_group(const double* rs, int n, const double* qs, double* qsum,
+                                           const double* tab, int lane)
 {
-  constexpr int D = DT;
-  constexpr int DP = PtLoad<DT>::DP;
-  __shared__ double tab[64];
+  constexpr int D = DT, DP = BaseGeo<DT>::DP;
+  constexpr int LG = GG == 8 ? 3 : GG == 4 ? 2 : GG == 2 ? 1 : 0;
+  double qv[GG][D];
+#pragma unroll
+  for (int i = 0; i < GG; ++i)
+#pragma unroll
+    for (int d = 0; d < D; ++d) qv[i][d] = qs[i * DP + d];
+  double acc[GG];
+#pragma unroll
+  for (int i = 0; i < GG; ++i) acc[i] = 0.0;
+  const unsigned tabs = (unsigned)__cvta_generic_to_shared(tab);
+  auto body = [&](int j) {
+    double r[DP];
+    PtLoad<DT>::load(rs, j, r);
+#pragma unroll
+    for (int i = 0; i < GG; ++i) {
+      double y = 0.0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const double t = qv[i][d] - r[d];
+        y = fma(t, t, y);
+      }
+      if constexpr (FAST) acc[i] += exp_negy_s(y, tabs);
+      else acc[i] += exp_negy_c(y, tabs);
+    }
+  };
+  // one copy of the body (instruction-cache footprint): lanes past the end of the
+  // stream idle in the last 32-block only
+  const int nceil = (n + 31) & ~31;
+  for (int j = lane; j < nceil; j += 32)
+    if (j < n) body(j);
+  // transpose-reduction: split steps on lane bits 4, 3, .. (each lane keeps half of its
+  // values, adds the partner's copy of that half), then butterflies on the rest
+#pragma unroll
+  for (int s = 0; s < LG; ++s) {
+    const int off = 16 >> s;
+    const bool up = lane & off;
+    const int h = GG >> (s + 1);
+#pragma unroll
+    for (int i = 0; i < GG / 2; ++i) {
+      if (i < h) {
+        const double send = up ? acc[i] : acc[i + h];
+        const double keep = up ? acc[i + h] : acc[i];
+        acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16 >> LG; off >= 1; off >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
+  if ((lane & ((32 >> LG) - 1)) == 0) qsum[lane >> (5 - LG)] += acc[0];
+}
+
+// Queries in groups of G, the remainder in groups of 4, 2, 1.  Each group size is one
+// out-of-line copy, to keep the kernel's hot code small.
+template <int DT, int GG, bool FAST>
+__device__ __noinline__ void base_group_call(const double* rs, int n, const double* qs, double* qsum,
+                                             const double* tab, int lane)
+{
+  base_group<DT, GG, FAST>(rs, n, qs, qsum, tab, lane);
+}
+
+template <int DT, bool FAST>
+__device__ __forceinline__ void base_groups(const double* rs, int n, const double* qs, double* qsum,
+                                            int qc, const double* tab, int lane)
+{
+  constexpr int DP = BaseGeo<DT>::DP, G = BaseGeo<DT>::G;
+  int g0 = 0;
+  for (; g0 + G <= qc; g0 += G) base_group_call<DT, G, FAST>(rs, n, qs + g0 * DP, qsum + g0, tab, lane);
+  if constexpr (G >= 8) {
+    if (qc - g0 >= 4) {
+      base_group_call<DT, 4, FAST>(rs, n, qs + g0 * DP, qsum + g0, tab, lane);
+      g0 += 4;
+    }
+  }
+  if (qc - g0 >= 2) {
+    base_group_call<DT, 2, FAST>(rs, n, qs + g0 * DP, qsum + g0, tab, lane);
+    g0 += 2;
+  }
+  if (qc - g0 >= 1) base_group_call<DT, 1, FAST>(rs, n, qs + g0 * DP, qsum + g0, tab, lane);
+}
+
+#ifndef DFGTB_BASE_MINB
+#define DFGTB_BASE_MINB 4  // CTAs per SM: 125 registers, chains interleaved by ptxas
+#endif
+template <int DT>
+__global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
+  k_base_case(TreeView Q, int K, const BTask* tasks, int ntasks, const int2* rec, const double* xq,
+              const double* xr, int nq, int nr, double* part, int* next)
+{
+  using Geo = BaseGeo<DT>;
+  constexpr int DP = Geo::DP, RMAX = Geo::RMAX;
+  __shared__ __align__(512) double tab[64];
+  __shared__ __align__(16) double sm[Geo::WARPS][Geo::WORDS];
   if (threadIdx.x < 64) tab[threadIdx.x] = c_exp2tab[threadIdx.x];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int w = w0; w < ntasks; w += nw) {
+  double* rs = sm[threadIdx.x >> 5];
+  double* qs = rs + RMAX * DP;
+  double* qsum = qs + 32 * DP;
+  int w = 0;
+  if (lane == 0) w = atomicAdd(next, 1);
+  w = __shfl_sync(0xffffffffu, w, 0);
+  while (w < ntasks) {
     const BTask t = tasks[w];
+    int wn = 0;
+    if (lane == 0) wn = atomicAdd(next, 1);  // the next task, fetched early
     const int slot = t.key / K, leaf = t.key - slot * K;
-    const double* xqs = xq + (size_t)slot * nq * DP;
-    const double* xrs = xr + (size_t)slot * nr * DP;
+    // all records of the task at once: lane k holds item k (kTaskItems <= 32)
+    const int nit = t.item1 - t.item0;
+    const int2 rc = lane < nit ? rec[t.item0 + lane] : make_int2(0, 0);
     const int qc = min(32, Q.count[leaf] - t.q0);
-    const int kq = 32 / qc;  // lanes per query
-    const int qi = lane % qc, sub = lane / qc;
-    const bool act = sub < kq;
-    double q[DP];
-    PtLoad<DT>::load(xqs, Q.begin[leaf] + t.q0 + qi, q);
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-    int2 nxt = rec[t.item0];
-    for (int k = t.item0; k < t.item1; ++k) {
-      const int2 cur = nxt;
-      if (k + 1 < t.item1) nxt = rec[k + 1];
-      const double* rp = xrs + (size_t)cur.x * DP;
-      const bool fast = cur.y > 0;
-      const int rc = fast ? cur.y : -cur.y;
-      if (!act) continue;
-      int j = sub;
-      if (fast) {
-        for (; j + kq < rc; j += 2 * kq) {
-          double a[DP], b[DP];
-          PtLoad<DT>::load(rp, j, a);
-          PtLoad<DT>::load(rp, j + kq, b);
-          double ya = 0.0, yb = 0.0;
+    const int qb = Q.begin[leaf];
+    const int cnt = rc.y > 0 ? rc.y : -rc.y;
+    const bool fast = __all_sync(0xffffffffu, lane >= nit || rc.y > 0);
+    int incl = cnt;
 #pragma unroll
-          for (int d = 0; d < D; ++d) {
-            const double ta = q[d] - a[d], tb = q[d] - b[d];
-            ya = fma(ta, ta, ya);
-            yb = fma(tb, tb, yb);
-          }
-          acc0 += exp_negy_t(ya, tab);  // two chains: ptxas interleaves them
-          acc1 += exp_negy_t(yb, tab);
-        }
-        for (; j < rc; j += kq) {
-          double a[DP];
-          PtLoad<DT>::load(rp, j, a);
-          double ya = 0.0;
+    for (int o = 1; o < kTaskItems; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, kTaskItems - 1);
+    int sk[kTaskItems], ok[kTaskItems];  // stream start of item k, source position - start
 #pragma unroll
-          for (int d = 0; d < D; ++d) {
-            const double ta = q[d] - a[d];
-            ya = fma(ta, ta, ya);
-          }
-          acc0 += exp_negy_t(ya, tab);
-        }
-      } else {
-        for (; j < rc; j += kq) {
-          double a[DP];
-          PtLoad<DT>::load(rp, j, a);
-          double ya = 0.0;
+    for (int k = 0; k < kTaskItems; ++k) {
+      sk[k] = k < nit ? __shfl_sync(0xffffffffu, incl - cnt, k) : INT_MAX;
+      ok[k] = __shfl_sync(0xffffffffu, rc.x - (incl - cnt), k);
+    }
+    const double* qsrc = xq + ((size_t)slot * nq + qb + t.q0) * DP;
+    if (lane < qc) PtLoad<DT>::copy(qsrc, lane, qs);
+    qsum[lane] = 0.0;
+    const double* xrs = xr + (size_t)slot * nr * DP;
+    for (int c0 = 0; c0 < total; c0 += RMAX) {
+      // stage stream positions [c0, c0 + n): every lane issues all its loads at once
+      const int n = min(RMAX, total - c0);
 #pragma unroll
-          for (int d = 0; d < D; ++d) {
-            const double ta = q[d] - a[d];
-            ya = fma(ta, ta, ya);
-          }
-          acc0 += ya <= 708.0 ? exp_negy(ya) : exp(-ya);
-        }
+      for (int i = 0; i < RMAX / 32; ++i) {
+        const int e = c0 + lane + 32 * i;
+        int off = ok[0];
+#pragma unroll
+        for (int k = 1; k < kTaskItems; ++k)
+          if (sk[k] <= e) off = ok[k];
+        if (e < c0 + n) PtLoad<DT>::copy2(xrs, off + e, rs, e - c0);
       }
+      __syncwarp();
+      if (fast) base_groups<DT, true>(rs, n, qs, qsum, qc, tab, lane);
+      else base_groups<DT, false>(rs, n, qs, qsum, qc, tab, lane);
+      __syncwarp();
     }
-    double acc = (acc0 + acc1) + (acc2 + acc3);
-    if (!act) acc = 0.0;
-    double tot = acc;
-    for (int s2 = 1; s2 < kq; ++s2) {  // lanes of the same query, fixed order
-      const double v = __shfl_sync(0xffffffffu, acc, (lane + s2 * qc) & 31);
-      tot += v;
-    }
-    if (sub == 0) part[(size_t)w * 32 + qi] = tot;
+    if (lane < qc) part[(size_t)w * 32 + lane] = qsum[lane];
+    __syncwarp();
+    w = __shfl_sync(0xffffffffu, wn, 0);
   }
 }
-
 
 // Generic dimension (D > 5): scalar loads of the scaled coordinates, libdevice exp.
 __global__ void __launch_bounds__(kBlock) k_base_case_any(TreeView Q, TreeView R, int K, int D,
@@ -806,12 +920,31 @@ __global__ void k_dfma_peak(double* out, int iters)
 
 int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }
 
+// Persistent grid: as many CTAs as fit on the GPU (or fewer for small task lists).
+template <int DT>
+void launch_base_t(int ntasks, cudaStream_t s, TreeView Q, int K, const BTask* tasks, const int2* rec,
+                   const double* xq, const double* xr, int nq, int nr, double* part, int* next)
+{
+  static int per_sm = 0, nsm = 0;
+  constexpr int threads = BaseGeo<DT>::WARPS * 32;
+  if (!per_sm) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_base_case<DT>, threads, 0));
+    per_sm = std::max(per_sm, 1);
+  }
+  const int grid = (int)std::min<long long>((long long)nsm * per_sm,
+                                            (ntasks + BaseGeo<DT>::WARPS - 1) / BaseGeo<DT>::WARPS);
+  CK(cudaMemsetAsync(next, 0, sizeof(int), s));
+  k_base_case<DT><<<grid, threads, 0, s>>>(Q, K, tasks, ntasks, rec, xq, xr, nq, nr, part, next);
+}
+
 void launch_base(int D, int grid, cudaStream_t s, TreeView Q, TreeView R, int K,
                  const BTask* tasks, int ntasks, const Item* items, const int2* rec,
-                 const double* xq, const double* xr, int nq, int nr, double* part)
+                 const double* xq, const double* xr, int nq, int nr, double* part, int* next)
 {
-#define BASE(DD) \
-  k_base_case<DD><<<grid, kBlock, 0, s>>>(Q, K, tasks, ntasks, rec, xq, xr, nq, nr, part)
+#define BASE(DD) launch_base_t<DD>(ntasks, s, Q, K, tasks, rec, xq, xr, nq, nr, part, next)
   switch (D) {
   case 1: BASE(1); break;
   case 2: BASE(2); break;
@@ -829,20 +962,9 @@ void launch_base(int D, int grid, cudaStream_t s, TreeView Q, TreeView R, int K,
 }  // namespace
 
 void init_exp_constants(cudaStream_t s)
-{  // log2(e), Cody-Waite ln2 split, then 1/12! ... 1/1!
-  double k[15];
-  k[0] = 1.4426950408889634;
-  k[1] = 6.93147180369123816490e-01;
-  k[2] = 1.90821492927058770002e-10;
-  double f = 1.0;
-  for (int i = 1; i <= 12; ++i) {
-    f *= i;
-    k[3 + (12 - i)] = 1.0 / f;
-  }
-  CK(cudaMemcpyToSymbolAsync(c_expk, k, sizeof(k), 0, cudaMemcpyHostToDevice, s));
-  // table-driven variant: 64 log2(e), Cody-Waite ln2/64 split, 1/5! .. 1/2!
-  double k64[7] = { 64.0 * 1.4426950408889634, 6.93147180369123816490e-01 / 64.0,
-                    1.90821492927058770002e-10 / 64.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5 };
+{  // base-case exp(-y): 64 log2(e), ln2/64, 1/5! .. 1/2!, table 2^(j/64)
+  double k64[6] = { 64.0 * 1.4426950408889634, 0.6931471805599453 / 64.0,  // RN(ln 2) / 2^6
+                    1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5 };
   double tab[64];
   for (int j = 0; j < 64; ++j) tab[j] = std::exp2((double)j / 64.0);  // correctly rounded in glibc
   CK(cudaMemcpyToSymbolAsync(c_exp64, k64, sizeof(k64), 0, cudaMemcpyHostToDevice, s));
@@ -1046,9 +1168,11 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
     }
   }
   CK(cudaEventRecord(ev_[9], s));
+  bnext_.reserve(1);
   if (ntasks)
     launch_base(D_, grid_warps(ntasks), s, Q, R, K, reinterpret_cast<const BTask*>(tasks_.p), ntasks,
-                sB_.p, reinterpret_cast<const int2*>(brec_.p), xq, xr, qt.n, rt_.n, bpart_.p);
+                sB_.p, reinterpret_cast<const int2*>(brec_.p), xq, xr, qt.n, rt_.n, bpart_.p,
+                bnext_.p);
   CK(cudaEventRecord(ev_[6], s));
   s_ff_.reserve((size_t)qt.n * nb);
   if (nF_) {

@@ -228,12 +228,27 @@ def test_l2l_chain_matches_direct_ancestor_evaluation(dfgtb, orc):
 
 
 def test_fast_exp_accuracy(dfgtb, orc):
-    """The base case's exp(-y) (Cody-Waite + degree-12 Taylor, constant-bank
-    coefficients) vs libm: eps = 0 base-case-only sums agree with the exact oracle
-    to summation-order rounding, including pairs deep in the underflow range."""
+    """The base case's table-driven exp(-y) vs libm: eps = 0 base-case-only sums agree
+    with the exact oracle to summation-order rounding, including pairs deep in the
+    underflow range (careful path)."""
     g = np.random.default_rng(3)
     x = g.random((600, 2)) * np.array([1.0, 0.01])
     for h in (0.002, 0.01, 0.05, 0.3):
         approx = dfgtb.dfd_kde(x, x, h, 0.0, 16)
         exact = orc.naive_kde(x, x, h)
         assert np.max(np.abs(approx - exact) / exact) <= 1e-13
+
+
+@pytest.mark.parametrize("d,leaf", [(1, 700), (2, 16), (2, 300), (3, 7), (3, 200), (4, 50), (5, 90)])
+def test_base_case_tiles_exact(dfgtb, orc, d, leaf):
+    """eps = 0: every pair goes through the base case.  Leaves larger than the
+    shared-memory stream tile (chunked staging), every query-group remainder, and
+    Q != R, all to summation-order rounding of the exact sums."""
+    g = np.random.default_rng(10 + d)
+    r = g.random((900, d))
+    q = g.random((333, d))
+    for h in (0.03, 0.2, 2.0):
+        for qq in (r, q):
+            approx = dfgtb.dfd_kde(qq, r, h, 0.0, leaf)
+            exact = orc.naive_kde(qq, r, h)
+            assert np.max(np.abs(approx - exact) / exact) <= 1e-13
