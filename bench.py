@@ -117,44 +117,62 @@ def config_block(w, world):
 
 # -------------------------------------------------------------------------- ours
 class Clocks:
+    """SM clock and clock-event reasons sampled DURING the timed region: an NVML
+    polling thread (~1 ms period; the timed region is only milliseconds long, too
+    short for `nvidia-smi -lms`).  NVML calls release the GIL (ctypes)."""
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
+
     def __init__(self, idx):
-        self.p = None
         self.idx = idx
+        self.rows = []
+        self.err = None
+
+    def _run(self):
+        import pynvml
+        try:
+            while not self.stop:
+                sm = pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((sm, rs))
+                time.sleep(0.001)
+        except Exception as e:  # pragma: no cover - reported in the line
+            self.err = repr(e)
 
     def __enter__(self):
+        import threading
         try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=clocks.sm,clocks.max.sm,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.p = None
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            phys = int(vis.split(",")[self.idx]) if vis and vis.split(",")[0].isdigit() else self.idx
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:
+            self.err = repr(e)
+            self.th = None
+            return self
+        self.stop = False
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+        while not self.rows and self.err is None and self.th.is_alive():  # first sample before timing
+            time.sleep(0.0005)
+        self.rows.clear()
         return self
 
     def __exit__(self, *a):
-        self.out = ""
-        if self.p:
-            self.p.terminate()
-            try:
-                self.out, _ = self.p.communicate(timeout=5)
-            except Exception:
-                self.out = ""
+        if self.th is not None:
+            self.stop = True
+            self.th.join(timeout=2)
 
     def summary(self):
-        rows = []
-        for line in (self.out or "").strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) >= 6 and f[0].isdigit():
-                rows.append(f)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(int(r[0]) for r in rows)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
-                "samples": len(rows)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "error": self.err}
+        sm = sorted(r[0] for r in self.rows)
+        reasons = sorted({n for _, m in self.rows for n, bit in self.REASONS if m & bit})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(self.max_mhz), "reasons": reasons,
+                "samples": len(self.rows), "sm_mhz_min": sm[0], "sampler": "nvml, ~1 ms period"}
 
 
 def run_ours(a, rank, world, local_rank):

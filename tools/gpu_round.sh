@@ -1,0 +1,19 @@
+#!/bin/bash
+# One GPU verification pass: gpu tests, bench line, launch list, base-case ncu capture.
+#   tools/gpu_round.sh TAG [skip_tests]
+TAG=${1:-r01}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${TAG}_gpu.txt 2>&1
+if [ "$2" != "skip_tests" ]; then
+  timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest.log 2>&1
+  echo "pytest exit $?" >> gpurun_out/${TAG}_pytest.log
+  tail -3 gpurun_out/${TAG}_pytest.log
+fi
+timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
+echo "bench exit $?"; tail -c 3000 gpurun_out/${TAG}_bench.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/${TAG}_launches.csv python tools/profile_step.py > gpurun_out/${TAG}_ncu_launch.log 2>&1
+echo "launch list exit $?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_base_case -s 1 -c 1 \
+  -o gpurun_out/${TAG}_base_case -f python tools/profile_step.py > gpurun_out/${TAG}_ncu_full.log 2>&1
+echo "ncu full exit $?"
