@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdfgtb.so")
+# DFGTB_LIB selects an alternative in-tree build (A/B experiments, tools/)
+LIB_PATH = os.environ.get("DFGTB_LIB") or os.path.join(_HERE, "libdfgtb.so")
 
 OK, EINVAL, ECUDA, ENOMEM = 0, 1, 2, 3
 

@@ -108,11 +108,11 @@ private:
   DevBuf<int> lnch_, lchoff_, lchunk_, ntask_, toff_, tasks_, leaf_task_, brec_, bnext_;
   DevBuf<double> lpart_, bpart_, xq_, xr_, slotp_;
   // frontier (double buffered) and per-level scratch
-  DevBuf<int> fq_[2], foff_[2], flen_[2], fr_[2];
+  DevBuf<int> fq_[2], foff_[2], flen_[2], fr_[2], pent_[2];
   DevBuf<double> fbase_[2];
   DevBuf<double> pkmax_, pkmin_;
   DevBuf<int> dec_, childlen_;
-  DevBuf<double> newbase_;
+  DevBuf<double> newbase_, pglo_;
   DevBuf<Cnt> cnt_, cntoff_, ctsum_, ctoff_;
   DevBuf<Item> itF_, itDT_, itB_, sF_, sDT_, sB_;
   DevBuf<unsigned char> scan_tmp_;

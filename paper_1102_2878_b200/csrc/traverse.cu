@@ -149,7 +149,9 @@ struct TravArgs {
   int D, pmax, cost, series, T;
   TravState* st;
   int *fq[2], *foff[2], *flen[2], *fr[2];
+  int* pent[2];  // entry index of every frontier pair (pair-balanced persistent path)
   double* fbase[2];
+  double* glo;   // per entry lower bound G^l (persistent path)
   double *pkmax, *pkmin;
   int* dec;
   Cnt *cnt, *cntoff, *tsum, *toff;
@@ -207,7 +209,7 @@ struct CntSum {
 };
 
 // Root pairs (slot b: key b*K -> reference root) and a fresh state.
-__global__ void k_trav_init(TravArgs a)
+__global__ void k_trav_init(const __grid_constant__ TravArgs a)
 {
   TravState& st = *a.st;
   const int nb = st.nslots;
@@ -217,6 +219,7 @@ __global__ void k_trav_init(TravArgs a)
     a.flen[0][b] = 1;
     a.fbase[0][b] = 0.0;
     a.fr[0][b] = 0;
+    a.pent[0][b] = b;
     for (int k = 0; k < sNStat; ++k) st.sst[b][k] = 0;
   }
   if (threadIdx.x == 0) {
@@ -340,7 +343,7 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
 }
 
 template <int DT>
-__global__ void __launch_bounds__(kBlock) k_classify(TravArgs a)
+__global__ void __launch_bounds__(kBlock) k_classify(const __grid_constant__ TravArgs a)
 {
   TravState& st = *a.st;
   const int cur = st.cur, m = st.m[cur];
@@ -353,7 +356,7 @@ __global__ void __launch_bounds__(kBlock) k_classify(TravArgs a)
 // Device-side exclusive scan of the per-entry counts (graph / host-loop paths):
 // tile sums -> one-block scan of the tiles (+ capacity check) -> tile rescan.
 constexpr int kScanTiles = 256;
-__global__ void __launch_bounds__(256) k_scan_tiles(TravArgs a)
+__global__ void __launch_bounds__(256) k_scan_tiles(const __grid_constant__ TravArgs a)
 {
   const TravState& st = *a.st;
   const int m = st.m[st.cur];
@@ -374,7 +377,7 @@ __device__ __forceinline__ bool over_capacity(const TravState& st, const Cnt& t,
          (long long)gDT + t.dt > st.capDT || (long long)gB + t.b > st.capB;
 }
 
-__global__ void __launch_bounds__(kScanTiles) k_scan_top(TravArgs a)
+__global__ void __launch_bounds__(kScanTiles) k_scan_top(const __grid_constant__ TravArgs a)
 {
   TravState& st = *a.st;
   using BS = cub::BlockScan<Cnt, kScanTiles>;
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(kScanTiles) k_scan_top(TravArgs a)
   }
 }
 
-__global__ void __launch_bounds__(256) k_scan_local(TravArgs a)
+__global__ void __launch_bounds__(256) k_scan_local(const __grid_constant__ TravArgs a)
 {
   const TravState& st = *a.st;
   const int m = st.m[st.cur];
@@ -462,15 +465,25 @@ __device__ __forceinline__ void emit_entry(const TravArgs& a, int K, int cur, in
     const int px = warp_excl_scan<W>(kind == kX ? (rleaf ? 1 : 2) : 0, lane, tot);
     if (kind == kX) {
       const int dst = o.p + runX + px;
+      int* pe = a.pent[nxt];
       if (rleaf) {
         nr[dst] = R;
-        if (!qleaf) nr[dst + cl] = R;
-      } else {
-        nr[dst] = a.R.left[R];
-        nr[dst + 1] = a.R.right[R];
+        pe[dst] = o.e;
         if (!qleaf) {
-          nr[dst + cl] = a.R.left[R];
-          nr[dst + cl + 1] = a.R.right[R];
+          nr[dst + cl] = R;
+          pe[dst + cl] = o.e + 1;
+        }
+      } else {
+        const int rl = a.R.left[R], rr = a.R.right[R];
+        nr[dst] = rl;
+        nr[dst + 1] = rr;
+        pe[dst] = o.e;
+        pe[dst + 1] = o.e;
+        if (!qleaf) {
+          nr[dst + cl] = rl;
+          nr[dst + cl + 1] = rr;
+          pe[dst + cl] = o.e + 1;
+          pe[dst + cl + 1] = o.e + 1;
         }
       }
     }
@@ -494,7 +507,7 @@ __device__ __forceinline__ void emit_entry(const TravArgs& a, int K, int cur, in
   }
 }
 
-__global__ void __launch_bounds__(kBlock) k_emit(TravArgs a)
+__global__ void __launch_bounds__(kBlock) k_emit(const __grid_constant__ TravArgs a)
 {
   const TravState& st = *a.st;
   if (st.overflow) return;
@@ -508,7 +521,7 @@ __global__ void __launch_bounds__(kBlock) k_emit(TravArgs a)
 
 // Close a level (graph / host-loop paths): fold its totals into the state, flip the
 // frontier buffers and tell the WHILE node whether another level follows.
-__global__ void k_advance(TravArgs a, cudaGraphConditionalHandle hc, int use_cond)
+__global__ void k_advance(const __grid_constant__ TravArgs a, cudaGraphConditionalHandle hc, int use_cond)
 {
   TravState& st = *a.st;
   if (!st.overflow) {
@@ -610,20 +623,6 @@ __device__ Cnt lookback(const TravArgs& a, int b, const Cnt& agg, unsigned long 
 #endif
 constexpr int kPBlock = KPBLOCK;  // one CTA per SM: 32 warps to hide classify latency
 
-// A CTA's contiguous entry range [b0, b1), W lanes per entry.  All lanes of a warp
-// run the same number of rounds (the group collectives need the full warp).
-template <int DT, int W>
-__device__ __forceinline__ void classify_range(const TravArgs& a, TravState& st, int cur, int b0,
-                                               int b1)
-{
-  const int g = threadIdx.x / W, lane = threadIdx.x % W;
-  constexpr int ng = kPBlock / W;
-  for (int base = b0; base < b1; base += ng) {
-    const int e = base + g;
-    if (__any_sync(0xffffffffu, e < b1)) classify_entry<DT, W>(a, st, cur, e, lane, e < b1);
-  }
-}
-
 template <int W>
 __device__ __forceinline__ void emit_range(const TravArgs& a, int K, int cur, int gF, int gDT, int gB,
                                            int b0, int b1)
@@ -636,8 +635,184 @@ __device__ __forceinline__ void emit_range(const TravArgs& a, int K, int cur, in
       emit_entry<W>(a, K, cur, gF, gDT, gB, e, e < b1 ? a.cntoff[e] : Cnt{}, lane, e < b1);
   }
 }
+// ---- pair-balanced level phases of k_traverse -------------------------------------
+// CTA b owns the entries whose pair lists start in [b p / G, (b+1) p / G): a
+// contiguous entry range holding ~p/G pairs (entry sizes differ by orders of
+// magnitude, so equal ENTRY ranges left most CTAs idle at the grid barrier).  The
+// heavy per-pair work (kernel bounds, method choice) runs flat over the CTA's pairs;
+// the per-entry reductions run one warp per entry in the same lane-strided order as
+// classify_entry, so the sums (and every decision) are bit-identical to it.
+
+// Smallest entry e with foff[e] >= target (foff increasing, entries non-empty), for
+// two targets at once, by a 1024-ary search with __syncthreads_count.
+__device__ __forceinline__ void entry_bounds(const int* foff, int m, long long t0, long long t1,
+                                             int& e0, int& e1)
+{
+  int lo0 = 0, hi0 = m, lo1 = 0, hi1 = m;
+  while (lo0 < hi0 || lo1 < hi1) {
+    const int S0 = (hi0 - lo0 + kPBlock - 1) / kPBlock, S1 = (hi1 - lo1 + kPBlock - 1) / kPBlock;
+    const int c0i = lo0 + (threadIdx.x + 1) * S0 - 1, c1i = lo1 + (threadIdx.x + 1) * S1 - 1;
+    const bool p0 = lo0 < hi0 && c0i < hi0 && foff[c0i] < t0;
+    const bool p1 = lo1 < hi1 && c1i < hi1 && foff[c1i] < t1;
+    const int c0 = __syncthreads_count(p0), c1 = __syncthreads_count(p1);
+    if (lo0 < hi0) {
+      const int nlo = lo0 + c0 * S0;
+      hi0 = min(hi0, lo0 + (c0 + 1) * S0 - 1);
+      lo0 = nlo;
+    }
+    if (lo1 < hi1) {
+      const int nlo = lo1 + c1 * S1;
+      hi1 = min(hi1, lo1 + (c1 + 1) * S1 - 1);
+      lo1 = nlo;
+    }
+  }
+  e0 = lo0;
+  e1 = lo1;
+}
+
+// Pass 1, one thread per pair: kernel bounds K(d_min), K(d_max).
 template <int DT>
-__global__ void __launch_bounds__(kPBlock) k_traverse(TravArgs a)
+__device__ __forceinline__ void pairs_bounds(const TravArgs& a, int cur, int K, int P0, int P1,
+                                             const double* s_scale)
+{
+  const int D = DT ? DT : a.D;
+  for (int j = P0 + threadIdx.x; j < P1; j += kPBlock) {
+    const int key = a.fq[cur][a.pent[cur][j]];
+    const int slot = key / K, Q = key - slot * K;
+    const int R = a.fr[cur][j];
+    double dl, du;
+    box_bounds<DT>(a.Q.lo + (size_t)Q * D, a.Q.hi + (size_t)Q * D, a.R.lo + (size_t)R * D,
+                   a.R.hi + (size_t)R * D, D, dl, du);
+    const double scale = s_scale[slot];
+    a.pkmax[j] = exp(scale * dl);  // kernel at closest approach
+    a.pkmin[j] = exp(scale * du);
+  }
+}
+
+// One warp per entry: G^l = base + sum |R| K(d_max) over the entry's live pairs.
+__device__ __forceinline__ void entries_glo(const TravArgs& a, int cur, int e0, int e1)
+{
+  const int lane = threadIdx.x & 31;
+  for (int e = e0 + (threadIdx.x >> 5); e < e1; e += kPBlock / 32) {
+    const int off = a.foff[cur][e], len = a.flen[cur][e];
+    double part = 0.0;
+    for (int j = lane; j < len; j += 32)
+      part += (double)a.R.count[a.fr[cur][off + j]] * a.pkmin[off + j];
+    const double g = a.fbase[cur][e] + group_sum<32>(part);
+    if (lane == 0) a.glo[e] = g;
+  }
+}
+
+// Pass 2, one thread per pair: the prune / summarise / base / expand decision
+// (engine.cpp:137-195 with choose_best_method, truncation.cpp:130-166).
+template <int DT>
+__device__ __forceinline__ void pairs_decide(const TravArgs& a, const TravState& st, int cur, int K,
+                                             int P0, int P1, const double* s_h)
+{
+  const int D = DT ? DT : a.D;
+  const double eps = st.eps, ntot = st.ntot;
+  for (int j = P0 + threadIdx.x; j < P1; j += kPBlock) {
+    const int e = a.pent[cur][j];
+    const int key = a.fq[cur][e];
+    const int slot = key / K, Q = key - slot * K;
+    const int R = a.fr[cur][j];
+    const double kmax = a.pkmax[j], kmin = a.pkmin[j];
+    const double nr = (double)a.R.count[R];
+    const double tau = eps * nr * a.glo[e] / ntot;
+    int kind = kX, order = 0;
+    if (0.5 * nr * (kmax - kmin) <= tau) {  // kernel-difference prune, engine.cpp:137-148
+      kind = kFD;
+    } else {
+      if (a.series) {
+        dev_choose((double)a.Q.count[Q], nr, a.Q.side[Q], a.R.side[R], s_h[slot], tau, a.pmax, D,
+                   a.cost, kind, order);
+        if (kind == kE) kind = kX;
+      }
+      if (kind == kX && a.Q.left[Q] < 0 && a.R.left[R] < 0) {
+        kind = kB;
+        // every pair of this leaf pair has y = d^2/2h^2 <= 708 (K(d_max) >= e^-707.97):
+        // the base case may use its fast exp without underflow handling
+        order = kmin >= 3.4e-308 ? 1 : 0;
+      }
+    }
+    a.dec[j] = kind | (order << 8);
+  }
+}
+
+// One warp per entry: the entry's counts, next-level size and lower-bound base, the
+// finite-difference constant, and the statistics (into the CTA's shared copy).
+__device__ __forceinline__ void entries_reduce(const TravArgs& a, int cur, int K, int e0, int e1,
+                                               unsigned long long (*s_sst)[sNStat])
+{
+  const int lane = threadIdx.x & 31;
+  for (int e = e0 + (threadIdx.x >> 5); e < e1; e += kPBlock / 32) {
+    const int key = a.fq[cur][e];
+    const int slot = key / K, Q = key - slot * K;
+    const int off = a.foff[cur][e], len = a.flen[cur][e];
+    const bool qleaf = a.Q.left[Q] < 0;
+    const unsigned long long nqi = (unsigned long long)a.Q.count[Q];
+    double fd_dlo = 0.0, fd_const = 0.0, ret = 0.0;
+    int nF = 0, nDT = 0, nT = 0, nB = 0, nFD = 0, slots = 0;
+    unsigned long long kev = 0;
+    for (int j = lane; j < len; j += 32) {
+      const int R = a.fr[cur][off + j];
+      const int kind = a.dec[off + j] & 0xff;
+      const int cr = a.R.count[R];
+      const double nr = (double)cr;
+      const double kmin = a.pkmin[off + j];
+      const double dlo = nr * kmin;
+      if (kind == kFD) {
+        fd_dlo += dlo;
+        fd_const += 0.5 * nr * (a.pkmax[off + j] + kmin);
+        ++nFD;
+      } else if (kind == kX) {
+        slots += a.R.left[R] < 0 ? 1 : 2;
+      } else if (kind == kB) {
+        ++nB;
+        kev += nqi * (unsigned long long)cr;
+        ret += dlo;
+      } else {
+        ret += dlo;
+        if (kind == kF) ++nF;
+        else {
+          ++nDT;
+          if (kind == kT) ++nT;
+        }
+      }
+    }
+    fd_dlo = group_sum<32>(fd_dlo);
+    fd_const = group_sum<32>(fd_const);
+    ret = group_sum<32>(ret);
+    nF = group_sum_i<32>(nF);
+    nDT = group_sum_i<32>(nDT);
+    nT = group_sum_i<32>(nT);
+    nB = group_sum_i<32>(nB);
+    nFD = group_sum_i<32>(nFD);
+    slots = group_sum_i<32>(slots);
+    kev = group_sum_i<32>(kev);
+    if (lane == 0) {
+      const int ne = slots > 0 ? (qleaf ? 1 : 2) : 0;
+      a.cnt[e] = Cnt{ ne, ne * slots, nF, nDT, nT, nB, nFD };
+      a.childlen[e] = slots;
+      a.newbase[e] = a.fbase[cur][e] + (fd_dlo + ret);
+      if (nFD) {
+        a.L[(size_t)key * a.T] += fd_const;  // constant local term (order 1)
+        if (a.Lord[key] < 1) a.Lord[key] = 1;
+      }
+      unsigned long long* ss = s_sst[slot];
+      atomicAdd(ss + sPairs, (unsigned long long)len);
+      if (nFD) atomicAdd(ss + sFD, (unsigned long long)nFD);
+      if (nF) atomicAdd(ss + sF, (unsigned long long)nF);
+      if (nDT - nT) atomicAdd(ss + sD, (unsigned long long)(nDT - nT));
+      if (nT) atomicAdd(ss + sT, (unsigned long long)nT);
+      if (nB) atomicAdd(ss + sB, (unsigned long long)nB);
+      if (kev) atomicAdd(ss + sKev, kev);
+    }
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__ TravArgs a)
 {
   cg::grid_group grid = cg::this_grid();
   TravState& st = *a.st;
@@ -648,22 +823,38 @@ __global__ void __launch_bounds__(kPBlock) k_traverse(TravArgs a)
     typename BS::TempStorage s;
   } tmp;
   __shared__ Cnt s_agg, s_excl;
+  __shared__ double s_h[kMaxSlots], s_scale[kMaxSlots];
+  __shared__ unsigned long long s_sst[kMaxSlots][sNStat];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int G = gridDim.x;
-  const int K = st.K;
+  const int K = st.K, nslots = st.nslots;
+  for (int i = threadIdx.x; i < kMaxSlots * sNStat; i += kPBlock) (&s_sst[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < nslots; i += kPBlock) {
+    s_h[i] = st.h[i];
+    s_scale[i] = st.scale[i];
+  }
+  __syncthreads();
   const unsigned long long epoch = (unsigned long long)st.epoch << 32;
-  int cur = 0, m = st.nslots, p = st.nslots, gF = 0, gDT = 0, gB = 0, levels = 0;
+  int cur = 0, m = nslots, p = nslots, gF = 0, gDT = 0, gB = 0, levels = 0;
   for (;;) {
     if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && levels < 512) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       a.trace[levels * 4] = t;
+      a.trace[2048 + levels * 2] = (unsigned long long)m;
+      a.trace[2048 + levels * 2 + 1] = (unsigned long long)p;
     }
-    const int per = (m + G - 1) / G;
-    const int b0 = min(m, blockIdx.x * per), b1 = min(m, b0 + per);
-    // one warp per entry (narrower lane groups for short lists were measured: no gain,
-    // more register spills -- classify is latency- not lane-bound)
-    classify_range<DT, 32>(a, st, cur, b0, b1);
+    int b0, b1;
+    entry_bounds(a.foff[cur], m, (long long)blockIdx.x * p / G, (long long)(blockIdx.x + 1) * p / G,
+                 b0, b1);
+    const int P0 = b0 < m ? a.foff[cur][b0] : p, P1 = b1 < m ? a.foff[cur][b1] : p;
+    pairs_bounds<DT>(a, cur, K, P0, P1, s_scale);
+    __syncthreads();
+    entries_glo(a, cur, b0, b1);
+    __syncthreads();
+    pairs_decide<DT>(a, st, cur, K, P0, P1, s_h);
+    __syncthreads();
+    entries_reduce(a, cur, K, b0, b1, s_sst);
     __syncthreads();
     Cnt acc{};
     for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) acc = CntSum()(acc, a.cnt[i]);
@@ -722,6 +913,11 @@ __global__ void __launch_bounds__(kPBlock) k_traverse(TravArgs a)
     p = lv.p;
     ++levels;
     if (m == 0) break;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nslots * sNStat; i += kPBlock) {
+    const unsigned long long v = (&s_sst[0][0])[i];
+    if (v) atomicAdd(&st.sst[0][0] + i, v);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st.cur = cur;
@@ -911,7 +1107,9 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
       flen_[b].reserve(capE_);
       fbase_[b].reserve(capE_);
       fr_[b].reserve(capP_);
+      pent_[b].reserve(capP_);
     }
+    pglo_.reserve(capE_);
     pkmax_.reserve(capP_);
     pkmin_.reserve(capP_);
     dec_.reserve(capP_);
@@ -940,7 +1138,9 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
       a.flen[b] = flen_[b].p;
       a.fr[b] = fr_[b].p;
       a.fbase[b] = fbase_[b].p;
+      a.pent[b] = pent_[b].p;
     }
+    a.glo = pglo_.p;
     a.pkmax = pkmax_.p;
     a.pkmin = pkmin_.p;
     a.dec = dec_.p;
@@ -965,14 +1165,14 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     a.tflag = tflag_.p;
     static const bool tracing = std::getenv("DFGTB_TRACE") != nullptr;
     if (tracing) {
-      trace_.reserve(512 * 4);
-      CK(cudaMemsetAsync(trace_.p, 0, sizeof(unsigned long long) * 512 * 4, s));
+      trace_.reserve(512 * 6);
+      CK(cudaMemsetAsync(trace_.p, 0, sizeof(unsigned long long) * 512 * 6, s));
       a.trace = trace_.p;
     }
     const std::vector<const void*> sig = {
       a.Q.lo, a.Q.hi, a.Q.cen, a.Q.side, a.Q.left, a.Q.right, a.Q.count, a.Q.begin,
       a.R.lo, a.R.hi, a.R.side, a.R.left, a.R.right, a.R.count,
-      a.st, a.fq[0], a.fq[1], a.foff[0], a.foff[1], a.flen[0], a.flen[1], a.fr[0], a.fr[1],
+      a.st, a.pent[0], a.pent[1], a.glo, a.fq[0], a.fq[1], a.foff[0], a.foff[1], a.flen[0], a.flen[1], a.fr[0], a.fr[1],
       a.fbase[0], a.fbase[1], a.pkmax, a.pkmin, a.dec, a.cnt, a.cntoff, a.tsum, a.toff,
       a.childlen, a.newbase, a.L, a.Lord, a.itF, a.itDT, a.itB, a.cntF, a.cntDT, a.cntB };
 
@@ -1001,13 +1201,13 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     CK(cudaStreamSynchronize(s));
     if (!use_persistent_ && use_graph_) launch_counter() += (uint64_t)hs->levels * kLevelKernels;
     if (a.trace) {  // per level: classify | scan | emit (microseconds)
-      std::vector<unsigned long long> tr(512 * 4);
+      std::vector<unsigned long long> tr(512 * 6);
       CK(cudaMemcpy(tr.data(), a.trace, sizeof(unsigned long long) * tr.size(),
                     cudaMemcpyDeviceToHost));
       for (int L = 0; L < std::min(hs->levels, 511); ++L)
-        std::fprintf(stderr, "DFGTB_TRACE level %d: classify+lookback %.1f us, emit+sync %.1f us (%.1f)\n", L,
-                     (tr[L * 4 + 1] - tr[L * 4]) * 1e-3, (tr[L * 4 + 2] - tr[L * 4 + 1]) * 1e-3,
-                     (tr[(L + 1) * 4 + 3] - tr[L * 4 + 2]) * 1e-3);
+        std::fprintf(stderr, "DFGTB_TRACE level %d: entries %llu pairs %llu classify+lookback %.1f us, emit+sync %.1f us\n",
+                     L, tr[2048 + L * 2], tr[2048 + L * 2 + 1], (tr[L * 4 + 1] - tr[L * 4]) * 1e-3,
+                     (tr[L * 4 + 2] - tr[L * 4 + 1]) * 1e-3);
     }
     if (!hs->overflow) break;
     if (attempt > 10) throw OutOfMemory("traversal buffers keep overflowing");
