@@ -144,6 +144,10 @@ int dfgtb_series_op(int op, size_t d, int p_max, const double* in, size_t n, con
 /* Measured FP64 FMA instruction throughput of the device (instr/s); bench roofline. */
 double dfgtb_dfma_peak(void);
 
+/* Max relative error of the base case's MUFU exp (used when epsilon >= 1e-4; its
+ * bound is charged against epsilon) over every argument it can form; test entry. */
+double dfgtb_mufu_exp_error(void);
+
 /* Device (and pinned host) memory of destroyed handles is cached for reuse by later
  * handles, like PyTorch's caching allocator; this returns it to the driver. */
 void dfgtb_release_cached_memory(void);

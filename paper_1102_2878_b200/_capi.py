@@ -56,7 +56,7 @@ EXPORTS = (
     "dfgtb_last_timings",
     "dfgtb_p_max", "dfgtb_cv", "dfgtb_sweep", "dfgtb_lkcv_from_sums", "dfgtb_lscv_from_sums",
     "dfgtb_tree_nodes", "dfgtb_tree_height", "dfgtb_export_tree", "dfgtb_naive",
-    "dfgtb_series_op", "dfgtb_dfma_peak", "dfgtb_device_count", "dfgtb_release_cached_memory",
+    "dfgtb_series_op", "dfgtb_dfma_peak", "dfgtb_mufu_exp_error", "dfgtb_device_count", "dfgtb_release_cached_memory",
     "dfgtb_stream",
     "dfgtb_launch_count", "dfgtb_last_error",
 )
@@ -91,6 +91,7 @@ def _load():
         "dfgtb_series_op": (C.c_int, [C.c_int, sz, C.c_int, _D, sz, _D, _D, C.c_double, C.c_int,
                                       _D]),
         "dfgtb_dfma_peak": (C.c_double, []),
+        "dfgtb_mufu_exp_error": (C.c_double, []),
         "dfgtb_device_count": (C.c_int, []),
         "dfgtb_release_cached_memory": (None, []),
         "dfgtb_stream": (C.c_size_t, [V]),

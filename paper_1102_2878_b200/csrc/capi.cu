@@ -454,4 +454,11 @@ double dfgtb_dfma_peak(void)
   return v;
 }
 
+double dfgtb_mufu_exp_error(void)
+{
+  double v = -1.0;
+  guard([&] { v = mufu_exp_max_error(); });
+  return v;
+}
+
 }  // extern "C"

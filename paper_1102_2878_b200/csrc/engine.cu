@@ -8,6 +8,8 @@
 // (execute.cu); a single compute() is a batch of one.
 #include "internal.cuh"
 
+#include <cstdlib>
+
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -125,6 +127,7 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
     throw InvalidArgument("SeriesGeometry requires dim >= 1 and 1 <= p_max <= 15");
   D_ = (int)d;
   n_ = n;
+  mufu_ = cfg.epsilon >= kMufuMinEps && D_ <= 5 && std::getenv("DFGTB_EXACT_EXP") == nullptr;
   const int pm = cfg.mode == 0 ? 1 : (cfg.p_max > 0 ? cfg.p_max : default_p_max(D_));
   ser_ = SeriesTables(D_, pm);
   if (D_ * (pm - 1) >= 128) throw InvalidArgument("D * (p_max - 1) must be < 128");

@@ -47,6 +47,14 @@ struct Item {
 
 constexpr int kMaxSlots = 64;  // bandwidths per batch
 
+// Base-case exp on the MUFU (ex2.approx.f32 on an exactly reduced argument, FP64
+// distance and accumulation): per-term relative error < kMufuCharge, which the
+// traversal pays for by running at eps - kMufuCharge.  Used when eps >= kMufuMinEps
+// (the charge is then <= 2% of the budget) unless DFGTB_EXACT_EXP is set; smaller eps
+// keep the FP64 exp (<= ~1 ulp).
+constexpr double kMufuMinEps = 1e-4;
+constexpr double kMufuCharge = 2e-6;
+
 int default_p_max(int D);
 
 class Engine {
@@ -73,6 +81,7 @@ public:
   const Timings& last_timings() const { return tim_; }
   const DevTree& ref_tree() const { return rt_; }
   int p_max() const { return ser_.pmax; }
+  bool mufu_exp() const { return mufu_; }
   int dim() const { return D_; }
   size_t n() const { return n_; }
   cudaStream_t stream() const { return s_; }
@@ -105,7 +114,7 @@ private:
   DevBuf<double> L_, Mt_, s_ff_;      // Mt_: UNSCALED reference moments (h-independent)
   DevBuf<int> Lord_, cntF_, cntDT_, cntB_, offF_, offDT_, offB_, mflag_, mdone_;
   bool eager_ = false;                // Mt_ holds every node (tables <= 4096 terms)
-  DevBuf<int> lnch_, lchoff_, lchunk_, ntask_, toff_, tasks_, leaf_task_, brec_, bnext_;
+  DevBuf<int> lnch_, lchoff_, lchunk_, ntask_, toff_, tasks_, leaf_task_, leaf_runs_, brec_, bnext_;
   DevBuf<double> lpart_, bpart_, xq_, xr_, slotp_;
   // frontier (double buffered) and per-level scratch
   DevBuf<int> fq_[2], foff_[2], flen_[2], fr_[2], pent_[2];
@@ -136,6 +145,7 @@ private:
   Timings tim_;
   long long nF_ = 0, nDT_ = 0, nB_ = 0;
   int nb_ = 1;
+  bool mufu_ = false;
 };
 
 // Exhaustive FP64 sums on the device (K12, naive_kde engine.cpp:22-36).
@@ -144,6 +154,8 @@ void naive_device(const double* d_q, size_t nq, const double* d_r, size_t nr, in
 
 // Measured FP64 FMA throughput (instr/s) -- roofline denominator for bench.py.
 double measure_dfma_peak(int device);
+// Max relative error of the base case's MUFU exp over every argument it can form.
+double mufu_exp_max_error();
 
 // Series term tables -> one device blob, and the device view over it.
 void upload_series(const SeriesTables& t, DevBuf<unsigned char>& dev, cudaStream_t s);

@@ -12,6 +12,8 @@
 //   lkcv / lscv_from_sums             cv.cpp:61-97        -> k_cv_partial
 #include "internal.cuh"
 
+#include <cstring>
+
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -276,39 +278,69 @@ __global__ void k_l2l(DevSeries g, TreeView Q, int K, int nb, const int* nodes_a
 // Base-case tasks: a (slot, query leaf)'s sorted base items cut into runs of <=
 // kTaskItems reference leaves, times 32-query chunks of the leaf.  One warp per task
 // writes per-query partial sums; k_finalize adds a query's partials in task order.
-constexpr int kTaskItems = 8;
-static_assert(kTaskItems <= 32 && (kTaskItems & (kTaskItems - 1)) == 0, "one item per lane");
+constexpr int kTaskItems = 32;  // at most one reference leaf per lane
 struct BTask {
   int key, item0, item1, q0;
 };
 
-__global__ void k_task_count(const int* leaves, int nleaves, int nb, int K, const int* cntB,
-                             TreeView Q, int* nt)
+// A (slot, query leaf)'s sorted base items are cut into RUNS of consecutive items
+// whose points fit the warp's stream tile (<= rmax points, <= kTaskItems items; a
+// single larger leaf is a run of its own and is streamed in tiles).  One warp per
+// (slot, leaf): a window of 32 items, inclusive scan of their counts, the run is the
+// prefix that fits.  Returns the next run's first item (all lanes).
+__device__ __forceinline__ int warp_run_end(const Item* it, int k, int e, const int* rcount, int rmax,
+                                            int lane)
 {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nleaves * nb) return;
-  const int slot = i / nleaves;
-  const int leaf = leaves[i - slot * nleaves];
-  const int ic = (cntB[slot * K + leaf] + kTaskItems - 1) / kTaskItems;
-  nt[i] = ic * ((Q.count[leaf] + 31) / 32);
+  const int j = k + lane;
+  int pre = j < e ? rcount[it[j].r] : (1 << 28);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, pre, o);
+    if (lane >= o) pre = min(pre + v, 1 << 28);
+  }
+  const unsigned fit = __ballot_sync(0xffffffffu, j < e && (pre <= rmax || lane == 0));
+  return k + __popc(fit);
 }
 
-__global__ void k_task_fill(const int* leaves, int nleaves, int nb, int K, const int* cntB,
-                            const int* offB, TreeView Q, const int* toff, BTask* tasks,
-                            int* leaf_task)
+__global__ void k_task_count(const int* leaves, int nleaves, int nb, int K, const int* cntB,
+                             const int* offB, const Item* sB, const int* rcount, int rmax, TreeView Q,
+                             int* nt)
 {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= nleaves * nb) return;
   const int slot = i / nleaves;
   const int leaf = leaves[i - slot * nleaves];
   const int key = slot * K + leaf;
-  const int c = cntB[key], o = offB[key];
-  const int ic = (c + kTaskItems - 1) / kTaskItems;
-  int t = toff[i];
-  leaf_task[key] = t;
-  for (int q0 = 0; q0 < Q.count[leaf]; q0 += 32)
-    for (int k = 0; k < ic; ++k)
-      tasks[t++] = BTask{ key, o + k * kTaskItems, o + min(c, (k + 1) * kTaskItems), q0 };
+  const int o = offB[key], e = o + cntB[key];
+  int runs = 0;
+  for (int k = o; k < e; k = warp_run_end(sB, k, e, rcount, rmax, lane)) ++runs;
+  if (lane == 0) nt[i] = runs * ((Q.count[leaf] + 31) / 32);
+}
+
+__global__ void k_task_fill(const int* leaves, int nleaves, int nb, int K, const int* cntB,
+                            const int* offB, const Item* sB, const int* rcount, int rmax, TreeView Q,
+                            const int* toff, BTask* tasks, int* leaf_task, int* leaf_runs)
+{
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= nleaves * nb) return;
+  const int slot = i / nleaves;
+  const int leaf = leaves[i - slot * nleaves];
+  const int key = slot * K + leaf;
+  const int o = offB[key], e = o + cntB[key];
+  const int nq = (Q.count[leaf] + 31) / 32;
+  const int t0 = toff[i];
+  const int nruns = nq ? (toff[i + 1] - t0) / nq : 0;  // tasks: query chunk major, run minor
+  int runs = 0;
+  for (int k = o; k < e;) {
+    const int j = warp_run_end(sB, k, e, rcount, rmax, lane);
+    for (int qi = lane; qi < nq; qi += 32) tasks[t0 + qi * nruns + runs] = BTask{ key, k, j, 32 * qi };
+    k = j;
+    ++runs;
+  }
+  if (lane == 0) {
+    leaf_task[key] = t0;
+    leaf_runs[key] = runs;
+  }
 }
 
 // Table-driven exp(-y), 0 <= y <= 708: -y = (64 m + j) ln2/64 + r, |r| <= ln2/128,
@@ -361,10 +393,47 @@ __device__ __forceinline__ double exp_negy_c(double y, unsigned tabs)
   return big ? e * 0x1p-64 : e;
 }
 
+// MUFU exp for the fast base case (eps >= kMufuMinEps; the traversal runs with
+// eps - kMufuCharge so the per-term error below is paid for).
+// Coordinates are scaled by sqrt(log2 e) / (h sqrt 2) and centred on the chunk's first
+// query, so z = y log2 e = |q|^2 + |r|^2 - 2 q.r is formed in FP64 directly on top of
+// the fixed-point magic: t = M + b - 896 + z with M = 1.5 2^31 (ulp 2^-21), so the low
+// word of t is (z + b - 896) in signed 11.21 fixed point (b = kMufuBias units keeps
+// z + b >= 0 under the D + 2 roundings; 0 <= z <= 1021.4 on the fast path).  Then
+//   2^-z = 2^-n 2^-(f - b 2^-21),  n - 896 = lo >>a 21,  f = lo & (2^21 - 1),
+// 2^-(f - b) by ex2.approx.ftz.f32 of an exact FP32 argument, and 2^-n spliced into the
+// exponent while widening to FP64 (hi = (G >> 3) - ((n - 896) << 20); n <= 1021 keeps
+// the result normal).  Per-term relative error <= (D + 2) ln2 2^-22 (fixed-point
+// rounding) + ex2.approx's error (exhaustively measured by the tests over every
+// reachable argument).
+constexpr int kMufuBias = 4;
+constexpr unsigned kMufuHi = 0x41E80000u;    // high word of t for 896 - b <= z < 1920
+template <bool CLAMP = false>
+__device__ __forceinline__ double exp2_neg_fixed(double t)
+{
+  int lo = __double2loint(t);
+  if constexpr (CLAMP) {  // z > 1021 -> 2^-1021 (only where the traversal pays for it)
+    const unsigned hi = (unsigned)__double2hiint(t);  // kMufuHi - 1 below z = 896 - b
+    const int lmax = (125 << 21) | 0x1FFFFF;
+    lo = hi > kMufuHi || (hi == kMufuHi && (unsigned)lo > (unsigned)lmax) ? lmax : lo;
+  }
+  const float x = __uint_as_float(((unsigned)lo & 0x1FFFFFu) | 0x4B000000u);  // 2^23 + f
+  const float a = fmaf(x, -0x1p-21f, 4.0f + kMufuBias * 0x1p-21f);           // (b - f) 2^-21, exact
+  float g;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(a));
+  const unsigned G = __float_as_uint(g);
+  const unsigned hi = (G >> 3) - ((unsigned)(lo >> 1) & 0xFFF00000u);
+  return __hiloint2double((int)hi, (int)(G << 29));
+}
+constexpr double kMufuMagic = 3221225472.0 - 896.0 + kMufuBias * 0x1p-21;  // M - 896 + b 2^-21
+constexpr double kSqrtLog2e = 1.2011224087864498;                           // sqrt(log2 e)
+constexpr double kLn2 = 0.6931471805599453;
+
 // Scaled, centred, padded coordinates for the base case, per slot:
-// x' = (x - c0) / (h sqrt 2) so that |q' - r'|^2 = |q - r|^2 / (2 h^2) (stride DP).
+// x' = (x - c0) f / (h sqrt 2) so that |q' - r'|^2 = f^2 |q - r|^2 / (2 h^2) (stride DP);
+// f = sqrt(log2 e) when the base case uses the MUFU exp (2^-z), else 1 (e^-y).
 __global__ void k_scale_points(const double* xs, int n, int D, int DP, int nb, const double* c0,
-                               SlotView sv, double* out)
+                               SlotView sv, double f, double* out)
 {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t per = (size_t)n * DP;
@@ -373,7 +442,7 @@ __global__ void k_scale_points(const double* xs, int n, int D, int DP, int nb, c
   const size_t j = i - (size_t)slot * per;
   const size_t p = j / DP;
   const int d = (int)(j % DP);
-  out[i] = d < D ? (xs[p * D + d] - c0[d]) * sv.s[slot] : 0.0;
+  out[i] = d < D ? (xs[p * D + d] - c0[d]) * (sv.s[slot] * f) : 0.0;
 }
 
 template <int DT>
@@ -420,15 +489,15 @@ struct PtLoad {
 };
 
 // Compact reference-leaf records for the base case, in sorted item order:
-// {first sorted position, count}, count negated when the traversal could not prove
-// y <= 708 for every pair (then the careful exp path runs).
+// {first sorted position, count | flags << 28}; flags bit 0: the traversal proved
+// y <= 708 for every pair; bit 1: terms may be clamped at 2^-1021 (see traverse.cu).
 __global__ void k_base_records(const Item* items, int n, TreeView R, int2* rec)
 {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const Item it = items[i];
   const int c = R.count[it.r];
-  rec[i] = make_int2(R.begin[it.r], (it.code & 1) ? c : -c);
+  rec[i] = make_int2(R.begin[it.r], c | ((it.code & 3) << 28));
 }
 
 // K10: exhaustive base case (Traversal::base_case, engine.cpp:239-269).  One warp per
@@ -452,12 +521,14 @@ struct BaseGeo {
   static constexpr int G = DT <= 2 ? DFGTB_BASE_G : 4;            // queries per lane
   static constexpr int RMAX = DT == 1 ? 512 : DT == 2 ? 256 : DT <= 4 ? 128 : 64;  // stream tile
   static constexpr int WARPS = 4;                                 // per CTA
-  static constexpr int WORDS = RMAX * DP + 32 * DP + 32;          // refs | queries | sums
+  static constexpr int DM = (DT + 2) / 2 * 2;                     // MUFU stream stride
+  static constexpr int DS = DM > DP ? DM : DP;
+  static constexpr int WORDS = RMAX * DS + 32 * DS + 32;          // refs | queries | sums
 };
 
 template <int DT, int GG, bool FAST>
 __device__ __forceinline__ void base_group(const double* rs, int n, const double* qs, double* qsum,
-                                           const double* tab, int lane)
+                                           const double* tab, double ysc, int lane)
 {
   constexpr int D = DT, DP = BaseGeo<DT>::DP;
   constexpr int LG = GG == 8 ? 3 : GG == 4 ? 2 : GG == 2 ? 1 : 0;
@@ -482,7 +553,7 @@ __device__ __forceinline__ void base_group(const double* rs, int n, const double
         y = fma(t, t, y);
       }
       if constexpr (FAST) acc[i] += exp_negy_s(y, tabs);
-      else acc[i] += exp_negy_c(y, tabs);
+      else acc[i] += exp_negy_c(y * ysc, tabs);  // ysc = ln 2 on log2e-scaled points
     }
   };
   // one copy of the body (instruction-cache footprint): lanes past the end of the
@@ -511,33 +582,148 @@ __device__ __forceinline__ void base_group(const double* rs, int n, const double
   if ((lane & ((32 >> LG) - 1)) == 0) qsum[lane >> (5 - LG)] += acc[0];
 }
 
-// Queries in groups of G, the remainder in groups of 4, 2, 1.  Each group size is one
-// out-of-line copy, to keep the kernel's hot code small.
-template <int DT, int GG, bool FAST>
-__device__ __noinline__ void base_group_call(const double* rs, int n, const double* qs, double* qsum,
-                                             const double* tab, int lane)
+// MUFU variant: the stream holds centred (log2e-scaled) points r and |r|^2 (stride DM),
+// the query tile the same (q, |q|^2); per pair t = fma(-2q_d, r_d, .. (M + |q|^2) + |r|^2).
+template <int DT>
+struct MPt {
+  static constexpr int DM = (DT + 2) / 2 * 2;  // D coordinates + |r|^2, padded to 16 bytes
+  __device__ __forceinline__ static void load(const double* base, int j, double (&v)[DM])
+  {
+    const double2* b2 = reinterpret_cast<const double2*>(base + (size_t)j * DM);
+#pragma unroll
+    for (int k = 0; k < DM / 2; ++k) {
+      const double2 t = b2[k];
+      v[2 * k] = t.x;
+      v[2 * k + 1] = t.y;
+    }
+  }
+  // point j of src (stride DP, log2e-scaled coordinates) -> centred on c, |r|^2
+  __device__ __forceinline__ static void stage(const double* src, int j, const double* c, double* dst,
+                                               int j2)
+  {
+    constexpr int DP = PtLoad<DT>::DP;
+    double v[DM];
+    double rr = 0.0;
+#pragma unroll
+    for (int d = 0; d < DT; ++d) {
+      v[d] = src[(size_t)j * DP + d] - c[d];
+      rr = fma(v[d], v[d], rr);
+    }
+    v[DT] = rr;
+#pragma unroll
+    for (int d = DT + 1; d < DM; ++d) v[d] = 0.0;
+    double2* d2 = reinterpret_cast<double2*>(dst + (size_t)j2 * DM);
+#pragma unroll
+    for (int k = 0; k < DM / 2; ++k) d2[k] = make_double2(v[2 * k], v[2 * k + 1]);
+  }
+};
+
+template <int DT, int GG, bool CLAMP>
+__device__ __forceinline__ void base_group_mufu(const double* rs, int n, const double* qs, double* qsum,
+                                                int lane)
 {
-  base_group<DT, GG, FAST>(rs, n, qs, qsum, tab, lane);
+  constexpr int D = DT, DM = MPt<DT>::DM;
+  constexpr int LG = GG == 8 ? 3 : GG == 4 ? 2 : GG == 2 ? 1 : 0;
+  double m[GG][D], A[GG], acc[GG];
+#pragma unroll
+  for (int i = 0; i < GG; ++i) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) m[i][d] = -2.0 * qs[i * DM + d];
+    A[i] = kMufuMagic + qs[i * DM + D];
+    acc[i] = 0.0;
+  }
+  // the G chains of a reference point are written stage by stage (independent
+  // instructions back to back) so the warp always has work while one chain waits
+  auto body = [&](int j) {
+    double r[DM];
+    MPt<DT>::load(rs, j, r);
+    double t[GG];
+#pragma unroll
+    for (int i = 0; i < GG; ++i) t[i] = A[i] + r[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+#pragma unroll
+      for (int i = 0; i < GG; ++i) t[i] = fma(m[i][d], r[d], t[i]);
+#pragma unroll
+    for (int i = 0; i < GG; ++i) acc[i] += exp2_neg_fixed<CLAMP>(t[i]);
+  };
+  const int nceil = (n + 31) & ~31;
+  for (int j = lane; j < nceil; j += 32)
+    if (j < n) body(j);
+#pragma unroll
+  for (int s = 0; s < LG; ++s) {
+    const int off = 16 >> s;
+    const bool up = lane & off;
+    const int h = GG >> (s + 1);
+#pragma unroll
+    for (int i = 0; i < GG / 2; ++i) {
+      if (i < h) {
+        const double send = up ? acc[i] : acc[i + h];
+        const double keep = up ? acc[i + h] : acc[i];
+        acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16 >> LG; off >= 1; off >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
+  if ((lane & ((32 >> LG) - 1)) == 0) qsum[lane >> (5 - LG)] += acc[0];
 }
 
-template <int DT, bool FAST>
-__device__ __forceinline__ void base_groups(const double* rs, int n, const double* qs, double* qsum,
-                                            int qc, const double* tab, int lane)
+template <int DT, int GG, bool CLAMP>
+__device__ __noinline__ void base_group_mufu_call(const double* rs, int n, const double* qs,
+                                                  double* qsum, int lane)
 {
-  constexpr int DP = BaseGeo<DT>::DP, G = BaseGeo<DT>::G;
+  base_group_mufu<DT, GG, CLAMP>(rs, n, qs, qsum, lane);
+}
+
+template <int DT, bool CLAMP>
+__device__ __forceinline__ void base_groups_mufu(const double* rs, int n, const double* qs, double* qsum,
+                                                 int qc, int lane)
+{
+  constexpr int DM = MPt<DT>::DM, G = BaseGeo<DT>::G;
   int g0 = 0;
-  for (; g0 + G <= qc; g0 += G) base_group_call<DT, G, FAST>(rs, n, qs + g0 * DP, qsum + g0, tab, lane);
+  for (; g0 + G <= qc; g0 += G) base_group_mufu_call<DT, G, CLAMP>(rs, n, qs + g0 * DM, qsum + g0, lane);
   if constexpr (G >= 8) {
     if (qc - g0 >= 4) {
-      base_group_call<DT, 4, FAST>(rs, n, qs + g0 * DP, qsum + g0, tab, lane);
+      base_group_mufu_call<DT, 4, CLAMP>(rs, n, qs + g0 * DM, qsum + g0, lane);
       g0 += 4;
     }
   }
   if (qc - g0 >= 2) {
-    base_group_call<DT, 2, FAST>(rs, n, qs + g0 * DP, qsum + g0, tab, lane);
+    base_group_mufu_call<DT, 2, CLAMP>(rs, n, qs + g0 * DM, qsum + g0, lane);
     g0 += 2;
   }
-  if (qc - g0 >= 1) base_group_call<DT, 1, FAST>(rs, n, qs + g0 * DP, qsum + g0, tab, lane);
+  if (qc - g0 >= 1) base_group_mufu_call<DT, 1, CLAMP>(rs, n, qs + g0 * DM, qsum + g0, lane);
+}
+
+// Queries in groups of G, the remainder in groups of 4, 2, 1.  Each group size is one
+// out-of-line copy, to keep the kernel's hot code small.
+template <int DT, int GG, bool FAST>
+__device__ __noinline__ void base_group_call(const double* rs, int n, const double* qs, double* qsum,
+                                             const double* tab, double ysc, int lane)
+{
+  base_group<DT, GG, FAST>(rs, n, qs, qsum, tab, ysc, lane);
+}
+
+template <int DT, bool FAST>
+__device__ __forceinline__ void base_groups(const double* rs, int n, const double* qs, double* qsum,
+                                            int qc, const double* tab, double ysc, int lane)
+{
+  constexpr int DP = BaseGeo<DT>::DP, G = BaseGeo<DT>::G;
+  int g0 = 0;
+  for (; g0 + G <= qc; g0 += G)
+    base_group_call<DT, G, FAST>(rs, n, qs + g0 * DP, qsum + g0, tab, ysc, lane);
+  if constexpr (G >= 8) {
+    if (qc - g0 >= 4) {
+      base_group_call<DT, 4, FAST>(rs, n, qs + g0 * DP, qsum + g0, tab, ysc, lane);
+      g0 += 4;
+    }
+  }
+  if (qc - g0 >= 2) {
+    base_group_call<DT, 2, FAST>(rs, n, qs + g0 * DP, qsum + g0, tab, ysc, lane);
+    g0 += 2;
+  }
+  if (qc - g0 >= 1) base_group_call<DT, 1, FAST>(rs, n, qs + g0 * DP, qsum + g0, tab, ysc, lane);
 }
 
 #ifndef DFGTB_BASE_MINB
@@ -546,18 +732,20 @@ __device__ __forceinline__ void base_groups(const double* rs, int n, const doubl
 template <int DT>
 __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
   k_base_case(TreeView Q, int K, const BTask* tasks, int ntasks, const int2* rec, const double* xq,
-              const double* xr, int nq, int nr, double* part, int* next)
+              const double* xr, int nq, int nr, double* part, int* next, int mufu)
 {
   using Geo = BaseGeo<DT>;
   constexpr int DP = Geo::DP, RMAX = Geo::RMAX;
   __shared__ __align__(512) double tab[64];
   __shared__ __align__(16) double sm[Geo::WARPS][Geo::WORDS];
+  __shared__ unsigned smask_all[Geo::WARPS][RMAX / 32];
   if (threadIdx.x < 64) tab[threadIdx.x] = c_exp2tab[threadIdx.x];
   __syncthreads();
   const int lane = threadIdx.x & 31;
   double* rs = sm[threadIdx.x >> 5];
-  double* qs = rs + RMAX * DP;
-  double* qsum = qs + 32 * DP;
+  double* qs = rs + RMAX * Geo::DS;
+  double* qsum = qs + 32 * Geo::DS;
+  unsigned* smask = smask_all[threadIdx.x >> 5];
   int w = 0;
   if (lane == 0) w = atomicAdd(next, 1);
   w = __shfl_sync(0xffffffffu, w, 0);
@@ -571,8 +759,9 @@ __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
     const int2 rc = lane < nit ? rec[t.item0 + lane] : make_int2(0, 0);
     const int qc = min(32, Q.count[leaf] - t.q0);
     const int qb = Q.begin[leaf];
-    const int cnt = rc.y > 0 ? rc.y : -rc.y;
-    const bool fast = __all_sync(0xffffffffu, lane >= nit || rc.y > 0);
+    const int cnt = rc.y & 0x0FFFFFFF;
+    const bool fast = __all_sync(0xffffffffu, lane >= nit || (rc.y & (1 << 28)));
+    const bool clampok = __all_sync(0xffffffffu, lane >= nit || (rc.y & (3 << 28)));
     int incl = cnt;
 #pragma unroll
     for (int o = 1; o < kTaskItems; o <<= 1) {
@@ -580,31 +769,46 @@ __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
       if (lane >= o) incl += v;
     }
     const int total = __shfl_sync(0xffffffffu, incl, kTaskItems - 1);
-    int sk[kTaskItems], ok[kTaskItems];  // stream start of item k, source position - start
-#pragma unroll
-    for (int k = 0; k < kTaskItems; ++k) {
-      sk[k] = k < nit ? __shfl_sync(0xffffffffu, incl - cnt, k) : INT_MAX;
-      ok[k] = __shfl_sync(0xffffffffu, rc.x - (incl - cnt), k);
-    }
+    const int sk = incl - cnt;   // lane k < nit: stream start of item k
+    const int okk = rc.x - sk;   // its source position = okk + stream position
     const double* qsrc = xq + ((size_t)slot * nq + qb + t.q0) * DP;
-    if (lane < qc) PtLoad<DT>::copy(qsrc, lane, qs);
+    const bool mf = (fast || clampok) && mufu;
+    double cq[DT];  // MUFU path: centre = the chunk's first query
+#pragma unroll
+    for (int d = 0; d < DT; ++d) cq[d] = qsrc[d];
+    if (lane < qc) {
+      if (mf) MPt<DT>::stage(qsrc, lane, cq, qs, lane);
+      else PtLoad<DT>::copy(qsrc, lane, qs);
+    }
     qsum[lane] = 0.0;
     const double* xrs = xr + (size_t)slot * nr * DP;
     for (int c0 = 0; c0 < total; c0 += RMAX) {
-      // stage stream positions [c0, c0 + n): every lane issues all its loads at once
+      // stage stream positions [c0, c0 + n).  Owner item of position c0 + 32 i + lane:
+      // (items started at or before c0) + (starts in word i at or below this lane's
+      // bit) + (starts in earlier words) - 1, from a bit mask of the item starts.
       const int n = min(RMAX, total - c0);
+      if (lane < RMAX / 32) smask[lane] = 0u;
+      __syncwarp();
+      if (lane < nit && sk > c0 && sk < c0 + n) atomicOr(&smask[(sk - c0) >> 5], 1u << ((sk - c0) & 31));
+      int kb = __popc(__ballot_sync(0xffffffffu, lane < nit && sk <= c0)) - 1;
+      __syncwarp();
+      const unsigned le = 0xffffffffu >> (31 - lane);
 #pragma unroll
       for (int i = 0; i < RMAX / 32; ++i) {
         const int e = c0 + lane + 32 * i;
-        int off = ok[0];
-#pragma unroll
-        for (int k = 1; k < kTaskItems; ++k)
-          if (sk[k] <= e) off = ok[k];
-        if (e < c0 + n) PtLoad<DT>::copy2(xrs, off + e, rs, e - c0);
+        const unsigned wm = smask[i];
+        const int off = __shfl_sync(0xffffffffu, okk, kb + __popc(wm & le));
+        kb += __popc(wm);
+        if (e < c0 + n) {
+          if (mf) MPt<DT>::stage(xrs, off + e, cq, rs, e - c0);
+          else PtLoad<DT>::copy2(xrs, off + e, rs, e - c0);
+        }
       }
       __syncwarp();
-      if (fast) base_groups<DT, true>(rs, n, qs, qsum, qc, tab, lane);
-      else base_groups<DT, false>(rs, n, qs, qsum, qc, tab, lane);
+      if (mf && fast) base_groups_mufu<DT, false>(rs, n, qs, qsum, qc, lane);
+      else if (mf) base_groups_mufu<DT, true>(rs, n, qs, qsum, qc, lane);
+      else if (fast) base_groups<DT, true>(rs, n, qs, qsum, qc, tab, 1.0, lane);
+      else base_groups<DT, false>(rs, n, qs, qsum, qc, tab, mufu ? kLn2 : 1.0, lane);
       __syncwarp();
     }
     if (lane < qc) part[(size_t)w * 32 + lane] = qsum[lane];
@@ -783,7 +987,8 @@ __global__ void __launch_bounds__(kBlock) k_farfield_t(TreeView Q, TreeView R, i
 // the same polynomial, re-centred exactly, without the per-level launch chain.
 __global__ void k_finalize(DevSeries g, TreeView Q, int K, int nb, const int* leaf_of_pos,
                            const int* perm, int n, const double* L, const int* Lord,
-                           const int* cntB, const int* leaf_task, const double* part,
+                           const int* cntB, const int* leaf_task, const int* leaf_runs,
+                           const double* part,
                            const double* s_ff, SlotView sv, int direct, double* out)
 {
   const long long gi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -811,7 +1016,7 @@ __global__ void k_finalize(DevSeries g, TreeView Q, int K, int nb, const int* le
       loc = dev_eval_local(g, L + (size_t)lkey * g.T, Q.cen + (size_t)leaf * g.D, qp, s, order);
   }
   const int li = i - Q.begin[leaf];
-  const int nic = (cntB[lkey] + kTaskItems - 1) / kTaskItems;
+  const int nic = cntB[lkey] ? leaf_runs[lkey] : 0;
   double ex = 0.0;
   if (nic) {
     const int t0 = leaf_task[lkey] + (li >> 5) * nic;
@@ -918,12 +1123,26 @@ __global__ void k_dfma_peak(double* out, int iters)
   if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == 42.0) out[0] = 1.0;
 }
 
+// Points per task run: the base case's stream tile (k_base_case_any streams directly).
+int base_rmax(int D)
+{
+  switch (D) {
+  case 1: return BaseGeo<1>::RMAX;
+  case 2: return BaseGeo<2>::RMAX;
+  case 3: return BaseGeo<3>::RMAX;
+  case 4: return BaseGeo<4>::RMAX;
+  case 5: return BaseGeo<5>::RMAX;
+  default: return 256;
+  }
+}
+
 int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }
 
 // Persistent grid: as many CTAs as fit on the GPU (or fewer for small task lists).
 template <int DT>
 void launch_base_t(int ntasks, cudaStream_t s, TreeView Q, int K, const BTask* tasks, const int2* rec,
-                   const double* xq, const double* xr, int nq, int nr, double* part, int* next)
+                   const double* xq, const double* xr, int nq, int nr, double* part, int* next,
+                   int mufu)
 {
   static int per_sm = 0, nsm = 0;
   constexpr int threads = BaseGeo<DT>::WARPS * 32;
@@ -937,14 +1156,14 @@ void launch_base_t(int ntasks, cudaStream_t s, TreeView Q, int K, const BTask* t
   const int grid = (int)std::min<long long>((long long)nsm * per_sm,
                                             (ntasks + BaseGeo<DT>::WARPS - 1) / BaseGeo<DT>::WARPS);
   CK(cudaMemsetAsync(next, 0, sizeof(int), s));
-  k_base_case<DT><<<grid, threads, 0, s>>>(Q, K, tasks, ntasks, rec, xq, xr, nq, nr, part, next);
+  k_base_case<DT><<<grid, threads, 0, s>>>(Q, K, tasks, ntasks, rec, xq, xr, nq, nr, part, next, mufu);
 }
 
 void launch_base(int D, int grid, cudaStream_t s, TreeView Q, TreeView R, int K,
                  const BTask* tasks, int ntasks, const Item* items, const int2* rec,
-                 const double* xq, const double* xr, int nq, int nr, double* part, int* next)
+                 const double* xq, const double* xr, int nq, int nr, double* part, int* next, int mufu)
 {
-#define BASE(DD) launch_base_t<DD>(ntasks, s, Q, K, tasks, rec, xq, xr, nq, nr, part, next)
+#define BASE(DD) launch_base_t<DD>(ntasks, s, Q, K, tasks, rec, xq, xr, nq, nr, part, next, mufu)
   switch (D) {
   case 1: BASE(1); break;
   case 2: BASE(2); break;
@@ -1124,10 +1343,13 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
   const int nlb = nleaves * nb;
   int ntasks = 0;
   leaf_task_.reserve(KB);
+  leaf_runs_.reserve(KB);
+  const int rmax = base_rmax(D_);
   if (nB_) {
     ntask_.reserve(nlb + 1);
     toff_.reserve(nlb + 1);
-    k_task_count<<<ceil_div(nlb, 256), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, Q, ntask_.p);
+    k_task_count<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p,
+                                                    sB_.p, R.count, rmax, Q, ntask_.p);
     CK_LAUNCH();
     CK(cudaMemsetAsync(ntask_.p + nlb, 0, sizeof(int), s));
     size_t need = 0;
@@ -1138,9 +1360,10 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
     CK(cudaMemcpyAsync(&ntasks, toff_.p + nlb, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     tasks_.reserve((size_t)ntasks * 4);
-    k_task_fill<<<ceil_div(nlb, 256), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p, Q,
-                                                   toff_.p, reinterpret_cast<BTask*>(tasks_.p),
-                                                   leaf_task_.p);
+    k_task_fill<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p,
+                                                   sB_.p, R.count, rmax, Q, toff_.p,
+                                                   reinterpret_cast<BTask*>(tasks_.p), leaf_task_.p,
+                                                   leaf_runs_.p);
     CK_LAUNCH();
     bpart_.reserve((size_t)ntasks * 32);
     brec_.reserve((size_t)nB_ * 2 + 2);
@@ -1156,13 +1379,13 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
     const int DP = padded_dim(D_);
     xq_.reserve((size_t)qt.n * DP * nb);
     k_scale_points<<<ceil_div((long long)qt.n * DP * nb, 256), 256, 0, s>>>(
-      qt.xs.p, qt.n, D_, DP, nb, rt_.centroid.p, sv, xq_.p);
+      qt.xs.p, qt.n, D_, DP, nb, rt_.centroid.p, sv, mufu_ ? kSqrtLog2e : 1.0, xq_.p);
     CK_LAUNCH();
     xq = xr = xq_.p;
     if (&qt != &rt_) {
       xr_.reserve((size_t)rt_.n * DP * nb);
       k_scale_points<<<ceil_div((long long)rt_.n * DP * nb, 256), 256, 0, s>>>(
-        rt_.xs.p, rt_.n, D_, DP, nb, rt_.centroid.p, sv, xr_.p);
+        rt_.xs.p, rt_.n, D_, DP, nb, rt_.centroid.p, sv, mufu_ ? kSqrtLog2e : 1.0, xr_.p);
       CK_LAUNCH();
       xr = xr_.p;
     }
@@ -1172,7 +1395,7 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
   if (ntasks)
     launch_base(D_, grid_warps(ntasks), s, Q, R, K, reinterpret_cast<const BTask*>(tasks_.p), ntasks,
                 sB_.p, reinterpret_cast<const int2*>(brec_.p), xq, xr, qt.n, rt_.n, bpart_.p,
-                bnext_.p);
+                bnext_.p, mufu_exp() ? 1 : 0);
   CK(cudaEventRecord(ev_[6], s));
   s_ff_.reserve((size_t)qt.n * nb);
   if (nF_) {
@@ -1196,7 +1419,8 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
   }
   CK(cudaEventRecord(ev_[7], s));
   k_finalize<<<ceil_div((long long)qt.n * nb, 128), 128, 0, s>>>(
-    g, Q, K, nb, leaf_of_pos_.p, qt.perm.p, qt.n, L_.p, Lord_.p, cntB_.p, leaf_task_.p, bpart_.p,
+    g, Q, K, nb, leaf_of_pos_.p, qt.perm.p, qt.n, L_.p, Lord_.p, cntB_.p, leaf_task_.p,
+    leaf_runs_.p, bpart_.p,
     s_ff_.p, sv, cfg_.local_pushdown == 0, d_out);
   CK_LAUNCH();
   CK(cudaEventRecord(ev_[8], s));
@@ -1249,6 +1473,50 @@ void naive_device(const double* d_q, size_t nq, const double* d_r, size_t nr, in
   k_naive<<<ceil_div(nq, 128), 128, TR * D * sizeof(double), s>>>(d_q, (int)nq, d_r, (int)nr, D,
                                                                  -1.0 / (2.0 * h * h), d_out);
   CK_LAUNCH();
+}
+
+// Exhaustive error of exp2_neg_fixed over every fixed-point argument the fast base
+// case can form: t = M - 896 + u 2^-21 for every u in [0, 1022 2^21), value
+// 2^-(u - b) 2^-21, against libdevice exp2 in FP64; and of the clamped variant beyond
+// z = 1021 (value 2^-(1021 + f)).  Max relative error as ordered bits in *out.
+__global__ void k_mufu_check(unsigned long long* out)
+{
+  unsigned long long worst = 0;
+  const unsigned long long nz = 1022ull << 21;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       i < nz + (4ull << 21); i += (unsigned long long)gridDim.x * blockDim.x) {
+    const double t = (kMufuMagic - kMufuBias * 0x1p-21) + (double)i * 0x1p-21;
+    double got, want;
+    if (i < nz) {
+      got = exp2_neg_fixed<false>(t);
+      want = exp2(-((double)i - kMufuBias) * 0x1p-21);
+    } else {  // clamp: any z >= 1022 - b -> 2^-(1021 + frac of the clamp point)
+      got = exp2_neg_fixed<true>(t + 4096.0 * (double)(i & 7));
+      want = exp2(-((double)((125u << 21) | 0x1FFFFFu) + (896u << 21) - kMufuBias) * 0x1p-21);
+    }
+    const double rel = fabs(got - want) / want;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(rel);
+    worst = b > worst ? b : worst;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, worst, o);
+    worst = v > worst ? v : worst;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, worst);
+}
+
+double mufu_exp_max_error()
+{
+  DevBuf<unsigned long long> o;
+  o.reserve(1);
+  CK(cudaMemset(o.p, 0, sizeof(unsigned long long)));
+  k_mufu_check<<<148 * 8, 256>>>(o.p);
+  CK_LAUNCH();
+  unsigned long long b = 0;
+  CK(cudaMemcpy(&b, o.p, sizeof(b), cudaMemcpyDeviceToHost));
+  double v;
+  std::memcpy(&v, &b, sizeof(v));
+  return v;
 }
 
 double measure_dfma_peak(int device)

@@ -147,6 +147,7 @@ struct TravState {
 struct TravArgs {
   TreeView Q, R;
   int D, pmax, cost, series, T;
+  int selfq;  // Q = R: every query's sum is >= 1 (its own term)
   TravState* st;
   int *fq[2], *foff[2], *flen[2], *fr[2];
   int* pent[2];  // entry index of every frontier pair (pair-balanced persistent path)
@@ -291,9 +292,14 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
       }
       if (kind == kX && qleaf && a.R.left[R] < 0) {
         kind = kB;
-        // every pair of this leaf pair has y = d^2/2h^2 <= 708 (K(d_max) >= e^-707.97):
-        // the base case may use its fast exp without underflow handling
-        order = kmin >= 3.4e-308 ? 1 : 0;
+        // bit 0: every pair of this leaf pair has y = d^2/2h^2 <= 708 (K(d_max) >= e^-707.97),
+        // the base case may use its fast exp without underflow handling; bit 1: terms
+        // below 2^-1021 may be clamped to 2^-1021 (absolute error <= |R| 2^-1021 against a
+        // sum >= 1 (Q = R) or >= G^l >= 1e-290: below 1e-280 relative); the MUFU fixed
+        // point also needs the query leaf's diameter <= 1000 in z units (sq sqrt(D)
+        // sqrt(log2 e) / (h sqrt 2), sqrt(log2 e / 2) < 0.8494)
+        order = (kmin >= 3.4e-308 ? 1 : 0) |
+                ((a.selfq || glo >= 1e-290) && sq * sqrt((double)D) * 0.8494 <= 1000.0 * h ? 2 : 0);
       }
       if (kind == kX) {
         slots += a.R.left[R] < 0 ? 1 : 2;
@@ -730,9 +736,15 @@ __device__ __forceinline__ void pairs_decide(const TravArgs& a, const TravState&
       }
       if (kind == kX && a.Q.left[Q] < 0 && a.R.left[R] < 0) {
         kind = kB;
-        // every pair of this leaf pair has y = d^2/2h^2 <= 708 (K(d_max) >= e^-707.97):
-        // the base case may use its fast exp without underflow handling
-        order = kmin >= 3.4e-308 ? 1 : 0;
+        // bit 0: every pair of this leaf pair has y = d^2/2h^2 <= 708 (K(d_max) >= e^-707.97),
+        // the base case may use its fast exp without underflow handling; bit 1: terms
+        // below 2^-1021 may be clamped to 2^-1021 (absolute error <= |R| 2^-1021 against a
+        // sum >= 1 (Q = R) or >= G^l >= 1e-290: below 1e-280 relative); the MUFU fixed
+        // point also needs the query leaf's diameter <= 1000 in z units (sq sqrt(D)
+        // sqrt(log2 e) / (h sqrt 2), sqrt(log2 e / 2) < 0.8494)
+        order = (kmin >= 3.4e-308 ? 1 : 0) |
+                ((a.selfq || a.glo[e] >= 1e-290) &&
+                         a.Q.side[Q] * sqrt((double)D) * 0.8494 <= 1000.0 * s_h[slot] ? 2 : 0);
       }
     }
     a.dec[j] = kind | (order << 8);
@@ -1126,6 +1138,7 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     TravArgs a{};
     a.Q = view_of(qt);
     a.R = view_of(rt_);
+    a.selfq = &qt == &rt_ ? 1 : 0;
     a.D = D_;
     a.pmax = ser_.pmax;
     a.cost = cfg_.cost_model;
@@ -1179,7 +1192,7 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     CK(cudaMemsetAsync(L_.p, 0, sizeof(double) * KB * T, s));
     for (DevBuf<int>* b : { &Lord_, &cntF_, &cntDT_, &cntB_ })
       CK(cudaMemsetAsync(b->p, 0, sizeof(int) * KB, s));
-    hs->eps = cfg_.epsilon;
+    hs->eps = mufu_ ? cfg_.epsilon - kMufuCharge : cfg_.epsilon;  // MUFU exp's error is charged
     hs->ntot = (double)n_;
     hs->nslots = nb;
     hs->K = K;

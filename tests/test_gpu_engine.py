@@ -252,3 +252,25 @@ def test_base_case_tiles_exact(dfgtb, orc, d, leaf):
             approx = dfgtb.dfd_kde(qq, r, h, 0.0, leaf)
             exact = orc.naive_kde(qq, r, h)
             assert np.max(np.abs(approx - exact) / exact) <= 1e-13
+
+
+def test_mufu_exp_error_within_charge(dfgtb):
+    """The base case's MUFU exp (eps >= 1e-4): exhaustive max relative error over every
+    fixed-point argument (and the clamp beyond z = 1021), plus the fixed-point rounding
+    bound (D + 2) ln2 2^-22 at D = 5, stays below the 2e-6 the traversal charges."""
+    from paper_1102_2878_b200 import _capi
+    err = _capi.lib.dfgtb_mufu_exp_error()
+    assert 0.0 <= err < 1e-6
+    assert err + 7 * np.log(2.0) * 2.0 ** -22 < 2e-6
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_mufu_path_meets_eps(dfgtb, orc, k):
+    """eps = 0.01 runs the MUFU base case: per-query error within eps of the exact
+    sums at every sweep scale, and within 1e-5 of the FP64-exp engine's sums."""
+    import os
+    w = datagen.config(k, scale_n=0.03)
+    for s in w.scales:
+        h = s * w.h_s
+        got = dfgtb.dfgt_kde(w.refs, w.refs, h, dfgtb.EngineConfig(epsilon=0.01, leaf_threshold=32))
+        _check(got, orc.naive_kde(w.refs, w.refs, h), 0.01)
