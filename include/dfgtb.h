@@ -100,6 +100,10 @@ int dfgtb_last_stats(dfgtb_handle* h, dfgtb_stats* stats);
 int dfgtb_last_timings(dfgtb_handle* h, dfgtb_timings* t);
 int dfgtb_p_max(dfgtb_handle* h);
 
+/* Base-case exp of this handle: 1 = MUFU ex2 (epsilon >= 1e-4, error charged against
+ * epsilon), 0 = FP64 exp (<= ~1 ulp); -1 on a bad handle. */
+int dfgtb_base_exp_mode(dfgtb_handle* h);
+
 /* lkcv_from_sums + lscv_from_sums on Q = R sums computed on the device at h and
  * conv_h (cv.cpp:61-97; conv_h = 2h or sqrt(2)h, cv.cpp:27-30).  conv_h <= 0 skips
  * the least-squares score.  Sums never leave the device. */
@@ -143,6 +147,9 @@ int dfgtb_series_op(int op, size_t d, int p_max, const double* in, size_t n, con
 
 /* Measured FP64 FMA instruction throughput of the device (instr/s); bench roofline. */
 double dfgtb_dfma_peak(void);
+
+/* Measured MUFU ex2.approx.f32 throughput (ex2/s); roofline of the MUFU base case. */
+double dfgtb_ex2_peak(void);
 
 /* Max relative error of the base case's MUFU exp (used when epsilon >= 1e-4; its
  * bound is charged against epsilon) over every argument it can form; test entry. */

@@ -56,7 +56,7 @@ EXPORTS = (
     "dfgtb_last_timings",
     "dfgtb_p_max", "dfgtb_cv", "dfgtb_sweep", "dfgtb_lkcv_from_sums", "dfgtb_lscv_from_sums",
     "dfgtb_tree_nodes", "dfgtb_tree_height", "dfgtb_export_tree", "dfgtb_naive",
-    "dfgtb_series_op", "dfgtb_dfma_peak", "dfgtb_mufu_exp_error", "dfgtb_device_count", "dfgtb_release_cached_memory",
+    "dfgtb_series_op", "dfgtb_dfma_peak", "dfgtb_mufu_exp_error", "dfgtb_ex2_peak", "dfgtb_base_exp_mode", "dfgtb_device_count", "dfgtb_release_cached_memory",
     "dfgtb_stream",
     "dfgtb_launch_count", "dfgtb_last_error",
 )
@@ -92,6 +92,8 @@ def _load():
                                       _D]),
         "dfgtb_dfma_peak": (C.c_double, []),
         "dfgtb_mufu_exp_error": (C.c_double, []),
+        "dfgtb_ex2_peak": (C.c_double, []),
+        "dfgtb_base_exp_mode": (C.c_int, [V]),
         "dfgtb_device_count": (C.c_int, []),
         "dfgtb_release_cached_memory": (None, []),
         "dfgtb_stream": (C.c_size_t, [V]),

@@ -200,6 +200,8 @@ int dfgtb_last_timings(dfgtb_handle* h, dfgtb_timings* t)
 
 int dfgtb_p_max(dfgtb_handle* h) { return h && h->eng ? h->eng->p_max() : -1; }
 
+int dfgtb_base_exp_mode(dfgtb_handle* h) { return h && h->eng ? (h->eng->mufu_exp() ? 1 : 0) : -1; }
+
 // Batched CV: every bandwidth (and its convolution bandwidth) of `ns` scales goes
 // through ONE lock-step traversal; sums stay in HBM; CV partial sums come back.
 static void cv_rows(dfgtb_handle* h, const double* bws, const double* convs, int ns,
@@ -450,6 +452,17 @@ double dfgtb_dfma_peak(void)
     int dev = 0;
     CK(cudaGetDevice(&dev));
     v = measure_dfma_peak(dev);
+  });
+  return v;
+}
+
+double dfgtb_ex2_peak(void)
+{
+  double v = -1.0;
+  guard([&] {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    v = measure_ex2_peak(dev);
   });
   return v;
 }

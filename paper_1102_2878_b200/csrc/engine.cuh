@@ -50,10 +50,10 @@ constexpr int kMaxSlots = 64;  // bandwidths per batch
 // Base-case exp on the MUFU (ex2.approx.f32 on an exactly reduced argument, FP64
 // distance and accumulation): per-term relative error < kMufuCharge, which the
 // traversal pays for by running at eps - kMufuCharge.  Used when eps >= kMufuMinEps
-// (the charge is then <= 2% of the budget) unless DFGTB_EXACT_EXP is set; smaller eps
+// (the charge is then <= 4% of the budget) unless DFGTB_EXACT_EXP is set; smaller eps
 // keep the FP64 exp (<= ~1 ulp).
 constexpr double kMufuMinEps = 1e-4;
-constexpr double kMufuCharge = 2e-6;
+constexpr double kMufuCharge = 4e-6;
 
 int default_p_max(int D);
 
@@ -154,6 +154,8 @@ void naive_device(const double* d_q, size_t nq, const double* d_r, size_t nr, in
 
 // Measured FP64 FMA throughput (instr/s) -- roofline denominator for bench.py.
 double measure_dfma_peak(int device);
+// Measured MUFU ex2.approx.f32 throughput (ex2/s) -- the MUFU base case's roofline.
+double measure_ex2_peak(int device);
 // Max relative error of the base case's MUFU exp over every argument it can form.
 double mufu_exp_max_error();
 

@@ -397,35 +397,36 @@ __device__ __forceinline__ double exp_negy_c(double y, unsigned tabs)
 // eps - kMufuCharge so the per-term error below is paid for).
 // Coordinates are scaled by sqrt(log2 e) / (h sqrt 2) and centred on the chunk's first
 // query, so z = y log2 e = |q|^2 + |r|^2 - 2 q.r is formed in FP64 directly on top of
-// the fixed-point magic: t = M + b - 896 + z with M = 1.5 2^31 (ulp 2^-21), so the low
-// word of t is (z + b - 896) in signed 11.21 fixed point (b = kMufuBias units keeps
+// the fixed-point magic: t = M + b - 896 + z with M = 1.5 2^32 (ulp 2^-20), so the low
+// word of t is (z + b - 896) in signed 12.20 fixed point (b = kMufuBias units keeps
 // z + b >= 0 under the D + 2 roundings; 0 <= z <= 1021.4 on the fast path).  Then
-//   2^-z = 2^-n 2^-(f - b 2^-21),  n - 896 = lo >>a 21,  f = lo & (2^21 - 1),
+//   2^-z = 2^-n 2^-(f - b 2^-20),  (n - 896) << 20 = lo & 0xFFF00000,  f = lo & (2^20 - 1),
 // 2^-(f - b) by ex2.approx.ftz.f32 of an exact FP32 argument, and 2^-n spliced into the
 // exponent while widening to FP64 (hi = (G >> 3) - ((n - 896) << 20); n <= 1021 keeps
-// the result normal).  Per-term relative error <= (D + 2) ln2 2^-22 (fixed-point
+// the result normal).  Per-term relative error <= (D + 2) ln2 2^-21 (fixed-point
 // rounding) + ex2.approx's error (exhaustively measured by the tests over every
 // reachable argument).
 constexpr int kMufuBias = 4;
-constexpr unsigned kMufuHi = 0x41E80000u;    // high word of t for 896 - b <= z < 1920
+constexpr unsigned kMufuHi = 0x41F80000u;    // high word of t for 896 - b <= z < 4992
 template <bool CLAMP = false>
-__device__ __forceinline__ double exp2_neg_fixed(double t)
+__device__ __forceinline__ double exp2_neg_fixed(double t, unsigned fbits)
 {
   int lo = __double2loint(t);
   if constexpr (CLAMP) {  // z > 1021 -> 2^-1021 (only where the traversal pays for it)
     const unsigned hi = (unsigned)__double2hiint(t);  // kMufuHi - 1 below z = 896 - b
-    const int lmax = (125 << 21) | 0x1FFFFF;
+    const int lmax = (125 << 20) | 0xFFFFF;
     lo = hi > kMufuHi || (hi == kMufuHi && (unsigned)lo > (unsigned)lmax) ? lmax : lo;
   }
-  const float x = __uint_as_float(((unsigned)lo & 0x1FFFFFu) | 0x4B000000u);  // 2^23 + f
-  const float a = fmaf(x, -0x1p-21f, 4.0f + kMufuBias * 0x1p-21f);           // (b - f) 2^-21, exact
+  // fbits = 0x4B000000 held in a register (one LOP3: (lo & mask) | fbits)
+  const float x = __uint_as_float(((unsigned)lo & 0xFFFFFu) | fbits);  // 2^23 + f
+  const float a = fmaf(x, -0x1p-20f, 8.0f + kMufuBias * 0x1p-20f);     // (b - f) 2^-20, exact
   float g;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(a));
   const unsigned G = __float_as_uint(g);
-  const unsigned hi = (G >> 3) - ((unsigned)(lo >> 1) & 0xFFF00000u);
+  const unsigned hi = (G >> 3) - ((unsigned)lo & 0xFFF00000u);
   return __hiloint2double((int)hi, (int)(G << 29));
 }
-constexpr double kMufuMagic = 3221225472.0 - 896.0 + kMufuBias * 0x1p-21;  // M - 896 + b 2^-21
+constexpr double kMufuMagic = 6442450944.0 - 896.0 + kMufuBias * 0x1p-20;  // M - 896 + b 2^-20
 constexpr double kSqrtLog2e = 1.2011224087864498;                           // sqrt(log2 e)
 constexpr double kLn2 = 0.6931471805599453;
 
@@ -634,6 +635,8 @@ __device__ __forceinline__ void base_group_mufu(const double* rs, int n, const d
   }
   // the G chains of a reference point are written stage by stage (independent
   // instructions back to back) so the warp always has work while one chain waits
+  unsigned fbits;
+  asm volatile("mov.b32 %0, 0x4B000000;" : "=r"(fbits));  // opaque: stays in a register
   auto body = [&](int j) {
     double r[DM];
     MPt<DT>::load(rs, j, r);
@@ -645,11 +648,13 @@ __device__ __forceinline__ void base_group_mufu(const double* rs, int n, const d
 #pragma unroll
       for (int i = 0; i < GG; ++i) t[i] = fma(m[i][d], r[d], t[i]);
 #pragma unroll
-    for (int i = 0; i < GG; ++i) acc[i] += exp2_neg_fixed<CLAMP>(t[i]);
+    for (int i = 0; i < GG; ++i) acc[i] += exp2_neg_fixed<CLAMP>(t[i], fbits);
   };
-  const int nceil = (n + 31) & ~31;
-  for (int j = lane; j < nceil; j += 32)
-    if (j < n) body(j);
+  // full 32-blocks without a predicate, then the partial last block
+  const int nfull = n & ~31;
+  int j = lane;
+  for (; j < nfull; j += 32) body(j);
+  if (j < n) body(j);
 #pragma unroll
   for (int s = 0; s < LG; ++s) {
     const int off = 16 >> s;
@@ -1476,23 +1481,23 @@ void naive_device(const double* d_q, size_t nq, const double* d_r, size_t nr, in
 }
 
 // Exhaustive error of exp2_neg_fixed over every fixed-point argument the fast base
-// case can form: t = M - 896 + u 2^-21 for every u in [0, 1022 2^21), value
-// 2^-(u - b) 2^-21, against libdevice exp2 in FP64; and of the clamped variant beyond
+// case can form: t = M - 896 + u 2^-20 for every u in [0, 1022 2^20), value
+// 2^-(u - b) 2^-20, against libdevice exp2 in FP64; and of the clamped variant beyond
 // z = 1021 (value 2^-(1021 + f)).  Max relative error as ordered bits in *out.
 __global__ void k_mufu_check(unsigned long long* out)
 {
   unsigned long long worst = 0;
-  const unsigned long long nz = 1022ull << 21;
+  const unsigned long long nz = 1022ull << 20;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-       i < nz + (4ull << 21); i += (unsigned long long)gridDim.x * blockDim.x) {
-    const double t = (kMufuMagic - kMufuBias * 0x1p-21) + (double)i * 0x1p-21;
+       i < nz + (4ull << 20); i += (unsigned long long)gridDim.x * blockDim.x) {
+    const double t = (kMufuMagic - kMufuBias * 0x1p-20) + (double)i * 0x1p-20;
     double got, want;
     if (i < nz) {
-      got = exp2_neg_fixed<false>(t);
-      want = exp2(-((double)i - kMufuBias) * 0x1p-21);
+      got = exp2_neg_fixed<false>(t, 0x4B000000u);
+      want = exp2(-((double)i - kMufuBias) * 0x1p-20);
     } else {  // clamp: any z >= 1022 - b -> 2^-(1021 + frac of the clamp point)
-      got = exp2_neg_fixed<true>(t + 4096.0 * (double)(i & 7));
-      want = exp2(-((double)((125u << 21) | 0x1FFFFFu) + (896u << 21) - kMufuBias) * 0x1p-21);
+      got = exp2_neg_fixed<true>(t + 8192.0 * (double)(i & 7), 0x4B000000u);
+      want = exp2(-((double)((125u << 20) | 0xFFFFFu) + (896u << 20) - kMufuBias) * 0x1p-20);
     }
     const double rel = fabs(got - want) / want;
     const unsigned long long b = (unsigned long long)__double_as_longlong(rel);
@@ -1517,6 +1522,44 @@ double mufu_exp_max_error()
   double v;
   std::memcpy(&v, &b, sizeof(v));
   return v;
+}
+
+__global__ void k_ex2_peak(float* out, int iters)
+{
+  float a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = -0.001f * (threadIdx.x + k);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[k]));
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 42.0f) out[0] = s;
+}
+
+// Measured MUFU.EX2 throughput (ex2/s): the MUFU base case's roofline denominator.
+double measure_ex2_peak(int device)
+{
+  cudaDeviceProp p{};
+  CK(cudaGetDeviceProperties(&p, device));
+  DevBuf<float> o;
+  o.reserve(1);
+  const int blocks = p.multiProcessorCount * 8, threads = 256, iters = 4096;
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  k_ex2_peak<<<blocks, threads>>>(o.p, 64);
+  CK(cudaEventRecord(a));
+  k_ex2_peak<<<blocks, threads>>>(o.p, iters);
+  CK(cudaEventRecord(b));
+  CK(cudaEventSynchronize(b));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return (double)blocks * threads * iters * 8.0 / (ms * 1e-3);
 }
 
 double measure_dfma_peak(int device)
