@@ -122,13 +122,12 @@ private:
   DevBuf<double> pkmax_, pkmin_;
   DevBuf<int> dec_, childlen_;
   DevBuf<double> newbase_, pglo_;
-  DevBuf<Cnt> cnt_, cntoff_, ctsum_, ctoff_;
+  DevBuf<Cnt> cnt_, cntoff_, ctsum_, ctoff_, lvlcnt_;
   DevBuf<Item> itF_, itDT_, itB_, sF_, sDT_, sB_;
   DevBuf<unsigned char> scan_tmp_;
   DevBuf<double> red_;
   DevBuf<unsigned long long> trace_;  // DFGTB_TRACE=1: per-level phase timestamps
-  DevBuf<unsigned long long> tflag_;  // look-back status words of the persistent traversal
-  unsigned int epoch_ = 0;
+  DevBuf<unsigned long long> lvlep_;  // per-level packed entry/pair counters (traversal)
   // device-driven level loop: state (device + pinned host mirror), capacities, graph
   void* hst_ = nullptr;
   size_t hst_bytes_ = 0;

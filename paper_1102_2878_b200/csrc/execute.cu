@@ -588,22 +588,23 @@ __device__ __forceinline__ void base_group(const double* rs, int n, const double
 template <int DT>
 struct MPt {
   static constexpr int DM = (DT + 2) / 2 * 2;  // D coordinates + |r|^2, padded to 16 bytes
+  static constexpr int PL = BaseGeo<DT>::RMAX * 2;  // stream: DM / 2 planes of double2
+  // stream point j: plane k holds its elements (2k, 2k+1) -- 16-byte lane stride, so a
+  // warp's LDS.128 of 32 consecutive points is conflict-free
   __device__ __forceinline__ static void load(const double* base, int j, double (&v)[DM])
   {
-    const double2* b2 = reinterpret_cast<const double2*>(base + (size_t)j * DM);
 #pragma unroll
     for (int k = 0; k < DM / 2; ++k) {
-      const double2 t = b2[k];
+      const double2 t = reinterpret_cast<const double2*>(base + k * PL)[j];
       v[2 * k] = t.x;
       v[2 * k + 1] = t.y;
     }
   }
   // point j of src (stride DP, log2e-scaled coordinates) -> centred on c, |r|^2
-  __device__ __forceinline__ static void stage(const double* src, int j, const double* c, double* dst,
-                                               int j2)
+  __device__ __forceinline__ static void centred(const double* src, int j, const double* c,
+                                                 double (&v)[DM])
   {
     constexpr int DP = PtLoad<DT>::DP;
-    double v[DM];
     double rr = 0.0;
 #pragma unroll
     for (int d = 0; d < DT; ++d) {
@@ -613,9 +614,25 @@ struct MPt {
     v[DT] = rr;
 #pragma unroll
     for (int d = DT + 1; d < DM; ++d) v[d] = 0.0;
-    double2* d2 = reinterpret_cast<double2*>(dst + (size_t)j2 * DM);
+  }
+  __device__ __forceinline__ static void stage(const double* src, int j, const double* c, double* dst,
+                                               int j2)
+  {
+    double v[DM];
+    centred(src, j, c, v);
 #pragma unroll
-    for (int k = 0; k < DM / 2; ++k) d2[k] = make_double2(v[2 * k], v[2 * k + 1]);
+    for (int k = 0; k < DM / 2; ++k)
+      reinterpret_cast<double2*>(dst + k * PL)[j2] = make_double2(v[2 * k], v[2 * k + 1]);
+  }
+  // query tile (broadcast reads): point-major, stride DM
+  __device__ __forceinline__ static void stage_q(const double* src, int j, const double* c,
+                                                 double* dst)
+  {
+    double v[DM];
+    centred(src, j, c, v);
+#pragma unroll
+    for (int k = 0; k < DM / 2; ++k)
+      reinterpret_cast<double2*>(dst + (size_t)j * DM)[k] = make_double2(v[2 * k], v[2 * k + 1]);
   }
 };
 
@@ -782,7 +799,7 @@ __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
 #pragma unroll
     for (int d = 0; d < DT; ++d) cq[d] = qsrc[d];
     if (lane < qc) {
-      if (mf) MPt<DT>::stage(qsrc, lane, cq, qs, lane);
+      if (mf) MPt<DT>::stage_q(qsrc, lane, cq, qs);
       else PtLoad<DT>::copy(qsrc, lane, qs);
     }
     qsum[lane] = 0.0;

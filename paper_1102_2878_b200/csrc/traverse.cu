@@ -129,6 +129,7 @@ __device__ void dev_choose(double nq, double nr, double sq, double sr, double h,
 // the level loop needs no host round trip.  Capacities are checked before anything
 // is written; on overflow the loop stops and the host regrows the buffers and reruns.
 enum SlotStat { sPairs = 0, sFD, sF, sD, sT, sB, sKev, sNStat };
+constexpr int kMaxLevels = 1024;
 struct TravState {
   double eps, ntot;                    // per batch (host)
   int nslots, K;
@@ -139,7 +140,6 @@ struct TravState {
   int nF, nDT, nB;                     // items emitted so far
   int overflow, levels;
   int done;                            // CTAs finished with their tile sum (unused)
-  unsigned int epoch;                  // per launch: tags the look-back status words
   Cnt lvl;                             // totals of the current level
   unsigned long long sst[kMaxSlots][sNStat];  // per-slot TraversalStats
 };
@@ -163,7 +163,8 @@ struct TravArgs {
   Item *itF, *itDT, *itB;
   int *cntF, *cntDT, *cntB;
   unsigned long long* trace;  // optional per-phase %globaltimer stamps (DFGTB_TRACE)
-  unsigned long long* tflag;  // look-back status words, one per CTA of k_traverse
+  Cnt* lvlcnt;                // per-level output counters of k_traverse (zeroed per launch)
+  unsigned long long* lvlep;  // per-level packed (entries << 32 | pairs) counters
 };
 
 __device__ __forceinline__ Cnt ldcg_cnt(const Cnt* p)
@@ -544,86 +545,12 @@ __global__ void k_advance(const __grid_constant__ TravArgs a, cudaGraphCondition
   if (use_cond) cudaGraphSetConditional(hc, more ? 1u : 0u);
 }
 
-// Decoupled look-back over the CTAs of k_traverse (single-pass scan of the per-CTA
-// level counts).  Status words carry (epoch, level) so stale words of earlier levels
-// or launches read as "not yet published"; flag 1 = aggregate, 2 = inclusive prefix.
-__device__ __forceinline__ void st_flag(unsigned long long* p, unsigned long long v)
-{
-  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_flag(const unsigned long long* p)
-{
-  unsigned long long v;
-  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ Cnt warp_sum_cnt(Cnt v)
-{
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    v.e += __shfl_xor_sync(0xffffffffu, v.e, o);
-    v.p += __shfl_xor_sync(0xffffffffu, v.p, o);
-    v.f += __shfl_xor_sync(0xffffffffu, v.f, o);
-    v.dt += __shfl_xor_sync(0xffffffffu, v.dt, o);
-    v.t += __shfl_xor_sync(0xffffffffu, v.t, o);
-    v.b += __shfl_xor_sync(0xffffffffu, v.b, o);
-    v.fd += __shfl_xor_sync(0xffffffffu, v.fd, o);
-  }
-  return v;
-}
-
-// Called by one whole warp; returns the exclusive prefix of tile b (valid in all
-// lanes).  The warp inspects 32 predecessors at a time: it waits until all of them
-// have published, then sums aggregates down to the nearest inclusive prefix.
-__device__ Cnt lookback(const TravArgs& a, int b, const Cnt& agg, unsigned long long tag, int lane)
-{
-  if (b == 0) {
-    if (lane == 0) {
-      a.toff[0] = agg;  // inclusive prefix of tile 0
-      __threadfence();
-      st_flag(a.tflag, tag | 2);
-    }
-    return Cnt{};
-  }
-  if (lane == 0) {
-    a.tsum[b] = agg;
-    __threadfence();
-    st_flag(a.tflag + b, tag | 1);
-  }
-  Cnt excl{};
-  for (int top = b - 1;; top -= 32) {
-    const int j = top - lane;  // lane 0 = nearest predecessor
-    unsigned long long f = 0;
-    if (j >= 0) {
-      do {
-        f = ld_flag(a.tflag + j);
-      } while ((f & ~3ull) != tag);
-    }
-    __threadfence();
-    const unsigned inc = __ballot_sync(0xffffffffu, j >= 0 && (f & 3) == 2);
-    const int stop = inc ? __ffs(inc) - 1 : 32;  // nearest inclusive predecessor
-    Cnt v{};
-    if (j >= 0 && lane < stop) v = ldcg_cnt(a.tsum + j);
-    if (lane == stop) v = ldcg_cnt(a.toff + j);
-    excl = CntSum()(excl, warp_sum_cnt(v));
-    if (inc) break;
-  }
-  if (lane == 0) {
-    a.toff[b] = CntSum()(excl, agg);
-    __threadfence();
-    st_flag(a.tflag + b, tag | 2);
-  }
-  return excl;
-}
-
 // The whole level loop in ONE cooperative launch (one CTA per SM).  Each level is a
-// single phase: CTA b owns a contiguous range of frontier entries; its warps classify
-// them, the CTA scans its counts, learns its global offset by a decoupled look-back
-// over the preceding CTAs, and emits its entries -- then ONE grid-wide barrier makes
-// the next frontier visible.  The last CTA publishes the level totals and the
-// capacity verdict.  Every CTA advances an identical private copy of (cur, m, item
-// offsets); CTA 0 writes the state back at the end.
+// single phase: CTA b owns a contiguous, pair-balanced range of frontier entries; it
+// classifies them, scans its counts, claims its output space with one atomic per
+// counter on the level's totals, and emits -- then ONE grid-wide barrier makes the
+// next frontier and the totals visible.  Every CTA advances an identical private copy
+// of (cur, m, item offsets) and checks capacity itself; CTA 0 writes the state back.
 #ifndef KPBLOCK
 #define KPBLOCK 1024
 #endif
@@ -837,7 +764,6 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
   __shared__ Cnt s_agg, s_excl;
   __shared__ double s_h[kMaxSlots], s_scale[kMaxSlots];
   __shared__ unsigned long long s_sst[kMaxSlots][sNStat];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int G = gridDim.x;
   const int K = st.K, nslots = st.nslots;
   for (int i = threadIdx.x; i < kMaxSlots * sNStat; i += kPBlock) (&s_sst[0][0])[i] = 0;
@@ -846,7 +772,6 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
     s_scale[i] = st.scale[i];
   }
   __syncthreads();
-  const unsigned long long epoch = (unsigned long long)st.epoch << 32;
   int cur = 0, m = nslots, p = nslots, gF = 0, gDT = 0, gB = 0, levels = 0;
   for (;;) {
     if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && levels < 512) {
@@ -873,17 +798,22 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
     const Cnt agg0 = BR(tmp.r).Reduce(acc, CntSum());
     if (threadIdx.x == 0) s_agg = agg0;
     __syncthreads();
-    if (wib == 0) {
-      const Cnt agg = s_agg;
-      const Cnt ex = lookback(a, blockIdx.x, agg, epoch | ((unsigned long long)levels << 2), lane);
-      if (lane == 0) {
-        s_excl = ex;
-        if (blockIdx.x == G - 1) {
-          const Cnt tot = CntSum()(ex, agg);
-          st.lvl = tot;
-          st.overflow = over_capacity(st, tot, gF, gDT, gB);
-        }
-      }
+    // the CTA's output offsets: one atomic per counter on the level's totals.  The
+    // order in which CTAs claim space only permutes the next frontier; work items carry
+    // their per-key rank and are counting-sorted by (key, rank) afterwards, so every
+    // result stays bit-reproducible.
+    // Entries and their pairs are claimed by ONE 64-bit atomic on the packed (e, p)
+    // totals, so pair offsets grow with entry index (entry_bounds relies on it).
+    if (threadIdx.x == 0) {
+      const unsigned long long v =
+        ((unsigned long long)(unsigned)s_agg.e << 32) | (unsigned)s_agg.p;
+      const unsigned long long o = v ? atomicAdd(&a.lvlep[levels], v) : 0ull;
+      s_excl.e = (int)(o >> 32);
+      s_excl.p = (int)(o & 0xffffffffu);
+    } else if (threadIdx.x < 6) {
+      const int k = threadIdx.x + 1;  // f, dt, t, b, fd
+      const int v = (&s_agg.e)[k];
+      (&s_excl.e)[k] = v ? atomicAdd(&a.lvlcnt[levels].e + k, v) : 0;
     }
     __syncthreads();
     if (a.trace && blockIdx.x == G - 1 && threadIdx.x == 0 && levels < 512) {
@@ -915,8 +845,19 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
       a.trace[levels * 4 + 2] = t;
       a.trace[(levels + 1) * 4 + 3] = t;
     }
-    const Cnt lv = ldcg_cnt(&st.lvl);
-    if (__ldcg(&st.overflow)) break;
+    Cnt lv = ldcg_cnt(&a.lvlcnt[levels]);
+    {
+      const unsigned long long ep = __ldcg(&a.lvlep[levels]);
+      lv.e = (int)(ep >> 32);
+      lv.p = (int)(ep & 0xffffffffu);
+    }
+    if (over_capacity(st, lv, gF, gDT, gB)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st.lvl = lv;
+        st.overflow = 1;
+      }
+      break;
+    }
     gF += lv.f;
     gDT += lv.dt;
     gB += lv.b;
@@ -925,6 +866,10 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
     p = lv.p;
     ++levels;
     if (m == 0) break;
+    if (levels == kMaxLevels) {  // deeper than any kd-tree pair can go; report, don't spin
+      if (blockIdx.x == 0 && threadIdx.x == 0) st.overflow = 2;
+      break;
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < nslots * sNStat; i += kPBlock) {
@@ -1171,11 +1116,12 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     a.cntF = cntF_.p;
     a.cntDT = cntDT_.p;
     a.cntB = cntB_.p;
-    if (!tflag_.p) {
-      tflag_.reserve(kScanTiles);
-      CK(cudaMemsetAsync(tflag_.p, 0, sizeof(unsigned long long) * kScanTiles, s));
-    }
-    a.tflag = tflag_.p;
+    lvlcnt_.reserve(kMaxLevels);
+    CK(cudaMemsetAsync(lvlcnt_.p, 0, sizeof(Cnt) * kMaxLevels, s));
+    a.lvlcnt = lvlcnt_.p;
+    lvlep_.reserve(kMaxLevels);
+    CK(cudaMemsetAsync(lvlep_.p, 0, sizeof(unsigned long long) * kMaxLevels, s));
+    a.lvlep = lvlep_.p;
     static const bool tracing = std::getenv("DFGTB_TRACE") != nullptr;
     if (tracing) {
       trace_.reserve(512 * 6);
@@ -1205,7 +1151,6 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     hs->capF = capF_;
     hs->capDT = capDT_;
     hs->capB = capB_;
-    hs->epoch = ++epoch_;  // never 0: zeroed status words read as unpublished
     CK(cudaMemcpyAsync(ds, hs, sizeof(TravState), cudaMemcpyHostToDevice, s));
     k_trav_init<<<1, 64, 0, s>>>(a);
     CK_LAUNCH();
@@ -1222,6 +1167,7 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
                      L, tr[2048 + L * 2], tr[2048 + L * 2 + 1], (tr[L * 4 + 1] - tr[L * 4]) * 1e-3,
                      (tr[L * 4 + 2] - tr[L * 4 + 1]) * 1e-3);
     }
+    if (hs->overflow == 2) throw CudaError("traversal exceeded 1024 levels");
     if (!hs->overflow) break;
     if (attempt > 10) throw OutOfMemory("traversal buffers keep overflowing");
     const Cnt l = hs->lvl;
