@@ -82,15 +82,43 @@ __global__ void k_moment_chunks(DevSeries g, TreeView R, const int* cnode, const
   }
 }
 
-__global__ void k_moment_reduce(DevSeries g, int nodes, const int* coff, const double* part,
-                                double* M)
+// One CTA per node: thread (term i, stripe k) sums chunks c = c0 + k, c0 + k + S, ...
+// (8 loads in flight), then the S stripe sums are added in stripe order: a fixed
+// summation order, latency ~count/(8 S) round trips instead of count.
+constexpr int kMomRedThreads = 256;
+__global__ void __launch_bounds__(kMomRedThreads) k_moment_reduce(DevSeries g, int nodes,
+                                                                  const int* coff,
+                                                                  const double* part, double* M)
 {
-  for (int n = blockIdx.x; n < nodes; n += gridDim.x)
-    for (int i = threadIdx.x; i < g.T; i += blockDim.x) {
+  __shared__ double red[kMomRedThreads];
+  const int T = g.T;
+  const int S = T <= kMomRedThreads ? kMomRedThreads / T : 1;
+  for (int n = blockIdx.x; n < nodes; n += gridDim.x) {
+    const int c0 = coff[n], c1 = coff[n + 1];
+    for (int i0 = 0; i0 < T; i0 += kMomRedThreads / S) {
+      const int i = i0 + threadIdx.x % (kMomRedThreads / S), k = threadIdx.x / (kMomRedThreads / S);
       double acc = 0.0;
-      for (int c = coff[n]; c < coff[n + 1]; ++c) acc += part[(size_t)c * g.T + i];
-      M[(size_t)n * g.T + g.pos[i]] = acc * g.invf[i];
+      if (i < T && k < S) {
+        int c = c0 + k;
+        for (; c + 7 * S < c1; c += 8 * S) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = part[(size_t)(c + u * S) * T + i];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc += v[u];
+        }
+        for (; c < c1; c += S) acc += part[(size_t)c * T + i];
+      }
+      red[threadIdx.x] = acc;
+      __syncthreads();
+      if (k == 0 && i < T) {
+        double sum = 0.0;
+        for (int kk = 0; kk < S; ++kk) sum += red[kk * (kMomRedThreads / S) + threadIdx.x];
+        M[(size_t)n * T + g.pos[i]] = sum * g.invf[i];
+      }
+      __syncthreads();
     }
+  }
 }
 
 // --------------------------------------------------- D / T items (local expansions)
@@ -225,31 +253,57 @@ __global__ void __launch_bounds__(kLocThreads) k_local_chunks_t(DevSeries g, Tre
   }
 }
 
-__global__ void k_local_reduce(DevSeries g, int keys, const int* cnt, const int* off,
+// One warp per query-node key that has D/T items (launched over the sorted items; the
+// warp of a key's first item does the work), lanes over terms.  Every term sums its
+// chunks in item order (8 loads in flight), so the result does not depend on the
+// launch shape.
+__global__ void k_local_reduce(DevSeries g, int nitems, const int* cnt, const int* off,
                                const Item* items, const int* choff, const double* part, double* L,
                                int* Lord)
 {
-  for (int n = blockIdx.x; n < keys; n += gridDim.x) {
-    const int c = cnt[n];
-    if (!c) continue;
-    const int i0 = off[n], i1 = i0 + c;
-    int ord = 0;
-    for (int k = i0; k < i1; ++k) ord = max(ord, items[k].code & 0xff);
-    const int nt = ipow_i(ord, g.D);
-    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
-      const uint64_t a = g.dig[t];
-      int mx = 0;
-      for (int d = 0; d < g.D; ++d) mx = max(mx, digit_of(a, d));
-      double acc = 0.0;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= nitems) return;
+  const int n = items[i].key;
+  const int i0 = off[n];
+  if (i != i0) return;  // not the first item of its key
+  const int i1 = i0 + cnt[n];
+  int ord = 0, omin = 1 << 20;
+  for (int k = i0 + lane; k < i1; k += 32) {
+    ord = max(ord, items[k].code & 0xff);
+    omin = min(omin, items[k].code & 0xff);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    ord = max(ord, __shfl_xor_sync(0xffffffffu, ord, o));
+    omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, o));
+  }
+  const int q0 = choff[i0], q1 = choff[i1];
+  const int nt = ipow_i(ord, g.D);
+  for (int t = lane; t < nt; t += 32) {
+    const uint64_t a = g.dig[t];
+    int mx = 0;
+    for (int d = 0; d < g.D; ++d) mx = max(mx, digit_of(a, d));
+    double acc = 0.0;
+    if (mx >= omin) {  // a term some item does not carry: walk the items
       for (int k = i0; k < i1; ++k) {
         if (mx >= (items[k].code & 0xff)) continue;  // term beyond this item's order
         for (int q = choff[k]; q < choff[k + 1]; ++q) acc += part[(size_t)q * g.T + t];
       }
-      const double sg = (g.degree[t] & 1) ? -1.0 : 1.0;
-      L[(size_t)n * g.T + t] += sg * g.invf[t] * acc;
+    } else {  // every item carries the term: its chunks are one contiguous run
+      int q = q0;
+      for (; q + 8 <= q1; q += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = part[(size_t)(q + u) * g.T + t];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += v[u];
+      }
+      for (; q < q1; ++q) acc += part[(size_t)q * g.T + t];
     }
-    if (threadIdx.x == 0 && Lord[n] < ord) Lord[n] = ord;
+    const double sg = (g.degree[t] & 1) ? -1.0 : 1.0;
+    L[(size_t)n * g.T + t] += sg * g.invf[t] * acc;
   }
+  if (lane == 0 && Lord[n] < ord) Lord[n] = ord;
 }
 
 // Top-down L2L of one depth level for every slot (post_process, engine.cpp:294-304).
@@ -1242,7 +1296,7 @@ void Engine::eager_moments()
   k_moment_chunks<<<std::min(nch, 148 * 16), 128, smem, s_>>>(g, view_of(t), dn.p, ds.p, nch,
                                                                part.p);
   CK_LAUNCH();
-  k_moment_reduce<<<std::min(K, 148 * 16), 128, 0, s_>>>(g, K, dof.p, part.p, Mt_.p);
+  k_moment_reduce<<<std::min(K, 148 * 8), kMomRedThreads, 0, s_>>>(g, K, dof.p, part.p, Mt_.p);
   CK_LAUNCH();
   CK(cudaStreamSynchronize(s_));
 }
@@ -1346,8 +1400,8 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
       k_local_chunks<<<gl, 64, smem, s>>>(g, Q, R, K, sDT_.p, ch, nch, Mt_.p, sv, lpart_.p);
 #undef LOC_T
     CK_LAUNCH();
-    k_local_reduce<<<std::min(KB, 148 * 16), 64, 0, s>>>(g, KB, cntDT_.p, offDT_.p, sDT_.p,
-                                                         lchoff_.p, lpart_.p, L_.p, Lord_.p);
+    k_local_reduce<<<ceil_div(nDT_, 8), 256, 0, s>>>(g, (int)nDT_, cntDT_.p, offDT_.p, sDT_.p,
+                                                     lchoff_.p, lpart_.p, L_.p, Lord_.p);
     CK_LAUNCH();
   }
   if (cfg_.local_pushdown == 1 && nLoc > 0) {
