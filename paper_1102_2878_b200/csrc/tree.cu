@@ -17,12 +17,16 @@
 // preorder ids at the end.
 #include "tree.cuh"
 
+#include <cooperative_groups.h>
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 
 namespace dfgtb {
+namespace cg = cooperative_groups;
 namespace {
 
 constexpr int kTile = 1024;
@@ -374,12 +378,355 @@ __global__ void k_iota(int* p, int n)
   if (i < n) p[i] = i;
 }
 
+// ------------------------------------------------------------------------------
+// Persistent build: every level in ONE cooperative launch (one CTA per SM), node
+// bookkeeping on the device, no host round trip per level.  Same arithmetic and the
+// same partition / nth_element semantics as the per-level kernels above; six grid
+// barriers per level:
+//   A bounds (ordered-key atomics)  | B decide  | C flags + chunk scans  |
+//   D P and child ids               | E slots + one-sided fallback  | F swaps + next seg
+// Positions are statically chunked over the CTAs (C scans its chunk locally, D adds
+// the preceding chunks' totals), so the prefix P and the BFS child ids are exactly
+// those of a sequential scan.
+constexpr int kPB = 1024;        // threads per CTA of k_build
+constexpr int kMaxTreeLevels = 256;
+
+struct BuildArgs {
+  const double* x;
+  int n, D, leaf;
+  int *perm, *seg, *flag, *P, *slot;
+  int *nbeg, *ncnt, *nleft, *nright, *npar, *ndep;  // BFS node ids
+  double *blo, *bhi, *bcen, *bside, *bsc;
+  int* bsd;
+  unsigned long long *kmin, *kmax;  // per level node * D
+  double* mid;                      // per level node
+  int *dosplit, *child, *lc;        // per level node
+  int* ctot;                        // 2 * gridDim.x chunk totals
+  int* lvl;                         // [0] = levels, [1..] = level base offsets
+};
+
+__device__ __forceinline__ void chunk_of(int total, int b, int G, int& lo, int& hi)
+{
+  lo = (int)((long long)total * b / G);
+  hi = (int)((long long)total * (b + 1) / G);
+}
+
+__global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildArgs a)
+{
+  cg::grid_group grid = cg::this_grid();
+  using BS = cub::BlockScan<int, kPB>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ int s_carry;
+  const int G = gridDim.x, bid = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const int n = a.n, D = a.D;
+  const size_t gt = (size_t)bid * kPB + tid, gs = (size_t)G * kPB;
+  for (size_t i = gt; i < (size_t)n; i += gs) {
+    a.perm[i] = (int)i;
+    a.seg[i] = 0;
+  }
+  for (size_t i = gt; i < (size_t)D; i += gs) {
+    a.kmin[i] = ~0ull;
+    a.kmax[i] = 0ull;
+  }
+  if (gt == 0) {
+    a.nbeg[0] = 0;
+    a.ncnt[0] = n;
+    a.npar[0] = -1;
+    a.ndep[0] = 0;
+  }
+  int p0, p1;
+  chunk_of(n, bid, G, p0, p1);
+  int base = 0, m = 1, level = 0;
+  grid.sync();
+  for (;;) {
+    if (gt == 0) a.lvl[1 + level] = base;
+    // A: exact bounds of every level node
+    for (int i0 = p0; i0 < p1; i0 += kPB) {
+      const int i = i0 + tid;
+      const int j = i < p1 ? a.seg[i] : -1;
+      const int j0 = __shfl_sync(0xffffffffu, j, 0);
+      const bool uni = __all_sync(0xffffffffu, j == j0) && j0 >= 0;
+      for (int d = 0; d < D; ++d) {
+        const unsigned long long k = j >= 0 ? dkey(a.x[(size_t)a.perm[i] * D + d]) : 0ull;
+        if (uni) {
+          unsigned long long mn = k, mx = k;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          }
+          if (lane == 0) {
+            atomicMin(&a.kmin[(size_t)j0 * D + d], mn);
+            atomicMax(&a.kmax[(size_t)j0 * D + d], mx);
+          }
+        } else if (j >= 0) {
+          atomicMin(&a.kmin[(size_t)j * D + d], k);
+          atomicMax(&a.kmax[(size_t)j * D + d], k);
+        }
+      }
+    }
+    grid.sync();
+    // B: bounds, centroid, widest side, split midpoint (kdtree.cpp:49-78)
+    for (size_t jj = gt; jj < (size_t)m; jj += gs) {
+      const int j = (int)jj;
+      const size_t o = (size_t)(base + j) * D;
+      int widest = 0;
+      double width = 0.0;
+      for (int d = 0; d < D; ++d) {
+        const double l = dkey_inv(a.kmin[(size_t)j * D + d]);
+        const double h = dkey_inv(a.kmax[(size_t)j * D + d]);
+        a.blo[o + d] = l;
+        a.bhi[o + d] = h;
+        a.bcen[o + d] = __dmul_rn(0.5, __dadd_rn(l, h));
+        const double w = __dadd_rn(h, -l);
+        if (d == 0 || w > width) {
+          width = w;
+          widest = d;
+        }
+      }
+      a.bside[base + j] = width;
+      const int split = a.ncnt[base + j] > a.leaf;
+      a.dosplit[j] = split;
+      a.bsd[base + j] = split ? widest : -1;
+      a.mid[j] = a.bcen[o + widest];
+    }
+    grid.sync();
+    // C: predicate flags and the CTA's chunk scans (positions; splitting level nodes)
+    {
+      if (tid == 0) s_carry = 0;
+      __syncthreads();
+      for (int i0 = p0; i0 < p1; i0 += kPB) {
+        const int i = i0 + tid;
+        int f = 0;
+        if (i < p1) {
+          const int j = a.seg[i];
+          if (j >= 0 && a.dosplit[j])
+            f = a.x[(size_t)a.perm[i] * D + a.bsd[base + j]] <= a.mid[j] ? 1 : 0;
+          a.flag[i] = f;
+        }
+        int ex, agg;
+        BS(tmp).ExclusiveSum(f, ex, agg);
+        if (i < p1) a.P[i] = s_carry + ex;  // chunk-local exclusive prefix
+        __syncthreads();
+        if (tid == 0) s_carry += agg;
+        __syncthreads();
+      }
+      if (tid == 0) a.ctot[bid] = s_carry;
+      int n0, n1;
+      chunk_of(m, bid, G, n0, n1);
+      if (tid == 0) s_carry = 0;
+      __syncthreads();
+      for (int j0 = n0; j0 < n1; j0 += kPB) {
+        const int j = j0 + tid;
+        const int f = j < n1 ? a.dosplit[j] : 0;
+        int ex, agg;
+        BS(tmp).ExclusiveSum(f, ex, agg);
+        if (j < n1) a.child[j] = s_carry + ex;  // chunk-local rank among splitting nodes
+        __syncthreads();
+        if (tid == 0) s_carry += agg;
+        __syncthreads();
+      }
+      if (tid == 0) a.ctot[G + bid] = s_carry;
+    }
+    grid.sync();
+    // D: global prefix P, child BFS ids and the children's records
+    int poff = 0, noff = 0, nsplit = 0;
+    {
+      int v0 = 0, v1 = 0, v2 = 0;
+      for (int b = lane; b < G; b += 32) {
+        const int t0 = __ldcg(&a.ctot[b]), t1 = __ldcg(&a.ctot[G + b]);
+        if (b < bid) {
+          v0 += t0;
+          v1 += t1;
+        }
+        v2 += t1;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+      }
+      poff = v0;
+      noff = v1;
+      nsplit = v2;
+    }
+    for (int i = p0 + tid; i < p1; i += kPB) a.P[i] += poff;
+    for (size_t i = gt; i < (size_t)2 * nsplit * D; i += gs) {  // next level's bounds keys
+      a.kmin[i] = ~0ull;
+      a.kmax[i] = 0ull;
+    }
+    if (bid == G - 1 && tid == 0) a.P[n] = poff + __ldcg(&a.ctot[bid]);
+    {
+      int n0, n1;
+      chunk_of(m, bid, G, n0, n1);
+      for (int j = n0 + tid; j < n1; j += kPB) {
+        const int id = base + j;
+        if (a.dosplit[j]) {
+          const int c = base + m + 2 * (noff + a.child[j]);
+          a.child[j] = c;
+          a.nleft[id] = c;
+          a.nright[id] = c + 1;
+          a.npar[c] = a.npar[c + 1] = id;
+          a.ndep[c] = a.ndep[c + 1] = a.ndep[id] + 1;
+        } else {
+          a.child[j] = -1;
+          a.nleft[id] = a.nright[id] = -1;
+          a.bsc[id] = 0.0;
+        }
+      }
+    }
+    grid.sync();
+    // E: right-block passers register their slots; one-sided splits run the median
+    // fallback (kdtree.cpp:85-94) on their own segment (no swaps happen there)
+    for (int i = p0 + tid; i < p1; i += kPB) {
+      const int j = a.seg[i];
+      if (j < 0 || !a.dosplit[j] || !a.flag[i]) continue;
+      const int b = a.nbeg[base + j], e = b + a.ncnt[base + j];
+      const int L = a.P[e] - a.P[b];
+      if (i >= b + L) a.slot[b + (a.P[e] - a.P[i] - 1)] = i;
+    }
+    {
+      int n0, n1;
+      chunk_of(m, bid, G, n0, n1);
+      for (int j = n0 + tid; j < n1; j += kPB) {
+        if (!a.dosplit[j]) continue;
+        const int id = base + j;
+        const int b = a.nbeg[id], c = a.ncnt[id];
+        const int L = a.P[b + c] - a.P[b];
+        int l;
+        if (L == 0 || L == c) {
+          KeyCmp cmp{ a.x, D, a.bsd[id] };
+          int* q0 = a.perm + b;
+          dev_nth_element(q0, q0 + c / 2, q0 + c, cmp);
+          l = c / 2;
+          a.bsc[id] = cmp.key(q0[c / 2]);
+        } else {
+          l = L;
+          a.bsc[id] = a.mid[j];
+        }
+        a.lc[j] = l;
+        const int ch = a.child[j];
+        a.nbeg[ch] = b;
+        a.ncnt[ch] = l;
+        a.nbeg[ch + 1] = b + l;
+        a.ncnt[ch + 1] = c - l;
+      }
+    }
+    grid.sync();
+    // F: left-block failers swap with their partners; every position learns its
+    // next-level node (its own CTA reads it next, in A)
+    const int nbase = base + m;
+    for (int i = p0 + tid; i < p1; i += kPB) {
+      const int j = a.seg[i];
+      if (j < 0) continue;
+      if (!a.dosplit[j]) {
+        a.seg[i] = -1;
+        continue;
+      }
+      const int b = a.nbeg[base + j];
+      const int L = a.P[b + a.ncnt[base + j]] - a.P[b];
+      if (i < b + L && !a.flag[i]) {
+        const int k = (i - b) - (a.P[i] - a.P[b]);
+        const int partner = a.slot[b + k];
+        const int t = a.perm[i];
+        a.perm[i] = a.perm[partner];
+        a.perm[partner] = t;
+      }
+      a.seg[i] = a.child[j] - nbase + (i < b + a.lc[j] ? 0 : 1);
+    }
+    base = nbase;
+    m = 2 * nsplit;
+    ++level;
+    if (m == 0 || level >= kMaxTreeLevels - 1) break;
+    grid.sync();
+  }
+  if (gt == 0) {
+    a.lvl[0] = level;
+    a.lvl[1 + level] = base;
+  }
+}
+
 }  // namespace
+
+// Preorder renumbering and the preorder device/host arrays, from BFS-indexed arrays.
+static void finish_tree(DevTree& t, const double* d_x, int n, int D, int K,
+                        const std::vector<int>& h_left, const std::vector<int>& h_right,
+                        const std::vector<int>& h_beg, const std::vector<int>& h_cnt,
+                        const std::vector<int>& level_off, const double* blo, const double* bhi,
+                        const double* bcen, const double* bside, const double* bsc, const int* bsd,
+                        const int* d_bleft, const int* d_bright, const int* d_bbeg, const int* d_bcnt,
+                        const int* d_bpar, const int* d_bdep, cudaStream_t s);
+
+static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, int leaf,
+                                  cudaStream_t s)
+{
+  int dev = 0, nsm = 0, per_sm = 0, coop = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_build, kPB, 0));
+  if (!coop || per_sm < 1) return false;
+  const int G = nsm;
+  const int maxK = 2 * n;
+  DevBuf<double> blo, bhi, bcen, bside, bsc, mid;
+  DevBuf<int> bsd, seg, flag, P, slot, nbeg, ncnt, nleft, nright, npar, ndep, dosplit, child, lc,
+    ctot, lvl;
+  DevBuf<unsigned long long> kmin, kmax;
+  blo.reserve((size_t)maxK * D);
+  bhi.reserve((size_t)maxK * D);
+  bcen.reserve((size_t)maxK * D);
+  bside.reserve(maxK);
+  bsc.reserve(maxK);
+  bsd.reserve(maxK);
+  for (DevBuf<int>* b : { &nbeg, &ncnt, &nleft, &nright, &npar, &ndep }) b->reserve(maxK);
+  for (DevBuf<int>* b : { &seg, &flag, &slot, &dosplit, &child, &lc }) b->reserve((size_t)n + 1);
+  P.reserve((size_t)n + 1);
+  mid.reserve((size_t)n + 1);
+  kmin.reserve((size_t)n * D + D);
+  kmax.reserve((size_t)n * D + D);
+  ctot.reserve(2 * G);
+  lvl.reserve(kMaxTreeLevels + 2);
+  t.perm.reserve(n);
+  BuildArgs a{ d_x, n, D, leaf, t.perm.p, seg.p, flag.p, P.p, slot.p, nbeg.p, ncnt.p, nleft.p,
+               nright.p, npar.p, ndep.p, blo.p, bhi.p, bcen.p, bside.p, bsc.p, bsd.p, kmin.p,
+               kmax.p, mid.p, dosplit.p, child.p, lc.p, ctot.p, lvl.p };
+  void* kargs[] = { &a };
+  CK(cudaLaunchCooperativeKernel((void*)k_build, G, kPB, kargs, 0, s));
+  CK_LAUNCH();
+  std::vector<int> hl(kMaxTreeLevels + 2);
+  CK(cudaMemcpyAsync(hl.data(), lvl.p, sizeof(int) * hl.size(), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int levels = hl[0];
+  if (levels >= kMaxTreeLevels - 1) throw CudaError("kd-tree deeper than 255 levels");
+  const int K = hl[1 + levels];
+  std::vector<int> level_off(hl.begin() + 1, hl.begin() + 2 + levels);
+  std::vector<int> h_left(K), h_right(K), h_beg(K), h_cnt(K);
+  CK(cudaMemcpyAsync(h_left.data(), nleft.p, sizeof(int) * K, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h_right.data(), nright.p, sizeof(int) * K, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h_beg.data(), nbeg.p, sizeof(int) * K, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h_cnt.data(), ncnt.p, sizeof(int) * K, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  t.n = n;
+  t.D = D;
+  t.leaf = leaf;
+  finish_tree(t, d_x, n, D, K, h_left, h_right, h_beg, h_cnt, level_off, blo.p, bhi.p, bcen.p,
+              bside.p, bsc.p, bsd.p, nleft.p, nright.p, nbeg.p, ncnt.p, npar.p, ndep.p, s);
+  return true;
+}
 
 void build_tree(DevTree& t, const double* d_x, int n, int D, int leaf, cudaStream_t s)
 {
   if (leaf < 1) throw InvalidArgument("leaf_threshold must be >= 1");
   if (n < 1 || D < 1) throw InvalidArgument("PointSet requires N >= 1 and D >= 1");
+  static const bool host_levels = std::getenv("DFGTB_TREE_HOST_LEVELS") != nullptr;
+  if (!host_levels && build_tree_persistent(t, d_x, n, D, leaf, s)) return;
+  build_tree_levels(t, d_x, n, D, leaf, s);
+}
+
+// Host-driven level loop (fallback when one CTA per SM cannot be co-scheduled).
+void build_tree_levels(DevTree& t, const double* d_x, int n, int D, int leaf, cudaStream_t s)
+{
   t.n = n;
   t.D = D;
   t.leaf = leaf;
@@ -497,6 +844,30 @@ void build_tree(DevTree& t, const double* d_x, int n, int D, int leaf, cudaStrea
   const int K = (int)h_beg.size();
   h_left.resize(K, -1);
   h_right.resize(K, -1);
+  DevBuf<int> d_bleft, d_bright, d_bbeg, d_bcnt, d_bpar, d_bdep;
+  auto up = [&](DevBuf<int>& b, const std::vector<int>& v) {
+    b.reserve(v.size());
+    CK(cudaMemcpyAsync(b.p, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice, s));
+  };
+  up(d_bleft, h_left);
+  up(d_bright, h_right);
+  up(d_bbeg, h_beg);
+  up(d_bcnt, h_cnt);
+  up(d_bpar, h_par);
+  up(d_bdep, h_dep);
+  finish_tree(t, d_x, n, D, K, h_left, h_right, h_beg, h_cnt, level_off, blo.p, bhi.p, bcen.p,
+              bside.p, bsc.p, bsd.p, d_bleft.p, d_bright.p, d_bbeg.p, d_bcnt.p, d_bpar.p, d_bdep.p,
+              s);
+}
+
+static void finish_tree(DevTree& t, const double* d_x, int n, int D, int K,
+                        const std::vector<int>& h_left, const std::vector<int>& h_right,
+                        const std::vector<int>& h_beg, const std::vector<int>& h_cnt,
+                        const std::vector<int>& level_off, const double* blo, const double* bhi,
+                        const double* bcen, const double* bside, const double* bsc, const int* bsd,
+                        const int* d_bleft, const int* d_bright, const int* d_bbeg, const int* d_bcnt,
+                        const int* d_bpar, const int* d_bdep, cudaStream_t s)
+{
   t.nodes = K;
   t.height = (int)level_off.size() - 1;
   t.depth_off = level_off;
@@ -512,19 +883,9 @@ void build_tree(DevTree& t, const double* d_x, int n, int D, int leaf, cudaStrea
       bfs2pre[h_left[i]] = bfs2pre[i] + 1;
       bfs2pre[h_right[i]] = bfs2pre[i] + 1 + sub[h_left[i]];
     }
-
-  DevBuf<int> d_map, d_bleft, d_bright, d_bbeg, d_bcnt, d_bpar, d_bdep;
-  auto up = [&](DevBuf<int>& b, const std::vector<int>& v) {
-    b.reserve(v.size());
-    CK(cudaMemcpyAsync(b.p, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice, s));
-  };
-  up(d_map, bfs2pre);
-  up(d_bleft, h_left);
-  up(d_bright, h_right);
-  up(d_bbeg, h_beg);
-  up(d_bcnt, h_cnt);
-  up(d_bpar, h_par);
-  up(d_bdep, h_dep);
+  DevBuf<int> d_map;
+  d_map.reserve(K);
+  CK(cudaMemcpyAsync(d_map.p, bfs2pre.data(), sizeof(int) * K, cudaMemcpyHostToDevice, s));
   t.lo.reserve((size_t)K * D);
   t.hi.reserve((size_t)K * D);
   t.centroid.reserve((size_t)K * D);
@@ -539,10 +900,9 @@ void build_tree(DevTree& t, const double* d_x, int n, int D, int leaf, cudaStrea
   t.depth.reserve(K);
   t.by_depth.reserve(K);
   k_to_preorder<<<ceil_div(K, 256), 256, 0, s>>>(
-    K, D, d_map.p, blo.p, bhi.p, bcen.p, bside.p, bsc.p, bsd.p, d_bleft.p, d_bright.p, d_bbeg.p,
-    d_bcnt.p, d_bpar.p, d_bdep.p, t.lo.p, t.hi.p, t.centroid.p, t.max_side.p, t.split_coord.p,
-    t.split_dim.p, t.left.p, t.right.p, t.begin.p, t.count.p, t.parent.p, t.depth.p,
-    t.by_depth.p);
+    K, D, d_map.p, blo, bhi, bcen, bside, bsc, bsd, d_bleft, d_bright, d_bbeg, d_bcnt, d_bpar,
+    d_bdep, t.lo.p, t.hi.p, t.centroid.p, t.max_side.p, t.split_coord.p, t.split_dim.p, t.left.p,
+    t.right.p, t.begin.p, t.count.p, t.parent.p, t.depth.p, t.by_depth.p);
   CK_LAUNCH();
   t.xs.reserve((size_t)n * D);
   k_gather_points<<<ceil_div((long long)n * D, 256), 256, 0, s>>>(d_x, t.perm.p, n, D, t.xs.p);

@@ -24,6 +24,9 @@ struct DevTree {
 
 // Builds the tree of the n x D row-major device points `d_x` (reference
 // split rule, std::partition pairing and the std::nth_element fallback).
+// One cooperative launch builds every level (device-side node bookkeeping); the
+// host-driven level loop below is the fallback (and DFGTB_TREE_HOST_LEVELS=1).
 void build_tree(DevTree& t, const double* d_x, int n, int D, int leaf, cudaStream_t s);
+void build_tree_levels(DevTree& t, const double* d_x, int n, int D, int leaf, cudaStream_t s);
 
 }  // namespace dfgtb
