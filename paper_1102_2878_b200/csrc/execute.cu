@@ -215,15 +215,22 @@ __global__ void __launch_bounds__(kLocThreads) k_local_chunks_t(DevSeries g, Tre
     for (int d = 0; d < D; ++d) cq[d] = qc[d];
     for (int j = threadIdx.x; j < lc.n; j += kLocThreads) {
       const double* rp = R.xs + (size_t)(lc.start + j) * D;
+      // Hermite functions H_k(t_d) = exp(-t_d^2) h_k(t_d): the Gaussians of all
+      // dimensions are one exp(-|t|^2), folded into dimension 0
       double H[D][PM];
+      double tt = 0.0;
 #pragma unroll
       for (int d = 0; d < D; ++d) {
         const double t = (cq[d] - rp[d]) * s;
-        H[d][0] = exp(-t * t);
-        if (PM > 1) H[d][1] = 2.0 * t * H[d][0];
+        tt = fma(t, t, tt);
+        H[d][0] = 1.0;
+        if (PM > 1) H[d][1] = 2.0 * t;
 #pragma unroll
-        for (int k = 1; k + 1 < PM; ++k) H[d][k + 1] = 2.0 * t * H[d][k] - 2.0 * k * H[d][k - 1];
+        for (int k = 1; k + 1 < PM; ++k) H[d][k + 1] = fma(2.0 * t, H[d][k], -2.0 * k * H[d][k - 1]);
       }
+      const double e = exp(-tt);
+#pragma unroll
+      for (int k = 0; k < PM; ++k) H[0][k] *= e;
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         double f = 1.0;
@@ -971,44 +978,61 @@ __global__ void __launch_bounds__(kBlock) k_farfield(DevSeries g, TreeView Q, Tr
   }
 }
 
-// Specialised far-field evaluation for the default tables (p_max == PM): every
-// multi-index is a compile-time constant, so the Hermite rows, s^|a| and the digit
-// products live in registers and the (position-layout) moments are read as
-// warp-uniform broadcast loads.  Same sum as dev_eval_farfield, position order.
+// Specialised far-field evaluation for the default tables (p_max == PM).  With
+// t = (q - c) s, h_k the Hermite polynomials and the Gaussian factored out of the
+// Hermite functions (prod_d exp(-t_d^2) = exp(-|t|^2), ONE exp per (query, item)):
+//   sum_a M_a s^|a| prod_d H_{a_d}(t_d) = exp(-|t|^2) sum_a M_a prod_d (s^{a_d} h_{a_d}(t_d)),
+// contracted one dimension at a time (last dimension first; position layout p =
+// sum_d a_d PM^(D-1-d)) over the truncation cube a_d < order: PM^D + PM^(D-1) + ..
+// FMAs instead of (D + 1) PM^D multiplies.  The moments are warp-uniform 16-byte loads.
 template <int D, int PM>
 __device__ __forceinline__ double ff_eval_t(const double* Mt, const double* c, const double* q,
                                             double s, int order,
                                             const double (&spw)[D * (PM - 1) + 1])
 {
-  double H[D][PM];
+  constexpr int NP = ipow_c(PM, D);
+  double h[D][PM];
+  double tt = 0.0;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     const double t = (q[d] - c[d]) * s;
-    H[d][0] = exp(-t * t);
-    if (PM > 1) H[d][1] = 2.0 * t * H[d][0];
+    tt = fma(t, t, tt);
+    h[d][0] = 1.0;
+    if (PM > 1) h[d][1] = 2.0 * t;
 #pragma unroll
-    for (int k = 1; k + 1 < PM; ++k) H[d][k + 1] = 2.0 * t * H[d][k] - 2.0 * k * H[d][k - 1];
+    for (int k = 1; k + 1 < PM; ++k) h[d][k + 1] = fma(2.0 * t, h[d][k], -2.0 * k * h[d][k - 1]);
+#pragma unroll
+    for (int k = 1; k < PM; ++k) h[d][k] *= spw[k];
   }
-  double sum = 0.0;
-  constexpr int NP = ipow_c(PM, D);
+  double v[NP];
+  if constexpr (NP % 2 == 0) {
+    const double2* M2 = reinterpret_cast<const double2*>(Mt);
 #pragma unroll
-  for (int p = 0; p < NP; ++p) {
-    int dig[D], mx = 0, deg = 0, rest = p;
-#pragma unroll
-    for (int d = D - 1; d >= 0; --d) {
-      dig[d] = rest % PM;
-      rest /= PM;
-      mx = dig[d] > mx ? dig[d] : mx;
-      deg += dig[d];
+    for (int p = 0; p < NP / 2; ++p) {
+      const double2 m2 = M2[p];
+      v[2 * p] = m2.x;
+      v[2 * p + 1] = m2.y;
     }
-    if (mx < order) {
-      double f = Mt[p] * spw[deg];
+  } else {
 #pragma unroll
-      for (int d = 0; d < D; ++d) f *= H[d][dig[d]];
-      sum += f;
+    for (int p = 0; p < NP; ++p) v[p] = Mt[p];
+  }
+  int len = NP;
+#pragma unroll
+  for (int d = D - 1; d >= 0; --d) {
+    len /= PM;
+#pragma unroll
+    for (int r = 0; r < ipow_c(PM, D - 1); ++r) {
+      if (r < len) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = PM - 1; k >= 0; --k)
+          if (k < order) acc = fma(v[r * PM + k], h[d][k], acc);
+        v[r] = acc;
+      }
     }
   }
-  return sum;
+  return exp(-tt) * v[0];
 }
 
 template <int D, int PM>

@@ -667,7 +667,10 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_build, kPB, 0));
   if (!coop || per_sm < 1) return false;
-  const int G = nsm;
+  // CTAs: 64 for small sets (measured: cheaper grid barriers, enough threads), one
+  // per SM from ~256k points; DFGTB_TREE_CTAS overrides (experiments)
+  static const int env_g = std::getenv("DFGTB_TREE_CTAS") ? std::atoi(std::getenv("DFGTB_TREE_CTAS")) : 0;
+  const int G = env_g > 0 ? std::min(env_g, nsm) : std::min(nsm, std::max(64, ceil_div(n, 4 * kPB)));
   const int maxK = 2 * n;
   DevBuf<double> blo, bhi, bcen, bside, bsc, mid;
   DevBuf<int> bsd, seg, flag, P, slot, nbeg, ncnt, nleft, nright, npar, ndep, dosplit, child, lc,
