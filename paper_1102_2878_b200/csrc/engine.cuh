@@ -91,9 +91,11 @@ public:
 
 private:
   void traverse(const DevTree& qt, const double* h, int nb);
+  bool traverse_finish();
   void run_levels(const void* trav_args, const std::vector<const void*>& sig);
   void destroy_graph();
   void run_phases(const DevTree& qt, const double* h, int nb, double* d_out);
+  void launch_phases(const DevTree& qt, const double* h, int nb, double* d_out);
   void eager_moments();
   void setup_leaves(const DevTree& t);
 
@@ -145,6 +147,12 @@ private:
   long long nF_ = 0, nDT_ = 0, nB_ = 0;
   int nb_ = 1;
   bool mufu_ = false;
+  // device-side counts of a batch (no host round trip until its end):
+  // [0] nF [1] nDT [2] nB [3] traversal overflow [4] local chunks [5] base tasks
+  DevBuf<int> bc_;
+  int trav_nb_ = 0;
+  bool trav_trace_ = false;
+  int capCh_ = 0, capTask_ = 0;  // local chunks / base tasks (grown on overflow)
 };
 
 // Exhaustive FP64 sums on the device (K12, naive_kde engine.cpp:22-36).

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <string>
 
 namespace dfgtb {
 using namespace detail;
@@ -26,10 +27,10 @@ using namespace detail;
 namespace {
 
 // ------------------------------------------------------------------- moments
-__global__ void k_mark_moments(const Item* it, int n, int* flag)
+__global__ void k_mark_moments(const Item* it, const int* n, int cap, int* flag)
 {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
+  const int m = min(*n, cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
     const int kind = it[i].code >> 8;
     if (kind == kF || kind == kT) flag[it[i].r] = 1;
   }
@@ -131,34 +132,45 @@ struct LChunk {
   int item, start, n;
 };
 
-__global__ void k_local_count(const Item* items, int n, TreeView R, int* nch)
+// chunk counts of the D/T items (0 past the item count, so one scan over the
+// capacity gives the offsets); counts come from the device
+__global__ void k_local_count(const Item* items, const int* n, int cap, TreeView R, int* nch)
 {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int kind = items[i].code >> 8;
-  nch[i] = kind == kD ? (R.count[items[i].r] + kLocChunk - 1) / kLocChunk : 1;
+  const int m = min(*n, cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= cap; i += gridDim.x * blockDim.x) {
+    int c = 0;
+    if (i < m) {
+      const int kind = items[i].code >> 8;
+      c = kind == kD ? (R.count[items[i].r] + kLocChunk - 1) / kLocChunk : 1;
+    }
+    nch[i] = c;
+  }
 }
 
-__global__ void k_local_fill(const Item* items, int n, TreeView R, const int* choff, LChunk* ch)
+__global__ void k_local_fill(const Item* items, const int* n, int cap, TreeView R, const int* choff,
+                             LChunk* ch, int chcap, int* nch_out)
 {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int kind = items[i].code >> 8;
-  const int r = items[i].r;
-  if (kind == kD) {
-    const int b = R.begin[r], c = R.count[r];
-    for (int k = 0, st = 0; st < c; ++k, st += kLocChunk)
-      ch[choff[i] + k] = LChunk{ i, b + st, min(kLocChunk, c - st) };
-  } else {
-    ch[choff[i]] = LChunk{ i, -1, 0 };
+  const int m = min(*n, cap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *nch_out = choff[m];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int kind = items[i].code >> 8;
+    const int r = items[i].r;
+    if (kind == kD) {
+      const int b = R.begin[r], c = R.count[r];
+      for (int k = 0, st = 0; st < c; ++k, st += kLocChunk)
+        if (choff[i] + k < chcap) ch[choff[i] + k] = LChunk{ i, b + st, min(kLocChunk, c - st) };
+    } else if (choff[i] < chcap) {
+      ch[choff[i]] = LChunk{ i, -1, 0 };
+    }
   }
 }
 
 __global__ void k_local_chunks(DevSeries g, TreeView Q, TreeView R, int K, const Item* items,
-                               const LChunk* ch, int nch, const double* Mt, SlotView sv,
-                               double* part)
+                               const LChunk* ch, const int* nchp, int chcap, const double* Mt,
+                               SlotView sv, double* part)
 {
   extern __shared__ double sm[];
+  const int nch = min(*nchp, chcap);
   for (int c = blockIdx.x; c < nch; c += gridDim.x) {
     const LChunk lc = ch[c];
     const Item it = items[lc.item];
@@ -186,13 +198,14 @@ constexpr int kLocThreads = 64;
 template <int D, int PM>
 __global__ void __launch_bounds__(kLocThreads) k_local_chunks_t(DevSeries g, TreeView Q, TreeView R,
                                                                int K, const Item* items,
-                                                               const LChunk* ch, int nch,
-                                                               const double* Mt, SlotView sv,
-                                                               double* part)
+                                                               const LChunk* ch, const int* nchp,
+                                                               int chcap, const double* Mt,
+                                                               SlotView sv, double* part)
 {
   constexpr int NP = ipow_c(PM, D);
   __shared__ double red[NP][kLocThreads + 1];
   extern __shared__ double sm[];
+  const int nch = min(*nchp, chcap);
   for (int c = blockIdx.x; c < nch; c += gridDim.x) {
     const LChunk lc = ch[c];
     const Item it = items[lc.item];
@@ -264,15 +277,17 @@ __global__ void __launch_bounds__(kLocThreads) k_local_chunks_t(DevSeries g, Tre
 // warp of a key's first item does the work), lanes over terms.  Every term sums its
 // chunks in item order (8 loads in flight), so the result does not depend on the
 // launch shape.
-__global__ void k_local_reduce(DevSeries g, int nitems, const int* cnt, const int* off,
-                               const Item* items, const int* choff, const double* part, double* L,
-                               int* Lord)
+__global__ void k_local_reduce(DevSeries g, const int* nitems_p, int cap, const int* cnt,
+                               const int* off, const Item* items, const int* choff,
+                               const double* part, double* L, int* Lord)
 {
-  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (i >= nitems) return;
+  const int nitems = min(*nitems_p, cap);
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nitems;
+       i += (gridDim.x * blockDim.x) >> 5) {
   const int n = items[i].key;
   const int i0 = off[n];
-  if (i != i0) return;  // not the first item of its key
+  if (i != i0) continue;  // not the first item of its key
   const int i1 = i0 + cnt[n];
   int ord = 0, omin = 1 << 20;
   for (int k = i0 + lane; k < i1; k += 32) {
@@ -311,6 +326,7 @@ __global__ void k_local_reduce(DevSeries g, int nitems, const int* cnt, const in
     L[(size_t)n * g.T + t] += sg * g.invf[t] * acc;
   }
   if (lane == 0 && Lord[n] < ord) Lord[n] = ord;
+  }
 }
 
 // Top-down L2L of one depth level for every slot (post_process, engine.cpp:294-304).
@@ -380,9 +396,11 @@ __global__ void k_task_count(const int* leaves, int nleaves, int nb, int K, cons
 
 __global__ void k_task_fill(const int* leaves, int nleaves, int nb, int K, const int* cntB,
                             const int* offB, const Item* sB, const int* rcount, int rmax, TreeView Q,
-                            const int* toff, BTask* tasks, int* leaf_task, int* leaf_runs)
+                            const int* toff, BTask* tasks, int tcap, int* ntasks_out,
+                            int* leaf_task, int* leaf_runs)
 {
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i == 0 && lane == 0) *ntasks_out = toff[nleaves * nb];
   if (i >= nleaves * nb) return;
   const int slot = i / nleaves;
   const int leaf = leaves[i - slot * nleaves];
@@ -394,7 +412,8 @@ __global__ void k_task_fill(const int* leaves, int nleaves, int nb, int K, const
   int runs = 0;
   for (int k = o; k < e;) {
     const int j = warp_run_end(sB, k, e, rcount, rmax, lane);
-    for (int qi = lane; qi < nq; qi += 32) tasks[t0 + qi * nruns + runs] = BTask{ key, k, j, 32 * qi };
+    for (int qi = lane; qi < nq; qi += 32)
+      if (t0 + qi * nruns + runs < tcap) tasks[t0 + qi * nruns + runs] = BTask{ key, k, j, 32 * qi };
     k = j;
     ++runs;
   }
@@ -553,13 +572,14 @@ struct PtLoad {
 // Compact reference-leaf records for the base case, in sorted item order:
 // {first sorted position, count | flags << 28}; flags bit 0: the traversal proved
 // y <= 708 for every pair; bit 1: terms may be clamped at 2^-1021 (see traverse.cu).
-__global__ void k_base_records(const Item* items, int n, TreeView R, int2* rec)
+__global__ void k_base_records(const Item* items, const int* n, int cap, TreeView R, int2* rec)
 {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const Item it = items[i];
-  const int c = R.count[it.r];
-  rec[i] = make_int2(R.begin[it.r], c | ((it.code & 3) << 28));
+  const int m = min(*n, cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const Item it = items[i];
+    const int c = R.count[it.r];
+    rec[i] = make_int2(R.begin[it.r], c | ((it.code & 3) << 28));
+  }
 }
 
 // K10: exhaustive base case (Traversal::base_case, engine.cpp:239-269).  One warp per
@@ -581,7 +601,7 @@ struct BaseGeo {
 #define DFGTB_BASE_G 8
 #endif
   static constexpr int G = DT <= 2 ? DFGTB_BASE_G : 4;            // queries per lane
-  static constexpr int RMAX = DT == 1 ? 512 : DT == 2 ? 256 : DT <= 4 ? 128 : 64;  // stream tile
+  static constexpr int RMAX = DT == 1 ? 512 : 256;              // stream tile (points)
   static constexpr int WARPS = 4;                                 // per CTA
   static constexpr int DM = (DT + 2) / 2 * 2;                     // MUFU stream stride
   static constexpr int DS = DM > DP ? DM : DP;
@@ -814,18 +834,19 @@ __device__ __forceinline__ void base_groups(const double* rs, int n, const doubl
 #endif
 template <int DT>
 __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
-  k_base_case(TreeView Q, int K, const BTask* tasks, int ntasks, const int2* rec, const double* xq,
-              const double* xr, int nq, int nr, double* part, int* next, int mufu)
+  k_base_case(TreeView Q, int K, const BTask* tasks, const int* ntasks_p, int tcap, const int2* rec,
+              const double* xq, const double* xr, int nq, int nr, double* part, int* next, int mufu)
 {
+  const int ntasks = min(*ntasks_p, tcap);
   using Geo = BaseGeo<DT>;
   constexpr int DP = Geo::DP, RMAX = Geo::RMAX;
   __shared__ __align__(512) double tab[64];
-  __shared__ __align__(16) double sm[Geo::WARPS][Geo::WORDS];
+  extern __shared__ __align__(16) double dsm[];  // WARPS x WORDS (dynamic: > 48 KB for D >= 3)
   __shared__ unsigned smask_all[Geo::WARPS][RMAX / 32];
   if (threadIdx.x < 64) tab[threadIdx.x] = c_exp2tab[threadIdx.x];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  double* rs = sm[threadIdx.x >> 5];
+  double* rs = dsm + (size_t)(threadIdx.x >> 5) * Geo::WORDS;
   double* qs = rs + RMAX * Geo::DS;
   double* qsum = qs + 32 * Geo::DS;
   unsigned* smask = smask_all[threadIdx.x >> 5];
@@ -902,7 +923,8 @@ __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
 
 // Generic dimension (D > 5): scalar loads of the scaled coordinates, libdevice exp.
 __global__ void __launch_bounds__(kBlock) k_base_case_any(TreeView Q, TreeView R, int K, int D,
-                                                          const BTask* tasks, int ntasks,
+                                                          const BTask* tasks, const int* ntasks_p,
+                                                          int tcap,
                                                           const Item* items, const double* xq,
                                                           const double* xr, int nq, int nr,
                                                           double* part)
@@ -910,6 +932,7 @@ __global__ void __launch_bounds__(kBlock) k_base_case_any(TreeView Q, TreeView R
   const int lane = threadIdx.x & 31;
   const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int ntasks = min(*ntasks_p, tcap);
   for (int w = w0; w < ntasks; w += nw) {
     const BTask t = tasks[w];
     const int slot = t.key / K, leaf = t.key - slot * K;
@@ -1240,30 +1263,33 @@ int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }
 
 // Persistent grid: as many CTAs as fit on the GPU (or fewer for small task lists).
 template <int DT>
-void launch_base_t(int ntasks, cudaStream_t s, TreeView Q, int K, const BTask* tasks, const int2* rec,
-                   const double* xq, const double* xr, int nq, int nr, double* part, int* next,
-                   int mufu)
+void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int K, const BTask* tasks,
+                   const int2* rec, const double* xq, const double* xr, int nq, int nr, double* part,
+                   int* next, int mufu)
 {
   static int per_sm = 0, nsm = 0;
   constexpr int threads = BaseGeo<DT>::WARPS * 32;
+  constexpr int smem = BaseGeo<DT>::WARPS * BaseGeo<DT>::WORDS * (int)sizeof(double);
   if (!per_sm) {
     int dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_base_case<DT>, threads, 0));
+    CK(cudaFuncSetAttribute(k_base_case<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_base_case<DT>, threads, smem));
     per_sm = std::max(per_sm, 1);
   }
   const int grid = (int)std::min<long long>((long long)nsm * per_sm,
-                                            (ntasks + BaseGeo<DT>::WARPS - 1) / BaseGeo<DT>::WARPS);
+                                            (tcap + BaseGeo<DT>::WARPS - 1) / BaseGeo<DT>::WARPS);
   CK(cudaMemsetAsync(next, 0, sizeof(int), s));
-  k_base_case<DT><<<grid, threads, 0, s>>>(Q, K, tasks, ntasks, rec, xq, xr, nq, nr, part, next, mufu);
+  k_base_case<DT><<<grid, threads, smem, s>>>(Q, K, tasks, ntasks, tcap, rec, xq, xr, nq, nr, part,
+                                              next, mufu);
 }
 
-void launch_base(int D, int grid, cudaStream_t s, TreeView Q, TreeView R, int K,
-                 const BTask* tasks, int ntasks, const Item* items, const int2* rec,
-                 const double* xq, const double* xr, int nq, int nr, double* part, int* next, int mufu)
+void launch_base(int D, cudaStream_t s, TreeView Q, TreeView R, int K, const BTask* tasks,
+                 const int* ntasks, int tcap, const Item* items, const int2* rec, const double* xq,
+                 const double* xr, int nq, int nr, double* part, int* next, int mufu)
 {
-#define BASE(DD) launch_base_t<DD>(ntasks, s, Q, K, tasks, rec, xq, xr, nq, nr, part, next, mufu)
+#define BASE(DD) launch_base_t<DD>(ntasks, tcap, s, Q, K, tasks, rec, xq, xr, nq, nr, part, next, mufu)
   switch (D) {
   case 1: BASE(1); break;
   case 2: BASE(2); break;
@@ -1271,7 +1297,8 @@ void launch_base(int D, int grid, cudaStream_t s, TreeView Q, TreeView R, int K,
   case 4: BASE(4); break;
   case 5: BASE(5); break;
   default:
-    k_base_case_any<<<grid, kBlock, 0, s>>>(Q, R, K, D, tasks, ntasks, items, xq, xr, nq, nr, part);
+    k_base_case_any<<<148 * 16, kBlock, 0, s>>>(Q, R, K, D, tasks, ntasks, tcap, items, xq, xr, nq, nr,
+                                                part);
     break;
   }
 #undef BASE
@@ -1339,7 +1366,47 @@ void Engine::setup_leaves(const DevTree& t)
   CK(cudaStreamSynchronize(s_));
 }
 
+// One batch: every launch is queued without a host round trip (counts live in bc_);
+// the host synchronises once at the end, reads the traversal verdict and the chunk /
+// task totals, and reruns the batch with larger buffers if anything overflowed.
 void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_out)
+{
+  for (int attempt = 0;; ++attempt) {
+    launch_phases(qt, h, nb, d_out);
+    CK(cudaStreamSynchronize(s_));
+    const bool trav_ok = traverse_finish();
+    bool ok = trav_ok;
+    if (trav_ok) {
+      int hb[8];
+      CK(cudaMemcpy(hb, bc_.p, sizeof(hb), cudaMemcpyDeviceToHost));
+      auto grow = [&](long long need) {
+        if (need > (1 << 28))
+          throw OutOfMemory("batch needs more than 2^28 chunks / tasks (" + std::to_string(hb[4]) +
+                            ", " + std::to_string(hb[5]) + ")");
+        return (int)(need + need / 4 + 1024);
+      };
+      if (hb[4] > capCh_) {
+        capCh_ = grow(hb[4]);
+        ok = false;
+      }
+      if (hb[5] > capTask_) {
+        capTask_ = grow(hb[5]);
+        ok = false;
+      }
+    }
+    if (ok) break;
+    if (attempt > 10) throw OutOfMemory("batch buffers keep overflowing");
+  }
+  CK(cudaEventElapsedTime(&tim_.traverse_ms, ev_[2], ev_[3]));
+  CK(cudaEventElapsedTime(&tim_.moments_ms, ev_[3], ev_[4]));
+  CK(cudaEventElapsedTime(&tim_.local_ms, ev_[4], ev_[5]));
+  CK(cudaEventElapsedTime(&tim_.base_ms, ev_[9], ev_[6]));
+  CK(cudaEventElapsedTime(&tim_.farfield_ms, ev_[6], ev_[7]));
+  CK(cudaEventElapsedTime(&tim_.final_ms, ev_[7], ev_[8]));
+  CK(cudaEventElapsedTime(&tim_.total_ms, ev_[2], ev_[8]));
+}
+
+void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d_out)
 {
   cudaStream_t s = s_;
   const DevSeries g = dev_series();
@@ -1364,25 +1431,19 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
   const SlotView sv{ slotp_.p, slotp_.p + nb, slotp_.p + 2 * nb };
   CK(cudaEventRecord(ev_[2], s));
   traverse(qt, h, nb);
+  const int* dnF = bc_.p + 0;
+  const int* dnDT = bc_.p + 1;
+  const int* dnB = bc_.p + 2;
   CK(cudaEventRecord(ev_[3], s));
   // moments of the reference nodes used by F/T items (large tables only; small
   // tables were computed for every node when the engine was built)
-  unsigned long long nFT = 0, nLoc = 0;
-  for (const Stats& st : slot_stats_) {
-    nFT += st.prunes_farfield + st.prunes_far_to_local;
-    nLoc += st.prunes_finite_diff + st.prunes_direct_local + st.prunes_far_to_local;
-  }
-  if (nFT && !eager_) {
+  if (!eager_ && cfg_.mode == 1) {
     mflag_.reserve(rt_.nodes);
     CK(cudaMemsetAsync(mflag_.p, 0, sizeof(int) * rt_.nodes, s));
-    if (nF_) {
-      k_mark_moments<<<ceil_div(nF_, 256), 256, 0, s>>>(sF_.p, (int)nF_, mflag_.p);
-      CK_LAUNCH();
-    }
-    if (nDT_) {
-      k_mark_moments<<<ceil_div(nDT_, 256), 256, 0, s>>>(sDT_.p, (int)nDT_, mflag_.p);
-      CK_LAUNCH();
-    }
+    k_mark_moments<<<148 * 4, 256, 0, s>>>(sF_.p, dnF, capF_, mflag_.p);
+    CK_LAUNCH();
+    k_mark_moments<<<148 * 4, 256, 0, s>>>(sDT_.p, dnDT, capDT_, mflag_.p);
+    CK_LAUNCH();
     const int smem = 32 * D_ * ser_.pmax * (int)sizeof(double);
     k_moments<<<std::min(rt_.nodes, 148 * 8), 128, smem, s>>>(g, R, rt_.nodes, mflag_.p, mdone_.p,
                                                              Mt_.p);
@@ -1390,45 +1451,43 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
   }
   CK(cudaEventRecord(ev_[4], s));
   // D/T items -> chunked partial tables -> per-(slot, query node) reduction
-  if (nDT_) {
-    lnch_.reserve(nDT_ + 1);
-    lchoff_.reserve(nDT_ + 1);
-    k_local_count<<<ceil_div(nDT_, 256), 256, 0, s>>>(sDT_.p, (int)nDT_, R, lnch_.p);
+  if (cfg_.mode == 1) {
+    lnch_.reserve((size_t)capDT_ + 1);
+    lchoff_.reserve((size_t)capDT_ + 1);
+    k_local_count<<<148 * 4, 256, 0, s>>>(sDT_.p, dnDT, capDT_, R, lnch_.p);
     CK_LAUNCH();
-    CK(cudaMemsetAsync(lnch_.p + nDT_, 0, sizeof(int), s));
     size_t need = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need, lnch_.p, lchoff_.p, (int)nDT_ + 1, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, need, lnch_.p, lchoff_.p, capDT_ + 1, s);
     scan_tmp_.reserve(need + 256);
     size_t have = scan_tmp_.cap;
-    cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, lnch_.p, lchoff_.p, (int)nDT_ + 1, s);
-    int nch = 0;
-    CK(cudaMemcpyAsync(&nch, lchoff_.p + nDT_, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    lchunk_.reserve((size_t)nch * 3);
+    cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, lnch_.p, lchoff_.p, capDT_ + 1, s);
+    capCh_ = std::max(capCh_, std::max(4096, capDT_));
+    lchunk_.reserve((size_t)capCh_ * 3);
     LChunk* ch = reinterpret_cast<LChunk*>(lchunk_.p);
-    k_local_fill<<<ceil_div(nDT_, 256), 256, 0, s>>>(sDT_.p, (int)nDT_, R, lchoff_.p, ch);
+    k_local_fill<<<148 * 4, 256, 0, s>>>(sDT_.p, dnDT, capDT_, R, lchoff_.p, ch, capCh_, bc_.p + 4);
     CK_LAUNCH();
-    lpart_.reserve((size_t)nch * T);
+    lpart_.reserve((size_t)capCh_ * T);
     const int smem = std::max(kLocSub * D_ * ser_.pmax, D_ * (2 * ser_.pmax)) * (int)sizeof(double);
-    const int gl = std::min(nch, 148 * 16);
+    const int gl = 148 * 16;
     const int pm = ser_.pmax;
+    const int* dnch = bc_.p + 4;
 #define LOC_T(DD, PP)                                                                            \
   k_local_chunks_t<DD, PP><<<gl, kLocThreads, D_ * (2 * PP) * (int)sizeof(double), s>>>(          \
-    g, Q, R, K, sDT_.p, ch, nch, Mt_.p, sv, lpart_.p)
+    g, Q, R, K, sDT_.p, ch, dnch, capCh_, Mt_.p, sv, lpart_.p)
     if (D_ == 1 && pm == 8) LOC_T(1, 8);
     else if (D_ == 2 && pm == 6) LOC_T(2, 6);
     else if (D_ == 3 && pm == 4) LOC_T(3, 4);
     else if (D_ == 4 && pm == 2) LOC_T(4, 2);
     else if (D_ == 5 && pm == 2) LOC_T(5, 2);
     else
-      k_local_chunks<<<gl, 64, smem, s>>>(g, Q, R, K, sDT_.p, ch, nch, Mt_.p, sv, lpart_.p);
+      k_local_chunks<<<gl, 64, smem, s>>>(g, Q, R, K, sDT_.p, ch, dnch, capCh_, Mt_.p, sv, lpart_.p);
 #undef LOC_T
     CK_LAUNCH();
-    k_local_reduce<<<ceil_div(nDT_, 8), 256, 0, s>>>(g, (int)nDT_, cntDT_.p, offDT_.p, sDT_.p,
-                                                     lchoff_.p, lpart_.p, L_.p, Lord_.p);
+    k_local_reduce<<<148 * 8, 256, 0, s>>>(g, dnDT, capDT_, cntDT_.p, offDT_.p, sDT_.p, lchoff_.p,
+                                           lpart_.p, L_.p, Lord_.p);
     CK_LAUNCH();
   }
-  if (cfg_.local_pushdown == 1 && nLoc > 0) {
+  if (cfg_.local_pushdown == 1) {
     const int smem = D_ * ser_.pmax * (int)sizeof(double);
     for (int d = 0; d + 1 < qt.height; ++d) {
       const int b = qt.depth_off[d], e = qt.depth_off[d + 1];
@@ -1441,64 +1500,56 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
   // base-case tasks
   const int nleaves = (int)qleaves_host_.size();
   const int nlb = nleaves * nb;
-  int ntasks = 0;
   leaf_task_.reserve(KB);
   leaf_runs_.reserve(KB);
   const int rmax = base_rmax(D_);
-  if (nB_) {
-    ntask_.reserve(nlb + 1);
-    toff_.reserve(nlb + 1);
-    k_task_count<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p,
-                                                    sB_.p, R.count, rmax, Q, ntask_.p);
-    CK_LAUNCH();
-    CK(cudaMemsetAsync(ntask_.p + nlb, 0, sizeof(int), s));
+  ntask_.reserve(nlb + 1);
+  toff_.reserve(nlb + 1);
+  k_task_count<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p, sB_.p,
+                                                  R.count, rmax, Q, ntask_.p);
+  CK_LAUNCH();
+  CK(cudaMemsetAsync(ntask_.p + nlb, 0, sizeof(int), s));
+  {
     size_t need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, ntask_.p, toff_.p, nlb + 1, s);
     scan_tmp_.reserve(need + 256);
     size_t have = scan_tmp_.cap;
     cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, ntask_.p, toff_.p, nlb + 1, s);
-    CK(cudaMemcpyAsync(&ntasks, toff_.p + nlb, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    tasks_.reserve((size_t)ntasks * 4);
-    k_task_fill<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p,
-                                                   sB_.p, R.count, rmax, Q, toff_.p,
-                                                   reinterpret_cast<BTask*>(tasks_.p), leaf_task_.p,
-                                                   leaf_runs_.p);
-    CK_LAUNCH();
-    bpart_.reserve((size_t)ntasks * 32);
-    brec_.reserve((size_t)nB_ * 2 + 2);
-    k_base_records<<<ceil_div(nB_, 256), 256, 0, s>>>(sB_.p, (int)nB_, R,
-                                                      reinterpret_cast<int2*>(brec_.p));
-    CK_LAUNCH();
-  } else {
-    bpart_.reserve(32);
   }
-  const double* xq = nullptr;
-  const double* xr = nullptr;
-  if (ntasks) {  // scaled, centred, padded coordinates per slot (Q and, if different, R)
-    const int DP = padded_dim(D_);
-    xq_.reserve((size_t)qt.n * DP * nb);
-    k_scale_points<<<ceil_div((long long)qt.n * DP * nb, 256), 256, 0, s>>>(
-      qt.xs.p, qt.n, D_, DP, nb, rt_.centroid.p, sv, mufu_ ? kSqrtLog2e : 1.0, xq_.p);
+  capTask_ = std::max(capTask_, std::max(4096, capB_ / 8));
+  tasks_.reserve((size_t)capTask_ * 4);
+  k_task_fill<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p, sB_.p,
+                                                 R.count, rmax, Q, toff_.p,
+                                                 reinterpret_cast<BTask*>(tasks_.p), capTask_,
+                                                 bc_.p + 5, leaf_task_.p, leaf_runs_.p);
+  CK_LAUNCH();
+  bpart_.reserve((size_t)capTask_ * 32);
+  brec_.reserve((size_t)capB_ * 2 + 2);
+  k_base_records<<<148 * 4, 256, 0, s>>>(sB_.p, dnB, capB_, R, reinterpret_cast<int2*>(brec_.p));
+  CK_LAUNCH();
+  // scaled, centred, padded coordinates per slot (Q and, if different, R)
+  const int DP = padded_dim(D_);
+  xq_.reserve((size_t)qt.n * DP * nb);
+  k_scale_points<<<ceil_div((long long)qt.n * DP * nb, 256), 256, 0, s>>>(
+    qt.xs.p, qt.n, D_, DP, nb, rt_.centroid.p, sv, mufu_ ? kSqrtLog2e : 1.0, xq_.p);
+  CK_LAUNCH();
+  const double* xq = xq_.p;
+  const double* xr = xq_.p;
+  if (&qt != &rt_) {
+    xr_.reserve((size_t)rt_.n * DP * nb);
+    k_scale_points<<<ceil_div((long long)rt_.n * DP * nb, 256), 256, 0, s>>>(
+      rt_.xs.p, rt_.n, D_, DP, nb, rt_.centroid.p, sv, mufu_ ? kSqrtLog2e : 1.0, xr_.p);
     CK_LAUNCH();
-    xq = xr = xq_.p;
-    if (&qt != &rt_) {
-      xr_.reserve((size_t)rt_.n * DP * nb);
-      k_scale_points<<<ceil_div((long long)rt_.n * DP * nb, 256), 256, 0, s>>>(
-        rt_.xs.p, rt_.n, D_, DP, nb, rt_.centroid.p, sv, mufu_ ? kSqrtLog2e : 1.0, xr_.p);
-      CK_LAUNCH();
-      xr = xr_.p;
-    }
+    xr = xr_.p;
   }
   CK(cudaEventRecord(ev_[9], s));
   bnext_.reserve(1);
-  if (ntasks)
-    launch_base(D_, grid_warps(ntasks), s, Q, R, K, reinterpret_cast<const BTask*>(tasks_.p), ntasks,
-                sB_.p, reinterpret_cast<const int2*>(brec_.p), xq, xr, qt.n, rt_.n, bpart_.p,
-                bnext_.p, mufu_exp() ? 1 : 0);
+  launch_base(D_, s, Q, R, K, reinterpret_cast<const BTask*>(tasks_.p), bc_.p + 5, capTask_, sB_.p,
+              reinterpret_cast<const int2*>(brec_.p), xq, xr, qt.n, rt_.n, bpart_.p, bnext_.p,
+              mufu_exp() ? 1 : 0);
   CK(cudaEventRecord(ev_[6], s));
   s_ff_.reserve((size_t)qt.n * nb);
-  if (nF_) {
+  if (cfg_.mode == 1) {
     const int gw = grid_warps(nlb);
     const int pm = ser_.pmax;
 #define FF_T(DD, PP)                                                                              \
@@ -1520,18 +1571,9 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
   CK(cudaEventRecord(ev_[7], s));
   k_finalize<<<ceil_div((long long)qt.n * nb, 128), 128, 0, s>>>(
     g, Q, K, nb, leaf_of_pos_.p, qt.perm.p, qt.n, L_.p, Lord_.p, cntB_.p, leaf_task_.p,
-    leaf_runs_.p, bpart_.p,
-    s_ff_.p, sv, cfg_.local_pushdown == 0, d_out);
+    leaf_runs_.p, bpart_.p, s_ff_.p, sv, cfg_.local_pushdown == 0, d_out);
   CK_LAUNCH();
   CK(cudaEventRecord(ev_[8], s));
-  CK(cudaStreamSynchronize(s));
-  CK(cudaEventElapsedTime(&tim_.traverse_ms, ev_[2], ev_[3]));
-  CK(cudaEventElapsedTime(&tim_.moments_ms, ev_[3], ev_[4]));
-  CK(cudaEventElapsedTime(&tim_.local_ms, ev_[4], ev_[5]));
-  CK(cudaEventElapsedTime(&tim_.base_ms, ev_[9], ev_[6]));
-  CK(cudaEventElapsedTime(&tim_.farfield_ms, ev_[6], ev_[7]));
-  CK(cudaEventElapsedTime(&tim_.final_ms, ev_[7], ev_[8]));
-  CK(cudaEventElapsedTime(&tim_.total_ms, ev_[2], ev_[8]));
 }
 
 void Engine::cv_reduce(const double* d_sums, const double* h, const double* d_conv,

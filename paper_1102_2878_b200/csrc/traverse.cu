@@ -920,14 +920,7 @@ void launch_level(const TravArgs& a, int D, cudaStream_t s, cudaGraphConditional
   CK_LAUNCH();
 }
 
-__global__ void k_scatter_items(const Item* in, int n, const int* noff, Item* out)
-{
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    const Item it = in[i];
-    out[noff[it.key] + it.rank] = it;
-  }
-}
+
 
 }  // namespace
 
@@ -1033,6 +1026,35 @@ void Engine::run_levels(const void* args, const std::vector<const void*>& sig)
   }
 }
 
+__global__ void k_trav_publish(const TravState* st, int* bc)
+{  // BatchCounts: nF, nDT, nB, traversal overflow (an overflowed batch is rerun: its
+   // item counts read as zero so nothing downstream follows a half-written list)
+  const int ovf = st->overflow;
+  bc[0] = ovf ? 0 : st->nF;
+  bc[1] = ovf ? 0 : st->nDT;
+  bc[2] = ovf ? 0 : st->nB;
+  bc[3] = ovf;
+}
+
+__global__ void k_trav_clear_on_overflow(const int* bc, int* cntF, int* cntDT, int* cntB, int KB)
+{
+  if (!bc[3]) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < KB; i += gridDim.x * blockDim.x)
+    cntF[i] = cntDT[i] = cntB[i] = 0;
+}
+
+__global__ void k_scatter_dev(const Item* in, const int* n, int cap, const int* noff, Item* out)
+{
+  const int m = min(*n, cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const Item it = in[i];
+    out[noff[it.key] + it.rank] = it;
+  }
+}
+
+// Launches the whole traversal of a batch and the counting sorts of its work items
+// WITHOUT a host round trip: the counts stay on the device (bc_), the host reads them
+// once at the end of the batch (traverse_finish) and reruns on overflow.
 void Engine::traverse(const DevTree& qt, const double* h, int nb)
 {
   const int K = qt.nodes;
@@ -1057,119 +1079,149 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     capDT_ = std::max(capDT_, std::max(4096, 2 * kb));
     capB_ = std::max(capB_, std::max(1 << 16, 16 * kb));
   }
-  for (int attempt = 0;; ++attempt) {
-    for (int b = 0; b < 2; ++b) {
-      fq_[b].reserve(capE_);
-      foff_[b].reserve(capE_);
-      flen_[b].reserve(capE_);
-      fbase_[b].reserve(capE_);
-      fr_[b].reserve(capP_);
-      pent_[b].reserve(capP_);
-    }
-    pglo_.reserve(capE_);
-    pkmax_.reserve(capP_);
-    pkmin_.reserve(capP_);
-    dec_.reserve(capP_);
-    cnt_.reserve(capE_);
-    cntoff_.reserve(capE_);
-    childlen_.reserve(capE_);
-    newbase_.reserve(capE_);
-    ctsum_.reserve(kScanTiles);
-    ctoff_.reserve(kScanTiles);
-    itF_.reserve(capF_);
-    itDT_.reserve(capDT_);
-    itB_.reserve(capB_);
+  for (int b = 0; b < 2; ++b) {
+    fq_[b].reserve(capE_);
+    foff_[b].reserve(capE_);
+    flen_[b].reserve(capE_);
+    fbase_[b].reserve(capE_);
+    fr_[b].reserve(capP_);
+    pent_[b].reserve(capP_);
+  }
+  pglo_.reserve(capE_);
+  pkmax_.reserve(capP_);
+  pkmin_.reserve(capP_);
+  dec_.reserve(capP_);
+  cnt_.reserve(capE_);
+  cntoff_.reserve(capE_);
+  childlen_.reserve(capE_);
+  newbase_.reserve(capE_);
+  ctsum_.reserve(kScanTiles);
+  ctoff_.reserve(kScanTiles);
+  itF_.reserve(capF_);
+  itDT_.reserve(capDT_);
+  itB_.reserve(capB_);
+  bc_.reserve(16);
+  CK(cudaMemsetAsync(bc_.p, 0, sizeof(int) * 16, s));
 
-    TravArgs a{};
-    a.Q = view_of(qt);
-    a.R = view_of(rt_);
-    a.selfq = &qt == &rt_ ? 1 : 0;
-    a.D = D_;
-    a.pmax = ser_.pmax;
-    a.cost = cfg_.cost_model;
-    a.series = cfg_.mode == 1;
-    a.T = T;
-    a.st = ds;
-    for (int b = 0; b < 2; ++b) {
-      a.fq[b] = fq_[b].p;
-      a.foff[b] = foff_[b].p;
-      a.flen[b] = flen_[b].p;
-      a.fr[b] = fr_[b].p;
-      a.fbase[b] = fbase_[b].p;
-      a.pent[b] = pent_[b].p;
-    }
-    a.glo = pglo_.p;
-    a.pkmax = pkmax_.p;
-    a.pkmin = pkmin_.p;
-    a.dec = dec_.p;
-    a.cnt = cnt_.p;
-    a.cntoff = cntoff_.p;
-    a.tsum = ctsum_.p;
-    a.toff = ctoff_.p;
-    a.childlen = childlen_.p;
-    a.newbase = newbase_.p;
-    a.L = L_.p;
-    a.Lord = Lord_.p;
-    a.itF = itF_.p;
-    a.itDT = itDT_.p;
-    a.itB = itB_.p;
-    a.cntF = cntF_.p;
-    a.cntDT = cntDT_.p;
-    a.cntB = cntB_.p;
-    lvlcnt_.reserve(kMaxLevels);
-    CK(cudaMemsetAsync(lvlcnt_.p, 0, sizeof(Cnt) * kMaxLevels, s));
-    a.lvlcnt = lvlcnt_.p;
-    lvlep_.reserve(kMaxLevels);
-    CK(cudaMemsetAsync(lvlep_.p, 0, sizeof(unsigned long long) * kMaxLevels, s));
-    a.lvlep = lvlep_.p;
-    static const bool tracing = std::getenv("DFGTB_TRACE") != nullptr;
-    if (tracing) {
-      trace_.reserve(512 * 6);
-      CK(cudaMemsetAsync(trace_.p, 0, sizeof(unsigned long long) * 512 * 6, s));
-      a.trace = trace_.p;
-    }
-    const std::vector<const void*> sig = {
-      a.Q.lo, a.Q.hi, a.Q.cen, a.Q.side, a.Q.left, a.Q.right, a.Q.count, a.Q.begin,
-      a.R.lo, a.R.hi, a.R.side, a.R.left, a.R.right, a.R.count,
-      a.st, a.pent[0], a.pent[1], a.glo, a.fq[0], a.fq[1], a.foff[0], a.foff[1], a.flen[0], a.flen[1], a.fr[0], a.fr[1],
-      a.fbase[0], a.fbase[1], a.pkmax, a.pkmin, a.dec, a.cnt, a.cntoff, a.tsum, a.toff,
-      a.childlen, a.newbase, a.L, a.Lord, a.itF, a.itDT, a.itB, a.cntF, a.cntDT, a.cntB };
+  TravArgs a{};
+  a.Q = view_of(qt);
+  a.R = view_of(rt_);
+  a.selfq = &qt == &rt_ ? 1 : 0;
+  a.D = D_;
+  a.pmax = ser_.pmax;
+  a.cost = cfg_.cost_model;
+  a.series = cfg_.mode == 1;
+  a.T = T;
+  a.st = ds;
+  for (int b = 0; b < 2; ++b) {
+    a.fq[b] = fq_[b].p;
+    a.foff[b] = foff_[b].p;
+    a.flen[b] = flen_[b].p;
+    a.fr[b] = fr_[b].p;
+    a.fbase[b] = fbase_[b].p;
+    a.pent[b] = pent_[b].p;
+  }
+  a.glo = pglo_.p;
+  a.pkmax = pkmax_.p;
+  a.pkmin = pkmin_.p;
+  a.dec = dec_.p;
+  a.cnt = cnt_.p;
+  a.cntoff = cntoff_.p;
+  a.tsum = ctsum_.p;
+  a.toff = ctoff_.p;
+  a.childlen = childlen_.p;
+  a.newbase = newbase_.p;
+  a.L = L_.p;
+  a.Lord = Lord_.p;
+  a.itF = itF_.p;
+  a.itDT = itDT_.p;
+  a.itB = itB_.p;
+  a.cntF = cntF_.p;
+  a.cntDT = cntDT_.p;
+  a.cntB = cntB_.p;
+  lvlcnt_.reserve(kMaxLevels);
+  CK(cudaMemsetAsync(lvlcnt_.p, 0, sizeof(Cnt) * kMaxLevels, s));
+  a.lvlcnt = lvlcnt_.p;
+  lvlep_.reserve(kMaxLevels);
+  CK(cudaMemsetAsync(lvlep_.p, 0, sizeof(unsigned long long) * kMaxLevels, s));
+  a.lvlep = lvlep_.p;
+  static const bool tracing = std::getenv("DFGTB_TRACE") != nullptr;
+  if (tracing) {
+    trace_.reserve(512 * 6);
+    CK(cudaMemsetAsync(trace_.p, 0, sizeof(unsigned long long) * 512 * 6, s));
+    a.trace = trace_.p;
+  }
+  const std::vector<const void*> sig = {
+    a.Q.lo, a.Q.hi, a.Q.cen, a.Q.side, a.Q.left, a.Q.right, a.Q.count, a.Q.begin,
+    a.R.lo, a.R.hi, a.R.side, a.R.left, a.R.right, a.R.count,
+    a.st, a.pent[0], a.pent[1], a.glo, a.fq[0], a.fq[1], a.foff[0], a.foff[1], a.flen[0], a.flen[1], a.fr[0], a.fr[1],
+    a.fbase[0], a.fbase[1], a.pkmax, a.pkmin, a.dec, a.cnt, a.cntoff, a.tsum, a.toff,
+    a.childlen, a.newbase, a.L, a.Lord, a.itF, a.itDT, a.itB, a.cntF, a.cntDT, a.cntB };
 
-    CK(cudaMemsetAsync(L_.p, 0, sizeof(double) * KB * T, s));
-    for (DevBuf<int>* b : { &Lord_, &cntF_, &cntDT_, &cntB_ })
-      CK(cudaMemsetAsync(b->p, 0, sizeof(int) * KB, s));
-    hs->eps = mufu_ ? cfg_.epsilon - kMufuCharge : cfg_.epsilon;  // MUFU exp's error is charged
-    hs->ntot = (double)n_;
-    hs->nslots = nb;
-    hs->K = K;
-    for (int b = 0; b < nb; ++b) {
-      hs->h[b] = h[b];
-      hs->scale[b] = -1.0 / (2.0 * h[b] * h[b]);
-    }
-    hs->capE = capE_;
-    hs->capP = capP_;
-    hs->capF = capF_;
-    hs->capDT = capDT_;
-    hs->capB = capB_;
-    CK(cudaMemcpyAsync(ds, hs, sizeof(TravState), cudaMemcpyHostToDevice, s));
-    k_trav_init<<<1, 64, 0, s>>>(a);
+  CK(cudaMemsetAsync(L_.p, 0, sizeof(double) * KB * T, s));
+  for (DevBuf<int>* b : { &Lord_, &cntF_, &cntDT_, &cntB_ })
+    CK(cudaMemsetAsync(b->p, 0, sizeof(int) * KB, s));
+  hs->eps = mufu_ ? cfg_.epsilon - kMufuCharge : cfg_.epsilon;  // MUFU exp's error is charged
+  hs->ntot = (double)n_;
+  hs->nslots = nb;
+  hs->K = K;
+  for (int b = 0; b < nb; ++b) {
+    hs->h[b] = h[b];
+    hs->scale[b] = -1.0 / (2.0 * h[b] * h[b]);
+  }
+  hs->capE = capE_;
+  hs->capP = capP_;
+  hs->capF = capF_;
+  hs->capDT = capDT_;
+  hs->capB = capB_;
+  CK(cudaMemcpyAsync(ds, hs, sizeof(TravState), cudaMemcpyHostToDevice, s));
+  k_trav_init<<<1, 64, 0, s>>>(a);
+  CK_LAUNCH();
+  run_levels(&a, sig);
+  k_trav_publish<<<1, 1, 0, s>>>(ds, bc_.p);
+  CK_LAUNCH();
+  k_trav_clear_on_overflow<<<148, 256, 0, s>>>(bc_.p, cntF_.p, cntDT_.p, cntB_.p, (int)KB);
+  CK_LAUNCH();
+  trav_nb_ = nb;
+  trav_trace_ = a.trace != nullptr;
+
+  // counting sort of the items by key (stable: level order, then emit order)
+  auto sort_items = [&](DevBuf<Item>& in, int cap, const int* dn, DevBuf<int>& cnt,
+                        DevBuf<int>& off, DevBuf<Item>& out) {
+    off.reserve((size_t)KB + 1);
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, cnt.p, off.p, (int)KB, s);
+    scan_tmp_.reserve(need + 256);
+    size_t have = scan_tmp_.cap;
+    cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, cnt.p, off.p, (int)KB, s);
+    out.reserve(cap);
+    k_scatter_dev<<<148 * 4, 256, 0, s>>>(in.p, dn, cap, off.p, out.p);
     CK_LAUNCH();
-    run_levels(&a, sig);
-    CK(cudaMemcpyAsync(hs, ds, sizeof(TravState), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (!use_persistent_ && use_graph_) launch_counter() += (uint64_t)hs->levels * kLevelKernels;
-    if (a.trace) {  // per level: classify | scan | emit (microseconds)
-      std::vector<unsigned long long> tr(512 * 6);
-      CK(cudaMemcpy(tr.data(), a.trace, sizeof(unsigned long long) * tr.size(),
-                    cudaMemcpyDeviceToHost));
-      for (int L = 0; L < std::min(hs->levels, 511); ++L)
-        std::fprintf(stderr, "DFGTB_TRACE level %d: entries %llu pairs %llu classify+lookback %.1f us, emit+sync %.1f us\n",
-                     L, tr[2048 + L * 2], tr[2048 + L * 2 + 1], (tr[L * 4 + 1] - tr[L * 4]) * 1e-3,
-                     (tr[L * 4 + 2] - tr[L * 4 + 1]) * 1e-3);
-    }
-    if (hs->overflow == 2) throw CudaError("traversal exceeded 1024 levels");
-    if (!hs->overflow) break;
-    if (attempt > 10) throw OutOfMemory("traversal buffers keep overflowing");
+  };
+  sort_items(itF_, capF_, bc_.p + 0, cntF_, offF_, sF_);
+  sort_items(itDT_, capDT_, bc_.p + 1, cntDT_, offDT_, sDT_);
+  sort_items(itB_, capB_, bc_.p + 2, cntB_, offB_, sB_);
+}
+
+// After the batch's final synchronisation: statistics, and the traversal verdict
+// (false: buffers overflowed and were regrown -- the batch must be rerun).
+bool Engine::traverse_finish()
+{
+  TravState* hs = static_cast<TravState*>(hst_);
+  const TravState* ds = reinterpret_cast<const TravState*>(dst_.p);
+  CK(cudaMemcpy(hs, ds, sizeof(TravState), cudaMemcpyDeviceToHost));
+  const int nb = trav_nb_;
+  if (!use_persistent_ && use_graph_) launch_counter() += (uint64_t)hs->levels * kLevelKernels;
+  if (trav_trace_) {  // per level: classify | scan | emit (microseconds)
+    std::vector<unsigned long long> tr(512 * 6);
+    CK(cudaMemcpy(tr.data(), trace_.p, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
+    for (int L = 0; L < std::min(hs->levels, 511); ++L)
+      std::fprintf(stderr, "DFGTB_TRACE level %d: entries %llu pairs %llu classify+lookback %.1f us, emit+sync %.1f us\n",
+                   L, tr[2048 + L * 2], tr[2048 + L * 2 + 1], (tr[L * 4 + 1] - tr[L * 4]) * 1e-3,
+                   (tr[L * 4 + 2] - tr[L * 4 + 1]) * 1e-3);
+  }
+  if (hs->overflow == 2) throw CudaError("traversal exceeded 1024 levels");
+  if (hs->overflow) {
     const Cnt l = hs->lvl;
     auto grow = [](int cap, long long need) {
       if (need > INT32_MAX / 2) throw OutOfMemory("traversal exceeds 2^30 entries");
@@ -1180,6 +1232,7 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     capF_ = grow(capF_, (long long)hs->nF + l.f);
     capDT_ = grow(capDT_, (long long)hs->nDT + l.dt);
     capB_ = grow(capB_, (long long)hs->nB + l.b);
+    return false;
   }
   slot_stats_.assign(nb, Stats{});
   for (int b = 0; b < nb; ++b) {
@@ -1197,24 +1250,7 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   nF_ = hs->nF;
   nDT_ = hs->nDT;
   nB_ = hs->nB;
-
-  // counting sort of the items by key (stable: level order, then emit order)
-  auto sort_items = [&](DevBuf<Item>& in, long long nitems, DevBuf<int>& cnt, DevBuf<int>& off,
-                        DevBuf<Item>& out) {
-    off.reserve((size_t)KB + 1);
-    if (nitems == 0) return;
-    size_t need = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need, cnt.p, off.p, (int)KB, s);
-    scan_tmp_.reserve(need + 256);
-    size_t have = scan_tmp_.cap;
-    cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, cnt.p, off.p, (int)KB, s);
-    out.reserve(nitems);
-    k_scatter_items<<<ceil_div(nitems, 256), 256, 0, s>>>(in.p, (int)nitems, off.p, out.p);
-    CK_LAUNCH();
-  };
-  sort_items(itF_, nF_, cntF_, offF_, sF_);
-  sort_items(itDT_, nDT_, cntDT_, offDT_, sDT_);
-  sort_items(itB_, nB_, cntB_, offB_, sB_);
+  return true;
 }
 
 }  // namespace dfgtb
