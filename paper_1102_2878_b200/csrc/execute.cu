@@ -492,10 +492,12 @@ template <bool CLAMP = false>
 __device__ __forceinline__ double exp2_neg_fixed(double t, unsigned fbits)
 {
   int lo = __double2loint(t);
-  if constexpr (CLAMP) {  // z > 1021 -> 2^-1021 (only where the traversal pays for it)
+  bool under = false;
+  if constexpr (CLAMP) {  // z > 1021 -> 0 (terms < 2^-1021; only where the traversal pays for it)
     const unsigned hi = (unsigned)__double2hiint(t);  // kMufuHi - 1 below z = 896 - b
     const int lmax = (125 << 20) | 0xFFFFF;
-    lo = hi > kMufuHi || (hi == kMufuHi && (unsigned)lo > (unsigned)lmax) ? lmax : lo;
+    under = hi > kMufuHi || (hi == kMufuHi && (unsigned)lo > (unsigned)lmax);
+    lo = under ? lmax : lo;
   }
   // fbits = 0x4B000000 held in a register (one LOP3: (lo & mask) | fbits)
   const float x = __uint_as_float(((unsigned)lo & 0xFFFFFu) | fbits);  // 2^23 + f
@@ -504,6 +506,8 @@ __device__ __forceinline__ double exp2_neg_fixed(double t, unsigned fbits)
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(a));
   const unsigned G = __float_as_uint(g);
   const unsigned hi = (G >> 3) - ((unsigned)lo & 0xFFF00000u);
+  if constexpr (CLAMP)
+    if (under) return 0.0;
   return __hiloint2double((int)hi, (int)(G << 29));
 }
 constexpr double kMufuMagic = 6442450944.0 - 896.0 + kMufuBias * 0x1p-20;  // M - 896 + b 2^-20
@@ -915,6 +919,20 @@ __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
       else base_groups<DT, false>(rs, n, qs, qsum, qc, tab, mufu ? kLn2 : 1.0, lane);
       __syncwarp();
     }
+    // Q = R: the run holding the query leaf itself contains every query's self pair,
+    // whose MUFU value is 1 +- O(2^-20).  Replace it by exactly K(0) = 1 (the LOO CV
+    // scores subtract exactly 1): recompute it with the loop's own operations and order.
+    if (mf && xq == xr && __any_sync(0xffffffffu, lane < nit && rc.x == qb) && lane < qc) {
+      constexpr int DM = MPt<DT>::DM;
+      unsigned fbits;
+      asm volatile("mov.b32 %0, 0x4B000000;" : "=r"(fbits));
+      const double qq = qs[lane * DM + DT];
+      double tq = (kMufuMagic + qq) + qq;
+#pragma unroll
+      for (int d = 0; d < DT; ++d) tq = fma(-2.0 * qs[lane * DM + d], qs[lane * DM + d], tq);
+      qsum[lane] += 1.0 - exp2_neg_fixed<false>(tq, fbits);
+    }
+    __syncwarp();
     if (lane < qc) part[(size_t)w * 32 + lane] = qsum[lane];
     __syncwarp();
     w = __shfl_sync(0xffffffffu, wn, 0);
@@ -1620,7 +1638,7 @@ void naive_device(const double* d_q, size_t nq, const double* d_r, size_t nr, in
 // Exhaustive error of exp2_neg_fixed over every fixed-point argument the fast base
 // case can form: t = M - 896 + u 2^-20 for every u in [0, 1022 2^20), value
 // 2^-(u - b) 2^-20, against libdevice exp2 in FP64; and of the clamped variant beyond
-// z = 1021 (value 2^-(1021 + f)).  Max relative error as ordered bits in *out.
+// z = 1021 (value exactly 0).  Max relative error as ordered bits in *out.
 __global__ void k_mufu_check(unsigned long long* out)
 {
   unsigned long long worst = 0;
@@ -1634,7 +1652,8 @@ __global__ void k_mufu_check(unsigned long long* out)
       want = exp2(-((double)i - kMufuBias) * 0x1p-20);
     } else {  // clamp: any z >= 1022 - b -> 2^-(1021 + frac of the clamp point)
       got = exp2_neg_fixed<true>(t + 8192.0 * (double)(i & 7), 0x4B000000u);
-      want = exp2(-((double)((125u << 20) | 0xFFFFFu) + (896u << 20) - kMufuBias) * 0x1p-20);
+      if (got != 0.0) worst = 0x7FF0000000000000ull;  // clamped terms must be exactly 0
+      continue;
     }
     const double rel = fabs(got - want) / want;
     const unsigned long long b = (unsigned long long)__double_as_longlong(rel);

@@ -295,7 +295,7 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
         kind = kB;
         // bit 0: every pair of this leaf pair has y = d^2/2h^2 <= 708 (K(d_max) >= e^-707.97),
         // the base case may use its fast exp without underflow handling; bit 1: terms
-        // below 2^-1021 may be clamped to 2^-1021 (absolute error <= |R| 2^-1021 against a
+        // below 2^-1021 may be dropped (absolute error <= |R| 2^-1021 against a
         // sum >= 1 (Q = R) or >= G^l >= 1e-290: below 1e-280 relative); the MUFU fixed
         // point also needs the query leaf's diameter <= 1000 in z units (sq sqrt(D)
         // sqrt(log2 e) / (h sqrt 2), sqrt(log2 e / 2) < 0.8494)
@@ -665,7 +665,7 @@ __device__ __forceinline__ void pairs_decide(const TravArgs& a, const TravState&
         kind = kB;
         // bit 0: every pair of this leaf pair has y = d^2/2h^2 <= 708 (K(d_max) >= e^-707.97),
         // the base case may use its fast exp without underflow handling; bit 1: terms
-        // below 2^-1021 may be clamped to 2^-1021 (absolute error <= |R| 2^-1021 against a
+        // below 2^-1021 may be dropped (absolute error <= |R| 2^-1021 against a
         // sum >= 1 (Q = R) or >= G^l >= 1e-290: below 1e-280 relative); the MUFU fixed
         // point also needs the query leaf's diameter <= 1000 in z units (sq sqrt(D)
         // sqrt(log2 e) / (h sqrt 2), sqrt(log2 e / 2) < 0.8494)

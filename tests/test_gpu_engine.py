@@ -274,3 +274,31 @@ def test_mufu_path_meets_eps(dfgtb, orc, k):
         h = s * w.h_s
         got = dfgtb.dfgt_kde(w.refs, w.refs, h, dfgtb.EngineConfig(epsilon=0.01, leaf_threshold=32))
         _check(got, orc.naive_kde(w.refs, w.refs, h), 0.01)
+
+
+def test_base_exp_mode_selection(dfgtb, orc, monkeypatch):
+    """eps >= 1e-4 runs the MUFU base case (charged), smaller eps or DFGTB_EXACT_EXP the
+    FP64 exp; both meet eps, and the MUFU self term is exactly K(0) = 1 (Q = R leave-
+    one-out sums G - 1 agree with the FP64 engine where they are well above eps G)."""
+    from paper_1102_2878_b200 import _capi
+    w = datagen.config(2, scale_n=0.04)
+    h = w.h_s
+    with dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(epsilon=0.01, leaf_threshold=32)) as e:
+        assert _capi.lib.dfgtb_base_exp_mode(e.handle) == 1
+        fast = e.compute(None, h)
+    with dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(epsilon=1e-5, leaf_threshold=32)) as e:
+        assert _capi.lib.dfgtb_base_exp_mode(e.handle) == 0
+    monkeypatch.setenv("DFGTB_EXACT_EXP", "1")
+    with dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(epsilon=0.01, leaf_threshold=32)) as e:
+        assert _capi.lib.dfgtb_base_exp_mode(e.handle) == 0
+        exact_path = e.compute(None, h)
+    exact = orc.naive_kde(w.refs, w.refs, h)
+    _check(fast, exact, 0.01)
+    _check(exact_path, exact, 0.01)
+    # tiny bandwidth: every query's sum is its self term plus a tiny rest
+    tiny = 1e-3 * w.h_s
+    with dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(epsilon=0.01, leaf_threshold=32)) as e:
+        monkeypatch.delenv("DFGTB_EXACT_EXP")
+        g = e.compute(None, tiny)
+    ex = orc.naive_kde(w.refs, w.refs, tiny)
+    assert np.all(g >= 1.0) and np.max(np.abs((g - 1.0) - (ex - 1.0))) <= 0.01 * np.max(ex)
