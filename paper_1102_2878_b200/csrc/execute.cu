@@ -277,6 +277,169 @@ __global__ void __launch_bounds__(kLocThreads) k_local_chunks_t(DevSeries g, Tre
 // warp of a key's first item does the work), lanes over terms.  Every term sums its
 // chunks in item order (8 loads in flight), so the result does not depend on the
 // launch shape.
+// Warp reduce-scatter of 32 per-lane values: afterwards lane l holds the sum over the
+// warp of value l (five halving exchange steps, fixed order).
+__device__ __forceinline__ double warp_reduce_scatter32(double (&v)[32], int lane)
+{
+#pragma unroll
+  for (int st = 0; st < 5; ++st) {
+    const int off = 16 >> st;
+    const bool up = lane & off;
+    const int h = 16 >> st;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i < h) {
+        const double send = up ? v[i] : v[i + h];
+        const double keep = up ? v[i + h] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+  }
+  return v[0];
+}
+
+// Specialised D/T chunks for the default tables (p_max == PM): ONE WARP per chunk.
+//  D: lanes over the chunk's points, Hermite products of every multi-index in
+//     registers (one exp(-|t|^2) per point), warp reduce-scatter per 32 terms.
+//  T: far-to-local of the reference node's moments contracted one dimension at a time
+//     in the warp's shared scratch: V <- sum_{a_d} V[.., a_d, ..] H_d[a_d + b_d]
+//     (D stages of PM^D outputs x PM FMAs instead of PM^{2D} products).
+// Both write the same unsigned partial table (term layout, terms < order^D) as
+// dev_direct_local_partial / dev_f2l_block.
+constexpr int kLocWarps = 4;
+template <int D, int PM>
+__global__ void __launch_bounds__(kLocWarps * 32) k_local_chunks_w(
+  DevSeries g, TreeView Q, TreeView R, int K, const Item* items, const LChunk* ch, const int* nchp,
+  int chcap, const double* Mt, SlotView sv, double* part)
+{
+  constexpr int NP = ipow_c(PM, D), HL = 2 * PM - 1, NB = (NP + 31) / 32;
+  __shared__ int tp[NP];
+  __shared__ double wsc[kLocWarps][2 * NP + D * HL];
+  for (int p = threadIdx.x; p < NP; p += blockDim.x) tp[p] = g.term_of_pos[p];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* V0 = wsc[wib];
+  double* V1 = V0 + NP;
+  double* H = V1 + NP;
+  const int nch = min(*nchp, chcap);
+  for (int c = blockIdx.x * kLocWarps + wib; c < nch; c += gridDim.x * kLocWarps) {
+    const LChunk lc = ch[c];
+    const Item it = items[lc.item];
+    const int slot = it.key / K, node = it.key - slot * K;
+    const int kind = it.code >> 8, order = it.code & 0xff;
+    const double s = sv.s[slot];
+    double* P = part + (size_t)c * g.T;
+    const double* qc = Q.cen + (size_t)node * D;
+    if (kind == kD) {
+      double acc[NB * 32];
+#pragma unroll
+      for (int p = 0; p < NB * 32; ++p) acc[p] = 0.0;
+      double cq[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) cq[d] = qc[d];
+      for (int j = lane; j < lc.n; j += 32) {
+        const double* rp = R.xs + (size_t)(lc.start + j) * D;
+        double Hh[D][PM];
+        double tt = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const double t = (cq[d] - rp[d]) * s;
+          tt = fma(t, t, tt);
+          Hh[d][0] = 1.0;
+          if (PM > 1) Hh[d][1] = 2.0 * t;
+#pragma unroll
+          for (int k = 1; k + 1 < PM; ++k) Hh[d][k + 1] = fma(2.0 * t, Hh[d][k], -2.0 * k * Hh[d][k - 1]);
+        }
+        const double e = exp(-tt);
+#pragma unroll
+        for (int k = 0; k < PM; ++k) Hh[0][k] *= e;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double f = 1.0;
+          int rest = p;
+#pragma unroll
+          for (int d = D - 1; d >= 0; --d) {
+            f *= Hh[d][rest % PM];
+            rest /= PM;
+          }
+          acc[p] += f;
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        double v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = acc[b * 32 + i];
+        const double tot = warp_reduce_scatter32(v, lane);
+        const int p = b * 32 + lane;
+        if (p < NP) {
+          int rest = p, mx = 0;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            mx = max(mx, rest % PM);
+            rest /= PM;
+          }
+          if (mx < order) P[tp[p]] = tot;
+        }
+      }
+    } else {
+      // Hermite function rows at t = (c_Q - c_R) s, one lane per dimension
+      const int r = it.r;
+      if (lane < D) {
+        const double t = (qc[lane] - R.cen[(size_t)r * D + lane]) * s;
+        double* h = H + lane * HL;
+        h[0] = exp(-t * t);
+        h[1] = 2.0 * t * h[0];
+#pragma unroll
+        for (int k = 1; k + 1 < HL; ++k) h[k + 1] = 2.0 * t * h[k] - 2.0 * k * h[k - 1];
+      }
+      // scaled, truncated moments M'_a = s^|a| M~_a (a_d < order), position layout
+      const double* sp = sv.spow + (size_t)slot * kSPow;
+      for (int p = lane; p < NP; p += 32) {
+        int rest = p, mx = 0, deg = 0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const int dg = rest % PM;
+          mx = max(mx, dg);
+          deg += dg;
+          rest /= PM;
+        }
+        V0[p] = mx < order ? Mt[(size_t)r * NP + p] * sp[deg] : 0.0;
+      }
+      __syncwarp();
+      double* src = V0;
+      double* dst = V1;
+#pragma unroll
+      for (int d = D - 1; d >= 0; --d) {
+        const int stride = ipow_c(PM, D - 1 - d);
+        const double* hd = H + d * HL;
+        for (int p = lane; p < NP; p += 32) {
+          const int bd = (p / stride) % PM;
+          const int base = p - bd * stride;
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < PM; ++k) acc = fma(src[base + k * stride], hd[k + bd], acc);
+          dst[p] = acc;
+        }
+        __syncwarp();
+        double* tmp = src;
+        src = dst;
+        dst = tmp;
+      }
+      for (int p = lane; p < NP; p += 32) {
+        int rest = p, mx = 0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          mx = max(mx, rest % PM);
+          rest /= PM;
+        }
+        if (mx < order) P[tp[p]] = src[p];
+      }
+      __syncwarp();
+    }
+  }
+}
+
 __global__ void k_local_reduce(DevSeries g, const int* nitems_p, int cap, const int* cnt,
                                const int* off, const Item* items, const int* choff,
                                const double* part, double* L, int* Lord)
@@ -1026,12 +1189,44 @@ __global__ void __launch_bounds__(kBlock) k_farfield(DevSeries g, TreeView Q, Tr
 // contracted one dimension at a time (last dimension first; position layout p =
 // sum_d a_d PM^(D-1-d)) over the truncation cube a_d < order: PM^D + PM^(D-1) + ..
 // FMAs instead of (D + 1) PM^D multiplies.  The moments are warp-uniform 16-byte loads.
+template <int D, int PM, int O>
+__device__ __forceinline__ double ff_eval_o(const double* Mt, const double (&h)[D][PM])
+{  // contraction over the truncation cube a_d < O (moments in position layout, stride PM)
+  constexpr int NO = ipow_c(O, D);
+  double v[NO];
+#pragma unroll
+  for (int p = 0; p < NO; ++p) {
+    int rest = p, pos = 0, mul = 1;
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) {
+      pos += (rest % O) * mul;
+      rest /= O;
+      mul *= PM;
+    }
+    v[p] = Mt[pos];
+  }
+  int len = NO;
+#pragma unroll
+  for (int d = D - 1; d >= 0; --d) {
+    len /= O;
+#pragma unroll
+    for (int r = 0; r < ipow_c(O, D - 1); ++r) {
+      if (r < len) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = O - 1; k >= 0; --k) acc = fma(v[r * O + k], h[d][k], acc);
+        v[r] = acc;
+      }
+    }
+  }
+  return v[0];
+}
+
 template <int D, int PM>
 __device__ __forceinline__ double ff_eval_t(const double* Mt, const double* c, const double* q,
                                             double s, int order,
                                             const double (&spw)[D * (PM - 1) + 1])
 {
-  constexpr int NP = ipow_c(PM, D);
   double h[D][PM];
   double tt = 0.0;
 #pragma unroll
@@ -1045,35 +1240,18 @@ __device__ __forceinline__ double ff_eval_t(const double* Mt, const double* c, c
 #pragma unroll
     for (int k = 1; k < PM; ++k) h[d][k] *= spw[k];
   }
-  double v[NP];
-  if constexpr (NP % 2 == 0) {
-    const double2* M2 = reinterpret_cast<const double2*>(Mt);
-#pragma unroll
-    for (int p = 0; p < NP / 2; ++p) {
-      const double2 m2 = M2[p];
-      v[2 * p] = m2.x;
-      v[2 * p + 1] = m2.y;
-    }
-  } else {
-#pragma unroll
-    for (int p = 0; p < NP; ++p) v[p] = Mt[p];
+  double v;
+  switch (order) {  // warp-uniform: one item per iteration for the whole warp
+  case 1: v = ff_eval_o<D, PM, 1>(Mt, h); break;
+  case 2: v = ff_eval_o<D, PM, (PM >= 2 ? 2 : 1)>(Mt, h); break;
+  case 3: v = ff_eval_o<D, PM, (PM >= 3 ? 3 : 1)>(Mt, h); break;
+  case 4: v = ff_eval_o<D, PM, (PM >= 4 ? 4 : 1)>(Mt, h); break;
+  case 5: v = ff_eval_o<D, PM, (PM >= 5 ? 5 : 1)>(Mt, h); break;
+  case 6: v = ff_eval_o<D, PM, (PM >= 6 ? 6 : 1)>(Mt, h); break;
+  case 7: v = ff_eval_o<D, PM, (PM >= 7 ? 7 : 1)>(Mt, h); break;
+  default: v = ff_eval_o<D, PM, PM>(Mt, h); break;
   }
-  int len = NP;
-#pragma unroll
-  for (int d = D - 1; d >= 0; --d) {
-    len /= PM;
-#pragma unroll
-    for (int r = 0; r < ipow_c(PM, D - 1); ++r) {
-      if (r < len) {
-        double acc = 0.0;
-#pragma unroll
-        for (int k = PM - 1; k >= 0; --k)
-          if (k < order) acc = fma(v[r * PM + k], h[d][k], acc);
-        v[r] = acc;
-      }
-    }
-  }
-  return exp(-tt) * v[0];
+  return exp(-tt) * v;
 }
 
 template <int D, int PM>
@@ -1155,6 +1333,97 @@ __global__ void k_finalize(DevSeries g, TreeView Q, int K, int nb, const int* le
     const int order = Lord[lkey];
     if (order > 0)
       loc = dev_eval_local(g, L + (size_t)lkey * g.T, Q.cen + (size_t)leaf * g.D, qp, s, order);
+  }
+  const int li = i - Q.begin[leaf];
+  const int nic = cntB[lkey] ? leaf_runs[lkey] : 0;
+  double ex = 0.0;
+  if (nic) {
+    const int t0 = leaf_task[lkey] + (li >> 5) * nic;
+    for (int k = 0; k < nic; ++k) ex += part[(size_t)(t0 + k) * 32 + (li & 31)];
+  }
+  out[(size_t)slot * n + perm[i]] = loc + s_ff[(size_t)slot * n + i] + ex;
+}
+
+// sum over the cube b_d < O of L_b prod_d u_d^{b_d}, Horner one dimension at a time
+// (tp: position -> term index of the table; entries beyond the table's order are 0)
+template <int D, int PM, int O>
+__device__ __forceinline__ double local_horner(const double* Lk, const int* tp, const double (&u)[D])
+{
+  constexpr int NO = ipow_c(O, D);
+  double v[NO];
+#pragma unroll
+  for (int p = 0; p < NO; ++p) {
+    int rest = p, pos = 0, mul = 1;
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) {
+      pos += (rest % O) * mul;
+      rest /= O;
+      mul *= PM;
+    }
+    v[p] = Lk[tp[pos]];
+  }
+  int len = NO;
+#pragma unroll
+  for (int d = D - 1; d >= 0; --d) {
+    len /= O;
+#pragma unroll
+    for (int r = 0; r < ipow_c(O, D - 1); ++r) {
+      if (r < len) {
+        double acc = v[r * O + O - 1];
+#pragma unroll
+        for (int k = O - 2; k >= 0; --k) acc = fma(acc, u[d], v[r * O + k]);
+        v[r] = acc;
+      }
+    }
+  }
+  return v[0];
+}
+
+// Specialised finalize for the default tables (p_max == PM): every ancestor's local
+// table is evaluated as a polynomial in u = (q - c) s, contracted one dimension at a
+// time (Horner per dimension, position layout via term_of_pos staged in shared
+// memory; entries beyond a table's order are zero).  Ancestors are walked from the
+// leaf up (no per-thread chain array).
+template <int D, int PM>
+__global__ void __launch_bounds__(128) k_finalize_t(DevSeries g, TreeView Q, int K, int nb,
+                                                    const int* leaf_of_pos, const int* perm, int n,
+                                                    const double* L, const int* Lord,
+                                                    const int* cntB, const int* leaf_task,
+                                                    const int* leaf_runs, const double* part,
+                                                    const double* s_ff, SlotView sv, double* out)
+{
+  constexpr int NP = ipow_c(PM, D);
+  __shared__ int tp[NP];
+  for (int p = threadIdx.x; p < NP; p += blockDim.x) tp[p] = g.term_of_pos[p];
+  __syncthreads();
+  const long long gi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= (long long)n * nb) return;
+  const int slot = (int)(gi / n);
+  const int i = (int)(gi - (long long)slot * n);
+  const int leaf = leaf_of_pos[i];
+  const int lkey = slot * K + leaf;
+  const double s = sv.s[slot];
+  double q[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) q[d] = Q.xs[(size_t)i * D + d];
+  double loc = 0.0;
+  for (int a = leaf; a >= 0; a = Q.parent[a]) {
+    const int key = slot * K + a;
+    if (Lord[key] <= 0) continue;
+    const double* Lk = L + (size_t)key * g.T;
+    double u[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) u[d] = (q[d] - Q.cen[(size_t)a * D + d]) * s;
+    const int ord = Lord[key];
+    if (ord == 1) {
+      loc += Lk[0];  // the finite-difference constant term only
+    } else if (ord == 2) {
+      loc += local_horner<D, PM, (PM >= 2 ? 2 : 1)>(Lk, tp, u);
+    } else if (ord == 3) {
+      loc += local_horner<D, PM, (PM >= 3 ? 3 : 1)>(Lk, tp, u);
+    } else {
+      loc += local_horner<D, PM, PM>(Lk, tp, u);
+    }
   }
   const int li = i - Q.begin[leaf];
   const int nic = cntB[lkey] ? leaf_runs[lkey] : 0;
@@ -1490,8 +1759,8 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
     const int pm = ser_.pmax;
     const int* dnch = bc_.p + 4;
 #define LOC_T(DD, PP)                                                                            \
-  k_local_chunks_t<DD, PP><<<gl, kLocThreads, D_ * (2 * PP) * (int)sizeof(double), s>>>(          \
-    g, Q, R, K, sDT_.p, ch, dnch, capCh_, Mt_.p, sv, lpart_.p)
+  k_local_chunks_w<DD, PP><<<gl, kLocWarps * 32, 0, s>>>(g, Q, R, K, sDT_.p, ch, dnch, capCh_,   \
+                                                         Mt_.p, sv, lpart_.p)
     if (D_ == 1 && pm == 8) LOC_T(1, 8);
     else if (D_ == 2 && pm == 6) LOC_T(2, 6);
     else if (D_ == 3 && pm == 4) LOC_T(3, 4);
@@ -1587,9 +1856,25 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
     CK(cudaMemsetAsync(s_ff_.p, 0, sizeof(double) * qt.n * nb, s));
   }
   CK(cudaEventRecord(ev_[7], s));
-  k_finalize<<<ceil_div((long long)qt.n * nb, 128), 128, 0, s>>>(
-    g, Q, K, nb, leaf_of_pos_.p, qt.perm.p, qt.n, L_.p, Lord_.p, cntB_.p, leaf_task_.p,
-    leaf_runs_.p, bpart_.p, s_ff_.p, sv, cfg_.local_pushdown == 0, d_out);
+  {
+    const int fgrid = ceil_div((long long)qt.n * nb, 128);
+    const int pm = ser_.pmax;
+    const bool direct = cfg_.local_pushdown == 0;
+#define FIN_T(DD, PP)                                                                             \
+  k_finalize_t<DD, PP><<<fgrid, 128, 0, s>>>(g, Q, K, nb, leaf_of_pos_.p, qt.perm.p, qt.n, L_.p,  \
+                                             Lord_.p, cntB_.p, leaf_task_.p, leaf_runs_.p,        \
+                                             bpart_.p, s_ff_.p, sv, d_out)
+    if (direct && cfg_.mode == 1 && D_ == 1 && pm == 8) FIN_T(1, 8);
+    else if (direct && cfg_.mode == 1 && D_ == 2 && pm == 6) FIN_T(2, 6);
+    else if (direct && cfg_.mode == 1 && D_ == 3 && pm == 4) FIN_T(3, 4);
+    else if (direct && cfg_.mode == 1 && D_ == 4 && pm == 2) FIN_T(4, 2);
+    else if (direct && cfg_.mode == 1 && D_ == 5 && pm == 2) FIN_T(5, 2);
+    else
+      k_finalize<<<fgrid, 128, 0, s>>>(g, Q, K, nb, leaf_of_pos_.p, qt.perm.p, qt.n, L_.p, Lord_.p,
+                                       cntB_.p, leaf_task_.p, leaf_runs_.p, bpart_.p, s_ff_.p, sv,
+                                       direct, d_out);
+#undef FIN_T
+  }
   CK_LAUNCH();
   CK(cudaEventRecord(ev_[8], s));
 }

@@ -297,8 +297,9 @@ def test_base_exp_mode_selection(dfgtb, orc, monkeypatch):
     _check(exact_path, exact, 0.01)
     # tiny bandwidth: every query's sum is its self term plus a tiny rest
     tiny = 1e-3 * w.h_s
+    monkeypatch.delenv("DFGTB_EXACT_EXP")
     with dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(epsilon=0.01, leaf_threshold=32)) as e:
-        monkeypatch.delenv("DFGTB_EXACT_EXP")
+        assert _capi.lib.dfgtb_base_exp_mode(e.handle) == 1
         g = e.compute(None, tiny)
     ex = orc.naive_kde(w.refs, w.refs, tiny)
     assert np.all(g >= 1.0) and np.max(np.abs((g - 1.0) - (ex - 1.0))) <= 0.01 * np.max(ex)

@@ -1,4 +1,4 @@
-python bench.py --steps 10 --warmup 3 > gpurun_out/r01x_bench.json 2> gpurun_out/r01x_bench.err; tail -c 2500 gpurun_out/r01x_bench.json
-timeout 1200 python tools/config_report.py --out gpurun_out/r01x_configs.json 2>&1 | cut -c1-330
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r01x_launches.csv python tools/profile_step.py > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_base_case -s 1 -c 1 -o gpurun_out/r01x_base2 -f python tools/profile_step.py --config 2 > /dev/null 2>&1; echo $?
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for c in 1 2 3 4 5; do python tools/profile_step.py --config $c 2>&1 | tail -1; done
+python bench.py --steps 5 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['e2e']['value'])"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r01z_launches.csv python tools/profile_step.py > /dev/null 2>&1
