@@ -762,6 +762,7 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
     typename BS::TempStorage s;
   } tmp;
   __shared__ Cnt s_agg, s_excl;
+  __shared__ int s_wsum[32][5];
   __shared__ double s_h[kMaxSlots], s_scale[kMaxSlots];
   __shared__ unsigned long long s_sst[kMaxSlots][sNStat];
   const int G = gridDim.x;
@@ -773,6 +774,13 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
   }
   __syncthreads();
   int cur = 0, m = nslots, p = nslots, gF = 0, gDT = 0, gB = 0, levels = 0;
+  // DFGTB_TRACE: per-phase %globaltimer stamps of CTA 0 (trace[4096 + 16 L + k])
+#define PH(k)                                                                                   \
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && levels < 512) {                       \
+    unsigned long long t_;                                                                      \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
+    a.trace[4096 + levels * 16 + (k)] = t_;                                                     \
+  }
   for (;;) {
     if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && levels < 512) {
       unsigned long long t;
@@ -785,33 +793,80 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
     entry_bounds(a.foff[cur], m, (long long)blockIdx.x * p / G, (long long)(blockIdx.x + 1) * p / G,
                  b0, b1);
     const int P0 = b0 < m ? a.foff[cur][b0] : p, P1 = b1 < m ? a.foff[cur][b1] : p;
+    PH(0);
     pairs_bounds<DT>(a, cur, K, P0, P1, s_scale);
     __syncthreads();
+    PH(1);
     entries_glo(a, cur, b0, b1);
     __syncthreads();
+    PH(2);
     pairs_decide<DT>(a, st, cur, K, P0, P1, s_h);
     __syncthreads();
+    PH(3);
     entries_reduce(a, cur, K, b0, b1, s_sst);
     __syncthreads();
-    Cnt acc{};
-    for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) acc = CntSum()(acc, a.cnt[i]);
-    const Cnt agg0 = BR(tmp.r).Reduce(acc, CntSum());
-    if (threadIdx.x == 0) s_agg = agg0;
-    __syncthreads();
-    // the CTA's output offsets: one atomic per counter on the level's totals.  The
-    // order in which CTAs claim space only permutes the next frontier; work items carry
-    // their per-key rank and are counting-sorted by (key, rank) afterwards, so every
-    // result stays bit-reproducible.
-    // Entries and their pairs are claimed by ONE 64-bit atomic on the packed (e, p)
-    // totals, so pair offsets grow with entry index (entry_bounds relies on it).
+    PH(4);
+    // CTA scan of the entries' counts (e, p, f, dt, b): each thread sums a contiguous
+    // segment, warp shuffle scan, scan of the 32 warp totals; the CTA total claims
+    // output space with atomics (the order in which CTAs claim space only permutes the
+    // next frontier; work items carry their per-key rank and are counting-sorted by
+    // (key, rank) afterwards, so every result stays bit-reproducible).  Entries and
+    // their pairs share ONE 64-bit atomic on the packed (e, p) totals, so pair offsets
+    // grow with entry index (entry_bounds relies on it).
+    const int nE = b1 - b0, per_t = (nE + kPBlock - 1) / kPBlock;
+    const int s0 = b0 + min(nE, threadIdx.x * per_t), s1 = b0 + min(nE, (threadIdx.x + 1) * per_t);
+    int v5[5] = { 0, 0, 0, 0, 0 };
+    for (int i = s0; i < s1; ++i) {
+      const Cnt c = a.cnt[i];
+      v5[0] += c.e;
+      v5[1] += c.p;
+      v5[2] += c.f;
+      v5[3] += c.dt;
+      v5[4] += c.b;
+    }
+    int x5[5];
+    {
+      const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        int x = v5[k];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        x5[k] = x - v5[k];  // exclusive within the warp
+        if (lane == 31) s_wsum[wib][k] = x;
+      }
+      __syncthreads();
+      if (wib == 0) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const int w = s_wsum[lane][k];
+          int x = w;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          s_wsum[lane][k] = x - w;  // exclusive warp prefix
+          if (lane == 31) (&s_agg.e)[k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 2 : k == 3 ? 3 : 5] = x;
+        }
+        if (lane == 0) s_agg.t = s_agg.fd = 0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 5; ++k) x5[k] += s_wsum[wib][k];
+    }
     if (threadIdx.x == 0) {
       const unsigned long long v =
         ((unsigned long long)(unsigned)s_agg.e << 32) | (unsigned)s_agg.p;
       const unsigned long long o = v ? atomicAdd(&a.lvlep[levels], v) : 0ull;
       s_excl.e = (int)(o >> 32);
       s_excl.p = (int)(o & 0xffffffffu);
-    } else if (threadIdx.x < 6) {
-      const int k = threadIdx.x + 1;  // f, dt, t, b, fd
+      s_excl.t = s_excl.fd = 0;
+    } else if (threadIdx.x < 4) {
+      const int k = threadIdx.x == 1 ? 2 : threadIdx.x == 2 ? 3 : 5;  // f, dt, b
       const int v = (&s_agg.e)[k];
       (&s_excl.e)[k] = v ? atomicAdd(&a.lvlcnt[levels].e + k, v) : 0;
     }
@@ -821,24 +876,28 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       a.trace[levels * 4 + 1] = t;
     }
+    PH(5);
     const Cnt excl = s_excl;
     // everything this CTA writes ends below excl + agg: emit only if that fits (on
     // overflow the level is abandoned and the host reruns with larger buffers)
     if (!over_capacity(st, CntSum()(excl, s_agg), gF, gDT, gB)) {
-      Cnt carry = excl;
-      for (int base = b0; base < b1; base += blockDim.x) {
-        const int i = base + threadIdx.x;
-        const Cnt x = i < b1 ? a.cnt[i] : Cnt{};
-        Cnt ex, ag;
-        __syncthreads();
-        BS(tmp.s).ExclusiveScan(x, ex, Cnt{}, CntSum(), ag);
-        if (i < b1) a.cntoff[i] = CntSum()(carry, ex);
-        carry = CntSum()(carry, ag);
+      Cnt run{ excl.e + x5[0], excl.p + x5[1], excl.f + x5[2], excl.dt + x5[3], 0, excl.b + x5[4], 0 };
+      for (int i = s0; i < s1; ++i) {
+        a.cntoff[i] = run;
+        const Cnt c = a.cnt[i];
+        run.e += c.e;
+        run.p += c.p;
+        run.f += c.f;
+        run.dt += c.dt;
+        run.b += c.b;
       }
       __syncthreads();
+      PH(6);
       emit_range<32>(a, K, cur, gF, gDT, gB, b0, b1);
     }
+    PH(7);
     grid.sync();
+    PH(8);
     if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && levels < 512) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1147,8 +1206,8 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   a.lvlep = lvlep_.p;
   static const bool tracing = std::getenv("DFGTB_TRACE") != nullptr;
   if (tracing) {
-    trace_.reserve(512 * 6);
-    CK(cudaMemsetAsync(trace_.p, 0, sizeof(unsigned long long) * 512 * 6, s));
+    trace_.reserve(4096 + 512 * 16);
+    CK(cudaMemsetAsync(trace_.p, 0, sizeof(unsigned long long) * (4096 + 512 * 16), s));
     a.trace = trace_.p;
   }
   const std::vector<const void*> sig = {
@@ -1213,12 +1272,18 @@ bool Engine::traverse_finish()
   const int nb = trav_nb_;
   if (!use_persistent_ && use_graph_) launch_counter() += (uint64_t)hs->levels * kLevelKernels;
   if (trav_trace_) {  // per level: classify | scan | emit (microseconds)
-    std::vector<unsigned long long> tr(512 * 6);
+    std::vector<unsigned long long> tr(4096 + 512 * 16);
     CK(cudaMemcpy(tr.data(), trace_.p, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
-    for (int L = 0; L < std::min(hs->levels, 511); ++L)
-      std::fprintf(stderr, "DFGTB_TRACE level %d: entries %llu pairs %llu classify+lookback %.1f us, emit+sync %.1f us\n",
+    for (int L = 0; L < std::min(hs->levels, 511); ++L) {
+      const unsigned long long* ph = tr.data() + 4096 + L * 16;
+      const double d = 1e-3;
+      std::fprintf(stderr, "DFGTB_TRACE level %d: entries %llu pairs %llu classify+lookback %.1f us, emit+sync %.1f us"
+                   " | split %.1f bounds %.1f glo %.1f decide %.1f reduce %.1f offsets %.1f scan %.1f emit %.1f sync %.1f\n",
                    L, tr[2048 + L * 2], tr[2048 + L * 2 + 1], (tr[L * 4 + 1] - tr[L * 4]) * 1e-3,
-                   (tr[L * 4 + 2] - tr[L * 4 + 1]) * 1e-3);
+                   (tr[L * 4 + 2] - tr[L * 4 + 1]) * 1e-3, (ph[0] - tr[L * 4]) * d, (ph[1] - ph[0]) * d,
+                   (ph[2] - ph[1]) * d, (ph[3] - ph[2]) * d, (ph[4] - ph[3]) * d, (ph[5] - ph[4]) * d,
+                   (ph[6] - ph[5]) * d, (ph[7] - ph[6]) * d, (ph[8] - ph[7]) * d);
+    }
   }
   if (hs->overflow == 2) throw CudaError("traversal exceeded 1024 levels");
   if (hs->overflow) {
