@@ -130,6 +130,8 @@ __device__ void dev_choose(double nq, double nr, double sq, double sr, double h,
 // is written; on overflow the loop stops and the host regrows the buffers and reruns.
 enum SlotStat { sPairs = 0, sFD, sF, sD, sT, sB, sKev, sNStat };
 constexpr int kMaxLevels = 1024;
+constexpr int kNch = 4;               // chunks per CTA on big levels (cyclic deal)
+constexpr int kCyclicPairs = 1 << 19;  // levels with at least this many pairs
 struct TravState {
   double eps, ntot;                    // per batch (host)
   int nslots, K;
@@ -603,22 +605,38 @@ __device__ __forceinline__ void entry_bounds(const int* foff, int m, long long t
   e1 = lo1;
 }
 
-// Pass 1, one thread per pair: kernel bounds K(d_min), K(d_max).
+// Pass 1, one thread per pair: kernel bounds K(d_min), K(d_max).  kPU pairs per thread
+// at a time with their loads issued back to back (the phase is latency-bound: each pair
+// is a chain entry -> key -> boxes).
+constexpr int kPU = 4;
 template <int DT>
 __device__ __forceinline__ void pairs_bounds(const TravArgs& a, int cur, int K, int P0, int P1,
                                              const double* s_scale)
 {
   const int D = DT ? DT : a.D;
-  for (int j = P0 + threadIdx.x; j < P1; j += kPBlock) {
-    const int key = a.fq[cur][a.pent[cur][j]];
-    const int slot = key / K, Q = key - slot * K;
-    const int R = a.fr[cur][j];
-    double dl, du;
-    box_bounds<DT>(a.Q.lo + (size_t)Q * D, a.Q.hi + (size_t)Q * D, a.R.lo + (size_t)R * D,
-                   a.R.hi + (size_t)R * D, D, dl, du);
-    const double scale = s_scale[slot];
-    a.pkmax[j] = exp(scale * dl);  // kernel at closest approach
-    a.pkmin[j] = exp(scale * du);
+  for (int j0 = P0 + threadIdx.x; j0 < P1; j0 += kPBlock * kPU) {
+    int e[kPU], R[kPU], key[kPU];
+#pragma unroll
+    for (int u = 0; u < kPU; ++u) {
+      const int j = j0 + u * kPBlock;
+      e[u] = j < P1 ? a.pent[cur][j] : -1;
+      R[u] = j < P1 ? a.fr[cur][j] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPU; ++u) key[u] = e[u] >= 0 ? a.fq[cur][e[u]] : 0;
+#pragma unroll
+    for (int u = 0; u < kPU; ++u) {
+      const int j = j0 + u * kPBlock;
+      if (j < P1) {
+        const int slot = key[u] / K, Q = key[u] - slot * K;
+        double dl, du;
+        box_bounds<DT>(a.Q.lo + (size_t)Q * D, a.Q.hi + (size_t)Q * D, a.R.lo + (size_t)R[u] * D,
+                       a.R.hi + (size_t)R[u] * D, D, dl, du);
+        const double scale = s_scale[slot];
+        a.pkmax[j] = exp(scale * dl);  // kernel at closest approach
+        a.pkmin[j] = exp(scale * du);
+      }
+    }
   }
 }
 
@@ -644,14 +662,32 @@ __device__ __forceinline__ void pairs_decide(const TravArgs& a, const TravState&
 {
   const int D = DT ? DT : a.D;
   const double eps = st.eps, ntot = st.ntot;
-  for (int j = P0 + threadIdx.x; j < P1; j += kPBlock) {
-    const int e = a.pent[cur][j];
-    const int key = a.fq[cur][e];
+  for (int j0 = P0 + threadIdx.x; j0 < P1; j0 += kPBlock * kPU) {
+  int ue[kPU], uR[kPU], ukey[kPU], ucnt[kPU];
+  double uglo[kPU];
+#pragma unroll
+  for (int u = 0; u < kPU; ++u) {
+    const int j = j0 + u * kPBlock;
+    ue[u] = j < P1 ? a.pent[cur][j] : -1;
+    uR[u] = j < P1 ? a.fr[cur][j] : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < kPU; ++u) {
+    ukey[u] = ue[u] >= 0 ? a.fq[cur][ue[u]] : 0;
+    uglo[u] = ue[u] >= 0 ? a.glo[ue[u]] : 0.0;
+    ucnt[u] = a.R.count[uR[u]];
+  }
+#pragma unroll 1
+  for (int u = 0; u < kPU; ++u) {
+    const int j = j0 + u * kPBlock;
+    if (j >= P1) break;
+    const int e = ue[u];
+    const int key = ukey[u];
     const int slot = key / K, Q = key - slot * K;
-    const int R = a.fr[cur][j];
+    const int R = uR[u];
     const double kmax = a.pkmax[j], kmin = a.pkmin[j];
-    const double nr = (double)a.R.count[R];
-    const double tau = eps * nr * a.glo[e] / ntot;
+    const double nr = (double)ucnt[u];
+    const double tau = eps * nr * uglo[u] / ntot;
     int kind = kX, order = 0;
     if (0.5 * nr * (kmax - kmin) <= tau) {  // kernel-difference prune, engine.cpp:137-148
       kind = kFD;
@@ -670,11 +706,13 @@ __device__ __forceinline__ void pairs_decide(const TravArgs& a, const TravState&
         // point also needs the query leaf's diameter <= 1000 in z units (sq sqrt(D)
         // sqrt(log2 e) / (h sqrt 2), sqrt(log2 e / 2) < 0.8494)
         order = (kmin >= 3.4e-308 ? 1 : 0) |
-                ((a.selfq || a.glo[e] >= 1e-290) &&
+                ((a.selfq || uglo[u] >= 1e-290) &&
                          a.Q.side[Q] * sqrt((double)D) * 0.8494 <= 1000.0 * s_h[slot] ? 2 : 0);
       }
     }
     a.dec[j] = kind | (order << 8);
+    (void)e;
+  }
   }
 }
 
@@ -789,23 +827,50 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
       a.trace[2048 + levels * 2] = (unsigned long long)m;
       a.trace[2048 + levels * 2 + 1] = (unsigned long long)p;
     }
-    int b0, b1;
-    entry_bounds(a.foff[cur], m, (long long)blockIdx.x * p / G, (long long)(blockIdx.x + 1) * p / G,
-                 b0, b1);
-    const int P0 = b0 < m ? a.foff[cur][b0] : p, P1 = b1 < m ? a.foff[cur][b1] : p;
+    // Big levels are cut into nch * G pair-balanced chunks dealt CYCLICALLY (CTA b takes
+    // chunks b, b + G, ..): per-pair cost depends strongly on the bandwidth slot, i.e.
+    // on the position in the frontier, and interleaving averages it out.  A CTA's
+    // output is the concatenation of its chunks (one scan, one claim), so nothing
+    // downstream needs contiguous input ranges.
+    const int nch = p >= kCyclicPairs ? kNch : 1;
+    int cb0[kNch], cb1[kNch];
+#pragma unroll
+    for (int j = 0; j < kNch; ++j) {
+      cb0[j] = cb1[j] = 0;
+      if (j < nch) {
+        const long long k = blockIdx.x + (long long)j * G, nk = (long long)G * nch;
+        entry_bounds(a.foff[cur], m, k * p / nk, (k + 1) * p / nk, cb0[j], cb1[j]);
+      }
+    }
+    auto pofs = [&](int e) { return e < m ? a.foff[cur][e] : p; };
     PH(0);
-    pairs_bounds<DT>(a, cur, K, P0, P1, s_scale);
+    for (int j = 0; j < nch; ++j) pairs_bounds<DT>(a, cur, K, pofs(cb0[j]), pofs(cb1[j]), s_scale);
     __syncthreads();
     PH(1);
-    entries_glo(a, cur, b0, b1);
+    for (int j = 0; j < nch; ++j) entries_glo(a, cur, cb0[j], cb1[j]);
     __syncthreads();
     PH(2);
-    pairs_decide<DT>(a, st, cur, K, P0, P1, s_h);
+    for (int j = 0; j < nch; ++j) pairs_decide<DT>(a, st, cur, K, pofs(cb0[j]), pofs(cb1[j]), s_h);
     __syncthreads();
     PH(3);
-    entries_reduce(a, cur, K, b0, b1, s_sst);
+    for (int j = 0; j < nch; ++j) entries_reduce(a, cur, K, cb0[j], cb1[j], s_sst);
     __syncthreads();
     PH(4);
+    // virtual index over the concatenated chunks -> frontier entry
+    int nE = 0, cofs[kNch + 1];
+#pragma unroll
+    for (int j = 0; j < kNch; ++j) {
+      cofs[j] = nE;
+      nE += cb1[j] - cb0[j];
+    }
+    cofs[kNch] = nE;
+    auto real = [&](int v) {
+      int j = 0;
+#pragma unroll
+      for (int jj = 1; jj < kNch; ++jj)
+        if (v >= cofs[jj]) j = jj;
+      return cb0[j] + (v - cofs[j]);
+    };
     // CTA scan of the entries' counts (e, p, f, dt, b): each thread sums a contiguous
     // segment, warp shuffle scan, scan of the 32 warp totals; the CTA total claims
     // output space with atomics (the order in which CTAs claim space only permutes the
@@ -813,11 +878,11 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
     // (key, rank) afterwards, so every result stays bit-reproducible).  Entries and
     // their pairs share ONE 64-bit atomic on the packed (e, p) totals, so pair offsets
     // grow with entry index (entry_bounds relies on it).
-    const int nE = b1 - b0, per_t = (nE + kPBlock - 1) / kPBlock;
-    const int s0 = b0 + min(nE, threadIdx.x * per_t), s1 = b0 + min(nE, (threadIdx.x + 1) * per_t);
+    const int per_t = (nE + kPBlock - 1) / kPBlock;
+    const int s0 = min(nE, threadIdx.x * per_t), s1 = min(nE, (threadIdx.x + 1) * per_t);
     int v5[5] = { 0, 0, 0, 0, 0 };
-    for (int i = s0; i < s1; ++i) {
-      const Cnt c = a.cnt[i];
+    for (int v = s0; v < s1; ++v) {
+      const Cnt c = a.cnt[real(v)];
       v5[0] += c.e;
       v5[1] += c.p;
       v5[2] += c.f;
@@ -882,7 +947,8 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
     // overflow the level is abandoned and the host reruns with larger buffers)
     if (!over_capacity(st, CntSum()(excl, s_agg), gF, gDT, gB)) {
       Cnt run{ excl.e + x5[0], excl.p + x5[1], excl.f + x5[2], excl.dt + x5[3], 0, excl.b + x5[4], 0 };
-      for (int i = s0; i < s1; ++i) {
+      for (int v = s0; v < s1; ++v) {
+        const int i = real(v);
         a.cntoff[i] = run;
         const Cnt c = a.cnt[i];
         run.e += c.e;
@@ -893,9 +959,14 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
       }
       __syncthreads();
       PH(6);
-      emit_range<32>(a, K, cur, gF, gDT, gB, b0, b1);
+      for (int j = 0; j < nch; ++j) emit_range<32>(a, K, cur, gF, gDT, gB, cb0[j], cb1[j]);
     }
     PH(7);
+    if (a.trace && threadIdx.x == 0 && levels < 64) {  // per-CTA busy time of the level
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      a.trace[4096 + 512 * 16 + levels * 160 + blockIdx.x] = t_;
+    }
     grid.sync();
     PH(8);
     if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && levels < 512) {
@@ -1206,8 +1277,8 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   a.lvlep = lvlep_.p;
   static const bool tracing = std::getenv("DFGTB_TRACE") != nullptr;
   if (tracing) {
-    trace_.reserve(4096 + 512 * 16);
-    CK(cudaMemsetAsync(trace_.p, 0, sizeof(unsigned long long) * (4096 + 512 * 16), s));
+    trace_.reserve(4096 + 512 * 16 + 64 * 160);
+    CK(cudaMemsetAsync(trace_.p, 0, sizeof(unsigned long long) * (4096 + 512 * 16 + 64 * 160), s));
     a.trace = trace_.p;
   }
   const std::vector<const void*> sig = {
@@ -1272,7 +1343,7 @@ bool Engine::traverse_finish()
   const int nb = trav_nb_;
   if (!use_persistent_ && use_graph_) launch_counter() += (uint64_t)hs->levels * kLevelKernels;
   if (trav_trace_) {  // per level: classify | scan | emit (microseconds)
-    std::vector<unsigned long long> tr(4096 + 512 * 16);
+    std::vector<unsigned long long> tr(4096 + 512 * 16 + 64 * 160);
     CK(cudaMemcpy(tr.data(), trace_.p, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
     for (int L = 0; L < std::min(hs->levels, 511); ++L) {
       const unsigned long long* ph = tr.data() + 4096 + L * 16;
@@ -1283,6 +1354,17 @@ bool Engine::traverse_finish()
                    (tr[L * 4 + 2] - tr[L * 4 + 1]) * 1e-3, (ph[0] - tr[L * 4]) * d, (ph[1] - ph[0]) * d,
                    (ph[2] - ph[1]) * d, (ph[3] - ph[2]) * d, (ph[4] - ph[3]) * d, (ph[5] - ph[4]) * d,
                    (ph[6] - ph[5]) * d, (ph[7] - ph[6]) * d, (ph[8] - ph[7]) * d);
+      if (L < 64) {  // CTA busy times: min / median / max (from the level start of CTA 0)
+        std::vector<double> bt;
+        for (int b = 0; b < 160; ++b) {
+          const unsigned long long v = tr[4096 + 512 * 16 + L * 160 + b];
+          if (v) bt.push_back((v - tr[L * 4]) * d);
+        }
+        std::sort(bt.begin(), bt.end());
+        if (!bt.empty())
+          std::fprintf(stderr, "DFGTB_TRACE level %d: CTA busy us min %.1f median %.1f p90 %.1f max %.1f\n", L,
+                       bt.front(), bt[bt.size() / 2], bt[bt.size() * 9 / 10], bt.back());
+      }
     }
   }
   if (hs->overflow == 2) throw CudaError("traversal exceeded 1024 levels");
