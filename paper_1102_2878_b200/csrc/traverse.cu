@@ -131,7 +131,10 @@ __device__ void dev_choose(double nq, double nr, double sq, double sr, double h,
 enum SlotStat { sPairs = 0, sFD, sF, sD, sT, sB, sKev, sNStat };
 constexpr int kMaxLevels = 1024;
 constexpr int kNch = 4;               // chunks per CTA on big levels (cyclic deal)
-constexpr int kCyclicPairs = 1 << 19;  // levels with at least this many pairs
+#ifndef DFGTB_CYCLIC_PAIRS
+#define DFGTB_CYCLIC_PAIRS 2000000000  // cyclic deal measured 3-5% slower on cfg3/cfg5: off
+#endif
+constexpr int kCyclicPairs = DFGTB_CYCLIC_PAIRS;  // levels with at least this many pairs
 struct TravState {
   double eps, ntot;                    // per batch (host)
   int nslots, K;
@@ -608,7 +611,10 @@ __device__ __forceinline__ void entry_bounds(const int* foff, int m, long long t
 // Pass 1, one thread per pair: kernel bounds K(d_min), K(d_max).  kPU pairs per thread
 // at a time with their loads issued back to back (the phase is latency-bound: each pair
 // is a chain entry -> key -> boxes).
-constexpr int kPU = 4;
+#ifndef DFGTB_TRAV_PU
+#define DFGTB_TRAV_PU 1  // measured: 2 and 4 pairs per thread gain nothing (spills at 64 registers)
+#endif
+constexpr int kPU = DFGTB_TRAV_PU;
 template <int DT>
 __device__ __forceinline__ void pairs_bounds(const TravArgs& a, int cur, int K, int P0, int P1,
                                              const double* s_scale)
