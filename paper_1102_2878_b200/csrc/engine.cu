@@ -127,12 +127,16 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
     throw InvalidArgument("SeriesGeometry requires dim >= 1 and 1 <= p_max <= 15");
   D_ = (int)d;
   n_ = n;
+  if (const char* sl = std::getenv("DFGTB_BASE_SLACK")) base_cta_slack_ = std::atoi(sl);
   mufu_ = cfg.epsilon >= kMufuMinEps && D_ <= 5 && std::getenv("DFGTB_EXACT_EXP") == nullptr;
   const int pm = cfg.mode == 0 ? 1 : (cfg.p_max > 0 ? cfg.p_max : default_p_max(D_));
   ser_ = SeriesTables(D_, pm);
   if (D_ * (pm - 1) >= 128) throw InvalidArgument("D * (p_max - 1) must be < 128");
   if (D_ > kMaxDim) throw InvalidArgument("dimension > 16 is not supported by the device engine");
   CK(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
   for (auto& e : ev_) CK(cudaEventCreate(&e));
   x_.reserve(n * d);
   CK(cudaMemcpyAsync(x_.p, refs, sizeof(double) * n * d,
@@ -164,6 +168,12 @@ Engine::~Engine()
   destroy_graph();
   if (hst_) pinned_free(hst_, hst_bytes_);
   for (auto& e : ev_) cudaEventDestroy(e);
+  if (fork_) cudaEventDestroy(fork_);
+  if (join_) cudaEventDestroy(join_);
+  if (s2_) {
+    cudaStreamSynchronize(s2_);
+    cudaStreamDestroy(s2_);
+  }
   if (s_) cudaStreamDestroy(s_);
 }
 

@@ -103,6 +103,8 @@ private:
   int D_ = 0;
   size_t n_ = 0;
   cudaStream_t s_ = nullptr;
+  cudaStream_t s2_ = nullptr;  // local expansions + far field run beside the base case
+  int base_cta_slack_ = 0;     // base-case CTA slots per SM left to s2_ (DFGTB_BASE_SLACK; 0 measured best)
   DevBuf<double> x_;        // reference points (original order)
   DevTree rt_;              // reference tree
   DevTree qt_tmp_;          // query tree (Q != R)
@@ -126,7 +128,7 @@ private:
   DevBuf<double> newbase_, pglo_;
   DevBuf<Cnt> cnt_, cntoff_, ctsum_, ctoff_, lvlcnt_;
   DevBuf<Item> itF_, itDT_, itB_, sF_, sDT_, sB_;
-  DevBuf<unsigned char> scan_tmp_;
+  DevBuf<unsigned char> scan_tmp_, scan_tmp2_;
   DevBuf<double> red_;
   DevBuf<unsigned long long> trace_;  // DFGTB_TRACE=1: per-level phase timestamps
   DevBuf<unsigned long long> lvlep_;  // per-level packed entry/pair counters (traversal)
@@ -141,7 +143,8 @@ private:
   cudaGraphExec_t gexec_ = nullptr;
   cudaGraphConditionalHandle hc_ = 0;
   std::vector<const void*> gsig_;
-  cudaEvent_t ev_[10];
+  cudaEvent_t ev_[12];
+  cudaEvent_t fork_ = nullptr, join_ = nullptr;
   std::vector<Stats> slot_stats_;
   Timings tim_;
   long long nF_ = 0, nDT_ = 0, nB_ = 0;

@@ -1552,7 +1552,7 @@ int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }
 template <int DT>
 void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int K, const BTask* tasks,
                    const int2* rec, const double* xq, const double* xr, int nq, int nr, double* part,
-                   int* next, int mufu)
+                   int* next, int mufu, int slack)
 {
   static int per_sm = 0, nsm = 0;
   constexpr int threads = BaseGeo<DT>::WARPS * 32;
@@ -1565,7 +1565,8 @@ void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int 
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_base_case<DT>, threads, smem));
     per_sm = std::max(per_sm, 1);
   }
-  const int grid = (int)std::min<long long>((long long)nsm * per_sm,
+  // leave `slack` CTA slots per SM to the kernels of the second stream
+  const int grid = (int)std::min<long long>((long long)nsm * std::max(1, per_sm - slack),
                                             (tcap + BaseGeo<DT>::WARPS - 1) / BaseGeo<DT>::WARPS);
   CK(cudaMemsetAsync(next, 0, sizeof(int), s));
   k_base_case<DT><<<grid, threads, smem, s>>>(Q, K, tasks, ntasks, tcap, rec, xq, xr, nq, nr, part,
@@ -1574,9 +1575,10 @@ void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int 
 
 void launch_base(int D, cudaStream_t s, TreeView Q, TreeView R, int K, const BTask* tasks,
                  const int* ntasks, int tcap, const Item* items, const int2* rec, const double* xq,
-                 const double* xr, int nq, int nr, double* part, int* next, int mufu)
+                 const double* xr, int nq, int nr, double* part, int* next, int mufu, int slack)
 {
-#define BASE(DD) launch_base_t<DD>(ntasks, tcap, s, Q, K, tasks, rec, xq, xr, nq, nr, part, next, mufu)
+#define BASE(DD)                                                                                 \
+  launch_base_t<DD>(ntasks, tcap, s, Q, K, tasks, rec, xq, xr, nq, nr, part, next, mufu, slack)
   switch (D) {
   case 1: BASE(1); break;
   case 2: BASE(2); break;
@@ -1687,7 +1689,7 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
   CK(cudaEventElapsedTime(&tim_.traverse_ms, ev_[2], ev_[3]));
   CK(cudaEventElapsedTime(&tim_.moments_ms, ev_[3], ev_[4]));
   CK(cudaEventElapsedTime(&tim_.local_ms, ev_[4], ev_[5]));
-  CK(cudaEventElapsedTime(&tim_.base_ms, ev_[9], ev_[6]));
+  CK(cudaEventElapsedTime(&tim_.base_ms, ev_[9], ev_[10]));
   CK(cudaEventElapsedTime(&tim_.farfield_ms, ev_[6], ev_[7]));
   CK(cudaEventElapsedTime(&tim_.final_ms, ev_[7], ev_[8]));
   CK(cudaEventElapsedTime(&tim_.total_ms, ev_[2], ev_[8]));
@@ -1722,36 +1724,43 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
   const int* dnDT = bc_.p + 1;
   const int* dnB = bc_.p + 2;
   CK(cudaEventRecord(ev_[3], s));
+  // Fork: the local expansions (D/T items) and the far field run on s2_ beside the
+  // base-case chain on s_ (they only read the traversal's sorted items and write their
+  // own buffers); the base case leaves a CTA slot per SM for them.  Join before
+  // finalize.
+  cudaStream_t s2 = s2_;
+  CK(cudaEventRecord(fork_, s));
+  CK(cudaStreamWaitEvent(s2, fork_, 0));
   // moments of the reference nodes used by F/T items (large tables only; small
   // tables were computed for every node when the engine was built)
   if (!eager_ && cfg_.mode == 1) {
     mflag_.reserve(rt_.nodes);
-    CK(cudaMemsetAsync(mflag_.p, 0, sizeof(int) * rt_.nodes, s));
-    k_mark_moments<<<148 * 4, 256, 0, s>>>(sF_.p, dnF, capF_, mflag_.p);
+    CK(cudaMemsetAsync(mflag_.p, 0, sizeof(int) * rt_.nodes, s2));
+    k_mark_moments<<<148 * 4, 256, 0, s2>>>(sF_.p, dnF, capF_, mflag_.p);
     CK_LAUNCH();
-    k_mark_moments<<<148 * 4, 256, 0, s>>>(sDT_.p, dnDT, capDT_, mflag_.p);
+    k_mark_moments<<<148 * 4, 256, 0, s2>>>(sDT_.p, dnDT, capDT_, mflag_.p);
     CK_LAUNCH();
     const int smem = 32 * D_ * ser_.pmax * (int)sizeof(double);
-    k_moments<<<std::min(rt_.nodes, 148 * 8), 128, smem, s>>>(g, R, rt_.nodes, mflag_.p, mdone_.p,
-                                                             Mt_.p);
+    k_moments<<<std::min(rt_.nodes, 148 * 8), 128, smem, s2>>>(g, R, rt_.nodes, mflag_.p, mdone_.p,
+                                                              Mt_.p);
     CK_LAUNCH();
   }
-  CK(cudaEventRecord(ev_[4], s));
+  CK(cudaEventRecord(ev_[4], s2));
   // D/T items -> chunked partial tables -> per-(slot, query node) reduction
   if (cfg_.mode == 1) {
     lnch_.reserve((size_t)capDT_ + 1);
     lchoff_.reserve((size_t)capDT_ + 1);
-    k_local_count<<<148 * 4, 256, 0, s>>>(sDT_.p, dnDT, capDT_, R, lnch_.p);
+    k_local_count<<<148 * 4, 256, 0, s2>>>(sDT_.p, dnDT, capDT_, R, lnch_.p);
     CK_LAUNCH();
     size_t need = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need, lnch_.p, lchoff_.p, capDT_ + 1, s);
-    scan_tmp_.reserve(need + 256);
-    size_t have = scan_tmp_.cap;
-    cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, lnch_.p, lchoff_.p, capDT_ + 1, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, need, lnch_.p, lchoff_.p, capDT_ + 1, s2);
+    scan_tmp2_.reserve(need + 256);
+    size_t have = scan_tmp2_.cap;
+    cub::DeviceScan::ExclusiveSum(scan_tmp2_.p, have, lnch_.p, lchoff_.p, capDT_ + 1, s2);
     capCh_ = std::max(capCh_, std::max(4096, capDT_));
     lchunk_.reserve((size_t)capCh_ * 3);
     LChunk* ch = reinterpret_cast<LChunk*>(lchunk_.p);
-    k_local_fill<<<148 * 4, 256, 0, s>>>(sDT_.p, dnDT, capDT_, R, lchoff_.p, ch, capCh_, bc_.p + 4);
+    k_local_fill<<<148 * 4, 256, 0, s2>>>(sDT_.p, dnDT, capDT_, R, lchoff_.p, ch, capCh_, bc_.p + 4);
     CK_LAUNCH();
     lpart_.reserve((size_t)capCh_ * T);
     const int smem = std::max(kLocSub * D_ * ser_.pmax, D_ * (2 * ser_.pmax)) * (int)sizeof(double);
@@ -1759,34 +1768,58 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
     const int pm = ser_.pmax;
     const int* dnch = bc_.p + 4;
 #define LOC_T(DD, PP)                                                                            \
-  k_local_chunks_w<DD, PP><<<gl, kLocWarps * 32, 0, s>>>(g, Q, R, K, sDT_.p, ch, dnch, capCh_,   \
-                                                         Mt_.p, sv, lpart_.p)
+  k_local_chunks_w<DD, PP><<<gl, kLocWarps * 32, 0, s2>>>(g, Q, R, K, sDT_.p, ch, dnch, capCh_,  \
+                                                          Mt_.p, sv, lpart_.p)
     if (D_ == 1 && pm == 8) LOC_T(1, 8);
     else if (D_ == 2 && pm == 6) LOC_T(2, 6);
     else if (D_ == 3 && pm == 4) LOC_T(3, 4);
     else if (D_ == 4 && pm == 2) LOC_T(4, 2);
     else if (D_ == 5 && pm == 2) LOC_T(5, 2);
     else
-      k_local_chunks<<<gl, 64, smem, s>>>(g, Q, R, K, sDT_.p, ch, dnch, capCh_, Mt_.p, sv, lpart_.p);
+      k_local_chunks<<<gl, 64, smem, s2>>>(g, Q, R, K, sDT_.p, ch, dnch, capCh_, Mt_.p, sv, lpart_.p);
 #undef LOC_T
     CK_LAUNCH();
-    k_local_reduce<<<148 * 8, 256, 0, s>>>(g, dnDT, capDT_, cntDT_.p, offDT_.p, sDT_.p, lchoff_.p,
-                                           lpart_.p, L_.p, Lord_.p);
+    k_local_reduce<<<148 * 8, 256, 0, s2>>>(g, dnDT, capDT_, cntDT_.p, offDT_.p, sDT_.p, lchoff_.p,
+                                            lpart_.p, L_.p, Lord_.p);
     CK_LAUNCH();
   }
   if (cfg_.local_pushdown == 1) {
     const int smem = D_ * ser_.pmax * (int)sizeof(double);
     for (int d = 0; d + 1 < qt.height; ++d) {
       const int b = qt.depth_off[d], e = qt.depth_off[d + 1];
-      k_l2l<<<std::min((e - b) * nb, 148 * 8), 64, smem, s>>>(g, Q, K, nb, qt.by_depth.p + b, e - b,
-                                                             sv, L_.p, Lord_.p);
+      k_l2l<<<std::min((e - b) * nb, 148 * 8), 64, smem, s2>>>(g, Q, K, nb, qt.by_depth.p + b, e - b,
+                                                              sv, L_.p, Lord_.p);
       CK_LAUNCH();
     }
   }
-  CK(cudaEventRecord(ev_[5], s));
-  // base-case tasks
+  CK(cudaEventRecord(ev_[5], s2));
+  // far field (s2_)
   const int nleaves = (int)qleaves_host_.size();
   const int nlb = nleaves * nb;
+  s_ff_.reserve((size_t)qt.n * nb);
+  CK(cudaEventRecord(ev_[6], s2));
+  if (cfg_.mode == 1) {
+    const int gw = grid_warps(nlb);
+    const int pm = ser_.pmax;
+#define FF_T(DD, PP)                                                                              \
+  k_farfield_t<DD, PP><<<gw, kBlock, 0, s2>>>(Q, R, K, nb, leaves_.p, nleaves, cntF_.p, offF_.p,  \
+                                              sF_.p, Mt_.p, sv, qt.n, s_ff_.p)
+    if (D_ == 1 && pm == 8) FF_T(1, 8);
+    else if (D_ == 2 && pm == 6) FF_T(2, 6);
+    else if (D_ == 3 && pm == 4) FF_T(3, 4);
+    else if (D_ == 4 && pm == 2) FF_T(4, 2);
+    else if (D_ == 5 && pm == 2) FF_T(5, 2);
+    else
+      k_farfield<<<gw, kBlock, 0, s2>>>(g, Q, R, K, nb, leaves_.p, nleaves, cntF_.p, offF_.p, sF_.p,
+                                       Mt_.p, sv, qt.n, s_ff_.p);
+#undef FF_T
+    CK_LAUNCH();
+  } else {
+    CK(cudaMemsetAsync(s_ff_.p, 0, sizeof(double) * qt.n * nb, s2));
+  }
+  CK(cudaEventRecord(ev_[7], s2));
+  CK(cudaEventRecord(join_, s2));
+  // base-case tasks (s_)
   leaf_task_.reserve(KB);
   leaf_runs_.reserve(KB);
   const int rmax = base_rmax(D_);
@@ -1833,29 +1866,10 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
   bnext_.reserve(1);
   launch_base(D_, s, Q, R, K, reinterpret_cast<const BTask*>(tasks_.p), bc_.p + 5, capTask_, sB_.p,
               reinterpret_cast<const int2*>(brec_.p), xq, xr, qt.n, rt_.n, bpart_.p, bnext_.p,
-              mufu_exp() ? 1 : 0);
-  CK(cudaEventRecord(ev_[6], s));
-  s_ff_.reserve((size_t)qt.n * nb);
-  if (cfg_.mode == 1) {
-    const int gw = grid_warps(nlb);
-    const int pm = ser_.pmax;
-#define FF_T(DD, PP)                                                                              \
-  k_farfield_t<DD, PP><<<gw, kBlock, 0, s>>>(Q, R, K, nb, leaves_.p, nleaves, cntF_.p, offF_.p,   \
-                                             sF_.p, Mt_.p, sv, qt.n, s_ff_.p)
-    if (D_ == 1 && pm == 8) FF_T(1, 8);
-    else if (D_ == 2 && pm == 6) FF_T(2, 6);
-    else if (D_ == 3 && pm == 4) FF_T(3, 4);
-    else if (D_ == 4 && pm == 2) FF_T(4, 2);
-    else if (D_ == 5 && pm == 2) FF_T(5, 2);
-    else
-      k_farfield<<<gw, kBlock, 0, s>>>(g, Q, R, K, nb, leaves_.p, nleaves, cntF_.p, offF_.p, sF_.p,
-                                      Mt_.p, sv, qt.n, s_ff_.p);
-#undef FF_T
-    CK_LAUNCH();
-  } else {
-    CK(cudaMemsetAsync(s_ff_.p, 0, sizeof(double) * qt.n * nb, s));
-  }
-  CK(cudaEventRecord(ev_[7], s));
+              mufu_exp() ? 1 : 0, base_cta_slack_);
+  CK(cudaEventRecord(ev_[10], s));
+  // join, finalize
+  CK(cudaStreamWaitEvent(s, join_, 0));
   {
     const int fgrid = ceil_div((long long)qt.n * nb, 128);
     const int pm = ser_.pmax;
