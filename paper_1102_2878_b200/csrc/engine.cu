@@ -103,6 +103,65 @@ void pinned_free(void* p, size_t bytes)
   host_cache()[bytes].push_back(p);
 }
 
+// Streams and events are pooled per device like memory: creating / destroying them
+// costs ~0.1-0.2 ms per engine, which a CV call that builds an engine per dataset pays
+// every time.
+struct StreamSet {
+  cudaStream_t s = nullptr, s2 = nullptr;
+  cudaEvent_t ev[12] = {}, fork = nullptr, join = nullptr;
+};
+static std::unordered_map<int, std::vector<StreamSet>>& stream_pool()
+{
+  static auto* p = new std::unordered_map<int, std::vector<StreamSet>>();
+  return *p;
+}
+
+static StreamSet acquire_streams()
+{
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    auto& v = stream_pool()[dev];
+    if (!v.empty()) {
+      StreamSet r = v.back();
+      v.pop_back();
+      return r;
+    }
+  }
+  StreamSet r;
+  CK(cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&r.s2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming));
+  for (auto& e : r.ev) CK(cudaEventCreate(&e));
+  return r;
+}
+
+static void release_streams(const StreamSet& r)
+{
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> g(g_cache_mu);
+  stream_pool()[dev].push_back(r);
+}
+
+// __constant__ tables (exp coefficients, truncation bounds) are per device and
+// h-independent: uploaded once per device and process.
+static void init_device_constants(cudaStream_t s)
+{
+  static std::mutex mu;
+  static std::unordered_map<int, bool> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  if (done[dev]) return;
+  init_exp_constants(s);
+  init_truncation_tables(s);
+  CK(cudaStreamSynchronize(s));
+  done[dev] = true;
+}
+
 int default_p_max(int D)
 {  // truncation.cpp:168-186
   switch (D) {
@@ -133,17 +192,19 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
   ser_ = SeriesTables(D_, pm);
   if (D_ * (pm - 1) >= 128) throw InvalidArgument("D * (p_max - 1) must be < 128");
   if (D_ > kMaxDim) throw InvalidArgument("dimension > 16 is not supported by the device engine");
-  CK(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
-  CK(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
-  for (auto& e : ev_) CK(cudaEventCreate(&e));
+  {
+    const StreamSet ss = acquire_streams();
+    s_ = ss.s;
+    s2_ = ss.s2;
+    fork_ = ss.fork;
+    join_ = ss.join;
+    for (int i = 0; i < 12; ++i) ev_[i] = ss.ev[i];
+  }
   x_.reserve(n * d);
   CK(cudaMemcpyAsync(x_.p, refs, sizeof(double) * n * d,
                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s_));
   upload_series(ser_, ser_dev_, s_);
-  init_exp_constants(s_);
-  init_truncation_tables(s_);
+  init_device_constants(s_);
   CK(cudaEventRecord(ev_[0], s_));
   build_tree(rt_, x_.p, (int)n, D_, cfg.leaf_threshold, s_);
   if (cfg.mode == 1) {
@@ -167,14 +228,16 @@ Engine::~Engine()
   if (s_) cudaStreamSynchronize(s_);
   destroy_graph();
   if (hst_) pinned_free(hst_, hst_bytes_);
-  for (auto& e : ev_) cudaEventDestroy(e);
-  if (fork_) cudaEventDestroy(fork_);
-  if (join_) cudaEventDestroy(join_);
-  if (s2_) {
-    cudaStreamSynchronize(s2_);
-    cudaStreamDestroy(s2_);
+  if (s2_) cudaStreamSynchronize(s2_);
+  if (s_) {
+    StreamSet ss;
+    ss.s = s_;
+    ss.s2 = s2_;
+    ss.fork = fork_;
+    ss.join = join_;
+    for (int i = 0; i < 12; ++i) ss.ev[i] = ev_[i];
+    release_streams(ss);  // pooled for the next engine on this device
   }
-  if (s_) cudaStreamDestroy(s_);
 }
 
 DevSeries Engine::dev_series() const { return series_view(ser_, ser_dev_); }

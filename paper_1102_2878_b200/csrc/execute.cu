@@ -83,6 +83,83 @@ __global__ void k_moment_chunks(DevSeries g, TreeView R, const int* cnode, const
   }
 }
 
+// Warp reduce-scatter of 32 per-lane values: afterwards lane l holds the sum over the
+// warp of value l (five halving exchange steps, fixed order).
+__device__ __forceinline__ double warp_reduce_scatter32(double (&v)[32], int lane)
+{
+#pragma unroll
+  for (int st = 0; st < 5; ++st) {
+    const int off = 16 >> st;
+    const bool up = lane & off;
+    const int h = 16 >> st;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i < h) {
+        const double send = up ? v[i] : v[i + h];
+        const double keep = up ? v[i + h] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+  }
+  return v[0];
+}
+
+// Specialised pass 1 for the default tables (p_max == PM, <= 64 terms): ONE WARP per
+// 64-point chunk, each lane's points' monomials prod_d (r - c)_d^{a_d} for every
+// multi-index accumulated in registers (compile-time digits), warp reduce-scatter,
+// partials in term order like k_moment_chunks.
+template <int D, int PM>
+__global__ void __launch_bounds__(128) k_moment_chunks_w(DevSeries g, TreeView R, const int* cnode,
+                                                         const int* cstart, int nchunks, double* part)
+{
+  constexpr int NP = ipow_c(PM, D), NB = (NP + 31) / 32;
+  __shared__ int tp[NP];
+  for (int p = threadIdx.x; p < NP; p += blockDim.x) tp[p] = g.term_of_pos[p];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nchunks;
+       c += (gridDim.x * blockDim.x) >> 5) {
+    const int n = cnode[c], st = cstart[c];
+    const int m = min(kMomChunk, R.begin[n] + R.count[n] - st);
+    double cen[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) cen[d] = R.cen[(size_t)n * D + d];
+    double acc[NB * 32];
+#pragma unroll
+    for (int p = 0; p < NB * 32; ++p) acc[p] = 0.0;
+    for (int j = lane; j < m; j += 32) {
+      double P[D][PM];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const double u = R.xs[(size_t)(st + j) * D + d] - cen[d];
+        P[d][0] = 1.0;
+#pragma unroll
+        for (int k = 1; k < PM; ++k) P[d][k] = P[d][k - 1] * u;
+      }
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        double f = 1.0;
+        int rest = p;
+#pragma unroll
+        for (int d = D - 1; d >= 0; --d) {
+          f *= P[d][rest % PM];
+          rest /= PM;
+        }
+        acc[p] += f;
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      double v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = acc[b * 32 + i];
+      const double tot = warp_reduce_scatter32(v, lane);
+      const int p = b * 32 + lane;
+      if (p < NP) part[(size_t)c * NP + tp[p]] = tot;
+    }
+  }
+}
+
 // One CTA per node: thread (term i, stripe k) sums chunks c = c0 + k, c0 + k + S, ...
 // (8 loads in flight), then the S stripe sums are added in stripe order: a fixed
 // summation order, latency ~count/(8 S) round trips instead of count.
@@ -277,27 +354,6 @@ __global__ void __launch_bounds__(kLocThreads) k_local_chunks_t(DevSeries g, Tre
 // warp of a key's first item does the work), lanes over terms.  Every term sums its
 // chunks in item order (8 loads in flight), so the result does not depend on the
 // launch shape.
-// Warp reduce-scatter of 32 per-lane values: afterwards lane l holds the sum over the
-// warp of value l (five halving exchange steps, fixed order).
-__device__ __forceinline__ double warp_reduce_scatter32(double (&v)[32], int lane)
-{
-#pragma unroll
-  for (int st = 0; st < 5; ++st) {
-    const int off = 16 >> st;
-    const bool up = lane & off;
-    const int h = 16 >> st;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      if (i < h) {
-        const double send = up ? v[i] : v[i + h];
-        const double keep = up ? v[i + h] : v[i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-      }
-    }
-  }
-  return v[0];
-}
-
 // Specialised D/T chunks for the default tables (p_max == PM): ONE WARP per chunk.
 //  D: lanes over the chunk's points, Hermite products of every multi-index in
 //     registers (one exp(-|t|^2) per point), warp reduce-scatter per 32 terms.
@@ -1633,8 +1689,18 @@ void Engine::eager_moments()
   Mt_.reserve((size_t)K * T);
   const DevSeries g = dev_series();
   const int smem = kMomChunk * D_ * ser_.pmax * (int)sizeof(double);
-  k_moment_chunks<<<std::min(nch, 148 * 16), 128, smem, s_>>>(g, view_of(t), dn.p, ds.p, nch,
-                                                               part.p);
+  const int pm = ser_.pmax;
+  const int gw = std::min(ceil_div(nch, 4), 148 * 16);
+#define MOM_T(DD, PP) k_moment_chunks_w<DD, PP><<<gw, 128, 0, s_>>>(g, view_of(t), dn.p, ds.p, nch, part.p)
+  if (D_ == 1 && pm == 8) MOM_T(1, 8);
+  else if (D_ == 2 && pm == 6) MOM_T(2, 6);
+  else if (D_ == 3 && pm == 4) MOM_T(3, 4);
+  else if (D_ == 4 && pm == 2) MOM_T(4, 2);
+  else if (D_ == 5 && pm == 2) MOM_T(5, 2);
+  else
+    k_moment_chunks<<<std::min(nch, 148 * 16), 128, smem, s_>>>(g, view_of(t), dn.p, ds.p, nch,
+                                                                 part.p);
+#undef MOM_T
   CK_LAUNCH();
   k_moment_reduce<<<std::min(K, 148 * 8), kMomRedThreads, 0, s_>>>(g, K, dof.p, part.p, Mt_.p);
   CK_LAUNCH();
