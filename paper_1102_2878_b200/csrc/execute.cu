@@ -824,6 +824,10 @@ struct BaseGeo {
 #define DFGTB_BASE_G 8
 #endif
   static constexpr int G = DT <= 2 ? DFGTB_BASE_G : 4;            // queries per lane
+#ifndef DFGTB_BASE_GM
+#define DFGTB_BASE_GM 8
+#endif
+  static constexpr int GM = DT <= 2 ? DFGTB_BASE_GM : 4;          // queries per lane, MUFU path
   static constexpr int RMAX = DT == 1 ? 512 : 256;              // stream tile (points)
   static constexpr int WARPS = 4;                                 // per CTA
   static constexpr int DM = (DT + 2) / 2 * 2;                     // MUFU stream stride
@@ -945,7 +949,7 @@ __device__ __forceinline__ void base_group_mufu(const double* rs, int n, const d
                                                 int lane)
 {
   constexpr int D = DT, DM = MPt<DT>::DM;
-  constexpr int LG = GG == 8 ? 3 : GG == 4 ? 2 : GG == 2 ? 1 : 0;
+  constexpr int LG = GG == 16 ? 4 : GG == 8 ? 3 : GG == 4 ? 2 : GG == 2 ? 1 : 0;
   double m[GG][D], A[GG], acc[GG];
 #pragma unroll
   for (int i = 0; i < GG; ++i) {
@@ -1006,9 +1010,15 @@ template <int DT, bool CLAMP>
 __device__ __forceinline__ void base_groups_mufu(const double* rs, int n, const double* qs, double* qsum,
                                                  int qc, int lane)
 {
-  constexpr int DM = MPt<DT>::DM, G = BaseGeo<DT>::G;
+  constexpr int DM = MPt<DT>::DM, G = BaseGeo<DT>::GM;
   int g0 = 0;
   for (; g0 + G <= qc; g0 += G) base_group_mufu_call<DT, G, CLAMP>(rs, n, qs + g0 * DM, qsum + g0, lane);
+  if constexpr (G >= 16) {
+    if (qc - g0 >= 8) {
+      base_group_mufu_call<DT, 8, CLAMP>(rs, n, qs + g0 * DM, qsum + g0, lane);
+      g0 += 8;
+    }
+  }
   if constexpr (G >= 8) {
     if (qc - g0 >= 4) {
       base_group_mufu_call<DT, 4, CLAMP>(rs, n, qs + g0 * DM, qsum + g0, lane);

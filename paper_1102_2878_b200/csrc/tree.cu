@@ -22,6 +22,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <numeric>
 
@@ -398,11 +399,13 @@ struct BuildArgs {
   int *nbeg, *ncnt, *nleft, *nright, *npar, *ndep;  // BFS node ids
   double *blo, *bhi, *bcen, *bside, *bsc;
   int* bsd;
-  unsigned long long *kmin, *kmax;  // per level node * D
+  unsigned long long *kmin, *kmax;  // bounds keys, two level buffers of 2n*D (level parity)
+  int* pslot;                       // next-level node -> its slot 2j+side in the keys buffer
   double* mid;                      // per level node
   int *dosplit, *child, *lc;        // per level node
   int* ctot;                        // 2 * gridDim.x chunk totals
   int* lvl;                         // [0] = levels, [1..] = level base offsets
+  unsigned long long* trace;        // DFGTB_TRACE: per level 8 %globaltimer stamps of CTA 0
 };
 
 __device__ __forceinline__ void chunk_of(int total, int b, int G, int& lo, int& hi)
@@ -438,43 +441,21 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
   chunk_of(n, bid, G, p0, p1);
   int base = 0, m = 1, level = 0;
   grid.sync();
-  for (;;) {
-    if (gt == 0) a.lvl[1 + level] = base;
-    // A: exact bounds of every level node
-    for (int i0 = p0; i0 < p1; i0 += kPB) {
-      const int i = i0 + tid;
-      const int j = i < p1 ? a.seg[i] : -1;
-      const int j0 = __shfl_sync(0xffffffffu, j, 0);
-      const bool uni = __all_sync(0xffffffffu, j == j0) && j0 >= 0;
-      for (int d = 0; d < D; ++d) {
-        const unsigned long long k = j >= 0 ? dkey(a.x[(size_t)a.perm[i] * D + d]) : 0ull;
-        if (uni) {
-          unsigned long long mn = k, mx = k;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          }
-          if (lane == 0) {
-            atomicMin(&a.kmin[(size_t)j0 * D + d], mn);
-            atomicMax(&a.kmax[(size_t)j0 * D + d], mx);
-          }
-        } else if (j >= 0) {
-          atomicMin(&a.kmin[(size_t)j * D + d], k);
-          atomicMax(&a.kmax[(size_t)j * D + d], k);
-        }
-      }
-    }
-    grid.sync();
-    // B: bounds, centroid, widest side, split midpoint (kdtree.cpp:49-78)
-    for (size_t jj = gt; jj < (size_t)m; jj += gs) {
+  const size_t KBUF = (size_t)2 * n * D;  // keys buffer stride (level parity)
+  const size_t NBL = (size_t)n + 1;        // per-level node arrays stride (level parity)
+  // B: bounds, centroid, widest side, split midpoint (kdtree.cpp:49-78) of the nodes of
+  // level `lev`; resets the keys its children will collect.  Runs in the same phase as
+  // the previous level's swaps (it only needs bounds, counts and child slots).
+  auto decide = [&](int lev, int bs, int mm) {
+    for (size_t jj = gt; jj < (size_t)mm; jj += gs) {
       const int j = (int)jj;
-      const size_t o = (size_t)(base + j) * D;
+      const size_t o = (size_t)(bs + j) * D;
       int widest = 0;
       double width = 0.0;
+      const size_t ks = (size_t)(lev == 0 ? j : a.pslot[j]) * D;
       for (int d = 0; d < D; ++d) {
-        const double l = dkey_inv(a.kmin[(size_t)j * D + d]);
-        const double h = dkey_inv(a.kmax[(size_t)j * D + d]);
+        const double l = dkey_inv(a.kmin[(lev & 1) * KBUF + ks + d]);
+        const double h = dkey_inv(a.kmax[(lev & 1) * KBUF + ks + d]);
         a.blo[o + d] = l;
         a.bhi[o + d] = h;
         a.bcen[o + d] = __dmul_rn(0.5, __dadd_rn(l, h));
@@ -484,25 +465,99 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
           widest = d;
         }
       }
-      a.bside[base + j] = width;
-      const int split = a.ncnt[base + j] > a.leaf;
-      a.dosplit[j] = split;
-      a.bsd[base + j] = split ? widest : -1;
-      a.mid[j] = a.bcen[o + widest];
+      a.bside[bs + j] = width;
+      const int split = a.ncnt[bs + j] > a.leaf;
+      a.dosplit[(lev & 1) * NBL + j] = split;
+      a.bsd[bs + j] = split ? widest : -1;
+      a.mid[(lev & 1) * NBL + j] = a.bcen[o + widest];
     }
-    grid.sync();
+    for (size_t i = gt; i < (size_t)2 * mm * D; i += gs) {  // children's bounds keys
+      a.kmin[((lev + 1) & 1) * KBUF + i] = ~0ull;
+      a.kmax[((lev + 1) & 1) * KBUF + i] = 0ull;
+    }
+  };
+  // A (root only): exact bounds.  Deeper levels get their bounds from the parent's
+  // predicate pass (C) -- the left child is exactly {x_w <= mid} -- or, for one-sided
+  // splits, from the median fallback (E).
+  for (int i0 = p0; i0 < p1; i0 += kPB) {
+    const int i = i0 + tid;
+    const int j = i < p1 ? a.seg[i] : -1;
+    const int j0 = __shfl_sync(0xffffffffu, j, 0);
+    const bool uni = __all_sync(0xffffffffu, j == j0) && j0 >= 0;
+    for (int d = 0; d < D; ++d) {
+      const unsigned long long k = j >= 0 ? dkey(a.x[(size_t)a.perm[i] * D + d]) : 0ull;
+      if (uni) {
+        unsigned long long mn = k, mx = k;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+          mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) {
+          atomicMin(&a.kmin[(size_t)j0 * D + d], mn);
+          atomicMax(&a.kmax[(size_t)j0 * D + d], mx);
+        }
+      } else if (j >= 0) {
+        atomicMin(&a.kmin[(size_t)j * D + d], k);
+        atomicMax(&a.kmax[(size_t)j * D + d], k);
+      }
+    }
+  }
+  grid.sync();
+  decide(0, 0, 1);
+  grid.sync();
+  for (;;) {
+    if (gt == 0) a.lvl[1 + level] = base;
+    if (a.trace && bid == 0 && tid == 0 && level < 64) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); a.trace[level * 8] = t_; }
+    const int* dsp = a.dosplit + (level & 1) * NBL;  // this level's split flags / midpoints
+    const double* mdp = a.mid + (level & 1) * NBL;
+    unsigned long long* cmin = a.kmin + ((level + 1) & 1) * KBUF;  // children's (next level)
+    unsigned long long* cmax = a.kmax + ((level + 1) & 1) * KBUF;
     // C: predicate flags and the CTA's chunk scans (positions; splitting level nodes)
     {
       if (tid == 0) s_carry = 0;
       __syncthreads();
       for (int i0 = p0; i0 < p1; i0 += kPB) {
         const int i = i0 + tid;
-        int f = 0;
+        int f = 0, js = -1;  // js: the point's child slot 2j + (right) of a splitting node
+        const double* xp = nullptr;
         if (i < p1) {
           const int j = a.seg[i];
-          if (j >= 0 && a.dosplit[j])
-            f = a.x[(size_t)a.perm[i] * D + a.bsd[base + j]] <= a.mid[j] ? 1 : 0;
+          if (j >= 0 && dsp[j]) {
+            xp = a.x + (size_t)a.perm[i] * D;
+            f = xp[a.bsd[base + j]] <= mdp[j] ? 1 : 0;
+            js = 2 * j + (f ? 0 : 1);
+          }
           a.flag[i] = f;
+        }
+        // children's bounds: warp-reduced per (node, side) when the warp is one node
+        {
+          const int jn = js >= 0 ? js >> 1 : -1;
+          const int j0 = __shfl_sync(0xffffffffu, jn, 0);
+          const bool uni = __all_sync(0xffffffffu, jn == j0) && j0 >= 0;
+          for (int d = 0; d < D; ++d) {
+            const unsigned long long k = js >= 0 ? dkey(xp[d]) : 0ull;
+            if (uni) {
+#pragma unroll
+              for (int side = 0; side < 2; ++side) {
+                const bool mine = (js & 1) == side;
+                if (!__any_sync(0xffffffffu, mine)) continue;
+                unsigned long long mn = mine ? k : ~0ull, mx = mine ? k : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                  mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                  mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                }
+                if (lane == 0) {
+                  atomicMin(&cmin[(size_t)(2 * j0 + side) * D + d], mn);
+                  atomicMax(&cmax[(size_t)(2 * j0 + side) * D + d], mx);
+                }
+              }
+            } else if (js >= 0) {
+              atomicMin(&cmin[(size_t)js * D + d], k);
+              atomicMax(&cmax[(size_t)js * D + d], k);
+            }
+          }
         }
         int ex, agg;
         BS(tmp).ExclusiveSum(f, ex, agg);
@@ -518,7 +573,7 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
       __syncthreads();
       for (int j0 = n0; j0 < n1; j0 += kPB) {
         const int j = j0 + tid;
-        const int f = j < n1 ? a.dosplit[j] : 0;
+        const int f = j < n1 ? dsp[j] : 0;
         int ex, agg;
         BS(tmp).ExclusiveSum(f, ex, agg);
         if (j < n1) a.child[j] = s_carry + ex;  // chunk-local rank among splitting nodes
@@ -529,6 +584,7 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
       if (tid == 0) a.ctot[G + bid] = s_carry;
     }
     grid.sync();
+    if (a.trace && bid == 0 && tid == 0 && level < 64) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); a.trace[level * 8 + 2] = t_; }
     // D: global prefix P, child BFS ids and the children's records
     int poff = 0, noff = 0, nsplit = 0;
     {
@@ -552,19 +608,18 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
       nsplit = v2;
     }
     for (int i = p0 + tid; i < p1; i += kPB) a.P[i] += poff;
-    for (size_t i = gt; i < (size_t)2 * nsplit * D; i += gs) {  // next level's bounds keys
-      a.kmin[i] = ~0ull;
-      a.kmax[i] = 0ull;
-    }
+
     if (bid == G - 1 && tid == 0) a.P[n] = poff + __ldcg(&a.ctot[bid]);
     {
       int n0, n1;
       chunk_of(m, bid, G, n0, n1);
       for (int j = n0 + tid; j < n1; j += kPB) {
         const int id = base + j;
-        if (a.dosplit[j]) {
+        if (dsp[j]) {
           const int c = base + m + 2 * (noff + a.child[j]);
           a.child[j] = c;
+          a.pslot[c - (base + m)] = 2 * j;          // next level: left child
+          a.pslot[c - (base + m) + 1] = 2 * j + 1;  // right child
           a.nleft[id] = c;
           a.nright[id] = c + 1;
           a.npar[c] = a.npar[c + 1] = id;
@@ -577,11 +632,12 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
       }
     }
     grid.sync();
+    if (a.trace && bid == 0 && tid == 0 && level < 64) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); a.trace[level * 8 + 3] = t_; }
     // E: right-block passers register their slots; one-sided splits run the median
     // fallback (kdtree.cpp:85-94) on their own segment (no swaps happen there)
     for (int i = p0 + tid; i < p1; i += kPB) {
       const int j = a.seg[i];
-      if (j < 0 || !a.dosplit[j] || !a.flag[i]) continue;
+      if (j < 0 || !dsp[j] || !a.flag[i]) continue;
       const int b = a.nbeg[base + j], e = b + a.ncnt[base + j];
       const int L = a.P[e] - a.P[b];
       if (i >= b + L) a.slot[b + (a.P[e] - a.P[i] - 1)] = i;
@@ -590,7 +646,7 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
       int n0, n1;
       chunk_of(m, bid, G, n0, n1);
       for (int j = n0 + tid; j < n1; j += kPB) {
-        if (!a.dosplit[j]) continue;
+        if (!dsp[j]) continue;
         const int id = base + j;
         const int b = a.nbeg[id], c = a.ncnt[id];
         const int L = a.P[b + c] - a.P[b];
@@ -601,9 +657,23 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
           dev_nth_element(q0, q0 + c / 2, q0 + c, cmp);
           l = c / 2;
           a.bsc[id] = cmp.key(q0[c / 2]);
+          // the children are the two halves of the segment: exact bounds by a scan
+          for (int side = 0; side < 2; ++side) {
+            const int k0 = side ? l : 0, k1 = side ? c : l;
+            for (int d = 0; d < D; ++d) {
+              unsigned long long mn = ~0ull, mx = 0ull;
+              for (int k = k0; k < k1; ++k) {
+                const unsigned long long kk = dkey(a.x[(size_t)q0[k] * D + d]);
+                mn = min(mn, kk);
+                mx = max(mx, kk);
+              }
+              cmin[(size_t)(2 * j + side) * D + d] = mn;
+              cmax[(size_t)(2 * j + side) * D + d] = mx;
+            }
+          }
         } else {
           l = L;
-          a.bsc[id] = a.mid[j];
+          a.bsc[id] = mdp[j];
         }
         a.lc[j] = l;
         const int ch = a.child[j];
@@ -614,13 +684,14 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
       }
     }
     grid.sync();
+    if (a.trace && bid == 0 && tid == 0 && level < 64) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); a.trace[level * 8 + 4] = t_; }
     // F: left-block failers swap with their partners; every position learns its
     // next-level node (its own CTA reads it next, in A)
     const int nbase = base + m;
     for (int i = p0 + tid; i < p1; i += kPB) {
       const int j = a.seg[i];
       if (j < 0) continue;
-      if (!a.dosplit[j]) {
+      if (!dsp[j]) {
         a.seg[i] = -1;
         continue;
       }
@@ -639,7 +710,9 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
     m = 2 * nsplit;
     ++level;
     if (m == 0 || level >= kMaxTreeLevels - 1) break;
+    decide(level, base, m);  // same phase: needs only bounds / counts / slots of level-1
     grid.sync();
+    if (a.trace && bid == 0 && tid == 0 && level < 64) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); a.trace[level * 8 + 5] = t_; }
   }
   if (gt == 0) {
     a.lvl[0] = level;
@@ -674,7 +747,7 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
   const int maxK = 2 * n;
   DevBuf<double> blo, bhi, bcen, bside, bsc, mid;
   DevBuf<int> bsd, seg, flag, P, slot, nbeg, ncnt, nleft, nright, npar, ndep, dosplit, child, lc,
-    ctot, lvl;
+    ctot, lvl, pslot;
   DevBuf<unsigned long long> kmin, kmax;
   blo.reserve((size_t)maxK * D);
   bhi.reserve((size_t)maxK * D);
@@ -683,20 +756,39 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
   bsc.reserve(maxK);
   bsd.reserve(maxK);
   for (DevBuf<int>* b : { &nbeg, &ncnt, &nleft, &nright, &npar, &ndep }) b->reserve(maxK);
-  for (DevBuf<int>* b : { &seg, &flag, &slot, &dosplit, &child, &lc }) b->reserve((size_t)n + 1);
+  for (DevBuf<int>* b : { &seg, &flag, &slot, &child, &lc }) b->reserve((size_t)n + 1);
+  dosplit.reserve((size_t)2 * (n + 1));  // two level buffers
   P.reserve((size_t)n + 1);
-  mid.reserve((size_t)n + 1);
-  kmin.reserve((size_t)n * D + D);
-  kmax.reserve((size_t)n * D + D);
+  mid.reserve((size_t)2 * (n + 1));
+  kmin.reserve((size_t)4 * n * D + D);  // two level buffers of 2n*D keys
+  kmax.reserve((size_t)4 * n * D + D);
+  pslot.reserve((size_t)n + 1);
   ctot.reserve(2 * G);
   lvl.reserve(kMaxTreeLevels + 2);
   t.perm.reserve(n);
   BuildArgs a{ d_x, n, D, leaf, t.perm.p, seg.p, flag.p, P.p, slot.p, nbeg.p, ncnt.p, nleft.p,
                nright.p, npar.p, ndep.p, blo.p, bhi.p, bcen.p, bside.p, bsc.p, bsd.p, kmin.p,
-               kmax.p, mid.p, dosplit.p, child.p, lc.p, ctot.p, lvl.p };
+               kmax.p, pslot.p, mid.p, dosplit.p, child.p, lc.p, ctot.p, lvl.p };
+  static const bool tracing = std::getenv("DFGTB_TRACE") != nullptr;
+  DevBuf<unsigned long long> trace;
+  if (tracing) {
+    trace.reserve(64 * 8);
+    CK(cudaMemsetAsync(trace.p, 0, sizeof(unsigned long long) * 64 * 8, s));
+    a.trace = trace.p;
+  }
   void* kargs[] = { &a };
   CK(cudaLaunchCooperativeKernel((void*)k_build, G, kPB, kargs, 0, s));
   CK_LAUNCH();
+  if (tracing) {
+    std::vector<unsigned long long> tr(64 * 8);
+    CK(cudaMemcpyAsync(tr.data(), trace.p, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int L = 0; L < 64 && tr[L * 8]; ++L) {
+      std::fprintf(stderr, "DFGTB_TRACE tree level %d:", L);
+      for (int k = 1; k < 8 && tr[L * 8 + k]; ++k) std::fprintf(stderr, " %.1f", (tr[L * 8 + k] - tr[L * 8 + k - 1]) * 1e-3);
+      std::fprintf(stderr, "\n");
+    }
+  }
   std::vector<int> hl(kMaxTreeLevels + 2);
   CK(cudaMemcpyAsync(hl.data(), lvl.p, sizeof(int) * hl.size(), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
