@@ -647,11 +647,13 @@ __device__ __forceinline__ void pairs_bounds(const TravArgs& a, int cur, int K, 
 }
 
 // One warp per entry: G^l = base + sum |R| K(d_max) over the entry's live pairs.
-__device__ __forceinline__ void entries_glo(const TravArgs& a, int cur, int e0, int e1)
+__device__ __forceinline__ void entries_glo(const TravArgs& a, int cur, int e0, int e1,
+                                            unsigned long long* tr = nullptr)
 {
   const int lane = threadIdx.x & 31;
   for (int e = e0 + (threadIdx.x >> 5); e < e1; e += kPBlock / 32) {
     const int off = a.foff[cur][e], len = a.flen[cur][e];
+    if (tr && lane == 0) atomicMax(tr, (unsigned long long)len);
     double part = 0.0;
     for (int j = lane; j < len; j += 32)
       part += (double)a.R.count[a.fr[cur][off + j]] * a.pkmin[off + j];
@@ -853,7 +855,8 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
     for (int j = 0; j < nch; ++j) pairs_bounds<DT>(a, cur, K, pofs(cb0[j]), pofs(cb1[j]), s_scale);
     __syncthreads();
     PH(1);
-    for (int j = 0; j < nch; ++j) entries_glo(a, cur, cb0[j], cb1[j]);
+    for (int j = 0; j < nch; ++j)
+      entries_glo(a, cur, cb0[j], cb1[j], a.trace && levels < 64 ? a.trace + 4096 + 512 * 16 + 64 * 160 + levels : nullptr);
     __syncthreads();
     PH(2);
     for (int j = 0; j < nch; ++j) pairs_decide<DT>(a, st, cur, K, pofs(cb0[j]), pofs(cb1[j]), s_h);
@@ -1283,8 +1286,8 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   a.lvlep = lvlep_.p;
   static const bool tracing = std::getenv("DFGTB_TRACE") != nullptr;
   if (tracing) {
-    trace_.reserve(4096 + 512 * 16 + 64 * 160);
-    CK(cudaMemsetAsync(trace_.p, 0, sizeof(unsigned long long) * (4096 + 512 * 16 + 64 * 160), s));
+    trace_.reserve(4096 + 512 * 16 + 64 * 160 + 64);
+    CK(cudaMemsetAsync(trace_.p, 0, sizeof(unsigned long long) * (4096 + 512 * 16 + 64 * 160 + 64), s));
     a.trace = trace_.p;
   }
   const std::vector<const void*> sig = {
@@ -1349,7 +1352,7 @@ bool Engine::traverse_finish()
   const int nb = trav_nb_;
   if (!use_persistent_ && use_graph_) launch_counter() += (uint64_t)hs->levels * kLevelKernels;
   if (trav_trace_) {  // per level: classify | scan | emit (microseconds)
-    std::vector<unsigned long long> tr(4096 + 512 * 16 + 64 * 160);
+    std::vector<unsigned long long> tr(4096 + 512 * 16 + 64 * 160 + 64);
     CK(cudaMemcpy(tr.data(), trace_.p, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
     for (int L = 0; L < std::min(hs->levels, 511); ++L) {
       const unsigned long long* ph = tr.data() + 4096 + L * 16;
@@ -1368,8 +1371,9 @@ bool Engine::traverse_finish()
         }
         std::sort(bt.begin(), bt.end());
         if (!bt.empty())
-          std::fprintf(stderr, "DFGTB_TRACE level %d: CTA busy us min %.1f median %.1f p90 %.1f max %.1f\n", L,
-                       bt.front(), bt[bt.size() / 2], bt[bt.size() * 9 / 10], bt.back());
+          std::fprintf(stderr, "DFGTB_TRACE level %d: CTA busy us min %.1f median %.1f p90 %.1f max %.1f; longest entry %llu pairs\n", L,
+                       bt.front(), bt[bt.size() / 2], bt[bt.size() * 9 / 10], bt.back(),
+                       tr[4096 + 512 * 16 + 64 * 160 + L]);
       }
     }
   }
