@@ -101,9 +101,10 @@ __device__ int d_order_f2l(double ratio, double count, double tau, int pmax, int
 __device__ void dev_choose(double nq, double nr, double sq, double sr, double h, double tau,
                            int pmax, int dim, int cost, int& kind, int& order)
 {
-  const int pf = d_order_ff(sr / (2.0 * h), nr, tau, pmax, dim);
-  const int pd = d_order_ff(sq / (2.0 * h), nr, tau, pmax, dim);
-  const int pt = d_order_f2l((sq < sr ? sr : sq) / (4.0 * h), nr, tau, pmax, dim);
+  const double i2h = 0.5 / h;  // one division per pair (ratios side / 2h, side / 4h)
+  const int pf = d_order_ff(sr * i2h, nr, tau, pmax, dim);
+  const int pd = d_order_ff(sq * i2h, nr, tau, pmax, dim);
+  const int pt = d_order_f2l((sq < sr ? sr : sq) * (0.5 * i2h), nr, tau, pmax, dim);
   const double D = (double)dim;
   double cf = CUDART_INF, cd = CUDART_INF, ct = CUDART_INF;
   if (cost == 0) {  // exponential model; integer powers are exact
@@ -284,7 +285,7 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
     const double kmax = a.pkmax[off + j], kmin = a.pkmin[off + j];
     const double nr = (double)a.R.count[R];
     const double dlo = nr * kmin;
-    const double tau = eps * nr * glo / ntot;
+    const double tau = (eps / ntot) * nr * glo;  // eps |R| G^l / N
     int kind = kX, order = 0;
     if (0.5 * nr * (kmax - kmin) <= tau) {  // kernel-difference prune, engine.cpp:137-148
       kind = kFD;
@@ -669,7 +670,7 @@ __device__ __forceinline__ void pairs_decide(const TravArgs& a, const TravState&
                                              int P0, int P1, const double* s_h)
 {
   const int D = DT ? DT : a.D;
-  const double eps = st.eps, ntot = st.ntot;
+  const double eps_nt = st.eps / st.ntot;
   for (int j0 = P0 + threadIdx.x; j0 < P1; j0 += kPBlock * kPU) {
   int ue[kPU], uR[kPU], ukey[kPU], ucnt[kPU];
   double uglo[kPU];
@@ -695,7 +696,7 @@ __device__ __forceinline__ void pairs_decide(const TravArgs& a, const TravState&
     const int R = uR[u];
     const double kmax = a.pkmax[j], kmin = a.pkmin[j];
     const double nr = (double)ucnt[u];
-    const double tau = eps * nr * uglo[u] / ntot;
+    const double tau = eps_nt * nr * uglo[u];  // eps |R| G^l / N
     int kind = kX, order = 0;
     if (0.5 * nr * (kmax - kmin) <= tau) {  // kernel-difference prune, engine.cpp:137-148
       kind = kFD;

@@ -1,4 +1,3 @@
-for v in default g3e8; do
-  if [ $v = default ]; then unset DFGTB_LIB; else export DFGTB_LIB=$PWD/paper_1102_2878_b200/build/v_$v/libdfgtb.so; fi
-  echo "== $v"; for c in 3 5; do python tools/profile_step.py --config $c; python tools/profile_step.py --config $c; done
-done
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for c in 1 2 3 4 5; do python tools/profile_step.py --config $c 2>&1 | tail -1; done
+python bench.py --steps 5 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['base_ms_per_step'], d['e2e']['value'])"
