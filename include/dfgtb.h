@@ -79,6 +79,10 @@ int dfgtb_create(const double* refs, size_t n, size_t d, const dfgtb_config* cfg
 /* Same with refs already in device memory. */
 int dfgtb_create_device(const double* d_refs, size_t n, size_t d, const dfgtb_config* cfg,
                         dfgtb_handle** out);
+/* float32 points (BASELINE config 5: fp32 inputs, fp64 accumulation): widened exactly
+ * to float64 on the device; identical results to dfgtb_create on the widened values. */
+int dfgtb_create_f32(const float* refs, size_t n, size_t d, const dfgtb_config* cfg,
+                     dfgtb_handle** out);
 void dfgtb_destroy(dfgtb_handle* h);
 
 /* DualTreeEngine::compute(queries, h)  engine.cpp:405-424 / engine.hpp:94-95.
@@ -96,6 +100,9 @@ int dfgtb_compute_batch(dfgtb_handle* h, const double* queries, size_t nq, const
                         size_t nb, double* out_sums, dfgtb_stats* stats);
 
 /* DualTreeEngine::last_stats / p_max  engine.hpp:97-99. */
+/* dfgtb_compute_batch with float32 queries (widened exactly on the device; Q != R). */
+int dfgtb_compute_batch_f32(dfgtb_handle* h, const float* queries, size_t nq, const double* bws,
+                            size_t nb, double* out_sums, dfgtb_stats* stats);
 int dfgtb_last_stats(dfgtb_handle* h, dfgtb_stats* stats);
 int dfgtb_last_timings(dfgtb_handle* h, dfgtb_timings* t);
 int dfgtb_p_max(dfgtb_handle* h);

@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("DFGTB_LIB") or os.path.join(_HERE, "libdfgtb.so")
 OK, EINVAL, ECUDA, ENOMEM = 0, 1, 2, 3
 
 _D = C.POINTER(C.c_double)
+_F = C.POINTER(C.c_float)
 _I = C.POINTER(C.c_int)
 _I64 = C.POINTER(C.c_int64)
 
@@ -51,7 +52,8 @@ class CvRow(C.Structure):
 
 # every symbol include/dfgtb.h declares (tests check the .so exports all of them)
 EXPORTS = (
-    "dfgtb_default_config", "dfgtb_create", "dfgtb_create_device", "dfgtb_destroy",
+    "dfgtb_default_config", "dfgtb_create", "dfgtb_create_device", "dfgtb_create_f32",
+    "dfgtb_compute_batch_f32", "dfgtb_destroy",
     "dfgtb_compute", "dfgtb_compute_device", "dfgtb_compute_batch", "dfgtb_last_stats",
     "dfgtb_last_timings",
     "dfgtb_p_max", "dfgtb_cv", "dfgtb_sweep", "dfgtb_lkcv_from_sums", "dfgtb_lscv_from_sums",
@@ -73,6 +75,8 @@ def _load():
         "dfgtb_default_config": (None, [C.POINTER(Config)]),
         "dfgtb_create": (C.c_int, [_D, sz, sz, C.POINTER(Config), C.POINTER(V)]),
         "dfgtb_create_device": (C.c_int, [V, sz, sz, C.POINTER(Config), C.POINTER(V)]),
+        "dfgtb_create_f32": (C.c_int, [_F, sz, sz, C.POINTER(Config), C.POINTER(V)]),
+        "dfgtb_compute_batch_f32": (C.c_int, [V, _F, sz, _D, sz, _D, C.POINTER(Stats)]),
         "dfgtb_destroy": (None, [V]),
         "dfgtb_compute": (C.c_int, [V, _D, sz, C.c_double, _D, C.POINTER(Stats)]),
         "dfgtb_compute_device": (C.c_int, [V, V, sz, C.c_double, V, C.POINTER(Stats)]),

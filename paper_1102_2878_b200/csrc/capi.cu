@@ -105,6 +105,24 @@ __global__ void k_series_op(DevSeries g, int op, const double* in, int n, const 
 
 }  // namespace
 
+__global__ void k_widen(const float* in, size_t n, double* out)
+{
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = (double)in[i];  // exact
+}
+
+// float32 host points -> float64 device points (the H2D moves half the bytes).
+static void widen_to_device(const float* h_in, size_t n, DevBuf<double>& out)
+{
+  DevBuf<float> f;
+  f.reserve(n);
+  out.reserve(n);
+  CK(cudaMemcpy(f.p, h_in, sizeof(float) * n, cudaMemcpyHostToDevice));
+  k_widen<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 16), 256>>>(f.p, n, out.p);
+  CK_LAUNCH();
+  CK(cudaDeviceSynchronize());
+}
+
 extern "C" {
 
 void dfgtb_default_config(dfgtb_config* c)
@@ -144,6 +162,26 @@ int dfgtb_create_device(const double* d_refs, size_t n, size_t d, const dfgtb_co
     auto* h = new dfgtb_handle;
     try {
       h->eng.reset(new Engine(d_refs, n, d, to_cfg(cfg), true));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int dfgtb_create_f32(const float* refs, size_t n, size_t d, const dfgtb_config* cfg,
+                     dfgtb_handle** out)
+{
+  return guard([&] {
+    if (!out) throw InvalidArgument("null output handle");
+    if (!refs && n) throw InvalidArgument("null reference points");
+    if (n == 0 || d == 0) throw InvalidArgument("PointSet requires N >= 1 and D >= 1");
+    DevBuf<double> wide;
+    widen_to_device(refs, n * d, wide);
+    auto* h = new dfgtb_handle;
+    try {
+      h->eng.reset(new Engine(wide.p, n, d, to_cfg(cfg), true));
     } catch (...) {
       delete h;
       throw;
@@ -291,6 +329,27 @@ int dfgtb_compute_batch(dfgtb_handle* h, const double* queries, size_t nq, const
       e.compute_batch(queries ? q.p : nullptr, nq, bws + b0, m, out.p);
       CK(cudaMemcpy(out_sums + b0 * n_out, out.p, sizeof(double) * n_out * m,
                     cudaMemcpyDeviceToHost));
+      if (stats)
+        for (int k = 0; k < m; ++k) fill_stats(e.last_stats(k), stats + b0 + k);
+    }
+  });
+}
+
+int dfgtb_compute_batch_f32(dfgtb_handle* h, const float* queries, size_t nq, const double* bws,
+                            size_t nb, double* out_sums, dfgtb_stats* stats)
+{
+  return guard([&] {
+    check_h(h);
+    Engine& e = *h->eng;
+    if (!queries) throw InvalidArgument("null query points");
+    if (nb == 0) throw InvalidArgument("empty bandwidth batch");
+    DevBuf<double> q, out;
+    widen_to_device(queries, nq * e.dim(), q);
+    out.reserve(nq * nb);
+    for (size_t b0 = 0; b0 < nb; b0 += kMaxSlots) {
+      const int m = (int)std::min<size_t>(kMaxSlots, nb - b0);
+      e.compute_batch(q.p, nq, bws + b0, m, out.p);
+      CK(cudaMemcpy(out_sums + b0 * nq, out.p, sizeof(double) * nq * m, cudaMemcpyDeviceToHost));
       if (stats)
         for (int k = 0; k < m; ++k) fill_stats(e.last_stats(k), stats + b0 + k);
     }

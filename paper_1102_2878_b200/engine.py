@@ -35,6 +35,7 @@ from . import _capi
 from ._capi import check, lib
 
 _D = C.POINTER(C.c_double)
+_F = C.POINTER(C.c_float)
 
 
 def _pts(x) -> np.ndarray:
@@ -128,13 +129,21 @@ class DualTreeEngine:
     the reference kd-tree there (KdTree::build bit-exact)."""
 
     def __init__(self, refs, mode: Mode = Mode.series, config: EngineConfig | None = None):
-        self.refs = _pts(refs)
         self.mode = Mode(mode)
         self.config = config or EngineConfig()
         h = C.c_void_p()
         cfg = self.config._c(self.mode)
-        check(lib.dfgtb_create(_dp(self.refs), self.refs.shape[0], self.refs.shape[1],
-                               C.byref(cfg), C.byref(h)))
+        if isinstance(refs, np.ndarray) and refs.dtype == np.float32:
+            # float32 points (BASELINE config 5): half the H2D bytes, widened exactly on
+            # the device; the host mirror keeps the widened values
+            r32 = np.ascontiguousarray(refs.reshape(-1, 1) if refs.ndim == 1 else refs)
+            self.refs = _pts(r32)
+            check(lib.dfgtb_create_f32(r32.ctypes.data_as(_F), r32.shape[0], r32.shape[1],
+                                       C.byref(cfg), C.byref(h)))
+        else:
+            self.refs = _pts(refs)
+            check(lib.dfgtb_create(_dp(self.refs), self.refs.shape[0], self.refs.shape[1],
+                                   C.byref(cfg), C.byref(h)))
         self._h = h
 
     def close(self):
@@ -173,6 +182,16 @@ class DualTreeEngine:
         """Sums for several bandwidths through one lock-step GPU traversal:
         row b = compute(queries, hs[b]).  Returns (len(hs), n_queries)."""
         hv = np.ascontiguousarray(hs, dtype=np.float64).ravel()
+        if isinstance(queries, np.ndarray) and queries.dtype == np.float32:
+            q32 = np.ascontiguousarray(queries.reshape(-1, 1) if queries.ndim == 1 else queries)
+            if q32.ndim != 2 or q32.shape[1] != self.refs.shape[1]:
+                raise ValueError("query and reference dimensions differ")
+            out = np.empty((hv.size, q32.shape[0]))
+            st = (_capi.Stats * max(1, hv.size))()
+            check(lib.dfgtb_compute_batch_f32(self._h, q32.ctypes.data_as(_F), q32.shape[0],
+                                              _dp(hv), hv.size, _dp(out), st))
+            self._batch_stats = [TraversalStats(**s.as_dict()) for s in st[:hv.size]]
+            return out
         if queries is None or queries is self.refs:
             q, nq, n_out = None, 0, self.refs.shape[0]
         else:

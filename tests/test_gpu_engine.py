@@ -303,3 +303,17 @@ def test_base_exp_mode_selection(dfgtb, orc, monkeypatch):
         g = e.compute(None, tiny)
     ex = orc.naive_kde(w.refs, w.refs, tiny)
     assert np.all(g >= 1.0) and np.max(np.abs((g - 1.0) - (ex - 1.0))) <= 0.01 * np.max(ex)
+
+
+def test_float32_inputs_match_widened(dfgtb):
+    """Config 5's fp32 inputs: dfgtb_create_f32 / dfgtb_compute_batch_f32 widen exactly
+    on the device, so results are bit-identical to the float64 path on the same values."""
+    w = datagen.config(5, scale_n=0.002)
+    r32, q32 = w.refs.astype(np.float32), w.queries.astype(np.float32)
+    hs = [s * w.h_s for s in w.scales]
+    cfg = dfgtb.EngineConfig(epsilon=0.01, leaf_threshold=32)
+    with dfgtb.DualTreeEngine(r32, config=cfg) as e32:
+        a = e32.compute_batch(q32, hs)
+    with dfgtb.DualTreeEngine(r32.astype(np.float64), config=cfg) as e64:
+        b = e64.compute_batch(q32.astype(np.float64), hs)
+    assert np.array_equal(a, b)
