@@ -1210,6 +1210,16 @@ __global__ void __launch_bounds__(kBlock) k_base_case_any(TreeView Q, TreeView R
 }
 
 // ---------------------------------------------------------------- far field
+// ancestor of `leaf` (depth dep) at depth k <= dep: the precomputed chain, or a parent
+// walk for leaves at least kMaxAnc deep
+__device__ __forceinline__ int ancestor_at(const TreeView& Q, int leaf, int dep, int k)
+{
+  if (dep < kMaxAnc) return Q.anc[(size_t)leaf * kMaxAnc + k];
+  int node = leaf;
+  for (int j = dep; j > k; --j) node = Q.parent[node];
+  return node;
+}
+
 // Every query evaluates the far-field expansions attached to its leaf or any ancestor,
 // root first (eval_farfield per query, engine.cpp:200-211).  One warp per (slot, leaf).
 __global__ void __launch_bounds__(kBlock) k_farfield(DevSeries g, TreeView Q, TreeView R, int K,
@@ -1228,16 +1238,14 @@ __global__ void __launch_bounds__(kBlock) k_farfield(DevSeries g, TreeView Q, Tr
     const double s = sv.s[slot];
     const double* spw = sv.spow + (size_t)slot * kSPow;
     const int qb = Q.begin[leaf], qc = Q.count[leaf];
-    int chain[64];
-    int depth = 0;
-    for (int n = leaf; n >= 0 && depth < 64; n = Q.parent[n]) chain[depth++] = n;
+    const int dep = Q.depth[leaf];
     for (int q0 = 0; q0 < qc; q0 += 32) {
       const int qi = q0 + lane;
       const bool act = qi < qc;
       const double* qp = Q.xs + (size_t)(qb + (act ? qi : 0)) * D;
       double acc = 0.0;
-      for (int k = depth - 1; k >= 0; --k) {
-        const int key = slot * K + chain[k];
+      for (int k = 0; k <= dep; ++k) {
+        const int key = slot * K + ancestor_at(Q, leaf, dep, k);
         const int c = cnt[key];
         const Item* it = items + off[key];
         for (int t = 0; t < c; ++t) {
@@ -1343,9 +1351,19 @@ __global__ void __launch_bounds__(kBlock) k_farfield_t(TreeView Q, TreeView R, i
 #pragma unroll
     for (int k = 0; k < ND; ++k) spw[k] = sv.spow[(size_t)slot * kSPow + k];
     const int qb = Q.begin[leaf], qc = Q.count[leaf];
-    int chain[64];
-    int depth = 0;
-    for (int n = leaf; n >= 0 && depth < 64; n = Q.parent[n]) chain[depth++] = n;
+    const int dep = Q.depth[leaf];
+    // the ancestors carrying far-field items, root first: one coalesced load of the
+    // leaf's chain per 32 levels and a ballot (deeper leaves walk parent pointers)
+    int anode[2] = { -1, -1 };
+    unsigned amask[2] = { 0u, 0u };
+    if (dep < kMaxAnc) {
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        const int k = w * 32 + lane;
+        if (k <= dep) anode[w] = Q.anc[(size_t)leaf * kMaxAnc + k];
+        amask[w] = __ballot_sync(0xffffffffu, anode[w] >= 0 && cnt[slot * K + anode[w]] > 0);
+      }
+    }
     for (int q0 = 0; q0 < qc; q0 += 32) {
       const int qi = q0 + lane;
       const bool act = qi < qc;
@@ -1353,14 +1371,22 @@ __global__ void __launch_bounds__(kBlock) k_farfield_t(TreeView Q, TreeView R, i
 #pragma unroll
       for (int d = 0; d < D; ++d) qv[d] = Q.xs[(size_t)(qb + (act ? qi : 0)) * D + d];
       double acc = 0.0;
-      for (int k = depth - 1; k >= 0; --k) {
-        const int key = slot * K + chain[k];
+      auto visit = [&](int node) {
+        const int key = slot * K + node;
         const int c = cnt[key];
         const Item* it = items + off[key];
         for (int t = 0; t < c; ++t) {
           const int r = it[t].r, order = it[t].code & 0xff;
           acc += ff_eval_t<D, PM>(Mt + (size_t)r * T, R.cen + (size_t)r * D, qv, s, order, spw);
         }
+      };
+      if (dep < kMaxAnc) {
+#pragma unroll
+        for (int w = 0; w < 2; ++w)
+          for (unsigned m = amask[w]; m; m &= m - 1)
+            visit(__shfl_sync(0xffffffffu, anode[w], __ffs(m) - 1));
+      } else {
+        for (int k = 0; k <= dep; ++k) visit(ancestor_at(Q, leaf, dep, k));
       }
       if (act) s_ff[(size_t)slot * nq + qb + qi] = acc;
     }
@@ -1389,14 +1415,13 @@ __global__ void k_finalize(DevSeries g, TreeView Q, int K, int nb, const int* le
   const double* qp = Q.xs + (size_t)i * g.D;
   double loc = 0.0;
   if (direct) {
-    int chain[64];
-    int depth = 0;
-    for (int a = leaf; a >= 0 && depth < 64; a = Q.parent[a]) chain[depth++] = a;
-    for (int k = depth - 1; k >= 0; --k) {
-      const int key = slot * K + chain[k];
+    const int dep = Q.depth[leaf];
+    for (int k = 0; k <= dep; ++k) {
+      const int a = ancestor_at(Q, leaf, dep, k);
+      const int key = slot * K + a;
       const int order = Lord[key];
       if (order > 0)
-        loc += dev_eval_local(g, L + (size_t)key * g.T, Q.cen + (size_t)chain[k] * g.D, qp, s, order);
+        loc += dev_eval_local(g, L + (size_t)key * g.T, Q.cen + (size_t)a * g.D, qp, s, order);
     }
   } else {
     const int order = Lord[lkey];
@@ -1476,7 +1501,11 @@ __global__ void __launch_bounds__(128) k_finalize_t(DevSeries g, TreeView Q, int
 #pragma unroll
   for (int d = 0; d < D; ++d) q[d] = Q.xs[(size_t)i * D + d];
   double loc = 0.0;
-  for (int a = leaf; a >= 0; a = Q.parent[a]) {
+  const int dep = Q.depth[leaf];
+  const int* anc = Q.anc + (size_t)leaf * kMaxAnc;
+  // leaf first; chains from the precomputed table (independent loads), deeper leaves
+  // walk parent pointers
+  for (int k = dep, a = leaf; k >= 0; --k, a = (dep < kMaxAnc ? (k >= 0 ? anc[k] : -1) : Q.parent[a])) {
     const int key = slot * K + a;
     if (Lord[key] <= 0) continue;
     const double* Lk = L + (size_t)key * g.T;

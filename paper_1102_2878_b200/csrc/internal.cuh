@@ -18,12 +18,13 @@ struct TreeView {
   const double *lo, *hi, *cen, *side;
   const int *left, *right, *count, *begin, *parent;
   const double* xs;
+  const int *depth, *anc;  // node depth; root-first ancestor chains (depth < kMaxAnc)
 };
 
 inline TreeView view_of(const DevTree& t)
 {
   return TreeView{ t.lo.p, t.hi.p, t.centroid.p, t.max_side.p, t.left.p, t.right.p,
-                   t.count.p, t.begin.p, t.parent.p, t.xs.p };
+                   t.count.p, t.begin.p, t.parent.p, t.xs.p, t.depth.p, t.anc.p };
 }
 
 inline int grid_warps(long long work)

@@ -365,6 +365,22 @@ __global__ void k_to_preorder(int K, int D, const int* bfs2pre, const double* bl
   by_depth[i] = p;
 }
 
+// Ancestor chain of every node (root first), for nodes with depth < kMaxAnc: kernels
+// that walk a leaf's ancestors read them with one coalesced load instead of a
+// dependent parent-pointer chain.
+__global__ void k_ancestors(int K, const int* parent, const int* depth, int* anc)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= K) return;
+  const int dp = depth[i];
+  if (dp >= kMaxAnc) return;
+  int a = i;
+  for (int k = dp; k >= 0; --k) {
+    anc[(size_t)i * kMaxAnc + k] = a;
+    a = parent[a];
+  }
+}
+
 __global__ void k_gather_points(const double* x, const int* perm, int n, int D, double* xs)
 {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -998,6 +1014,9 @@ static void finish_tree(DevTree& t, const double* d_x, int n, int D, int K,
     K, D, d_map.p, blo, bhi, bcen, bside, bsc, bsd, d_bleft, d_bright, d_bbeg, d_bcnt, d_bpar,
     d_bdep, t.lo.p, t.hi.p, t.centroid.p, t.max_side.p, t.split_coord.p, t.split_dim.p, t.left.p,
     t.right.p, t.begin.p, t.count.p, t.parent.p, t.depth.p, t.by_depth.p);
+  CK_LAUNCH();
+  t.anc.reserve((size_t)K * kMaxAnc);
+  k_ancestors<<<ceil_div(K, 256), 256, 0, s>>>(K, t.parent.p, t.depth.p, t.anc.p);
   CK_LAUNCH();
   t.xs.reserve((size_t)n * D);
   k_gather_points<<<ceil_div((long long)n * D, 256), 256, 0, s>>>(d_x, t.perm.p, n, D, t.xs.p);

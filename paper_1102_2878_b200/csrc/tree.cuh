@@ -5,6 +5,8 @@
 
 namespace dfgtb {
 
+constexpr int kMaxAnc = 64;
+
 // Device-resident kd-tree.  Node arrays are indexed by the reference's PREORDER
 // node id (root = 0, left child = parent + 1); `by_depth` lists the preorder ids
 // level by level (BFS order), with `depth_off` the host-side level offsets.
@@ -16,6 +18,8 @@ struct DevTree {
   DevBuf<double> max_side, split_coord; // nodes
   DevBuf<int> left, right, split_dim, begin, count, parent, depth;  // nodes
   DevBuf<int> by_depth;       // nodes (preorder ids grouped by depth)
+  DevBuf<int> anc;            // nodes x kMaxAnc: ancestors root first (anc[d] at depth d),
+                              // for nodes shallower than kMaxAnc
   std::vector<int> depth_off; // height+1 offsets into by_depth
   std::vector<int> h_count;   // host copy of count (preorder)
   std::vector<int> h_left;    // host copy of left (preorder)
