@@ -23,11 +23,20 @@ uint64_t& launch_counter()
 }
 
 // ---------------------------------------------------------- caching allocators
+// Device blocks are cached per (device, size).  A freed block may still be in use by
+// work queued on its owner's streams, so frees go to a pending list and become
+// reusable after ONE device synchronisation, taken only when an allocation could
+// reuse them (not one synchronisation per free: an engine releases ~40 buffers).
 namespace {
 std::mutex g_cache_mu;
-std::unordered_map<size_t, std::vector<void*>>& dev_cache()
+std::unordered_map<uint64_t, std::vector<void*>>& dev_cache()
 {
-  static auto* c = new std::unordered_map<size_t, std::vector<void*>>();  // never destroyed
+  static auto* c = new std::unordered_map<uint64_t, std::vector<void*>>();  // never destroyed
+  return *c;
+}
+std::vector<std::pair<uint64_t, void*>>& dev_pending()
+{
+  static auto* c = new std::vector<std::pair<uint64_t, void*>>();
   return *c;
 }
 std::unordered_map<size_t, std::vector<void*>>& host_cache()
@@ -35,17 +44,39 @@ std::unordered_map<size_t, std::vector<void*>>& host_cache()
   static auto* c = new std::unordered_map<size_t, std::vector<void*>>();
   return *c;
 }
+uint64_t cache_key(size_t bytes)
+{
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return ((uint64_t)bytes << 8) | (uint64_t)(dev & 0xff);
+}
+void* take_cached(uint64_t key)  // g_cache_mu held
+{
+  auto it = dev_cache().find(key);
+  if (it == dev_cache().end() || it->second.empty()) return nullptr;
+  void* p = it->second.back();
+  it->second.pop_back();
+  return p;
+}
 }  // namespace
 
 void* cache_alloc(size_t bytes)
 {
+  const uint64_t key = cache_key(bytes);
   {
-    std::lock_guard<std::mutex> g(g_cache_mu);
-    auto it = dev_cache().find(bytes);
-    if (it != dev_cache().end() && !it->second.empty()) {
-      void* p = it->second.back();
-      it->second.pop_back();
-      return p;
+    std::unique_lock<std::mutex> g(g_cache_mu);
+    if (void* p = take_cached(key)) return p;
+    bool match = false;
+    for (const auto& e : dev_pending()) match = match || e.first == key;
+    if (match) {
+      // only the blocks pending before the synchronisation are known idle afterwards
+      std::vector<std::pair<uint64_t, void*>> idle;
+      idle.swap(dev_pending());
+      g.unlock();
+      if (cudaDeviceSynchronize() != cudaSuccess) cudaGetLastError();
+      g.lock();
+      for (auto& e : idle) dev_cache()[e.first].push_back(e.second);
+      if (void* p = take_cached(key)) return p;
     }
   }
   void* p = nullptr;
@@ -61,12 +92,9 @@ void* cache_alloc(size_t bytes)
 
 void cache_free(void* p, size_t bytes)
 {
-  if (cudaDeviceSynchronize() != cudaSuccess) {  // context gone (process exit) or faulted
-    cudaGetLastError();
-    return;
-  }
+  const uint64_t key = cache_key(bytes);
   std::lock_guard<std::mutex> g(g_cache_mu);
-  dev_cache()[bytes].push_back(p);
+  dev_pending().emplace_back(key, p);
 }
 
 void cache_release_all()
@@ -76,6 +104,8 @@ void cache_release_all()
   for (auto& kv : dev_cache())
     for (void* p : kv.second) cudaFree(p);
   dev_cache().clear();
+  for (auto& e : dev_pending()) cudaFree(e.second);
+  dev_pending().clear();
   for (auto& kv : host_cache())
     for (void* p : kv.second) cudaFreeHost(p);
   host_cache().clear();
@@ -207,6 +237,13 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
   init_device_constants(s_);
   CK(cudaEventRecord(ev_[0], s_));
   build_tree(rt_, x_.p, (int)n, D_, cfg.leaf_threshold, s_);
+  if (std::getenv("DFGTB_TRACE")) {
+    CK(cudaEventRecord(ev_[2], s_));
+    CK(cudaEventSynchronize(ev_[2]));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ev_[0], ev_[2]));
+    std::fprintf(stderr, "DFGTB_TRACE create: upload+tree %.3f ms\n", ms);
+  }
   if (cfg.mode == 1) {
     if (ser_.T <= 4096) {
       eager_ = true;

@@ -15,6 +15,7 @@
 //                  on the node's segment; these nodes are rare (duplicates).
 // Nodes are numbered in BFS order while building and renumbered to the reference's
 // preorder ids at the end.
+#include <chrono>
 #include "tree.cuh"
 
 #include <cooperative_groups.h>
@@ -793,6 +794,7 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
     a.trace = trace.p;
   }
   void* kargs[] = { &a };
+  const auto c0 = std::chrono::steady_clock::now();
   CK(cudaLaunchCooperativeKernel((void*)k_build, G, kPB, kargs, 0, s));
   CK_LAUNCH();
   if (tracing) {
@@ -800,8 +802,14 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
     CK(cudaMemcpyAsync(tr.data(), trace.p, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     for (int L = 0; L < 64 && tr[L * 8]; ++L) {
-      std::fprintf(stderr, "DFGTB_TRACE tree level %d:", L);
-      for (int k = 1; k < 8 && tr[L * 8 + k]; ++k) std::fprintf(stderr, " %.1f", (tr[L * 8 + k] - tr[L * 8 + k - 1]) * 1e-3);
+      std::fprintf(stderr, "DFGTB_TRACE tree level %d (us):", L);
+      unsigned long long prev = tr[L * 8];
+      for (int k = 1; k < 8; ++k)
+        if (tr[L * 8 + k]) {
+          std::fprintf(stderr, " p%d %.1f", k, (tr[L * 8 + k] - prev) * 1e-3);
+          prev = tr[L * 8 + k];
+        }
+      if (L + 1 < 64 && tr[L * 8 + 8]) std::fprintf(stderr, " total %.1f", (tr[L * 8 + 8] - tr[L * 8]) * 1e-3);
       std::fprintf(stderr, "\n");
     }
   }
@@ -821,8 +829,15 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
   t.n = n;
   t.D = D;
   t.leaf = leaf;
+  const auto c1 = std::chrono::steady_clock::now();
   finish_tree(t, d_x, n, D, K, h_left, h_right, h_beg, h_cnt, level_off, blo.p, bhi.p, bcen.p,
               bside.p, bsc.p, bsd.p, nleft.p, nright.p, nbeg.p, ncnt.p, npar.p, ndep.p, s);
+  if (tracing) {
+    const auto c2 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "DFGTB_TRACE tree host: build+copies %.1f us, finish %.1f us (G=%d, levels %d, K %d)\n",
+                 std::chrono::duration<double, std::micro>(c1 - c0).count(),
+                 std::chrono::duration<double, std::micro>(c2 - c1).count(), G, levels, K);
+  }
   return true;
 }
 
