@@ -112,6 +112,8 @@ private:
   SeriesTables ser_;
   DevBuf<unsigned char> ser_dev_;
   DevBuf<int> leaves_, leaf_of_pos_;  // of the current query tree
+  DevBuf<int> mom_node_, mom_start_, mom_off_;  // eager moments: chunk lists
+  DevBuf<double> mom_part_;                     // eager moments: chunk partials
   std::vector<int> qleaves_host_;
   int leaves_src_ = -1;     // 0: leaves_ describe the reference tree, 1: a query tree
   // per batch (node-indexed arrays are slot-major: key = slot * K + node)

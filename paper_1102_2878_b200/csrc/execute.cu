@@ -1705,6 +1705,8 @@ void init_exp_constants(cudaStream_t s)
 }
 
 // Unscaled moments of every reference node, once per tree (tables <= 4096 terms).
+// Queued on s2_ without a host wait: every consumer of Mt_ runs on s2_ after it, so
+// the moments overlap whatever the caller does next (the first batch's traversal).
 void Engine::eager_moments()
 {
   const DevTree& t = rt_;
@@ -1719,34 +1721,38 @@ void Engine::eager_moments()
   }
   coff[K] = (int)cnode.size();
   const int nch = (int)cnode.size();
-  DevBuf<int> dn, ds, dof;
-  DevBuf<double> part;
+  DevBuf<int>& dn = mom_node_;
+  DevBuf<int>& ds = mom_start_;
+  DevBuf<int>& dof = mom_off_;
+  DevBuf<double>& part = mom_part_;  // members: alive until the queued kernels are done
+  cudaStream_t s2 = s2_;
+  CK(cudaEventRecord(fork_, s_));
+  CK(cudaStreamWaitEvent(s2, fork_, 0));
   dn.reserve(nch);
   ds.reserve(nch);
   dof.reserve(K + 1);
   part.reserve((size_t)nch * T);
-  CK(cudaMemcpyAsync(dn.p, cnode.data(), sizeof(int) * nch, cudaMemcpyHostToDevice, s_));
-  CK(cudaMemcpyAsync(ds.p, cstart.data(), sizeof(int) * nch, cudaMemcpyHostToDevice, s_));
-  CK(cudaMemcpyAsync(dof.p, coff.data(), sizeof(int) * (K + 1), cudaMemcpyHostToDevice, s_));
+  CK(cudaMemcpyAsync(dn.p, cnode.data(), sizeof(int) * nch, cudaMemcpyHostToDevice, s2));
+  CK(cudaMemcpyAsync(ds.p, cstart.data(), sizeof(int) * nch, cudaMemcpyHostToDevice, s2));
+  CK(cudaMemcpyAsync(dof.p, coff.data(), sizeof(int) * (K + 1), cudaMemcpyHostToDevice, s2));
   Mt_.reserve((size_t)K * T);
   const DevSeries g = dev_series();
   const int smem = kMomChunk * D_ * ser_.pmax * (int)sizeof(double);
   const int pm = ser_.pmax;
   const int gw = std::min(ceil_div(nch, 4), 148 * 16);
-#define MOM_T(DD, PP) k_moment_chunks_w<DD, PP><<<gw, 128, 0, s_>>>(g, view_of(t), dn.p, ds.p, nch, part.p)
+#define MOM_T(DD, PP) k_moment_chunks_w<DD, PP><<<gw, 128, 0, s2>>>(g, view_of(t), dn.p, ds.p, nch, part.p)
   if (D_ == 1 && pm == 8) MOM_T(1, 8);
   else if (D_ == 2 && pm == 6) MOM_T(2, 6);
   else if (D_ == 3 && pm == 4) MOM_T(3, 4);
   else if (D_ == 4 && pm == 2) MOM_T(4, 2);
   else if (D_ == 5 && pm == 2) MOM_T(5, 2);
   else
-    k_moment_chunks<<<std::min(nch, 148 * 16), 128, smem, s_>>>(g, view_of(t), dn.p, ds.p, nch,
+    k_moment_chunks<<<std::min(nch, 148 * 16), 128, smem, s2>>>(g, view_of(t), dn.p, ds.p, nch,
                                                                  part.p);
 #undef MOM_T
   CK_LAUNCH();
-  k_moment_reduce<<<std::min(K, 148 * 8), kMomRedThreads, 0, s_>>>(g, K, dof.p, part.p, Mt_.p);
+  k_moment_reduce<<<std::min(K, 148 * 8), kMomRedThreads, 0, s2>>>(g, K, dof.p, part.p, Mt_.p);
   CK_LAUNCH();
-  CK(cudaStreamSynchronize(s_));
 }
 
 void Engine::setup_leaves(const DevTree& t)
