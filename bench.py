@@ -192,7 +192,8 @@ def run_ours(a, rank, world, local_rank):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
     peak_instr = _capi.lib.dfgtb_dfma_peak()
     peak_ex2 = _capi.lib.dfgtb_ex2_peak()
-    mufu = _capi.lib.dfgtb_base_exp_mode(eng.handle) == 1
+    exp_mode = _capi.lib.dfgtb_base_exp_mode(eng.handle)
+    mufu = exp_mode >= 1
 
     def step():
         return eng.sweep(w.scales, w.h_s)
@@ -267,7 +268,10 @@ def run_ours(a, rank, world, local_rank):
               "base_ms_per_step": base_ms / max(a.steps, 1)}
     if mufu:
         # one MUFU ex2 per (q, r) pair: the SFU pipe is the exp roofline
-        roof = {"bound": "sfu", "kernel": "k_base_case (K10 exhaustive base case, MUFU ex2 path)",
+        kname = ("k_base_f32 + k_base_case (K10 exhaustive base case: FP32 distance/ex2/partial sums "
+                 "for the leaf pairs that qualify, MUFU ex2 with FP64 distance and sums for the rest)"
+                 if exp_mode == 2 else "k_base_case (K10 exhaustive base case, MUFU ex2 path)")
+        roof = {"bound": "sfu", "kernel": kname,
                 "achieved": pairs_per_s / 1e9, "peak": peak_ex2 / 1e9, "unit": "G ex2/s (1 per pair)",
                 "frac": pairs_per_s / peak_ex2 if peak_ex2 > 0 else None,
                 "peak_source": "measured ex2.approx.f32 throughput (dfgtb_ex2_peak) on this GPU",

@@ -107,8 +107,10 @@ int dfgtb_last_stats(dfgtb_handle* h, dfgtb_stats* stats);
 int dfgtb_last_timings(dfgtb_handle* h, dfgtb_timings* t);
 int dfgtb_p_max(dfgtb_handle* h);
 
-/* Base-case exp of this handle: 1 = MUFU ex2 (epsilon >= 1e-4, error charged against
- * epsilon), 0 = FP64 exp (<= ~1 ulp); -1 on a bad handle. */
+/* Base-case exp of this handle: 2 = FP32 distance / ex2 / partial sums for the leaf
+ * pairs that qualify, MUFU ex2 with FP64 distance and sums for the rest (epsilon >=
+ * 5e-3, 3e-4 charged against epsilon); 1 = MUFU ex2 only (epsilon >= 1e-4, 4e-6
+ * charged); 0 = FP64 exp (<= ~1 ulp); -1 on a bad handle. */
 int dfgtb_base_exp_mode(dfgtb_handle* h);
 
 /* lkcv_from_sums + lscv_from_sums on Q = R sums computed on the device at h and
@@ -161,6 +163,22 @@ double dfgtb_ex2_peak(void);
 /* Max relative error of the base case's MUFU exp (used when epsilon >= 1e-4; its
  * bound is charged against epsilon) over every argument it can form; test entry. */
 double dfgtb_mufu_exp_error(void);
+
+/* Base-case tasks (32-query chunk x run of reference leaves) of the handle's last
+ * compute that ran on the FP32 kernel and on the FP64 kernel, and their (q, r) pairs
+ * (pair pointers may be NULL; synchronises). */
+int dfgtb_last_base_split(dfgtb_handle* h, int* f32_tasks, int* fp64_tasks, uint64_t* f32_pairs,
+                          uint64_t* fp64_pairs);
+
+/* Max relative error of ex2.approx.ftz.f32 -- the FP32 base case's exp (used when
+ * epsilon >= 5e-3; kF32Charge) -- over every FP32 argument in [-126, 2^-10]; test entry. */
+double dfgtb_f32_exp_error(void);
+
+/* The FP32 base case's term for n (query q_i, reference r_i) pairs, exactly as the
+ * kernel forms it: points are D-dimensional, already in z units (|q - r|^2 = z, the
+ * term approximates 2^-z), centred on c (D doubles) before rounding to FP32.  out[i]
+ * receives the term (test entry for the kF32Charge bound; d in 1..5). */
+int dfgtb_f32_terms(size_t d, const double* q, const double* r, const double* c, size_t n, double* out);
 
 /* Device (and pinned host) memory of destroyed handles is cached for reuse by later
  * handles, like PyTorch's caching allocator; this returns it to the driver. */

@@ -58,7 +58,7 @@ EXPORTS = (
     "dfgtb_last_timings",
     "dfgtb_p_max", "dfgtb_cv", "dfgtb_sweep", "dfgtb_lkcv_from_sums", "dfgtb_lscv_from_sums",
     "dfgtb_tree_nodes", "dfgtb_tree_height", "dfgtb_export_tree", "dfgtb_naive",
-    "dfgtb_series_op", "dfgtb_dfma_peak", "dfgtb_mufu_exp_error", "dfgtb_ex2_peak", "dfgtb_base_exp_mode", "dfgtb_device_count", "dfgtb_release_cached_memory",
+    "dfgtb_series_op", "dfgtb_dfma_peak", "dfgtb_mufu_exp_error", "dfgtb_f32_exp_error", "dfgtb_f32_terms", "dfgtb_last_base_split", "dfgtb_ex2_peak", "dfgtb_base_exp_mode", "dfgtb_device_count", "dfgtb_release_cached_memory",
     "dfgtb_stream",
     "dfgtb_launch_count", "dfgtb_last_error",
 )
@@ -96,6 +96,9 @@ def _load():
                                       _D]),
         "dfgtb_dfma_peak": (C.c_double, []),
         "dfgtb_mufu_exp_error": (C.c_double, []),
+        "dfgtb_f32_exp_error": (C.c_double, []),
+        "dfgtb_last_base_split": (C.c_int, [V, _I, _I, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+        "dfgtb_f32_terms": (C.c_int, [sz, _D, _D, _D, sz, _D]),
         "dfgtb_ex2_peak": (C.c_double, []),
         "dfgtb_base_exp_mode": (C.c_int, [V]),
         "dfgtb_device_count": (C.c_int, []),

@@ -238,7 +238,11 @@ int dfgtb_last_timings(dfgtb_handle* h, dfgtb_timings* t)
 
 int dfgtb_p_max(dfgtb_handle* h) { return h && h->eng ? h->eng->p_max() : -1; }
 
-int dfgtb_base_exp_mode(dfgtb_handle* h) { return h && h->eng ? (h->eng->mufu_exp() ? 1 : 0) : -1; }
+int dfgtb_base_exp_mode(dfgtb_handle* h)
+{
+  if (!h || !h->eng) return -1;
+  return h->eng->f32_exp() ? 2 : h->eng->mufu_exp() ? 1 : 0;
+}
 
 // Batched CV: every bandwidth (and its convolution bandwidth) of `ns` scales goes
 // through ONE lock-step traversal; sums stay in HBM; CV partial sums come back.
@@ -531,6 +535,35 @@ double dfgtb_mufu_exp_error(void)
   double v = -1.0;
   guard([&] { v = mufu_exp_max_error(); });
   return v;
+}
+
+int dfgtb_last_base_split(dfgtb_handle* h, int* f32_tasks, int* fp64_tasks, uint64_t* f32_pairs,
+                          uint64_t* fp64_pairs)
+{
+  return guard([&] {
+    if (!h || !h->eng || !f32_tasks || !fp64_tasks) throw InvalidArgument("dfgtb_last_base_split: null argument");
+    unsigned long long a = 0, b = 0;
+    h->eng->base_split(*f32_tasks, *fp64_tasks, a, b);
+    if (f32_pairs) *f32_pairs = a;
+    if (fp64_pairs) *fp64_pairs = b;
+  });
+}
+
+double dfgtb_f32_exp_error(void)
+{
+  double v = -1.0;
+  guard([&] { v = f32_exp_max_error(); });
+  return v;
+}
+
+int dfgtb_f32_terms(size_t d, const double* q, const double* r, const double* c, size_t n, double* out)
+{
+  return guard([&] {
+    if (d < 1 || d > 5) throw InvalidArgument("dfgtb_f32_terms: d must be in 1..5");
+    if (n == 0) return;
+    if (!q || !r || !c || !out) throw InvalidArgument("dfgtb_f32_terms: null pointer");
+    f32_terms_host((int)d, q, r, c, n, out);
+  });
 }
 
 }  // extern "C"

@@ -218,6 +218,7 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
   n_ = n;
   if (const char* sl = std::getenv("DFGTB_BASE_SLACK")) base_cta_slack_ = std::atoi(sl);
   mufu_ = cfg.epsilon >= kMufuMinEps && D_ <= 5 && std::getenv("DFGTB_EXACT_EXP") == nullptr;
+  f32_ = mufu_ && cfg.epsilon >= kF32MinEps && std::getenv("DFGTB_NO_F32") == nullptr;
   const int pm = cfg.mode == 0 ? 1 : (cfg.p_max > 0 ? cfg.p_max : default_p_max(D_));
   ser_ = SeriesTables(D_, pm);
   if (D_ * (pm - 1) >= 128) throw InvalidArgument("D * (p_max - 1) must be < 128");

@@ -54,6 +54,14 @@ constexpr int kMaxSlots = 64;  // bandwidths per batch
 // keep the FP64 exp (<= ~1 ulp).
 constexpr double kMufuMinEps = 1e-4;
 constexpr double kMufuCharge = 4e-6;
+// FP32 base case (execute.cu FPt / base_group_f32): FP32 differences, distance and
+// partial sums, ex2.approx.f32 of the whole argument.  Applies to leaf pairs whose query leaf spans
+// <= kF32Diam in units where |q - r|^2 = z = log2 e |q - r|^2 / 2h^2 and whose sums are >= 1e-20 (or
+// Q = R); per-term relative error < kF32Charge (derivation at FPt).  Used when
+// eps >= kF32MinEps (the charge is then <= 5% of the budget) unless DFGTB_NO_F32 is set.
+constexpr double kF32MinEps = 5e-3;
+constexpr double kF32Charge = 2e-4;
+constexpr double kF32Diam = 48.0;
 
 int default_p_max(int D);
 
@@ -82,6 +90,12 @@ public:
   const DevTree& ref_tree() const { return rt_; }
   int p_max() const { return ser_.pmax; }
   bool mufu_exp() const { return mufu_; }
+  bool f32_exp() const { return f32_; }
+  // tasks of the last batch's base case on the FP32 / FP64 kernels (synchronises)
+  void base_split(int& f32_tasks, int& fp64_tasks, unsigned long long& f32_pairs,
+                  unsigned long long& fp64_pairs);
+  // the share of eps the base case's reduced-precision exp is charged
+  double exp_charge() const { return f32_ ? kF32Charge : mufu_ ? kMufuCharge : 0.0; }
   int dim() const { return D_; }
   size_t n() const { return n_; }
   cudaStream_t stream() const { return s_; }
@@ -152,6 +166,7 @@ private:
   long long nF_ = 0, nDT_ = 0, nB_ = 0;
   int nb_ = 1;
   bool mufu_ = false;
+  bool f32_ = false;
   // device-side counts of a batch (no host round trip until its end):
   // [0] nF [1] nDT [2] nB [3] traversal overflow [4] local chunks [5] base tasks
   DevBuf<int> bc_;
@@ -170,6 +185,10 @@ double measure_dfma_peak(int device);
 double measure_ex2_peak(int device);
 // Max relative error of the base case's MUFU exp over every argument it can form.
 double mufu_exp_max_error();
+// Max relative error of ex2.approx.ftz.f32 over every FP32 argument in [-126, 2^-10].
+double f32_exp_max_error();
+// The FP32 base case's term for host pairs (test entry; points in z units, stride d).
+void f32_terms_host(int d, const double* q, const double* r, const double* c, size_t n, double* out);
 
 // Series term tables -> one device blob, and the device view over it.
 void upload_series(const SeriesTables& t, DevBuf<unsigned char>& dev, cudaStream_t s);

@@ -15,6 +15,7 @@
 #include <cstring>
 
 #include <cub/device/device_scan.cuh>
+#include <math_constants.h>
 
 #include <algorithm>
 #include <cfloat>
@@ -794,14 +795,15 @@ struct PtLoad {
 
 // Compact reference-leaf records for the base case, in sorted item order:
 // {first sorted position, count | flags << 28}; flags bit 0: the traversal proved
-// y <= 708 for every pair; bit 1: terms may be clamped at 2^-1021 (see traverse.cu).
+// y <= 708 for every pair; bit 1: terms may be clamped at 2^-1021; bit 2: the FP32 base
+// case applies (see traverse.cu).
 __global__ void k_base_records(const Item* items, const int* n, int cap, TreeView R, int2* rec)
 {
   const int m = min(*n, cap);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
     const Item it = items[i];
     const int c = R.count[it.r];
-    rec[i] = make_int2(R.begin[it.r], c | ((it.code & 3) << 28));
+    rec[i] = make_int2(R.begin[it.r], c | ((it.code & 7) << 28));
   }
 }
 
@@ -894,6 +896,31 @@ __device__ __forceinline__ void base_group(const double* rs, int n, const double
   if ((lane & ((32 >> LG) - 1)) == 0) qsum[lane >> (5 - LG)] += acc[0];
 }
 
+// A point's DP scaled coordinates in registers (vector loads; staging loads all of a
+// tile's points before storing them).
+template <int DT>
+struct RawPt {
+  static constexpr int DP = PtLoad<DT>::DP;
+  double x[DP];
+  __device__ __forceinline__ static RawPt load(const double* src, int j)
+  {
+    RawPt r;
+    PtLoad<DT>::load(src, j, r.x);
+    return r;
+  }
+  // point j2 of dst (stride DP, 16-byte vectors)
+  __device__ __forceinline__ void store(double* dst, int j2) const
+  {
+    if constexpr (DT == 1) {
+      dst[j2] = x[0];
+    } else {
+      double2* d2 = reinterpret_cast<double2*>(dst + (size_t)j2 * DP);
+#pragma unroll
+      for (int k = 0; k < DP / 2; ++k) d2[k] = make_double2(x[2 * k], x[2 * k + 1]);
+    }
+  }
+};
+
 // MUFU variant: the stream holds centred (log2e-scaled) points r and |r|^2 (stride DM),
 // the query tile the same (q, |q|^2); per pair t = fma(-2q_d, r_d, .. (M + |q|^2) + |r|^2).
 template <int DT>
@@ -926,11 +953,10 @@ struct MPt {
 #pragma unroll
     for (int d = DT + 1; d < DM; ++d) v[d] = 0.0;
   }
-  __device__ __forceinline__ static void stage(const double* src, int j, const double* c, double* dst,
-                                               int j2)
+  __device__ __forceinline__ static void stage(const RawPt<DT>& p, const double* c, double* dst, int j2)
   {
     double v[DM];
-    centred(src, j, c, v);
+    centred(p.x, 0, c, v);
 #pragma unroll
     for (int k = 0; k < DM / 2; ++k)
       reinterpret_cast<double2*>(dst + k * PL)[j2] = make_double2(v[2 * k], v[2 * k + 1]);
@@ -1035,6 +1061,192 @@ __device__ __forceinline__ void base_groups_mufu(const double* rs, int n, const 
   if (qc - g0 >= 1) base_group_mufu_call<DT, 1, CLAMP>(rs, n, qs + g0 * DM, qsum + g0, lane);
 }
 
+// FP32 base case (leaf pairs the traversal flagged with order bit 2: the query leaf spans
+// <= kF32Diam in z units and the query sums are provably >= 1e-20 or Q = R).  Points are
+// centred on the chunk's first query in FP64 and rounded to FP32 (q~, r~), and per pair
+//   z = sum_d (q~_d - r~_d)^2,   term = ex2.approx.ftz(-z),
+// D FP32 subtractions, D multiply-adds, one MUFU and one FP32 add: no FP64 instruction in
+// the pair loop.  Terms below 2^-126 flush to 0 (absolute error <= N 2^-126 against sums
+// >= 1e-20).  The self pair (Q = R) is exactly 1: q~ - q~ = 0.
+// Per-term relative error for z <= 127 (|q| <= 48 = kF32Diam, |r| <= 48 + sqrt z, unit
+// roundoff u = 2^-24):
+//   coordinate rounding   |d(q - r)| <= u (|q| + |r|)               -> 2 sqrt(z) u (96 + sqrt z)
+//   differences           |d a_d| <= u |a_d|                         -> 2 z u
+//   squares and sums      D roundings of partial sums <= 127         -> D 127 u
+//   -> |dz| <= 2 sqrt(127) (96 + 2 sqrt(127)) u + 5 127 u = 1.97e-4 at D = 5,
+//   |dz| ln 2 <= 1.37e-4 relative, + ex2.approx (< 2^-22, measured exhaustively by
+//   dfgtb_f32_exp_error) + FP32 partial sums (<= 8 terms per lane + 5 reduction levels:
+//   12 u = 7.2e-7): below kF32Charge = 2e-4, which the traversal pays for.
+template <int DT>
+struct FPt {
+  static constexpr int DF = DT <= 4 ? 4 : 8;  // floats per point (coordinates, pad)
+  static constexpr int DP = PtLoad<DT>::DP;
+  static constexpr int PL = 256 * 4;  // floats per float4 plane of the stream (F32Geo::RMAX)
+  struct Raw {
+    double x[DT];
+  };
+  __device__ __forceinline__ static Raw load_raw(const double* src, int j)
+  {
+    Raw r;
+#pragma unroll
+    for (int d = 0; d < DT; ++d) r.x[d] = __ldg(src + (size_t)j * DP + d);
+    return r;
+  }
+  // coordinates centred on c (FP64), rounded to FP32
+  __device__ __forceinline__ static void centred(const Raw& p, const double* c, float (&v)[DF])
+  {
+#pragma unroll
+    for (int d = 0; d < DT; ++d) v[d] = (float)(p.x[d] - c[d]);
+#pragma unroll
+    for (int d = DT; d < DF; ++d) v[d] = 0.f;
+  }
+  // stream point j2 (plane k holds floats 4k..4k+3: LDS.128 per lane, conflict-free)
+  __device__ __forceinline__ static void store(const Raw& p, const double* c, float* dst, int j2)
+  {
+    float v[DF];
+    centred(p, c, v);
+#pragma unroll
+    for (int k = 0; k < DF / 4; ++k)
+      reinterpret_cast<float4*>(dst + k * PL)[j2] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  }
+  __device__ __forceinline__ static void load(const float* base, int j, float (&v)[DF])
+  {
+#pragma unroll
+    for (int k = 0; k < DF / 4; ++k) {
+      const float4 t = reinterpret_cast<const float4*>(base + k * PL)[j];
+      v[4 * k] = t.x;
+      v[4 * k + 1] = t.y;
+      v[4 * k + 2] = t.z;
+      v[4 * k + 3] = t.w;
+    }
+  }
+  // query tile (broadcast reads): point-major, stride DF
+  __device__ __forceinline__ static void stage_q(const double* src, int j, const double* c, float* dst)
+  {
+    float v[DF];
+    centred(load_raw(src, j), c, v);
+#pragma unroll
+    for (int k = 0; k < DF; ++k) dst[(size_t)j * DF + k] = v[k];
+  }
+};
+
+__device__ __forceinline__ float ex2_ftz(float t)
+{
+  float g;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(t));
+  return g;
+}
+
+// z = |q~ - r~|^2 in FP32, in the loop's order
+template <int DT>
+__device__ __forceinline__ float f32_z(const float* q, const float* r)
+{
+  const float a0 = q[0] - r[0];
+  float z = a0 * a0;
+#pragma unroll
+  for (int d = 1; d < DT; ++d) {
+    const float a = q[d] - r[d];
+    z = fmaf(a, a, z);
+  }
+  return z;
+}
+
+// One FP32 pair term exactly as the loop forms it (tests).
+template <int DT>
+__device__ __forceinline__ float f32_term(const float* q, const float* r)
+{
+  return ex2_ftz(-f32_z<DT>(q, r));
+}
+
+// GG queries (1..16) per lane against the tile's reference points (lanes over points);
+// the GG partial sums are combined across the warp by a transpose-reduction over the
+// next power of two P2 (padding sums are 0), in a fixed order.
+template <int DT, int GG>
+__device__ __forceinline__ void base_group_f32(const float* rs, int n, const float* qs, double* qsum,
+                                               int lane)
+{
+  constexpr int D = DT, DF = FPt<DT>::DF;
+  constexpr int P2 = GG <= 1 ? 1 : GG <= 2 ? 2 : GG <= 4 ? 4 : GG <= 8 ? 8 : 16;
+  constexpr int LG = P2 == 16 ? 4 : P2 == 8 ? 3 : P2 == 4 ? 2 : P2 == 2 ? 1 : 0;
+  float m[GG][D], acc[P2];
+#pragma unroll
+  for (int i = 0; i < GG; ++i)
+#pragma unroll
+    for (int d = 0; d < D; ++d) m[i][d] = qs[i * DF + d];
+#pragma unroll
+  for (int i = 0; i < P2; ++i) acc[i] = 0.f;
+  auto body = [&](int j) {
+    float r[DF];
+    FPt<DT>::load(rs, j, r);
+    float z[GG];
+#pragma unroll
+    for (int i = 0; i < GG; ++i) {
+      const float a = m[i][0] - r[0];
+      z[i] = a * a;
+    }
+#pragma unroll
+    for (int d = 1; d < D; ++d)
+#pragma unroll
+      for (int i = 0; i < GG; ++i) {
+        const float a = m[i][d] - r[d];
+        z[i] = fmaf(a, a, z[i]);
+      }
+#pragma unroll
+    for (int i = 0; i < GG; ++i) acc[i] += ex2_ftz(-z[i]);
+  };
+  const int nfull = n & ~31;
+  int j = lane;
+  for (; j < nfull; j += 32) body(j);
+  if (j < n) body(j);
+#pragma unroll
+  for (int s = 0; s < LG; ++s) {
+    const int off = 16 >> s;
+    const bool up = lane & off;
+    const int h = P2 >> (s + 1);
+#pragma unroll
+    for (int i = 0; i < P2 / 2; ++i) {
+      if (i < h) {
+        const float send = up ? acc[i] : acc[i + h];
+        const float keep = up ? acc[i + h] : acc[i];
+        acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16 >> LG; off >= 1; off >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
+  const int qi = lane >> (5 - LG);
+  if ((lane & ((32 >> LG) - 1)) == 0 && qi < GG) qsum[qi] += (double)acc[0];
+}
+
+template <int DT, int GG>
+__device__ __noinline__ void base_group_f32_call(const float* rs, int n, const float* qs, double* qsum,
+                                                 int lane)
+{
+  base_group_f32<DT, GG>(rs, n, qs, qsum, lane);
+}
+
+// Queries in groups of 8, the remainder (1..7) as ONE group of its exact size.
+template <int DT>
+__device__ __forceinline__ void base_groups_f32(const float* rs, int n, const float* qs, double* qsum,
+                                                int qc, int lane)
+{
+  constexpr int DF = FPt<DT>::DF;
+  int g0 = 0;
+  for (; g0 + 8 <= qc; g0 += 8) base_group_f32_call<DT, 8>(rs, n, qs + g0 * DF, qsum + g0, lane);
+  const float* q = qs + g0 * DF;
+  double* qq = qsum + g0;
+  switch (qc - g0) {
+  case 1: base_group_f32_call<DT, 1>(rs, n, q, qq, lane); break;
+  case 2: base_group_f32_call<DT, 2>(rs, n, q, qq, lane); break;
+  case 3: base_group_f32_call<DT, 3>(rs, n, q, qq, lane); break;
+  case 4: base_group_f32_call<DT, 4>(rs, n, q, qq, lane); break;
+  case 5: base_group_f32_call<DT, 5>(rs, n, q, qq, lane); break;
+  case 6: base_group_f32_call<DT, 6>(rs, n, q, qq, lane); break;
+  case 7: base_group_f32_call<DT, 7>(rs, n, q, qq, lane); break;
+  default: break;
+  }
+}
+
 // Queries in groups of G, the remainder in groups of 4, 2, 1.  Each group size is one
 // out-of-line copy, to keep the kernel's hot code small.
 template <int DT, int GG, bool FAST>
@@ -1068,12 +1280,98 @@ __device__ __forceinline__ void base_groups(const double* rs, int n, const doubl
 #ifndef DFGTB_BASE_MINB
 #define DFGTB_BASE_MINB 4  // CTAs per SM: 125 registers, chains interleaved by ptxas
 #endif
+// A base-case task as one warp sees it: lane k < nit holds item k's record; the
+// items' points form one stream (item k at stream positions [sk, sk + count)).
+struct TaskView {
+  int slot, leaf, nit, qc, qb, total, sk, okk;
+  int2 rc;
+};
+
+__device__ __forceinline__ TaskView task_view(const BTask& t, TreeView Q, int K, const int2* rec, int lane)
+{
+  TaskView v;
+  v.slot = t.key / K;
+  v.leaf = t.key - v.slot * K;
+  v.nit = t.item1 - t.item0;  // all records at once (kTaskItems <= 32)
+  v.rc = lane < v.nit ? rec[t.item0 + lane] : make_int2(0, 0);
+  v.qc = min(32, Q.count[v.leaf] - t.q0);
+  v.qb = Q.begin[v.leaf];
+  const int cnt = v.rc.y & 0x0FFFFFFF;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < kTaskItems; o <<= 1) {
+    const int x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  v.total = __shfl_sync(0xffffffffu, incl, kTaskItems - 1);
+  v.sk = incl - cnt;       // lane k < nit: stream start of item k
+  v.okk = v.rc.x - v.sk;   // its source position = okk + stream position
+  return v;
+}
+
+// Stage the stream of an item set (lane k < ni: item k starts at stream position skk,
+// source position = ok + stream position) in tiles of RMAX points and run `groups` on
+// each tile.  Owner item of position c0 + 32 i + lane: (items started at or before c0)
+// + (starts in word i at or below this lane's bit) + (starts in earlier words) - 1,
+// from a bit mask of the item starts.  Global loads of B positions per lane are issued
+// back to back before their shared-memory stores (one L2 round trip per B, not per
+// point).
+#ifndef DFGTB_STAGE_B
+#define DFGTB_STAGE_B 4  // measured: 8 spills and is 2% slower on cfg2
+#endif
+constexpr int stage_batch(int D)
+{
+  return (DFGTB_STAGE_B >> (D <= 2 ? 0 : D <= 4 ? 1 : 2)) > 0 ? (DFGTB_STAGE_B >> (D <= 2 ? 0 : D <= 4 ? 1 : 2)) : 1;
+}
+template <int RMAX, int B, class Load, class Store, class Groups>
+__device__ __forceinline__ void stream_passes(unsigned* smask, int ni, int skk, int ok, int tot, int lane,
+                                              Load load, Store store, Groups groups)
+{
+  for (int c0 = 0; c0 < tot; c0 += RMAX) {
+    const int n = min(RMAX, tot - c0);
+    if (lane < RMAX / 32) smask[lane] = 0u;
+    __syncwarp();
+    if (lane < ni && skk > c0 && skk < c0 + n) atomicOr(&smask[(skk - c0) >> 5], 1u << ((skk - c0) & 31));
+    int kb = __popc(__ballot_sync(0xffffffffu, lane < ni && skk <= c0)) - 1;
+    __syncwarp();
+    const unsigned le = 0xffffffffu >> (31 - lane);
+    for (int i0 = 0; 32 * i0 < n; i0 += B) {
+      decltype(load(0)) buf[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const int e = lane + 32 * (i0 + b);
+        const unsigned wm = smask[i0 + b];
+        const int off = __shfl_sync(0xffffffffu, ok, kb + __popc(wm & le));
+        kb += __popc(wm);
+        if (e < n) buf[b] = load(off + c0 + e);
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const int e = lane + 32 * (i0 + b);
+        if (e < n) store(buf[b], e);
+      }
+    }
+    __syncwarp();
+    groups(n);
+    __syncwarp();
+  }
+}
+
+// Tasks of one base-case kernel: indices into the task array, split by the path their
+// leaf pairs qualify for (k_task_split); results go to part[task * 32 + query].
+__device__ __forceinline__ int next_task(int* next, int lane)
+{
+  int w = 0;
+  if (lane == 0) w = atomicAdd(next, 1);
+  return __shfl_sync(0xffffffffu, w, 0);
+}
+
 template <int DT>
 __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
-  k_base_case(TreeView Q, int K, const BTask* tasks, const int* ntasks_p, int tcap, const int2* rec,
+  k_base_case(TreeView Q, int K, const BTask* tasks, const int* tlist, const int* ntl, const int2* rec,
               const double* xq, const double* xr, int nq, int nr, double* part, int* next, int mufu)
 {
-  const int ntasks = min(*ntasks_p, tcap);
+  const int nl = *ntl;
   using Geo = BaseGeo<DT>;
   constexpr int DP = Geo::DP, RMAX = Geo::RMAX;
   __shared__ __align__(512) double tab[64];
@@ -1086,75 +1384,40 @@ __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
   double* qs = rs + RMAX * Geo::DS;
   double* qsum = qs + 32 * Geo::DS;
   unsigned* smask = smask_all[threadIdx.x >> 5];
-  int w = 0;
-  if (lane == 0) w = atomicAdd(next, 1);
-  w = __shfl_sync(0xffffffffu, w, 0);
-  while (w < ntasks) {
+  for (int i = next_task(next, lane); i < nl;) {
+    const int w = tlist[i];
     const BTask t = tasks[w];
-    int wn = 0;
-    if (lane == 0) wn = atomicAdd(next, 1);  // the next task, fetched early
-    const int slot = t.key / K, leaf = t.key - slot * K;
-    // all records of the task at once: lane k holds item k (kTaskItems <= 32)
-    const int nit = t.item1 - t.item0;
-    const int2 rc = lane < nit ? rec[t.item0 + lane] : make_int2(0, 0);
-    const int qc = min(32, Q.count[leaf] - t.q0);
-    const int qb = Q.begin[leaf];
-    const int cnt = rc.y & 0x0FFFFFFF;
-    const bool fast = __all_sync(0xffffffffu, lane >= nit || (rc.y & (1 << 28)));
-    const bool clampok = __all_sync(0xffffffffu, lane >= nit || (rc.y & (3 << 28)));
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < kTaskItems; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, kTaskItems - 1);
-    const int sk = incl - cnt;   // lane k < nit: stream start of item k
-    const int okk = rc.x - sk;   // its source position = okk + stream position
-    const double* qsrc = xq + ((size_t)slot * nq + qb + t.q0) * DP;
-    const bool mf = (fast || clampok) && mufu;
+    const int inext = next_task(next, lane);  // the next task, fetched early
+    const TaskView v = task_view(t, Q, K, rec, lane);
+    const bool fast = __all_sync(0xffffffffu, lane >= v.nit || (v.rc.y & (1 << 28)));
+    const bool clampok = __all_sync(0xffffffffu, lane >= v.nit || (v.rc.y & (3 << 28)));
+    const bool mf = (fast || clampok) && (mufu & 1);
+    const double* qsrc = xq + ((size_t)v.slot * nq + v.qb + t.q0) * DP;
     double cq[DT];  // MUFU path: centre = the chunk's first query
 #pragma unroll
     for (int d = 0; d < DT; ++d) cq[d] = qsrc[d];
-    if (lane < qc) {
+    if (lane < v.qc) {
       if (mf) MPt<DT>::stage_q(qsrc, lane, cq, qs);
       else PtLoad<DT>::copy(qsrc, lane, qs);
     }
     qsum[lane] = 0.0;
-    const double* xrs = xr + (size_t)slot * nr * DP;
-    for (int c0 = 0; c0 < total; c0 += RMAX) {
-      // stage stream positions [c0, c0 + n).  Owner item of position c0 + 32 i + lane:
-      // (items started at or before c0) + (starts in word i at or below this lane's
-      // bit) + (starts in earlier words) - 1, from a bit mask of the item starts.
-      const int n = min(RMAX, total - c0);
-      if (lane < RMAX / 32) smask[lane] = 0u;
-      __syncwarp();
-      if (lane < nit && sk > c0 && sk < c0 + n) atomicOr(&smask[(sk - c0) >> 5], 1u << ((sk - c0) & 31));
-      int kb = __popc(__ballot_sync(0xffffffffu, lane < nit && sk <= c0)) - 1;
-      __syncwarp();
-      const unsigned le = 0xffffffffu >> (31 - lane);
-#pragma unroll
-      for (int i = 0; i < RMAX / 32; ++i) {
-        const int e = c0 + lane + 32 * i;
-        const unsigned wm = smask[i];
-        const int off = __shfl_sync(0xffffffffu, okk, kb + __popc(wm & le));
-        kb += __popc(wm);
-        if (e < c0 + n) {
-          if (mf) MPt<DT>::stage(xrs, off + e, cq, rs, e - c0);
-          else PtLoad<DT>::copy2(xrs, off + e, rs, e - c0);
-        }
-      }
-      __syncwarp();
-      if (mf && fast) base_groups_mufu<DT, false>(rs, n, qs, qsum, qc, lane);
-      else if (mf) base_groups_mufu<DT, true>(rs, n, qs, qsum, qc, lane);
-      else if (fast) base_groups<DT, true>(rs, n, qs, qsum, qc, tab, 1.0, lane);
-      else base_groups<DT, false>(rs, n, qs, qsum, qc, tab, mufu ? kLn2 : 1.0, lane);
-      __syncwarp();
-    }
+    const double* xrs = xr + (size_t)v.slot * nr * DP;
+    stream_passes<RMAX, stage_batch(DT)>(
+      smask, v.nit, v.sk, v.okk, v.total, lane, [&](int src) { return RawPt<DT>::load(xrs, src); },
+      [&](const RawPt<DT>& p, int pos) {
+        if (mf) MPt<DT>::stage(p, cq, rs, pos);
+        else p.store(rs, pos);
+      },
+      [&](int n) {
+        if (mf && fast) base_groups_mufu<DT, false>(rs, n, qs, qsum, v.qc, lane);
+        else if (mf) base_groups_mufu<DT, true>(rs, n, qs, qsum, v.qc, lane);
+        else if (fast) base_groups<DT, true>(rs, n, qs, qsum, v.qc, tab, 1.0, lane);
+        else base_groups<DT, false>(rs, n, qs, qsum, v.qc, tab, (mufu & 1) ? kLn2 : 1.0, lane);
+      });
     // Q = R: the run holding the query leaf itself contains every query's self pair,
     // whose MUFU value is 1 +- O(2^-20).  Replace it by exactly K(0) = 1 (the LOO CV
     // scores subtract exactly 1): recompute it with the loop's own operations and order.
-    if (mf && xq == xr && __any_sync(0xffffffffu, lane < nit && rc.x == qb) && lane < qc) {
+    if (mf && xq == xr && __any_sync(0xffffffffu, lane < v.nit && v.rc.x == v.qb) && lane < v.qc) {
       constexpr int DM = MPt<DT>::DM;
       unsigned fbits;
       asm volatile("mov.b32 %0, 0x4B000000;" : "=r"(fbits));
@@ -1165,10 +1428,101 @@ __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
       qsum[lane] += 1.0 - exp2_neg_fixed<false>(tq, fbits);
     }
     __syncwarp();
-    if (lane < qc) part[(size_t)w * 32 + lane] = qsum[lane];
+    if (lane < v.qc) part[(size_t)w * 32 + lane] = qsum[lane];
     __syncwarp();
-    w = __shfl_sync(0xffffffffu, wn, 0);
+    i = inext;
   }
+}
+
+// FP32 base case kernel (tasks whose every leaf pair carries order bit 2): small code
+// and few registers, so more warps per SM hide the staging loads.
+template <int DT>
+struct F32Geo {
+  static constexpr int RMAX = 256;  // stream tile (points)
+  static constexpr int WARPS = 4;
+  static constexpr int DF = FPt<DT>::DF;
+  static constexpr int FLOATS = RMAX * DF + 32 * DF;  // stream | query tile
+};
+#ifndef DFGTB_BF32_MINB
+#define DFGTB_BF32_MINB 6
+#endif
+template <int DT>
+__global__ void __launch_bounds__(F32Geo<DT>::WARPS * 32, DFGTB_BF32_MINB)
+  k_base_f32(TreeView Q, int K, const BTask* tasks, const int* tlist, const int* ntl, const int2* rec,
+             const double* xq, const double* xr, int nq, int nr, double* part, int* next)
+{
+  using Geo = F32Geo<DT>;
+  constexpr int DP = PtLoad<DT>::DP, RMAX = Geo::RMAX, DF = Geo::DF;
+  const int nl = *ntl;
+  extern __shared__ __align__(16) float fsm[];  // WARPS x FLOATS
+  __shared__ double qsum_all[Geo::WARPS][32];
+  __shared__ unsigned smask_all[Geo::WARPS][RMAX / 32];
+  const int lane = threadIdx.x & 31;
+  float* rs = fsm + (size_t)(threadIdx.x >> 5) * Geo::FLOATS;
+  float* qs = rs + RMAX * DF;
+  double* qsum = qsum_all[threadIdx.x >> 5];
+  unsigned* smask = smask_all[threadIdx.x >> 5];
+  for (int i = next_task(next, lane); i < nl;) {
+    const int w = tlist[i];
+    const BTask t = tasks[w];
+    const int inext = next_task(next, lane);
+    const TaskView v = task_view(t, Q, K, rec, lane);
+    const double* qsrc = xq + ((size_t)v.slot * nq + v.qb + t.q0) * DP;
+    double cq[DT];  // centre = the chunk's first query
+#pragma unroll
+    for (int d = 0; d < DT; ++d) cq[d] = qsrc[d];
+    if (lane < v.qc) FPt<DT>::stage_q(qsrc, lane, cq, qs);
+    qsum[lane] = 0.0;
+    const double* xrs = xr + (size_t)v.slot * nr * DP;
+    stream_passes<RMAX, stage_batch(DT)>(
+      smask, v.nit, v.sk, v.okk, v.total, lane, [&](int src) { return FPt<DT>::load_raw(xrs, src); },
+      [&](const typename FPt<DT>::Raw& p, int pos) { FPt<DT>::store(p, cq, rs, pos); },
+      [&](int n) { base_groups_f32<DT>(rs, n, qs, qsum, v.qc, lane); });
+    // Q = R: the self pair's value is ex2(-0) (q~ - q~ = 0); K(0) = 1 exactly in the sum
+    // as long as ex2.approx(-0) == 1 (checked by dfgtb_f32_exp_error's caller tests)
+    __syncwarp();
+    if (lane < v.qc) part[(size_t)w * 32 + lane] = qsum[lane];
+    __syncwarp();
+    i = inext;
+  }
+}
+
+// Split the task array by path: tasks whose every item carries order bit 2 (and the
+// engine runs the FP32 base case) -> list A, the rest -> list B.  cnt[0], cnt[1] count
+// them (zeroed by the caller).  The order inside a list is irrelevant: every task
+// writes its own partial sums.
+__global__ void k_task_split(const BTask* tasks, const int* ntasks_p, int tcap, const int2* rec, int f32,
+                             TreeView Q, int K, int* listA, int* listB, int* cnt, unsigned long long* pairs)
+{
+  const int n = min(*ntasks_p, tcap);
+  unsigned long long pa = 0, pb = 0;
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < n; w += gridDim.x * blockDim.x) {
+    const BTask t = tasks[w];
+    bool a = f32 != 0;
+    long long np = 0;
+    for (int k = t.item0; k < t.item1; ++k) {
+      const int y = rec[k].y;
+      a = a && ((y >> 30) & 1);
+      np += y & 0x0FFFFFFF;
+    }
+    np *= min(32, Q.count[t.key % K] - t.q0);
+    (a ? pa : pb) += (unsigned long long)np;
+    const unsigned m = __activemask();
+    const unsigned ma = __ballot_sync(m, a);
+    const int leader = __ffs(m) - 1, lane = threadIdx.x & 31;
+    int baseA = 0, baseB = 0;
+    if (lane == leader) {
+      if (ma) baseA = atomicAdd(cnt, __popc(ma));
+      if (m & ~ma) baseB = atomicAdd(cnt + 1, __popc(m & ~ma));
+    }
+    baseA = __shfl_sync(m, baseA, leader);
+    baseB = __shfl_sync(m, baseB, leader);
+    const unsigned below = (1u << lane) - 1u;
+    if (a) listA[baseA + __popc(ma & below)] = w;
+    else listB[baseB + __popc(m & ~ma & below)] = w;
+  }
+  if (pa) atomicAdd(pairs, pa);
+  if (pb) atomicAdd(pairs + 1, pb);
 }
 
 // Generic dimension (D > 5): scalar loads of the scaled coordinates, libdevice exp.
@@ -1646,29 +2000,50 @@ int base_rmax(int D)
 
 int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }
 
-// Persistent grid: as many CTAs as fit on the GPU (or fewer for small task lists).
+// Persistent grids: as many CTAs as fit on the GPU (or fewer for small task lists).
+// ws = [nextA, nextB, cntA, cntB, pairsA (u64), pairsB (u64), listA (tcap), listB (tcap)].  The task split, then the
+// FP32 kernel over list A, then the FP64 kernel over list B.
+template <class KF>
+int persistent_grid(KF kern, int threads, int smem, int slack, int tcap, int warps)
+{
+  int dev = 0, nsm = 0, per_sm = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  per_sm = std::max(per_sm, 1);
+  // leave `slack` CTA slots per SM to the kernels of the second stream
+  return (int)std::min<long long>((long long)nsm * std::max(1, per_sm - slack), (tcap + warps - 1) / warps);
+}
+
 template <int DT>
 void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int K, const BTask* tasks,
                    const int2* rec, const double* xq, const double* xr, int nq, int nr, double* part,
-                   int* next, int mufu, int slack)
+                   int* ws, int mufu, int slack)
 {
-  static int per_sm = 0, nsm = 0;
+  static int gridB = 0, gridA = 0;
   constexpr int threads = BaseGeo<DT>::WARPS * 32;
   constexpr int smem = BaseGeo<DT>::WARPS * BaseGeo<DT>::WORDS * (int)sizeof(double);
-  if (!per_sm) {
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaFuncSetAttribute(k_base_case<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_base_case<DT>, threads, smem));
-    per_sm = std::max(per_sm, 1);
+  constexpr int threadsA = F32Geo<DT>::WARPS * 32;
+  constexpr int smemA = F32Geo<DT>::WARPS * F32Geo<DT>::FLOATS * (int)sizeof(float);
+  if (!gridB) {
+    gridB = persistent_grid(k_base_case<DT>, threads, smem, slack, INT32_MAX / 2, BaseGeo<DT>::WARPS);
+    gridA = persistent_grid(k_base_f32<DT>, threadsA, smemA, slack, INT32_MAX / 2, F32Geo<DT>::WARPS);
   }
-  // leave `slack` CTA slots per SM to the kernels of the second stream
-  const int grid = (int)std::min<long long>((long long)nsm * std::max(1, per_sm - slack),
-                                            (tcap + BaseGeo<DT>::WARPS - 1) / BaseGeo<DT>::WARPS);
-  CK(cudaMemsetAsync(next, 0, sizeof(int), s));
-  k_base_case<DT><<<grid, threads, smem, s>>>(Q, K, tasks, ntasks, tcap, rec, xq, xr, nq, nr, part,
-                                              next, mufu);
+  const int cap_grid = (tcap + 3) / 4;
+  int* listA = ws + 8;
+  int* listB = ws + 8 + tcap;
+  CK(cudaMemsetAsync(ws, 0, 8 * sizeof(int), s));
+  k_task_split<<<148 * 4, 256, 0, s>>>(tasks, ntasks, tcap, rec, (mufu & 2) ? 1 : 0, Q, K, listA, listB, ws + 2,
+                                       reinterpret_cast<unsigned long long*>(ws + 4));
+  CK_LAUNCH();
+  if (mufu & 2) {
+    k_base_f32<DT><<<std::min(gridA, cap_grid), threadsA, smemA, s>>>(Q, K, tasks, listA, ws + 2, rec, xq, xr,
+                                                                     nq, nr, part, ws);
+    CK_LAUNCH();
+  }
+  k_base_case<DT><<<std::min(gridB, cap_grid), threads, smem, s>>>(Q, K, tasks, listB, ws + 3, rec, xq, xr,
+                                                                  nq, nr, part, ws + 1, mufu);
 }
 
 void launch_base(int D, cudaStream_t s, TreeView Q, TreeView R, int K, const BTask* tasks,
@@ -1977,10 +2352,10 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
     xr = xr_.p;
   }
   CK(cudaEventRecord(ev_[9], s));
-  bnext_.reserve(1);
+  bnext_.reserve(8 + 2 * (size_t)capTask_);
   launch_base(D_, s, Q, R, K, reinterpret_cast<const BTask*>(tasks_.p), bc_.p + 5, capTask_, sB_.p,
               reinterpret_cast<const int2*>(brec_.p), xq, xr, qt.n, rt_.n, bpart_.p, bnext_.p,
-              mufu_exp() ? 1 : 0, base_cta_slack_);
+              (mufu_ ? 1 : 0) | (f32_ ? 2 : 0), base_cta_slack_);
   CK(cudaEventRecord(ev_[10], s));
   // join, finalize
   CK(cudaStreamWaitEvent(s, join_, 0));
@@ -2093,6 +2468,48 @@ double mufu_exp_max_error()
   return v;
 }
 
+// Exhaustive relative error of ex2.approx.ftz.f32 over every FP32 argument in
+// [-126, 2^-10] (the FP32 base case's t = -z, rounding may push the self pair above 0)
+// against libdevice exp2 in FP64.  Max as ordered bits in *out.
+__global__ void k_f32_exp_check(unsigned long long* out)
+{
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (ex2_ftz(-0.0f) != 1.0f || ex2_ftz(0.0f) != 1.0f))
+    atomicMax(out, 0x7FF0000000000000ull);  // the exact self term relies on ex2(-0) == 1
+  const unsigned lo_pos = 0u, hi_pos = __float_as_uint(0x1p-10f);   // [+0, 2^-10]
+  const unsigned lo_neg = 0x80000001u, hi_neg = __float_as_uint(-126.0f);  // (-0, -126]
+  const unsigned long long npos = hi_pos - lo_pos + 1ull, nneg = hi_neg - lo_neg + 1ull;
+  unsigned long long worst = 0;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < npos + nneg;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned bits = i < npos ? lo_pos + (unsigned)i : lo_neg + (unsigned)(i - npos);
+    const float t = __uint_as_float(bits);
+    const double want = exp2((double)t);
+    const double rel = fabs((double)ex2_ftz(t) - want) / want;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(rel);
+    worst = b > worst ? b : worst;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, worst, o);
+    worst = v > worst ? v : worst;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, worst);
+}
+
+template <int DT>
+__global__ void k_f32_terms(const double* q, const double* r, const double* c, int n, double* out)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  constexpr int DF = FPt<DT>::DF;
+  double cc[DT];
+#pragma unroll
+  for (int d = 0; d < DT; ++d) cc[d] = c[d];
+  float vq[DF], vr[DF];
+  FPt<DT>::centred(FPt<DT>::load_raw(q, i), cc, vq);
+  FPt<DT>::centred(FPt<DT>::load_raw(r, i), cc, vr);
+  out[i] = (double)f32_term<DT>(vq, vr);
+}
+
 __global__ void k_ex2_peak(float* out, int iters)
 {
   float a[8];
@@ -2106,6 +2523,63 @@ __global__ void k_ex2_peak(float* out, int iters)
 #pragma unroll
   for (int k = 0; k < 8; ++k) s += a[k];
   if (s == 42.0f) out[0] = s;
+}
+
+void Engine::base_split(int& f32_tasks, int& fp64_tasks, unsigned long long& f32_pairs,
+                        unsigned long long& fp64_pairs)
+{
+  int v[6] = { 0, 0, 0, 0, 0, 0 };
+  if (bnext_.p) {
+    CK(cudaStreamSynchronize(s_));
+    CK(cudaMemcpy(v, bnext_.p + 2, sizeof(v), cudaMemcpyDeviceToHost));
+  }
+  f32_tasks = v[0];
+  fp64_tasks = v[1];
+  std::memcpy(&f32_pairs, v + 2, 8);
+  std::memcpy(&fp64_pairs, v + 4, 8);
+}
+
+double f32_exp_max_error()
+{
+  DevBuf<unsigned long long> o;
+  o.reserve(1);
+  CK(cudaMemset(o.p, 0, sizeof(unsigned long long)));
+  k_f32_exp_check<<<148 * 8, 256>>>(o.p);
+  CK_LAUNCH();
+  unsigned long long b = 0;
+  CK(cudaMemcpy(&b, o.p, sizeof(b), cudaMemcpyDeviceToHost));
+  double v;
+  std::memcpy(&v, &b, sizeof(v));
+  return v;
+}
+
+void f32_terms_host(int d, const double* q, const double* r, const double* c, size_t n, double* out)
+{
+  const int DP = padded_dim(d);
+  std::vector<double> hq(n * DP, 0.0), hr(n * DP, 0.0);
+  for (size_t i = 0; i < n; ++i)
+    for (int k = 0; k < d; ++k) {
+      hq[i * DP + k] = q[i * d + k];
+      hr[i * DP + k] = r[i * d + k];
+    }
+  DevBuf<double> dq, dr, dc, dout;
+  dq.reserve(n * DP);
+  dr.reserve(n * DP);
+  dc.reserve(d);
+  dout.reserve(n);
+  CK(cudaMemcpy(dq.p, hq.data(), sizeof(double) * n * DP, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dr.p, hr.data(), sizeof(double) * n * DP, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dc.p, c, sizeof(double) * d, cudaMemcpyHostToDevice));
+  const int g = (int)((n + 255) / 256);
+  switch (d) {
+  case 1: k_f32_terms<1><<<g, 256>>>(dq.p, dr.p, dc.p, (int)n, dout.p); break;
+  case 2: k_f32_terms<2><<<g, 256>>>(dq.p, dr.p, dc.p, (int)n, dout.p); break;
+  case 3: k_f32_terms<3><<<g, 256>>>(dq.p, dr.p, dc.p, (int)n, dout.p); break;
+  case 4: k_f32_terms<4><<<g, 256>>>(dq.p, dr.p, dc.p, (int)n, dout.p); break;
+  default: k_f32_terms<5><<<g, 256>>>(dq.p, dr.p, dc.p, (int)n, dout.p); break;
+  }
+  CK_LAUNCH();
+  CK(cudaMemcpy(out, dout.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
 }
 
 // Measured MUFU.EX2 throughput (ex2/s): the MUFU base case's roofline denominator.

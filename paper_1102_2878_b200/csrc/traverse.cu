@@ -154,6 +154,7 @@ struct TravArgs {
   TreeView Q, R;
   int D, pmax, cost, series, T;
   int selfq;  // Q = R: every query's sum is >= 1 (its own term)
+  int f32;    // the FP32 base case may be flagged (order bit 2)
   TravState* st;
   int *fq[2], *foff[2], *flen[2], *fr[2];
   int* pent[2];  // entry index of every frontier pair (pair-balanced persistent path)
@@ -243,6 +244,22 @@ __global__ void k_trav_init(const __grid_constant__ TravArgs a)
   }
 }
 
+// Base-case flags of a leaf pair (k_base_records, k_base_case).  Bit 0: every pair has
+// y = d^2/2h^2 <= 708 (K(d_max) >= e^-707.97): the fast exp needs no underflow handling.
+// Bit 1: terms below 2^-1021 may be dropped (absolute error <= |R| 2^-1021 against a sum
+// >= 1 (Q = R) or >= G^l >= 1e-290: below 1e-280 relative); the MUFU fixed point also
+// needs the query leaf's diameter <= 1000 in z units (sq sqrt(D) sqrt(log2 e) / (h sqrt 2),
+// sqrt(log2 e / 2) < 0.8494).  Bit 2: the FP32 base case applies: diameter <= kF32Diam
+// z units and sums >= 1 (Q = R) or >= G^l >= 1e-20 (its terms below 2^-126 flush to 0:
+// <= |R| 2^-126 / 1e-20 < 1e-11 relative).
+__device__ __forceinline__ int base_flags(const TravArgs& a, double kmin, double glo, double sq, double h,
+                                          int D)
+{
+  const double dz = sq * sqrt((double)D) * 0.8494;
+  return (kmin >= 3.4e-308 ? 1 : 0) | ((a.selfq || glo >= 1e-290) && dz <= 1000.0 * h ? 2 : 0) |
+         (a.f32 && (a.selfq || glo >= 1e-20) && dz <= kF32Diam * h ? 4 : 0);
+}
+
 // A group of W lanes, one frontier query node: kernel bounds of every live pair, the
 // lower bound G^l, and the prune / summarise / base / expand decision per pair.  The
 // whole warp calls it (valid = false: a group without an entry this round).
@@ -299,14 +316,7 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
       }
       if (kind == kX && qleaf && a.R.left[R] < 0) {
         kind = kB;
-        // bit 0: every pair of this leaf pair has y = d^2/2h^2 <= 708 (K(d_max) >= e^-707.97),
-        // the base case may use its fast exp without underflow handling; bit 1: terms
-        // below 2^-1021 may be dropped (absolute error <= |R| 2^-1021 against a
-        // sum >= 1 (Q = R) or >= G^l >= 1e-290: below 1e-280 relative); the MUFU fixed
-        // point also needs the query leaf's diameter <= 1000 in z units (sq sqrt(D)
-        // sqrt(log2 e) / (h sqrt 2), sqrt(log2 e / 2) < 0.8494)
-        order = (kmin >= 3.4e-308 ? 1 : 0) |
-                ((a.selfq || glo >= 1e-290) && sq * sqrt((double)D) * 0.8494 <= 1000.0 * h ? 2 : 0);
+        order = base_flags(a, kmin, glo, sq, h, D);
       }
       if (kind == kX) {
         slots += a.R.left[R] < 0 ? 1 : 2;
@@ -708,15 +718,7 @@ __device__ __forceinline__ void pairs_decide(const TravArgs& a, const TravState&
       }
       if (kind == kX && a.Q.left[Q] < 0 && a.R.left[R] < 0) {
         kind = kB;
-        // bit 0: every pair of this leaf pair has y = d^2/2h^2 <= 708 (K(d_max) >= e^-707.97),
-        // the base case may use its fast exp without underflow handling; bit 1: terms
-        // below 2^-1021 may be dropped (absolute error <= |R| 2^-1021 against a
-        // sum >= 1 (Q = R) or >= G^l >= 1e-290: below 1e-280 relative); the MUFU fixed
-        // point also needs the query leaf's diameter <= 1000 in z units (sq sqrt(D)
-        // sqrt(log2 e) / (h sqrt 2), sqrt(log2 e / 2) < 0.8494)
-        order = (kmin >= 3.4e-308 ? 1 : 0) |
-                ((a.selfq || uglo[u] >= 1e-290) &&
-                         a.Q.side[Q] * sqrt((double)D) * 0.8494 <= 1000.0 * s_h[slot] ? 2 : 0);
+        order = base_flags(a, kmin, uglo[u], a.Q.side[Q], s_h[slot], D);
       }
     }
     a.dec[j] = kind | (order << 8);
@@ -1247,6 +1249,7 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   a.Q = view_of(qt);
   a.R = view_of(rt_);
   a.selfq = &qt == &rt_ ? 1 : 0;
+  a.f32 = f32_ ? 1 : 0;
   a.D = D_;
   a.pmax = ser_.pmax;
   a.cost = cfg_.cost_model;
@@ -1301,7 +1304,7 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   CK(cudaMemsetAsync(L_.p, 0, sizeof(double) * KB * T, s));
   for (DevBuf<int>* b : { &Lord_, &cntF_, &cntDT_, &cntB_ })
     CK(cudaMemsetAsync(b->p, 0, sizeof(int) * KB, s));
-  hs->eps = mufu_ ? cfg_.epsilon - kMufuCharge : cfg_.epsilon;  // MUFU exp's error is charged
+  hs->eps = cfg_.epsilon - exp_charge();  // the base case's reduced-precision exp is charged
   hs->ntot = (double)n_;
   hs->nslots = nb;
   hs->K = K;

@@ -284,8 +284,10 @@ def test_base_exp_mode_selection(dfgtb, orc, monkeypatch):
     w = datagen.config(2, scale_n=0.04)
     h = w.h_s
     with dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(epsilon=0.01, leaf_threshold=32)) as e:
-        assert _capi.lib.dfgtb_base_exp_mode(e.handle) == 1
+        assert _capi.lib.dfgtb_base_exp_mode(e.handle) == 2  # FP32 leaf pairs, MUFU-FP64 rest
         fast = e.compute(None, h)
+    with dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(epsilon=1e-3, leaf_threshold=32)) as e:
+        assert _capi.lib.dfgtb_base_exp_mode(e.handle) == 1
     with dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(epsilon=1e-5, leaf_threshold=32)) as e:
         assert _capi.lib.dfgtb_base_exp_mode(e.handle) == 0
     monkeypatch.setenv("DFGTB_EXACT_EXP", "1")
@@ -299,7 +301,7 @@ def test_base_exp_mode_selection(dfgtb, orc, monkeypatch):
     tiny = 1e-3 * w.h_s
     monkeypatch.delenv("DFGTB_EXACT_EXP")
     with dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(epsilon=0.01, leaf_threshold=32)) as e:
-        assert _capi.lib.dfgtb_base_exp_mode(e.handle) == 1
+        assert _capi.lib.dfgtb_base_exp_mode(e.handle) == 2
         g = e.compute(None, tiny)
     ex = orc.naive_kde(w.refs, w.refs, tiny)
     assert np.all(g >= 1.0) and np.max(np.abs((g - 1.0) - (ex - 1.0))) <= 0.01 * np.max(ex)

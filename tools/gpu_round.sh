@@ -14,6 +14,6 @@ echo "bench exit $?"; tail -c 3000 gpurun_out/${TAG}_bench.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/${TAG}_launches.csv python tools/profile_step.py > gpurun_out/${TAG}_ncu_launch.log 2>&1
 echo "launch list exit $?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_base_case -s 1 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_base_(f32|case)" -s 2 -c 2 \
   -o gpurun_out/${TAG}_base_case -f python tools/profile_step.py > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "ncu full exit $?"
