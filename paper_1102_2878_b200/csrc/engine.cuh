@@ -55,13 +55,13 @@ constexpr int kMaxSlots = 64;  // bandwidths per batch
 constexpr double kMufuMinEps = 1e-4;
 constexpr double kMufuCharge = 4e-6;
 // FP32 base case (execute.cu FPt / base_group_f32): FP32 differences, distance and
-// partial sums, ex2.approx.f32 of the whole argument.  Applies to leaf pairs whose query leaf spans
-// <= kF32Diam in units where |q - r|^2 = z = log2 e |q - r|^2 / 2h^2 and whose sums are >= 1e-20 (or
+// partial sums, ex2.approx.f32 of the whole argument.  Applies to leaf pairs whose query leaf's
+// box diagonal is <= kF32Diam in units where |q - r|^2 = z = log2 e |q - r|^2 / 2h^2 and whose sums are >= 1e-20 (or
 // Q = R); per-term relative error < kF32Charge (derivation at FPt).  Used when
 // eps >= kF32MinEps (the charge is then <= 5% of the budget) unless DFGTB_NO_F32 is set.
 constexpr double kF32MinEps = 5e-3;
 constexpr double kF32Charge = 2e-4;
-constexpr double kF32Diam = 48.0;
+constexpr double kF32Diam = 150.0;
 
 int default_p_max(int D);
 
@@ -167,6 +167,8 @@ private:
   int nb_ = 1;
   bool mufu_ = false;
   bool f32_ = false;
+  const DevTree* last_q_ = nullptr;  // query tree and node count of the last batch (diagnostics)
+  int last_K_ = 0;
   // device-side counts of a batch (no host round trip until its end):
   // [0] nF [1] nDT [2] nB [3] traversal overflow [4] local chunks [5] base tasks
   DevBuf<int> bc_;

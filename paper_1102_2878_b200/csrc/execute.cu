@@ -617,7 +617,7 @@ __global__ void k_task_count(const int* leaves, int nleaves, int nb, int K, cons
 __global__ void k_task_fill(const int* leaves, int nleaves, int nb, int K, const int* cntB,
                             const int* offB, const Item* sB, const int* rcount, int rmax, TreeView Q,
                             const int* toff, BTask* tasks, int tcap, int* ntasks_out,
-                            int* leaf_task, int* leaf_runs)
+                            int* leaf_task, int* leaf_runs, int* tflag)
 {
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i == 0 && lane == 0) *ntasks_out = toff[nleaves * nb];
@@ -632,8 +632,13 @@ __global__ void k_task_fill(const int* leaves, int nleaves, int nb, int K, const
   int runs = 0;
   for (int k = o; k < e;) {
     const int j = warp_run_end(sB, k, e, rcount, rmax, lane);
+    // the FP32 kernel may take the run iff every item carries order bit 2
+    const bool f32 = __all_sync(0xffffffffu, k + lane >= j || (sB[k + lane].code & 4));
     for (int qi = lane; qi < nq; qi += 32)
-      if (t0 + qi * nruns + runs < tcap) tasks[t0 + qi * nruns + runs] = BTask{ key, k, j, 32 * qi };
+      if (t0 + qi * nruns + runs < tcap) {
+        tasks[t0 + qi * nruns + runs] = BTask{ key, k, j, 32 * qi };
+        tflag[t0 + qi * nruns + runs] = f32 ? 1 : 0;
+      }
     k = j;
     ++runs;
   }
@@ -1061,20 +1066,21 @@ __device__ __forceinline__ void base_groups_mufu(const double* rs, int n, const 
   if (qc - g0 >= 1) base_group_mufu_call<DT, 1, CLAMP>(rs, n, qs + g0 * DM, qsum + g0, lane);
 }
 
-// FP32 base case (leaf pairs the traversal flagged with order bit 2: the query leaf spans
-// <= kF32Diam in z units and the query sums are provably >= 1e-20 or Q = R).  Points are
-// centred on the chunk's first query in FP64 and rounded to FP32 (q~, r~), and per pair
+// FP32 base case (leaf pairs the traversal flagged with order bit 2: the query leaf's box
+// diagonal is <= kF32Diam = 150 in units where |q - r|^2 = z, and the query sums are
+// provably >= 1e-20 or Q = R).  Points are centred on the query leaf's box centre in FP64
+// (every query within 75 of it) and rounded to FP32 (q~, r~), and per pair
 //   z = sum_d (q~_d - r~_d)^2,   term = ex2.approx.ftz(-z),
 // D FP32 subtractions, D multiply-adds, one MUFU and one FP32 add: no FP64 instruction in
 // the pair loop.  Terms below 2^-126 flush to 0 (absolute error <= N 2^-126 against sums
 // >= 1e-20).  The self pair (Q = R) is exactly 1: q~ - q~ = 0.
-// Per-term relative error for z <= 127 (|q| <= 48 = kF32Diam, |r| <= 48 + sqrt z, unit
-// roundoff u = 2^-24):
-//   coordinate rounding   |d(q - r)| <= u (|q| + |r|)               -> 2 sqrt(z) u (96 + sqrt z)
+// Per-term relative error for z <= 127 (|q| <= 75, |r| <= 75 + sqrt z, unit roundoff
+// u = 2^-24):
+//   coordinate rounding   |d(q - r)| <= u (|q| + |r|)               -> 2 sqrt(z) u (150 + sqrt z)
 //   differences           |d a_d| <= u |a_d|                         -> 2 z u
 //   squares and sums      D roundings of partial sums <= 127         -> D 127 u
-//   -> |dz| <= 2 sqrt(127) (96 + 2 sqrt(127)) u + 5 127 u = 1.97e-4 at D = 5,
-//   |dz| ln 2 <= 1.37e-4 relative, + ex2.approx (< 2^-22, measured exhaustively by
+//   -> |dz| <= 2 sqrt(127) (150 + 2 sqrt(127)) u + 5 127 u = 2.70e-4 at D = 5,
+//   |dz| ln 2 <= 1.87e-4 relative, + ex2.approx (< 2^-22, measured exhaustively by
 //   dfgtb_f32_exp_error) + FP32 partial sums (<= 8 terms per lane + 5 reduction levels:
 //   12 u = 7.2e-7): below kF32Charge = 2e-4, which the traversal pays for.
 template <int DT>
@@ -1161,6 +1167,28 @@ __device__ __forceinline__ float f32_term(const float* q, const float* r)
 // GG queries (1..16) per lane against the tile's reference points (lanes over points);
 // the GG partial sums are combined across the warp by a transpose-reduction over the
 // next power of two P2 (padding sums are 0), in a fixed order.
+template <int P2, int LG>
+__device__ __forceinline__ float transpose_reduce(float (&acc)[P2], int lane)
+{
+#pragma unroll
+  for (int s = 0; s < LG; ++s) {
+    const int off = 16 >> s;
+    const bool up = lane & off;
+    const int h = P2 >> (s + 1);
+#pragma unroll
+    for (int i = 0; i < P2 / 2; ++i) {
+      if (i < h) {
+        const float send = up ? acc[i] : acc[i + h];
+        const float keep = up ? acc[i + h] : acc[i];
+        acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16 >> LG; off >= 1; off >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
+  return acc[0];
+}
+
 template <int DT, int GG>
 __device__ __forceinline__ void base_group_f32(const float* rs, int n, const float* qs, double* qsum,
                                                int lane)
@@ -1198,24 +1226,9 @@ __device__ __forceinline__ void base_group_f32(const float* rs, int n, const flo
   int j = lane;
   for (; j < nfull; j += 32) body(j);
   if (j < n) body(j);
-#pragma unroll
-  for (int s = 0; s < LG; ++s) {
-    const int off = 16 >> s;
-    const bool up = lane & off;
-    const int h = P2 >> (s + 1);
-#pragma unroll
-    for (int i = 0; i < P2 / 2; ++i) {
-      if (i < h) {
-        const float send = up ? acc[i] : acc[i + h];
-        const float keep = up ? acc[i + h] : acc[i];
-        acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-      }
-    }
-  }
-#pragma unroll
-  for (int off = 16 >> LG; off >= 1; off >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
+  const double v = (double)transpose_reduce<P2, LG>(acc, lane);
   const int qi = lane >> (5 - LG);
-  if ((lane & ((32 >> LG) - 1)) == 0 && qi < GG) qsum[qi] += (double)acc[0];
+  if ((lane & ((32 >> LG) - 1)) == 0 && qi < GG) qsum[qi] += v;
 }
 
 template <int DT, int GG>
@@ -1310,12 +1323,12 @@ __device__ __forceinline__ TaskView task_view(const BTask& t, TreeView Q, int K,
 }
 
 // Stage the stream of an item set (lane k < ni: item k starts at stream position skk,
-// source position = ok + stream position) in tiles of RMAX points and run `groups` on
-// each tile.  Owner item of position c0 + 32 i + lane: (items started at or before c0)
-// + (starts in word i at or below this lane's bit) + (starts in earlier words) - 1,
-// from a bit mask of the item starts.  Global loads of B positions per lane are issued
-// back to back before their shared-memory stores (one L2 round trip per B, not per
-// point).
+// source position = ok + stream position) in tiles of RMAX positions and run `groups` on
+// each tile.  Owner item of position c0 + 32 i + lane: (items started at
+// or before c0) + (starts in word i at or below this lane's bit) + (starts in earlier
+// words) - 1, from a bit mask of the item starts.  Global loads of B positions per lane
+// are issued back to back before their shared-memory stores (one L2 round trip per B,
+// not per point).
 #ifndef DFGTB_STAGE_B
 #define DFGTB_STAGE_B 4  // measured: 8 spills and is 2% slower on cfg2
 #endif
@@ -1369,7 +1382,8 @@ __device__ __forceinline__ int next_task(int* next, int lane)
 template <int DT>
 __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
   k_base_case(TreeView Q, int K, const BTask* tasks, const int* tlist, const int* ntl, const int2* rec,
-              const double* xq, const double* xr, int nq, int nr, double* part, int* next, int mufu)
+              const double* xq, const double* xr, int nq, int nr, double* part, int* next, int mufu,
+              const double* c0, SlotView sv, double f)
 {
   const int nl = *ntl;
   using Geo = BaseGeo<DT>;
@@ -1449,7 +1463,8 @@ struct F32Geo {
 template <int DT>
 __global__ void __launch_bounds__(F32Geo<DT>::WARPS * 32, DFGTB_BF32_MINB)
   k_base_f32(TreeView Q, int K, const BTask* tasks, const int* tlist, const int* ntl, const int2* rec,
-             const double* xq, const double* xr, int nq, int nr, double* part, int* next)
+             const double* xq, const double* xr, int nq, int nr, double* part, int* next, const double* c0,
+             SlotView sv, double f)
 {
   using Geo = F32Geo<DT>;
   constexpr int DP = PtLoad<DT>::DP, RMAX = Geo::RMAX, DF = Geo::DF;
@@ -1468,9 +1483,10 @@ __global__ void __launch_bounds__(F32Geo<DT>::WARPS * 32, DFGTB_BF32_MINB)
     const int inext = next_task(next, lane);
     const TaskView v = task_view(t, Q, K, rec, lane);
     const double* qsrc = xq + ((size_t)v.slot * nq + v.qb + t.q0) * DP;
-    double cq[DT];  // centre = the chunk's first query
+    double cq[DT];  // centre = the query leaf's box centre, scaled like the points
+    const double sc = sv.s[v.slot] * f;
 #pragma unroll
-    for (int d = 0; d < DT; ++d) cq[d] = qsrc[d];
+    for (int d = 0; d < DT; ++d) cq[d] = (Q.cen[(size_t)v.leaf * DT + d] - c0[d]) * sc;
     if (lane < v.qc) FPt<DT>::stage_q(qsrc, lane, cq, qs);
     qsum[lane] = 0.0;
     const double* xrs = xr + (size_t)v.slot * nr * DP;
@@ -1478,8 +1494,6 @@ __global__ void __launch_bounds__(F32Geo<DT>::WARPS * 32, DFGTB_BF32_MINB)
       smask, v.nit, v.sk, v.okk, v.total, lane, [&](int src) { return FPt<DT>::load_raw(xrs, src); },
       [&](const typename FPt<DT>::Raw& p, int pos) { FPt<DT>::store(p, cq, rs, pos); },
       [&](int n) { base_groups_f32<DT>(rs, n, qs, qsum, v.qc, lane); });
-    // Q = R: the self pair's value is ex2(-0) (q~ - q~ = 0); K(0) = 1 exactly in the sum
-    // as long as ex2.approx(-0) == 1 (checked by dfgtb_f32_exp_error's caller tests)
     __syncwarp();
     if (lane < v.qc) part[(size_t)w * 32 + lane] = qsum[lane];
     __syncwarp();
@@ -1491,38 +1505,44 @@ __global__ void __launch_bounds__(F32Geo<DT>::WARPS * 32, DFGTB_BF32_MINB)
 // engine runs the FP32 base case) -> list A, the rest -> list B.  cnt[0], cnt[1] count
 // them (zeroed by the caller).  The order inside a list is irrelevant: every task
 // writes its own partial sums.
-__global__ void k_task_split(const BTask* tasks, const int* ntasks_p, int tcap, const int2* rec, int f32,
-                             TreeView Q, int K, int* listA, int* listB, int* cnt, unsigned long long* pairs)
+__global__ void k_task_split(const int* ntasks_p, int tcap, const int* tflag, int f32, int* listA, int* listB,
+                             int* cnt)
 {
   const int n = min(*ntasks_p, tcap);
-  unsigned long long pa = 0, pb = 0;
-  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < n; w += gridDim.x * blockDim.x) {
-    const BTask t = tasks[w];
-    bool a = f32 != 0;
-    long long np = 0;
-    for (int k = t.item0; k < t.item1; ++k) {
-      const int y = rec[k].y;
-      a = a && ((y >> 30) & 1);
-      np += y & 0x0FFFFFFF;
-    }
-    np *= min(32, Q.count[t.key % K] - t.q0);
-    (a ? pa : pb) += (unsigned long long)np;
-    const unsigned m = __activemask();
-    const unsigned ma = __ballot_sync(m, a);
-    const int leader = __ffs(m) - 1, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
+  const int nb = (n + 31) & ~31;  // whole warps in the loop (ballots)
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nb; w += gridDim.x * blockDim.x) {
+    const bool in = w < n;
+    const bool a = in && f32 && tflag[w];
+    const unsigned ma = __ballot_sync(0xffffffffu, a), mb = __ballot_sync(0xffffffffu, in && !a);
     int baseA = 0, baseB = 0;
-    if (lane == leader) {
+    if (lane == 0) {
       if (ma) baseA = atomicAdd(cnt, __popc(ma));
-      if (m & ~ma) baseB = atomicAdd(cnt + 1, __popc(m & ~ma));
+      if (mb) baseB = atomicAdd(cnt + 1, __popc(mb));
     }
-    baseA = __shfl_sync(m, baseA, leader);
-    baseB = __shfl_sync(m, baseB, leader);
+    baseA = __shfl_sync(0xffffffffu, baseA, 0);
+    baseB = __shfl_sync(0xffffffffu, baseB, 0);
     const unsigned below = (1u << lane) - 1u;
     if (a) listA[baseA + __popc(ma & below)] = w;
-    else listB[baseB + __popc(m & ~ma & below)] = w;
+    else if (in) listB[baseB + __popc(mb & below)] = w;
   }
-  if (pa) atomicAdd(pairs, pa);
-  if (pb) atomicAdd(pairs + 1, pb);
+}
+
+// (q, r) pairs of the tasks in a list (diagnostics: Engine::base_split)
+__global__ void k_task_pairs(const BTask* tasks, const int* list, const int* nl, const int2* rec, TreeView Q,
+                             int K, unsigned long long* out)
+{
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  unsigned long long acc = 0;
+  for (int i = w0; i < *nl; i += nw) {
+    const BTask t = tasks[list[i]];
+    const int k = t.item0 + lane;
+    const unsigned c = k < t.item1 ? (unsigned)(rec[k].y & 0x0FFFFFFF) : 0u;
+    const unsigned tot = __reduce_add_sync(0xffffffffu, c);
+    acc += (unsigned long long)tot * (unsigned long long)min(32, Q.count[t.key % K] - t.q0);
+  }
+  if (lane == 0 && acc) atomicAdd(out, acc);
 }
 
 // Generic dimension (D > 5): scalar loads of the scaled coordinates, libdevice exp.
@@ -1985,9 +2005,13 @@ __global__ void k_dfma_peak(double* out, int iters)
   if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == 42.0) out[0] = 1.0;
 }
 
-// Points per task run: the base case's stream tile (k_base_case_any streams directly).
+// Points per task run: the base case's stream tile (k_base_case_any streams directly),
+// or DFGTB_RUN_POINTS.
 int base_rmax(int D)
 {
+#ifdef DFGTB_RUN_POINTS
+  if (D <= 5) return DFGTB_RUN_POINTS;
+#endif
   switch (D) {
   case 1: return BaseGeo<1>::RMAX;
   case 2: return BaseGeo<2>::RMAX;
@@ -2001,7 +2025,8 @@ int base_rmax(int D)
 int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }
 
 // Persistent grids: as many CTAs as fit on the GPU (or fewer for small task lists).
-// ws = [nextA, nextB, cntA, cntB, pairsA (u64), pairsB (u64), listA (tcap), listB (tcap)].  The task split, then the
+// ws = [nextA, nextB, cntA, cntB, pairsA (u64), pairsB (u64), listA (tcap), listB (tcap),
+// task flags (tcap, written by k_task_fill)].  The task split, then the
 // FP32 kernel over list A, then the FP64 kernel over list B.
 template <class KF>
 int persistent_grid(KF kern, int threads, int smem, int slack, int tcap, int warps)
@@ -2019,7 +2044,7 @@ int persistent_grid(KF kern, int threads, int smem, int slack, int tcap, int war
 template <int DT>
 void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int K, const BTask* tasks,
                    const int2* rec, const double* xq, const double* xr, int nq, int nr, double* part,
-                   int* ws, int mufu, int slack)
+                   int* ws, int mufu, int slack, const double* c0, SlotView sv, double f)
 {
   static int gridB = 0, gridA = 0;
   constexpr int threads = BaseGeo<DT>::WARPS * 32;
@@ -2034,24 +2059,25 @@ void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int 
   int* listA = ws + 8;
   int* listB = ws + 8 + tcap;
   CK(cudaMemsetAsync(ws, 0, 8 * sizeof(int), s));
-  k_task_split<<<148 * 4, 256, 0, s>>>(tasks, ntasks, tcap, rec, (mufu & 2) ? 1 : 0, Q, K, listA, listB, ws + 2,
-                                       reinterpret_cast<unsigned long long*>(ws + 4));
+  k_task_split<<<148 * 4, 256, 0, s>>>(ntasks, tcap, ws + 8 + 2 * (size_t)tcap, (mufu & 2) ? 1 : 0, listA, listB,
+                                       ws + 2);
   CK_LAUNCH();
   if (mufu & 2) {
     k_base_f32<DT><<<std::min(gridA, cap_grid), threadsA, smemA, s>>>(Q, K, tasks, listA, ws + 2, rec, xq, xr,
-                                                                     nq, nr, part, ws);
+                                                                     nq, nr, part, ws, c0, sv, f);
     CK_LAUNCH();
   }
   k_base_case<DT><<<std::min(gridB, cap_grid), threads, smem, s>>>(Q, K, tasks, listB, ws + 3, rec, xq, xr,
-                                                                  nq, nr, part, ws + 1, mufu);
+                                                                  nq, nr, part, ws + 1, mufu, c0, sv, f);
 }
 
 void launch_base(int D, cudaStream_t s, TreeView Q, TreeView R, int K, const BTask* tasks,
                  const int* ntasks, int tcap, const Item* items, const int2* rec, const double* xq,
-                 const double* xr, int nq, int nr, double* part, int* next, int mufu, int slack)
+                 const double* xr, int nq, int nr, double* part, int* next, int mufu, int slack,
+                 const double* c0, SlotView sv, double f)
 {
 #define BASE(DD)                                                                                 \
-  launch_base_t<DD>(ntasks, tcap, s, Q, K, tasks, rec, xq, xr, nq, nr, part, next, mufu, slack)
+  launch_base_t<DD>(ntasks, tcap, s, Q, K, tasks, rec, xq, xr, nq, nr, part, next, mufu, slack, c0, sv, f)
   switch (D) {
   case 1: BASE(1); break;
   case 2: BASE(2); break;
@@ -2186,6 +2212,8 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
 
 void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d_out)
 {
+  last_q_ = &qt;
+  last_K_ = qt.nodes;
   cudaStream_t s = s_;
   const DevSeries g = dev_series();
   const TreeView Q = view_of(qt), R = view_of(rt_);
@@ -2327,10 +2355,12 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
   }
   capTask_ = std::max(capTask_, std::max(4096, capB_ / 8));
   tasks_.reserve((size_t)capTask_ * 4);
+  bnext_.reserve(8 + 3 * (size_t)capTask_);  // base-case lists and task flags (launch_base_t)
   k_task_fill<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p, sB_.p,
                                                  R.count, rmax, Q, toff_.p,
                                                  reinterpret_cast<BTask*>(tasks_.p), capTask_,
-                                                 bc_.p + 5, leaf_task_.p, leaf_runs_.p);
+                                                 bc_.p + 5, leaf_task_.p, leaf_runs_.p,
+                                                 bnext_.p + 8 + 2 * (size_t)capTask_);
   CK_LAUNCH();
   bpart_.reserve((size_t)capTask_ * 32);
   brec_.reserve((size_t)capB_ * 2 + 2);
@@ -2352,10 +2382,10 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
     xr = xr_.p;
   }
   CK(cudaEventRecord(ev_[9], s));
-  bnext_.reserve(8 + 2 * (size_t)capTask_);
   launch_base(D_, s, Q, R, K, reinterpret_cast<const BTask*>(tasks_.p), bc_.p + 5, capTask_, sB_.p,
               reinterpret_cast<const int2*>(brec_.p), xq, xr, qt.n, rt_.n, bpart_.p, bnext_.p,
-              (mufu_ ? 1 : 0) | (f32_ ? 2 : 0), base_cta_slack_);
+              (mufu_ ? 1 : 0) | (f32_ ? 2 : 0), base_cta_slack_, rt_.centroid.p, sv,
+              mufu_ ? kSqrtLog2e : 1.0);
   CK(cudaEventRecord(ev_[10], s));
   // join, finalize
   CK(cudaStreamWaitEvent(s, join_, 0));
@@ -2529,7 +2559,15 @@ void Engine::base_split(int& f32_tasks, int& fp64_tasks, unsigned long long& f32
                         unsigned long long& fp64_pairs)
 {
   int v[6] = { 0, 0, 0, 0, 0, 0 };
-  if (bnext_.p) {
+  if (bnext_.p && tasks_.p && brec_.p) {
+    CK(cudaMemsetAsync(bnext_.p + 4, 0, 4 * sizeof(int), s_));
+    const TreeView Q = view_of(last_q_ ? *last_q_ : rt_);
+    auto* pr = reinterpret_cast<unsigned long long*>(bnext_.p + 4);
+    const BTask* tk = reinterpret_cast<const BTask*>(tasks_.p);
+    const int2* rc = reinterpret_cast<const int2*>(brec_.p);
+    k_task_pairs<<<148 * 4, 256, 0, s_>>>(tk, bnext_.p + 8, bnext_.p + 2, rc, Q, last_K_, pr);
+    k_task_pairs<<<148 * 4, 256, 0, s_>>>(tk, bnext_.p + 8 + capTask_, bnext_.p + 3, rc, Q, last_K_, pr + 1);
+    CK_LAUNCH();
     CK(cudaStreamSynchronize(s_));
     CK(cudaMemcpy(v, bnext_.p + 2, sizeof(v), cudaMemcpyDeviceToHost));
   }

@@ -250,14 +250,21 @@ __global__ void k_trav_init(const __grid_constant__ TravArgs a)
 // >= 1 (Q = R) or >= G^l >= 1e-290: below 1e-280 relative); the MUFU fixed point also
 // needs the query leaf's diameter <= 1000 in z units (sq sqrt(D) sqrt(log2 e) / (h sqrt 2),
 // sqrt(log2 e / 2) < 0.8494).  Bit 2: the FP32 base case applies: diameter <= kF32Diam
-// z units and sums >= 1 (Q = R) or >= G^l >= 1e-20 (its terms below 2^-126 flush to 0:
-// <= |R| 2^-126 / 1e-20 < 1e-11 relative).
+// (every query within kF32Diam / 2 of the leaf's box centre), and for Q != R sums >=
+// G^l >= 1e-20 (its terms below 2^-126 flush to 0: <= |R| 2^-126 / 1e-20 < 1e-11
+// relative); for Q = R a provable leave-one-out floor G - 1 >= 2^-10 (from G^l, or from
+// a neighbour in the query leaf itself): the terms below 2^-126 that flush and the
+// <= 12 u G rounding of FP32 partial sums that hold the self term 1 stay below 1e-3
+// relative to the G - 1 the CV scores take logarithms of.
 __device__ __forceinline__ int base_flags(const TravArgs& a, double kmin, double glo, double sq, double h,
-                                          int D)
+                                          int D, int nq)
 {
   const double dz = sq * sqrt((double)D) * 0.8494;
+  // Q = R leave-one-out floor: a query leaf of >= 2 points whose diagonal is <= 3.16
+  // z-units gives every query a neighbour with K >= 2^-10, so G - 1 >= 2^-10 as well
+  const bool loo = glo >= 1.0 + 0x1p-10 || (nq >= 2 && dz <= 3.16 * h);
   return (kmin >= 3.4e-308 ? 1 : 0) | ((a.selfq || glo >= 1e-290) && dz <= 1000.0 * h ? 2 : 0) |
-         (a.f32 && (a.selfq || glo >= 1e-20) && dz <= kF32Diam * h ? 4 : 0);
+         (a.f32 && (a.selfq ? loo : glo >= 1e-20) && dz <= kF32Diam * h ? 4 : 0);
 }
 
 // A group of W lanes, one frontier query node: kernel bounds of every live pair, the
@@ -316,7 +323,7 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
       }
       if (kind == kX && qleaf && a.R.left[R] < 0) {
         kind = kB;
-        order = base_flags(a, kmin, glo, sq, h, D);
+        order = base_flags(a, kmin, glo, sq, h, D, a.Q.count[Q]);
       }
       if (kind == kX) {
         slots += a.R.left[R] < 0 ? 1 : 2;
@@ -718,7 +725,7 @@ __device__ __forceinline__ void pairs_decide(const TravArgs& a, const TravState&
       }
       if (kind == kX && a.Q.left[Q] < 0 && a.R.left[R] < 0) {
         kind = kB;
-        order = base_flags(a, kmin, uglo[u], a.Q.side[Q], s_h[slot], D);
+        order = base_flags(a, kmin, uglo[u], a.Q.side[Q], s_h[slot], D, a.Q.count[Q]);
       }
     }
     a.dec[j] = kind | (order << 8);

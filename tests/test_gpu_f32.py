@@ -31,14 +31,14 @@ def test_f32_exp_error_exhaustive():
     err = _capi.lib.dfgtb_f32_exp_error()
     assert 0.0 <= err < 2.0 ** -21
     # the charge covers the exp, the distance bound at D = 5 and the partial sums
-    dz = 2 * np.sqrt(127.0) * (96 + 2 * np.sqrt(127.0)) * U + 5 * 127 * U
+    dz = 2 * np.sqrt(127.0) * (150 + 2 * np.sqrt(127.0)) * U + 5 * 127 * U
     assert err + dz * np.log(2.0) + 12 * U < F32_CHARGE
 
 
 @pytest.mark.parametrize("d", [1, 2, 3, 4, 5])
 def test_f32_terms_within_charge(d):
-    """Pairs at the extremes the traversal allows: queries up to 48 units from the
-    centre (the query leaf's diameter bound), references at any distance with z <= 125
+    """Pairs at the extremes the traversal allows: queries up to 75 units from the
+    centre (half the query leaf's diagonal bound), references at any distance with z <= 125
     (terms >= 2^-125, no flush), the reference on the far side of the centre (largest
     |r|), large centre offsets; against 2^-z in FP64."""
     g = np.random.default_rng(100 + d)
@@ -46,7 +46,7 @@ def test_f32_terms_within_charge(d):
     c = g.uniform(-300.0, 300.0, d)
     u = g.standard_normal((n, d))
     u /= np.linalg.norm(u, axis=1, keepdims=True)
-    rad = np.where(g.random(n) < 0.5, 48.0, 48.0 * g.random(n) ** (1.0 / d))
+    rad = np.where(g.random(n) < 0.5, 75.0, 75.0 * g.random(n) ** (1.0 / d))
     q = c + u * rad[:, None]
     v = g.standard_normal((n, d))
     v /= np.linalg.norm(v, axis=1, keepdims=True)
@@ -68,7 +68,7 @@ def test_f32_far_terms_flush_to_zero():
     g = np.random.default_rng(7)
     d, n = 3, 10000
     c = np.zeros(d)
-    q = g.uniform(-27.0, 27.0, (n, d))
+    q = g.uniform(-43.0, 43.0, (n, d))
     v = g.standard_normal((n, d))
     v /= np.linalg.norm(v, axis=1, keepdims=True)
     z = 127.0 + g.exponential(2000.0, n)
