@@ -344,7 +344,8 @@ __global__ void k_to_preorder(int K, int D, const int* bfs2pre, const double* bl
                               const int* bright, const int* bbeg, const int* bcnt,
                               const int* bpar, const int* bdep, double* lo, double* hi,
                               double* cen, double* side, double* sc, int* sd, int* left,
-                              int* right, int* beg, int* cnt, int* par, int* dep, int* by_depth)
+                              int* right, int* beg, int* cnt, int* par, int* dep, int* by_depth,
+                              const int* rank)
 {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= K) return;
@@ -363,7 +364,7 @@ __global__ void k_to_preorder(int K, int D, const int* bfs2pre, const double* bl
   cnt[p] = bcnt[i];
   par[p] = bpar[i] < 0 ? -1 : bfs2pre[bpar[i]];
   dep[p] = bdep[i];
-  by_depth[i] = p;
+  by_depth[rank ? rank[i] : i] = p;
 }
 
 // Ancestor chain of every node (root first), for nodes with depth < kMaxAnc: kernels
@@ -423,12 +424,284 @@ struct BuildArgs {
   int* ctot;                        // 2 * gridDim.x chunk totals
   int* lvl;                         // [0] = levels, [1..] = level base offsets
   unsigned long long* trace;        // DFGTB_TRACE: per level 8 %globaltimer stamps of CTA 0
+  int* lvlmax;                      // per level: largest count of a splitting node
+  int* kcount;                      // node count (ids handed out by the local phase)
+  int local_S;                      // subtree size of the CTA-local phase (0: off)
 };
 
 __device__ __forceinline__ void chunk_of(int total, int b, int G, int& lo, int& hi)
 {
   lo = (int)((long long)total * b / G);
   hi = (int)((long long)total * (b + 1) / G);
+}
+
+// ---- CTA-local subtrees ---------------------------------------------------------
+// Once every splitting node of a level holds <= local_S points, each CTA builds whole
+// subtrees (the level's nodes b, b + G, ..) in shared memory: the same bounds / split
+// rule / partition pairing / nth_element fallback as the global phases, one local level
+// per step with __syncthreads only.  Node ids of the new nodes come from an atomic
+// counter (any labelling with children after parents works: the host renumbers to
+// preorder and ranks nodes by depth).
+constexpr int kLS = 4096;  // positions per subtree (shared memory)
+constexpr int kLN = 256;   // nodes per local level
+constexpr int kLMaxD = 8;  // dimensions the local phase supports
+int local_smem_bytes(int D)
+{
+  return 5 * kLS * 4 + 4                          // sp, seg, flag, P (+1), slot
+         + 2 * kLN * (6 * 4 + 8) + kLN * 2 * 4     // two node buffers, lc, rank
+         + 2 * 2 * kLN * D * 8;                    // child key min / max
+}
+
+template <class TS>
+__device__ void local_subtrees(const BuildArgs& a, TS& tmp, unsigned char* lsm, int base, int m, int level,
+                               const int* dsp, const double* mdp)
+{
+  using BS = cub::BlockScan<int, kPB>;
+  const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, D = a.D;
+  int* sp = reinterpret_cast<int*>(lsm);
+  int* sseg = sp + kLS;
+  int* sflag = sseg + kLS;
+  int* sP = sflag + kLS;  // kLS + 1
+  int* sslot = sP + kLS + 1;
+  int* nb0 = sslot + kLS;  // node buffers: id, bg, cn, ds, w (5 x kLN ints) each
+  int* nb1 = nb0 + 5 * kLN;
+  int* nlc = nb1 + 5 * kLN;
+  int* nrk = nlc + kLN;
+  double* nmid0 = reinterpret_cast<double*>(reinterpret_cast<uintptr_t>(nrk + kLN + 1) & ~(uintptr_t)7);
+  double* nmid1 = nmid0 + kLN;
+  unsigned long long* kmn = reinterpret_cast<unsigned long long*>(nmid1 + kLN);
+  unsigned long long* kmx = kmn + 2 * kLN * D;
+  __shared__ int s_ns, s_cbase;
+  for (int j = blockIdx.x; j < m; j += G) {
+    const int id0 = base + j, b0 = a.nbeg[id0], c = a.ncnt[id0];
+    for (int k = tid; k < c; k += kPB) {
+      sp[k] = a.perm[b0 + k];
+      sseg[k] = 0;
+    }
+    int* cur = nb0;
+    int* nxt = nb1;
+    double* cmid = nmid0;
+    double* xmid = nmid1;
+    if (tid == 0) {
+      cur[0] = id0;
+      cur[kLN] = 0;
+      cur[2 * kLN] = c;
+      cur[3 * kLN] = dsp[j];
+      cur[4 * kLN] = a.bsd[id0];
+      cmid[0] = mdp[j];
+    }
+    int ncur = 1, lev = level;
+    __syncthreads();
+    while (ncur > 0) {
+      const int* nid = cur;
+      const int* nbg = cur + kLN;
+      const int* ncn = cur + 2 * kLN;
+      const int* nds = cur + 3 * kLN;
+      const int* nw = cur + 4 * kLN;
+      for (int i = tid; i < 2 * ncur * D; i += kPB) {
+        kmn[i] = ~0ull;
+        kmx[i] = 0ull;
+      }
+      __syncthreads();
+      // predicate x_w <= mid, children's bound keys (warp-reduced when the warp is one node)
+      for (int k0 = 0; k0 < c; k0 += kPB) {
+        const int k = k0 + tid;
+        int f = 0, js = -1;
+        const double* xp = nullptr;
+        if (k < c) {
+          const int jj = sseg[k];
+          if (jj >= 0 && nds[jj]) {
+            xp = a.x + (size_t)sp[k] * D;
+            f = xp[nw[jj]] <= cmid[jj] ? 1 : 0;
+            js = 2 * jj + (f ? 0 : 1);
+          }
+          sflag[k] = f;
+        }
+        const int jn = js >= 0 ? js >> 1 : -1;
+        const int j0 = __shfl_sync(0xffffffffu, jn, 0);
+        const bool uni = __all_sync(0xffffffffu, jn == j0) && j0 >= 0;
+        for (int d = 0; d < D; ++d) {
+          const unsigned long long key = js >= 0 ? dkey(xp[d]) : 0ull;
+          if (uni) {
+#pragma unroll
+            for (int side = 0; side < 2; ++side) {
+              const bool mine = (js & 1) == side;
+              if (!__any_sync(0xffffffffu, mine)) continue;
+              unsigned long long mn = mine ? key : ~0ull, mx = mine ? key : 0ull;
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) {
+                mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+              }
+              if (lane == 0) {
+                atomicMin(&kmn[(2 * j0 + side) * D + d], mn);
+                atomicMax(&kmx[(2 * j0 + side) * D + d], mx);
+              }
+            }
+          } else if (js >= 0) {
+            atomicMin(&kmn[js * D + d], key);
+            atomicMax(&kmx[js * D + d], key);
+          }
+        }
+      }
+      __syncthreads();
+      // exclusive prefix of the flags over the subtree's positions
+      {
+        constexpr int IPT = kLS / kPB;
+        int in[IPT], out[IPT], agg;
+#pragma unroll
+        for (int t = 0; t < IPT; ++t) {
+          const int k = tid * IPT + t;
+          in[t] = k < c ? sflag[k] : 0;
+        }
+        BS(tmp).ExclusiveSum(in, out, agg);
+#pragma unroll
+        for (int t = 0; t < IPT; ++t) {
+          const int k = tid * IPT + t;
+          if (k < c) sP[k] = out[t];
+        }
+        if (tid == 0) sP[c] = agg;
+      }
+      __syncthreads();
+      // per node: final left count (median fallback for one-sided splits, kdtree.cpp:85-94);
+      // per position: right-block passers register their slots
+      for (int jj = tid; jj < ncur; jj += kPB) {
+        const int id = nid[jj];
+        if (!nds[jj]) {
+          a.bsc[id] = 0.0;
+          a.nleft[id] = a.nright[id] = -1;
+          continue;
+        }
+        const int bg = nbg[jj], cn = ncn[jj];
+        const int L = sP[bg + cn] - sP[bg];
+        int l;
+        if (L == 0 || L == cn) {
+          KeyCmp cmp{ a.x, D, nw[jj] };
+          int* q0 = sp + bg;
+          dev_nth_element(q0, q0 + cn / 2, q0 + cn, cmp);
+          l = cn / 2;
+          a.bsc[id] = cmp.key(q0[cn / 2]);
+          for (int side = 0; side < 2; ++side) {
+            const int k0 = side ? l : 0, k1 = side ? cn : l;
+            for (int d = 0; d < D; ++d) {
+              unsigned long long mn = ~0ull, mx = 0ull;
+              for (int k = k0; k < k1; ++k) {
+                const unsigned long long kk = dkey(a.x[(size_t)q0[k] * D + d]);
+                mn = min(mn, kk);
+                mx = max(mx, kk);
+              }
+              kmn[(2 * jj + side) * D + d] = mn;
+              kmx[(2 * jj + side) * D + d] = mx;
+            }
+          }
+        } else {
+          l = L;
+          a.bsc[id] = cmid[jj];
+        }
+        nlc[jj] = l;
+      }
+      for (int k = tid; k < c; k += kPB) {
+        const int jj = sseg[k];
+        if (jj < 0 || !nds[jj] || !sflag[k]) continue;
+        const int bg = nbg[jj], e = bg + ncn[jj];
+        const int L = sP[e] - sP[bg];
+        if (k >= bg + L) sslot[bg + (sP[e] - sP[k] - 1)] = k;
+      }
+      __syncthreads();
+      // left-block failers swap with their partners (libstdc++ partition pairing)
+      for (int k = tid; k < c; k += kPB) {
+        const int jj = sseg[k];
+        if (jj < 0 || !nds[jj] || sflag[k]) continue;
+        const int bg = nbg[jj];
+        const int L = sP[bg + ncn[jj]] - sP[bg];
+        if (k < bg + L) {
+          const int kk = (k - bg) - (sP[k] - sP[bg]);
+          const int partner = sslot[bg + kk];
+          const int t = sp[k];
+          sp[k] = sp[partner];
+          sp[partner] = t;
+        }
+      }
+      // children: ranks among splitting nodes, ids, records, next-level node buffers
+      if (tid < 32) {
+        int run = 0;
+        for (int j0 = 0; j0 < ncur; j0 += 32) {
+          const int jj = j0 + lane;
+          const int sflg = jj < ncur ? nds[jj] : 0;
+          int x = sflg;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          if (jj < ncur) nrk[jj] = run + x - sflg;
+          run += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (lane == 0) {
+          s_ns = run;
+          s_cbase = run ? atomicAdd(a.kcount, 2 * run) : 0;
+        }
+      }
+      __syncthreads();
+      const int ns = s_ns, cbase = s_cbase;
+      for (int jj = tid; jj < ncur; jj += kPB) {
+        if (!nds[jj]) continue;
+        const int id = nid[jj], bg = nbg[jj], cn = ncn[jj], l = nlc[jj], r = nrk[jj];
+        const int cid = cbase + 2 * r;
+        a.nleft[id] = cid;
+        a.nright[id] = cid + 1;
+        for (int side = 0; side < 2; ++side) {
+          const int ch = cid + side, q = 2 * r + side;
+          const int cb = side ? bg + l : bg, cc = side ? cn - l : l;
+          a.npar[ch] = id;
+          a.ndep[ch] = lev + 1;
+          a.nbeg[ch] = b0 + cb;
+          a.ncnt[ch] = cc;
+          const size_t o = (size_t)ch * D;
+          int widest = 0;
+          double width = 0.0;
+          for (int d = 0; d < D; ++d) {
+            const double lo = dkey_inv(kmn[(2 * jj + side) * D + d]);
+            const double hi = dkey_inv(kmx[(2 * jj + side) * D + d]);
+            a.blo[o + d] = lo;
+            a.bhi[o + d] = hi;
+            a.bcen[o + d] = __dmul_rn(0.5, __dadd_rn(lo, hi));
+            const double w = __dadd_rn(hi, -lo);
+            if (d == 0 || w > width) {
+              width = w;
+              widest = d;
+            }
+          }
+          a.bside[ch] = width;
+          const int split = cc > a.leaf;
+          a.bsd[ch] = split ? widest : -1;
+          nxt[q] = ch;
+          nxt[kLN + q] = cb;
+          nxt[2 * kLN + q] = cc;
+          nxt[3 * kLN + q] = split;
+          nxt[4 * kLN + q] = split ? widest : -1;
+          xmid[q] = a.bcen[o + widest];
+        }
+      }
+      // positions move to their child (next-level index) or retire
+      for (int k = tid; k < c; k += kPB) {
+        const int jj = sseg[k];
+        if (jj < 0) continue;
+        sseg[k] = nds[jj] ? 2 * nrk[jj] + (k < nbg[jj] + nlc[jj] ? 0 : 1) : -1;
+      }
+      __syncthreads();
+      int* t = cur;
+      cur = nxt;
+      nxt = t;
+      double* tm = cmid;
+      cmid = xmid;
+      xmid = tm;
+      ncur = 2 * ns;
+      ++lev;
+    }
+    for (int k = tid; k < c; k += kPB) a.perm[b0 + k] = sp[k];
+    __syncthreads();
+  }
 }
 
 __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildArgs a)
@@ -484,6 +757,7 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
       }
       a.bside[bs + j] = width;
       const int split = a.ncnt[bs + j] > a.leaf;
+      if (split) atomicMax(&a.lvlmax[lev], a.ncnt[bs + j]);
       a.dosplit[(lev & 1) * NBL + j] = split;
       a.bsd[bs + j] = split ? widest : -1;
       a.mid[(lev & 1) * NBL + j] = a.bcen[o + widest];
@@ -523,11 +797,19 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
   grid.sync();
   decide(0, 0, 1);
   grid.sync();
+  bool local = false;
   for (;;) {
     if (gt == 0) a.lvl[1 + level] = base;
     if (a.trace && bid == 0 && tid == 0 && level < 64) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); a.trace[level * 8] = t_; }
     const int* dsp = a.dosplit + (level & 1) * NBL;  // this level's split flags / midpoints
     const double* mdp = a.mid + (level & 1) * NBL;
+    if (a.local_S > 0 && level > 0 && __ldcg(&a.lvlmax[level]) <= a.local_S) {
+      // every subtree below this level fits one CTA's shared memory: build them there
+      extern __shared__ __align__(16) unsigned char lsm[];
+      local_subtrees(a, tmp, lsm, base, m, level, dsp, mdp);
+      local = true;
+      break;
+    }
     unsigned long long* cmin = a.kmin + ((level + 1) & 1) * KBUF;  // children's (next level)
     unsigned long long* cmax = a.kmax + ((level + 1) & 1) * KBUF;
     // C: predicate flags and the CTA's chunk scans (positions; splitting level nodes)
@@ -727,13 +1009,15 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
     m = 2 * nsplit;
     ++level;
     if (m == 0 || level >= kMaxTreeLevels - 1) break;
+    if (gt == 0) *a.kcount = base + m;  // ids the local phase hands out start here
     decide(level, base, m);  // same phase: needs only bounds / counts / slots of level-1
     grid.sync();
     if (a.trace && bid == 0 && tid == 0 && level < 64) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); a.trace[level * 8 + 5] = t_; }
   }
-  if (gt == 0) {
+  if (gt == 0 && !local) {
     a.lvl[0] = level;
     a.lvl[1 + level] = base;
+    *a.kcount = base;
   }
 }
 
@@ -746,7 +1030,8 @@ static void finish_tree(DevTree& t, const double* d_x, int n, int D, int K,
                         const std::vector<int>& level_off, const double* blo, const double* bhi,
                         const double* bcen, const double* bside, const double* bsc, const int* bsd,
                         const int* d_bleft, const int* d_bright, const int* d_bbeg, const int* d_bcnt,
-                        const int* d_bpar, const int* d_bdep, cudaStream_t s);
+                        const int* d_bpar, const int* d_bdep, cudaStream_t s,
+                        const std::vector<int>* rank = nullptr);
 
 static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, int leaf,
                                   cudaStream_t s)
@@ -755,7 +1040,14 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_build, kPB, 0));
+  // CTA-local subtree phase: subtrees of <= local_S points (kLN nodes per local level
+  // bound it by the leaf size), D <= kLMaxD; DFGTB_TREE_LOCAL=0 turns it off
+  static const int local_env = std::getenv("DFGTB_TREE_LOCAL") ? std::atoi(std::getenv("DFGTB_TREE_LOCAL")) : -1;
+  const int local_cap = local_env >= 0 ? std::min(local_env, kLS) : kLS;
+  const int local_S = (local_env == 0 || D > kLMaxD) ? 0 : (int)std::min<long long>(local_cap, (long long)kLN * (leaf + 1) / 2);
+  const int smem = local_S >= 512 ? local_smem_bytes(D) : 0;
+  if (smem) CK(cudaFuncSetAttribute(k_build, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_build, kPB, smem));
   if (!coop || per_sm < 1) return false;
   // CTAs: 64 for small sets (measured: cheaper grid barriers, enough threads), one
   // per SM from ~256k points; DFGTB_TREE_CTAS overrides (experiments)
@@ -764,7 +1056,7 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
   const int maxK = 2 * n;
   DevBuf<double> blo, bhi, bcen, bside, bsc, mid;
   DevBuf<int> bsd, seg, flag, P, slot, nbeg, ncnt, nleft, nright, npar, ndep, dosplit, child, lc,
-    ctot, lvl, pslot;
+    ctot, lvl, pslot, lvlmax, kcount;
   DevBuf<unsigned long long> kmin, kmax;
   blo.reserve((size_t)maxK * D);
   bhi.reserve((size_t)maxK * D);
@@ -783,9 +1075,15 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
   ctot.reserve(2 * G);
   lvl.reserve(kMaxTreeLevels + 2);
   t.perm.reserve(n);
+  lvlmax.reserve(kMaxTreeLevels);
+  kcount.reserve(1);
+  CK(cudaMemsetAsync(lvlmax.p, 0, sizeof(int) * kMaxTreeLevels, s));
   BuildArgs a{ d_x, n, D, leaf, t.perm.p, seg.p, flag.p, P.p, slot.p, nbeg.p, ncnt.p, nleft.p,
                nright.p, npar.p, ndep.p, blo.p, bhi.p, bcen.p, bside.p, bsc.p, bsd.p, kmin.p,
                kmax.p, pslot.p, mid.p, dosplit.p, child.p, lc.p, ctot.p, lvl.p };
+  a.lvlmax = lvlmax.p;
+  a.kcount = kcount.p;
+  a.local_S = smem ? local_S : 0;
   static const bool tracing = std::getenv("DFGTB_TRACE") != nullptr;
   DevBuf<unsigned long long> trace;
   if (tracing) {
@@ -795,7 +1093,7 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
   }
   void* kargs[] = { &a };
   const auto c0 = std::chrono::steady_clock::now();
-  CK(cudaLaunchCooperativeKernel((void*)k_build, G, kPB, kargs, 0, s));
+  CK(cudaLaunchCooperativeKernel((void*)k_build, G, kPB, kargs, smem, s));
   CK_LAUNCH();
   if (tracing) {
     std::vector<unsigned long long> tr(64 * 8);
@@ -813,25 +1111,37 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
       std::fprintf(stderr, "\n");
     }
   }
-  std::vector<int> hl(kMaxTreeLevels + 2);
-  CK(cudaMemcpyAsync(hl.data(), lvl.p, sizeof(int) * hl.size(), cudaMemcpyDeviceToHost, s));
+  int K = 0;
+  CK(cudaMemcpyAsync(&K, kcount.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  const int levels = hl[0];
-  if (levels >= kMaxTreeLevels - 1) throw CudaError("kd-tree deeper than 255 levels");
-  const int K = hl[1 + levels];
-  std::vector<int> level_off(hl.begin() + 1, hl.begin() + 2 + levels);
   std::vector<int> h_left(K), h_right(K), h_beg(K), h_cnt(K);
   CK(cudaMemcpyAsync(h_left.data(), nleft.p, sizeof(int) * K, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(h_right.data(), nright.p, sizeof(int) * K, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(h_beg.data(), nbeg.p, sizeof(int) * K, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(h_cnt.data(), ncnt.p, sizeof(int) * K, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  // depth of every node (children have larger ids than their parent), the depth-major
+  // rank (BFS ids of the global levels keep their order) and the level offsets
+  std::vector<int> h_dep(K, 0), cnt_d(1, 0);
+  for (int i = 0; i < K; ++i) {
+    if ((size_t)h_dep[i] >= cnt_d.size()) cnt_d.resize(h_dep[i] + 1, 0);
+    ++cnt_d[h_dep[i]];
+    if (h_left[i] >= 0) h_dep[h_left[i]] = h_dep[h_right[i]] = h_dep[i] + 1;
+  }
+  const int levels = (int)cnt_d.size();
+  if (levels >= kMaxTreeLevels - 1) throw CudaError("kd-tree deeper than 255 levels");
+  std::vector<int> level_off(levels + 1, 0), rank(K);
+  for (int d = 0; d < levels; ++d) level_off[d + 1] = level_off[d] + cnt_d[d];
+  {
+    std::vector<int> fill(level_off.begin(), level_off.end() - 1);
+    for (int i = 0; i < K; ++i) rank[i] = fill[h_dep[i]]++;
+  }
   t.n = n;
   t.D = D;
   t.leaf = leaf;
   const auto c1 = std::chrono::steady_clock::now();
   finish_tree(t, d_x, n, D, K, h_left, h_right, h_beg, h_cnt, level_off, blo.p, bhi.p, bcen.p,
-              bside.p, bsc.p, bsd.p, nleft.p, nright.p, nbeg.p, ncnt.p, npar.p, ndep.p, s);
+              bside.p, bsc.p, bsd.p, nleft.p, nright.p, nbeg.p, ncnt.p, npar.p, ndep.p, s, &rank);
   if (tracing) {
     const auto c2 = std::chrono::steady_clock::now();
     std::fprintf(stderr, "DFGTB_TRACE tree host: build+copies %.1f us, finish %.1f us (G=%d, levels %d, K %d)\n",
@@ -992,7 +1302,8 @@ static void finish_tree(DevTree& t, const double* d_x, int n, int D, int K,
                         const std::vector<int>& level_off, const double* blo, const double* bhi,
                         const double* bcen, const double* bside, const double* bsc, const int* bsd,
                         const int* d_bleft, const int* d_bright, const int* d_bbeg, const int* d_bcnt,
-                        const int* d_bpar, const int* d_bdep, cudaStream_t s)
+                        const int* d_bpar, const int* d_bdep, cudaStream_t s,
+                        const std::vector<int>* rank)
 {
   t.nodes = K;
   t.height = (int)level_off.size() - 1;
@@ -1009,9 +1320,13 @@ static void finish_tree(DevTree& t, const double* d_x, int n, int D, int K,
       bfs2pre[h_left[i]] = bfs2pre[i] + 1;
       bfs2pre[h_right[i]] = bfs2pre[i] + 1 + sub[h_left[i]];
     }
-  DevBuf<int> d_map;
+  DevBuf<int> d_map, d_rank;
   d_map.reserve(K);
   CK(cudaMemcpyAsync(d_map.p, bfs2pre.data(), sizeof(int) * K, cudaMemcpyHostToDevice, s));
+  if (rank) {
+    d_rank.reserve(K);
+    CK(cudaMemcpyAsync(d_rank.p, rank->data(), sizeof(int) * K, cudaMemcpyHostToDevice, s));
+  }
   t.lo.reserve((size_t)K * D);
   t.hi.reserve((size_t)K * D);
   t.centroid.reserve((size_t)K * D);
@@ -1028,7 +1343,7 @@ static void finish_tree(DevTree& t, const double* d_x, int n, int D, int K,
   k_to_preorder<<<ceil_div(K, 256), 256, 0, s>>>(
     K, D, d_map.p, blo, bhi, bcen, bside, bsc, bsd, d_bleft, d_bright, d_bbeg, d_bcnt, d_bpar,
     d_bdep, t.lo.p, t.hi.p, t.centroid.p, t.max_side.p, t.split_coord.p, t.split_dim.p, t.left.p,
-    t.right.p, t.begin.p, t.count.p, t.parent.p, t.depth.p, t.by_depth.p);
+    t.right.p, t.begin.p, t.count.p, t.parent.p, t.depth.p, t.by_depth.p, rank ? d_rank.p : nullptr);
   CK_LAUNCH();
   t.anc.reserve((size_t)K * kMaxAnc);
   k_ancestors<<<ceil_div(K, 256), 256, 0, s>>>(K, t.parent.p, t.depth.p, t.anc.p);

@@ -1,6 +1,3 @@
-for v in default sk0 sk2 sk3; do
-  if [ $v = default ]; then unset DFGTB_LIB; else export DFGTB_LIB=paper_1102_2878_b200/build/v_$v/libdfgtb.so; fi
-  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r03p_launches_$v.csv python tools/profile_step.py > /dev/null 2>&1
-  python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', d['value'], d['ms_per_step'], d['roofline']['frac'], d['roofline']['base_ms_per_step'], d['e2e']['value'])"
-  python tools/profile_step.py --config 3 | tail -1; python tools/profile_step.py --config 5 | tail -1
-done
+for S in 4096 2048 1024 0; do for g in 64 148; do
+  echo "S=$S G=$g"; DFGTB_TREE_LOCAL=$S DFGTB_TREE_CTAS=$g python tools/e2e_breakdown.py 2 2>&1 | tail -1
+done; done
