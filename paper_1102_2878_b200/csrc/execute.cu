@@ -1238,13 +1238,21 @@ __device__ __noinline__ void base_group_f32_call(const float* rs, int n, const f
   base_group_f32<DT, GG>(rs, n, qs, qsum, lane);
 }
 
-// Queries in groups of 8, the remainder (1..7) as ONE group of its exact size.
+#ifndef DFGTB_F32_G16
+#define DFGTB_F32_G16 0
+#endif
+// Queries in groups of 8 (16 first with DFGTB_F32_G16, D <= 2), the remainder (1..7)
+// as ONE group of its exact size.
 template <int DT>
 __device__ __forceinline__ void base_groups_f32(const float* rs, int n, const float* qs, double* qsum,
                                                 int qc, int lane)
 {
   constexpr int DF = FPt<DT>::DF;
   int g0 = 0;
+#if DFGTB_F32_G16
+  if constexpr (DT <= 2)
+    for (; g0 + 16 <= qc; g0 += 16) base_group_f32_call<DT, 16>(rs, n, qs + g0 * DF, qsum + g0, lane);
+#endif
   for (; g0 + 8 <= qc; g0 += 8) base_group_f32_call<DT, 8>(rs, n, qs + g0 * DF, qsum + g0, lane);
   const float* q = qs + g0 * DF;
   double* qq = qsum + g0;

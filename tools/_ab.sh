@@ -1,3 +1,6 @@
-for S in 4096 2048 1024 0; do for g in 64 148; do
-  echo "S=$S G=$g"; DFGTB_TREE_LOCAL=$S DFGTB_TREE_CTAS=$g python tools/e2e_breakdown.py 2 2>&1 | tail -1
-done; done
+python -m pytest tests/test_gpu_engine.py tests/test_gpu_cv.py tests/test_gpu_fuzz.py -x -q 2>&1 | tail -1
+for v in default solo0 solo1024 solo4096 solo8192; do
+  if [ $v = default ]; then unset DFGTB_LIB; else export DFGTB_LIB=paper_1102_2878_b200/build/v_$v/libdfgtb.so; fi
+  for i in 1 2; do python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['ms_per_step'],4), round(d['roofline']['frac'],4), round(d['roofline']['base_ms_per_step'],4), d['e2e']['value'])"; done
+  python tools/phase_report.py --config 3 2>/dev/null | python tools/show_phases.py /dev/stdin | tail -1
+done
