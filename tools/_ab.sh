@@ -1,6 +1,5 @@
-python -m pytest tests/test_gpu_engine.py tests/test_gpu_cv.py tests/test_gpu_fuzz.py -x -q 2>&1 | tail -1
-for v in default solo0 solo1024 solo4096 solo8192; do
+for v in default cap0 head default cap0 head; do
   if [ $v = default ]; then unset DFGTB_LIB; else export DFGTB_LIB=paper_1102_2878_b200/build/v_$v/libdfgtb.so; fi
-  for i in 1 2; do python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['ms_per_step'],4), round(d['roofline']['frac'],4), round(d['roofline']['base_ms_per_step'],4), d['e2e']['value'])"; done
+  python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['ms_per_step'],4), round(d['roofline']['base_ms_per_step'],4), d['e2e']['value'])"
   python tools/phase_report.py --config 3 2>/dev/null | python tools/show_phases.py /dev/stdin | tail -1
 done

@@ -29,12 +29,15 @@ KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg", "launch__registers_p
 def raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
-    return r[0], r[1], r[2]
+    return r[0], r[1], r[2:]
 
 
 def main():
     rep = sys.argv[1]
-    h, u, v = raw(rep)
+    h, u, vs = raw(rep)
+    # --kernel SUBSTR picks the first launch whose name contains it (default: the first)
+    want = sys.argv[sys.argv.index("--kernel") + 1] if "--kernel" in sys.argv else None
+    v = next((x for x in vs if want is None or want in x[h.index("Kernel Name")]), vs[0])
     print(f"kernel: {v[h.index('Kernel Name')][:100]}")
     for k in KEYS:
         if k in h:
