@@ -806,8 +806,12 @@ __device__ __forceinline__ void entries_reduce(const TravArgs& a, int cur, int K
   }
 }
 
+#ifndef DFGTB_TRAV_CTAS_PER_SM
+#define DFGTB_TRAV_CTAS_PER_SM 1
+#endif
+constexpr int kPerSM = DFGTB_TRAV_CTAS_PER_SM;  // co-resident traversal CTAs per SM
 template <int DT>
-__global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__ TravArgs a)
+__global__ void __launch_bounds__(kPBlock, kPerSM) k_traverse(const __grid_constant__ TravArgs a)
 {
   cg::grid_group grid = cg::this_grid();
   TravState& st = *a.st;
@@ -926,7 +930,7 @@ __global__ void __launch_bounds__(kPBlock, 1) k_traverse(const __grid_constant__
       if (wib == 0) {
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
-          const int w = s_wsum[lane][k];
+          const int w = lane < kPBlock / 32 ? s_wsum[lane][k] : 0;
           int x = w;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
@@ -1123,7 +1127,7 @@ void Engine::run_levels(const void* args, const std::vector<const void*>& sig)
     if (per_sm >= 1) {
       TravArgs copy = a;
       void* kargs[] = { &copy };
-      CK(cudaLaunchCooperativeKernel(fn, nsm, kPBlock, kargs, 0, s_));
+      CK(cudaLaunchCooperativeKernel(fn, nsm * std::min(per_sm, kPerSM), kPBlock, kargs, 0, s_));
       ++launch_counter();
       return;
     }
