@@ -16,6 +16,7 @@ k in {-3,-2,-1,-0.5,0,0.5,1,2,3}, each with kernel sums at h and at 2h (18 sums 
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import math
 import os
@@ -205,6 +206,7 @@ def run_ours(a, rank, world, local_rank):
         torch.distributed.barrier()
     l0 = _capi.lib.dfgtb_launch_count(eng.handle)
     ms, base_ms, base_pairs, rows = [], 0.0, 0, None
+    f32_ms, fp64_ms = 0.0, 0.0
     with Clocks(local_rank) as clk:
         for _ in range(a.steps):
             with torch.cuda.stream(stream):
@@ -219,7 +221,13 @@ def run_ours(a, rank, world, local_rank):
             ms.append(e0.elapsed_time(e1))
             base_ms += sum(r.base_ms for r in rows)
             base_pairs += sum(r.base_pairs for r in rows)
+            tm = eng.last_timings()
+            f32_ms += tm["base_f32_ms"]
+            fp64_ms += tm["base_fp64_ms"]
     launches = _capi.lib.dfgtb_launch_count(eng.handle) - l0
+    # the base-case pairs on each kernel (every step runs the same sweep)
+    ta, tb, pa, pb = C.c_int(), C.c_int(), C.c_uint64(), C.c_uint64()
+    _capi.check(_capi.lib.dfgtb_last_base_split(eng.handle, C.byref(ta), C.byref(tb), C.byref(pa), C.byref(pb)))
     torch.cuda.synchronize()
     t_step = float(np.mean(ms))
     if world > 1:
@@ -267,6 +275,16 @@ def run_ours(a, rank, world, local_rank):
             traffic = None
     common = {"traffic": traffic, "base_pairs_per_step": base_pairs // max(a.steps, 1),
               "base_ms_per_step": base_ms / max(a.steps, 1)}
+    if mufu and exp_mode == 2:
+        # each base-case kernel against the same ex2 peak (events around each launch)
+        per = []
+        for name, pairs, t in (("k_task_split + k_base_f32 (FP32 path)", pa.value, f32_ms),
+                               ("k_base_case (FP64 distance, MUFU / FP64 exp)", pb.value, fp64_ms)):
+            tk = t / max(a.steps, 1)
+            rate = pairs / (tk * 1e-3) if tk > 0 else 0.0
+            per.append({"kernel": name, "pairs_per_step": int(pairs), "ms_per_step": tk,
+                        "achieved": rate / 1e9, "frac": rate / peak_ex2 if peak_ex2 > 0 else None})
+        common["per_kernel"] = per
     if mufu:
         # one MUFU ex2 per (q, r) pair: the SFU pipe is the exp roofline
         kname = ("k_base_f32 + k_base_case (K10 exhaustive base case: FP32 distance/ex2/partial sums "

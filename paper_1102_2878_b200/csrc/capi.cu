@@ -233,6 +233,8 @@ int dfgtb_last_timings(dfgtb_handle* h, dfgtb_timings* t)
     t->farfield_ms = s.farfield_ms;
     t->final_ms = s.final_ms;
     t->total_ms = s.total_ms;
+    t->base_f32_ms = s.base_f32_ms;
+    t->base_fp64_ms = s.base_fp64_ms;
   });
 }
 

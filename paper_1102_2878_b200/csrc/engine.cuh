@@ -32,7 +32,7 @@ struct Stats {
 // engine stream).
 struct Timings {
   float tree_ms = 0, traverse_ms = 0, moments_ms = 0, local_ms = 0, base_ms = 0, farfield_ms = 0,
-        final_ms = 0, total_ms = 0;
+        final_ms = 0, total_ms = 0, base_f32_ms = 0, base_fp64_ms = 0;
 };
 
 struct Cnt {

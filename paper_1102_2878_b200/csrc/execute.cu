@@ -2052,7 +2052,7 @@ int persistent_grid(KF kern, int threads, int smem, int slack, int tcap, int war
 template <int DT>
 void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int K, const BTask* tasks,
                    const int2* rec, const double* xq, const double* xr, int nq, int nr, double* part,
-                   int* ws, int mufu, int slack, const double* c0, SlotView sv, double f)
+                   int* ws, int mufu, int slack, const double* c0, SlotView sv, double f, cudaEvent_t mid)
 {
   static int gridB = 0, gridA = 0;
   constexpr int threads = BaseGeo<DT>::WARPS * 32;
@@ -2075,6 +2075,7 @@ void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int 
                                                                      nq, nr, part, ws, c0, sv, f);
     CK_LAUNCH();
   }
+  if (mid) CK(cudaEventRecord(mid, s));
   k_base_case<DT><<<std::min(gridB, cap_grid), threads, smem, s>>>(Q, K, tasks, listB, ws + 3, rec, xq, xr,
                                                                   nq, nr, part, ws + 1, mufu, c0, sv, f);
 }
@@ -2082,10 +2083,10 @@ void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int 
 void launch_base(int D, cudaStream_t s, TreeView Q, TreeView R, int K, const BTask* tasks,
                  const int* ntasks, int tcap, const Item* items, const int2* rec, const double* xq,
                  const double* xr, int nq, int nr, double* part, int* next, int mufu, int slack,
-                 const double* c0, SlotView sv, double f)
+                 const double* c0, SlotView sv, double f, cudaEvent_t mid)
 {
 #define BASE(DD)                                                                                 \
-  launch_base_t<DD>(ntasks, tcap, s, Q, K, tasks, rec, xq, xr, nq, nr, part, next, mufu, slack, c0, sv, f)
+  launch_base_t<DD>(ntasks, tcap, s, Q, K, tasks, rec, xq, xr, nq, nr, part, next, mufu, slack, c0, sv, f, mid)
   switch (D) {
   case 1: BASE(1); break;
   case 2: BASE(2); break;
@@ -2093,6 +2094,7 @@ void launch_base(int D, cudaStream_t s, TreeView Q, TreeView R, int K, const BTa
   case 4: BASE(4); break;
   case 5: BASE(5); break;
   default:
+    if (mid) CK(cudaEventRecord(mid, s));
     k_base_case_any<<<148 * 16, kBlock, 0, s>>>(Q, R, K, D, tasks, ntasks, tcap, items, xq, xr, nq, nr,
                                                 part);
     break;
@@ -2213,6 +2215,8 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
   CK(cudaEventElapsedTime(&tim_.moments_ms, ev_[3], ev_[4]));
   CK(cudaEventElapsedTime(&tim_.local_ms, ev_[4], ev_[5]));
   CK(cudaEventElapsedTime(&tim_.base_ms, ev_[9], ev_[10]));
+  CK(cudaEventElapsedTime(&tim_.base_f32_ms, ev_[9], ev_[11]));
+  CK(cudaEventElapsedTime(&tim_.base_fp64_ms, ev_[11], ev_[10]));
   CK(cudaEventElapsedTime(&tim_.farfield_ms, ev_[6], ev_[7]));
   CK(cudaEventElapsedTime(&tim_.final_ms, ev_[7], ev_[8]));
   CK(cudaEventElapsedTime(&tim_.total_ms, ev_[2], ev_[8]));
@@ -2393,7 +2397,7 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
   launch_base(D_, s, Q, R, K, reinterpret_cast<const BTask*>(tasks_.p), bc_.p + 5, capTask_, sB_.p,
               reinterpret_cast<const int2*>(brec_.p), xq, xr, qt.n, rt_.n, bpart_.p, bnext_.p,
               (mufu_ ? 1 : 0) | (f32_ ? 2 : 0), base_cta_slack_, rt_.centroid.p, sv,
-              mufu_ ? kSqrtLog2e : 1.0);
+              mufu_ ? kSqrtLog2e : 1.0, ev_[11]);
   CK(cudaEventRecord(ev_[10], s));
   // join, finalize
   CK(cudaStreamWaitEvent(s, join_, 0));
