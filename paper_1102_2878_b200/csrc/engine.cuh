@@ -134,7 +134,7 @@ private:
   DevBuf<double> L_, Mt_, s_ff_;      // Mt_: UNSCALED reference moments (h-independent)
   DevBuf<int> Lord_, cntF_, cntDT_, cntB_, offF_, offDT_, offB_, mflag_, mdone_;
   bool eager_ = false;                // Mt_ holds every node (tables <= 4096 terms)
-  DevBuf<int> lnch_, lchoff_, lchunk_, ntask_, toff_, tasks_, leaf_task_, leaf_runs_, brec_, bnext_;
+  DevBuf<int> lnch_, lchoff_, lchunk_, tasks_, leaf_task_, leaf_runs_, brec_, bnext_;
   DevBuf<double> lpart_, bpart_, xq_, xr_, slotp_;
   // frontier (double buffered) and per-level scratch
   DevBuf<int> fq_[2], foff_[2], flen_[2], fr_[2], pent_[2];

@@ -599,36 +599,27 @@ __device__ __forceinline__ int warp_run_end(const Item* it, int k, int e, const 
   return k + __popc(fit);
 }
 
-__global__ void k_task_count(const int* leaves, int nleaves, int nb, int K, const int* cntB,
+// Base-case tasks in one pass: the (slot, leaf)'s warp counts its runs,
+// claims its task range with one atomic (bc[5] = tasks so far; a key's tasks stay
+// contiguous, query chunk major, run minor, which is all k_finalize relies on), then
+// writes the tasks.  Tasks past tcap are dropped; the host sees bc[5] > tcap and reruns.
+__global__ void k_task_build(const int* leaves, int nleaves, int nb, int K, const int* cntB,
                              const int* offB, const Item* sB, const int* rcount, int rmax, TreeView Q,
-                             int* nt)
+                             BTask* tasks, int tcap, int* ntasks, int* leaf_task, int* leaf_runs,
+                             int* tflag)
 {
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (i >= nleaves * nb) return;
-  const int slot = i / nleaves;
-  const int leaf = leaves[i - slot * nleaves];
-  const int key = slot * K + leaf;
-  const int o = offB[key], e = o + cntB[key];
-  int runs = 0;
-  for (int k = o; k < e; k = warp_run_end(sB, k, e, rcount, rmax, lane)) ++runs;
-  if (lane == 0) nt[i] = runs * ((Q.count[leaf] + 31) / 32);
-}
-
-__global__ void k_task_fill(const int* leaves, int nleaves, int nb, int K, const int* cntB,
-                            const int* offB, const Item* sB, const int* rcount, int rmax, TreeView Q,
-                            const int* toff, BTask* tasks, int tcap, int* ntasks_out,
-                            int* leaf_task, int* leaf_runs, int* tflag)
-{
-  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (i == 0 && lane == 0) *ntasks_out = toff[nleaves * nb];
   if (i >= nleaves * nb) return;
   const int slot = i / nleaves;
   const int leaf = leaves[i - slot * nleaves];
   const int key = slot * K + leaf;
   const int o = offB[key], e = o + cntB[key];
   const int nq = (Q.count[leaf] + 31) / 32;
-  const int t0 = toff[i];
-  const int nruns = nq ? (toff[i + 1] - t0) / nq : 0;  // tasks: query chunk major, run minor
+  int nruns = 0;
+  for (int k = o; k < e; k = warp_run_end(sB, k, e, rcount, rmax, lane)) ++nruns;
+  int t0 = 0;
+  if (lane == 0 && nruns) t0 = atomicAdd(ntasks, nruns * nq);
+  t0 = __shfl_sync(0xffffffffu, t0, 0);
   int runs = 0;
   for (int k = o; k < e;) {
     const int j = warp_run_end(sB, k, e, rcount, rmax, lane);
@@ -2034,7 +2025,7 @@ int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }
 
 // Persistent grids: as many CTAs as fit on the GPU (or fewer for small task lists).
 // ws = [nextA, nextB, cntA, cntB, pairsA (u64), pairsB (u64), listA (tcap), listB (tcap),
-// task flags (tcap, written by k_task_fill)].  The task split, then the
+// task flags (tcap, written by k_task_build)].  The task split, then the
 // FP32 kernel over list A, then the FP64 kernel over list B.
 template <class KF>
 int persistent_grid(KF kern, int threads, int smem, int slack, int tcap, int warps)
@@ -2352,27 +2343,14 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
   leaf_task_.reserve(KB);
   leaf_runs_.reserve(KB);
   const int rmax = base_rmax(D_);
-  ntask_.reserve(nlb + 1);
-  toff_.reserve(nlb + 1);
-  k_task_count<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p, sB_.p,
-                                                  R.count, rmax, Q, ntask_.p);
-  CK_LAUNCH();
-  CK(cudaMemsetAsync(ntask_.p + nlb, 0, sizeof(int), s));
-  {
-    size_t need = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need, ntask_.p, toff_.p, nlb + 1, s);
-    scan_tmp_.reserve(need + 256);
-    size_t have = scan_tmp_.cap;
-    cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, ntask_.p, toff_.p, nlb + 1, s);
-  }
   capTask_ = std::max(capTask_, std::max(4096, capB_ / 8));
   tasks_.reserve((size_t)capTask_ * 4);
   bnext_.reserve(8 + 3 * (size_t)capTask_);  // base-case lists and task flags (launch_base_t)
-  k_task_fill<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p, sB_.p,
-                                                 R.count, rmax, Q, toff_.p,
-                                                 reinterpret_cast<BTask*>(tasks_.p), capTask_,
-                                                 bc_.p + 5, leaf_task_.p, leaf_runs_.p,
-                                                 bnext_.p + 8 + 2 * (size_t)capTask_);
+  CK(cudaMemsetAsync(bc_.p + 5, 0, sizeof(int), s));
+  k_task_build<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p, sB_.p,
+                                                  R.count, rmax, Q, reinterpret_cast<BTask*>(tasks_.p),
+                                                  capTask_, bc_.p + 5, leaf_task_.p, leaf_runs_.p,
+                                                  bnext_.p + 8 + 2 * (size_t)capTask_);
   CK_LAUNCH();
   bpart_.reserve((size_t)capTask_ * 32);
   brec_.reserve((size_t)capB_ * 2 + 2);
