@@ -278,7 +278,7 @@ def run_ours(a, rank, world, local_rank):
     if mufu and exp_mode == 2:
         # each base-case kernel against the same ex2 peak (events around each launch)
         per = []
-        for name, pairs, t in (("k_task_split + k_base_f32 (FP32 path)", pa.value, f32_ms),
+        for name, pairs, t in (("k_base_f32 (FP32 path)", pa.value, f32_ms),
                                ("k_base_case (FP64 distance, MUFU / FP64 exp)", pb.value, fp64_ms)):
             tk = t / max(a.steps, 1)
             rate = pairs / (tk * 1e-3) if tk > 0 else 0.0

@@ -53,7 +53,7 @@ typedef struct dfgtb_stats {
 /* Device time (ms, CUDA events on the handle's stream) of the last compute. */
 typedef struct dfgtb_timings {
   float tree_ms, traverse_ms, moments_ms, local_ms, base_ms, farfield_ms, final_ms, total_ms;
-  float base_f32_ms, base_fp64_ms; /* base_ms split: task split + FP32 kernel | FP64 kernel */
+  float base_f32_ms, base_fp64_ms; /* base_ms split: FP32 kernel | FP64 kernel */
 } dfgtb_timings;
 
 /* One bandwidth of a CV sweep (CvRow, cv.hpp:49-56 + ScoreResult cv.hpp:25-32). */

@@ -1504,26 +1504,37 @@ __global__ void __launch_bounds__(F32Geo<DT>::WARPS * 32, DFGTB_BF32_MINB)
 // engine runs the FP32 base case) -> list A, the rest -> list B.  cnt[0], cnt[1] count
 // them (zeroed by the caller).  The order inside a list is irrelevant: every task
 // writes its own partial sums.
-__global__ void k_task_split(const int* ntasks_p, int tcap, const int* tflag, int f32, int* listA, int* listB,
-                             int* cnt)
+__global__ void k_task_split(const int* leaves, int nleaves, int nb, int K, const int* cntB,
+                             const int* leaf_task, const int* leaf_runs, TreeView Q, int tcap,
+                             const int* tflag, int f32, int* listA, int* listB, int* cnt)
 {
-  const int n = min(*ntasks_p, tcap);
+  // one warp per (slot, leaf) key in key order, lanes over its tasks: the lists keep a
+  // key's tasks together (the query tile and reference leaves stay hot in L1 / L2)
   const int lane = threadIdx.x & 31;
-  const int nb = (n + 31) & ~31;  // whole warps in the loop (ballots)
-  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nb; w += gridDim.x * blockDim.x) {
-    const bool in = w < n;
-    const bool a = in && f32 && tflag[w];
-    const unsigned ma = __ballot_sync(0xffffffffu, a), mb = __ballot_sync(0xffffffffu, in && !a);
-    int baseA = 0, baseB = 0;
-    if (lane == 0) {
-      if (ma) baseA = atomicAdd(cnt, __popc(ma));
-      if (mb) baseB = atomicAdd(cnt + 1, __popc(mb));
+  const unsigned below = (1u << lane) - 1u;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nleaves * nb;
+       i += (gridDim.x * blockDim.x) >> 5) {
+    const int slot = i / nleaves;
+    const int leaf = leaves[i - slot * nleaves];
+    const int key = slot * K + leaf;
+    if (!cntB[key]) continue;
+    const int t0 = leaf_task[key];
+    const int nt = leaf_runs[key] * ((Q.count[leaf] + 31) / 32);
+    for (int j0 = 0; j0 < nt; j0 += 32) {
+      const int w = t0 + j0 + lane;
+      const bool in = j0 + lane < nt && w < tcap;
+      const bool a = in && f32 && tflag[w];
+      const unsigned ma = __ballot_sync(0xffffffffu, a), mb = __ballot_sync(0xffffffffu, in && !a);
+      int baseA = 0, baseB = 0;
+      if (lane == 0) {
+        if (ma) baseA = atomicAdd(cnt, __popc(ma));
+        if (mb) baseB = atomicAdd(cnt + 1, __popc(mb));
+      }
+      baseA = __shfl_sync(0xffffffffu, baseA, 0);
+      baseB = __shfl_sync(0xffffffffu, baseB, 0);
+      if (a) listA[baseA + __popc(ma & below)] = w;
+      else if (in) listB[baseB + __popc(mb & below)] = w;
     }
-    baseA = __shfl_sync(0xffffffffu, baseA, 0);
-    baseB = __shfl_sync(0xffffffffu, baseB, 0);
-    const unsigned below = (1u << lane) - 1u;
-    if (a) listA[baseA + __popc(ma & below)] = w;
-    else if (in) listB[baseB + __popc(mb & below)] = w;
   }
 }
 
@@ -2025,7 +2036,7 @@ int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }
 
 // Persistent grids: as many CTAs as fit on the GPU (or fewer for small task lists).
 // ws = [nextA, nextB, cntA, cntB, pairsA (u64), pairsB (u64), listA (tcap), listB (tcap),
-// task flags (tcap, written by k_task_build)].  The task split, then the
+// task flags (tcap, written by k_task_build)]; the lists come from k_task_split.  Then the
 // FP32 kernel over list A, then the FP64 kernel over list B.
 template <class KF>
 int persistent_grid(KF kern, int threads, int smem, int slack, int tcap, int warps)
@@ -2057,10 +2068,7 @@ void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int 
   const int cap_grid = (tcap + 3) / 4;
   int* listA = ws + 8;
   int* listB = ws + 8 + tcap;
-  CK(cudaMemsetAsync(ws, 0, 8 * sizeof(int), s));
-  k_task_split<<<148 * 4, 256, 0, s>>>(ntasks, tcap, ws + 8 + 2 * (size_t)tcap, (mufu & 2) ? 1 : 0, listA, listB,
-                                       ws + 2);
-  CK_LAUNCH();
+  (void)ntasks;  // the lists were built by k_task_split (launch_phases)
   if (mufu & 2) {
     k_base_f32<DT><<<std::min(gridA, cap_grid), threadsA, smemA, s>>>(Q, K, tasks, listA, ws + 2, rec, xq, xr,
                                                                      nq, nr, part, ws, c0, sv, f);
@@ -2351,6 +2359,11 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
                                                   R.count, rmax, Q, reinterpret_cast<BTask*>(tasks_.p),
                                                   capTask_, bc_.p + 5, leaf_task_.p, leaf_runs_.p,
                                                   bnext_.p + 8 + 2 * (size_t)capTask_);
+  CK_LAUNCH();
+  CK(cudaMemsetAsync(bnext_.p, 0, 8 * sizeof(int), s));
+  k_task_split<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, leaf_task_.p, leaf_runs_.p, Q,
+                                                  capTask_, bnext_.p + 8 + 2 * (size_t)capTask_, f32_ ? 1 : 0,
+                                                  bnext_.p + 8, bnext_.p + 8 + capTask_, bnext_.p + 2);
   CK_LAUNCH();
   bpart_.reserve((size_t)capTask_ * 32);
   brec_.reserve((size_t)capB_ * 2 + 2);
