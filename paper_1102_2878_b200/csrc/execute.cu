@@ -703,18 +703,16 @@ __device__ __forceinline__ double exp_negy_c(double y, unsigned tabs)
 // rounding) + ex2.approx's error (exhaustively measured by the tests over every
 // reachable argument).
 constexpr int kMufuBias = 4;
-constexpr unsigned kMufuHi = 0x41F80000u;    // high word of t for 896 - b <= z < 4992
+// t above this (high word 0x41F80000, low word (125 << 20) | 0xFFFFF) is z > 1021 - b
+constexpr double kMufuClampT = 0x1.8000007dfffffp+32;
 template <bool CLAMP = false>
 __device__ __forceinline__ double exp2_neg_fixed(double t, unsigned fbits)
 {
-  int lo = __double2loint(t);
-  bool under = false;
-  if constexpr (CLAMP) {  // z > 1021 -> 0 (terms < 2^-1021; only where the traversal pays for it)
-    const unsigned hi = (unsigned)__double2hiint(t);  // kMufuHi - 1 below z = 896 - b
-    const int lmax = (125 << 20) | 0xFFFFF;
-    under = hi > kMufuHi || (hi == kMufuHi && (unsigned)lo > (unsigned)lmax);
-    lo = under ? lmax : lo;
-  }
+  // z > 1021 -> 0 (terms < 2^-1021; only where the traversal pays for it): one FP64
+  // compare on t (positive doubles order like their bit patterns), the term is computed
+  // from whatever t is and discarded
+  const bool under = CLAMP && t > kMufuClampT;
+  const int lo = __double2loint(t);
   // fbits = 0x4B000000 held in a register (one LOP3: (lo & mask) | fbits)
   const float x = __uint_as_float(((unsigned)lo & 0xFFFFFu) | fbits);  // 2^23 + f
   const float a = fmaf(x, -0x1p-20f, 8.0f + kMufuBias * 0x1p-20f);     // (b - f) 2^-20, exact
@@ -722,9 +720,8 @@ __device__ __forceinline__ double exp2_neg_fixed(double t, unsigned fbits)
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(a));
   const unsigned G = __float_as_uint(g);
   const unsigned hi = (G >> 3) - ((unsigned)lo & 0xFFF00000u);
-  if constexpr (CLAMP)
-    if (under) return 0.0;
-  return __hiloint2double((int)hi, (int)(G << 29));
+  const double v = __hiloint2double((int)hi, (int)(G << 29));
+  return under ? 0.0 : v;
 }
 constexpr double kMufuMagic = 6442450944.0 - 896.0 + kMufuBias * 0x1p-20;  // M - 896 + b 2^-20
 constexpr double kSqrtLog2e = 1.2011224087864498;                           // sqrt(log2 e)
