@@ -137,8 +137,8 @@ void pinned_free(void* p, size_t bytes)
 // costs ~0.1-0.2 ms per engine, which a CV call that builds an engine per dataset pays
 // every time.
 struct StreamSet {
-  cudaStream_t s = nullptr, s2 = nullptr;
-  cudaEvent_t ev[12] = {}, fork = nullptr, join = nullptr;
+  cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
+  cudaEvent_t ev[14] = {}, fork = nullptr, join = nullptr, fork3 = nullptr, join3 = nullptr;
 };
 static std::unordered_map<int, std::vector<StreamSet>>& stream_pool()
 {
@@ -162,8 +162,11 @@ static StreamSet acquire_streams()
   StreamSet r;
   CK(cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&r.s2, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&r.s3, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&r.fork3, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&r.join3, cudaEventDisableTiming));
   for (auto& e : r.ev) CK(cudaEventCreate(&e));
   return r;
 }
@@ -229,7 +232,10 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
     s2_ = ss.s2;
     fork_ = ss.fork;
     join_ = ss.join;
-    for (int i = 0; i < 12; ++i) ev_[i] = ss.ev[i];
+    for (int i = 0; i < 14; ++i) ev_[i] = ss.ev[i];
+    s3_ = ss.s3;
+    fork3_ = ss.fork3;
+    join3_ = ss.join3;
   }
   x_.reserve(n * d);
   CK(cudaMemcpyAsync(x_.p, refs, sizeof(double) * n * d,
@@ -273,7 +279,10 @@ Engine::~Engine()
     ss.s2 = s2_;
     ss.fork = fork_;
     ss.join = join_;
-    for (int i = 0; i < 12; ++i) ss.ev[i] = ev_[i];
+    for (int i = 0; i < 14; ++i) ss.ev[i] = ev_[i];
+    ss.s3 = s3_;
+    ss.fork3 = fork3_;
+    ss.join3 = join3_;
     release_streams(ss);  // pooled for the next engine on this device
   }
 }

@@ -159,7 +159,9 @@ private:
   cudaGraphExec_t gexec_ = nullptr;
   cudaGraphConditionalHandle hc_ = 0;
   std::vector<const void*> gsig_;
-  cudaEvent_t ev_[12];
+  cudaEvent_t ev_[14];
+  cudaStream_t s3_ = nullptr;  // the FP64 base-case kernel beside the FP32 one
+  cudaEvent_t fork3_ = nullptr, join3_ = nullptr;
   cudaEvent_t fork_ = nullptr, join_ = nullptr;
   std::vector<Stats> slot_stats_;
   Timings tim_;
@@ -167,6 +169,7 @@ private:
   int nb_ = 1;
   bool mufu_ = false;
   bool f32_ = false;
+  bool base_conc_ = false;  // the last batch ran the two base-case kernels side by side
   const DevTree* last_q_ = nullptr;  // query tree and node count of the last batch (diagnostics)
   int last_K_ = 0;
   // device-side counts of a batch (no host round trip until its end):

@@ -2035,6 +2035,20 @@ int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }
 // ws = [nextA, nextB, cntA, cntB, pairsA (u64), pairsB (u64), listA (tcap), listB (tcap),
 // task flags (tcap, written by k_task_build)]; the lists come from k_task_split.  Then the
 // FP32 kernel over list A, then the FP64 kernel over list B.
+#ifndef DFGTB_BASE_CONC
+#define DFGTB_BASE_CONC 0  // measured: side by side is no faster than one after the other (c32) or slower
+#endif
+#ifndef DFGTB_CONC_F32
+#define DFGTB_CONC_F32 4
+#endif
+#ifndef DFGTB_CONC_FP64
+#define DFGTB_CONC_FP64 1
+#endif
+constexpr int kConcF32 = DFGTB_CONC_F32, kConcFP64 = DFGTB_CONC_FP64;  // CTAs per SM side by side
+struct BaseConc {
+  cudaStream_t s3 = nullptr;  // nullptr: the two kernels run one after the other on `s`
+  cudaEvent_t fork3 = nullptr, join3 = nullptr, b0 = nullptr, b1 = nullptr;
+};
 template <class KF>
 int persistent_grid(KF kern, int threads, int smem, int slack, int tcap, int warps)
 {
@@ -2051,7 +2065,8 @@ int persistent_grid(KF kern, int threads, int smem, int slack, int tcap, int war
 template <int DT>
 void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int K, const BTask* tasks,
                    const int2* rec, const double* xq, const double* xr, int nq, int nr, double* part,
-                   int* ws, int mufu, int slack, const double* c0, SlotView sv, double f, cudaEvent_t mid)
+                   int* ws, int mufu, int slack, const double* c0, SlotView sv, double f, cudaEvent_t mid,
+                   const BaseConc& cc)
 {
   static int gridB = 0, gridA = 0;
   constexpr int threads = BaseGeo<DT>::WARPS * 32;
@@ -2066,6 +2081,30 @@ void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int 
   int* listA = ws + 8;
   int* listB = ws + 8 + tcap;
   (void)ntasks;  // the lists were built by k_task_split (launch_phases)
+  if ((mufu & 2) && cc.s3) {
+    // both kernels at once: the FP32 one (XU / FP32 pipes) on `s` with kConcF32 CTAs per
+    // SM, the FP64 one (FP64 pipe) on `s3` with the register file's remainder
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    CK(cudaEventRecord(cc.fork3, s));
+    CK(cudaStreamWaitEvent(cc.s3, cc.fork3, 0));
+    CK(cudaEventRecord(cc.b0, cc.s3));
+    k_base_case<DT><<<std::min(nsm * kConcFP64, cap_grid), threads, smem, cc.s3>>>(
+      Q, K, tasks, listB, ws + 3, rec, xq, xr, nq, nr, part, ws + 1, mufu, c0, sv, f);
+    CK_LAUNCH();
+    CK(cudaEventRecord(cc.b1, cc.s3));
+    CK(cudaEventRecord(cc.join3, cc.s3));
+    k_base_f32<DT><<<std::min(nsm * kConcF32, cap_grid), threadsA, smemA, s>>>(Q, K, tasks, listA, ws + 2, rec,
+                                                                               xq, xr, nq, nr, part, ws, c0, sv, f);
+    CK_LAUNCH();
+    if (mid) CK(cudaEventRecord(mid, s));
+    CK(cudaStreamWaitEvent(s, cc.join3, 0));
+    return;
+  }
   if (mufu & 2) {
     k_base_f32<DT><<<std::min(gridA, cap_grid), threadsA, smemA, s>>>(Q, K, tasks, listA, ws + 2, rec, xq, xr,
                                                                      nq, nr, part, ws, c0, sv, f);
@@ -2079,10 +2118,10 @@ void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int 
 void launch_base(int D, cudaStream_t s, TreeView Q, TreeView R, int K, const BTask* tasks,
                  const int* ntasks, int tcap, const Item* items, const int2* rec, const double* xq,
                  const double* xr, int nq, int nr, double* part, int* next, int mufu, int slack,
-                 const double* c0, SlotView sv, double f, cudaEvent_t mid)
+                 const double* c0, SlotView sv, double f, cudaEvent_t mid, const BaseConc& cc)
 {
 #define BASE(DD)                                                                                 \
-  launch_base_t<DD>(ntasks, tcap, s, Q, K, tasks, rec, xq, xr, nq, nr, part, next, mufu, slack, c0, sv, f, mid)
+  launch_base_t<DD>(ntasks, tcap, s, Q, K, tasks, rec, xq, xr, nq, nr, part, next, mufu, slack, c0, sv, f, mid, cc)
   switch (D) {
   case 1: BASE(1); break;
   case 2: BASE(2); break;
@@ -2212,7 +2251,8 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
   CK(cudaEventElapsedTime(&tim_.local_ms, ev_[4], ev_[5]));
   CK(cudaEventElapsedTime(&tim_.base_ms, ev_[9], ev_[10]));
   CK(cudaEventElapsedTime(&tim_.base_f32_ms, ev_[9], ev_[11]));
-  CK(cudaEventElapsedTime(&tim_.base_fp64_ms, ev_[11], ev_[10]));
+  if (base_conc_) CK(cudaEventElapsedTime(&tim_.base_fp64_ms, ev_[12], ev_[13]));
+  else CK(cudaEventElapsedTime(&tim_.base_fp64_ms, ev_[11], ev_[10]));
   CK(cudaEventElapsedTime(&tim_.farfield_ms, ev_[6], ev_[7]));
   CK(cudaEventElapsedTime(&tim_.final_ms, ev_[7], ev_[8]));
   CK(cudaEventElapsedTime(&tim_.total_ms, ev_[2], ev_[8]));
@@ -2382,10 +2422,19 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
     xr = xr_.p;
   }
   CK(cudaEventRecord(ev_[9], s));
+  BaseConc conc;
+  if (DFGTB_BASE_CONC && f32_ && !std::getenv("DFGTB_BASE_SERIAL")) {
+    conc.s3 = s3_;
+    conc.fork3 = fork3_;
+    conc.join3 = join3_;
+    conc.b0 = ev_[12];
+    conc.b1 = ev_[13];
+  }
+  base_conc_ = conc.s3 != nullptr;
   launch_base(D_, s, Q, R, K, reinterpret_cast<const BTask*>(tasks_.p), bc_.p + 5, capTask_, sB_.p,
               reinterpret_cast<const int2*>(brec_.p), xq, xr, qt.n, rt_.n, bpart_.p, bnext_.p,
               (mufu_ ? 1 : 0) | (f32_ ? 2 : 0), base_cta_slack_, rt_.centroid.p, sv,
-              mufu_ ? kSqrtLog2e : 1.0, ev_[11]);
+              mufu_ ? kSqrtLog2e : 1.0, ev_[11], conc);
   CK(cudaEventRecord(ev_[10], s));
   // join, finalize
   CK(cudaStreamWaitEvent(s, join_, 0));
