@@ -1226,25 +1226,11 @@ __device__ __noinline__ void base_group_f32_call(const float* rs, int n, const f
   base_group_f32<DT, GG>(rs, n, qs, qsum, lane);
 }
 
-#ifndef DFGTB_F32_G16
-#define DFGTB_F32_G16 0
-#endif
-// Queries in groups of 8 (16 first with DFGTB_F32_G16, D <= 2), the remainder (1..7)
-// as ONE group of its exact size.
 template <int DT>
-__device__ __forceinline__ void base_groups_f32(const float* rs, int n, const float* qs, double* qsum,
-                                                int qc, int lane)
+__device__ __forceinline__ void base_group_f32_n(const float* rs, int n, const float* q, double* qq, int g,
+                                                 int lane)
 {
-  constexpr int DF = FPt<DT>::DF;
-  int g0 = 0;
-#if DFGTB_F32_G16
-  if constexpr (DT <= 2)
-    for (; g0 + 16 <= qc; g0 += 16) base_group_f32_call<DT, 16>(rs, n, qs + g0 * DF, qsum + g0, lane);
-#endif
-  for (; g0 + 8 <= qc; g0 += 8) base_group_f32_call<DT, 8>(rs, n, qs + g0 * DF, qsum + g0, lane);
-  const float* q = qs + g0 * DF;
-  double* qq = qsum + g0;
-  switch (qc - g0) {
+  switch (g) {
   case 1: base_group_f32_call<DT, 1>(rs, n, q, qq, lane); break;
   case 2: base_group_f32_call<DT, 2>(rs, n, q, qq, lane); break;
   case 3: base_group_f32_call<DT, 3>(rs, n, q, qq, lane); break;
@@ -1252,8 +1238,21 @@ __device__ __forceinline__ void base_groups_f32(const float* rs, int n, const fl
   case 5: base_group_f32_call<DT, 5>(rs, n, q, qq, lane); break;
   case 6: base_group_f32_call<DT, 6>(rs, n, q, qq, lane); break;
   case 7: base_group_f32_call<DT, 7>(rs, n, q, qq, lane); break;
+  case 8: base_group_f32_call<DT, 8>(rs, n, q, qq, lane); break;
   default: break;
   }
+}
+
+// Queries in groups of 8, the remainder (1..7) as ONE group of its exact size (measured:
+// near-equal group sizes, e.g. 21 -> 7 + 7 + 7, are 7% slower).
+template <int DT>
+__device__ __forceinline__ void base_groups_f32(const float* rs, int n, const float* qs, double* qsum,
+                                                int qc, int lane)
+{
+  constexpr int DF = FPt<DT>::DF;
+  int g0 = 0;
+  for (; g0 + 8 <= qc; g0 += 8) base_group_f32_call<DT, 8>(rs, n, qs + g0 * DF, qsum + g0, lane);
+  base_group_f32_n<DT>(rs, n, qs + g0 * DF, qsum + g0, qc - g0, lane);
 }
 
 // Queries in groups of G, the remainder in groups of 4, 2, 1.  Each group size is one
