@@ -252,6 +252,8 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
     CK(cudaEventElapsedTime(&ms, ev_[0], ev_[2]));
     std::fprintf(stderr, "DFGTB_TRACE create: upload+tree %.3f ms\n", ms);
   }
+  nn2_.reserve(rt_.nodes);
+  leaf_nn2(rt_, nn2_.p, s_);
   if (cfg.mode == 1) {
     if (ser_.T <= 4096) {
       eager_ = true;

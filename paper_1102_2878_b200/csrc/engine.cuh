@@ -169,7 +169,9 @@ private:
   int nb_ = 1;
   bool mufu_ = false;
   bool f32_ = false;
-  bool base_conc_ = false;  // the last batch ran the two base-case kernels side by side
+  bool base_conc_ = false;
+  DevBuf<double> nn2_;  // per reference leaf: max over its points of the squared distance to
+                        // the nearest other point of the leaf (+inf for internal / 1-point nodes)  // the last batch ran the two base-case kernels side by side
   const DevTree* last_q_ = nullptr;  // query tree and node count of the last batch (diagnostics)
   int last_K_ = 0;
   // device-side counts of a batch (no host round trip until its end):
@@ -190,6 +192,9 @@ double measure_dfma_peak(int device);
 double measure_ex2_peak(int device);
 // Max relative error of the base case's MUFU exp over every argument it can form.
 double mufu_exp_max_error();
+// Per leaf of t: the largest squared distance of a point to its nearest other point in
+// the leaf (+inf for internal nodes and 1-point leaves).
+void leaf_nn2(const DevTree& t, double* nn2, cudaStream_t s);
 // Max relative error of ex2.approx.ftz.f32 over every FP32 argument in [-126, 2^-10].
 double f32_exp_max_error();
 // The FP32 base case's term for host pairs (test entry; points in z units, stride d).

@@ -2603,6 +2603,43 @@ __global__ void k_ex2_peak(float* out, int iters)
   if (s == 42.0f) out[0] = s;
 }
 
+__global__ void k_leaf_nn2(int K, int D, const int* left, const int* begin, const int* count,
+                           const double* xs, double* nn2)
+{
+  const int lane = threadIdx.x & 31;
+  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < K; k += (gridDim.x * blockDim.x) >> 5) {
+    const int b = begin[k], c = count[k];
+    double worst = 0.0;
+    if (left[k] < 0 && c >= 2) {
+      for (int i = lane; i < c; i += 32) {
+        double best = CUDART_INF;
+        for (int j = 0; j < c; ++j) {
+          if (j == i) continue;
+          double d2 = 0.0;
+          for (int d = 0; d < D; ++d) {
+            const double t = xs[(size_t)(b + i) * D + d] - xs[(size_t)(b + j) * D + d];
+            d2 = fma(t, t, d2);
+          }
+          best = fmin(best, d2);
+        }
+        worst = fmax(worst, best);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+    } else {
+      worst = CUDART_INF;
+    }
+    if (lane == 0) nn2[k] = worst;
+  }
+}
+
+void leaf_nn2(const DevTree& t, double* nn2, cudaStream_t s)
+{
+  k_leaf_nn2<<<std::min(ceil_div((long long)t.nodes * 32, 256), 148 * 16), 256, 0, s>>>(
+    t.nodes, t.D, t.left.p, t.begin.p, t.count.p, t.xs.p, nn2);
+  CK_LAUNCH();
+}
+
 void Engine::base_split(int& f32_tasks, int& fp64_tasks, unsigned long long& f32_pairs,
                         unsigned long long& fp64_pairs)
 {

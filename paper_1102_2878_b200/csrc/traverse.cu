@@ -155,6 +155,8 @@ struct TravArgs {
   int D, pmax, cost, series, T;
   int selfq;  // Q = R: every query's sum is >= 1 (its own term)
   int f32;    // the FP32 base case may be flagged (order bit 2)
+  const double* qnn2;  // Q = R: per leaf the largest squared distance of a point to its
+                       // nearest neighbour inside the leaf (+inf: none / not a leaf)
   TravState* st;
   int *fq[2], *foff[2], *flen[2], *fr[2];
   int* pent[2];  // entry index of every frontier pair (pair-balanced persistent path)
@@ -257,12 +259,13 @@ __global__ void k_trav_init(const __grid_constant__ TravArgs a)
 // <= 12 u G rounding of FP32 partial sums that hold the self term 1 stay below 1e-3
 // relative to the G - 1 the CV scores take logarithms of.
 __device__ __forceinline__ int base_flags(const TravArgs& a, double kmin, double glo, double sq, double h,
-                                          int D, int nq)
+                                          int D, int nq, int Q)
 {
   const double dz = sq * sqrt((double)D) * 0.8494;
-  // Q = R leave-one-out floor: a query leaf of >= 2 points whose diagonal is <= 3.16
-  // z-units gives every query a neighbour with K >= 2^-10, so G - 1 >= 2^-10 as well
-  const bool loo = glo >= 1.0 + 0x1p-10 || (nq >= 2 && dz <= 3.16 * h);
+  // Q = R leave-one-out floor: every query of the leaf has a neighbour inside it with
+  // K >= 2^-10 (its nearest one within z = 10: log2 e d^2 / 2h^2 <= 10), so G - 1 >= 2^-10
+  const bool loo = glo >= 1.0 + 0x1p-10 ||
+                   (nq >= 2 && a.qnn2 && a.qnn2[Q] * 0.7213475204444817 <= 10.0 * h * h);
   return (kmin >= 3.4e-308 ? 1 : 0) | ((a.selfq || glo >= 1e-290) && dz <= 1000.0 * h ? 2 : 0) |
          (a.f32 && (a.selfq ? loo : glo >= 1e-20) && dz <= kF32Diam * h ? 4 : 0);
 }
@@ -323,7 +326,7 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
       }
       if (kind == kX && qleaf && a.R.left[R] < 0) {
         kind = kB;
-        order = base_flags(a, kmin, glo, sq, h, D, a.Q.count[Q]);
+        order = base_flags(a, kmin, glo, sq, h, D, a.Q.count[Q], Q);
       }
       if (kind == kX) {
         slots += a.R.left[R] < 0 ? 1 : 2;
@@ -725,7 +728,7 @@ __device__ __forceinline__ void pairs_decide(const TravArgs& a, const TravState&
       }
       if (kind == kX && a.Q.left[Q] < 0 && a.R.left[R] < 0) {
         kind = kB;
-        order = base_flags(a, kmin, uglo[u], a.Q.side[Q], s_h[slot], D, a.Q.count[Q]);
+        order = base_flags(a, kmin, uglo[u], a.Q.side[Q], s_h[slot], D, a.Q.count[Q], Q);
       }
     }
     a.dec[j] = kind | (order << 8);
@@ -1261,6 +1264,7 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   a.R = view_of(rt_);
   a.selfq = &qt == &rt_ ? 1 : 0;
   a.f32 = f32_ ? 1 : 0;
+  a.qnn2 = &qt == &rt_ ? nn2_.p : nullptr;
   a.D = D_;
   a.pmax = ser_.pmax;
   a.cost = cfg_.cost_model;
