@@ -114,7 +114,30 @@ def _load():
     return lib
 
 
-lib = _load()
+class _Lib:
+    """The loaded libdfgtb.so, opened on first use.
+
+    Importing the package checks that the library exists (no CPU fallback) but does
+    not map it: processes that only need the package's host helpers (e.g. the
+    datagen of bench.py's reference arm) never load the CUDA library.
+    """
+
+    _lib = None
+
+    def __getattr__(self, name):
+        if _Lib._lib is None:
+            _Lib._lib = _load()
+        return getattr(_Lib._lib, name)
+
+    @property
+    def loaded(self) -> bool:
+        return _Lib._lib is not None
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `make -C {_HERE}` "
+                      "(or __graft_entry__.build()); there is no CPU fallback")
+lib = _Lib()
 
 
 def check(rc: int) -> None:

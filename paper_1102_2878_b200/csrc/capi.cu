@@ -207,6 +207,7 @@ int dfgtb_compute_device(dfgtb_handle* h, const double* dq, size_t nq, double bw
 {
   return guard([&] {
     check_h(h);
+    h->eng->wait_legacy_stream();  // inputs produced on the legacy stream are ordered first
     h->eng->compute_device(dq, nq, bw, dout);
     fill_stats(h->eng->last_stats(), st);
   });
@@ -252,6 +253,7 @@ static void cv_rows(dfgtb_handle* h, const double* bws, const double* convs, int
                     dfgtb_cv_row* rows)
 {
   Engine& e = *h->eng;
+  DeviceGuard dg(e.device());
   const size_t n = e.n();
   if (n < 2) throw InvalidArgument("likelihood CV requires at least 2 points");
   const bool ls = convs != nullptr;
@@ -326,15 +328,20 @@ int dfgtb_compute_batch(dfgtb_handle* h, const double* queries, size_t nq, const
     if (nb == 0) throw InvalidArgument("empty bandwidth batch");
     DevBuf<double> q, out;
     out.reserve(n_out * nb);
+    DeviceGuard dg(e.device());
+    // every copy is ordered on the engine's stream (pageable host memory: the async
+    // copies are staged by the driver; the stream synchronisation ends the call)
     if (queries) {
       q.reserve(nq * e.dim());
-      CK(cudaMemcpy(q.p, queries, sizeof(double) * nq * e.dim(), cudaMemcpyHostToDevice));
+      CK(cudaMemcpyAsync(q.p, queries, sizeof(double) * nq * e.dim(), cudaMemcpyHostToDevice,
+                         e.stream()));
     }
     for (size_t b0 = 0; b0 < nb; b0 += kMaxSlots) {
       const int m = (int)std::min<size_t>(kMaxSlots, nb - b0);
       e.compute_batch(queries ? q.p : nullptr, nq, bws + b0, m, out.p);
-      CK(cudaMemcpy(out_sums + b0 * n_out, out.p, sizeof(double) * n_out * m,
-                    cudaMemcpyDeviceToHost));
+      CK(cudaMemcpyAsync(out_sums + b0 * n_out, out.p, sizeof(double) * n_out * m,
+                         cudaMemcpyDeviceToHost, e.stream()));
+      CK(cudaStreamSynchronize(e.stream()));
       if (stats)
         for (int k = 0; k < m; ++k) fill_stats(e.last_stats(k), stats + b0 + k);
     }
@@ -349,13 +356,16 @@ int dfgtb_compute_batch_f32(dfgtb_handle* h, const float* queries, size_t nq, co
     Engine& e = *h->eng;
     if (!queries) throw InvalidArgument("null query points");
     if (nb == 0) throw InvalidArgument("empty bandwidth batch");
+    DeviceGuard dg(e.device());
     DevBuf<double> q, out;
     widen_to_device(queries, nq * e.dim(), q);
     out.reserve(nq * nb);
     for (size_t b0 = 0; b0 < nb; b0 += kMaxSlots) {
       const int m = (int)std::min<size_t>(kMaxSlots, nb - b0);
       e.compute_batch(q.p, nq, bws + b0, m, out.p);
-      CK(cudaMemcpy(out_sums + b0 * nq, out.p, sizeof(double) * nq * m, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpyAsync(out_sums + b0 * nq, out.p, sizeof(double) * nq * m, cudaMemcpyDeviceToHost,
+                         e.stream()));
+      CK(cudaStreamSynchronize(e.stream()));
       if (stats)
         for (int k = 0; k < m; ++k) fill_stats(e.last_stats(k), stats + b0 + k);
     }
@@ -405,6 +415,8 @@ int dfgtb_export_tree(dfgtb_handle* h, int* perm, double* lo, double* hi, double
 {
   return guard([&] {
     check_h(h);
+    DeviceGuard dg(h->eng->device());
+    CK(cudaStreamSynchronize(h->eng->stream()));
     const DevTree& t = h->eng->ref_tree();
     const size_t K = t.nodes, D = t.D;
     auto cp = [&](void* dst, const void* src, size_t bytes) {

@@ -47,22 +47,48 @@ uint64_t& launch_counter();
 // instead of paying cudaMalloc/cudaFree each time.  A block returned to the cache
 // may still be read by queued kernels, so returning synchronises the device first
 // (the guarantee cudaFree gave).  dfgtb_release_cached_memory() empties the cache.
+// Blocks are keyed by the device they were allocated on (DevBuf records it), so a
+// buffer freed while another device is current returns to its own device's pool.
 void* cache_alloc(size_t bytes);
-void cache_free(void* p, size_t bytes);
+void cache_free(void* p, size_t bytes, int device);
 void cache_release_all();
+int current_device();
+
+// Makes `dev` current for a scope and restores the previous device afterwards.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev)
+  {
+    if (dev < 0) return;
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      cudaGetLastError();
+      prev = -1;
+      return;
+    }
+    if (prev != dev && cudaSetDevice(dev) != cudaSuccess) cudaGetLastError();
+  }
+  ~DeviceGuard()
+  {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
 
 // Growable device buffer (capacity only ever grows; contents not preserved on growth).
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t cap = 0;
+  int dev = -1;  // device the block was allocated on
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release()
   {
-    if (p) cache_free(p, cap * sizeof(T));
+    if (p) cache_free(p, cap * sizeof(T), dev);
     p = nullptr;
     cap = 0;
   }
@@ -76,6 +102,7 @@ struct DevBuf {
     release();
     p = static_cast<T*>(cache_alloc(c * sizeof(T)));
     cap = c;
+    dev = current_device();
     return p;
   }
 };

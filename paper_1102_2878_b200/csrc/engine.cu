@@ -44,12 +44,7 @@ std::unordered_map<size_t, std::vector<void*>>& host_cache()
   static auto* c = new std::unordered_map<size_t, std::vector<void*>>();
   return *c;
 }
-uint64_t cache_key(size_t bytes)
-{
-  int dev = 0;
-  cudaGetDevice(&dev);
-  return ((uint64_t)bytes << 8) | (uint64_t)(dev & 0xff);
-}
+uint64_t cache_key(size_t bytes, int dev) { return ((uint64_t)bytes << 8) | (uint64_t)(dev & 0xff); }
 void* take_cached(uint64_t key)  // g_cache_mu held
 {
   auto it = dev_cache().find(key);
@@ -60,18 +55,31 @@ void* take_cached(uint64_t key)  // g_cache_mu held
 }
 }  // namespace
 
+int current_device()
+{
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return dev;
+}
+
 void* cache_alloc(size_t bytes)
 {
-  const uint64_t key = cache_key(bytes);
+  const int dev = current_device();
+  const uint64_t key = cache_key(bytes, dev);
   {
     std::unique_lock<std::mutex> g(g_cache_mu);
     if (void* p = take_cached(key)) return p;
     bool match = false;
     for (const auto& e : dev_pending()) match = match || e.first == key;
     if (match) {
-      // only the blocks pending before the synchronisation are known idle afterwards
-      std::vector<std::pair<uint64_t, void*>> idle;
-      idle.swap(dev_pending());
+      // Only the blocks of THIS device pending before the synchronisation are known
+      // idle afterwards (cudaDeviceSynchronize covers the current device only).
+      std::vector<std::pair<uint64_t, void*>> idle, keep;
+      for (auto& e : dev_pending()) ((int)(e.first & 0xff) == (dev & 0xff) ? idle : keep).push_back(e);
+      dev_pending().swap(keep);
       g.unlock();
       if (cudaDeviceSynchronize() != cudaSuccess) cudaGetLastError();
       g.lock();
@@ -90,22 +98,31 @@ void* cache_alloc(size_t bytes)
   return p;
 }
 
-void cache_free(void* p, size_t bytes)
+void cache_free(void* p, size_t bytes, int device)
 {
-  const uint64_t key = cache_key(bytes);
+  const uint64_t key = cache_key(bytes, device >= 0 ? device : current_device());
   std::lock_guard<std::mutex> g(g_cache_mu);
   dev_pending().emplace_back(key, p);
 }
 
 void cache_release_all()
 {
-  cudaDeviceSynchronize();
   std::lock_guard<std::mutex> g(g_cache_mu);
+  const int cur = current_device();
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) cudaGetLastError();
+  for (int d = 0; d < ndev; ++d)  // every device's queued work must be idle first
+    if (cudaSetDevice(d) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) cudaGetLastError();
+  auto free_on = [](uint64_t key, void* p) {
+    if (cudaSetDevice((int)(key & 0xff)) != cudaSuccess) cudaGetLastError();
+    cudaFree(p);
+  };
   for (auto& kv : dev_cache())
-    for (void* p : kv.second) cudaFree(p);
+    for (void* p : kv.second) free_on(kv.first, p);
   dev_cache().clear();
-  for (auto& e : dev_pending()) cudaFree(e.second);
+  for (auto& e : dev_pending()) free_on(e.first, e.second);
   dev_pending().clear();
+  if (ndev > 0 && cudaSetDevice(cur) != cudaSuccess) cudaGetLastError();
   for (auto& kv : host_cache())
     for (void* p : kv.second) cudaFreeHost(p);
   host_cache().clear();
@@ -138,7 +155,8 @@ void pinned_free(void* p, size_t bytes)
 // every time.
 struct StreamSet {
   cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
-  cudaEvent_t ev[14] = {}, fork = nullptr, join = nullptr, fork3 = nullptr, join3 = nullptr;
+  cudaEvent_t ev[14] = {}, fork = nullptr, join = nullptr, fork3 = nullptr, join3 = nullptr,
+              legacy = nullptr;
 };
 static std::unordered_map<int, std::vector<StreamSet>>& stream_pool()
 {
@@ -167,6 +185,7 @@ static StreamSet acquire_streams()
   CK(cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&r.fork3, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&r.join3, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&r.legacy, cudaEventDisableTiming));
   for (auto& e : r.ev) CK(cudaEventCreate(&e));
   return r;
 }
@@ -219,6 +238,7 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
     throw InvalidArgument("SeriesGeometry requires dim >= 1 and 1 <= p_max <= 15");
   D_ = (int)d;
   n_ = n;
+  dev_ = current_device();
   if (const char* sl = std::getenv("DFGTB_BASE_SLACK")) base_cta_slack_ = std::atoi(sl);
   mufu_ = cfg.epsilon >= kMufuMinEps && D_ <= 5 && std::getenv("DFGTB_EXACT_EXP") == nullptr;
   f32_ = mufu_ && cfg.epsilon >= kF32MinEps && std::getenv("DFGTB_NO_F32") == nullptr;
@@ -236,8 +256,10 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
     s3_ = ss.s3;
     fork3_ = ss.fork3;
     join3_ = ss.join3;
+    legacy_ev_ = ss.legacy;
   }
   x_.reserve(n * d);
+  if (on_device) wait_legacy_stream();  // the caller's producer of refs
   CK(cudaMemcpyAsync(x_.p, refs, sizeof(double) * n * d,
                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s_));
   upload_series(ser_, ser_dev_, s_);
@@ -271,6 +293,7 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
 
 Engine::~Engine()
 {
+  DeviceGuard dg(dev_);  // streams go back to this device's pool
   if (s_) cudaStreamSynchronize(s_);
   destroy_graph();
   if (hst_) pinned_free(hst_, hst_bytes_);
@@ -285,6 +308,7 @@ Engine::~Engine()
     ss.s3 = s3_;
     ss.fork3 = fork3_;
     ss.join3 = join3_;
+    ss.legacy = legacy_ev_;
     release_streams(ss);  // pooled for the next engine on this device
   }
 }
@@ -335,9 +359,17 @@ DevSeries series_view(const SeriesTables& t, const DevBuf<unsigned char>& dev)
   return g;
 }
 
+void Engine::wait_legacy_stream()
+{
+  DeviceGuard dg(dev_);
+  CK(cudaEventRecord(legacy_ev_, cudaStreamLegacy));
+  CK(cudaStreamWaitEvent(s_, legacy_ev_, 0));
+}
+
 void Engine::compute_batch(const double* d_queries, size_t nq, const double* h, int nb,
                            double* d_out)
 {
+  DeviceGuard dg(dev_);
   if (nb < 1 || nb > kMaxSlots) throw InvalidArgument("batch size outside [1, 64]");
   for (int b = 0; b < nb; ++b) {
     if (!(h[b] > 0.0)) throw InvalidArgument("bandwidth must be positive");
@@ -359,6 +391,7 @@ void Engine::compute_batch(const double* d_queries, size_t nq, const double* h, 
 
 void Engine::compute_host(const double* h_queries, size_t nq, double h, double* h_out)
 {
+  DeviceGuard dg(dev_);
   const size_t n_out = h_queries ? nq : n_;
   DevBuf<double> out;
   out.reserve(n_out);

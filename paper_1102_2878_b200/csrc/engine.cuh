@@ -99,6 +99,10 @@ public:
   int dim() const { return D_; }
   size_t n() const { return n_; }
   cudaStream_t stream() const { return s_; }
+  int device() const { return dev_; }
+  // Make the engine's stream wait for everything queued so far on the legacy default
+  // stream (where callers of the *_device entry points typically produced their inputs).
+  void wait_legacy_stream();
   const SeriesTables& series() const { return ser_; }
   DevSeries dev_series() const;
   const double* d_refs() const { return x_.p; }
@@ -114,6 +118,7 @@ private:
   void setup_leaves(const DevTree& t);
 
   Config cfg_;
+  int dev_ = -1;  // device the engine was created on (made current by every entry point)
   int D_ = 0;
   size_t n_ = 0;
   cudaStream_t s_ = nullptr;
@@ -163,6 +168,7 @@ private:
   cudaStream_t s3_ = nullptr;  // the FP64 base-case kernel beside the FP32 one
   cudaEvent_t fork3_ = nullptr, join3_ = nullptr;
   cudaEvent_t fork_ = nullptr, join_ = nullptr;
+  cudaEvent_t legacy_ev_ = nullptr;  // orders s_ after the legacy stream (wait_legacy_stream)
   std::vector<Stats> slot_stats_;
   Timings tim_;
   long long nF_ = 0, nDT_ = 0, nB_ = 0;

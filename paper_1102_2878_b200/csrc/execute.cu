@@ -2463,6 +2463,7 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
 void Engine::cv_reduce(const double* d_sums, const double* h, const double* d_conv,
                        const double* conv_h, int ns, double* lk, int* clamped, double* ls)
 {
+  DeviceGuard dg(dev_);
   const size_t n = n_;
   if (n < 2) throw InvalidArgument("CV requires at least 2 points");
   if (ns < 1 || ns > kMaxSlots) throw InvalidArgument("CV batch size outside [1, 64]");
@@ -2643,6 +2644,7 @@ void leaf_nn2(const DevTree& t, double* nn2, cudaStream_t s)
 void Engine::base_split(int& f32_tasks, int& fp64_tasks, unsigned long long& f32_pairs,
                         unsigned long long& fp64_pairs)
 {
+  DeviceGuard dg(dev_);
   int v[6] = { 0, 0, 0, 0, 0, 0 };
   if (bnext_.p && tasks_.p && brec_.p) {
     CK(cudaMemsetAsync(bnext_.p + 4, 0, 4 * sizeof(int), s_));
