@@ -48,6 +48,11 @@ typedef struct dfgtb_stats {
   uint64_t prunes_direct_local;
   uint64_t prunes_far_to_local;
   uint64_t levels;
+  /* Coverage (the reference's CoverageProbe, tests/probes.hpp:13-44): sum over every
+   * retired node pair (finite-difference prune, F, D, T, base case) of |Q| * |R|.
+   * Every (query, reference) pair is retired exactly once, so this equals
+   * n_queries * n_refs. */
+  uint64_t pairs_covered;
 } dfgtb_stats;
 
 /* Device time (ms, CUDA events on the handle's stream) of the last compute. */
@@ -62,7 +67,10 @@ typedef struct dfgtb_cv_row {
   double lk_score;  /* lkcv_from_sums  (cv.cpp:61-76) */
   int lk_clamped;
   double ls_score;  /* lscv_from_sums  (cv.cpp:78-97) */
-  double seconds;   /* device time of this row's computes */
+  double seconds;   /* device time of this row's computes.  dfgtb_sweep runs all rows'
+                       bandwidths through ONE batched traversal, so this is the batch's
+                       device time divided evenly over the rows (a share, not a per-h
+                       measurement); dfgtb_cv rows are measured individually. */
   double base_ms;   /* device time of the base-case kernel launches of this row */
   uint64_t base_pairs;          /* (q, r) kernel evaluations in those base cases */
   uint64_t kernel_evaluations;  /* TraversalStats::kernel_evaluations, summed */
@@ -124,6 +132,11 @@ int dfgtb_cv(dfgtb_handle* h, double bandwidth, double conv_h, dfgtb_cv_row* row
 int dfgtb_sweep(dfgtb_handle* h, const double* scales, size_t ns, double base_h, int sqrt2,
                 dfgtb_cv_row* rows);
 
+/* h* of a sweep: lk_best = argmax lk_score, ls_best = argmin ls_score over the rows
+ * (first index on ties, the argmin of acceptance.cpp:633-641).
+ * Either output pointer may be NULL. */
+int dfgtb_sweep_best(const dfgtb_cv_row* rows, size_t ns, size_t* lk_best, size_t* ls_best);
+
 /* CV scores from host sums (lkcv_from_sums / lscv_from_sums, cv.cpp:61-97). */
 int dfgtb_lkcv_from_sums(size_t n, size_t d, double bandwidth, const double* sums,
                          double* score, int* clamped);
@@ -154,6 +167,18 @@ int dfgtb_naive(const double* queries, size_t nq, const double* refs, size_t nr,
  * written for 2/3/4 like the reference's accumulate-into semantics. */
 int dfgtb_series_op(int op, size_t d, int p_max, const double* in, size_t n, const double* a,
                     const double* b, double bandwidth, int order, double* out);
+
+/* choose_best_method (truncation.cpp:130-166) and the least orders farfield_order /
+ * local_accum_order / f2l_order (truncation.cpp:98-128) exactly as the traversal
+ * evaluates them on the device, for n tuples.  args: n x 9 doubles (n_query, n_ref,
+ * max_side_query, max_side_ref, h, tau, p_max, dim, cost_model); out: n x 5 ints
+ * (kind: 0 exhaustive, 1 farfield, 2 direct_local, 3 far_to_local -- ApproxChoice::Kind
+ * truncation.hpp:43-48; order; p_F; p_D; p_T, 0 = none).  Test entry. */
+int dfgtb_choose_methods(size_t n, const double* args, int* out);
+
+/* box_distance_bounds_sq (kdtree.cpp:122-141) as the traversal evaluates it on the
+ * device.  boxes: n x 4d doubles (a_lo, a_hi, b_lo, b_hi); out: n x 2 (lo^2, hi^2). */
+int dfgtb_box_bounds(size_t n, size_t d, const double* boxes, double* out);
 
 /* Measured FP64 FMA instruction throughput of the device (instr/s); bench roofline. */
 double dfgtb_dfma_peak(void);

@@ -28,7 +28,8 @@ class Config(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "kernel_evaluations", "pairs_visited", "base_cases", "prunes_finite_diff",
-        "prunes_farfield", "prunes_direct_local", "prunes_far_to_local", "levels")]
+        "prunes_farfield", "prunes_direct_local", "prunes_far_to_local", "levels",
+        "pairs_covered")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -59,7 +60,7 @@ EXPORTS = (
     "dfgtb_p_max", "dfgtb_cv", "dfgtb_sweep", "dfgtb_lkcv_from_sums", "dfgtb_lscv_from_sums",
     "dfgtb_tree_nodes", "dfgtb_tree_height", "dfgtb_export_tree", "dfgtb_naive",
     "dfgtb_series_op", "dfgtb_dfma_peak", "dfgtb_mufu_exp_error", "dfgtb_f32_exp_error", "dfgtb_f32_terms", "dfgtb_last_base_split", "dfgtb_ex2_peak", "dfgtb_base_exp_mode", "dfgtb_device_count", "dfgtb_release_cached_memory",
-    "dfgtb_stream",
+    "dfgtb_stream", "dfgtb_choose_methods", "dfgtb_box_bounds", "dfgtb_sweep_best",
     "dfgtb_launch_count", "dfgtb_last_error",
 )
 
@@ -104,6 +105,9 @@ def _load():
         "dfgtb_device_count": (C.c_int, []),
         "dfgtb_release_cached_memory": (None, []),
         "dfgtb_stream": (C.c_size_t, [V]),
+        "dfgtb_choose_methods": (C.c_int, [sz, _D, _I]),
+        "dfgtb_sweep_best": (C.c_int, [C.POINTER(CvRow), sz, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+        "dfgtb_box_bounds": (C.c_int, [sz, sz, _D, _D]),
         "dfgtb_launch_count": (C.c_uint64, [V]),
         "dfgtb_last_error": (C.c_char_p, []),
     }

@@ -70,6 +70,7 @@ void fill_stats(const Stats& s, dfgtb_stats* o)
   o->prunes_direct_local = s.prunes_direct_local;
   o->prunes_far_to_local = s.prunes_far_to_local;
   o->levels = (uint64_t)s.levels;
+  o->pairs_covered = s.pairs_covered;
 }
 
 void check_h(dfgtb_handle* h)
@@ -318,6 +319,20 @@ int dfgtb_sweep(dfgtb_handle* h, const double* scales, size_t ns, double base_h,
   });
 }
 
+int dfgtb_sweep_best(const dfgtb_cv_row* rows, size_t ns, size_t* lk_best, size_t* ls_best)
+{
+  return guard([&] {
+    if (ns == 0 || !rows) throw InvalidArgument("empty sweep");
+    size_t bk = 0, bs = 0;
+    for (size_t i = 1; i < ns; ++i) {
+      if (rows[i].lk_score > rows[bk].lk_score) bk = i;
+      if (rows[i].ls_score < rows[bs].ls_score) bs = i;
+    }
+    if (lk_best) *lk_best = bk;
+    if (ls_best) *ls_best = bs;
+  });
+}
+
 int dfgtb_compute_batch(dfgtb_handle* h, const double* queries, size_t nq, const double* bws,
                         size_t nb, double* out_sums, dfgtb_stats* stats)
 {
@@ -496,6 +511,28 @@ int dfgtb_series_op(int op, size_t d, int p_max, const double* in, size_t n, con
     if (scalar) out[0] = hout[0];
     else
       for (size_t i = 0; i < T; ++i) out[t.pos[i]] = hout[i];
+  });
+}
+
+int dfgtb_choose_methods(size_t n, const double* args, int* out)
+{
+  return guard([&] {
+    if (n && (!args || !out)) throw InvalidArgument("dfgtb_choose_methods: null pointer");
+    for (size_t i = 0; i < n; ++i) {
+      const double* a = args + 9 * i;
+      if (a[6] < 1 || a[6] > 15 || a[7] < 1 || a[7] > kMaxDim || (a[8] != 0 && a[8] != 1))
+        throw InvalidArgument("dfgtb_choose_methods: p_max in [1, 15], dim in [1, 16], cost 0/1");
+    }
+    choose_methods_device(n, args, out);
+  });
+}
+
+int dfgtb_box_bounds(size_t n, size_t d, const double* boxes, double* out)
+{
+  return guard([&] {
+    if (d < 1 || d > (size_t)kMaxDim) throw InvalidArgument("dimension must be in [1, 16]");
+    if (n && (!boxes || !out)) throw InvalidArgument("dfgtb_box_bounds: null pointer");
+    box_bounds_device(n, (int)d, boxes, out);
   });
 }
 

@@ -200,7 +200,7 @@ static void release_streams(const StreamSet& r)
 
 // __constant__ tables (exp coefficients, truncation bounds) are per device and
 // h-independent: uploaded once per device and process.
-static void init_device_constants(cudaStream_t s)
+void init_device_constants(cudaStream_t s)
 {
   static std::mutex mu;
   static std::unordered_map<int, bool> done;

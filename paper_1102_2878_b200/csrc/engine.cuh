@@ -26,6 +26,7 @@ struct Stats {
                      prunes_finite_diff = 0, prunes_farfield = 0, prunes_direct_local = 0,
                      prunes_far_to_local = 0;
   int levels = 0;
+  unsigned long long pairs_covered = 0;  // sum of |Q| |R| over retired pairs (== |Q| |R_total|)
 };
 
 // Device milliseconds of the last compute batch, per phase (CUDA events on the
@@ -218,5 +219,13 @@ void pinned_free(void* p, size_t bytes);
 void init_exp_constants(cudaStream_t s);
 // Constant tables of the error bounds (traverse.cu).
 void init_truncation_tables(cudaStream_t s);
+// Both of the above, once per device and process (engine.cu).
+void init_device_constants(cudaStream_t s);
+// Test entries (traverse.cu): choose_best_method / the least orders and
+// box_distance_bounds_sq exactly as the traversal evaluates them on the device.
+//   args: n x 9 (nq, nr, sq, sr, h, tau, p_max, d, cost) -> out: n x 5 (kind, order, pf, pd, pt)
+void choose_methods_device(size_t n, const double* args, int* out);
+//   boxes: n x 4d (alo, ahi, blo, bhi) -> out: n x 2 (lo^2, hi^2)
+void box_bounds_device(size_t n, int d, const double* boxes, double* out);
 
 }  // namespace dfgtb

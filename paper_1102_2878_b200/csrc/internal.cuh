@@ -53,10 +53,10 @@ __device__ __forceinline__ void box_bounds(const double* alo, const double* ahi,
     const double g1 = blo[k] - ahi[k];
     const double g2 = alo[k] - bhi[k];
     const double l = 0.5 * (g1 + fabs(g1) + g2 + fabs(g2));
-    lo += l * l;
+    lo = __dadd_rn(lo, __dmul_rn(l, l));  // no FMA: bit-identical to the reference's sums
     const double u1 = bhi[k] - alo[k], u2 = ahi[k] - blo[k];
     const double u = u1 < u2 ? u2 : u1;
-    hi += u * u;
+    hi = __dadd_rn(hi, __dmul_rn(u, u));
   }
   lo2 = lo;
   hi2 = hi;

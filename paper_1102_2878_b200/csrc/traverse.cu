@@ -37,26 +37,32 @@ using namespace detail;
 namespace {
 
 // ------------------------------------------------------------------ truncation
-// Error bounds of truncation.cpp:40-81 in division-free form.  The reference tests
-//   bound(p) = count / (1-s)^(D*dpow) * S(p) <= tau,
-//   S(p) = sum_{k<D} C(D,k) a^k b^(D-k),
-// in increasing p (least_order, truncation.cpp:85-94).  (1-s) > 0 wherever a bound is
-// evaluated, so the test is count * S(p) <= tau * (1-s)^(D*dpow): the same decision
-// without the overflow of the prefactor (the reference's log-space fallback exists
-// only for that, truncation.cpp:46-52) and without one FP64 divide and square root
-// per candidate order.  1/sqrt(p!) and C(D,k) come from constant tables.
+// Error bounds of truncation.cpp:40-81.  The reference tests, in increasing p
+// (least_order, truncation.cpp:85-94),
+//   bound(p) = count / (1-s)^(D*dpow) * S(p) <= tau,   S(p) = sum_{k<D} C(D,k) a^k b^(D-k).
+// The fast test here is the division-free form count * S(p) <= tau * (1-s)^(D*dpow)
+// ((1-s) > 0 wherever a bound is evaluated) with b = r^p * (1/sqrt(p!)) from a table:
+// no FP64 divide per candidate order and no overflow of the prefactor.  Its result
+// can differ from the reference's only when the two sides agree to ~(D+4) ulp, so
+// within a relative margin of 1e-13 (or when tau (1-s)^n leaves the normal range) the
+// reference's own expression is evaluated instead (division by sqrt(p!), prefactor,
+// log-space fallback of truncation.cpp:46-52): the decisions are the reference's,
+// bit for bit.  The ratios are formed exactly as the reference forms them:
+// side / (2h) and side / (4h) are (side / h) * 0.5 and * 0.25 exactly.
 __constant__ double c_isf[16];        // 1 / sqrt(p!)
-__constant__ double c_binom[17][17];  // C(n, k)
+__constant__ double c_sf[16];         // sqrt(p!)      (sqrt_factorial, truncation.cpp:20-27)
+__constant__ double c_binom[17][17];  // C(n, k)       (binomial, truncation.cpp:11-18)
+constexpr double kTieMargin = 1e-13;
 
 __device__ __forceinline__ double d_ipow(double x, int n)
-{
+{  // int_pow, truncation.cpp:29-36
   double r = 1.0;
   for (int i = 0; i < n; ++i) r *= x;
   return r;
 }
 
 __device__ __forceinline__ double bound_sum_S(double a, double b, int dim)
-{  // sum_{k<dim} C(dim,k) a^k b^(dim-k)
+{  // sum_{k<dim} C(dim,k) a^k b^(dim-k), same operation order as truncation.cpp:43-45
   double bp[kMaxDim + 1];
   bp[0] = 1.0;
   for (int k = 1; k <= dim; ++k) bp[k] = bp[k - 1] * b;
@@ -68,16 +74,47 @@ __device__ __forceinline__ double bound_sum_S(double a, double b, int dim)
   return sum;
 }
 
+// bound_sum (truncation.cpp:40-54) exactly as the reference evaluates it: explicit
+// round-to-nearest products and sums (no FMA contraction, which the reference's x86-64
+// build does not do either).  Only the log-space branch (prefactor overflow, i.e.
+// 1 - s < ~1e-9) uses CUDA's log / exp / log1p, which may differ from glibc's by an ulp.
+__device__ __noinline__ double ref_bound_sum(double count, double s, int dpow, double a, double b,
+                                             int dim)
+{
+  double sum = 0.0;
+  for (int k = 0; k < dim; ++k)
+    sum = __dadd_rn(sum, __dmul_rn(__dmul_rn(c_binom[dim][k], d_ipow(a, k)), d_ipow(b, dim - k)));
+  const double prefactor = count / d_ipow(1.0 - s, dim * dpow);
+  double bound = __dmul_rn(prefactor, sum);
+  if (!isfinite(bound) && count > 0.0 && sum > 0.0)
+    bound = exp(__dadd_rn(__dsub_rn(log(count), __dmul_rn((double)(dim * dpow), log1p(-s))), log(sum)));
+  return bound;
+}
+
+// One candidate order: fast test, the reference's expression near a tie.
+__device__ __forceinline__ bool bound_ok(double count, double S, double thr, double tau, double s,
+                                         int dpow, double a, double b_exact, int dim)
+{
+  const double lhs = count * S;
+  if (thr > 1e-290) {
+    if (lhs <= thr * (1.0 - kTieMargin)) return true;
+    if (lhs > thr * (1.0 + kTieMargin)) return false;
+  }
+  return ref_bound_sum(count, s, dpow, a, b_exact, dim) <= tau;
+}
+
 // farfield_order / local_accum_order (truncation.cpp:98-112): least p <= pmax with
 // the Lemma 3/4 bound <= tau, 0 if none or ratio >= 1.
 __device__ int d_order_ff(double ratio, double count, double tau, int pmax, int dim)
 {
   if (ratio >= 1.0) return 0;
   const double thr = tau * d_ipow(1.0 - ratio, dim);
-  double rp = 1.0;
+  double rp = 1.0;  // int_pow(r, p): the same product sequence
   for (int p = 1; p <= pmax; ++p) {
     rp *= ratio;
-    if (count * bound_sum_S(1.0 - rp, rp * c_isf[p], dim) <= thr) return p;
+    if (bound_ok(count, bound_sum_S(1.0 - rp, rp * c_isf[p], dim), thr, tau, ratio, 1, 1.0 - rp,
+                 rp / c_sf[p], dim))
+      return p;
   }
   return 0;
 }
@@ -92,7 +129,9 @@ __device__ int d_order_f2l(double ratio, double count, double tau, int pmax, int
   for (int p = 1; p <= pmax; ++p) {
     sp *= s;
     const double a = (1.0 - sp) * (1.0 - sp);
-    if (count * bound_sum_S(a, sp * (2.0 - sp) * c_isf[p], dim) <= thr) return p;
+    if (bound_ok(count, bound_sum_S(a, sp * (2.0 - sp) * c_isf[p], dim), thr, tau, s, 2, a,
+                 sp * (2.0 - sp) / c_sf[p], dim))
+      return p;
   }
   return 0;
 }
@@ -101,13 +140,13 @@ __device__ int d_order_f2l(double ratio, double count, double tau, int pmax, int
 __device__ void dev_choose(double nq, double nr, double sq, double sr, double h, double tau,
                            int pmax, int dim, int cost, int& kind, int& order)
 {
-  const double i2h = 0.5 / h;  // one division per pair (ratios side / 2h, side / 4h)
-  const int pf = d_order_ff(sr * i2h, nr, tau, pmax, dim);
-  const int pd = d_order_ff(sq * i2h, nr, tau, pmax, dim);
-  const int pt = d_order_f2l((sq < sr ? sr : sq) * (0.5 * i2h), nr, tau, pmax, dim);
+  const double uq = sq / h, ur = sr / h;  // side / (2h) = (side / h) * 0.5 exactly
+  const int pf = d_order_ff(ur * 0.5, nr, tau, pmax, dim);
+  const int pd = d_order_ff(uq * 0.5, nr, tau, pmax, dim);
+  const int pt = d_order_f2l((uq < ur ? ur : uq) * 0.25, nr, tau, pmax, dim);
   const double D = (double)dim;
   double cf = CUDART_INF, cd = CUDART_INF, ct = CUDART_INF;
-  if (cost == 0) {  // exponential model; integer powers are exact
+  if (cost == 0) {  // exponential model; integer powers of D <= 5 are exact
     if (pf) cf = nq * d_ipow(D, pf + 1);
     if (pd) cd = nr * d_ipow(D, pd + 1);
     if (pt) ct = d_ipow(D, 2 * pt + 1);
@@ -129,7 +168,9 @@ __device__ void dev_choose(double nq, double nr, double sq, double sr, double h,
 // Device-resident traversal state: every kernel reads the frontier size here, so
 // the level loop needs no host round trip.  Capacities are checked before anything
 // is written; on overflow the loop stops and the host regrows the buffers and reruns.
-enum SlotStat { sPairs = 0, sFD, sF, sD, sT, sB, sKev, sNStat };
+// sCov: sum over retired pairs (FD, F, D, T, base case) of |Q| |R| -- every (q, r) pair
+// is retired exactly once, so it must equal |Q| |R_total| (CoverageProbe, tests/probes.hpp:13-44)
+enum SlotStat { sPairs = 0, sFD, sF, sD, sT, sB, sKev, sCov, sNStat };
 constexpr int kMaxLevels = 1024;
 constexpr int kNch = 4;               // chunks per CTA on big levels (cyclic deal)
 #ifndef DFGTB_CYCLIC_PAIRS
@@ -306,7 +347,7 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
   // pass 2: decisions
   double fd_dlo = 0.0, fd_const = 0.0, ret = 0.0;
   int nF = 0, nDT = 0, nT = 0, nB = 0, nFD = 0, slots = 0;
-  unsigned long long kev = 0;
+  unsigned long long kev = 0, cov = 0;
   for (int j = lane; j < len; j += W) {
     const int R = fr[off + j];
     const double kmax = a.pkmax[off + j], kmin = a.pkmin[off + j];
@@ -343,6 +384,7 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
         }
       }
     }
+    if (kind != kX) cov += (unsigned long long)a.Q.count[Q] * (unsigned long long)a.R.count[R];
     a.dec[off + j] = kind | (order << 8);
   }
   fd_dlo = group_sum<W>(fd_dlo);
@@ -355,6 +397,7 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
   nFD = group_sum_i<W>(nFD);
   slots = group_sum_i<W>(slots);
   kev = group_sum_i<W>(kev);
+  cov = group_sum_i<W>(cov);
   if (lane == 0 && valid) {
     const int ne = slots > 0 ? (qleaf ? 1 : 2) : 0;
     a.cnt[e] = Cnt{ ne, ne * slots, nF, nDT, nT, nB, nFD };
@@ -372,6 +415,7 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
     if (nT) atomicAdd(ss + sT, (unsigned long long)nT);
     if (nB) atomicAdd(ss + sB, (unsigned long long)nB);
     if (kev) atomicAdd(ss + sKev, kev);
+    if (cov) atomicAdd(ss + sCov, cov);
   }
 }
 
@@ -751,11 +795,12 @@ __device__ __forceinline__ void entries_reduce(const TravArgs& a, int cur, int K
     const unsigned long long nqi = (unsigned long long)a.Q.count[Q];
     double fd_dlo = 0.0, fd_const = 0.0, ret = 0.0;
     int nF = 0, nDT = 0, nT = 0, nB = 0, nFD = 0, slots = 0;
-    unsigned long long kev = 0;
+    unsigned long long kev = 0, cov = 0;
     for (int j = lane; j < len; j += 32) {
       const int R = a.fr[cur][off + j];
       const int kind = a.dec[off + j] & 0xff;
       const int cr = a.R.count[R];
+      if (kind != kX) cov += nqi * (unsigned long long)cr;
       const double nr = (double)cr;
       const double kmin = a.pkmin[off + j];
       const double dlo = nr * kmin;
@@ -788,6 +833,7 @@ __device__ __forceinline__ void entries_reduce(const TravArgs& a, int cur, int K
     nFD = group_sum_i<32>(nFD);
     slots = group_sum_i<32>(slots);
     kev = group_sum_i<32>(kev);
+    cov = group_sum_i<32>(cov);
     if (lane == 0) {
       const int ne = slots > 0 ? (qleaf ? 1 : 2) : 0;
       a.cnt[e] = Cnt{ ne, ne * slots, nF, nDT, nT, nB, nFD };
@@ -805,6 +851,7 @@ __device__ __forceinline__ void entries_reduce(const TravArgs& a, int cur, int K
       if (nT) atomicAdd(ss + sT, (unsigned long long)nT);
       if (nB) atomicAdd(ss + sB, (unsigned long long)nB);
       if (kev) atomicAdd(ss + sKev, kev);
+      if (cov) atomicAdd(ss + sCov, cov);
     }
   }
 }
@@ -1082,11 +1129,12 @@ void launch_level(const TravArgs& a, int D, cudaStream_t s, cudaGraphConditional
 
 void init_truncation_tables(cudaStream_t s)
 {
-  double isf[16], bin[17][17];
+  double isf[16], sf[16], bin[17][17];
   double f = 1.0;
   for (int p = 0; p < 16; ++p) {
-    if (p > 1) f *= p;
-    isf[p] = 1.0 / std::sqrt(f);
+    if (p > 1) f *= p;  // sqrt_factorial, truncation.cpp:20-27
+    sf[p] = std::sqrt(f);
+    isf[p] = 1.0 / sf[p];
   }
   for (int n = 0; n <= 16; ++n)
     for (int k = 0; k <= 16; ++k) {
@@ -1095,7 +1143,62 @@ void init_truncation_tables(cudaStream_t s)
       bin[n][k] = b;
     }
   CK(cudaMemcpyToSymbolAsync(c_isf, isf, sizeof(isf), 0, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyToSymbolAsync(c_sf, sf, sizeof(sf), 0, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyToSymbolAsync(c_binom, bin, sizeof(bin), 0, cudaMemcpyHostToDevice, s));
+}
+
+// ------------------------------------------------------------------ test entries
+namespace {
+__global__ void k_choose_test(int n, const double* args, int* out)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* a = args + (size_t)9 * i;
+  const int pmax = (int)a[6], dim = (int)a[7], cost = (int)a[8];
+  int kind = kE, order = 0;
+  dev_choose(a[0], a[1], a[2], a[3], a[4], a[5], pmax, dim, cost, kind, order);
+  const double uq = a[2] / a[4], ur = a[3] / a[4];
+  int* o = out + (size_t)5 * i;
+  o[0] = kind;
+  o[1] = order;
+  o[2] = d_order_ff(ur * 0.5, a[1], a[5], pmax, dim);
+  o[3] = d_order_ff(uq * 0.5, a[1], a[5], pmax, dim);
+  o[4] = d_order_f2l((uq < ur ? ur : uq) * 0.25, a[1], a[5], pmax, dim);
+}
+
+__global__ void k_box_test(int n, int d, const double* boxes, double* out)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* b = boxes + (size_t)4 * d * i;
+  box_bounds<0>(b, b + d, b + 2 * d, b + 3 * d, d, out[2 * i], out[2 * i + 1]);
+}
+}  // namespace
+
+void choose_methods_device(size_t n, const double* args, int* out)
+{
+  if (n == 0) return;
+  init_device_constants(0);
+  DevBuf<double> da;
+  DevBuf<int> dout;
+  da.reserve(9 * n);
+  dout.reserve(5 * n);
+  CK(cudaMemcpy(da.p, args, sizeof(double) * 9 * n, cudaMemcpyHostToDevice));
+  k_choose_test<<<ceil_div((long long)n, 128), 128>>>((int)n, da.p, dout.p);
+  CK_LAUNCH();
+  CK(cudaMemcpy(out, dout.p, sizeof(int) * 5 * n, cudaMemcpyDeviceToHost));
+}
+
+void box_bounds_device(size_t n, int d, const double* boxes, double* out)
+{
+  if (n == 0) return;
+  DevBuf<double> db, dout;
+  db.reserve(4 * (size_t)d * n);
+  dout.reserve(2 * n);
+  CK(cudaMemcpy(db.p, boxes, sizeof(double) * 4 * d * n, cudaMemcpyHostToDevice));
+  k_box_test<<<ceil_div((long long)n, 128), 128>>>((int)n, d, db.p, dout.p);
+  CK_LAUNCH();
+  CK(cudaMemcpy(out, dout.p, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost));
 }
 
 void Engine::destroy_graph()
@@ -1422,6 +1525,7 @@ bool Engine::traverse_finish()
     st.prunes_far_to_local = ss[sT];
     st.base_cases = ss[sB];
     st.kernel_evaluations = 2ull * ss[sPairs] + ss[sKev];
+    st.pairs_covered = ss[sCov];
   }
   nF_ = hs->nF;
   nDT_ = hs->nDT;

@@ -100,6 +100,7 @@ class TraversalStats:
     prunes_direct_local: int = 0
     prunes_far_to_local: int = 0
     levels: int = 0
+    pairs_covered: int = 0  # sum of |Q||R| over retired node pairs (== n_queries * n_refs)
 
 
 @dataclass
@@ -252,10 +253,20 @@ class DualTreeEngine:
         return row
 
     def sweep(self, scales: Sequence[float], base_h: float, sqrt2: bool = False):
+        """bandwidth_sweep (cv.cpp:141-182) for both scores, every h and conv h in one
+        batched GPU traversal.  Rows' `seconds` are shares of the batch's device time."""
         sc = np.ascontiguousarray(scales, dtype=np.float64)
         rows = (_capi.CvRow * len(sc))()
         check(lib.dfgtb_sweep(self._h, _dp(sc), len(sc), float(base_h), int(sqrt2), rows))
         return list(rows)
+
+    @staticmethod
+    def best(rows) -> tuple[int, int]:
+        """h* of a sweep: (argmax lk_score, argmin ls_score), first index on ties."""
+        arr = (_capi.CvRow * len(rows))(*rows)
+        ik, il = C.c_size_t(), C.c_size_t()
+        check(lib.dfgtb_sweep_best(arr, len(rows), C.byref(ik), C.byref(il)))
+        return int(ik.value), int(il.value)
 
 
 # ----------------------------------------------------------------- free functions
@@ -405,10 +416,19 @@ def pilot_bandwidth(refs) -> float:
     n, d = r.shape
     if n < 2:
         raise ValueError("pilot bandwidth requires at least 2 points")
-    sigma = float(np.mean(np.std(r, axis=0, ddof=1)))
+    # the reference's summation order (sequential sums per dimension, two passes):
+    # cumsum is a left-to-right sum, so h is bit-identical to cv.cpp's
+    sigma_sum = 0.0
+    for k in range(d):
+        col = r[:, k]
+        mean = float(np.cumsum(col)[-1]) / n
+        t = col - mean
+        var = float(np.cumsum(t * t)[-1])
+        sigma_sum += math.sqrt(var / (n - 1))
+    sigma = sigma_sum / d
     if not sigma > 0.0:
         raise ValueError("pilot bandwidth undefined for zero-variance data")
-    return sigma * n ** (-1.0 / (d + 4.0))
+    return sigma * math.pow(float(n), -1.0 / (d + 4.0))
 
 
 @dataclass
