@@ -59,6 +59,7 @@ typedef struct dfgtb_stats {
 typedef struct dfgtb_timings {
   float tree_ms, traverse_ms, moments_ms, local_ms, base_ms, farfield_ms, final_ms, total_ms;
   float base_f32_ms, base_fp64_ms; /* base_ms split: FP32 kernel | FP64 kernel */
+  float moments_build_ms;           /* the handle's one-time unscaled moments (K2/K3) */
 } dfgtb_timings;
 
 /* One bandwidth of a CV sweep (CvRow, cv.hpp:49-56 + ScoreResult cv.hpp:25-32). */

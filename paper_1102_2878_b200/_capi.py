@@ -38,7 +38,7 @@ class Stats(C.Structure):
 class Timings(C.Structure):
     _fields_ = [(n, C.c_float) for n in (
         "tree_ms", "traverse_ms", "moments_ms", "local_ms", "base_ms", "farfield_ms", "final_ms",
-        "total_ms", "base_f32_ms", "base_fp64_ms")]
+        "total_ms", "base_f32_ms", "base_fp64_ms", "moments_build_ms")]
 
     def as_dict(self):
         return {n: float(getattr(self, n)) for n, _ in self._fields_}

@@ -237,6 +237,7 @@ int dfgtb_last_timings(dfgtb_handle* h, dfgtb_timings* t)
     t->total_ms = s.total_ms;
     t->base_f32_ms = s.base_f32_ms;
     t->base_fp64_ms = s.base_fp64_ms;
+    t->moments_build_ms = h->eng->moments_build_ms();
   });
 }
 

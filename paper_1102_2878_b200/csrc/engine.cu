@@ -156,7 +156,7 @@ void pinned_free(void* p, size_t bytes)
 struct StreamSet {
   cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
   cudaEvent_t ev[14] = {}, fork = nullptr, join = nullptr, fork3 = nullptr, join3 = nullptr,
-              legacy = nullptr;
+              legacy = nullptr, mom0 = nullptr, mom1 = nullptr;
 };
 static std::unordered_map<int, std::vector<StreamSet>>& stream_pool()
 {
@@ -186,6 +186,8 @@ static StreamSet acquire_streams()
   CK(cudaEventCreateWithFlags(&r.fork3, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&r.join3, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&r.legacy, cudaEventDisableTiming));
+  CK(cudaEventCreate(&r.mom0));
+  CK(cudaEventCreate(&r.mom1));
   for (auto& e : r.ev) CK(cudaEventCreate(&e));
   return r;
 }
@@ -257,6 +259,8 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
     fork3_ = ss.fork3;
     join3_ = ss.join3;
     legacy_ev_ = ss.legacy;
+    mom_ev_[0] = ss.mom0;
+    mom_ev_[1] = ss.mom1;
   }
   x_.reserve(n * d);
   if (on_device) wait_legacy_stream();  // the caller's producer of refs
@@ -266,7 +270,7 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
   init_device_constants(s_);
   CK(cudaEventRecord(ev_[0], s_));
   build_tree(rt_, x_.p, (int)n, D_, cfg.leaf_threshold, s_);
-  CK(cudaEventRecord(ev_[1], s_));  // tree_ms: upload + tree (the moments overlap later work)
+  CK(cudaEventRecord(ev_[1], s_));  // tree_ms: the tree build (the upload precedes ev_[0])
   if (std::getenv("DFGTB_TRACE")) {
     CK(cudaEventRecord(ev_[2], s_));
     CK(cudaEventSynchronize(ev_[2]));
@@ -309,6 +313,8 @@ Engine::~Engine()
     ss.fork3 = fork3_;
     ss.join3 = join3_;
     ss.legacy = legacy_ev_;
+    ss.mom0 = mom_ev_[0];
+    ss.mom1 = mom_ev_[1];
     release_streams(ss);  // pooled for the next engine on this device
   }
 }
@@ -387,6 +393,16 @@ void Engine::compute_batch(const double* d_queries, size_t nq, const double* h, 
     leaves_src_ = 0;
   }
   run_phases(*qt, h, nb, d_out);
+}
+
+float Engine::moments_build_ms()
+{
+  if (!eager_) return 0.f;
+  DeviceGuard dg(dev_);
+  float ms = 0.f;
+  CK(cudaEventSynchronize(mom_ev_[1]));
+  CK(cudaEventElapsedTime(&ms, mom_ev_[0], mom_ev_[1]));
+  return ms;
 }
 
 void Engine::compute_host(const double* h_queries, size_t nq, double h, double* h_out)

@@ -88,6 +88,8 @@ public:
 
   const Stats& last_stats(int slot = 0) const { return slot_stats_[slot]; }
   const Timings& last_timings() const { return tim_; }
+  // device time of the engine's one-time moment kernels (K2/K3; waits for them)
+  float moments_build_ms();
   const DevTree& ref_tree() const { return rt_; }
   int p_max() const { return ser_.pmax; }
   bool mufu_exp() const { return mufu_; }
@@ -169,7 +171,8 @@ private:
   cudaStream_t s3_ = nullptr;  // the FP64 base-case kernel beside the FP32 one
   cudaEvent_t fork3_ = nullptr, join3_ = nullptr;
   cudaEvent_t fork_ = nullptr, join_ = nullptr;
-  cudaEvent_t legacy_ev_ = nullptr;  // orders s_ after the legacy stream (wait_legacy_stream)
+  cudaEvent_t legacy_ev_ = nullptr;
+  cudaEvent_t mom_ev_[2] = { nullptr, nullptr };  // around the eager moment kernels (s2_)  // orders s_ after the legacy stream (wait_legacy_stream)
   std::vector<Stats> slot_stats_;
   Timings tim_;
   long long nF_ = 0, nDT_ = 0, nB_ = 0;

@@ -2181,6 +2181,7 @@ void Engine::eager_moments()
   CK(cudaMemcpyAsync(ds.p, cstart.data(), sizeof(int) * nch, cudaMemcpyHostToDevice, s2));
   CK(cudaMemcpyAsync(dof.p, coff.data(), sizeof(int) * (K + 1), cudaMemcpyHostToDevice, s2));
   Mt_.reserve((size_t)K * T);
+  CK(cudaEventRecord(mom_ev_[0], s2));
   const DevSeries g = dev_series();
   const int smem = kMomChunk * D_ * ser_.pmax * (int)sizeof(double);
   const int pm = ser_.pmax;
@@ -2198,6 +2199,7 @@ void Engine::eager_moments()
   CK_LAUNCH();
   k_moment_reduce<<<std::min(K, 148 * 8), kMomRedThreads, 0, s2>>>(g, K, dof.p, part.p, Mt_.p);
   CK_LAUNCH();
+  CK(cudaEventRecord(mom_ev_[1], s2));
 }
 
 void Engine::setup_leaves(const DevTree& t)

@@ -56,20 +56,26 @@ class ShardedRow:
 def sharded_sweep(refs: np.ndarray, scales: Sequence[float], base_h: float,
                   sums_for: Callable[[np.ndarray, Sequence[float]], np.ndarray],
                   rank: int, world: int, allreduce: Callable[[np.ndarray], np.ndarray],
-                  sqrt2: bool = False) -> list[ShardedRow]:
+                  sqrt2: bool = False, order: np.ndarray | None = None) -> list[ShardedRow]:
     """CV sweep with the queries sharded across ranks.
 
     sums_for(queries, hs) -> (len(hs), len(queries)) kernel sums against ALL of
     `refs` (on a GPU: DualTreeEngine(refs).compute_batch(queries, hs)).  allreduce
     sums a float64 array over ranks (on GPUs: NCCL all_reduce).  Every rank returns
-    the same rows."""
+    the same rows.
+
+    order (optional): a permutation of the points -- e.g. the reference kd-tree's
+    `perm` -- whose contiguous ranges become the shards, so every rank's queries are
+    a few spatially compact subtrees (a smaller query tree and fewer node pairs than
+    a random slice of the input order)."""
     n, d = refs.shape
     lo, hi = shard_range(n, rank, world)
+    mine = slice(lo, hi) if order is None else np.asarray(order)[lo:hi]
     hs = [s * base_h for s in scales]
     cs = [(math.sqrt(2.0) if sqrt2 else 2.0) * h for h in hs]
     part = np.zeros((len(hs), 3))
     if hi > lo:
-        g = sums_for(refs[lo:hi], list(hs) + list(cs))
+        g = sums_for(refs[mine], list(hs) + list(cs))
         for k, (h, c) in enumerate(zip(hs, cs)):
             part[k] = cv_partials(g[k], g[len(hs) + k], n, d, h, c)
     tot = allreduce(part.ravel()).reshape(part.shape)
