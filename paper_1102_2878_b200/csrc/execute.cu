@@ -1075,7 +1075,6 @@ template <int DT>
 struct FPt {
   static constexpr int DF = DT <= 4 ? 4 : 8;  // floats per point (coordinates, pad)
   static constexpr int DP = PtLoad<DT>::DP;
-  static constexpr int PL = 256 * 4;  // floats per float4 plane of the stream (F32Geo::RMAX)
   struct Raw {
     double x[DT];
   };
@@ -1093,34 +1092,6 @@ struct FPt {
     for (int d = 0; d < DT; ++d) v[d] = (float)(p.x[d] - c[d]);
 #pragma unroll
     for (int d = DT; d < DF; ++d) v[d] = 0.f;
-  }
-  // stream point j2 (plane k holds floats 4k..4k+3: LDS.128 per lane, conflict-free)
-  __device__ __forceinline__ static void store(const Raw& p, const double* c, float* dst, int j2)
-  {
-    float v[DF];
-    centred(p, c, v);
-#pragma unroll
-    for (int k = 0; k < DF / 4; ++k)
-      reinterpret_cast<float4*>(dst + k * PL)[j2] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-  }
-  __device__ __forceinline__ static void load(const float* base, int j, float (&v)[DF])
-  {
-#pragma unroll
-    for (int k = 0; k < DF / 4; ++k) {
-      const float4 t = reinterpret_cast<const float4*>(base + k * PL)[j];
-      v[4 * k] = t.x;
-      v[4 * k + 1] = t.y;
-      v[4 * k + 2] = t.z;
-      v[4 * k + 3] = t.w;
-    }
-  }
-  // query tile (broadcast reads): point-major, stride DF
-  __device__ __forceinline__ static void stage_q(const double* src, int j, const double* c, float* dst)
-  {
-    float v[DF];
-    centred(load_raw(src, j), c, v);
-#pragma unroll
-    for (int k = 0; k < DF; ++k) dst[(size_t)j * DF + k] = v[k];
   }
 };
 
@@ -1443,54 +1414,266 @@ __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
   }
 }
 
-// FP32 base case kernel (tasks whose every leaf pair carries order bit 2): small code
-// and few registers, so more warps per SM hide the staging loads.
-template <int DT>
-struct F32Geo {
-  static constexpr int RMAX = 256;  // stream tile (points)
-  static constexpr int WARPS = 4;
-  static constexpr int DF = FPt<DT>::DF;
-  static constexpr int FLOATS = RMAX * DF + 32 * DF;  // stream | query tile
-};
-#ifndef DFGTB_BF32_MINB
-#define DFGTB_BF32_MINB 6
+// ---- packed FP32x2 base case (Blackwell FADD2 / FMUL2 / FFMA2) ----------------------
+// Lanes own reference points (P per pass, registers); the warp walks the task's queries
+// in PAIRS: one packed instruction forms a coordinate difference for two queries against
+// one point, so per two (q, r) pairs the loop issues D FADD2 + 1 FMUL2 + (D - 1) FFMA2 +
+// 2 MUFU.EX2 + 1 FADD2 (accumulate): 3.5 issue slots per pair at D = 2 against the MUFU
+// rate's budget of 8.  The arithmetic per term is exactly FPt's (q~ + (-r~) = q~ - r~;
+// FMUL then FFMA, both round-to-nearest), so kF32Charge's derivation is unchanged; each
+// lane's accumulator of a query sums <= RMAX / 32 = 8 terms per tile as before.
+//   points: negated centred FP32 coordinates, each stored twice ((-x, -x), (-y, -y), ..),
+//           PF floats per point in float4 planes (conflict-free LDS.128 per lane);
+//   queries: pair k, dimension d at float2 index k * DT + d = (q_2k[d], q_2k+1[d]);
+//            padding queries (>= qc) sit at 1e18 (their terms are 0, their sums unused).
+#ifndef DFGTB_F32_SMEM_REDUCE
+#define DFGTB_F32_SMEM_REDUCE 0  // measured: the shuffle transpose is as fast
+#endif
+#ifndef DFGTB_F32_KB
+#define DFGTB_F32_KB 2
 #endif
 template <int DT>
+struct F2Pt {
+  static constexpr int PF = (2 * DT + 3) / 4 * 4;  // floats per point
+  static constexpr int NPL = PF / 4;               // float4 planes
+  static constexpr int RMAX = 256;
+  static constexpr int PL = RMAX * 4;              // floats per plane
+  static constexpr int P = DT <= 3 ? 4 : 2;        // points per lane per pass
+  static constexpr int QF = 32 * DT;               // floats of the query tile
+  static constexpr int FLOATS = RMAX * PF + QF;
+  __device__ __forceinline__ static void store(const typename FPt<DT>::Raw& p, const double* c, float* dst, int j)
+  {
+    float v[PF];
+#pragma unroll
+    for (int d = 0; d < DT; ++d) v[2 * d] = v[2 * d + 1] = -(float)(p.x[d] - c[d]);
+#pragma unroll
+    for (int k = 2 * DT; k < PF; ++k) v[k] = 0.f;
+#pragma unroll
+    for (int k = 0; k < NPL; ++k)
+      reinterpret_cast<float4*>(dst + k * PL)[j] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  }
+  __device__ __forceinline__ static void load(const float* base, int j, float2 (&r)[DT])
+  {
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+      const float4 t = reinterpret_cast<const float4*>(base + k * PL)[j];
+      if (2 * k < DT) r[2 * k] = make_float2(t.x, t.y);
+      if (2 * k + 1 < DT) r[2 * k + 1] = make_float2(t.z, t.w);
+    }
+  }
+  // query `lane` of the chunk (lane >= qc: padding) into the pair layout
+  __device__ __forceinline__ static void stage_q(const double* src, int lane, int qc, const double* c, float* qs)
+  {
+    float v[DT];
+    if (lane < qc) {
+      const typename FPt<DT>::Raw p = FPt<DT>::load_raw(src, lane);
+#pragma unroll
+      for (int d = 0; d < DT; ++d) v[d] = (float)(p.x[d] - c[d]);
+    } else {
+#pragma unroll
+      for (int d = 0; d < DT; ++d) v[d] = 1e18f;
+    }
+#pragma unroll
+    for (int d = 0; d < DT; ++d) qs[((lane >> 1) * DT + d) * 2 + (lane & 1)] = v[d];
+  }
+};
+
+// One tile of n <= RMAX points against the chunk's qc queries; adds each query's tile sum
+// to qsum (FP64).
+template <int DT>
+__device__ __forceinline__ void base_tile_f32x2(const float* rs, int n, const float* qs, double* qsum, int qc,
+                                                int lane)
+{
+  constexpr int P = F2Pt<DT>::P;
+  constexpr int KB = DFGTB_F32_KB;  // query pairs per branch-free block
+  const float2* q2 = reinterpret_cast<const float2*>(qs);
+  const int np = (qc + 1) >> 1;
+  float2 acc[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc[k] = make_float2(0.f, 0.f);
+  for (int c = 0; c < n; c += 32 * P) {
+    float2 r[P][DT];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int j = c + 32 * p + lane;
+      if (j < n) F2Pt<DT>::load(rs, j, r[p]);
+      else
+#pragma unroll
+        for (int d = 0; d < DT; ++d) r[p][d] = make_float2(-1e18f, -1e18f);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; k += KB) {
+      if (k < np) {  // KB query pairs per block, branch-free inside (padding queries add 0)
+#pragma unroll
+        for (int kk = 0; kk < KB; ++kk) {
+          float2 q[DT];
+#pragma unroll
+          for (int d = 0; d < DT; ++d) q[d] = q2[(k + kk) * DT + d];
+          float2 e[P];
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            float2 a = __fadd2_rn(q[0], r[p][0]);
+            float2 z = __fmul2_rn(a, a);
+#pragma unroll
+            for (int d = 1; d < DT; ++d) {
+              a = __fadd2_rn(q[d], r[p][d]);
+              z = __ffma2_rn(a, a, z);
+            }
+            e[p] = make_float2(ex2_ftz(-z.x), ex2_ftz(-z.y));
+          }
+          // the P terms by a fixed tree, then into the accumulator
+#pragma unroll
+          for (int w = P / 2; w >= 1; w >>= 1)
+#pragma unroll
+            for (int p = 0; p < w; ++p) e[p] = __fadd2_rn(e[p], e[p + w]);
+          acc[k + kk] = __fadd2_rn(acc[k + kk], e[0]);
+        }
+      }
+    }
+  }
+#if DFGTB_F32_SMEM_REDUCE
+  // transpose through shared memory (the point tile is free again after the passes):
+  // lane l writes its 32 partials as row l, lane q sums column q by a fixed 5-level tree
+  // (XOR-swizzled columns: both accesses are bank-conflict free)
+  __syncwarp();
+  float* tr = const_cast<float*>(rs);  // 32 x 32 floats
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    tr[lane * 32 + ((2 * k) ^ lane)] = acc[k].x;
+    tr[lane * 32 + ((2 * k + 1) ^ lane)] = acc[k].y;
+  }
+  __syncwarp();
+  float c32[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) c32[l] = tr[l * 32 + (lane ^ l)];
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1)
+#pragma unroll
+    for (int l = 0; l < w; ++l) c32[l] += c32[l + w];
+  __syncwarp();
+  if (lane < qc) qsum[lane] += (double)c32[0];
+#else
+  float a32[32];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    a32[2 * k] = acc[k].x;
+    a32[2 * k + 1] = acc[k].y;
+  }
+  const float v = transpose_reduce<32, 5>(a32, lane);  // lane l: query l's tile sum
+  if (lane < qc) qsum[lane] += (double)v;
+#endif
+}
+
+// FP32 base case kernel (tasks whose every leaf pair carries order bit 2).
+// A base-case task's metadata (from its packed list record).
+template <int DT>
+struct TaskMeta {
+  int w, key, item0, nit, q0;
+  int2 rc;         // lane < nit: item lane's record
+  int qcount, qb;  // query leaf count and first position
+  double cen[DT];  // query leaf's box centre
+  double s;        // slot scale
+};
+
+template <int DT>
+__device__ __forceinline__ TaskMeta<DT> fetch_meta(const int4& r, bool ok, TreeView Q, int K, const int2* rec,
+                                                   SlotView sv, int lane)
+{
+  TaskMeta<DT> m;
+  m.w = r.w;
+  m.key = r.x;
+  m.item0 = r.y;
+  m.nit = r.z & 63;
+  m.q0 = (r.z >> 6) << 5;
+  const int slot = ok ? r.x / K : 0, leaf = ok ? r.x - slot * K : 0;
+  m.rc = ok && lane < m.nit ? rec[m.item0 + lane] : make_int2(0, 0);
+  m.qcount = ok ? Q.count[leaf] : 0;
+  m.qb = ok ? Q.begin[leaf] : 0;
+#pragma unroll
+  for (int d = 0; d < DT; ++d) m.cen[d] = ok ? Q.cen[(size_t)leaf * DT + d] : 0.0;
+  m.s = ok ? sv.s[slot] : 0.0;
+  return m;
+}
+
+// TaskView from prefetched metadata (same fields as task_view, no memory access).
+__device__ __forceinline__ TaskView task_view_m(int key, int K, int nit, int q0, int2 rc, int qcount, int qb, int lane)
+{
+  TaskView v;
+  v.slot = key / K;
+  v.leaf = key - v.slot * K;
+  v.nit = nit;
+  v.rc = rc;
+  v.qc = min(32, qcount - q0);
+  v.qb = qb;
+  const int cnt = v.rc.y & 0x0FFFFFFF;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < kTaskItems; o <<= 1) {
+    const int x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  v.total = __shfl_sync(0xffffffffu, incl, kTaskItems - 1);
+  v.sk = incl - cnt;
+  v.okk = v.rc.x - v.sk;
+  return v;
+}
+
+template <int DT>
+struct F32Geo {
+  static constexpr int RMAX = F2Pt<DT>::RMAX;  // stream tile (points)
+  static constexpr int WARPS = 4;
+  static constexpr int FLOATS = F2Pt<DT>::FLOATS;  // stream | query tile
+};
+#ifndef DFGTB_BF32_MINB
+#define DFGTB_BF32_MINB 5
+#endif
+// Tasks come from the packed list (one 16-byte record per task; measured: prefetching
+// the next task's metadata a task ahead gains nothing -- the MUFU pipe, not the fetch
+// chain, bounds this kernel).
+template <int DT>
 __global__ void __launch_bounds__(F32Geo<DT>::WARPS * 32, DFGTB_BF32_MINB)
-  k_base_f32(TreeView Q, int K, const BTask* tasks, const int* tlist, const int* ntl, const int2* rec,
-             const double* xq, const double* xr, int nq, int nr, double* part, int* next, const double* c0,
-             SlotView sv, double f)
+  k_base_f32(TreeView Q, int K, const int4* tl, const int* ntl, const int2* rec, const double* xq,
+             const double* xr, int nq, int nr, double* part, int* next, const double* c0, SlotView sv,
+             double f)
 {
   using Geo = F32Geo<DT>;
-  constexpr int DP = PtLoad<DT>::DP, RMAX = Geo::RMAX, DF = Geo::DF;
+  constexpr int DP = PtLoad<DT>::DP, RMAX = Geo::RMAX;
   const int nl = *ntl;
   extern __shared__ __align__(16) float fsm[];  // WARPS x FLOATS
   __shared__ double qsum_all[Geo::WARPS][32];
   __shared__ unsigned smask_all[Geo::WARPS][RMAX / 32];
   const int lane = threadIdx.x & 31;
   float* rs = fsm + (size_t)(threadIdx.x >> 5) * Geo::FLOATS;
-  float* qs = rs + RMAX * DF;
+  float* qs = rs + RMAX * F2Pt<DT>::PF;
   double* qsum = qsum_all[threadIdx.x >> 5];
   unsigned* smask = smask_all[threadIdx.x >> 5];
   for (int i = next_task(next, lane); i < nl;) {
-    const int w = tlist[i];
-    const BTask t = tasks[w];
+    const int4 r4 = tl[i];
     const int inext = next_task(next, lane);
-    const TaskView v = task_view(t, Q, K, rec, lane);
-    const double* qsrc = xq + ((size_t)v.slot * nq + v.qb + t.q0) * DP;
+    const TaskMeta<DT> mc = fetch_meta<DT>(r4, true, Q, K, rec, sv, lane);
+    const TaskView v = task_view_m(mc.key, K, mc.nit, mc.q0, mc.rc, mc.qcount, mc.qb, lane);
+    const double* qsrc = xq + ((size_t)v.slot * nq + v.qb + mc.q0) * DP;
     double cq[DT];  // centre = the query leaf's box centre, scaled like the points
-    const double sc = sv.s[v.slot] * f;
+    const double sc = mc.s * f;
 #pragma unroll
-    for (int d = 0; d < DT; ++d) cq[d] = (Q.cen[(size_t)v.leaf * DT + d] - c0[d]) * sc;
-    if (lane < v.qc) FPt<DT>::stage_q(qsrc, lane, cq, qs);
+    for (int d = 0; d < DT; ++d) cq[d] = (mc.cen[d] - c0[d]) * sc;
+    F2Pt<DT>::stage_q(qsrc, lane, v.qc, cq, qs);
     qsum[lane] = 0.0;
     const double* xrs = xr + (size_t)v.slot * nr * DP;
+#if defined(DFGTB_EXP_NOSTAGE)  // timing experiments only (results wrong)
+    for (int c0t = 0; c0t < v.total; c0t += RMAX) base_tile_f32x2<DT>(rs, min(RMAX, v.total - c0t), qs, qsum, v.qc, lane);
+#else
     stream_passes<RMAX, stage_batch(DT)>(
       smask, v.nit, v.sk, v.okk, v.total, lane, [&](int src) { return FPt<DT>::load_raw(xrs, src); },
-      [&](const typename FPt<DT>::Raw& p, int pos) { FPt<DT>::store(p, cq, rs, pos); },
-      [&](int n) { base_groups_f32<DT>(rs, n, qs, qsum, v.qc, lane); });
+      [&](const typename FPt<DT>::Raw& p, int pos) { F2Pt<DT>::store(p, cq, rs, pos); },
+      [&](int n) {
+#if !defined(DFGTB_EXP_NOCOMPUTE)
+        base_tile_f32x2<DT>(rs, n, qs, qsum, v.qc, lane);
+#endif
+      });
+#endif
     __syncwarp();
-    if (lane < v.qc) part[(size_t)w * 32 + lane] = qsum[lane];
+    if (lane < v.qc) part[(size_t)mc.w * 32 + lane] = qsum[lane];
     __syncwarp();
     i = inext;
   }
@@ -1502,7 +1685,8 @@ __global__ void __launch_bounds__(F32Geo<DT>::WARPS * 32, DFGTB_BF32_MINB)
 // writes its own partial sums.
 __global__ void k_task_split(const int* leaves, int nleaves, int nb, int K, const int* cntB,
                              const int* leaf_task, const int* leaf_runs, TreeView Q, int tcap,
-                             const int* tflag, int f32, int* listA, int* listB, int* cnt)
+                             const int* tflag, int f32, int* listA, int* listB, int* cnt,
+                             const BTask* tasks, int4* l4A, int4* l4B)
 {
   // one warp per (slot, leaf) key in key order, lanes over its tasks: the lists keep a
   // key's tasks together (the query tile and reference leaves stay hot in L1 / L2)
@@ -1528,8 +1712,20 @@ __global__ void k_task_split(const int* leaves, int nleaves, int nb, int K, cons
       }
       baseA = __shfl_sync(0xffffffffu, baseA, 0);
       baseB = __shfl_sync(0xffffffffu, baseB, 0);
-      if (a) listA[baseA + __popc(ma & below)] = w;
-      else if (in) listB[baseB + __popc(mb & below)] = w;
+      // packed copies {key, item0, nit | (q0 / 32) << 6, w}: the base kernels' task fetch
+      // is ONE 16-byte load (no index -> record chain)
+      int4 rec4 = make_int4(0, 0, 0, 0);
+      if (in) {
+        const BTask t = tasks[w];
+        rec4 = make_int4(t.key, t.item0, (t.item1 - t.item0) | ((t.q0 >> 5) << 6), w);
+      }
+      if (a) {
+        listA[baseA + __popc(ma & below)] = w;
+        l4A[baseA + __popc(ma & below)] = rec4;
+      } else if (in) {
+        listB[baseB + __popc(mb & below)] = w;
+        l4B[baseB + __popc(mb & below)] = rec4;
+      }
     }
   }
 }
@@ -2097,16 +2293,16 @@ void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int 
     CK_LAUNCH();
     CK(cudaEventRecord(cc.b1, cc.s3));
     CK(cudaEventRecord(cc.join3, cc.s3));
-    k_base_f32<DT><<<std::min(nsm * kConcF32, cap_grid), threadsA, smemA, s>>>(Q, K, tasks, listA, ws + 2, rec,
-                                                                               xq, xr, nq, nr, part, ws, c0, sv, f);
+    k_base_f32<DT><<<std::min(nsm * kConcF32, cap_grid), threadsA, smemA, s>>>(
+      Q, K, reinterpret_cast<const int4*>(tasks + tcap), ws + 2, rec, xq, xr, nq, nr, part, ws, c0, sv, f);
     CK_LAUNCH();
     if (mid) CK(cudaEventRecord(mid, s));
     CK(cudaStreamWaitEvent(s, cc.join3, 0));
     return;
   }
   if (mufu & 2) {
-    k_base_f32<DT><<<std::min(gridA, cap_grid), threadsA, smemA, s>>>(Q, K, tasks, listA, ws + 2, rec, xq, xr,
-                                                                     nq, nr, part, ws, c0, sv, f);
+    k_base_f32<DT><<<std::min(gridA, cap_grid), threadsA, smemA, s>>>(
+      Q, K, reinterpret_cast<const int4*>(tasks + tcap), ws + 2, rec, xq, xr, nq, nr, part, ws, c0, sv, f);
     CK_LAUNCH();
   }
   if (mid) CK(cudaEventRecord(mid, s));
@@ -2390,7 +2586,7 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
   leaf_runs_.reserve(KB);
   const int rmax = base_rmax(D_);
   capTask_ = std::max(capTask_, std::max(4096, capB_ / 8));
-  tasks_.reserve((size_t)capTask_ * 4);
+  tasks_.reserve((size_t)capTask_ * 12);  // BTask array | packed list A | packed list B
   bnext_.reserve(8 + 3 * (size_t)capTask_);  // base-case lists and task flags (launch_base_t)
   CK(cudaMemsetAsync(bc_.p + 5, 0, sizeof(int), s));
   k_task_build<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p, sB_.p,
@@ -2401,7 +2597,10 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
   CK(cudaMemsetAsync(bnext_.p, 0, 8 * sizeof(int), s));
   k_task_split<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, leaf_task_.p, leaf_runs_.p, Q,
                                                   capTask_, bnext_.p + 8 + 2 * (size_t)capTask_, f32_ ? 1 : 0,
-                                                  bnext_.p + 8, bnext_.p + 8 + capTask_, bnext_.p + 2);
+                                                  bnext_.p + 8, bnext_.p + 8 + capTask_, bnext_.p + 2,
+                                                  reinterpret_cast<const BTask*>(tasks_.p),
+                                                  reinterpret_cast<int4*>(tasks_.p + (size_t)capTask_ * 4),
+                                                  reinterpret_cast<int4*>(tasks_.p + (size_t)capTask_ * 8));
   CK_LAUNCH();
   bpart_.reserve((size_t)capTask_ * 32);
   brec_.reserve((size_t)capB_ * 2 + 2);
@@ -2588,7 +2787,16 @@ __global__ void k_f32_terms(const double* q, const double* r, const double* c, i
   float vq[DF], vr[DF];
   FPt<DT>::centred(FPt<DT>::load_raw(q, i), cc, vq);
   FPt<DT>::centred(FPt<DT>::load_raw(r, i), cc, vr);
-  out[i] = (double)f32_term<DT>(vq, vr);
+  // exactly as base_tile_f32x2 forms it: q~ + (-r~) packed, FMUL2 then FFMA2
+  float2 a = __fadd2_rn(make_float2(vq[0], vq[0]), make_float2(-vr[0], -vr[0]));
+  float2 z = __fmul2_rn(a, a);
+#pragma unroll
+  for (int d = 1; d < DT; ++d) {
+    a = __fadd2_rn(make_float2(vq[d], vq[d]), make_float2(-vr[d], -vr[d]));
+    z = __ffma2_rn(a, a, z);
+  }
+  out[i] = (double)ex2_ftz(-z.x);
+  if (ex2_ftz(-z.y) != ex2_ftz(-z.x) || ex2_ftz(-z.x) != f32_term<DT>(vq, vr)) out[i] = -1.0;  // lanes agree
 }
 
 __global__ void k_ex2_peak(float* out, int iters)
