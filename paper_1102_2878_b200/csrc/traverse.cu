@@ -189,6 +189,8 @@ struct TravState {
   int done;                            // CTAs finished with their tile sum (unused)
   Cnt lvl;                             // totals of the current level
   unsigned long long sst[kMaxSlots][sNStat];  // per-slot TraversalStats
+  int ahead, atail, aptail, apending;          // asynchronous traversal (k_trav_async)
+  int xF, xDT, xB;                             // async: item array extents (>= nF.. : gaps)
 };
 
 struct TravArgs {
@@ -280,6 +282,7 @@ __global__ void k_trav_init(const __grid_constant__ TravArgs a)
     st.p[0] = nb;
     st.m[1] = st.p[1] = 0;
     st.nF = st.nDT = st.nB = 0;
+    st.xF = st.xDT = st.xB = 0;
     st.overflow = 0;
     st.levels = 0;
     st.done = 0;
@@ -316,7 +319,8 @@ __device__ __forceinline__ int base_flags(const TravArgs& a, double kmin, double
 // whole warp calls it (valid = false: a group without an entry this round).
 template <int DT, int W>
 __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st, int cur, int e,
-                                               int lane, bool valid)
+                                               int lane, bool valid,
+                                               unsigned long long (*sst)[sNStat] = nullptr)
 {
   const int* fr = a.fr[cur];
   const int D = DT ? DT : a.D;
@@ -407,7 +411,7 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
       a.L[(size_t)key * a.T] += fd_const;  // constant local term (order 1)
       if (a.Lord[key] < 1) a.Lord[key] = 1;
     }
-    unsigned long long* ss = st.sst[slot];
+    unsigned long long* ss = sst ? sst[slot] : st.sst[slot];
     atomicAdd(ss + sPairs, (unsigned long long)len);
     if (nFD) atomicAdd(ss + sFD, (unsigned long long)nFD);
     if (nF) atomicAdd(ss + sF, (unsigned long long)nF);
@@ -491,9 +495,12 @@ __global__ void __launch_bounds__(256) k_scan_local(const __grid_constant__ Trav
 // A group of W lanes, one frontier query node: its part of the next frontier and its
 // work items, at the offsets `o` (exclusive scan of the level's counts).  The whole
 // warp calls it (valid = false: no entry for this group).
+// cdec / cR (optional): the CTA's smem copies of the pairs' decisions and reference
+// nodes, indexed by pair - cP0 (PairCache).
 template <int W>
 __device__ __forceinline__ void emit_entry(const TravArgs& a, int K, int cur, int gF, int gDT,
-                                           int gB, int e, const Cnt& o, int lane, bool valid)
+                                           int gB, int e, const Cnt& o, int lane, bool valid,
+                                           const int* cdec = nullptr, const int* cR = nullptr, int cP0 = 0)
 {
   const int nxt = cur ^ 1;
   const int* fr = a.fr[cur];
@@ -532,10 +539,10 @@ __device__ __forceinline__ void emit_entry(const TravArgs& a, int K, int cur, in
     const int j = j0 + lane;
     int kind = kE, order = 0, R = 0;
     if (j < len) {
-      const int dcode = a.dec[off + j];
+      const int dcode = cdec ? cdec[off - cP0 + j] : a.dec[off + j];
       kind = dcode & 0xff;
       order = dcode >> 8;
-      R = fr[off + j];
+      R = cR ? cR[off - cP0 + j] : fr[off + j];
     }
     const bool rleaf = (j < len) ? a.R.left[R] < 0 : true;
     int tot;
@@ -628,16 +635,50 @@ constexpr int kPBlock = KPBLOCK;  // one CTA per SM: 32 warps to hide classify l
 
 template <int W>
 __device__ __forceinline__ void emit_range(const TravArgs& a, int K, int cur, int gF, int gDT, int gB,
-                                           int b0, int b1)
+                                           int b0, int b1, const int* cdec = nullptr, const int* cR = nullptr,
+                                           int cP0 = 0)
 {
   const int g = threadIdx.x / W, lane = threadIdx.x % W;
   constexpr int ng = kPBlock / W;
   for (int base = b0; base < b1; base += ng) {
     const int e = base + g;
     if (__any_sync(0xffffffffu, e < b1))
-      emit_entry<W>(a, K, cur, gF, gDT, gB, e, e < b1 ? a.cntoff[e] : Cnt{}, lane, e < b1);
+      emit_entry<W>(a, K, cur, gF, gDT, gB, e, e < b1 ? a.cntoff[e] : Cnt{}, lane, e < b1, cdec, cR, cP0);
   }
 }
+
+// ---- shared-memory pair cache of a level's CTA range ------------------------------
+// When a CTA's pair range [P0, P1) and entry range [e0, e1) fit, its pairs' reference
+// node, count, kernel bounds and decision, and its entries' key, offset, length and G^l
+// live in shared memory between the level's phases instead of round-tripping through
+// L2 (the phases are latency-bound chains of dependent loads).  Same arithmetic, same
+// lane-strided reduction order: identical results to the uncached phases.
+#ifndef DFGTB_TRAV_CACHE
+#define DFGTB_TRAV_CACHE 0  // measured: the level phases are not bound by these loads (0.80 vs 0.85 ms, cfg2)
+#endif
+constexpr bool kUseCache = DFGTB_TRAV_CACHE != 0;
+constexpr int kCacheP = 4096;  // pairs
+constexpr int kCacheE = 2048;  // entries
+constexpr int kCacheBytes = kCacheP * (8 + 8 + 4 + 4 + 4 + 4) + kCacheE * (8 + 4 + 4 + 4);
+struct PairCache {
+  double *kmax, *kmin, *glo;
+  int *R, *el, *cnt, *dec, *key, *off, *len;
+  __device__ static PairCache at(unsigned char* p)
+  {
+    PairCache c;
+    c.kmax = reinterpret_cast<double*>(p);
+    c.kmin = c.kmax + kCacheP;
+    c.glo = c.kmin + kCacheP;
+    c.R = reinterpret_cast<int*>(c.glo + kCacheE);
+    c.el = c.R + kCacheP;
+    c.cnt = c.el + kCacheP;
+    c.dec = c.cnt + kCacheP;
+    c.key = c.dec + kCacheP;
+    c.off = c.key + kCacheE;
+    c.len = c.off + kCacheE;
+    return c;
+  }
+};
 // ---- pair-balanced level phases of k_traverse -------------------------------------
 // CTA b owns the entries whose pair lists start in [b p / G, (b+1) p / G): a
 // contiguous entry range holding ~p/G pairs (entry sizes differ by orders of
@@ -856,6 +897,634 @@ __device__ __forceinline__ void entries_reduce(const TravArgs& a, int cur, int K
   }
 }
 
+// Cached phases (PairCache): the same computations as pairs_bounds / entries_glo /
+// pairs_decide / entries_reduce on the CTA's range [P0, P1) x [e0, e1).
+template <int DT>
+__device__ __forceinline__ void pairs_bounds_c(const TravArgs& a, int cur, int K, int P0, int P1, int e0,
+                                               int e1, const double* s_scale, const PairCache& c)
+{
+  const int D = DT ? DT : a.D;
+  for (int el = threadIdx.x; el < e1 - e0; el += kPBlock) {
+    c.key[el] = a.fq[cur][e0 + el];
+    c.off[el] = a.foff[cur][e0 + el] - P0;
+    c.len[el] = a.flen[cur][e0 + el];
+  }
+  for (int j = P0 + threadIdx.x; j < P1; j += kPBlock) {
+    const int e = a.pent[cur][j], R = a.fr[cur][j];
+    const int key = a.fq[cur][e];
+    const int slot = key / K, Q = key - slot * K;
+    double dl, du;
+    box_bounds<DT>(a.Q.lo + (size_t)Q * D, a.Q.hi + (size_t)Q * D, a.R.lo + (size_t)R * D,
+                   a.R.hi + (size_t)R * D, D, dl, du);
+    const double scale = s_scale[slot];
+    const int l = j - P0;
+    c.kmax[l] = exp(scale * dl);
+    c.kmin[l] = exp(scale * du);
+    c.R[l] = R;
+    c.el[l] = e - e0;
+    c.cnt[l] = a.R.count[R];
+  }
+}
+
+__device__ __forceinline__ void entries_glo_c(const TravArgs& a, int cur, int e0, int e1, const PairCache& c)
+{
+  const int lane = threadIdx.x & 31;
+  for (int el = threadIdx.x >> 5; el < e1 - e0; el += kPBlock / 32) {
+    const int off = c.off[el], len = c.len[el];
+    double part = 0.0;
+    for (int j = lane; j < len; j += 32) part += (double)c.cnt[off + j] * c.kmin[off + j];
+    const double g = a.fbase[cur][e0 + el] + group_sum<32>(part);
+    if (lane == 0) c.glo[el] = g;
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ void pairs_decide_c(const TravArgs& a, const TravState& st, int K, int P0, int P1,
+                                               const double* s_h, const PairCache& c)
+{
+  const int D = DT ? DT : a.D;
+  const double eps_nt = st.eps / st.ntot;
+  for (int l = threadIdx.x; l < P1 - P0; l += kPBlock) {
+    const int el = c.el[l];
+    const int key = c.key[el];
+    const int slot = key / K, Q = key - slot * K;
+    const int R = c.R[l];
+    const double kmax = c.kmax[l], kmin = c.kmin[l], glo = c.glo[el];
+    const double nr = (double)c.cnt[l];
+    const double tau = eps_nt * nr * glo;  // eps |R| G^l / N
+    int kind = kX, order = 0;
+    if (0.5 * nr * (kmax - kmin) <= tau) {  // kernel-difference prune, engine.cpp:137-148
+      kind = kFD;
+    } else {
+      if (a.series) {
+        dev_choose((double)a.Q.count[Q], nr, a.Q.side[Q], a.R.side[R], s_h[slot], tau, a.pmax, D, a.cost,
+                   kind, order);
+        if (kind == kE) kind = kX;
+      }
+      if (kind == kX && a.Q.left[Q] < 0 && a.R.left[R] < 0) {
+        kind = kB;
+        order = base_flags(a, kmin, glo, a.Q.side[Q], s_h[slot], D, a.Q.count[Q], Q);
+      }
+    }
+    c.dec[l] = kind | (order << 8);
+  }
+}
+
+__device__ __forceinline__ void entries_reduce_c(const TravArgs& a, int cur, int K, int e0, int e1,
+                                                 unsigned long long (*s_sst)[sNStat], const PairCache& c)
+{
+  const int lane = threadIdx.x & 31;
+  for (int el = threadIdx.x >> 5; el < e1 - e0; el += kPBlock / 32) {
+    const int e = e0 + el;
+    const int key = c.key[el];
+    const int slot = key / K, Q = key - slot * K;
+    const int off = c.off[el], len = c.len[el];
+    const bool qleaf = a.Q.left[Q] < 0;
+    const unsigned long long nqi = (unsigned long long)a.Q.count[Q];
+    double fd_dlo = 0.0, fd_const = 0.0, ret = 0.0;
+    int nF = 0, nDT = 0, nT = 0, nB = 0, nFD = 0, slots = 0;
+    unsigned long long kev = 0, cov = 0;
+    for (int j = lane; j < len; j += 32) {
+      const int kind = c.dec[off + j] & 0xff;
+      const int cr = c.cnt[off + j];
+      if (kind != kX) cov += nqi * (unsigned long long)cr;
+      const double nr = (double)cr;
+      const double kmin = c.kmin[off + j];
+      const double dlo = nr * kmin;
+      if (kind == kFD) {
+        fd_dlo += dlo;
+        fd_const += 0.5 * nr * (c.kmax[off + j] + kmin);
+        ++nFD;
+      } else if (kind == kX) {
+        slots += a.R.left[c.R[off + j]] < 0 ? 1 : 2;
+      } else if (kind == kB) {
+        ++nB;
+        kev += nqi * (unsigned long long)cr;
+        ret += dlo;
+      } else {
+        ret += dlo;
+        if (kind == kF) ++nF;
+        else {
+          ++nDT;
+          if (kind == kT) ++nT;
+        }
+      }
+    }
+    fd_dlo = group_sum<32>(fd_dlo);
+    fd_const = group_sum<32>(fd_const);
+    ret = group_sum<32>(ret);
+    nF = group_sum_i<32>(nF);
+    nDT = group_sum_i<32>(nDT);
+    nT = group_sum_i<32>(nT);
+    nB = group_sum_i<32>(nB);
+    nFD = group_sum_i<32>(nFD);
+    slots = group_sum_i<32>(slots);
+    kev = group_sum_i<32>(kev);
+    cov = group_sum_i<32>(cov);
+    if (lane == 0) {
+      const int ne = slots > 0 ? (qleaf ? 1 : 2) : 0;
+      a.cnt[e] = Cnt{ ne, ne * slots, nF, nDT, nT, nB, nFD };
+      a.childlen[e] = slots;
+      a.newbase[e] = a.fbase[cur][e] + (fd_dlo + ret);
+      if (nFD) {
+        a.L[(size_t)key * a.T] += fd_const;  // constant local term (order 1)
+        if (a.Lord[key] < 1) a.Lord[key] = 1;
+      }
+      unsigned long long* ss = s_sst[slot];
+      atomicAdd(ss + sPairs, (unsigned long long)len);
+      if (nFD) atomicAdd(ss + sFD, (unsigned long long)nFD);
+      if (nF) atomicAdd(ss + sF, (unsigned long long)nF);
+      if (nDT - nT) atomicAdd(ss + sD, (unsigned long long)(nDT - nT));
+      if (nT) atomicAdd(ss + sT, (unsigned long long)nT);
+      if (nB) atomicAdd(ss + sB, (unsigned long long)nB);
+      if (kev) atomicAdd(ss + sKev, kev);
+      if (cov) atomicAdd(ss + sCov, cov);
+    }
+  }
+}
+
+// ---- asynchronous (barrier-free) traversal ------------------------------------------
+// Every frontier entry (slot, query node, its live reference nodes, lower-bound base)
+// depends only on the entry that created it, so the levels need no grid-wide barrier:
+// warps claim entries from one global queue in creation order, wait for a claimed
+// entry to be published, classify it (classify_entry: the same arithmetic and lane-
+// strided reduction order as the level kernels), reserve space for its children and
+// work items with atomics, emit them (emit_entry), and publish the children.  A key
+// (slot, query node) has at most one live entry at a time (a query leaf's successive
+// entries form a chain, an internal node's entry creates its children's), so the per-
+// key rank counters, local-expansion constants and orders need no atomics, and every
+// item keeps the (key, rank) of the level-synchronous traversal: the counting sort that
+// follows makes the results bit-identical to it.  `pending` counts published-but-
+// unfinished entries; a warp waiting on a slot leaves when it drops to zero.
+// Counters, each on its own 128-byte line (kAsyncCtr ints apart): the hot atomics of
+// different roles never queue behind each other in one L2 slice.
+constexpr int kAsyncCtr = 32;
+enum AsyncCounter { acHead = 0, acTail, acPool, acF, acDT, acB, acPending, acRF, acRDT, acRB, acNum };
+struct AsyncQ {
+  int* ready;               // per queue slot: 1 published, 2 dead (its producer overflowed)
+  int* ctr;                 // acNum counters, kAsyncCtr ints apart
+  unsigned char* depth;     // per slot: level of the entry
+  unsigned long long* tr;   // DFGTB_ASYNC_TRACE builds: per slot {published, started, finished} (ns)
+  __device__ int* c(int k) const { return ctr + k * kAsyncCtr; }
+};
+constexpr int kAsyncChunkP = 1024;  // pairs reserved per pool refill of a warp
+constexpr int kAsyncChunkI = 128;   // items reserved per refill of a warp (each kind)
+constexpr int kAsyncBlock = 128;  // 4 warps, each with a WarpScratch
+constexpr long long kAsyncMaxPolls = 1ll << 23;
+#ifndef DFGTB_ASYNC_SLEEP
+#define DFGTB_ASYNC_SLEEP 256
+#endif
+constexpr unsigned kAsyncMaxSleep = DFGTB_ASYNC_SLEEP;  // ns, polling backoff cap  // a stuck wait reports an error, never hangs
+
+__device__ __forceinline__ int ld_acquire(const int* p)
+{
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v)
+{
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// One entry of the asynchronous traversal, fused (classify_entry + emit_entry with the
+// pairs' data in registers and the warp's shared scratch instead of global memory: the
+// entry's dependent memory round trips drop from ~12 to ~5).  Identical arithmetic and
+// reduction / emission order to classify_entry<DT, 32> + emit_entry<32>, so the items,
+// ranks, local constants and statistics are the same.  Entries with > kFuseMax pairs take
+// the unfused path.  Returns the children published (for `pending`).
+constexpr int kFuseMax = 256;
+constexpr int kAsyncSmem = 4 * (kFuseMax * (8 + 8 + 5 * 4));  // kAsyncBlock / 32 WarpScratch
+struct WarpScratch {  // per warp, kFuseMax pairs
+  double kmax[kFuseMax], kmin[kFuseMax];
+  int R[kFuseMax], cnt[kFuseMax], dec[kFuseMax], rl[kFuseMax], rr[kFuseMax];
+};
+// Per-warp reservation of a kind of output space: refills take chunks of the global
+// counter; an abandoned chunk tail is reported through `gap` (items: marked invalid).
+struct Reserve {
+  int pos = 0, end = 0;
+};
+__device__ __forceinline__ int reserve(Reserve& r, int need, int* ctr, int chunk, int cap, int lane,
+                                       int& gap0, int& gap1)
+{  // warp-uniform; returns the first position or -1 when the space is exhausted
+  gap0 = gap1 = 0;
+  if (need == 0) return 0;
+  if (r.pos + need > r.end) {
+    int b = 0;
+    const int n = max(chunk, need);
+    if (lane == 0) b = atomicAdd(ctr, n);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    gap0 = r.pos;
+    gap1 = r.end;
+    r.pos = b;
+    r.end = b + n;
+  }
+  if (r.pos + need > cap) return -1;
+  const int p = r.pos;
+  r.pos += need;
+  return p;
+}
+
+__device__ __forceinline__ void invalidate_items(Item* it, int p0, int p1, int cap, int lane)
+{
+  for (int k = p0 + lane; k < min(p1, cap); k += 32) it[k].key = -1;
+}
+
+template <int DT>
+__device__ __forceinline__ int async_entry(const TravArgs& a, TravState& st, const AsyncQ& q, int i, int lane,
+                                           WarpScratch& w, unsigned long long (*sst)[sNStat], Reserve& rp,
+                                           Reserve& rf, Reserve& rdt, Reserve& rb, int& totF, int& totDT,
+                                           int& totB, const double* s_h, const double* s_scale, int K)
+{
+  const int D = DT ? DT : a.D;
+  // the entry, its query node, its per-key counters (independent loads)
+  const int key = a.fq[0][i], off = a.foff[0][i], len = a.flen[0][i];
+  const double fb = a.fbase[0][i];
+  const int slot = key / K;
+  const int Q = key - slot * K;
+  const double h = s_h[slot], scale = s_scale[slot], eps = st.eps, ntot = st.ntot;
+  const int qleft = a.Q.left[Q], qright = a.Q.right[Q];
+  const bool qleaf = qleft < 0;
+  const int qcount = a.Q.count[Q];
+  const double nq = (double)qcount;
+  const double sq = a.Q.side[Q];
+  const double* qlo = a.Q.lo + (size_t)Q * D;
+  const double* qhi = a.Q.hi + (size_t)Q * D;
+  const int rF = a.cntF[key], rDT = a.cntDT[key], rB = a.cntB[key];
+#ifdef DFGTB_ASYNC_TRACE
+#define APH(k)                                                                              \
+  if (lane == 0) {                                                                          \
+    unsigned long long t_;                                                                  \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                  \
+    q.tr[3 * (size_t)st.capE + 8 * (size_t)i + (k)] = t_;                                   \
+  }
+#else
+#define APH(k)
+#endif
+  if (lane == 0 && (rF | rDT | rB | qright | qcount) == -7) a.L[0] = 0.0;  // (keeps the loads ahead of APH)
+  APH(0);
+  // pass 1: kernel bounds and the lower-bound mass of every live pair (lane-strided)
+  double part = 0.0;
+  for (int j = lane; j < len; j += 32) {
+    const int R = a.fr[0][off + j];
+    double dl, du;
+    box_bounds<DT>(qlo, qhi, a.R.lo + (size_t)R * D, a.R.hi + (size_t)R * D, D, dl, du);
+    const double kmax = exp(scale * dl);
+    const double kmin = exp(scale * du);
+    const int cr = a.R.count[R];
+    w.kmax[j] = kmax;
+    w.kmin[j] = kmin;
+    w.R[j] = R;
+    w.cnt[j] = cr;
+    w.rl[j] = a.R.left[R];
+    w.rr[j] = a.R.right[R];
+    part += (double)cr * kmin;
+  }
+  const double glo = fb + group_sum<32>(part);
+  APH(1);
+  // pass 2: decisions
+  double fd_dlo = 0.0, fd_const = 0.0, ret = 0.0;
+  int nF = 0, nDT = 0, nT = 0, nB = 0, nFD = 0, slots = 0;
+  unsigned long long kev = 0, cov = 0;
+  for (int j = lane; j < len; j += 32) {
+    const int R = w.R[j];
+    const double kmax = w.kmax[j], kmin = w.kmin[j];
+    const double nr = (double)w.cnt[j];
+    const double dlo = nr * kmin;
+    const double tau = (eps / ntot) * nr * glo;  // eps |R| G^l / N
+    const bool rleaf = w.rl[j] < 0;
+    int kind = kX, order = 0;
+    if (0.5 * nr * (kmax - kmin) <= tau) {  // kernel-difference prune, engine.cpp:137-148
+      kind = kFD;
+      fd_dlo += dlo;
+      fd_const += 0.5 * nr * (kmax + kmin);
+      ++nFD;
+    } else {
+      if (a.series) {
+        dev_choose(nq, nr, sq, a.R.side[R], h, tau, a.pmax, D, a.cost, kind, order);
+        if (kind == kE) kind = kX;
+      }
+      if (kind == kX && qleaf && rleaf) {
+        kind = kB;
+        order = base_flags(a, kmin, glo, sq, h, D, qcount, Q);
+      }
+      if (kind == kX) {
+        slots += rleaf ? 1 : 2;
+      } else if (kind == kB) {
+        ++nB;
+        kev += (unsigned long long)qcount * (unsigned long long)w.cnt[j];
+        ret += dlo;
+      } else {
+        ret += dlo;
+        if (kind == kF) ++nF;
+        else {
+          ++nDT;
+          if (kind == kT) ++nT;
+        }
+      }
+    }
+    if (kind != kX) cov += (unsigned long long)qcount * (unsigned long long)w.cnt[j];
+    w.dec[j] = kind | (order << 8);
+  }
+  fd_dlo = group_sum<32>(fd_dlo);
+  fd_const = group_sum<32>(fd_const);
+  ret = group_sum<32>(ret);
+  nF = group_sum_i<32>(nF);
+  nDT = group_sum_i<32>(nDT);
+  nT = group_sum_i<32>(nT);
+  nB = group_sum_i<32>(nB);
+  nFD = group_sum_i<32>(nFD);
+  slots = group_sum_i<32>(slots);
+  kev = group_sum_i<32>(kev);
+  cov = group_sum_i<32>(cov);
+  const int ne = slots > 0 ? (qleaf ? 1 : 2) : 0;
+  const int cl = slots;
+  const double newbase = fb + (fd_dlo + ret);
+  APH(2);
+  if (lane == 0) {
+    if (nFD) {
+      a.L[(size_t)key * a.T] += fd_const;  // constant local term (order 1)
+      if (a.Lord[key] < 1) a.Lord[key] = 1;
+    }
+    unsigned long long* ss = sst[slot];
+    atomicAdd(ss + sPairs, (unsigned long long)len);
+    if (nFD) atomicAdd(ss + sFD, (unsigned long long)nFD);
+    if (nF) atomicAdd(ss + sF, (unsigned long long)nF);
+    if (nDT - nT) atomicAdd(ss + sD, (unsigned long long)(nDT - nT));
+    if (nT) atomicAdd(ss + sT, (unsigned long long)nT);
+    if (nB) atomicAdd(ss + sB, (unsigned long long)nB);
+    if (kev) atomicAdd(ss + sKev, kev);
+    if (cov) atomicAdd(ss + sCov, cov);
+  }
+  // space: children's queue slots (dense), pairs and items (per-warp chunks)
+  int qe = 0;
+  if (lane == 0 && ne) qe = atomicAdd(q.c(acTail), ne);
+  qe = __shfl_sync(0xffffffffu, qe, 0);
+  int g0, g1;
+  const int pp = reserve(rp, ne * slots, q.c(acPool), kAsyncChunkP, st.capP, lane, g0, g1);
+  const int pf = reserve(rf, nF, q.c(acF), kAsyncChunkI, st.capF, lane, g0, g1);
+  invalidate_items(a.itF, g0, g1, st.capF, lane);
+  const int pdt = reserve(rdt, nDT, q.c(acDT), kAsyncChunkI, st.capDT, lane, g0, g1);
+  invalidate_items(a.itDT, g0, g1, st.capDT, lane);
+  const int pb = reserve(rb, nB, q.c(acB), kAsyncChunkI, st.capB, lane, g0, g1);
+  invalidate_items(a.itB, g0, g1, st.capB, lane);
+  APH(3);
+  if (!(qe + ne <= st.capE && pp >= 0 && pf >= 0 && pdt >= 0 && pb >= 0)) {
+    if (lane == 0) atomicExch(&st.overflow, 1);
+    const bool dead = lane < ne && qe + lane < st.capE;
+    if (dead) st_release(q.ready + qe + lane, 2);
+    return __popc(__ballot_sync(0xffffffffu, dead));
+  }
+  // emit (emit_entry's order): children entries, their pairs, the work items
+  if (lane == 0 && ne) {
+    if (qleaf) {
+      a.fq[0][qe] = key;
+      a.fbase[0][qe] = newbase;
+      a.foff[0][qe] = pp;
+      a.flen[0][qe] = cl;
+    } else {
+      a.fq[0][qe] = slot * K + qleft;
+      a.fq[0][qe + 1] = slot * K + qright;
+      a.fbase[0][qe] = newbase;
+      a.fbase[0][qe + 1] = newbase;
+      a.foff[0][qe] = pp;
+      a.foff[0][qe + 1] = pp + cl;
+      a.flen[0][qe] = cl;
+      a.flen[0][qe + 1] = cl;
+    }
+  }
+  int* pool = a.fr[0];
+  int runX = 0, runF = 0, runDT = 0, runB = 0;
+  for (int j0 = 0; j0 < len; j0 += 32) {
+    const int j = j0 + lane;
+    int kind = kE, order = 0, R = 0, rl = -1, rr = -1;
+    if (j < len) {
+      const int dcode = w.dec[j];
+      kind = dcode & 0xff;
+      order = dcode >> 8;
+      R = w.R[j];
+      rl = w.rl[j];
+      rr = w.rr[j];
+    }
+    const bool rleaf = (j < len) ? rl < 0 : true;
+    int tot;
+    const int px = warp_excl_scan<32>(kind == kX ? (rleaf ? 1 : 2) : 0, lane, tot);
+    if (kind == kX) {
+      const int dst = pp + runX + px;
+      if (rleaf) {
+        pool[dst] = R;
+        if (!qleaf) pool[dst + cl] = R;
+      } else {
+        pool[dst] = rl;
+        pool[dst + 1] = rr;
+        if (!qleaf) {
+          pool[dst + cl] = rl;
+          pool[dst + cl + 1] = rr;
+        }
+      }
+    }
+    runX += tot;
+    int t2;
+    const int xf = warp_excl_scan<32>(kind == kF, lane, t2);
+    if (kind == kF) a.itF[pf + runF + xf] = Item{ key, R, order | (kF << 8), rF + runF + xf };
+    runF += t2;
+    const int xd = warp_excl_scan<32>(kind == kD || kind == kT, lane, t2);
+    if (kind == kD || kind == kT) a.itDT[pdt + runDT + xd] = Item{ key, R, order | (kind << 8), rDT + runDT + xd };
+    runDT += t2;
+    const int xb = warp_excl_scan<32>(kind == kB, lane, t2);
+    if (kind == kB) a.itB[pb + runB + xb] = Item{ key, R, (kB << 8) | order, rB + runB + xb };
+    runB += t2;
+  }
+  if (lane == 0) {
+    a.cntF[key] = rF + runF;
+    a.cntDT[key] = rDT + runDT;
+    a.cntB[key] = rB + runB;
+  }
+  totF += nF;
+  totDT += nDT;
+  totB += nB;
+  APH(4);
+  __threadfence();
+  __syncwarp();
+  APH(5);
+  if (lane < ne) {
+    q.depth[qe + lane] = (unsigned char)min(255, q.depth[i] + 1);
+#ifdef DFGTB_ASYNC_TRACE
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    q.tr[3 * (size_t)(qe + lane)] = t_;
+#endif
+    st_release(q.ready + qe + lane, 1);
+  }
+#ifdef DFGTB_ASYNC_TRACE
+  if (lane == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    q.tr[3 * (size_t)i + 2] = t_;
+  }
+#endif
+  if (lane == 0 && ne) atomicMax(&st.levels, (int)q.depth[i] + 2);
+  return ne;
+}
+
+#ifndef DFGTB_ASYNC_MINB
+#define DFGTB_ASYNC_MINB 6
+#endif
+template <int DT>
+__global__ void __launch_bounds__(kAsyncBlock, DFGTB_ASYNC_MINB) k_trav_async(const __grid_constant__ TravArgs a, AsyncQ q)
+{
+  TravState& st = *a.st;
+  const int lane = threadIdx.x & 31;
+  const int K = st.K;
+  __shared__ unsigned long long s_sst[kMaxSlots][sNStat];
+  __shared__ double s_h[kMaxSlots], s_scale[kMaxSlots];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  WarpScratch* s_ws = reinterpret_cast<WarpScratch*>(s_dyn);  // one per warp (dynamic)
+  for (int k = threadIdx.x; k < kMaxSlots * sNStat; k += blockDim.x) (&s_sst[0][0])[k] = 0;
+  for (int k = threadIdx.x; k < st.nslots; k += blockDim.x) {
+    s_h[k] = st.h[k];
+    s_scale[k] = st.scale[k];
+  }
+  __syncthreads();
+  Reserve rp, rf, rdt, rb;
+  int g0, g1, totF = 0, totDT = 0, totB = 0;
+  for (;;) {
+    int i = 0;
+    if (lane == 0) i = atomicAdd(q.c(acHead), 1);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= st.capE) break;  // past every slot that can ever be published
+    int ok = 0;  // 1: an entry to process, 2: a dead slot (its producer overflowed), 0: done
+    if (lane == 0) {
+      unsigned ns = 32;
+      for (long long polls = 0;; ++polls) {
+        ok = ld_acquire(q.ready + i);
+        if (ok) break;
+        if ((polls & 15) == 15 && ld_acquire(q.c(acPending)) == 0) {
+          ok = ld_acquire(q.ready + i);
+          break;
+        }
+        if (polls > kAsyncMaxPolls) {
+          if (atomicExch(&st.overflow, 3) != 3)
+            st.lvl = Cnt{ i, *q.c(acHead), *q.c(acTail), *q.c(acPending), *q.c(acPool), 0, 0 };
+          break;
+        }
+        __nanosleep(ns);
+        ns = ns < kAsyncMaxSleep ? 2 * ns : kAsyncMaxSleep;
+      }
+      if (ok == 2) atomicAdd(q.c(acPending), -1);
+    }
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    if (!ok) break;
+    if (ok == 2) continue;
+    __syncwarp();  // lane 0's acquire orders the whole warp's reads of the entry
+#ifdef DFGTB_ASYNC_TRACE
+    if (lane == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      q.tr[3 * (size_t)i + 1] = t_;
+    }
+#endif
+    if (a.flen[0][i] <= kFuseMax) {
+      const int nchild = async_entry<DT>(a, st, q, i, lane, s_ws[threadIdx.x >> 5], s_sst, rp, rf, rdt, rb,
+                                         totF, totDT, totB, s_h, s_scale, K);
+      if (lane == 0) atomicAdd(q.c(acPending), nchild - 1);
+      continue;
+    }
+    classify_entry<DT, 32>(a, st, 0, i, lane, true, s_sst);
+    __syncwarp();
+    // space for the children's queue slots (dense: consumers claim them in order), pairs
+    // and work items (per-warp chunks: gaps are harmless / marked invalid)
+    const Cnt c = a.cnt[i];
+    int qe = 0;
+    if (lane == 0 && c.e) qe = atomicAdd(q.c(acTail), c.e);
+    qe = __shfl_sync(0xffffffffu, qe, 0);
+    const int pp = reserve(rp, c.p, q.c(acPool), kAsyncChunkP, st.capP, lane, g0, g1);
+    const int pf = reserve(rf, c.f, q.c(acF), kAsyncChunkI, st.capF, lane, g0, g1);
+    invalidate_items(a.itF, g0, g1, st.capF, lane);
+    const int pdt = reserve(rdt, c.dt, q.c(acDT), kAsyncChunkI, st.capDT, lane, g0, g1);
+    invalidate_items(a.itDT, g0, g1, st.capDT, lane);
+    const int pb = reserve(rb, c.b, q.c(acB), kAsyncChunkI, st.capB, lane, g0, g1);
+    invalidate_items(a.itB, g0, g1, st.capB, lane);
+    const bool fits = qe + c.e <= st.capE && pp >= 0 && pf >= 0 && pdt >= 0 && pb >= 0;
+    int nchild = 0;
+    if (fits) {
+      const Cnt o{ qe, pp, pf, pdt, 0, pb, 0 };
+      emit_entry<32>(a, K, 0, 0, 0, 0, i, o, lane, true);
+      nchild = c.e;
+      totF += c.f;
+      totDT += c.dt;
+      totB += c.b;
+      __threadfence();
+      __syncwarp();
+      if (lane < nchild) {
+        q.depth[qe + lane] = (unsigned char)min(255, q.depth[i] + 1);
+#ifdef DFGTB_ASYNC_TRACE
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        q.tr[3 * (size_t)(qe + lane)] = t_;
+        if (lane == 0) q.tr[3 * (size_t)i + 2] = t_;
+#endif
+        st_release(q.ready + qe + lane, 1);
+      }
+      if (lane == 0 && nchild) atomicMax(&st.levels, (int)q.depth[i] + 2);
+    } else {
+      // the host regrows the buffers and reruns the batch; the reserved slots are
+      // published dead, so their claimants move on (a live entry beyond them must still
+      // be claimed)
+      if (lane == 0) atomicExch(&st.overflow, 1);
+      const bool dead = lane < c.e && qe + lane < st.capE;
+      if (dead) st_release(q.ready + qe + lane, 2);
+      nchild = __popc(__ballot_sync(0xffffffffu, dead));
+    }
+    if (lane == 0) atomicAdd(q.c(acPending), nchild - 1);
+  }
+  if (lane == 0) {  // real item totals (the extents include the invalidated gaps)
+    if (totF) atomicAdd(q.c(acRF), totF);
+    if (totDT) atomicAdd(q.c(acRDT), totDT);
+    if (totB) atomicAdd(q.c(acRB), totB);
+  }
+  // unused tails of this warp's item chunks
+  invalidate_items(a.itF, rf.pos, rf.end, st.capF, lane);
+  invalidate_items(a.itDT, rdt.pos, rdt.end, st.capDT, lane);
+  invalidate_items(a.itB, rb.pos, rb.end, st.capB, lane);
+  __syncthreads();
+  for (int k = threadIdx.x; k < st.nslots * sNStat; k += blockDim.x) {
+    const unsigned long long v = (&s_sst[0][0])[k];
+    if (v) atomicAdd(&st.sst[0][0] + k, v);
+  }
+}
+
+// Totals of the asynchronous traversal into the state (k_trav_publish reads nF / nDT / nB;
+// positions past the last reservation are never written).
+__global__ void k_async_finish(const __grid_constant__ TravArgs a, AsyncQ q)
+{
+  TravState& st = *a.st;
+  st.xF = *q.c(acF);
+  st.xDT = *q.c(acDT);
+  st.xB = *q.c(acB);
+  st.nF = *q.c(acRF);
+  st.nDT = *q.c(acRDT);
+  st.nB = *q.c(acRB);
+  st.atail = *q.c(acTail);
+  st.aptail = *q.c(acPool);
+}
+
+// The root entries (k_trav_init wrote them at slots 0..nb-1) are published.
+__global__ void k_async_init(const __grid_constant__ TravArgs a, AsyncQ q)
+{
+  TravState& st = *a.st;
+  const int nb = st.nslots;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    q.ready[b] = 1;
+    q.depth[b] = 0;
+  }
+  if (threadIdx.x < acNum) {
+    const int k = threadIdx.x;
+    *q.c(k) = k == acTail || k == acPool || k == acPending ? nb : 0;
+  }
+  if (threadIdx.x == 0) st.levels = 1;
+}
+
 #ifndef DFGTB_TRAV_CTAS_PER_SM
 #define DFGTB_TRAV_CTAS_PER_SM 1
 #endif
@@ -875,6 +1544,8 @@ __global__ void __launch_bounds__(kPBlock, kPerSM) k_traverse(const __grid_const
   __shared__ int s_wsum[32][5];
   __shared__ double s_h[kMaxSlots], s_scale[kMaxSlots];
   __shared__ unsigned long long s_sst[kMaxSlots][sNStat];
+  extern __shared__ __align__(16) unsigned char s_cache[];  // PairCache (kCacheBytes, dynamic)
+  const PairCache pc = PairCache::at(s_cache);
   const int G = gridDim.x;
   const int K = st.K, nslots = st.nslots;
   for (int i = threadIdx.x; i < kMaxSlots * sNStat; i += kPBlock) (&s_sst[0][0])[i] = 0;
@@ -915,19 +1586,35 @@ __global__ void __launch_bounds__(kPBlock, kPerSM) k_traverse(const __grid_const
       }
     }
     auto pofs = [&](int e) { return e < m ? a.foff[cur][e] : p; };
+    const int cP0 = pofs(cb0[0]), cP1 = pofs(cb1[0]);
+    const bool cached = kUseCache && nch == 1 && cP1 - cP0 <= kCacheP && cb1[0] - cb0[0] <= kCacheE;
     PH(0);
-    for (int j = 0; j < nch; ++j) pairs_bounds<DT>(a, cur, K, pofs(cb0[j]), pofs(cb1[j]), s_scale);
-    __syncthreads();
-    PH(1);
-    for (int j = 0; j < nch; ++j)
-      entries_glo(a, cur, cb0[j], cb1[j], a.trace && levels < 64 ? a.trace + 4096 + 512 * 16 + 64 * 160 + levels : nullptr);
-    __syncthreads();
-    PH(2);
-    for (int j = 0; j < nch; ++j) pairs_decide<DT>(a, st, cur, K, pofs(cb0[j]), pofs(cb1[j]), s_h);
-    __syncthreads();
-    PH(3);
-    for (int j = 0; j < nch; ++j) entries_reduce(a, cur, K, cb0[j], cb1[j], s_sst);
-    __syncthreads();
+    if (cached) {
+      pairs_bounds_c<DT>(a, cur, K, cP0, cP1, cb0[0], cb1[0], s_scale, pc);
+      __syncthreads();
+      PH(1);
+      entries_glo_c(a, cur, cb0[0], cb1[0], pc);
+      __syncthreads();
+      PH(2);
+      pairs_decide_c<DT>(a, st, K, cP0, cP1, s_h, pc);
+      __syncthreads();
+      PH(3);
+      entries_reduce_c(a, cur, K, cb0[0], cb1[0], s_sst, pc);
+      __syncthreads();
+    } else {
+      for (int j = 0; j < nch; ++j) pairs_bounds<DT>(a, cur, K, pofs(cb0[j]), pofs(cb1[j]), s_scale);
+      __syncthreads();
+      PH(1);
+      for (int j = 0; j < nch; ++j)
+        entries_glo(a, cur, cb0[j], cb1[j], a.trace && levels < 64 ? a.trace + 4096 + 512 * 16 + 64 * 160 + levels : nullptr);
+      __syncthreads();
+      PH(2);
+      for (int j = 0; j < nch; ++j) pairs_decide<DT>(a, st, cur, K, pofs(cb0[j]), pofs(cb1[j]), s_h);
+      __syncthreads();
+      PH(3);
+      for (int j = 0; j < nch; ++j) entries_reduce(a, cur, K, cb0[j], cb1[j], s_sst);
+      __syncthreads();
+    }
     PH(4);
     // virtual index over the concatenated chunks -> frontier entry
     int nE = 0, cofs[kNch + 1];
@@ -1032,7 +1719,9 @@ __global__ void __launch_bounds__(kPBlock, kPerSM) k_traverse(const __grid_const
       }
       __syncthreads();
       PH(6);
-      for (int j = 0; j < nch; ++j) emit_range<32>(a, K, cur, gF, gDT, gB, cb0[j], cb1[j]);
+      if (cached) emit_range<32>(a, K, cur, gF, gDT, gB, cb0[0], cb1[0], pc.dec, pc.R, cP0);
+      else
+        for (int j = 0; j < nch; ++j) emit_range<32>(a, K, cur, gF, gDT, gB, cb0[j], cb1[j]);
     }
     PH(7);
     if (a.trace && threadIdx.x == 0 && levels < 64) {  // per-CTA busy time of the level
@@ -1229,11 +1918,13 @@ void Engine::run_levels(const void* args, const std::vector<const void*>& sig)
     int dev = 0, nsm = 0, per_sm = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPBlock, 0));
+    const int smem = kUseCache ? kCacheBytes : 0;
+    if (smem) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPBlock, smem));
     if (per_sm >= 1) {
       TravArgs copy = a;
       void* kargs[] = { &copy };
-      CK(cudaLaunchCooperativeKernel(fn, nsm * std::min(per_sm, kPerSM), kPBlock, kargs, 0, s_));
+      CK(cudaLaunchCooperativeKernel(fn, nsm * std::min(per_sm, kPerSM), kPBlock, kargs, smem, s_));
       ++launch_counter();
       return;
     }
@@ -1293,6 +1984,9 @@ __global__ void k_trav_publish(const TravState* st, int* bc)
   bc[1] = ovf ? 0 : st->nDT;
   bc[2] = ovf ? 0 : st->nB;
   bc[3] = ovf;
+  bc[8] = ovf ? 0 : max(st->nF, st->xF);  // extents of the unsorted item arrays
+  bc[9] = ovf ? 0 : max(st->nDT, st->xDT);
+  bc[10] = ovf ? 0 : max(st->nB, st->xB);
 }
 
 __global__ void k_trav_clear_on_overflow(const int* bc, int* cntF, int* cntDT, int* cntB, int KB)
@@ -1307,7 +2001,7 @@ __global__ void k_scatter_dev(const Item* in, const int* n, int cap, const int* 
   const int m = min(*n, cap);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
     const Item it = in[i];
-    out[noff[it.key] + it.rank] = it;
+    if (it.key >= 0) out[noff[it.key] + it.rank] = it;  // async traversal: gaps are key -1
   }
 }
 
@@ -1338,22 +2032,43 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     capDT_ = std::max(capDT_, std::max(4096, 2 * kb));
     capB_ = std::max(capB_, std::max(1 << 16, 16 * kb));
   }
-  for (int b = 0; b < 2; ++b) {
-    fq_[b].reserve(capE_);
-    foff_[b].reserve(capE_);
-    flen_[b].reserve(capE_);
-    fbase_[b].reserve(capE_);
-    fr_[b].reserve(capP_);
-    pent_[b].reserve(capP_);
+  if (use_async_) {  // one queue of every entry of the batch, one pool of every pair
+    const int kb = (int)std::min<long long>(KB, INT32_MAX / 128);
+    capEA_ = std::max(capEA_, std::max(1 << 16, 16 * kb));
+    capPA_ = std::max(capPA_, std::max(1 << 20, 64 * kb));
+    fq_[0].reserve(capEA_);
+    foff_[0].reserve(capEA_);
+    flen_[0].reserve(capEA_);
+    fbase_[0].reserve(capEA_);
+    fr_[0].reserve(capPA_);
+    pent_[0].reserve(capPA_);
+    pkmax_.reserve(capPA_);
+    pkmin_.reserve(capPA_);
+    dec_.reserve(capPA_);
+    cnt_.reserve(capEA_);
+    childlen_.reserve(capEA_);
+    newbase_.reserve(capEA_);
+    aready_.reserve(capEA_);
+    adepth_.reserve(capEA_);
+    CK(cudaMemsetAsync(aready_.p, 0, sizeof(int) * capEA_, s));
+  } else {
+    for (int b = 0; b < 2; ++b) {
+      fq_[b].reserve(capE_);
+      foff_[b].reserve(capE_);
+      flen_[b].reserve(capE_);
+      fbase_[b].reserve(capE_);
+      fr_[b].reserve(capP_);
+      pent_[b].reserve(capP_);
+    }
+    pglo_.reserve(capE_);
+    pkmax_.reserve(capP_);
+    pkmin_.reserve(capP_);
+    dec_.reserve(capP_);
+    cnt_.reserve(capE_);
+    cntoff_.reserve(capE_);
+    childlen_.reserve(capE_);
+    newbase_.reserve(capE_);
   }
-  pglo_.reserve(capE_);
-  pkmax_.reserve(capP_);
-  pkmin_.reserve(capP_);
-  dec_.reserve(capP_);
-  cnt_.reserve(capE_);
-  cntoff_.reserve(capE_);
-  childlen_.reserve(capE_);
-  newbase_.reserve(capE_);
   ctsum_.reserve(kScanTiles);
   ctoff_.reserve(kScanTiles);
   itF_.reserve(capF_);
@@ -1374,13 +2089,14 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   a.series = cfg_.mode == 1;
   a.T = T;
   a.st = ds;
-  for (int b = 0; b < 2; ++b) {
-    a.fq[b] = fq_[b].p;
-    a.foff[b] = foff_[b].p;
-    a.flen[b] = flen_[b].p;
-    a.fr[b] = fr_[b].p;
-    a.fbase[b] = fbase_[b].p;
-    a.pent[b] = pent_[b].p;
+  for (int b = 0; b < 2; ++b) {  // async: both "levels" are the one queue / pool
+    const int bb = use_async_ ? 0 : b;
+    a.fq[b] = fq_[bb].p;
+    a.foff[b] = foff_[bb].p;
+    a.flen[b] = flen_[bb].p;
+    a.fr[b] = fr_[bb].p;
+    a.fbase[b] = fbase_[bb].p;
+    a.pent[b] = pent_[bb].p;
   }
   a.glo = pglo_.p;
   a.pkmax = pkmax_.p;
@@ -1430,15 +2146,50 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     hs->h[b] = h[b];
     hs->scale[b] = -1.0 / (2.0 * h[b] * h[b]);
   }
-  hs->capE = capE_;
-  hs->capP = capP_;
+  hs->capE = use_async_ ? capEA_ : capE_;
+  hs->capP = use_async_ ? capPA_ : capP_;
   hs->capF = capF_;
   hs->capDT = capDT_;
   hs->capB = capB_;
   CK(cudaMemcpyAsync(ds, hs, sizeof(TravState), cudaMemcpyHostToDevice, s));
   k_trav_init<<<1, 64, 0, s>>>(a);
   CK_LAUNCH();
-  run_levels(&a, sig);
+  if (use_async_) {
+    actr_.reserve(acNum * kAsyncCtr);
+    AsyncQ q{ aready_.p, actr_.p, adepth_.p, nullptr };
+#ifdef DFGTB_ASYNC_TRACE
+    atrace_.reserve((size_t)11 * capEA_);
+    CK(cudaMemsetAsync(atrace_.p, 0, sizeof(unsigned long long) * 11 * capEA_, s));
+    q.tr = atrace_.p;
+#endif
+    k_async_init<<<1, 64, 0, s>>>(a, q);
+    CK_LAUNCH();
+    static int grid = 0;
+    if (!grid) {
+      int dev = 0, nsm = 0, per_sm = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      for (void* f : { (void*)k_trav_async<0>, (void*)k_trav_async<1>, (void*)k_trav_async<2>, (void*)k_trav_async<3>,
+                       (void*)k_trav_async<4>, (void*)k_trav_async<5> })
+        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsyncSmem));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_async<2>, kAsyncBlock, kAsyncSmem));
+      const char* env = std::getenv("DFGTB_ASYNC_CTAS");
+      grid = nsm * std::max(1, env ? std::min(per_sm, std::atoi(env)) : per_sm);
+    }
+    switch (D_) {
+    case 1: k_trav_async<1><<<grid, kAsyncBlock, kAsyncSmem, s>>>(a, q); break;
+    case 2: k_trav_async<2><<<grid, kAsyncBlock, kAsyncSmem, s>>>(a, q); break;
+    case 3: k_trav_async<3><<<grid, kAsyncBlock, kAsyncSmem, s>>>(a, q); break;
+    case 4: k_trav_async<4><<<grid, kAsyncBlock, kAsyncSmem, s>>>(a, q); break;
+    case 5: k_trav_async<5><<<grid, kAsyncBlock, kAsyncSmem, s>>>(a, q); break;
+    default: k_trav_async<0><<<grid, kAsyncBlock, kAsyncSmem, s>>>(a, q); break;
+    }
+    CK_LAUNCH();
+    k_async_finish<<<1, 1, 0, s>>>(a, q);
+    CK_LAUNCH();
+  } else {
+    run_levels(&a, sig);
+  }
   k_trav_publish<<<1, 1, 0, s>>>(ds, bc_.p);
   CK_LAUNCH();
   k_trav_clear_on_overflow<<<148, 256, 0, s>>>(bc_.p, cntF_.p, cntDT_.p, cntB_.p, (int)KB);
@@ -1459,9 +2210,9 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     k_scatter_dev<<<148 * 4, 256, 0, s>>>(in.p, dn, cap, off.p, out.p);
     CK_LAUNCH();
   };
-  sort_items(itF_, capF_, bc_.p + 0, cntF_, offF_, sF_);
-  sort_items(itDT_, capDT_, bc_.p + 1, cntDT_, offDT_, sDT_);
-  sort_items(itB_, capB_, bc_.p + 2, cntB_, offB_, sB_);
+  sort_items(itF_, capF_, bc_.p + 8, cntF_, offF_, sF_);
+  sort_items(itDT_, capDT_, bc_.p + 9, cntDT_, offDT_, sDT_);
+  sort_items(itB_, capB_, bc_.p + 10, cntB_, offB_, sB_);
 }
 
 // After the batch's final synchronisation: statistics, and the traversal verdict
@@ -1500,6 +2251,85 @@ bool Engine::traverse_finish()
     }
   }
   if (hs->overflow == 2) throw CudaError("traversal exceeded 1024 levels");
+#ifdef DFGTB_ASYNC_TRACE
+  if (use_async_ && !hs->overflow) {
+    const int ne = hs->atail;
+    std::vector<unsigned long long> tr((size_t)3 * ne);
+    std::vector<int> len(ne);
+    std::vector<unsigned char> dep(ne);
+    CK(cudaMemcpy(tr.data(), atrace_.p, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(len.data(), flen_[0].p, sizeof(int) * ne, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(dep.data(), adepth_.p, ne, cudaMemcpyDeviceToHost));
+    unsigned long long t0 = ~0ull, t1 = 0;
+    double hand = 0, proc = 0, lproc[6] = {}, lcnt[6] = {};
+    int nh = 0;
+    std::vector<double> dstart(256, 1e30), dend(256, 0);
+    for (int i = 0; i < ne; ++i) {
+      const unsigned long long pub = tr[3 * i], st0 = tr[3 * i + 1], fin = tr[3 * i + 2];
+      if (!st0) continue;
+      t0 = std::min(t0, st0);
+      t1 = std::max(t1, fin ? fin : st0);
+      if (pub) {
+        hand += (double)(st0 - pub);
+        ++nh;
+      }
+      if (fin) {
+        const double pt = (double)(fin - st0);
+        proc += pt;
+        const int b = len[i] <= 8 ? 0 : len[i] <= 32 ? 1 : len[i] <= 64 ? 2 : len[i] <= 128 ? 3 : len[i] <= 256 ? 4 : 5;
+        lproc[b] += pt;
+        lcnt[b] += 1;
+      }
+      dstart[dep[i]] = std::min(dstart[dep[i]], (double)st0);
+      dend[dep[i]] = std::max(dend[dep[i]], (double)(fin ? fin : st0));
+    }
+    std::fprintf(stderr, "DFGTB_ASYNC_TRACE entries %d span %.1f us, handoff mean %.2f us, processing mean %.2f us; by length "
+                 "<=8 %.2f <=32 %.2f <=64 %.2f <=128 %.2f <=256 %.2f >256 %.2f us\n", ne, (t1 - t0) * 1e-3,
+                 nh ? hand / nh * 1e-3 : 0.0, proc / std::max(1, ne) * 1e-3, lproc[0] / std::max(1.0, lcnt[0]) * 1e-3,
+                 lproc[1] / std::max(1.0, lcnt[1]) * 1e-3, lproc[2] / std::max(1.0, lcnt[2]) * 1e-3,
+                 lproc[3] / std::max(1.0, lcnt[3]) * 1e-3, lproc[4] / std::max(1.0, lcnt[4]) * 1e-3,
+                 lproc[5] / std::max(1.0, lcnt[5]) * 1e-3);
+    {
+      std::vector<unsigned long long> ph((size_t)8 * ne);
+      CK(cudaMemcpy(ph.data(), atrace_.p + (size_t)3 * capEA_, sizeof(unsigned long long) * ph.size(),
+                    cudaMemcpyDeviceToHost));
+      double acc[6] = {};
+      int nn = 0;
+      for (int i = 0; i < ne; ++i) {
+        const unsigned long long* p = ph.data() + 8 * i;
+        const unsigned long long st0 = tr[3 * i + 1], fin = tr[3 * i + 2];
+        if (!p[0] || !p[5] || !st0 || !fin) continue;
+        acc[0] += (double)(p[0] - st0);
+        for (int k = 1; k <= 5; ++k) acc[k] += (double)(p[k] - p[k - 1]);
+        ++nn;
+      }
+      std::fprintf(stderr, "  phases (us, mean of %d fused entries): loads %.2f pass1 %.2f pass2 %.2f reserve %.2f emit %.2f fence %.2f\n",
+                   nn, acc[0] / nn * 1e-3, acc[1] / nn * 1e-3, acc[2] / nn * 1e-3, acc[3] / nn * 1e-3, acc[4] / nn * 1e-3,
+                   acc[5] / nn * 1e-3);
+    }
+    for (int d = 0; d < 64 && dend[d] > 0; ++d)
+      std::fprintf(stderr, "  depth %d: first start %.1f us, last finish %.1f us\n", d, (dstart[d] - t0) * 1e-3,
+                   (dend[d] - t0) * 1e-3);
+  }
+#endif
+  if (hs->overflow == 3)
+    throw CudaError("asynchronous traversal: queue slot " + std::to_string(hs->lvl.e) + " was never published (head " +
+                    std::to_string(hs->lvl.p) + ", tail " + std::to_string(hs->lvl.f) + ", pending " +
+                    std::to_string(hs->lvl.dt) + ", pairs " + std::to_string(hs->lvl.t) + ", cap " +
+                    std::to_string(capEA_) + "/" + std::to_string(capPA_) + ")");
+  if (hs->overflow && use_async_) {
+    auto grow2 = [](int cap, long long need) {
+      if (need <= cap) return cap;
+      if (need > INT32_MAX / 4) throw OutOfMemory("traversal exceeds 2^29 entries / pairs / items");
+      return (int)std::max<long long>(2ll * cap, 2 * need);
+    };
+    capEA_ = grow2(capEA_, hs->atail);
+    capPA_ = grow2(capPA_, hs->aptail);
+    capF_ = grow2(capF_, std::max(hs->nF, hs->xF));
+    capDT_ = grow2(capDT_, std::max(hs->nDT, hs->xDT));
+    capB_ = grow2(capB_, std::max(hs->nB, hs->xB));
+    return false;
+  }
   if (hs->overflow) {
     const Cnt l = hs->lvl;
     auto grow = [](int cap, long long need) {

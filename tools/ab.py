@@ -50,7 +50,7 @@ def main():
     for lib in args:
         env = dict(os.environ, DFGTB_LIB=os.path.abspath(lib), ROOT=root, CFG=cfg, STEPS=steps)
         out = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
-        line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-500:]
+        line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-1500:]
         print(f"{lib}: {line}", flush=True)
 
 
