@@ -310,6 +310,35 @@ __device__ void dev_nth_element(int* first, int* nth, int* last, const KeyCmp& c
   dev_insertion_sort(first, last, cmp);
 }
 
+// dev_nth_element on n EQUAL keys (a node of identical points, whose midpoint split is
+// always one-sided) with the whole CTA: libstdc++'s introselect then does, per round,
+// __move_median_to_first = swap(first, mid) and an __unguarded_partition that swaps
+// (f + i, last - 1 - i) for i < (last - f) / 2 (f = first + 1) and returns f + that
+// count; the closing insertion sort moves nothing.  Same swaps, in parallel per round.
+template <int NT>
+__device__ void par_equal_nth(int* q, int n, int tid)
+{
+  if (n <= 0) return;
+  const int nth = n / 2;
+  int first = 0, last = n;
+  int lg = 0;
+  for (int t = n; t > 1; t >>= 1) ++lg;
+  int depth = 2 * lg;  // never exhausted: every round halves the range
+  while (last - first > 3 && depth > 0) {
+    --depth;
+    const int mid = first + (last - first) / 2;
+    __syncthreads();
+    if (tid == 0) dswap(q + first, q + mid);
+    __syncthreads();
+    const int f = first + 1, ts = (last - f) / 2;
+    for (int i = tid; i < ts; i += NT) dswap(q + f + i, q + last - 1 - i);
+    const int cut = f + ts;
+    if (cut <= nth) first = cut;
+    else last = cut;
+  }
+  __syncthreads();
+}
+
 // One thread per splitting node: final left count / split coordinate, running the
 // median fallback when the midpoint split is one-sided (kdtree.cpp:85-94).
 __global__ void k_finish_split(LevelArgs a, int m, int base, const int* do_split,
@@ -427,6 +456,7 @@ struct BuildArgs {
   int* lvlmax;                      // per level: largest count of a splitting node
   int* kcount;                      // node count (ids handed out by the local phase)
   int local_S;                      // subtree size of the CTA-local phase (0: off)
+  int* loc;                         // {base, m, level} of the local phase (m = 0: none)
 };
 
 __device__ __forceinline__ void chunk_of(int total, int b, int G, int& lo, int& hi)
@@ -445,17 +475,21 @@ __device__ __forceinline__ void chunk_of(int total, int b, int G, int& lo, int& 
 constexpr int kLS = 4096;  // positions per subtree (shared memory)
 constexpr int kLN = 256;   // nodes per local level
 constexpr int kLMaxD = 8;  // dimensions the local phase supports
+constexpr int kLEq = 64;      // identical-point nodes per local level handled by the whole CTA
+constexpr int kLCacheD = 2;  // D <= 2: the subtree's coordinates are staged in shared memory
 int local_smem_bytes(int D)
 {
   return 5 * kLS * 4 + 4                          // sp, seg, flag, P (+1), slot
          + 2 * kLN * (6 * 4 + 8) + kLN * 2 * 4     // two node buffers, lc, rank
-         + 2 * 2 * kLN * D * 8;                    // child key min / max
+         + 2 * 2 * kLN * D * 8                     // child key min / max
+         + (D <= kLCacheD ? kLS * (8 * D + 4) : 0);  // coordinates + point ids (local ids in sp)
 }
 
-template <class TS>
+template <int NT, class TS>
 __device__ void local_subtrees(const BuildArgs& a, TS& tmp, unsigned char* lsm, int base, int m, int level,
                                const int* dsp, const double* mdp)
 {
+  constexpr int kPB = NT;  // threads of the calling CTA
   using BS = cub::BlockScan<int, kPB>;
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, D = a.D;
   int* sp = reinterpret_cast<int*>(lsm);
@@ -471,11 +505,31 @@ __device__ void local_subtrees(const BuildArgs& a, TS& tmp, unsigned char* lsm, 
   double* nmid1 = nmid0 + kLN;
   unsigned long long* kmn = reinterpret_cast<unsigned long long*>(nmid1 + kLN);
   unsigned long long* kmx = kmn + 2 * kLN * D;
-  __shared__ int s_ns, s_cbase;
+  // D <= kLCacheD: sp holds LOCAL ids into the staged coordinates xl (the nth_element
+  // swaps are the same, the keys compare equal): no global load per comparison
+  const bool cache = D <= kLCacheD;
+  double* xl = reinterpret_cast<double*>(kmx + 2 * kLN * D);
+  int* gid = reinterpret_cast<int*>(xl + kLS * D);
+  const double* X = cache ? xl : a.x;
+  __shared__ int s_ns, s_cbase, s_neq;
+  __shared__ int2 s_eq[kLEq];  // this local level's nodes of identical points
+  if (tid == 0) s_neq = 0;
   for (int j = blockIdx.x; j < m; j += G) {
+#ifdef DFGTB_TREE_DEBUG
+    unsigned long long t0_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0_));
+    int levels_ = 0, maxnodes_ = 0, eqn_ = 0;
+#endif
     const int id0 = base + j, b0 = a.nbeg[id0], c = a.ncnt[id0];
     for (int k = tid; k < c; k += kPB) {
-      sp[k] = a.perm[b0 + k];
+      const int g = a.perm[b0 + k];
+      if (cache) {
+        gid[k] = g;
+        sp[k] = k;
+        for (int d = 0; d < D; ++d) xl[(size_t)k * D + d] = a.x[(size_t)g * D + d];
+      } else {
+        sp[k] = g;
+      }
       sseg[k] = 0;
     }
     int* cur = nb0;
@@ -503,46 +557,13 @@ __device__ void local_subtrees(const BuildArgs& a, TS& tmp, unsigned char* lsm, 
         kmx[i] = 0ull;
       }
       __syncthreads();
-      // predicate x_w <= mid, children's bound keys (warp-reduced when the warp is one node)
-      for (int k0 = 0; k0 < c; k0 += kPB) {
-        const int k = k0 + tid;
-        int f = 0, js = -1;
-        const double* xp = nullptr;
-        if (k < c) {
-          const int jj = sseg[k];
-          if (jj >= 0 && nds[jj]) {
-            xp = a.x + (size_t)sp[k] * D;
-            f = xp[nw[jj]] <= cmid[jj] ? 1 : 0;
-            js = 2 * jj + (f ? 0 : 1);
-          }
-          sflag[k] = f;
-        }
-        const int jn = js >= 0 ? js >> 1 : -1;
-        const int j0 = __shfl_sync(0xffffffffu, jn, 0);
-        const bool uni = __all_sync(0xffffffffu, jn == j0) && j0 >= 0;
-        for (int d = 0; d < D; ++d) {
-          const unsigned long long key = js >= 0 ? dkey(xp[d]) : 0ull;
-          if (uni) {
-#pragma unroll
-            for (int side = 0; side < 2; ++side) {
-              const bool mine = (js & 1) == side;
-              if (!__any_sync(0xffffffffu, mine)) continue;
-              unsigned long long mn = mine ? key : ~0ull, mx = mine ? key : 0ull;
-#pragma unroll
-              for (int o = 16; o > 0; o >>= 1) {
-                mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-                mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-              }
-              if (lane == 0) {
-                atomicMin(&kmn[(2 * j0 + side) * D + d], mn);
-                atomicMax(&kmx[(2 * j0 + side) * D + d], mx);
-              }
-            }
-          } else if (js >= 0) {
-            atomicMin(&kmn[js * D + d], key);
-            atomicMax(&kmx[js * D + d], key);
-          }
-        }
+      // predicate x_w <= mid (the children's bounds are reduced after the partition, over
+      // their contiguous position ranges: no shared-memory atomics)
+      for (int k = tid; k < c; k += kPB) {
+        int f = 0;
+        const int jj = sseg[k];
+        if (jj >= 0 && nds[jj]) f = X[(size_t)sp[k] * D + nw[jj]] <= cmid[jj] ? 1 : 0;
+        sflag[k] = f;
       }
       __syncthreads();
       // exclusive prefix of the flags over the subtree's positions
@@ -576,24 +597,23 @@ __device__ void local_subtrees(const BuildArgs& a, TS& tmp, unsigned char* lsm, 
         const int L = sP[bg + cn] - sP[bg];
         int l;
         if (L == 0 || L == cn) {
-          KeyCmp cmp{ a.x, D, nw[jj] };
+          KeyCmp cmp{ X, D, nw[jj] };
           int* q0 = sp + bg;
+          if (a.bside[id] == 0.0 && cn > 3) {
+            // identical points: both children's bounds are the node's, and the median
+            // permutation is par_equal_nth's (run by the whole CTA below)
+            const int k = atomicAdd(&s_neq, 1);
+            if (k < kLEq) {
+              s_eq[k] = make_int2(bg, cn);
+              l = cn / 2;
+              a.bsc[id] = cmp.key(q0[0]);
+              nlc[jj] = l;
+              continue;
+            }
+          }
           dev_nth_element(q0, q0 + cn / 2, q0 + cn, cmp);
           l = cn / 2;
           a.bsc[id] = cmp.key(q0[cn / 2]);
-          for (int side = 0; side < 2; ++side) {
-            const int k0 = side ? l : 0, k1 = side ? cn : l;
-            for (int d = 0; d < D; ++d) {
-              unsigned long long mn = ~0ull, mx = 0ull;
-              for (int k = k0; k < k1; ++k) {
-                const unsigned long long kk = dkey(a.x[(size_t)q0[k] * D + d]);
-                mn = min(mn, kk);
-                mx = max(mx, kk);
-              }
-              kmn[(2 * jj + side) * D + d] = mn;
-              kmx[(2 * jj + side) * D + d] = mx;
-            }
-          }
         } else {
           l = L;
           a.bsc[id] = cmid[jj];
@@ -608,6 +628,15 @@ __device__ void local_subtrees(const BuildArgs& a, TS& tmp, unsigned char* lsm, 
         if (k >= bg + L) sslot[bg + (sP[e] - sP[k] - 1)] = k;
       }
       __syncthreads();
+#ifdef DFGTB_TREE_DEBUG
+      ++levels_;
+      maxnodes_ = max(maxnodes_, ncur);
+      eqn_ += min(s_neq, kLEq);
+#endif
+      const int neq = min(s_neq, kLEq);
+      for (int e = 0; e < neq; ++e) par_equal_nth<kPB>(sp + s_eq[e].x, s_eq[e].y, tid);
+      __syncthreads();
+      if (tid == 0) s_neq = 0;
       // left-block failers swap with their partners (libstdc++ partition pairing)
       for (int k = tid; k < c; k += kPB) {
         const int jj = sseg[k];
@@ -640,6 +669,32 @@ __device__ void local_subtrees(const BuildArgs& a, TS& tmp, unsigned char* lsm, 
         if (lane == 0) {
           s_ns = run;
           s_cbase = run ? atomicAdd(a.kcount, 2 * run) : 0;
+        }
+      }
+      __syncthreads();
+      // children's bounds: one warp per child over its contiguous positions (after the
+      // swaps above), the same min / max keys as the reference's bounds pass
+      for (int c2 = tid >> 5; c2 < 2 * ncur; c2 += kPB / 32) {
+        const int jj = c2 >> 1, side = c2 & 1;
+        if (!nds[jj]) continue;
+        const int bg = nbg[jj], cn = ncn[jj], l = nlc[jj];
+        const int k0 = side ? bg + l : bg, k1 = side ? bg + cn : bg + l;
+        for (int d = 0; d < D; ++d) {
+          unsigned long long mn = ~0ull, mx = 0ull;
+          for (int k = k0 + lane; k < k1; k += 32) {
+            const unsigned long long kk = dkey(X[(size_t)sp[k] * D + d]);
+            mn = min(mn, kk);
+            mx = max(mx, kk);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          }
+          if (lane == 0) {
+            kmn[c2 * D + d] = mn;
+            kmx[c2 * D + d] = mx;
+          }
         }
       }
       __syncthreads();
@@ -699,7 +754,12 @@ __device__ void local_subtrees(const BuildArgs& a, TS& tmp, unsigned char* lsm, 
       ncur = 2 * ns;
       ++lev;
     }
-    for (int k = tid; k < c; k += kPB) a.perm[b0 + k] = sp[k];
+#ifdef DFGTB_TREE_DEBUG
+    unsigned long long t1_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1_));
+    if (tid == 0) printf("TREEDBG subtree %d: %d points, %d local levels, max %d nodes/level, %d equal-key nodes, %.1f us\n", j, c, levels_, maxnodes_, eqn_, (t1_ - t0_) * 1e-3);
+#endif
+    for (int k = tid; k < c; k += kPB) a.perm[b0 + k] = cache ? gid[sp[k]] : sp[k];
     __syncthreads();
   }
 }
@@ -804,9 +864,13 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
     const int* dsp = a.dosplit + (level & 1) * NBL;  // this level's split flags / midpoints
     const double* mdp = a.mid + (level & 1) * NBL;
     if (a.local_S > 0 && level > 0 && __ldcg(&a.lvlmax[level]) <= a.local_S) {
-      // every subtree below this level fits one CTA's shared memory: build them there
-      extern __shared__ __align__(16) unsigned char lsm[];
-      local_subtrees(a, tmp, lsm, base, m, level, dsp, mdp);
+      // every subtree below this level fits one CTA's shared memory: k_build_local builds
+      // them there, one subtree per CTA (more, smaller CTAs than this kernel's)
+      if (gt == 0) {
+        a.loc[0] = base;
+        a.loc[1] = m;
+        a.loc[2] = level;
+      }
       local = true;
       break;
     }
@@ -1021,6 +1085,22 @@ __global__ void __launch_bounds__(kPB, 1) k_build(const __grid_constant__ BuildA
   }
 }
 
+// The CTA-local subtree phase, launched after k_build (which stops at the level where
+// every splitting node holds <= local_S points): one kLocalThreads CTA per subtree.
+constexpr int kLocalThreads = 512;
+__global__ void __launch_bounds__(kLocalThreads) k_build_local(const __grid_constant__ BuildArgs a)
+{
+  const int m = a.loc[1];
+  if (m == 0) return;
+  const int base = a.loc[0], level = a.loc[2];
+  const size_t NBL = (size_t)a.n + 1;
+  using BS = cub::BlockScan<int, kLocalThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  extern __shared__ __align__(16) unsigned char lsm[];
+  local_subtrees<kLocalThreads>(a, tmp, lsm, base, m, level, a.dosplit + (level & 1) * NBL,
+                                a.mid + (level & 1) * NBL);
+}
+
 }  // namespace
 
 // Preorder renumbering and the preorder device/host arrays, from BFS-indexed arrays.
@@ -1045,8 +1125,9 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
   static const int local_env = std::getenv("DFGTB_TREE_LOCAL") ? std::atoi(std::getenv("DFGTB_TREE_LOCAL")) : -1;
   const int local_cap = local_env >= 0 ? std::min(local_env, kLS) : kLS;
   const int local_S = (local_env == 0 || D > kLMaxD) ? 0 : (int)std::min<long long>(local_cap, (long long)kLN * (leaf + 1) / 2);
-  const int smem = local_S >= 512 ? local_smem_bytes(D) : 0;
-  if (smem) CK(cudaFuncSetAttribute(k_build, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int lsmem = local_S >= 512 ? local_smem_bytes(D) : 0;  // k_build_local
+  if (lsmem) CK(cudaFuncSetAttribute(k_build_local, cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem));
+  const int smem = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_build, kPB, smem));
   if (!coop || per_sm < 1) return false;
   // CTAs: 64 for small sets (measured: cheaper grid barriers, enough threads), one
@@ -1083,7 +1164,11 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
                kmax.p, pslot.p, mid.p, dosplit.p, child.p, lc.p, ctot.p, lvl.p };
   a.lvlmax = lvlmax.p;
   a.kcount = kcount.p;
-  a.local_S = smem ? local_S : 0;
+  a.local_S = lsmem ? local_S : 0;
+  DevBuf<int> loc;
+  loc.reserve(4);
+  CK(cudaMemsetAsync(loc.p, 0, sizeof(int) * 4, s));
+  a.loc = loc.p;
   static const bool tracing = std::getenv("DFGTB_TRACE") != nullptr;
   DevBuf<unsigned long long> trace;
   if (tracing) {
@@ -1095,6 +1180,16 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
   const auto c0 = std::chrono::steady_clock::now();
   CK(cudaLaunchCooperativeKernel((void*)k_build, G, kPB, kargs, smem, s));
   CK_LAUNCH();
+  if (lsmem) {
+    static int lgrid = 0;
+    if (!lgrid) {
+      int lper = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lper, k_build_local, kLocalThreads, lsmem));
+      lgrid = nsm * std::max(1, lper);
+    }
+    k_build_local<<<lgrid, kLocalThreads, lsmem, s>>>(a);
+    CK_LAUNCH();
+  }
   if (tracing) {
     std::vector<unsigned long long> tr(64 * 8);
     CK(cudaMemcpyAsync(tr.data(), trace.p, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost, s));
