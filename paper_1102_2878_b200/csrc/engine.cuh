@@ -119,6 +119,7 @@ private:
   void launch_phases(const DevTree& qt, const double* h, int nb, double* d_out);
   void eager_moments();
   void setup_leaves(const DevTree& t);
+  void start_frontier(const DevTree& qt, void* trav_args);
 
   Config cfg_;
   int dev_ = -1;  // device the engine was created on (made current by every entry point)
@@ -165,6 +166,7 @@ private:
   int capEA_ = 0, capPA_ = 0;    // async: total entries / pairs of a batch (grown on overflow)
   DevBuf<int> aready_;           // async: per entry slot published flag
   DevBuf<int> actr_;             // async: padded counters
+  DevBuf<int> sfront_;           // start frontier node lists (DFGTB_TRAV_START_DEPTH)
   DevBuf<unsigned char> adepth_; // async: per entry slot level
   DevBuf<unsigned long long> atrace_;  // DFGTB_ASYNC_TRACE builds
   bool use_persistent_ = true;  // one cooperative kernel runs every level

@@ -2273,7 +2273,6 @@ void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int 
     gridA = persistent_grid(k_base_f32<DT>, threadsA, smemA, slack, INT32_MAX / 2, F32Geo<DT>::WARPS);
   }
   const int cap_grid = (tcap + 3) / 4;
-  int* listA = ws + 8;
   int* listB = ws + 8 + tcap;
   (void)ntasks;  // the lists were built by k_task_split (launch_phases)
   if ((mufu & 2) && cc.s3) {

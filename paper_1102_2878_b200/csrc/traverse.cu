@@ -215,6 +215,9 @@ struct TravArgs {
   Item *itF, *itDT, *itB;
   int *cntF, *cntDT, *cntB;
   unsigned long long* trace;  // optional per-phase %globaltimer stamps (DFGTB_TRACE)
+  const int* sq;              // start frontier: query nodes (nsq) x reference nodes (nsr)
+  const int* sr;              //   (nullptr: the roots); see Engine::start_frontier
+  int nsq, nsr;
   Cnt* lvlcnt;                // per-level output counters of k_traverse (zeroed per launch)
   unsigned long long* lvlep;  // per-level packed (entries << 32 | pairs) counters
 };
@@ -267,19 +270,27 @@ __global__ void k_trav_init(const __grid_constant__ TravArgs a)
 {
   TravState& st = *a.st;
   const int nb = st.nslots;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-    a.fq[0][b] = b * st.K;
-    a.foff[0][b] = b;
-    a.flen[0][b] = 1;
-    a.fbase[0][b] = 0.0;
-    a.fr[0][b] = 0;
-    a.pent[0][b] = b;
-    for (int k = 0; k < sNStat; ++k) st.sst[b][k] = 0;
+  // start frontier: every (slot, query start node) entry pairs with every reference start
+  // node (the roots unless a start depth is set: the levels above it are skipped -- a
+  // valid dual-tree traversal whose first lower bounds already sum over many nodes)
+  const int nq = a.sq ? a.nsq : 1, nr = a.sq ? a.nsr : 1;
+  for (int e = threadIdx.x; e < nb * nq; e += blockDim.x) {
+    const int b = e / nq, qi = e - b * nq;
+    a.fq[0][e] = b * st.K + (a.sq ? a.sq[qi] : 0);
+    a.foff[0][e] = e * nr;
+    a.flen[0][e] = nr;
+    a.fbase[0][e] = 0.0;
   }
+  for (int j = threadIdx.x; j < nb * nq * nr; j += blockDim.x) {
+    a.fr[0][j] = a.sq ? a.sr[j % nr] : 0;
+    a.pent[0][j] = j / nr;
+  }
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+    for (int k = 0; k < sNStat; ++k) st.sst[b][k] = 0;
   if (threadIdx.x == 0) {
     st.cur = 0;
-    st.m[0] = nb;
-    st.p[0] = nb;
+    st.m[0] = nb * nq;
+    st.p[0] = nb * nq * nr;
     st.m[1] = st.p[1] = 0;
     st.nF = st.nDT = st.nB = 0;
     st.xF = st.xDT = st.xB = 0;
@@ -1513,14 +1524,14 @@ __global__ void k_async_finish(const __grid_constant__ TravArgs a, AsyncQ q)
 __global__ void k_async_init(const __grid_constant__ TravArgs a, AsyncQ q)
 {
   TravState& st = *a.st;
-  const int nb = st.nslots;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+  const int m0 = st.m[0], p0 = st.p[0];  // the start frontier (k_trav_init)
+  for (int b = threadIdx.x; b < m0; b += blockDim.x) {
     q.ready[b] = 1;
     q.depth[b] = 0;
   }
   if (threadIdx.x < acNum) {
     const int k = threadIdx.x;
-    *q.c(k) = k == acTail || k == acPool || k == acPending ? nb : 0;
+    *q.c(k) = k == acTail || k == acPending ? m0 : k == acPool ? p0 : 0;
   }
   if (threadIdx.x == 0) st.levels = 1;
 }
@@ -1554,7 +1565,7 @@ __global__ void __launch_bounds__(kPBlock, kPerSM) k_traverse(const __grid_const
     s_scale[i] = st.scale[i];
   }
   __syncthreads();
-  int cur = 0, m = nslots, p = nslots, gF = 0, gDT = 0, gB = 0, levels = 0;
+  int cur = 0, m = st.m[0], p = st.p[0], gF = 0, gDT = 0, gB = 0, levels = 0;
   // DFGTB_TRACE: per-phase %globaltimer stamps of CTA 0 (trace[4096 + 16 L + k])
 #define PH(k)                                                                                   \
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && levels < 512) {                       \
@@ -2005,6 +2016,57 @@ __global__ void k_scatter_dev(const Item* in, const int* n, int cap, const int* 
   }
 }
 
+// Start frontier of the traversal: the nodes at depth d0 (DFGTB_TRAV_START_DEPTH, default
+// 5; 0 = the roots) and the leaves above it, of the query and of the reference tree.  The
+// top levels of the level loop hold few pairs but cost a full level each (~15 us of
+// barriers and dependent loads); starting below them is still a dual-tree traversal of a
+// partition of Q x R, so the lower bounds and the eps guarantee hold unchanged.
+static void frontier_nodes(const DevTree& t, int d0, std::vector<int>& out)
+{
+  out.clear();
+  // preorder ids: the right child follows the left subtree; a node is in the frontier
+  // if its depth is d0, or it is a leaf above that depth
+  std::vector<std::pair<int, int>> stack{ { 0, 0 } };
+  std::vector<int> sub(t.nodes, 1);
+  for (int i = t.nodes - 1; i >= 0; --i)
+    if (t.h_left[i] >= 0) sub[i] = 1 + sub[t.h_left[i]] + sub[t.h_left[i] + sub[t.h_left[i]]];
+  while (!stack.empty()) {
+    const auto [v, d] = stack.back();
+    stack.pop_back();
+    if (d == d0 || t.h_left[v] < 0) {
+      out.push_back(v);
+      continue;
+    }
+    const int l = t.h_left[v], r = l + sub[l];
+    stack.push_back({ r, d + 1 });
+    stack.push_back({ l, d + 1 });
+  }
+}
+
+void Engine::start_frontier(const DevTree& qt, void* args)
+{
+  TravArgs& a = *static_cast<TravArgs*>(args);
+  // measured (cfg2 sweep): depth 0 1.47 ms, 3 1.43, 4 1.39, 5 1.37, 6 1.38; cfg3 neutral
+  static const int d0 = std::getenv("DFGTB_TRAV_START_DEPTH") ? std::atoi(std::getenv("DFGTB_TRAV_START_DEPTH")) : 5;
+  a.sq = a.sr = nullptr;
+  a.nsq = a.nsr = 1;
+  // only deep trees have top levels worth skipping (a shallow tree keeps the reference's
+  // schedule, e.g. a loose eps still prunes the root pair alone)
+  const int d = std::min(d0, std::min(qt.height, rt_.height) - 10);
+  if (d <= 0) return;
+  std::vector<int> qn, rn;
+  frontier_nodes(qt, d, qn);
+  frontier_nodes(rt_, d, rn);
+  std::vector<int> both(qn);
+  both.insert(both.end(), rn.begin(), rn.end());
+  sfront_.reserve(both.size());
+  CK(cudaMemcpyAsync(sfront_.p, both.data(), sizeof(int) * both.size(), cudaMemcpyHostToDevice, s_));
+  a.sq = sfront_.p;
+  a.sr = sfront_.p + qn.size();
+  a.nsq = (int)qn.size();
+  a.nsr = (int)rn.size();
+}
+
 // Launches the whole traversal of a batch and the counting sorts of its work items
 // WITHOUT a host round trip: the counts stay on the device (bc_), the host reads them
 // once at the end of the batch (traverse_finish) and reruns on overflow.
@@ -2152,7 +2214,8 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   hs->capDT = capDT_;
   hs->capB = capB_;
   CK(cudaMemcpyAsync(ds, hs, sizeof(TravState), cudaMemcpyHostToDevice, s));
-  k_trav_init<<<1, 64, 0, s>>>(a);
+  start_frontier(qt, &a);
+  k_trav_init<<<1, 256, 0, s>>>(a);
   CK_LAUNCH();
   if (use_async_) {
     actr_.reserve(acNum * kAsyncCtr);

@@ -149,7 +149,10 @@ class DualTreeEngine:
 
     def close(self):
         if getattr(self, "_h", None):
-            lib.dfgtb_destroy(self._h)
+            try:
+                lib.dfgtb_destroy(self._h)
+            except (AttributeError, TypeError):  # interpreter shutdown: the library is gone
+                pass
             self._h = None
 
     def __del__(self):
