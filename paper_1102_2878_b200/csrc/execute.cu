@@ -1063,14 +1063,17 @@ __device__ __forceinline__ void base_groups_mufu(const double* rs, int n, const 
 // the pair loop.  Terms below 2^-126 flush to 0 (absolute error <= N 2^-126 against sums
 // >= 1e-20).  The self pair (Q = R) is exactly 1: q~ - q~ = 0.
 // Per-term relative error for z <= 127 (|q| <= 75, |r| <= 75 + sqrt z, unit roundoff
-// u = 2^-24):
-//   coordinate rounding   |d(q - r)| <= u (|q| + |r|)               -> 2 sqrt(z) u (150 + sqrt z)
-//   differences           |d a_d| <= u |a_d|                         -> 2 z u
-//   squares and sums      D roundings of partial sums <= 127         -> D 127 u
-//   -> |dz| <= 2 sqrt(127) (150 + 2 sqrt(127)) u + 5 127 u = 2.70e-4 at D = 5,
-//   |dz| ln 2 <= 1.87e-4 relative, + ex2.approx (< 2^-22, measured exhaustively by
-//   dfgtb_f32_exp_error) + FP32 partial sums (<= 8 terms per lane + 5 reduction levels:
-//   12 u = 7.2e-7): below kF32Charge = 2e-4, which the traversal pays for.
+// u = 2^-24; z = sum_d a_d^2 with a_d = q~_d - r~_d):
+//   coordinate rounding   |d(q - r)| <= u (|q| + |r|) <= u (150 + sqrt z)
+//                         -> |dz| <= 2 sqrt(z) u (150 + sqrt z)
+//   differences           a~_d = a_d (1 + d), |d| <= u        -> |dz| <= 2 z u
+//   squares and sums      D roundings of partial sums <= z     -> |dz| <= D z u
+//   total at z = 127, D = 5:
+//     2 sqrt(127) (150 + sqrt(127)) u + 2 127 u + 5 127 u
+//       = 3635 u + 254 u + 635 u = 4524 u = 2.70e-4 = 2 sqrt(127) (150 + 2 sqrt(127)) u + 5 127 u,
+//   |dz| ln 2 <= 1.87e-4 relative, + ex2.approx (< 2^-22 = 2.4e-7, measured exhaustively by
+//   dfgtb_f32_exp_error) + FP32 partial sums (<= 8 roundings per lane + 5 reduction levels:
+//   13 u = 7.7e-7): 1.88e-4 < kF32Charge = 2e-4, which the traversal pays for.
 template <int DT>
 struct FPt {
   static constexpr int DF = DT <= 4 ? 4 : 8;  // floats per point (coordinates, pad)
