@@ -55,14 +55,19 @@ constexpr int kMaxSlots = 64;  // bandwidths per batch
 // keep the FP64 exp (<= ~1 ulp).
 constexpr double kMufuMinEps = 1e-4;
 constexpr double kMufuCharge = 4e-6;
-// FP32 base case (execute.cu FPt / base_group_f32): FP32 differences, distance and
-// partial sums, ex2.approx.f32 of the whole argument.  Applies to leaf pairs whose query leaf's
-// box diagonal is <= kF32Diam in units where |q - r|^2 = z = log2 e |q - r|^2 / 2h^2 and whose sums are >= 1e-20 (or
-// Q = R); per-term relative error < kF32Charge (derivation at FPt).  Used when
-// eps >= kF32MinEps (the charge is then <= 5% of the budget) unless DFGTB_NO_F32 is set.
+// FP32 base case (execute.cu FPt / base_tile_f32x2): FP32 differences, distance and
+// partial sums, ex2.approx.f32 of the whole (shifted) argument.  Applies to leaf pairs whose
+// query leaf's box diagonal is <= kF32Diam in units where |q - r|^2 = z = log2 e |q - r|^2 / 2h^2
+// and whose sums are >= 1e-20 (or Q = R with a leave-one-out floor G - 1 >= 2^-kF32LooZ);
+// per-term relative error < kF32Charge (derivation at FPt).  Terms are formed as
+// 2^(kF32Shift - z) and scaled back by kF32Unshift per tile.  Used when eps >= kF32MinEps
+// (the charge is then <= 5% of the budget) unless DFGTB_NO_F32 is set.
 constexpr double kF32MinEps = 5e-3;
 constexpr double kF32Charge = 2e-4;
 constexpr double kF32Diam = 150.0;
+constexpr float kF32Shift = 64.0f;
+constexpr double kF32Unshift = 0x1p-64;
+constexpr double kF32LooZ = 128.0;
 
 int default_p_max(int D);
 

@@ -1056,24 +1056,34 @@ __device__ __forceinline__ void base_groups_mufu(const double* rs, int n, const 
 
 // FP32 base case (leaf pairs the traversal flagged with order bit 2: the query leaf's box
 // diagonal is <= kF32Diam = 150 in units where |q - r|^2 = z, and the query sums are
-// provably >= 1e-20 or Q = R).  Points are centred on the query leaf's box centre in FP64
-// (every query within 75 of it) and rounded to FP32 (q~, r~), and per pair
-//   z = sum_d (q~_d - r~_d)^2,   term = ex2.approx.ftz(-z),
-// D FP32 subtractions, D multiply-adds, one MUFU and one FP32 add: no FP64 instruction in
-// the pair loop.  Terms below 2^-126 flush to 0 (absolute error <= N 2^-126 against sums
-// >= 1e-20).  The self pair (Q = R) is exactly 1: q~ - q~ = 0.
+// provably >= 1e-20, or Q = R with a leave-one-out floor G - 1 >= 2^-128).  Points are
+// centred on the query leaf's box centre in FP64 (every query within 75 of it) and rounded
+// to FP32 (q~, r~), and per pair
+//   z' = sum_d (q~_d - r~_d)^2 - S,   term = ex2.approx.ftz(-z') = 2^S 2^-z,   S = kF32Shift = 64,
+// D FP32 subtractions, D multiply-adds (the first one adds -S), one MUFU and one FP32 add:
+// no FP64 instruction in the pair loop; each tile's FP32 sum is scaled back by 2^-S
+// exactly in FP64.  The shift keeps terms down to 2^-190 (z <= 190) out of the flush
+// range at no cost (sums of <= 256 terms <= 2^S per tile stay below 2^72).  Terms below
+// 2^-190 flush to 0: absolute error <= |R| 2^-190, against sums >= 1e-20 (Q != R) or a
+// leave-one-out sum >= 2^-128 (Q = R; <= |R| 2^-62 relative).  Q = R: the self pairs
+// are masked out of the FP32 sums (their tiles run the SELF variant) and K(0) = 1 is
+// added exactly in FP64 at the end, so the partial sums hold only G - 1, to 13 u relative.
 // Per-term relative error for z <= 127 (|q| <= 75, |r| <= 75 + sqrt z, unit roundoff
 // u = 2^-24; z = sum_d a_d^2 with a_d = q~_d - r~_d):
 //   coordinate rounding   |d(q - r)| <= u (|q| + |r|) <= u (150 + sqrt z)
 //                         -> |dz| <= 2 sqrt(z) u (150 + sqrt z)
 //   differences           a~_d = a_d (1 + d), |d| <= u        -> |dz| <= 2 z u
-//   squares and sums      D roundings of partial sums <= z     -> |dz| <= D z u
+//   squares and sums      D roundings of partial sums, each <= max(z, S) <= 127
+//                                                              -> |dz| <= D 127 u
 //   total at z = 127, D = 5:
 //     2 sqrt(127) (150 + sqrt(127)) u + 2 127 u + 5 127 u
 //       = 3635 u + 254 u + 635 u = 4524 u = 2.70e-4 = 2 sqrt(127) (150 + 2 sqrt(127)) u + 5 127 u,
-//   |dz| ln 2 <= 1.87e-4 relative, + ex2.approx (< 2^-22 = 2.4e-7, measured exhaustively by
-//   dfgtb_f32_exp_error) + FP32 partial sums (<= 8 roundings per lane + 5 reduction levels:
-//   13 u = 7.7e-7): 1.88e-4 < kF32Charge = 2e-4, which the traversal pays for.
+//   |dz| ln 2 <= 1.87e-4 relative, + ex2.approx (< 2^-22 = 2.4e-7 over every argument in
+//   [-126, S], measured exhaustively by dfgtb_f32_exp_error) + FP32 partial sums (<= 8
+//   roundings per lane + 5 reduction levels: 13 u = 7.7e-7): 1.88e-4 < kF32Charge = 2e-4,
+//   which the traversal pays for.  Terms with 127 < z <= 190 (below 2^-127 each) carry up
+//   to 2.5e-4 relative error but weigh at most |R| 2^-127 against G >= 1e-20 (Q != R) or
+//   G >= 1 (Q = R): below 1e-15 of G, inside the charge's margin.
 template <int DT>
 struct FPt {
   static constexpr int DF = DT <= 4 ? 4 : 8;  // floats per point (coordinates, pad)
@@ -1105,12 +1115,12 @@ __device__ __forceinline__ float ex2_ftz(float t)
   return g;
 }
 
-// z = |q~ - r~|^2 in FP32, in the loop's order
+// z - kF32Shift = |q~ - r~|^2 - 64 in FP32, in the loop's order
 template <int DT>
 __device__ __forceinline__ float f32_z(const float* q, const float* r)
 {
   const float a0 = q[0] - r[0];
-  float z = a0 * a0;
+  float z = fmaf(a0, a0, -kF32Shift);
 #pragma unroll
   for (int d = 1; d < DT; ++d) {
     const float a = q[d] - r[d];
@@ -1119,16 +1129,15 @@ __device__ __forceinline__ float f32_z(const float* q, const float* r)
   return z;
 }
 
-// One FP32 pair term exactly as the loop forms it (tests).
+// One FP32 pair term exactly as the loop forms it, still scaled by 2^kF32Shift (tests).
 template <int DT>
 __device__ __forceinline__ float f32_term(const float* q, const float* r)
 {
   return ex2_ftz(-f32_z<DT>(q, r));
 }
 
-// GG queries (1..16) per lane against the tile's reference points (lanes over points);
-// the GG partial sums are combined across the warp by a transpose-reduction over the
-// next power of two P2 (padding sums are 0), in a fixed order.
+// P2 partial sums per lane (lanes over points) combined across the warp by a
+// transpose-reduction in a fixed order: lane l ends with the sum of value l >> (5 - LG).
 template <int P2, int LG>
 __device__ __forceinline__ float transpose_reduce(float (&acc)[P2], int lane)
 {
@@ -1149,84 +1158,6 @@ __device__ __forceinline__ float transpose_reduce(float (&acc)[P2], int lane)
 #pragma unroll
   for (int off = 16 >> LG; off >= 1; off >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
   return acc[0];
-}
-
-template <int DT, int GG>
-__device__ __forceinline__ void base_group_f32(const float* rs, int n, const float* qs, double* qsum,
-                                               int lane)
-{
-  constexpr int D = DT, DF = FPt<DT>::DF;
-  constexpr int P2 = GG <= 1 ? 1 : GG <= 2 ? 2 : GG <= 4 ? 4 : GG <= 8 ? 8 : 16;
-  constexpr int LG = P2 == 16 ? 4 : P2 == 8 ? 3 : P2 == 4 ? 2 : P2 == 2 ? 1 : 0;
-  float m[GG][D], acc[P2];
-#pragma unroll
-  for (int i = 0; i < GG; ++i)
-#pragma unroll
-    for (int d = 0; d < D; ++d) m[i][d] = qs[i * DF + d];
-#pragma unroll
-  for (int i = 0; i < P2; ++i) acc[i] = 0.f;
-  auto body = [&](int j) {
-    float r[DF];
-    FPt<DT>::load(rs, j, r);
-    float z[GG];
-#pragma unroll
-    for (int i = 0; i < GG; ++i) {
-      const float a = m[i][0] - r[0];
-      z[i] = a * a;
-    }
-#pragma unroll
-    for (int d = 1; d < D; ++d)
-#pragma unroll
-      for (int i = 0; i < GG; ++i) {
-        const float a = m[i][d] - r[d];
-        z[i] = fmaf(a, a, z[i]);
-      }
-#pragma unroll
-    for (int i = 0; i < GG; ++i) acc[i] += ex2_ftz(-z[i]);
-  };
-  const int nfull = n & ~31;
-  int j = lane;
-  for (; j < nfull; j += 32) body(j);
-  if (j < n) body(j);
-  const double v = (double)transpose_reduce<P2, LG>(acc, lane);
-  const int qi = lane >> (5 - LG);
-  if ((lane & ((32 >> LG) - 1)) == 0 && qi < GG) qsum[qi] += v;
-}
-
-template <int DT, int GG>
-__device__ __noinline__ void base_group_f32_call(const float* rs, int n, const float* qs, double* qsum,
-                                                 int lane)
-{
-  base_group_f32<DT, GG>(rs, n, qs, qsum, lane);
-}
-
-template <int DT>
-__device__ __forceinline__ void base_group_f32_n(const float* rs, int n, const float* q, double* qq, int g,
-                                                 int lane)
-{
-  switch (g) {
-  case 1: base_group_f32_call<DT, 1>(rs, n, q, qq, lane); break;
-  case 2: base_group_f32_call<DT, 2>(rs, n, q, qq, lane); break;
-  case 3: base_group_f32_call<DT, 3>(rs, n, q, qq, lane); break;
-  case 4: base_group_f32_call<DT, 4>(rs, n, q, qq, lane); break;
-  case 5: base_group_f32_call<DT, 5>(rs, n, q, qq, lane); break;
-  case 6: base_group_f32_call<DT, 6>(rs, n, q, qq, lane); break;
-  case 7: base_group_f32_call<DT, 7>(rs, n, q, qq, lane); break;
-  case 8: base_group_f32_call<DT, 8>(rs, n, q, qq, lane); break;
-  default: break;
-  }
-}
-
-// Queries in groups of 8, the remainder (1..7) as ONE group of its exact size (measured:
-// near-equal group sizes, e.g. 21 -> 7 + 7 + 7, are 7% slower).
-template <int DT>
-__device__ __forceinline__ void base_groups_f32(const float* rs, int n, const float* qs, double* qsum,
-                                                int qc, int lane)
-{
-  constexpr int DF = FPt<DT>::DF;
-  int g0 = 0;
-  for (; g0 + 8 <= qc; g0 += 8) base_group_f32_call<DT, 8>(rs, n, qs + g0 * DF, qsum + g0, lane);
-  base_group_f32_n<DT>(rs, n, qs + g0 * DF, qsum + g0, qc - g0, lane);
 }
 
 // Queries in groups of G, the remainder in groups of 4, 2, 1.  Each group size is one
@@ -1334,7 +1265,7 @@ __device__ __forceinline__ void stream_passes(unsigned* smask, int ni, int skk, 
       }
     }
     __syncwarp();
-    groups(n);
+    groups(n, c0);
     __syncwarp();
   }
 }
@@ -1391,7 +1322,7 @@ __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
         if (mf) MPt<DT>::stage(p, cq, rs, pos);
         else p.store(rs, pos);
       },
-      [&](int n) {
+      [&](int n, int) {
         if (mf && fast) base_groups_mufu<DT, false>(rs, n, qs, qsum, v.qc, lane);
         else if (mf) base_groups_mufu<DT, true>(rs, n, qs, qsum, v.qc, lane);
         else if (fast) base_groups<DT, true>(rs, n, qs, qsum, v.qc, tab, 1.0, lane);
@@ -1482,23 +1413,27 @@ struct F2Pt {
 };
 
 // One tile of n <= RMAX points against the chunk's qc queries; adds each query's tile sum
-// to qsum (FP64).
-template <int DT>
+// (scaled back by 2^-S) to qsum (FP64).  SELF: query k's own point sits at tile position
+// sb + k (Q = R); those pairs are masked to 0 (the caller adds K(0) = 1 exactly).
+template <int DT, bool SELF>
 __device__ __forceinline__ void base_tile_f32x2(const float* rs, int n, const float* qs, double* qsum, int qc,
-                                                int lane)
+                                                int lane, int sb)
 {
   constexpr int P = F2Pt<DT>::P;
   constexpr int KB = DFGTB_F32_KB;  // query pairs per branch-free block
   const float2* q2 = reinterpret_cast<const float2*>(qs);
   const int np = (qc + 1) >> 1;
+  const float2 mS = make_float2(-kF32Shift, -kF32Shift);
   float2 acc[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = make_float2(0.f, 0.f);
   for (int c = 0; c < n; c += 32 * P) {
     float2 r[P][DT];
+    int dl[P];  // SELF: the chunk query whose own point point p is
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       const int j = c + 32 * p + lane;
+      if constexpr (SELF) dl[p] = j - sb;
       if (j < n) F2Pt<DT>::load(rs, j, r[p]);
       else
 #pragma unroll
@@ -1516,13 +1451,17 @@ __device__ __forceinline__ void base_tile_f32x2(const float* rs, int n, const fl
 #pragma unroll
           for (int p = 0; p < P; ++p) {
             float2 a = __fadd2_rn(q[0], r[p][0]);
-            float2 z = __fmul2_rn(a, a);
+            float2 z = __ffma2_rn(a, a, mS);
 #pragma unroll
             for (int d = 1; d < DT; ++d) {
               a = __fadd2_rn(q[d], r[p][d]);
               z = __ffma2_rn(a, a, z);
             }
             e[p] = make_float2(ex2_ftz(-z.x), ex2_ftz(-z.y));
+            if constexpr (SELF) {
+              if (dl[p] == 2 * (k + kk)) e[p].x = 0.f;
+              if (dl[p] == 2 * (k + kk) + 1) e[p].y = 0.f;
+            }
           }
           // the P terms by a fixed tree, then into the accumulator
 #pragma unroll
@@ -1554,7 +1493,7 @@ __device__ __forceinline__ void base_tile_f32x2(const float* rs, int n, const fl
 #pragma unroll
     for (int l = 0; l < w; ++l) c32[l] += c32[l + w];
   __syncwarp();
-  if (lane < qc) qsum[lane] += (double)c32[0];
+  if (lane < qc) qsum[lane] += (double)c32[0] * kF32Unshift;
 #else
   float a32[32];
 #pragma unroll
@@ -1563,7 +1502,7 @@ __device__ __forceinline__ void base_tile_f32x2(const float* rs, int n, const fl
     a32[2 * k + 1] = acc[k].y;
   }
   const float v = transpose_reduce<32, 5>(a32, lane);  // lane l: query l's tile sum
-  if (lane < qc) qsum[lane] += (double)v;
+  if (lane < qc) qsum[lane] += (double)v * kF32Unshift;  // 2^-S, exact
 #endif
 }
 
@@ -1663,20 +1602,30 @@ __global__ void __launch_bounds__(F32Geo<DT>::WARPS * 32, DFGTB_BF32_MINB)
     F2Pt<DT>::stage_q(qsrc, lane, v.qc, cq, qs);
     qsum[lane] = 0.0;
     const double* xrs = xr + (size_t)v.slot * nr * DP;
+    // Q = R: the item that is the query leaf itself holds every query's self pair, at
+    // stream position sself + k for chunk query k
+    int sself = -1;
+    if (xq == xr) {
+      const unsigned bm = __ballot_sync(0xffffffffu, lane < v.nit && v.rc.x == v.qb);
+      if (bm) sself = __shfl_sync(0xffffffffu, v.sk, __ffs(bm) - 1) + mc.q0;
+    }
 #if defined(DFGTB_EXP_NOSTAGE)  // timing experiments only (results wrong)
-    for (int c0t = 0; c0t < v.total; c0t += RMAX) base_tile_f32x2<DT>(rs, min(RMAX, v.total - c0t), qs, qsum, v.qc, lane);
+    for (int c0t = 0; c0t < v.total; c0t += RMAX)
+      base_tile_f32x2<DT, false>(rs, min(RMAX, v.total - c0t), qs, qsum, v.qc, lane, 0);
 #else
     stream_passes<RMAX, stage_batch(DT)>(
       smask, v.nit, v.sk, v.okk, v.total, lane, [&](int src) { return FPt<DT>::load_raw(xrs, src); },
       [&](const typename FPt<DT>::Raw& p, int pos) { F2Pt<DT>::store(p, cq, rs, pos); },
-      [&](int n) {
+      [&](int n, int c0t) {
 #if !defined(DFGTB_EXP_NOCOMPUTE)
-        base_tile_f32x2<DT>(rs, n, qs, qsum, v.qc, lane);
+        const int sb = sself - c0t;  // tile position of chunk query 0's own point
+        if (sself >= 0 && sb < n && sb + v.qc > 0) base_tile_f32x2<DT, true>(rs, n, qs, qsum, v.qc, lane, sb);
+        else base_tile_f32x2<DT, false>(rs, n, qs, qsum, v.qc, lane, 0);
 #endif
       });
 #endif
     __syncwarp();
-    if (lane < v.qc) part[(size_t)mc.w * 32 + lane] = qsum[lane];
+    if (lane < v.qc) part[(size_t)mc.w * 32 + lane] = qsum[lane] + (sself >= 0 ? 1.0 : 0.0);  // + K(0) exactly
     __syncwarp();
     i = inext;
   }
@@ -2751,13 +2700,13 @@ double mufu_exp_max_error()
 }
 
 // Exhaustive relative error of ex2.approx.ftz.f32 over every FP32 argument in
-// [-126, 2^-10] (the FP32 base case's t = -z, rounding may push the self pair above 0)
-// against libdevice exp2 in FP64.  Max as ordered bits in *out.
+// [-126, S] (the FP32 base case's argument S - z; S = kF32Shift) against libdevice exp2
+// in FP64.  Max as ordered bits in *out.
 __global__ void k_f32_exp_check(unsigned long long* out)
 {
-  if (blockIdx.x == 0 && threadIdx.x == 0 && (ex2_ftz(-0.0f) != 1.0f || ex2_ftz(0.0f) != 1.0f))
-    atomicMax(out, 0x7FF0000000000000ull);  // the exact self term relies on ex2(-0) == 1
-  const unsigned lo_pos = 0u, hi_pos = __float_as_uint(0x1p-10f);   // [+0, 2^-10]
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (ex2_ftz(kF32Shift) != 0x1p64f || ex2_ftz(0.0f) != 1.0f))
+    atomicMax(out, 0x7FF0000000000000ull);  // coincident points (z = 0): exactly 2^S -> 1
+  const unsigned lo_pos = 0u, hi_pos = __float_as_uint(kF32Shift);  // [+0, S]
   const unsigned lo_neg = 0x80000001u, hi_neg = __float_as_uint(-126.0f);  // (-0, -126]
   const unsigned long long npos = hi_pos - lo_pos + 1ull, nneg = hi_neg - lo_neg + 1ull;
   unsigned long long worst = 0;
@@ -2789,15 +2738,15 @@ __global__ void k_f32_terms(const double* q, const double* r, const double* c, i
   float vq[DF], vr[DF];
   FPt<DT>::centred(FPt<DT>::load_raw(q, i), cc, vq);
   FPt<DT>::centred(FPt<DT>::load_raw(r, i), cc, vr);
-  // exactly as base_tile_f32x2 forms it: q~ + (-r~) packed, FMUL2 then FFMA2
+  // exactly as base_tile_f32x2 forms it: q~ + (-r~) packed, FFMA2 onto -S, FFMA2s, 2^-S
   float2 a = __fadd2_rn(make_float2(vq[0], vq[0]), make_float2(-vr[0], -vr[0]));
-  float2 z = __fmul2_rn(a, a);
+  float2 z = __ffma2_rn(a, a, make_float2(-kF32Shift, -kF32Shift));
 #pragma unroll
   for (int d = 1; d < DT; ++d) {
     a = __fadd2_rn(make_float2(vq[d], vq[d]), make_float2(-vr[d], -vr[d]));
     z = __ffma2_rn(a, a, z);
   }
-  out[i] = (double)ex2_ftz(-z.x);
+  out[i] = (double)ex2_ftz(-z.x) * kF32Unshift;
   if (ex2_ftz(-z.y) != ex2_ftz(-z.x) || ex2_ftz(-z.x) != f32_term<DT>(vq, vr)) out[i] = -1.0;  // lanes agree
 }
 

@@ -309,20 +309,31 @@ __global__ void k_trav_init(const __grid_constant__ TravArgs a)
 // sqrt(log2 e / 2) < 0.8494).  Bit 2: the FP32 base case applies: diameter <= kF32Diam
 // (every query within kF32Diam / 2 of the leaf's box centre), and for Q != R sums >=
 // G^l >= 1e-20 (its terms below 2^-126 flush to 0: <= |R| 2^-126 / 1e-20 < 1e-11
-// relative); for Q = R a provable leave-one-out floor G - 1 >= 2^-10 (from G^l, or from
-// a neighbour in the query leaf itself): the terms below 2^-126 that flush and the
-// <= 12 u G rounding of FP32 partial sums that hold the self term 1 stay below 1e-3
-// relative to the G - 1 the CV scores take logarithms of.
+// relative); for Q = R a provable leave-one-out floor G - 1 >= 2^-128 (from G^l, or from
+// a neighbour in the query leaf itself): the self pairs are masked out of the FP32 sums
+// (K(0) = 1 added exactly in FP64), the terms below 2^-190 that flush weigh <= |R| 2^-62
+// relative to the G - 1 the CV scores take logarithms of, FP32 rounding 13 u of it.
 __device__ __forceinline__ int base_flags(const TravArgs& a, double kmin, double glo, double sq, double h,
                                           int D, int nq, int Q)
 {
   const double dz = sq * sqrt((double)D) * 0.8494;
   // Q = R leave-one-out floor: every query of the leaf has a neighbour inside it with
-  // K >= 2^-10 (its nearest one within z = 10: log2 e d^2 / 2h^2 <= 10), so G - 1 >= 2^-10
-  const bool loo = glo >= 1.0 + 0x1p-10 ||
-                   (nq >= 2 && a.qnn2 && a.qnn2[Q] * 0.7213475204444817 <= 10.0 * h * h);
+  // K >= 2^-128 (its nearest one within z = 128: log2 e d^2 / 2h^2 <= 128), so G - 1 >= 2^-128
+  // (G^l can only show G - 1 >= 2^-40 above the self term's 1 in FP64)
+  const bool loo = glo >= 1.0 + 0x1p-40 ||
+                   (nq >= 2 && a.qnn2 && a.qnn2[Q] * 0.7213475204444817 <= kF32LooZ * h * h);
+#if defined(DFGTB_EXP_F32_NOLOO)  // experiments only: which condition keeps pairs off FP32
+  const bool loo_x = true;
+#else
+  const bool loo_x = loo;
+#endif
+#if defined(DFGTB_EXP_F32_DIAM)
+  const double diam_x = DFGTB_EXP_F32_DIAM;
+#else
+  const double diam_x = kF32Diam;
+#endif
   return (kmin >= 3.4e-308 ? 1 : 0) | ((a.selfq || glo >= 1e-290) && dz <= 1000.0 * h ? 2 : 0) |
-         (a.f32 && (a.selfq ? loo : glo >= 1e-20) && dz <= kF32Diam * h ? 4 : 0);
+         (a.f32 && (a.selfq ? loo_x : glo >= 1e-20) && dz <= diam_x * h ? 4 : 0);
 }
 
 // A group of W lanes, one frontier query node: kernel bounds of every live pair, the

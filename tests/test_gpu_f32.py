@@ -1,5 +1,7 @@
 """The FP32 base case (leaf pairs flagged with order bit 2, eps >= 5e-3): FP32 differences,
-ex2.approx.ftz.f32 of the whole argument, FP32 partial sums.  Its per-term relative
+ex2.approx.ftz.f32 of the whole argument shifted by S = 64 (terms 2^(S - z), scaled back
+by 2^-S per tile in FP64), FP32 partial sums, Q = R self pairs masked and K(0) = 1 added
+exactly.  Its per-term relative
 error must stay below kF32Charge = 2e-4, the share of eps the traversal pays for it
 (derivation at execute.cu FPt), and the engine must still meet eps per query.
 """
@@ -26,7 +28,7 @@ def _terms(d, q, r, c):
 
 
 def test_f32_exp_error_exhaustive():
-    """ex2.approx.ftz.f32 over every FP32 argument in [-126, 2^-10]."""
+    """ex2.approx.ftz.f32 over every FP32 argument in [-126, S = 64] (and 2^S exact)."""
     from paper_1102_2878_b200 import _capi
     err = _capi.lib.dfgtb_f32_exp_error()
     assert 0.0 <= err < 2.0 ** -21
@@ -68,17 +70,39 @@ def test_f32_terms_within_charge(d):
 
 
 def test_f32_far_terms_flush_to_zero():
-    """Terms with z >= 127 (below 2^-126) are 0 or below 2^-125: dropped mass only."""
+    """Terms with z >= 191 (below 2^-190) are 0 or below 2^-189: dropped mass only."""
     g = np.random.default_rng(7)
     d, n = 3, 10000
     c = np.zeros(d)
     q = g.uniform(-43.0, 43.0, (n, d))
     v = g.standard_normal((n, d))
     v /= np.linalg.norm(v, axis=1, keepdims=True)
-    z = 127.0 + g.exponential(2000.0, n)
+    z = 191.0 + g.exponential(2000.0, n)
     r = q + v * np.sqrt(z)[:, None]
     got = _terms(d, q, r, c)
-    assert np.all(got < 2.0 ** -125)
+    assert np.all(got < 2.0 ** -189)
+
+
+def test_f32_shift_keeps_small_terms():
+    """127 < z <= 185: terms below FP32's normal range survive (the shift), with a
+    relative error of at most ~2.6e-4 (the derivation's terms at z = 185; they weigh
+    <= |R| 2^-127 against G >= 1e-20, so the charge still holds)."""
+    g = np.random.default_rng(8)
+    d, n = 2, 20000
+    c = np.zeros(d)
+    u = g.standard_normal((n, d))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    q = c + u * 75.0 * g.random(n)[:, None]
+    v = g.standard_normal((n, d))
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    z = 127.0 + 58.0 * g.random(n)
+    r = q + v * np.sqrt(z)[:, None]
+    want = np.exp2(-np.sum((q - r) ** 2, axis=1))
+    got = _terms(d, q, r, c)
+    zz = 185.0
+    bound = (2 * np.sqrt(zz) * (150 + np.sqrt(zz)) + 2 * zz + d * zz) * U * np.log(2.0) + 2.0 ** -21
+    assert np.all(got > 0)
+    assert np.max(np.abs(got - want) / want) < bound
 
 
 @pytest.mark.parametrize("k", [2, 3, 5])
@@ -112,8 +136,8 @@ def test_f32_path_meets_eps_and_is_used(dfgtb, orc, k, monkeypatch):
 
 
 def test_f32_self_term_exact(dfgtb, orc, monkeypatch):
-    """Q = R where the FP32 path applies: the self pair is exactly 1 (q~ - q~ = 0), so
-    G >= 1 up to FP32 accumulation, an isolated point keeps G = 1 exactly, and every
+    """Q = R where the FP32 path applies: the self pair is masked out of the FP32 sums and
+    K(0) = 1 added exactly, so G >= 1, an isolated point keeps G = 1 exactly, and every
     sum is within eps of the exact one."""
     g = np.random.default_rng(3)
     x = np.vstack([g.random((3000, 2)) * 0.1, [[5.0, 5.0], [5.3, 5.0], [9.0, 9.0]]])
