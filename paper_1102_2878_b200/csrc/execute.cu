@@ -1232,9 +1232,14 @@ __device__ __forceinline__ TaskView task_view(const BTask& t, TreeView Q, int K,
 #ifndef DFGTB_STAGE_B
 #define DFGTB_STAGE_B 4  // measured: 8 spills and is 2% slower on cfg2
 #endif
+#ifndef DFGTB_STAGE_B3
+#define DFGTB_STAGE_B3 0  // D = 3 override (0: the rule below)
+#endif
 constexpr int stage_batch(int D)
 {
-  return (DFGTB_STAGE_B >> (D <= 2 ? 0 : D <= 4 ? 1 : 2)) > 0 ? (DFGTB_STAGE_B >> (D <= 2 ? 0 : D <= 4 ? 1 : 2)) : 1;
+  return D == 3 && DFGTB_STAGE_B3 > 0 ? DFGTB_STAGE_B3
+         : (DFGTB_STAGE_B >> (D <= 2 ? 0 : D <= 4 ? 1 : 2)) > 0 ? (DFGTB_STAGE_B >> (D <= 2 ? 0 : D <= 4 ? 1 : 2))
+                                                                 : 1;
 }
 template <int RMAX, int B, class Load, class Store, class Groups>
 __device__ __forceinline__ void stream_passes(unsigned* smask, int ni, int skk, int ok, int tot, int lane,
@@ -1348,51 +1353,63 @@ __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
   }
 }
 
-// ---- packed FP32x2 base case (Blackwell FADD2 / FMUL2 / FFMA2) ----------------------
+// ---- packed FP32x2 base case (Blackwell FADD2 / FFMA2) ------------------------------
 // Lanes own reference points (P per pass, registers); the warp walks the task's queries
 // in PAIRS: one packed instruction forms a coordinate difference for two queries against
-// one point, so per two (q, r) pairs the loop issues D FADD2 + 1 FMUL2 + (D - 1) FFMA2 +
-// 2 MUFU.EX2 + 1 FADD2 (accumulate): 3.5 issue slots per pair at D = 2 against the MUFU
-// rate's budget of 8.  The arithmetic per term is exactly FPt's (q~ + (-r~) = q~ - r~;
-// FMUL then FFMA, both round-to-nearest), so kF32Charge's derivation is unchanged; each
-// lane's accumulator of a query sums <= RMAX / 32 = 8 terms per tile as before.
-//   points: negated centred FP32 coordinates, each stored twice ((-x, -x), (-y, -y), ..),
-//           PF floats per point in float4 planes (conflict-free LDS.128 per lane);
+// one point (the point's coordinate is the instruction's scalar broadcast operand, so
+// points are stored once, not duplicated), so per two (q, r) pairs the loop issues
+// D FADD2 + D FFMA2 (the first one adds -S) + 2 MUFU.EX2 + 1 FADD2 (accumulate): 3.5
+// issue slots per pair at D = 2 against the MUFU rate's budget of 8.  The arithmetic per
+// term is exactly FPt's (q~ + (-r~) = q~ - r~; FFMA onto -S, FFMAs, all round-to-nearest),
+// so kF32Charge's derivation holds; each lane's accumulator of a query sums
+// <= RMAX / 32 = 8 terms per tile.
+//   points: negated centred FP32 coordinates, zero padded to PF floats per point, in
+//           planes of V-float vectors (conflict-free LDS.64 / LDS.128 per lane);
 //   queries: pair k, dimension d at float2 index k * DT + d = (q_2k[d], q_2k+1[d]);
 //            padding queries (>= qc) sit at 1e18 (their terms are 0, their sums unused).
-#ifndef DFGTB_F32_SMEM_REDUCE
-#define DFGTB_F32_SMEM_REDUCE 0  // measured: the shuffle transpose is as fast
-#endif
 #ifndef DFGTB_F32_KB
 #define DFGTB_F32_KB 2
 #endif
 template <int DT>
 struct F2Pt {
-  static constexpr int PF = (2 * DT + 3) / 4 * 4;  // floats per point
-  static constexpr int NPL = PF / 4;               // float4 planes
+  static constexpr int PF = DT <= 2 ? 2 : DT <= 4 ? 4 : 8;  // floats per point
+  static constexpr int V = PF >= 4 ? 4 : 2;                 // floats per vector
+  static constexpr int NPL = PF / V;                        // planes
   static constexpr int RMAX = 256;
-  static constexpr int PL = RMAX * 4;              // floats per plane
-  static constexpr int P = DT <= 3 ? 4 : 2;        // points per lane per pass
-  static constexpr int QF = 32 * DT;               // floats of the query tile
+  static constexpr int PL = RMAX * V;                       // floats per plane
+  static constexpr int P = DT <= 3 ? 4 : 2;                 // points per lane per pass
+  static constexpr int QF = 32 * DT;                        // floats of the query tile
   static constexpr int FLOATS = RMAX * PF + QF;
   __device__ __forceinline__ static void store(const typename FPt<DT>::Raw& p, const double* c, float* dst, int j)
   {
     float v[PF];
 #pragma unroll
-    for (int d = 0; d < DT; ++d) v[2 * d] = v[2 * d + 1] = -(float)(p.x[d] - c[d]);
+    for (int d = 0; d < DT; ++d) v[d] = -(float)(p.x[d] - c[d]);
 #pragma unroll
-    for (int k = 2 * DT; k < PF; ++k) v[k] = 0.f;
+    for (int k = DT; k < PF; ++k) v[k] = 0.f;
 #pragma unroll
-    for (int k = 0; k < NPL; ++k)
-      reinterpret_cast<float4*>(dst + k * PL)[j] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    for (int k = 0; k < NPL; ++k) {
+      if constexpr (V == 4)
+        reinterpret_cast<float4*>(dst + k * PL)[j] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+      else
+        reinterpret_cast<float2*>(dst + k * PL)[j] = make_float2(v[2 * k], v[2 * k + 1]);
+    }
   }
-  __device__ __forceinline__ static void load(const float* base, int j, float2 (&r)[DT])
+  __device__ __forceinline__ static void load(const float* base, int j, float (&r)[DT])
   {
 #pragma unroll
     for (int k = 0; k < NPL; ++k) {
-      const float4 t = reinterpret_cast<const float4*>(base + k * PL)[j];
-      if (2 * k < DT) r[2 * k] = make_float2(t.x, t.y);
-      if (2 * k + 1 < DT) r[2 * k + 1] = make_float2(t.z, t.w);
+      float t[V];
+      if constexpr (V == 4) {
+        const float4 u = reinterpret_cast<const float4*>(base + k * PL)[j];
+        t[0] = u.x; t[1] = u.y; t[2] = u.z; t[3] = u.w;
+      } else {
+        const float2 u = reinterpret_cast<const float2*>(base + k * PL)[j];
+        t[0] = u.x; t[1] = u.y;
+      }
+#pragma unroll
+      for (int i = 0; i < V; ++i)
+        if (V * k + i < DT) r[V * k + i] = t[i];
     }
   }
   // query `lane` of the chunk (lane >= qc: padding) into the pair layout
@@ -1428,7 +1445,7 @@ __device__ __forceinline__ void base_tile_f32x2(const float* rs, int n, const fl
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = make_float2(0.f, 0.f);
   for (int c = 0; c < n; c += 32 * P) {
-    float2 r[P][DT];
+    float r[P][DT];
     int dl[P];  // SELF: the chunk query whose own point point p is
 #pragma unroll
     for (int p = 0; p < P; ++p) {
@@ -1437,7 +1454,7 @@ __device__ __forceinline__ void base_tile_f32x2(const float* rs, int n, const fl
       if (j < n) F2Pt<DT>::load(rs, j, r[p]);
       else
 #pragma unroll
-        for (int d = 0; d < DT; ++d) r[p][d] = make_float2(-1e18f, -1e18f);
+        for (int d = 0; d < DT; ++d) r[p][d] = -1e18f;
     }
 #pragma unroll
     for (int k = 0; k < 16; k += KB) {
@@ -1450,11 +1467,11 @@ __device__ __forceinline__ void base_tile_f32x2(const float* rs, int n, const fl
           float2 e[P];
 #pragma unroll
           for (int p = 0; p < P; ++p) {
-            float2 a = __fadd2_rn(q[0], r[p][0]);
+            float2 a = __fadd2_rn(q[0], make_float2(r[p][0], r[p][0]));  // scalar broadcast operand
             float2 z = __ffma2_rn(a, a, mS);
 #pragma unroll
             for (int d = 1; d < DT; ++d) {
-              a = __fadd2_rn(q[d], r[p][d]);
+              a = __fadd2_rn(q[d], make_float2(r[p][d], r[p][d]));
               z = __ffma2_rn(a, a, z);
             }
             e[p] = make_float2(ex2_ftz(-z.x), ex2_ftz(-z.y));
@@ -1473,28 +1490,6 @@ __device__ __forceinline__ void base_tile_f32x2(const float* rs, int n, const fl
       }
     }
   }
-#if DFGTB_F32_SMEM_REDUCE
-  // transpose through shared memory (the point tile is free again after the passes):
-  // lane l writes its 32 partials as row l, lane q sums column q by a fixed 5-level tree
-  // (XOR-swizzled columns: both accesses are bank-conflict free)
-  __syncwarp();
-  float* tr = const_cast<float*>(rs);  // 32 x 32 floats
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    tr[lane * 32 + ((2 * k) ^ lane)] = acc[k].x;
-    tr[lane * 32 + ((2 * k + 1) ^ lane)] = acc[k].y;
-  }
-  __syncwarp();
-  float c32[32];
-#pragma unroll
-  for (int l = 0; l < 32; ++l) c32[l] = tr[l * 32 + (lane ^ l)];
-#pragma unroll
-  for (int w = 16; w >= 1; w >>= 1)
-#pragma unroll
-    for (int l = 0; l < w; ++l) c32[l] += c32[l + w];
-  __syncwarp();
-  if (lane < qc) qsum[lane] += (double)c32[0] * kF32Unshift;
-#else
   float a32[32];
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
@@ -1503,7 +1498,6 @@ __device__ __forceinline__ void base_tile_f32x2(const float* rs, int n, const fl
   }
   const float v = transpose_reduce<32, 5>(a32, lane);  // lane l: query l's tile sum
   if (lane < qc) qsum[lane] += (double)v * kF32Unshift;  // 2^-S, exact
-#endif
 }
 
 // FP32 base case kernel (tasks whose every leaf pair carries order bit 2).

@@ -3,7 +3,7 @@
 resident): for each libdfgtb.so given, a fresh process times --steps sweeps and prints
 ms/step and the per-phase device times.
 
-  python tools/ab.py [--config 2] [--steps 20] lib1.so lib2.so ...
+  python tools/ab.py [--config 2] [--steps 20] lib1.so lib2.so:DFGTB_TRAV_ASYNC=1 ...
 """
 import json
 import os
@@ -47,11 +47,13 @@ def main():
             steps = args[1]
         args = args[2:]
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for lib in args:
+    for spec in args:  # lib.so[:VAR=VALUE[,VAR=VALUE..]]
+        lib, _, extra = spec.partition(":")
         env = dict(os.environ, DFGTB_LIB=os.path.abspath(lib), ROOT=root, CFG=cfg, STEPS=steps)
+        env.update(kv.split("=", 1) for kv in extra.split(",") if kv)
         out = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
         line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-1500:]
-        print(f"{lib}: {line}", flush=True)
+        print(f"{spec}: {line}", flush=True)
 
 
 if __name__ == "__main__":
