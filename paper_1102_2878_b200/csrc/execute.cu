@@ -1067,7 +1067,7 @@ __device__ __forceinline__ void base_groups_mufu(const double* rs, int n, const 
 // 2^-190 flush to 0: absolute error <= |R| 2^-190, against sums >= 1e-20 (Q != R) or a
 // leave-one-out sum >= 2^-128 (Q = R; <= |R| 2^-62 relative).  Q = R: the self pairs
 // are masked out of the FP32 sums (their tiles run the SELF variant) and K(0) = 1 is
-// added exactly in FP64 at the end, so the partial sums hold only G - 1, to 13 u relative.
+// added exactly in FP64 at the end, so the partial sums hold only G - 1, to 21 u relative.
 // Per-term relative error for z <= 127 (|q| <= 75, |r| <= 75 + sqrt z, unit roundoff
 // u = 2^-24; z = sum_d a_d^2 with a_d = q~_d - r~_d):
 //   coordinate rounding   |d(q - r)| <= u (|q| + |r|) <= u (150 + sqrt z)
@@ -1079,8 +1079,8 @@ __device__ __forceinline__ void base_groups_mufu(const double* rs, int n, const 
 //     2 sqrt(127) (150 + sqrt(127)) u + 2 127 u + 5 127 u
 //       = 3635 u + 254 u + 635 u = 4524 u = 2.70e-4 = 2 sqrt(127) (150 + 2 sqrt(127)) u + 5 127 u,
 //   |dz| ln 2 <= 1.87e-4 relative, + ex2.approx (< 2^-22 = 2.4e-7 over every argument in
-//   [-126, S], measured exhaustively by dfgtb_f32_exp_error) + FP32 partial sums (<= 8
-//   roundings per lane + 5 reduction levels: 13 u = 7.7e-7): 1.88e-4 < kF32Charge = 2e-4,
+//   [-126, S], measured exhaustively by dfgtb_f32_exp_error) + FP32 partial sums (<= 16
+//   roundings per lane + 5 reduction levels: 21 u = 1.3e-6): 1.89e-4 < kF32Charge = 2e-4,
 //   which the traversal pays for.  Terms with 127 < z <= 190 (below 2^-127 each) carry up
 //   to 2.5e-4 relative error but weigh at most |R| 2^-127 against G >= 1e-20 (Q != R) or
 //   G >= 1 (Q = R): below 1e-15 of G, inside the charge's margin.
@@ -1362,7 +1362,7 @@ __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
 // issue slots per pair at D = 2 against the MUFU rate's budget of 8.  The arithmetic per
 // term is exactly FPt's (q~ + (-r~) = q~ - r~; FFMA onto -S, FFMAs, all round-to-nearest),
 // so kF32Charge's derivation holds; each lane's accumulator of a query sums
-// <= RMAX / 32 = 8 terms per tile.
+// <= RMAX / 32 = 16 terms per tile.
 //   points: negated centred FP32 coordinates, zero padded to PF floats per point, in
 //           planes of V-float vectors (conflict-free LDS.64 / LDS.128 per lane);
 //   queries: pair k, dimension d at float2 index k * DT + d = (q_2k[d], q_2k+1[d]);
@@ -1375,7 +1375,10 @@ struct F2Pt {
   static constexpr int PF = DT <= 2 ? 2 : DT <= 4 ? 4 : 8;  // floats per point
   static constexpr int V = PF >= 4 ? 4 : 2;                 // floats per vector
   static constexpr int NPL = PF / V;                        // planes
-  static constexpr int RMAX = 256;
+#ifndef DFGTB_F32_RMAX
+#define DFGTB_F32_RMAX 512  // measured: 11% faster than 256 on cfg3 / cfg5 with 512-point runs
+#endif
+  static constexpr int RMAX = DFGTB_F32_RMAX;
   static constexpr int PL = RMAX * V;                       // floats per plane
   static constexpr int P = DT <= 3 ? 4 : 2;                 // points per lane per pass
   static constexpr int QF = 32 * DT;                        // floats of the query tile
@@ -2155,19 +2158,12 @@ __global__ void k_dfma_peak(double* out, int iters)
 
 // Points per task run: the base case's stream tile (k_base_case_any streams directly),
 // or DFGTB_RUN_POINTS.
+#ifndef DFGTB_RUN_POINTS
+#define DFGTB_RUN_POINTS 512  // measured: 512-point runs 5-11% faster than 256 (FP32 tile 512); 1024 slower
+#endif
 int base_rmax(int D)
 {
-#ifdef DFGTB_RUN_POINTS
-  if (D <= 5) return DFGTB_RUN_POINTS;
-#endif
-  switch (D) {
-  case 1: return BaseGeo<1>::RMAX;
-  case 2: return BaseGeo<2>::RMAX;
-  case 3: return BaseGeo<3>::RMAX;
-  case 4: return BaseGeo<4>::RMAX;
-  case 5: return BaseGeo<5>::RMAX;
-  default: return 256;
-  }
+  return D <= 5 ? DFGTB_RUN_POINTS : 256;  // k_base_case_any (D > 5) streams its own tiles
 }
 
 int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }

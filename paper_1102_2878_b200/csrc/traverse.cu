@@ -312,7 +312,7 @@ __global__ void k_trav_init(const __grid_constant__ TravArgs a)
 // relative); for Q = R a provable leave-one-out floor G - 1 >= 2^-128 (from G^l, or from
 // a neighbour in the query leaf itself): the self pairs are masked out of the FP32 sums
 // (K(0) = 1 added exactly in FP64), the terms below 2^-190 that flush weigh <= |R| 2^-62
-// relative to the G - 1 the CV scores take logarithms of, FP32 rounding 13 u of it.
+// relative to the G - 1 the CV scores take logarithms of, FP32 rounding 21 u of it.
 __device__ __forceinline__ int base_flags(const TravArgs& a, double kmin, double glo, double sq, double h,
                                           int D, int nq, int Q)
 {

@@ -34,11 +34,11 @@ def test_f32_exp_error_exhaustive():
     assert 0.0 <= err < 2.0 ** -21
     # the charge covers the exp, the distance bound at D = 5 (coordinate rounding
     # 2 sqrt(z) u (150 + sqrt z), differences 2 z u, sums D z u at z = 127) and the FP32
-    # partial sums (13 roundings)
+    # partial sums (21 roundings: <= 16 terms per lane per 512-point tile + 5 warp levels)
     z = 127.0
     dz = 2 * np.sqrt(z) * (150 + np.sqrt(z)) * U + 2 * z * U + 5 * z * U
     assert abs(dz - 2.697e-4) < 1e-6
-    assert err + dz * np.log(2.0) + 13 * U < F32_CHARGE
+    assert err + dz * np.log(2.0) + 21 * U < F32_CHARGE
 
 
 @pytest.mark.parametrize("d", [1, 2, 3, 4, 5])
@@ -63,7 +63,7 @@ def test_f32_terms_within_charge(d):
     want = np.exp2(-np.sum((q - r) ** 2, axis=1))
     got = _terms(d, q, r, c)
     rel = np.abs(got - want) / want
-    assert rel.max() < F32_CHARGE - 13 * U, rel.max()
+    assert rel.max() < F32_CHARGE - 21 * U, rel.max()
     # the self pair (q = r) is exactly 2^-0 = 1
     got0 = _terms(d, q[:1000], q[:1000], c)
     assert np.all(got0 == 1.0)
