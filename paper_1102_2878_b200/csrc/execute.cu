@@ -1856,8 +1856,11 @@ __device__ __forceinline__ double ff_eval_t(const double* Mt, const double* c, c
   return exp(-tt) * v;
 }
 
+#ifndef DFGTB_FF_MINB
+#define DFGTB_FF_MINB 3  // 80 registers, 3 CTAs per SM: measured 1-7% faster than the unbounded 96-register build
+#endif
 template <int D, int PM>
-__global__ void __launch_bounds__(kBlock) k_farfield_t(TreeView Q, TreeView R, int K, int nb,
+__global__ void __launch_bounds__(kBlock, DFGTB_FF_MINB) k_farfield_t(TreeView Q, TreeView R, int K, int nb,
                                                        const int* leaves, int nleaves,
                                                        const int* cnt, const int* off,
                                                        const Item* items, const double* Mt,
