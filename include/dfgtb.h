@@ -211,6 +211,14 @@ int dfgtb_f32_terms(size_t d, const double* q, const double* r, const double* c,
  * handles, like PyTorch's caching allocator; this returns it to the driver. */
 void dfgtb_release_cached_memory(void);
 
+/* Guard mode (environment variable DFGTB_GUARD set before the first allocation): every
+ * device block carries a 4 KB guard band past its end; dfgtb_guard_check() synchronises
+ * and returns how many bands were written into (0: no out-of-bounds write seen), -1 when
+ * guard mode is off.  dfgtb_guard_selftest() writes one element past a block and returns
+ * 1 if the check caught it (test entry).  A debug aid, not part of the reference ABI. */
+int dfgtb_guard_check(void);
+int dfgtb_guard_selftest(void);
+
 /* Number of visible CUDA devices (0 when none; never raises). */
 int dfgtb_device_count(void);
 

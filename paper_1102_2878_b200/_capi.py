@@ -61,7 +61,7 @@ EXPORTS = (
     "dfgtb_tree_nodes", "dfgtb_tree_height", "dfgtb_export_tree", "dfgtb_naive",
     "dfgtb_series_op", "dfgtb_dfma_peak", "dfgtb_mufu_exp_error", "dfgtb_f32_exp_error", "dfgtb_f32_terms", "dfgtb_last_base_split", "dfgtb_ex2_peak", "dfgtb_base_exp_mode", "dfgtb_device_count", "dfgtb_release_cached_memory",
     "dfgtb_stream", "dfgtb_choose_methods", "dfgtb_box_bounds", "dfgtb_sweep_best",
-    "dfgtb_launch_count", "dfgtb_last_error",
+    "dfgtb_launch_count", "dfgtb_last_error", "dfgtb_guard_check", "dfgtb_guard_selftest",
 )
 
 
@@ -110,6 +110,8 @@ def _load():
         "dfgtb_box_bounds": (C.c_int, [sz, sz, _D, _D]),
         "dfgtb_launch_count": (C.c_uint64, [V]),
         "dfgtb_last_error": (C.c_char_p, []),
+        "dfgtb_guard_check": (C.c_int, []),
+        "dfgtb_guard_selftest": (C.c_int, []),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

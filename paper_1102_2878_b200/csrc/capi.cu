@@ -560,6 +560,39 @@ int dfgtb_device_count(void)
 
 void dfgtb_release_cached_memory(void) { cache_release_all(); }
 
+int dfgtb_guard_check(void)
+{
+  try {
+    return guard_check();
+  } catch (...) {
+    return -2;
+  }
+}
+
+namespace {
+__global__ void k_guard_poke(int* p, int at) { p[at] = 7; }  // one element past the end
+}  // namespace
+
+int dfgtb_guard_selftest(void)
+{
+  if (!guard_mode()) return -1;
+  try {
+    int detected = 0;
+    {
+      DevBuf<int> b;
+      b.reserve(256);
+      const int before = guard_check();
+      k_guard_poke<<<1, 1>>>(b.p, (int)b.cap);
+      CK_LAUNCH();
+      detected = guard_check() > before ? 1 : 0;
+      CK(cudaMemset(reinterpret_cast<unsigned char*>(b.p + b.cap), kGuardByte, kGuardBytes));  // repair
+    }
+    return detected;
+  } catch (...) {
+    return -2;
+  }
+}
+
 double dfgtb_dfma_peak(void)
 {
   double v = -1.0;

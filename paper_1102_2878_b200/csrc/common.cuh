@@ -52,6 +52,14 @@ uint64_t& launch_counter();
 void* cache_alloc(size_t bytes);
 void cache_free(void* p, size_t bytes, int device);
 void cache_release_all();
+// Guard mode (DFGTB_GUARD set when the library first allocates): every device block gets a
+// kGuardBytes band past its end filled with kGuardByte; guard_check() synchronises and
+// counts the bands some kernel wrote into (an out-of-bounds-write detector standing in
+// for compute-sanitizer memcheck, which this pool does not run).
+bool guard_mode();
+int guard_check();
+constexpr size_t kGuardBytes = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
 int current_device();
 
 // Makes `dev` current for a scope and restores the previous device afterwards.

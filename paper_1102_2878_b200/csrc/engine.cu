@@ -45,6 +45,11 @@ std::unordered_map<size_t, std::vector<void*>>& host_cache()
   return *c;
 }
 uint64_t cache_key(size_t bytes, int dev) { return ((uint64_t)bytes << 8) | (uint64_t)(dev & 0xff); }
+std::unordered_map<void*, std::pair<size_t, int>>& guard_blocks()  // block -> (bytes, device)
+{
+  static auto* c = new std::unordered_map<void*, std::pair<size_t, int>>();
+  return *c;
+}
 void* take_cached(uint64_t key)  // g_cache_mu held
 {
   auto it = dev_cache().find(key);
@@ -88,14 +93,52 @@ void* cache_alloc(size_t bytes)
     }
   }
   void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, bytes);
+  const size_t extra = guard_mode() ? kGuardBytes : 0;
+  cudaError_t e = cudaMalloc(&p, bytes + extra);
   if (e == cudaErrorMemoryAllocation) {  // give the cache back and retry once
     cudaGetLastError();
     cache_release_all();
-    e = cudaMalloc(&p, bytes);
+    e = cudaMalloc(&p, bytes + extra);
   }
   CK(e);
+  if (extra) {
+    CK(cudaMemset(static_cast<unsigned char*>(p) + bytes, kGuardByte, kGuardBytes));
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    guard_blocks()[p] = { bytes, dev };
+  }
   return p;
+}
+
+bool guard_mode()
+{
+  static const bool on = std::getenv("DFGTB_GUARD") != nullptr;
+  return on;
+}
+
+int guard_check()
+{
+  if (!guard_mode()) return -1;
+  std::vector<std::pair<void*, std::pair<size_t, int>>> blocks;
+  {
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    blocks.assign(guard_blocks().begin(), guard_blocks().end());
+  }
+  const int cur = current_device();
+  std::vector<unsigned char> band(kGuardBytes);
+  int bad = 0;
+  for (const auto& b : blocks) {
+    CK(cudaSetDevice(b.second.second));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(band.data(), static_cast<unsigned char*>(b.first) + b.second.first, kGuardBytes,
+                  cudaMemcpyDeviceToHost));
+    for (unsigned char c : band)
+      if (c != kGuardByte) {
+        ++bad;
+        break;
+      }
+  }
+  CK(cudaSetDevice(cur));
+  return bad;
 }
 
 void cache_free(void* p, size_t bytes, int device)
@@ -116,6 +159,7 @@ void cache_release_all()
   auto free_on = [](uint64_t key, void* p) {
     if (cudaSetDevice((int)(key & 0xff)) != cudaSuccess) cudaGetLastError();
     cudaFree(p);
+    guard_blocks().erase(p);
   };
   for (auto& kv : dev_cache())
     for (void* p : kv.second) free_on(kv.first, p);

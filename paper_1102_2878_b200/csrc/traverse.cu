@@ -2098,12 +2098,15 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   TravState* hs = static_cast<TravState*>(hst_);
   TravState* ds = reinterpret_cast<TravState*>(dst_.p);
   {  // first guesses; overflow regrows and the engine keeps the sizes
+    // DFGTB_TINY_CAPS (tests): start from 64-element buffers, so first batches overflow,
+    // regrow and rerun several times
+    static const bool tiny = std::getenv("DFGTB_TINY_CAPS") != nullptr;
     const int kb = (int)std::min<long long>(KB, INT32_MAX / 64);
-    capE_ = std::max(capE_, std::max(4096, 2 * kb));
-    capP_ = std::max(capP_, std::max(1 << 16, 16 * kb));
-    capF_ = std::max(capF_, std::max(4096, 2 * kb));
-    capDT_ = std::max(capDT_, std::max(4096, 2 * kb));
-    capB_ = std::max(capB_, std::max(1 << 16, 16 * kb));
+    capE_ = std::max(capE_, tiny ? 64 : std::max(4096, 2 * kb));
+    capP_ = std::max(capP_, tiny ? 64 : std::max(1 << 16, 16 * kb));
+    capF_ = std::max(capF_, tiny ? 64 : std::max(4096, 2 * kb));
+    capDT_ = std::max(capDT_, tiny ? 64 : std::max(4096, 2 * kb));
+    capB_ = std::max(capB_, tiny ? 64 : std::max(1 << 16, 16 * kb));
   }
   if (use_async_) {  // one queue of every entry of the batch, one pool of every pair
     const int kb = (int)std::min<long long>(KB, INT32_MAX / 128);

@@ -1,4 +1,6 @@
-"""Workload for compute-sanitizer runs (tools/sanitize.sh): smoke(), then a config-2
+"""Memory-safety workload: run under compute-sanitizer (tools/sanitize.sh, where the pool
+allows it) or with DFGTB_GUARD=1, where every phase is followed by dfgtb_guard_check()
+(guard bands past every device block; tests/test_gpu_guard.py).  smoke(), then a config-2
 sweep at 5% of N on FRESH engines (the first batch of an engine runs with optimistic
 buffers and overflows -> the host regrows and reruns it), a Q != R batch, the FP64-only
 base case, the L2L chain and the DFD mode -- every kernel family of the product path.
@@ -18,9 +20,26 @@ def main():
     small = "--small" in sys.argv
     import __graft_entry__ as g
     import paper_1102_2878_b200 as dfgtb
-    from paper_1102_2878_b200 import datagen
+    from paper_1102_2878_b200 import _capi, datagen
 
+    guard = os.environ.get("DFGTB_GUARD") is not None
+    import builtins
+    _print = builtins.print
+
+    def print(*a):  # noqa: A001 -- every phase line is followed by the guard verdict
+        _print(*a, flush=True)
+        if guard:
+            bad = _capi.lib.dfgtb_guard_check()
+            _print(f"  guard bands written: {bad}", flush=True)
+            if bad != 0:
+                raise SystemExit(f"out-of-bounds write detected after: {a[0]}")
+
+    if guard:
+        if _capi.lib.dfgtb_guard_selftest() != 1:
+            raise SystemExit("guard self-test did not detect its own out-of-bounds write")
+        print("guard self-test ok")
     g.smoke()
+    print("smoke ok")
     n = 1000 if small else 2500  # 5% of cfg2's 50k
     x = datagen.gauss_mixture_2d(n, seed=7)
     hs = float(dfgtb.pilot_bandwidth(x))
