@@ -22,6 +22,9 @@ def main():
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 20
     hdr = next(r for r in rows if len(r) > 2 and r[0] == "Address")
     data = [dict(zip(hdr, r)) for r in rows if len(r) == len(hdr) and r[0].startswith("0x")]
+    h = len(data) // 2
+    if h and len(data) % 2 == 0 and all(data[i]["Source"] == data[h + i]["Source"] for i in range(h)):
+        data = data[:h]  # the source page repeats the listing once per profiled pass
     scols = [c for c in hdr if c.startswith("stall_") and "Not Issued" not in c]
     blocks, cur = [], None
     for i, r in enumerate(data):
