@@ -654,6 +654,9 @@ __global__ void k_advance(const __grid_constant__ TravArgs a, cudaGraphCondition
 #define KPBLOCK 1024
 #endif
 constexpr int kPBlock = KPBLOCK;  // one CTA per SM: 32 warps to hide classify latency
+constexpr int kTrAll = 4096 + 512 * 16 + 64 * 160 + 64;  // DFGTB_TRACE: per-level phase sums over CTAs
+constexpr int kTrCta = kTrAll + 64 * 16;  // per level, per CTA: phase durations, pairs, entries
+constexpr int kTrLen = kTrCta + 64 * 160 * 10;
 
 template <int W>
 __device__ __forceinline__ void emit_range(const TravArgs& a, int K, int cur, int gF, int gDT, int gB,
@@ -711,6 +714,13 @@ struct PairCache {
 
 // Smallest entry e with foff[e] >= target (foff increasing, entries non-empty), for
 // two targets at once, by a 1024-ary search with __syncthreads_count.
+// The key is the entry's cost offset foff[e] + kEntryCost e (pairs plus a per-entry
+// charge: the per-entry phases -- G^l, counts, emission -- run one warp per entry, so a
+// range of many small entries costs more than its pairs say).
+#ifndef DFGTB_ENTRY_COST
+#define DFGTB_ENTRY_COST 8
+#endif
+constexpr long long kEntryCost = DFGTB_ENTRY_COST;
 __device__ __forceinline__ void entry_bounds(const int* foff, int m, long long t0, long long t1,
                                              int& e0, int& e1)
 {
@@ -718,8 +728,8 @@ __device__ __forceinline__ void entry_bounds(const int* foff, int m, long long t
   while (lo0 < hi0 || lo1 < hi1) {
     const int S0 = (hi0 - lo0 + kPBlock - 1) / kPBlock, S1 = (hi1 - lo1 + kPBlock - 1) / kPBlock;
     const int c0i = lo0 + (threadIdx.x + 1) * S0 - 1, c1i = lo1 + (threadIdx.x + 1) * S1 - 1;
-    const bool p0 = lo0 < hi0 && c0i < hi0 && foff[c0i] < t0;
-    const bool p1 = lo1 < hi1 && c1i < hi1 && foff[c1i] < t1;
+    const bool p0 = lo0 < hi0 && c0i < hi0 && foff[c0i] + kEntryCost * c0i < t0;
+    const bool p1 = lo1 < hi1 && c1i < hi1 && foff[c1i] + kEntryCost * c1i < t1;
     const int c0 = __syncthreads_count(p0), c1 = __syncthreads_count(p1);
     if (lo0 < hi0) {
       const int nlo = lo0 + c0 * S0;
@@ -1578,13 +1588,19 @@ __global__ void __launch_bounds__(kPBlock, kPerSM) k_traverse(const __grid_const
   __syncthreads();
   int cur = 0, m = st.m[0], p = st.p[0], gF = 0, gDT = 0, gB = 0, levels = 0;
   // DFGTB_TRACE: per-phase %globaltimer stamps of CTA 0 (trace[4096 + 16 L + k])
+  // and, from every CTA, the phase durations summed over CTAs (trace[kTrAll + 16 L + k])
+  unsigned long long tph = 0;
 #define PH(k)                                                                                   \
-  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && levels < 512) {                       \
+  if (a.trace && threadIdx.x == 0 && levels < 512) {                                           \
     unsigned long long t_;                                                                      \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
-    a.trace[4096 + levels * 16 + (k)] = t_;                                                     \
+    if (blockIdx.x == 0) a.trace[4096 + levels * 16 + (k)] = t_;                                \
+    if (levels < 64) atomicAdd(a.trace + kTrAll + levels * 16 + (k), t_ - tph);                 \
+    if (levels < 64 && blockIdx.x < 160) a.trace[kTrCta + ((size_t)levels * 160 + blockIdx.x) * 10 + (k)] = t_ - tph; \
+    tph = t_;                                                                                   \
   }
   for (;;) {
+    if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tph));
     if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && levels < 512) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1604,12 +1620,16 @@ __global__ void __launch_bounds__(kPBlock, kPerSM) k_traverse(const __grid_const
       cb0[j] = cb1[j] = 0;
       if (j < nch) {
         const long long k = blockIdx.x + (long long)j * G, nk = (long long)G * nch;
-        entry_bounds(a.foff[cur], m, k * p / nk, (k + 1) * p / nk, cb0[j], cb1[j]);
+        const long long tot = p + kEntryCost * m;  // cost of the level (see entry_bounds)
+        entry_bounds(a.foff[cur], m, k * tot / nk, (k + 1) * tot / nk, cb0[j], cb1[j]);
       }
     }
     auto pofs = [&](int e) { return e < m ? a.foff[cur][e] : p; };
     const int cP0 = pofs(cb0[0]), cP1 = pofs(cb1[0]);
     const bool cached = kUseCache && nch == 1 && cP1 - cP0 <= kCacheP && cb1[0] - cb0[0] <= kCacheE;
+    if (a.trace && threadIdx.x == 0 && levels < 64 && blockIdx.x < 160)
+      a.trace[kTrCta + ((size_t)levels * 160 + blockIdx.x) * 10 + 9] =
+        ((unsigned long long)(cb1[0] - cb0[0]) << 32) | (unsigned)(cP1 - cP0);
     PH(0);
     if (cached) {
       pairs_bounds_c<DT>(a, cur, K, cP0, cP1, cb0[0], cb1[0], s_scale, pc);
@@ -2200,8 +2220,8 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   a.lvlep = lvlep_.p;
   static const bool tracing = std::getenv("DFGTB_TRACE") != nullptr;
   if (tracing) {
-    trace_.reserve(4096 + 512 * 16 + 64 * 160 + 64);
-    CK(cudaMemsetAsync(trace_.p, 0, sizeof(unsigned long long) * (4096 + 512 * 16 + 64 * 160 + 64), s));
+    trace_.reserve(kTrLen);
+    CK(cudaMemsetAsync(trace_.p, 0, sizeof(unsigned long long) * (kTrLen), s));
     a.trace = trace_.p;
   }
   const std::vector<const void*> sig = {
@@ -2302,7 +2322,7 @@ bool Engine::traverse_finish()
   const int nb = trav_nb_;
   if (!use_persistent_ && use_graph_) launch_counter() += (uint64_t)hs->levels * kLevelKernels;
   if (trav_trace_) {  // per level: classify | scan | emit (microseconds)
-    std::vector<unsigned long long> tr(4096 + 512 * 16 + 64 * 160 + 64);
+    std::vector<unsigned long long> tr(kTrLen);
     CK(cudaMemcpy(tr.data(), trace_.p, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
     for (int L = 0; L < std::min(hs->levels, 511); ++L) {
       const unsigned long long* ph = tr.data() + 4096 + L * 16;
@@ -2313,6 +2333,31 @@ bool Engine::traverse_finish()
                    (tr[L * 4 + 2] - tr[L * 4 + 1]) * 1e-3, (ph[0] - tr[L * 4]) * d, (ph[1] - ph[0]) * d,
                    (ph[2] - ph[1]) * d, (ph[3] - ph[2]) * d, (ph[4] - ph[3]) * d, (ph[5] - ph[4]) * d,
                    (ph[6] - ph[5]) * d, (ph[7] - ph[6]) * d, (ph[8] - ph[7]) * d);
+      if (L < 64) {  // phase durations averaged over the CTAs
+        const unsigned long long* pa = tr.data() + kTrAll + L * 16;
+        const double g = 148.0;
+        std::fprintf(stderr, "DFGTB_TRACE level %d: mean over CTAs us | split %.1f bounds %.1f glo %.1f decide %.1f "
+                     "reduce %.1f offsets %.1f scan %.1f emit %.1f sync %.1f\n", L, pa[0] * d / g, pa[1] * d / g,
+                     pa[2] * d / g, pa[3] * d / g, pa[4] * d / g, pa[5] * d / g, pa[6] * d / g, pa[7] * d / g,
+                     pa[8] * d / g);
+      }
+      if (L < 64) {  // the slowest and the median CTA (sum of phases 0-7): phases, pairs, entries
+        std::vector<std::pair<double, int>> bs;
+        for (int b = 0; b < 148; ++b) {
+          const unsigned long long* c = tr.data() + kTrCta + ((size_t)L * 160 + b) * 10;
+          double t = 0;
+          for (int k = 0; k < 8; ++k) t += c[k] * d;
+          bs.push_back({ t, b });
+        }
+        std::sort(bs.begin(), bs.end());
+        for (int w : { (int)bs.size() / 2, (int)bs.size() - 1 }) {
+          const unsigned long long* c = tr.data() + kTrCta + ((size_t)L * 160 + bs[w].second) * 10;
+          std::fprintf(stderr, "DFGTB_TRACE level %d: %s CTA %d busy %.1f us | split %.1f bounds %.1f glo %.1f decide %.1f "
+                       "reduce %.1f offsets %.1f scan %.1f emit %.1f | pairs %llu entries %llu\n", L,
+                       w == (int)bs.size() - 1 ? "slowest" : "median", bs[w].second, bs[w].first, c[0] * d, c[1] * d,
+                       c[2] * d, c[3] * d, c[4] * d, c[5] * d, c[6] * d, c[7] * d, c[9] & 0xffffffffull, c[9] >> 32);
+        }
+      }
       if (L < 64) {  // CTA busy times: min / median / max (from the level start of CTA 0)
         std::vector<double> bt;
         for (int b = 0; b < 160; ++b) {
