@@ -136,14 +136,55 @@ __device__ int d_order_f2l(double ratio, double count, double tau, int pmax, int
   return 0;
 }
 
+// The three least-order searches of choose_best_method run interleaved, one candidate
+// order of each per step: the same arithmetic per search as d_order_ff / d_order_f2l
+// (identical orders), but three independent dependency chains instead of one three
+// times as long (the method choice is a latency-bound phase of every traversal level).
+__device__ __forceinline__ void orders3(double rF, double rD, double rT, double count, double tau, int pmax,
+                                        int dim, int& pf, int& pd, int& pt)
+{
+  pf = pd = pt = 0;
+  bool doneF = rF >= 1.0, doneD = rD >= 1.0, doneT = rT >= 0.5;
+  const double sT = 2.0 * rT;
+  const double thrF = doneF ? 0.0 : tau * d_ipow(1.0 - rF, dim);
+  const double thrD = doneD ? 0.0 : tau * d_ipow(1.0 - rD, dim);
+  const double thrT = doneT ? 0.0 : tau * d_ipow(1.0 - sT, 2 * dim);
+  double rpF = 1.0, rpD = 1.0, spT = 1.0;
+  for (int p = 1; p <= pmax && !(doneF && doneD && doneT); ++p) {
+    const double isf = c_isf[p], sf = c_sf[p];
+    if (!doneF) {
+      rpF *= rF;
+      if (bound_ok(count, bound_sum_S(1.0 - rpF, rpF * isf, dim), thrF, tau, rF, 1, 1.0 - rpF, rpF / sf, dim)) {
+        pf = p;
+        doneF = true;
+      }
+    }
+    if (!doneD) {
+      rpD *= rD;
+      if (bound_ok(count, bound_sum_S(1.0 - rpD, rpD * isf, dim), thrD, tau, rD, 1, 1.0 - rpD, rpD / sf, dim)) {
+        pd = p;
+        doneD = true;
+      }
+    }
+    if (!doneT) {
+      spT *= sT;
+      const double aT = (1.0 - spT) * (1.0 - spT);
+      if (bound_ok(count, bound_sum_S(aT, spT * (2.0 - spT) * isf, dim), thrT, tau, sT, 2, aT,
+                   spT * (2.0 - spT) / sf, dim)) {
+        pt = p;
+        doneT = true;
+      }
+    }
+  }
+}
+
 // choose_best_method, truncation.cpp:130-166 (ties F > D > T > E)
 __device__ void dev_choose(double nq, double nr, double sq, double sr, double h, double tau,
                            int pmax, int dim, int cost, int& kind, int& order)
 {
   const double uq = sq / h, ur = sr / h;  // side / (2h) = (side / h) * 0.5 exactly
-  const int pf = d_order_ff(ur * 0.5, nr, tau, pmax, dim);
-  const int pd = d_order_ff(uq * 0.5, nr, tau, pmax, dim);
-  const int pt = d_order_f2l((uq < ur ? ur : uq) * 0.25, nr, tau, pmax, dim);
+  int pf, pd, pt;
+  orders3(ur * 0.5, uq * 0.5, (uq < ur ? ur : uq) * 0.25, nr, tau, pmax, dim, pf, pd, pt);
   const double D = (double)dim;
   double cf = CUDART_INF, cd = CUDART_INF, ct = CUDART_INF;
   if (cost == 0) {  // exponential model; integer powers of D <= 5 are exact
