@@ -133,6 +133,8 @@ private:
   cudaStream_t s_ = nullptr;
   cudaStream_t s2_ = nullptr;  // local expansions + far field run beside the base case
   int base_cta_slack_ = 0;     // base-case CTA slots per SM left to s2_ (DFGTB_BASE_SLACK; 0 measured best)
+  bool one_stream_ = false;    // DFGTB_ONE_STREAM: the s2_ chain on s_ too (serialised; per-kernel timings
+                               // without SM sharing; measured 10% slower on cfg2 than the overlap)
   DevBuf<double> x_;        // reference points (original order)
   DevTree rt_;              // reference tree
   DevTree qt_tmp_;          // query tree (Q != R)

@@ -2434,7 +2434,7 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
   // base-case chain on s_ (they only read the traversal's sorted items and write their
   // own buffers); the base case leaves a CTA slot per SM for them.  Join before
   // finalize.
-  cudaStream_t s2 = s2_;
+  cudaStream_t s2 = one_stream_ ? s : s2_;  // DFGTB_ONE_STREAM: isolated kernel timings
   CK(cudaEventRecord(fork_, s));
   CK(cudaStreamWaitEvent(s2, fork_, 0));
   // moments of the reference nodes used by F/T items (large tables only; small
