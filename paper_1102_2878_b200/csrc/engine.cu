@@ -287,9 +287,6 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
   dev_ = current_device();
   if (const char* sl = std::getenv("DFGTB_BASE_SLACK")) base_cta_slack_ = std::atoi(sl);
   one_stream_ = std::getenv("DFGTB_ONE_STREAM") != nullptr;
-  // the barrier-free traversal is bit-identical to the level loop; measured faster only on
-  // some large configs (cfg3, cfg4) and slower on cfg1/cfg2/cfg5, so it is opt-in
-  use_async_ = std::getenv("DFGTB_TRAV_ASYNC") != nullptr;
   mufu_ = cfg.epsilon >= kMufuMinEps && D_ <= 5 && std::getenv("DFGTB_EXACT_EXP") == nullptr;
   f32_ = mufu_ && cfg.epsilon >= kF32MinEps && std::getenv("DFGTB_NO_F32") == nullptr;
   const int pm = cfg.mode == 0 ? 1 : (cfg.p_max > 0 ? cfg.p_max : default_p_max(D_));

@@ -169,13 +169,7 @@ private:
   size_t hst_bytes_ = 0;
   DevBuf<unsigned char> dst_;
   int capE_ = 0, capP_ = 0, capF_ = 0, capDT_ = 0, capB_ = 0;
-  bool use_async_ = true;        // barrier-free traversal (k_trav_async); else the level loop
-  int capEA_ = 0, capPA_ = 0;    // async: total entries / pairs of a batch (grown on overflow)
-  DevBuf<int> aready_;           // async: per entry slot published flag
-  DevBuf<int> actr_;             // async: padded counters
   DevBuf<int> sfront_;           // start frontier node lists (DFGTB_TRAV_START_DEPTH)
-  DevBuf<unsigned char> adepth_; // async: per entry slot level
-  DevBuf<unsigned long long> atrace_;  // DFGTB_ASYNC_TRACE builds
   bool use_persistent_ = true;  // one cooperative kernel runs every level
   bool use_graph_ = true;       // else: CUDA-graph WHILE loop; else host loop
   cudaGraph_t graph_ = nullptr;

@@ -230,8 +230,6 @@ struct TravState {
   int done;                            // CTAs finished with their tile sum (unused)
   Cnt lvl;                             // totals of the current level
   unsigned long long sst[kMaxSlots][sNStat];  // per-slot TraversalStats
-  int ahead, atail, aptail, apending;          // asynchronous traversal (k_trav_async)
-  int xF, xDT, xB;                             // async: item array extents (>= nF.. : gaps)
 };
 
 struct TravArgs {
@@ -334,7 +332,6 @@ __global__ void k_trav_init(const __grid_constant__ TravArgs a)
     st.p[0] = nb * nq * nr;
     st.m[1] = st.p[1] = 0;
     st.nF = st.nDT = st.nB = 0;
-    st.xF = st.xDT = st.xB = 0;
     st.overflow = 0;
     st.levels = 0;
     st.done = 0;
@@ -1116,487 +1113,6 @@ __device__ __forceinline__ void entries_reduce_c(const TravArgs& a, int cur, int
   }
 }
 
-// ---- asynchronous (barrier-free) traversal ------------------------------------------
-// Every frontier entry (slot, query node, its live reference nodes, lower-bound base)
-// depends only on the entry that created it, so the levels need no grid-wide barrier:
-// warps claim entries from one global queue in creation order, wait for a claimed
-// entry to be published, classify it (classify_entry: the same arithmetic and lane-
-// strided reduction order as the level kernels), reserve space for its children and
-// work items with atomics, emit them (emit_entry), and publish the children.  A key
-// (slot, query node) has at most one live entry at a time (a query leaf's successive
-// entries form a chain, an internal node's entry creates its children's), so the per-
-// key rank counters, local-expansion constants and orders need no atomics, and every
-// item keeps the (key, rank) of the level-synchronous traversal: the counting sort that
-// follows makes the results bit-identical to it.  `pending` counts published-but-
-// unfinished entries; a warp waiting on a slot leaves when it drops to zero.
-// Counters, each on its own 128-byte line (kAsyncCtr ints apart): the hot atomics of
-// different roles never queue behind each other in one L2 slice.
-constexpr int kAsyncCtr = 32;
-enum AsyncCounter { acHead = 0, acTail, acPool, acF, acDT, acB, acPending, acRF, acRDT, acRB, acNum };
-struct AsyncQ {
-  int* ready;               // per queue slot: 1 published, 2 dead (its producer overflowed)
-  int* ctr;                 // acNum counters, kAsyncCtr ints apart
-  unsigned char* depth;     // per slot: level of the entry
-  unsigned long long* tr;   // DFGTB_ASYNC_TRACE builds: per slot {published, started, finished} (ns)
-  __device__ int* c(int k) const { return ctr + k * kAsyncCtr; }
-};
-constexpr int kAsyncChunkP = 1024;  // pairs reserved per pool refill of a warp
-constexpr int kAsyncChunkI = 128;   // items reserved per refill of a warp (each kind)
-constexpr int kAsyncBlock = 128;  // 4 warps, each with a WarpScratch
-constexpr long long kAsyncMaxPolls = 1ll << 23;
-#ifndef DFGTB_ASYNC_SLEEP
-#define DFGTB_ASYNC_SLEEP 256
-#endif
-constexpr unsigned kAsyncMaxSleep = DFGTB_ASYNC_SLEEP;  // ns, polling backoff cap  // a stuck wait reports an error, never hangs
-
-__device__ __forceinline__ int ld_acquire(const int* p)
-{
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v)
-{
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// One entry of the asynchronous traversal, fused (classify_entry + emit_entry with the
-// pairs' data in registers and the warp's shared scratch instead of global memory: the
-// entry's dependent memory round trips drop from ~12 to ~5).  Identical arithmetic and
-// reduction / emission order to classify_entry<DT, 32> + emit_entry<32>, so the items,
-// ranks, local constants and statistics are the same.  Entries with > kFuseMax pairs take
-// the unfused path.  Returns the children published (for `pending`).
-constexpr int kFuseMax = 256;
-constexpr int kAsyncSmem = 4 * (kFuseMax * (8 + 8 + 5 * 4));  // kAsyncBlock / 32 WarpScratch
-struct WarpScratch {  // per warp, kFuseMax pairs
-  double kmax[kFuseMax], kmin[kFuseMax];
-  int R[kFuseMax], cnt[kFuseMax], dec[kFuseMax], rl[kFuseMax], rr[kFuseMax];
-};
-// Per-warp reservation of a kind of output space: refills take chunks of the global
-// counter; an abandoned chunk tail is reported through `gap` (items: marked invalid).
-struct Reserve {
-  int pos = 0, end = 0;
-};
-__device__ __forceinline__ int reserve(Reserve& r, int need, int* ctr, int chunk, int cap, int lane,
-                                       int& gap0, int& gap1)
-{  // warp-uniform; returns the first position or -1 when the space is exhausted
-  gap0 = gap1 = 0;
-  if (need == 0) return 0;
-  if (r.pos + need > r.end) {
-    int b = 0;
-    const int n = max(chunk, need);
-    if (lane == 0) b = atomicAdd(ctr, n);
-    b = __shfl_sync(0xffffffffu, b, 0);
-    gap0 = r.pos;
-    gap1 = r.end;
-    r.pos = b;
-    r.end = b + n;
-  }
-  if (r.pos + need > cap) return -1;
-  const int p = r.pos;
-  r.pos += need;
-  return p;
-}
-
-__device__ __forceinline__ void invalidate_items(Item* it, int p0, int p1, int cap, int lane)
-{
-  for (int k = p0 + lane; k < min(p1, cap); k += 32) it[k].key = -1;
-}
-
-template <int DT>
-__device__ __forceinline__ int async_entry(const TravArgs& a, TravState& st, const AsyncQ& q, int i, int lane,
-                                           WarpScratch& w, unsigned long long (*sst)[sNStat], Reserve& rp,
-                                           Reserve& rf, Reserve& rdt, Reserve& rb, int& totF, int& totDT,
-                                           int& totB, const double* s_h, const double* s_scale, int K)
-{
-  const int D = DT ? DT : a.D;
-  // the entry, its query node, its per-key counters (independent loads)
-  const int key = a.fq[0][i], off = a.foff[0][i], len = a.flen[0][i];
-  const double fb = a.fbase[0][i];
-  const int slot = key / K;
-  const int Q = key - slot * K;
-  const double h = s_h[slot], scale = s_scale[slot], eps = st.eps, ntot = st.ntot;
-  const int qleft = a.Q.left[Q], qright = a.Q.right[Q];
-  const bool qleaf = qleft < 0;
-  const int qcount = a.Q.count[Q];
-  const double nq = (double)qcount;
-  const double sq = a.Q.side[Q];
-  const double* qlo = a.Q.lo + (size_t)Q * D;
-  const double* qhi = a.Q.hi + (size_t)Q * D;
-  const int rF = a.cntF[key], rDT = a.cntDT[key], rB = a.cntB[key];
-#ifdef DFGTB_ASYNC_TRACE
-#define APH(k)                                                                              \
-  if (lane == 0) {                                                                          \
-    unsigned long long t_;                                                                  \
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                  \
-    q.tr[3 * (size_t)st.capE + 8 * (size_t)i + (k)] = t_;                                   \
-  }
-#else
-#define APH(k)
-#endif
-  if (lane == 0 && (rF | rDT | rB | qright | qcount) == -7) a.L[0] = 0.0;  // (keeps the loads ahead of APH)
-  APH(0);
-  // pass 1: kernel bounds and the lower-bound mass of every live pair (lane-strided)
-  double part = 0.0;
-  for (int j = lane; j < len; j += 32) {
-    const int R = a.fr[0][off + j];
-    double dl, du;
-    box_bounds<DT>(qlo, qhi, a.R.lo + (size_t)R * D, a.R.hi + (size_t)R * D, D, dl, du);
-    const double kmax = exp(scale * dl);
-    const double kmin = exp(scale * du);
-    const int cr = a.R.count[R];
-    w.kmax[j] = kmax;
-    w.kmin[j] = kmin;
-    w.R[j] = R;
-    w.cnt[j] = cr;
-    w.rl[j] = a.R.left[R];
-    w.rr[j] = a.R.right[R];
-    part += (double)cr * kmin;
-  }
-  const double glo = fb + group_sum<32>(part);
-  APH(1);
-  // pass 2: decisions
-  double fd_dlo = 0.0, fd_const = 0.0, ret = 0.0;
-  int nF = 0, nDT = 0, nT = 0, nB = 0, nFD = 0, slots = 0;
-  unsigned long long kev = 0, cov = 0;
-  for (int j = lane; j < len; j += 32) {
-    const int R = w.R[j];
-    const double kmax = w.kmax[j], kmin = w.kmin[j];
-    const double nr = (double)w.cnt[j];
-    const double dlo = nr * kmin;
-    const double tau = (eps / ntot) * nr * glo;  // eps |R| G^l / N
-    const bool rleaf = w.rl[j] < 0;
-    int kind = kX, order = 0;
-    if (0.5 * nr * (kmax - kmin) <= tau) {  // kernel-difference prune, engine.cpp:137-148
-      kind = kFD;
-      fd_dlo += dlo;
-      fd_const += 0.5 * nr * (kmax + kmin);
-      ++nFD;
-    } else {
-      if (a.series) {
-        dev_choose(nq, nr, sq, a.R.side[R], h, tau, a.pmax, D, a.cost, kind, order);
-        if (kind == kE) kind = kX;
-      }
-      if (kind == kX && qleaf && rleaf) {
-        kind = kB;
-        order = base_flags(a, kmin, glo, sq, h, D, qcount, Q);
-      }
-      if (kind == kX) {
-        slots += rleaf ? 1 : 2;
-      } else if (kind == kB) {
-        ++nB;
-        kev += (unsigned long long)qcount * (unsigned long long)w.cnt[j];
-        ret += dlo;
-      } else {
-        ret += dlo;
-        if (kind == kF) ++nF;
-        else {
-          ++nDT;
-          if (kind == kT) ++nT;
-        }
-      }
-    }
-    if (kind != kX) cov += (unsigned long long)qcount * (unsigned long long)w.cnt[j];
-    w.dec[j] = kind | (order << 8);
-  }
-  fd_dlo = group_sum<32>(fd_dlo);
-  fd_const = group_sum<32>(fd_const);
-  ret = group_sum<32>(ret);
-  nF = group_sum_i<32>(nF);
-  nDT = group_sum_i<32>(nDT);
-  nT = group_sum_i<32>(nT);
-  nB = group_sum_i<32>(nB);
-  nFD = group_sum_i<32>(nFD);
-  slots = group_sum_i<32>(slots);
-  kev = group_sum_i<32>(kev);
-  cov = group_sum_i<32>(cov);
-  const int ne = slots > 0 ? (qleaf ? 1 : 2) : 0;
-  const int cl = slots;
-  const double newbase = fb + (fd_dlo + ret);
-  APH(2);
-  if (lane == 0) {
-    if (nFD) {
-      a.L[(size_t)key * a.T] += fd_const;  // constant local term (order 1)
-      if (a.Lord[key] < 1) a.Lord[key] = 1;
-    }
-    unsigned long long* ss = sst[slot];
-    atomicAdd(ss + sPairs, (unsigned long long)len);
-    if (nFD) atomicAdd(ss + sFD, (unsigned long long)nFD);
-    if (nF) atomicAdd(ss + sF, (unsigned long long)nF);
-    if (nDT - nT) atomicAdd(ss + sD, (unsigned long long)(nDT - nT));
-    if (nT) atomicAdd(ss + sT, (unsigned long long)nT);
-    if (nB) atomicAdd(ss + sB, (unsigned long long)nB);
-    if (kev) atomicAdd(ss + sKev, kev);
-    if (cov) atomicAdd(ss + sCov, cov);
-  }
-  // space: children's queue slots (dense), pairs and items (per-warp chunks)
-  int qe = 0;
-  if (lane == 0 && ne) qe = atomicAdd(q.c(acTail), ne);
-  qe = __shfl_sync(0xffffffffu, qe, 0);
-  int g0, g1;
-  const int pp = reserve(rp, ne * slots, q.c(acPool), kAsyncChunkP, st.capP, lane, g0, g1);
-  const int pf = reserve(rf, nF, q.c(acF), kAsyncChunkI, st.capF, lane, g0, g1);
-  invalidate_items(a.itF, g0, g1, st.capF, lane);
-  const int pdt = reserve(rdt, nDT, q.c(acDT), kAsyncChunkI, st.capDT, lane, g0, g1);
-  invalidate_items(a.itDT, g0, g1, st.capDT, lane);
-  const int pb = reserve(rb, nB, q.c(acB), kAsyncChunkI, st.capB, lane, g0, g1);
-  invalidate_items(a.itB, g0, g1, st.capB, lane);
-  APH(3);
-  if (!(qe + ne <= st.capE && pp >= 0 && pf >= 0 && pdt >= 0 && pb >= 0)) {
-    if (lane == 0) atomicExch(&st.overflow, 1);
-    const bool dead = lane < ne && qe + lane < st.capE;
-    if (dead) st_release(q.ready + qe + lane, 2);
-    return __popc(__ballot_sync(0xffffffffu, dead));
-  }
-  // emit (emit_entry's order): children entries, their pairs, the work items
-  if (lane == 0 && ne) {
-    if (qleaf) {
-      a.fq[0][qe] = key;
-      a.fbase[0][qe] = newbase;
-      a.foff[0][qe] = pp;
-      a.flen[0][qe] = cl;
-    } else {
-      a.fq[0][qe] = slot * K + qleft;
-      a.fq[0][qe + 1] = slot * K + qright;
-      a.fbase[0][qe] = newbase;
-      a.fbase[0][qe + 1] = newbase;
-      a.foff[0][qe] = pp;
-      a.foff[0][qe + 1] = pp + cl;
-      a.flen[0][qe] = cl;
-      a.flen[0][qe + 1] = cl;
-    }
-  }
-  int* pool = a.fr[0];
-  int runX = 0, runF = 0, runDT = 0, runB = 0;
-  for (int j0 = 0; j0 < len; j0 += 32) {
-    const int j = j0 + lane;
-    int kind = kE, order = 0, R = 0, rl = -1, rr = -1;
-    if (j < len) {
-      const int dcode = w.dec[j];
-      kind = dcode & 0xff;
-      order = dcode >> 8;
-      R = w.R[j];
-      rl = w.rl[j];
-      rr = w.rr[j];
-    }
-    const bool rleaf = (j < len) ? rl < 0 : true;
-    int tot;
-    const int px = warp_excl_scan<32>(kind == kX ? (rleaf ? 1 : 2) : 0, lane, tot);
-    if (kind == kX) {
-      const int dst = pp + runX + px;
-      if (rleaf) {
-        pool[dst] = R;
-        if (!qleaf) pool[dst + cl] = R;
-      } else {
-        pool[dst] = rl;
-        pool[dst + 1] = rr;
-        if (!qleaf) {
-          pool[dst + cl] = rl;
-          pool[dst + cl + 1] = rr;
-        }
-      }
-    }
-    runX += tot;
-    int t2;
-    const int xf = warp_excl_scan<32>(kind == kF, lane, t2);
-    if (kind == kF) a.itF[pf + runF + xf] = Item{ key, R, order | (kF << 8), rF + runF + xf };
-    runF += t2;
-    const int xd = warp_excl_scan<32>(kind == kD || kind == kT, lane, t2);
-    if (kind == kD || kind == kT) a.itDT[pdt + runDT + xd] = Item{ key, R, order | (kind << 8), rDT + runDT + xd };
-    runDT += t2;
-    const int xb = warp_excl_scan<32>(kind == kB, lane, t2);
-    if (kind == kB) a.itB[pb + runB + xb] = Item{ key, R, (kB << 8) | order, rB + runB + xb };
-    runB += t2;
-  }
-  if (lane == 0) {
-    a.cntF[key] = rF + runF;
-    a.cntDT[key] = rDT + runDT;
-    a.cntB[key] = rB + runB;
-  }
-  totF += nF;
-  totDT += nDT;
-  totB += nB;
-  APH(4);
-  __threadfence();
-  __syncwarp();
-  APH(5);
-  if (lane < ne) {
-    q.depth[qe + lane] = (unsigned char)min(255, q.depth[i] + 1);
-#ifdef DFGTB_ASYNC_TRACE
-    unsigned long long t_;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-    q.tr[3 * (size_t)(qe + lane)] = t_;
-#endif
-    st_release(q.ready + qe + lane, 1);
-  }
-#ifdef DFGTB_ASYNC_TRACE
-  if (lane == 0) {
-    unsigned long long t_;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-    q.tr[3 * (size_t)i + 2] = t_;
-  }
-#endif
-  if (lane == 0 && ne) atomicMax(&st.levels, (int)q.depth[i] + 2);
-  return ne;
-}
-
-#ifndef DFGTB_ASYNC_MINB
-#define DFGTB_ASYNC_MINB 6
-#endif
-template <int DT>
-__global__ void __launch_bounds__(kAsyncBlock, DFGTB_ASYNC_MINB) k_trav_async(const __grid_constant__ TravArgs a, AsyncQ q)
-{
-  TravState& st = *a.st;
-  const int lane = threadIdx.x & 31;
-  const int K = st.K;
-  __shared__ unsigned long long s_sst[kMaxSlots][sNStat];
-  __shared__ double s_h[kMaxSlots], s_scale[kMaxSlots];
-  extern __shared__ __align__(16) unsigned char s_dyn[];
-  WarpScratch* s_ws = reinterpret_cast<WarpScratch*>(s_dyn);  // one per warp (dynamic)
-  for (int k = threadIdx.x; k < kMaxSlots * sNStat; k += blockDim.x) (&s_sst[0][0])[k] = 0;
-  for (int k = threadIdx.x; k < st.nslots; k += blockDim.x) {
-    s_h[k] = st.h[k];
-    s_scale[k] = st.scale[k];
-  }
-  __syncthreads();
-  Reserve rp, rf, rdt, rb;
-  int g0, g1, totF = 0, totDT = 0, totB = 0;
-  for (;;) {
-    int i = 0;
-    if (lane == 0) i = atomicAdd(q.c(acHead), 1);
-    i = __shfl_sync(0xffffffffu, i, 0);
-    if (i >= st.capE) break;  // past every slot that can ever be published
-    int ok = 0;  // 1: an entry to process, 2: a dead slot (its producer overflowed), 0: done
-    if (lane == 0) {
-      unsigned ns = 32;
-      for (long long polls = 0;; ++polls) {
-        ok = ld_acquire(q.ready + i);
-        if (ok) break;
-        if ((polls & 15) == 15 && ld_acquire(q.c(acPending)) == 0) {
-          ok = ld_acquire(q.ready + i);
-          break;
-        }
-        if (polls > kAsyncMaxPolls) {
-          if (atomicExch(&st.overflow, 3) != 3)
-            st.lvl = Cnt{ i, *q.c(acHead), *q.c(acTail), *q.c(acPending), *q.c(acPool), 0, 0 };
-          break;
-        }
-        __nanosleep(ns);
-        ns = ns < kAsyncMaxSleep ? 2 * ns : kAsyncMaxSleep;
-      }
-      if (ok == 2) atomicAdd(q.c(acPending), -1);
-    }
-    ok = __shfl_sync(0xffffffffu, ok, 0);
-    if (!ok) break;
-    if (ok == 2) continue;
-    __syncwarp();  // lane 0's acquire orders the whole warp's reads of the entry
-#ifdef DFGTB_ASYNC_TRACE
-    if (lane == 0) {
-      unsigned long long t_;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-      q.tr[3 * (size_t)i + 1] = t_;
-    }
-#endif
-    if (a.flen[0][i] <= kFuseMax) {
-      const int nchild = async_entry<DT>(a, st, q, i, lane, s_ws[threadIdx.x >> 5], s_sst, rp, rf, rdt, rb,
-                                         totF, totDT, totB, s_h, s_scale, K);
-      if (lane == 0) atomicAdd(q.c(acPending), nchild - 1);
-      continue;
-    }
-    classify_entry<DT, 32>(a, st, 0, i, lane, true, s_sst);
-    __syncwarp();
-    // space for the children's queue slots (dense: consumers claim them in order), pairs
-    // and work items (per-warp chunks: gaps are harmless / marked invalid)
-    const Cnt c = a.cnt[i];
-    int qe = 0;
-    if (lane == 0 && c.e) qe = atomicAdd(q.c(acTail), c.e);
-    qe = __shfl_sync(0xffffffffu, qe, 0);
-    const int pp = reserve(rp, c.p, q.c(acPool), kAsyncChunkP, st.capP, lane, g0, g1);
-    const int pf = reserve(rf, c.f, q.c(acF), kAsyncChunkI, st.capF, lane, g0, g1);
-    invalidate_items(a.itF, g0, g1, st.capF, lane);
-    const int pdt = reserve(rdt, c.dt, q.c(acDT), kAsyncChunkI, st.capDT, lane, g0, g1);
-    invalidate_items(a.itDT, g0, g1, st.capDT, lane);
-    const int pb = reserve(rb, c.b, q.c(acB), kAsyncChunkI, st.capB, lane, g0, g1);
-    invalidate_items(a.itB, g0, g1, st.capB, lane);
-    const bool fits = qe + c.e <= st.capE && pp >= 0 && pf >= 0 && pdt >= 0 && pb >= 0;
-    int nchild = 0;
-    if (fits) {
-      const Cnt o{ qe, pp, pf, pdt, 0, pb, 0 };
-      emit_entry<32>(a, K, 0, 0, 0, 0, i, o, lane, true);
-      nchild = c.e;
-      totF += c.f;
-      totDT += c.dt;
-      totB += c.b;
-      __threadfence();
-      __syncwarp();
-      if (lane < nchild) {
-        q.depth[qe + lane] = (unsigned char)min(255, q.depth[i] + 1);
-#ifdef DFGTB_ASYNC_TRACE
-        unsigned long long t_;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-        q.tr[3 * (size_t)(qe + lane)] = t_;
-        if (lane == 0) q.tr[3 * (size_t)i + 2] = t_;
-#endif
-        st_release(q.ready + qe + lane, 1);
-      }
-      if (lane == 0 && nchild) atomicMax(&st.levels, (int)q.depth[i] + 2);
-    } else {
-      // the host regrows the buffers and reruns the batch; the reserved slots are
-      // published dead, so their claimants move on (a live entry beyond them must still
-      // be claimed)
-      if (lane == 0) atomicExch(&st.overflow, 1);
-      const bool dead = lane < c.e && qe + lane < st.capE;
-      if (dead) st_release(q.ready + qe + lane, 2);
-      nchild = __popc(__ballot_sync(0xffffffffu, dead));
-    }
-    if (lane == 0) atomicAdd(q.c(acPending), nchild - 1);
-  }
-  if (lane == 0) {  // real item totals (the extents include the invalidated gaps)
-    if (totF) atomicAdd(q.c(acRF), totF);
-    if (totDT) atomicAdd(q.c(acRDT), totDT);
-    if (totB) atomicAdd(q.c(acRB), totB);
-  }
-  // unused tails of this warp's item chunks
-  invalidate_items(a.itF, rf.pos, rf.end, st.capF, lane);
-  invalidate_items(a.itDT, rdt.pos, rdt.end, st.capDT, lane);
-  invalidate_items(a.itB, rb.pos, rb.end, st.capB, lane);
-  __syncthreads();
-  for (int k = threadIdx.x; k < st.nslots * sNStat; k += blockDim.x) {
-    const unsigned long long v = (&s_sst[0][0])[k];
-    if (v) atomicAdd(&st.sst[0][0] + k, v);
-  }
-}
-
-// Totals of the asynchronous traversal into the state (k_trav_publish reads nF / nDT / nB;
-// positions past the last reservation are never written).
-__global__ void k_async_finish(const __grid_constant__ TravArgs a, AsyncQ q)
-{
-  TravState& st = *a.st;
-  st.xF = *q.c(acF);
-  st.xDT = *q.c(acDT);
-  st.xB = *q.c(acB);
-  st.nF = *q.c(acRF);
-  st.nDT = *q.c(acRDT);
-  st.nB = *q.c(acRB);
-  st.atail = *q.c(acTail);
-  st.aptail = *q.c(acPool);
-}
-
-// The root entries (k_trav_init wrote them at slots 0..nb-1) are published.
-__global__ void k_async_init(const __grid_constant__ TravArgs a, AsyncQ q)
-{
-  TravState& st = *a.st;
-  const int m0 = st.m[0], p0 = st.p[0];  // the start frontier (k_trav_init)
-  for (int b = threadIdx.x; b < m0; b += blockDim.x) {
-    q.ready[b] = 1;
-    q.depth[b] = 0;
-  }
-  if (threadIdx.x < acNum) {
-    const int k = threadIdx.x;
-    *q.c(k) = k == acTail || k == acPending ? m0 : k == acPool ? p0 : 0;
-  }
-  if (threadIdx.x == 0) st.levels = 1;
-}
 
 #ifndef DFGTB_TRAV_CTAS_PER_SM
 #define DFGTB_TRAV_CTAS_PER_SM 1
@@ -2067,9 +1583,9 @@ __global__ void k_trav_publish(const TravState* st, int* bc)
   bc[1] = ovf ? 0 : st->nDT;
   bc[2] = ovf ? 0 : st->nB;
   bc[3] = ovf;
-  bc[8] = ovf ? 0 : max(st->nF, st->xF);  // extents of the unsorted item arrays
-  bc[9] = ovf ? 0 : max(st->nDT, st->xDT);
-  bc[10] = ovf ? 0 : max(st->nB, st->xB);
+  bc[8] = ovf ? 0 : st->nF;  // extents of the unsorted item arrays
+  bc[9] = ovf ? 0 : st->nDT;
+  bc[10] = ovf ? 0 : st->nB;
 }
 
 __global__ void k_trav_clear_on_overflow(const int* bc, int* cntF, int* cntDT, int* cntB, int KB)
@@ -2084,7 +1600,7 @@ __global__ void k_scatter_dev(const Item* in, const int* n, int cap, const int* 
   const int m = min(*n, cap);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
     const Item it = in[i];
-    if (it.key >= 0) out[noff[it.key] + it.rank] = it;  // async traversal: gaps are key -1
+    if (it.key >= 0) out[noff[it.key] + it.rank] = it;
   }
 }
 
@@ -2169,26 +1685,7 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     capDT_ = std::max(capDT_, tiny ? 64 : std::max(4096, 2 * kb));
     capB_ = std::max(capB_, tiny ? 64 : std::max(1 << 16, 16 * kb));
   }
-  if (use_async_) {  // one queue of every entry of the batch, one pool of every pair
-    const int kb = (int)std::min<long long>(KB, INT32_MAX / 128);
-    capEA_ = std::max(capEA_, std::max(1 << 16, 16 * kb));
-    capPA_ = std::max(capPA_, std::max(1 << 20, 64 * kb));
-    fq_[0].reserve(capEA_);
-    foff_[0].reserve(capEA_);
-    flen_[0].reserve(capEA_);
-    fbase_[0].reserve(capEA_);
-    fr_[0].reserve(capPA_);
-    pent_[0].reserve(capPA_);
-    pkmax_.reserve(capPA_);
-    pkmin_.reserve(capPA_);
-    dec_.reserve(capPA_);
-    cnt_.reserve(capEA_);
-    childlen_.reserve(capEA_);
-    newbase_.reserve(capEA_);
-    aready_.reserve(capEA_);
-    adepth_.reserve(capEA_);
-    CK(cudaMemsetAsync(aready_.p, 0, sizeof(int) * capEA_, s));
-  } else {
+  {
     for (int b = 0; b < 2; ++b) {
       fq_[b].reserve(capE_);
       foff_[b].reserve(capE_);
@@ -2226,8 +1723,8 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   a.series = cfg_.mode == 1;
   a.T = T;
   a.st = ds;
-  for (int b = 0; b < 2; ++b) {  // async: both "levels" are the one queue / pool
-    const int bb = use_async_ ? 0 : b;
+  for (int b = 0; b < 2; ++b) {
+    const int bb = b;
     a.fq[b] = fq_[bb].p;
     a.foff[b] = foff_[bb].p;
     a.flen[b] = flen_[bb].p;
@@ -2283,8 +1780,8 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     hs->h[b] = h[b];
     hs->scale[b] = -1.0 / (2.0 * h[b] * h[b]);
   }
-  hs->capE = use_async_ ? capEA_ : capE_;
-  hs->capP = use_async_ ? capPA_ : capP_;
+  hs->capE = capE_;
+  hs->capP = capP_;
   hs->capF = capF_;
   hs->capDT = capDT_;
   hs->capB = capB_;
@@ -2292,42 +1789,7 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   start_frontier(qt, &a);
   k_trav_init<<<1, 256, 0, s>>>(a);
   CK_LAUNCH();
-  if (use_async_) {
-    actr_.reserve(acNum * kAsyncCtr);
-    AsyncQ q{ aready_.p, actr_.p, adepth_.p, nullptr };
-#ifdef DFGTB_ASYNC_TRACE
-    atrace_.reserve((size_t)11 * capEA_);
-    CK(cudaMemsetAsync(atrace_.p, 0, sizeof(unsigned long long) * 11 * capEA_, s));
-    q.tr = atrace_.p;
-#endif
-    k_async_init<<<1, 64, 0, s>>>(a, q);
-    CK_LAUNCH();
-    static int grid = 0;
-    if (!grid) {
-      int dev = 0, nsm = 0, per_sm = 0;
-      CK(cudaGetDevice(&dev));
-      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-      for (void* f : { (void*)k_trav_async<0>, (void*)k_trav_async<1>, (void*)k_trav_async<2>, (void*)k_trav_async<3>,
-                       (void*)k_trav_async<4>, (void*)k_trav_async<5> })
-        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsyncSmem));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trav_async<2>, kAsyncBlock, kAsyncSmem));
-      const char* env = std::getenv("DFGTB_ASYNC_CTAS");
-      grid = nsm * std::max(1, env ? std::min(per_sm, std::atoi(env)) : per_sm);
-    }
-    switch (D_) {
-    case 1: k_trav_async<1><<<grid, kAsyncBlock, kAsyncSmem, s>>>(a, q); break;
-    case 2: k_trav_async<2><<<grid, kAsyncBlock, kAsyncSmem, s>>>(a, q); break;
-    case 3: k_trav_async<3><<<grid, kAsyncBlock, kAsyncSmem, s>>>(a, q); break;
-    case 4: k_trav_async<4><<<grid, kAsyncBlock, kAsyncSmem, s>>>(a, q); break;
-    case 5: k_trav_async<5><<<grid, kAsyncBlock, kAsyncSmem, s>>>(a, q); break;
-    default: k_trav_async<0><<<grid, kAsyncBlock, kAsyncSmem, s>>>(a, q); break;
-    }
-    CK_LAUNCH();
-    k_async_finish<<<1, 1, 0, s>>>(a, q);
-    CK_LAUNCH();
-  } else {
-    run_levels(&a, sig);
-  }
+  run_levels(&a, sig);
   k_trav_publish<<<1, 1, 0, s>>>(ds, bc_.p);
   CK_LAUNCH();
   k_trav_clear_on_overflow<<<148, 256, 0, s>>>(bc_.p, cntF_.p, cntDT_.p, cntB_.p, (int)KB);
@@ -2414,85 +1876,6 @@ bool Engine::traverse_finish()
     }
   }
   if (hs->overflow == 2) throw CudaError("traversal exceeded 1024 levels");
-#ifdef DFGTB_ASYNC_TRACE
-  if (use_async_ && !hs->overflow) {
-    const int ne = hs->atail;
-    std::vector<unsigned long long> tr((size_t)3 * ne);
-    std::vector<int> len(ne);
-    std::vector<unsigned char> dep(ne);
-    CK(cudaMemcpy(tr.data(), atrace_.p, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(len.data(), flen_[0].p, sizeof(int) * ne, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(dep.data(), adepth_.p, ne, cudaMemcpyDeviceToHost));
-    unsigned long long t0 = ~0ull, t1 = 0;
-    double hand = 0, proc = 0, lproc[6] = {}, lcnt[6] = {};
-    int nh = 0;
-    std::vector<double> dstart(256, 1e30), dend(256, 0);
-    for (int i = 0; i < ne; ++i) {
-      const unsigned long long pub = tr[3 * i], st0 = tr[3 * i + 1], fin = tr[3 * i + 2];
-      if (!st0) continue;
-      t0 = std::min(t0, st0);
-      t1 = std::max(t1, fin ? fin : st0);
-      if (pub) {
-        hand += (double)(st0 - pub);
-        ++nh;
-      }
-      if (fin) {
-        const double pt = (double)(fin - st0);
-        proc += pt;
-        const int b = len[i] <= 8 ? 0 : len[i] <= 32 ? 1 : len[i] <= 64 ? 2 : len[i] <= 128 ? 3 : len[i] <= 256 ? 4 : 5;
-        lproc[b] += pt;
-        lcnt[b] += 1;
-      }
-      dstart[dep[i]] = std::min(dstart[dep[i]], (double)st0);
-      dend[dep[i]] = std::max(dend[dep[i]], (double)(fin ? fin : st0));
-    }
-    std::fprintf(stderr, "DFGTB_ASYNC_TRACE entries %d span %.1f us, handoff mean %.2f us, processing mean %.2f us; by length "
-                 "<=8 %.2f <=32 %.2f <=64 %.2f <=128 %.2f <=256 %.2f >256 %.2f us\n", ne, (t1 - t0) * 1e-3,
-                 nh ? hand / nh * 1e-3 : 0.0, proc / std::max(1, ne) * 1e-3, lproc[0] / std::max(1.0, lcnt[0]) * 1e-3,
-                 lproc[1] / std::max(1.0, lcnt[1]) * 1e-3, lproc[2] / std::max(1.0, lcnt[2]) * 1e-3,
-                 lproc[3] / std::max(1.0, lcnt[3]) * 1e-3, lproc[4] / std::max(1.0, lcnt[4]) * 1e-3,
-                 lproc[5] / std::max(1.0, lcnt[5]) * 1e-3);
-    {
-      std::vector<unsigned long long> ph((size_t)8 * ne);
-      CK(cudaMemcpy(ph.data(), atrace_.p + (size_t)3 * capEA_, sizeof(unsigned long long) * ph.size(),
-                    cudaMemcpyDeviceToHost));
-      double acc[6] = {};
-      int nn = 0;
-      for (int i = 0; i < ne; ++i) {
-        const unsigned long long* p = ph.data() + 8 * i;
-        const unsigned long long st0 = tr[3 * i + 1], fin = tr[3 * i + 2];
-        if (!p[0] || !p[5] || !st0 || !fin) continue;
-        acc[0] += (double)(p[0] - st0);
-        for (int k = 1; k <= 5; ++k) acc[k] += (double)(p[k] - p[k - 1]);
-        ++nn;
-      }
-      std::fprintf(stderr, "  phases (us, mean of %d fused entries): loads %.2f pass1 %.2f pass2 %.2f reserve %.2f emit %.2f fence %.2f\n",
-                   nn, acc[0] / nn * 1e-3, acc[1] / nn * 1e-3, acc[2] / nn * 1e-3, acc[3] / nn * 1e-3, acc[4] / nn * 1e-3,
-                   acc[5] / nn * 1e-3);
-    }
-    for (int d = 0; d < 64 && dend[d] > 0; ++d)
-      std::fprintf(stderr, "  depth %d: first start %.1f us, last finish %.1f us\n", d, (dstart[d] - t0) * 1e-3,
-                   (dend[d] - t0) * 1e-3);
-  }
-#endif
-  if (hs->overflow == 3)
-    throw CudaError("asynchronous traversal: queue slot " + std::to_string(hs->lvl.e) + " was never published (head " +
-                    std::to_string(hs->lvl.p) + ", tail " + std::to_string(hs->lvl.f) + ", pending " +
-                    std::to_string(hs->lvl.dt) + ", pairs " + std::to_string(hs->lvl.t) + ", cap " +
-                    std::to_string(capEA_) + "/" + std::to_string(capPA_) + ")");
-  if (hs->overflow && use_async_) {
-    auto grow2 = [](int cap, long long need) {
-      if (need <= cap) return cap;
-      if (need > INT32_MAX / 4) throw OutOfMemory("traversal exceeds 2^29 entries / pairs / items");
-      return (int)std::max<long long>(2ll * cap, 2 * need);
-    };
-    capEA_ = grow2(capEA_, hs->atail);
-    capPA_ = grow2(capPA_, hs->aptail);
-    capF_ = grow2(capF_, std::max(hs->nF, hs->xF));
-    capDT_ = grow2(capDT_, std::max(hs->nDT, hs->xDT));
-    capB_ = grow2(capB_, std::max(hs->nB, hs->xB));
-    return false;
-  }
   if (hs->overflow) {
     const Cnt l = hs->lvl;
     auto grow = [](int cap, long long need) {

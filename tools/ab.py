@@ -3,7 +3,7 @@
 resident): for each libdfgtb.so given, a fresh process times --steps sweeps and prints
 ms/step and the per-phase device times.
 
-  python tools/ab.py [--config 2] [--steps 20] lib1.so lib2.so:DFGTB_TRAV_ASYNC=1 ...
+  python tools/ab.py [--config 2] [--steps 20] lib1.so lib2.so:DFGTB_ONE_STREAM=1 ...
 """
 import json
 import os
