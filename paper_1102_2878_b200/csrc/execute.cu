@@ -1303,28 +1303,16 @@ __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
   double* qs = rs + RMAX * Geo::DS;
   double* qsum = qs + 32 * Geo::DS;
   unsigned* smask = smask_all[threadIdx.x >> 5];
-  // work unit = (task, query sub-chunk of kQS): when this kernel gets few tasks (cfg2:
-  // the small-h leaf pairs off the FP32 path, ~2 per warp) their query chunks are split
-  // in 4 to keep more warps busy (each sub-chunk stages the run itself: slower when the
-  // tasks are plentiful, measured on cfg3 / cfg5)
-  const int nwarps = gridDim.x * Geo::WARPS;
-  const int split = nl <= 2 * nwarps ? 4 : 1;
-  const int kQS = 32 / split;
-  for (int i = next_task(next, lane); i < nl * split;) {
-    const int w = tlist[i / split], qlo = (i % split) * kQS;
+  for (int i = next_task(next, lane); i < nl;) {
+    const int w = tlist[i];
     const BTask t = tasks[w];
-    const int inext = next_task(next, lane);  // the next unit, fetched early
-    TaskView v = task_view(t, Q, K, rec, lane);
-    v.qc = max(0, min(kQS, v.qc - qlo));  // this sub-chunk's queries
-    if (v.qc == 0) {
-      i = inext;
-      continue;
-    }
+    const int inext = next_task(next, lane);  // the next task, fetched early
+    const TaskView v = task_view(t, Q, K, rec, lane);
     const bool fast = __all_sync(0xffffffffu, lane >= v.nit || (v.rc.y & (1 << 28)));
     const bool clampok = __all_sync(0xffffffffu, lane >= v.nit || (v.rc.y & (3 << 28)));
     const bool mf = (fast || clampok) && (mufu & 1);
-    const double* qsrc = xq + ((size_t)v.slot * nq + v.qb + t.q0 + qlo) * DP;
-    double cq[DT];  // MUFU path: centre = the sub-chunk's first query
+    const double* qsrc = xq + ((size_t)v.slot * nq + v.qb + t.q0) * DP;
+    double cq[DT];  // MUFU path: centre = the chunk's first query
 #pragma unroll
     for (int d = 0; d < DT; ++d) cq[d] = qsrc[d];
     if (lane < v.qc) {
@@ -1359,7 +1347,7 @@ __global__ void __launch_bounds__(BaseGeo<DT>::WARPS * 32, DFGTB_BASE_MINB)
       qsum[lane] += 1.0 - exp2_neg_fixed<false>(tq, fbits);
     }
     __syncwarp();
-    if (lane < v.qc) part[(size_t)w * 32 + qlo + lane] = qsum[lane];
+    if (lane < v.qc) part[(size_t)w * 32 + lane] = qsum[lane];
     __syncwarp();
     i = inext;
   }
@@ -2262,7 +2250,7 @@ void launch_base_t(const int* ntasks, int tcap, cudaStream_t s, TreeView Q, int 
     CK_LAUNCH();
   }
   if (mid) CK(cudaEventRecord(mid, s));
-  k_base_case<DT><<<std::min(gridB, cap_grid * 4), threads, smem, s>>>(Q, K, tasks, listB, ws + 3, rec, xq, xr,
+  k_base_case<DT><<<std::min(gridB, cap_grid), threads, smem, s>>>(Q, K, tasks, listB, ws + 3, rec, xq, xr,
                                                                   nq, nr, part, ws + 1, mufu, c0, sv, f);
 }
 
