@@ -182,20 +182,29 @@ class DualTreeEngine:
         check(lib.dfgtb_compute(self._h, _dp(q), q.shape[0], float(h), _dp(out), None))
         return out
 
-    def compute_batch(self, queries, hs) -> np.ndarray:
+    def compute_batch(self, queries, hs, out: np.ndarray | None = None) -> np.ndarray:
         """Sums for several bandwidths through one lock-step GPU traversal:
-        row b = compute(queries, hs[b]).  Returns (len(hs), n_queries)."""
+        row b = compute(queries, hs[b]).  Returns (len(hs), n_queries), written into
+        `out` when given (a C-contiguous float64 array of that shape, e.g. pinned host
+        memory reused across calls)."""
         hv = np.ascontiguousarray(hs, dtype=np.float64).ravel()
+
+        def _out(n):
+            if out is None:
+                return np.empty((hv.size, n))
+            if out.dtype != np.float64 or out.shape != (hv.size, n) or not out.flags.c_contiguous:
+                raise ValueError(f"out must be a C-contiguous float64 array of shape {(hv.size, n)}")
+            return out
         if isinstance(queries, np.ndarray) and queries.dtype == np.float32:
             q32 = np.ascontiguousarray(queries.reshape(-1, 1) if queries.ndim == 1 else queries)
             if q32.ndim != 2 or q32.shape[1] != self.refs.shape[1]:
                 raise ValueError("query and reference dimensions differ")
-            out = np.empty((hv.size, q32.shape[0]))
+            res = _out(q32.shape[0])
             st = (_capi.Stats * max(1, hv.size))()
             check(lib.dfgtb_compute_batch_f32(self._h, q32.ctypes.data_as(_F), q32.shape[0],
-                                              _dp(hv), hv.size, _dp(out), st))
+                                              _dp(hv), hv.size, _dp(res), st))
             self._batch_stats = [TraversalStats(**s.as_dict()) for s in st[:hv.size]]
-            return out
+            return res
         if queries is None or queries is self.refs:
             q, nq, n_out = None, 0, self.refs.shape[0]
         else:
@@ -203,12 +212,12 @@ class DualTreeEngine:
             if q.shape[1] != self.refs.shape[1]:
                 raise ValueError("query and reference dimensions differ")
             nq = n_out = q.shape[0]
-        out = np.empty((hv.size, n_out))
+        res = _out(n_out)
         st = (_capi.Stats * max(1, hv.size))()
         check(lib.dfgtb_compute_batch(self._h, _dp(q) if q is not None else None, nq, _dp(hv),
-                                      hv.size, _dp(out), st))
+                                      hv.size, _dp(res), st))
         self._batch_stats = [TraversalStats(**s.as_dict()) for s in st[:hv.size]]
-        return out
+        return res
 
     def batch_stats(self):
         return list(getattr(self, "_batch_stats", []))

@@ -319,3 +319,19 @@ def test_float32_inputs_match_widened(dfgtb):
     with dfgtb.DualTreeEngine(r32.astype(np.float64), config=cfg) as e64:
         b = e64.compute_batch(q32.astype(np.float64), hs)
     assert np.array_equal(a, b)
+
+
+def test_compute_batch_into_out(dfgtb):
+    """compute_batch(..., out=) writes the same sums into a caller's (e.g. pinned) buffer,
+    for float64 and float32 queries, and rejects a wrongly shaped one."""
+    g = np.random.default_rng(12)
+    r, q = g.random((3000, 3)), g.random((1000, 3))
+    hs = [0.02, 0.05, 0.2]
+    with dfgtb.DualTreeEngine(r, config=dfgtb.EngineConfig(epsilon=0.01, leaf_threshold=32)) as e:
+        for qq in (q, q.astype(np.float32)):
+            want = e.compute_batch(qq, hs)
+            out = np.full((3, 1000), -1.0)
+            got = e.compute_batch(qq, hs, out=out)
+            assert got is out and np.array_equal(out, want)
+        with pytest.raises(ValueError):
+            e.compute_batch(q, hs, out=np.empty((2, 1000)))
