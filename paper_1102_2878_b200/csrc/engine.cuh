@@ -148,7 +148,13 @@ private:
   int leaves_src_ = -1;     // 0: leaves_ describe the reference tree, 1: a query tree
   // per batch (node-indexed arrays are slot-major: key = slot * K + node)
   DevBuf<double> L_, Mt_, s_ff_;      // Mt_: UNSCALED reference moments (h-independent)
-  DevBuf<int> Lord_, cntF_, cntDT_, cntB_, offF_, offDT_, offB_, mflag_, mdone_;
+  DevBuf<int> Lord_, mflag_, mdone_;
+  // per-key item counts and their exclusive scans, F | DT | B back to back (one scan and
+  // one scatter launch sort all three item kinds); the names view the three segments
+  DevBuf<int> cntAll_, offAll_, offLoc_;
+  struct IntView {
+    int* p = nullptr;
+  } cntF_, cntDT_, cntB_, offF_, offDT_, offB_;
   bool eager_ = false;                // Mt_ holds every node (tables <= 4096 terms)
   DevBuf<int> lnch_, lchoff_, lchunk_, tasks_, leaf_task_, leaf_runs_, brec_, bnext_;
   DevBuf<double> lpart_, bpart_, xq_, xr_, slotp_;

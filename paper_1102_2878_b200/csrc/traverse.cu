@@ -313,17 +313,19 @@ __global__ void k_trav_init(const __grid_constant__ TravArgs a)
   // node (the roots unless a start depth is set: the levels above it are skipped -- a
   // valid dual-tree traversal whose first lower bounds already sum over many nodes)
   const int nq = a.sq ? a.nsq : 1, nr = a.sq ? a.nsr : 1;
-  for (int e = threadIdx.x; e < nb * nq; e += blockDim.x) {
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int e = t0; e < nb * nq; e += nt) {
     const int b = e / nq, qi = e - b * nq;
     a.fq[0][e] = b * st.K + (a.sq ? a.sq[qi] : 0);
     a.foff[0][e] = e * nr;
     a.flen[0][e] = nr;
     a.fbase[0][e] = 0.0;
   }
-  for (int j = threadIdx.x; j < nb * nq * nr; j += blockDim.x) {
+  for (int j = t0; j < nb * nq * nr; j += nt) {
     a.fr[0][j] = a.sq ? a.sr[j % nr] : 0;
     a.pent[0][j] = j / nr;
   }
+  if (blockIdx.x != 0) return;
   for (int b = threadIdx.x; b < nb; b += blockDim.x)
     for (int k = 0; k < sNStat; ++k) st.sst[b][k] = 0;
   if (threadIdx.x == 0) {
@@ -1595,12 +1597,29 @@ __global__ void k_trav_clear_on_overflow(const int* bc, int* cntF, int* cntDT, i
     cntF[i] = cntDT[i] = cntB[i] = 0;
 }
 
-__global__ void k_scatter_dev(const Item* in, const int* n, int cap, const int* noff, Item* out)
+// Counting sort of the three item kinds by (key, rank).  scan = exclusive scan of the
+// F | DT | B per-key counts (3 KB); n = the item totals (bc[8..10]).  Writes each kind's
+// per-key offsets rebased to its segment start (offLoc, 3 segments of KB) and its items
+// to sorted position (offset of its key + its rank).
+__global__ void k_sort_items3(const int* scan, int KB, const int* n, const Item* inF, const Item* inDT,
+                              const Item* inB, int capF, int capDT, int capB, int* offLoc, Item* outF,
+                              Item* outDT, Item* outB)
 {
-  const int m = min(*n, cap);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    const Item it = in[i];
-    if (it.key >= 0) out[noff[it.key] + it.rank] = it;
+  const int b1 = scan[KB], b2 = scan[2 * KB];  // segment starts (the first one is 0)
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int i = t0; i < 3 * KB; i += nt) offLoc[i] = scan[i] - (i < KB ? 0 : i < 2 * KB ? b1 : b2);
+  const int mF = min(n[0], capF), mDT = min(n[1], capDT), mB = min(n[2], capB);
+  for (int i = t0; i < mF + mDT + mB; i += nt) {
+    if (i < mF) {
+      const Item it = inF[i];
+      if (it.key >= 0) outF[scan[it.key] + it.rank] = it;
+    } else if (i < mF + mDT) {
+      const Item it = inDT[i - mF];
+      if (it.key >= 0) outDT[scan[KB + it.key] - b1 + it.rank] = it;
+    } else {
+      const Item it = inB[i - mF - mDT];
+      if (it.key >= 0) outB[scan[2 * KB + it.key] - b2 + it.rank] = it;
+    }
   }
 }
 
@@ -1666,7 +1685,11 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   if (KB > INT32_MAX / 2) throw OutOfMemory("batch too large: slots * nodes exceeds 2^30");
   cudaStream_t s = s_;
   L_.reserve((size_t)KB * T);
-  for (DevBuf<int>* b : { &Lord_, &cntF_, &cntDT_, &cntB_ }) b->reserve(KB);
+  Lord_.reserve(KB);
+  cntAll_.reserve((size_t)3 * KB);
+  cntF_.p = cntAll_.p;
+  cntDT_.p = cntAll_.p + KB;
+  cntB_.p = cntAll_.p + 2 * (size_t)KB;
   if (!hst_) {
     hst_ = pinned_alloc(sizeof(TravState));
     hst_bytes_ = sizeof(TravState);
@@ -1770,8 +1793,8 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
     a.childlen, a.newbase, a.L, a.Lord, a.itF, a.itDT, a.itB, a.cntF, a.cntDT, a.cntB };
 
   CK(cudaMemsetAsync(L_.p, 0, sizeof(double) * KB * T, s));
-  for (DevBuf<int>* b : { &Lord_, &cntF_, &cntDT_, &cntB_ })
-    CK(cudaMemsetAsync(b->p, 0, sizeof(int) * KB, s));
+  CK(cudaMemsetAsync(Lord_.p, 0, sizeof(int) * KB, s));
+  CK(cudaMemsetAsync(cntAll_.p, 0, sizeof(int) * 3 * KB, s));
   hs->eps = cfg_.epsilon - exp_charge();  // the base case's reduced-precision exp is charged
   hs->ntot = (double)n_;
   hs->nslots = nb;
@@ -1787,7 +1810,7 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   hs->capB = capB_;
   CK(cudaMemcpyAsync(ds, hs, sizeof(TravState), cudaMemcpyHostToDevice, s));
   start_frontier(qt, &a);
-  k_trav_init<<<1, 256, 0, s>>>(a);
+  k_trav_init<<<32, 256, 0, s>>>(a);
   CK_LAUNCH();
   run_levels(&a, sig);
   k_trav_publish<<<1, 1, 0, s>>>(ds, bc_.p);
@@ -1798,21 +1821,24 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   trav_trace_ = a.trace != nullptr;
 
   // counting sort of the items by key (stable: level order, then emit order)
-  auto sort_items = [&](DevBuf<Item>& in, int cap, const int* dn, DevBuf<int>& cnt,
-                        DevBuf<int>& off, DevBuf<Item>& out) {
-    off.reserve((size_t)KB + 1);
-    size_t need = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need, cnt.p, off.p, (int)KB, s);
-    scan_tmp_.reserve(need + 256);
-    size_t have = scan_tmp_.cap;
-    cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, cnt.p, off.p, (int)KB, s);
-    out.reserve(cap);
-    k_scatter_dev<<<148 * 4, 256, 0, s>>>(in.p, dn, cap, off.p, out.p);
-    CK_LAUNCH();
-  };
-  sort_items(itF_, capF_, bc_.p + 8, cntF_, offF_, sF_);
-  sort_items(itDT_, capDT_, bc_.p + 9, cntDT_, offDT_, sDT_);
-  sort_items(itB_, capB_, bc_.p + 10, cntB_, offB_, sB_);
+  // all three kinds at once: one exclusive scan of the F | DT | B counts, then one kernel
+  // rebases each segment's offsets to 0 and scatters the items to (key offset + rank)
+  offAll_.reserve((size_t)3 * KB);
+  offLoc_.reserve((size_t)3 * KB + 1);
+  offF_.p = offLoc_.p;
+  offDT_.p = offLoc_.p + KB;
+  offB_.p = offLoc_.p + 2 * (size_t)KB;
+  size_t need = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, need, cntAll_.p, offAll_.p, 3 * (int)KB, s);
+  scan_tmp_.reserve(need + 256);
+  size_t have = scan_tmp_.cap;
+  cub::DeviceScan::ExclusiveSum(scan_tmp_.p, have, cntAll_.p, offAll_.p, 3 * (int)KB, s);
+  sF_.reserve(capF_);
+  sDT_.reserve(capDT_);
+  sB_.reserve(capB_);
+  k_sort_items3<<<148 * 4, 256, 0, s>>>(offAll_.p, (int)KB, bc_.p + 8, itF_.p, itDT_.p, itB_.p, capF_, capDT_,
+                                        capB_, offLoc_.p, sF_.p, sDT_.p, sB_.p);
+  CK_LAUNCH();
 }
 
 // After the batch's final synchronisation: statistics, and the traversal verdict
