@@ -136,6 +136,9 @@ __device__ int d_order_f2l(double ratio, double count, double tau, int pmax, int
   return 0;
 }
 
+#ifndef DFGTB_ORDER_LB
+#define DFGTB_ORDER_LB 1
+#endif
 // The three least-order searches of choose_best_method run interleaved, one candidate
 // order of each per step: the same arithmetic per search as d_order_ff / d_order_f2l
 // (identical orders), but three independent dependency chains instead of one three
@@ -149,6 +152,26 @@ __device__ __forceinline__ void orders3(double rF, double rD, double rT, double 
   const double thrF = doneF ? 0.0 : tau * d_ipow(1.0 - rF, dim);
   const double thrD = doneD ? 0.0 : tau * d_ipow(1.0 - rD, dim);
   const double thrT = doneT ? 0.0 : tau * d_ipow(1.0 - sT, 2 * dim);
+#if DFGTB_ORDER_LB
+  // Hopeless searches end before they start.  Every S(p) holds the term k = D - 1,
+  //   S(p) >= D a_p^(D-1) b_p,
+  // and over 1 <= p <= pmax: a_p >= a_1 (= 1 - r, resp. (1 - s)^2) and b_p >= b_pmax
+  // (r^p / sqrt(p!) falls with p; x (2 - x) grows with x = s^p), so with the threshold's
+  // own power of (1 - r) cancelled
+  //   count D b_pmax > tau (1 - r)        (F, D)    count D b_pmax > tau (1 - s)^2   (T)
+  // implies count S(p) > thr for every p: with the 1e-9 margin (roundings are ~1e-15)
+  // bound_ok's fast test returns false for each of them, i.e. order 0 -- the reference's
+  // decision.  Most pairs of a big level expand, and those ran all 3 pmax candidates.
+  {
+    const double cD = count * (double)dim * c_isf[pmax], tm = tau * (1.0 + 1e-9);
+    if (!doneF && thrF > 1e-290 && cD * d_ipow(rF, pmax) > tm * (1.0 - rF)) doneF = true;
+    if (!doneD && thrD > 1e-290 && cD * d_ipow(rD, pmax) > tm * (1.0 - rD)) doneD = true;
+    if (!doneT && thrT > 1e-290) {
+      const double x = d_ipow(sT, pmax);
+      if (cD * x * (2.0 - x) > tm * (1.0 - sT) * (1.0 - sT)) doneT = true;
+    }
+  }
+#endif
   double rpF = 1.0, rpD = 1.0, spT = 1.0;
   for (int p = 1; p <= pmax && !(doneF && doneD && doneT); ++p) {
     const double isf = c_isf[p], sf = c_sf[p];
