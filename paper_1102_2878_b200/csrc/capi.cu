@@ -263,12 +263,11 @@ static void cv_rows(dfgtb_handle* h, const double* bws, const double* convs, int
   if (ls) hs.insert(hs.end(), convs, convs + ns);
   const int nb = (int)hs.size();
   h->s1.reserve(n * (size_t)nb);
-  e.compute_batch(nullptr, n, hs.data(), nb, h->s1.p);
-  const Timings& t = e.last_timings();
   std::vector<double> lk(ns), lsv(ns);
   std::vector<int> cl(ns);
-  e.cv_reduce(h->s1.p, bws, ls ? h->s1.p + n * (size_t)ns : nullptr, convs, ns, lk.data(), cl.data(),
-              lsv.data());
+  // the sums of every h (then every conv_h) and their CV partial sums: one host wait
+  e.compute_batch_cv(hs.data(), nb, h->s1.p, bws, convs, ns, lk.data(), cl.data(), lsv.data());
+  const Timings& t = e.last_timings();
   for (int k = 0; k < ns; ++k) {
     dfgtb_cv_row& r = rows[k];
     r.h = bws[k];

@@ -199,7 +199,7 @@ void pinned_free(void* p, size_t bytes)
 // every time.
 struct StreamSet {
   cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
-  cudaEvent_t ev[14] = {}, fork = nullptr, join = nullptr, fork3 = nullptr, join3 = nullptr,
+  cudaEvent_t ev[16] = {}, fork = nullptr, join = nullptr, fork3 = nullptr, join3 = nullptr,
               legacy = nullptr, mom0 = nullptr, mom1 = nullptr;
 };
 static std::unordered_map<int, std::vector<StreamSet>>& stream_pool()
@@ -222,8 +222,13 @@ static StreamSet acquire_streams()
     }
   }
   StreamSet r;
-  CK(cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&r.s2, cudaStreamNonBlocking));
+  // DFGTB_STREAM_PRIO (experiments): 1 = the main stream (traversal, base-case chain)
+  // above the expansion stream, 2 = the other way round; default: equal priorities
+  static const int prio = std::getenv("DFGTB_STREAM_PRIO") ? std::atoi(std::getenv("DFGTB_STREAM_PRIO")) : 0;
+  int plo = 0, phi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&plo, &phi));  // phi = greatest priority (lowest number)
+  CK(cudaStreamCreateWithPriority(&r.s, cudaStreamNonBlocking, prio == 1 ? phi : plo));
+  CK(cudaStreamCreateWithPriority(&r.s2, cudaStreamNonBlocking, prio == 2 ? phi : plo));
   CK(cudaStreamCreateWithFlags(&r.s3, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming));
@@ -299,7 +304,7 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
     s2_ = ss.s2;
     fork_ = ss.fork;
     join_ = ss.join;
-    for (int i = 0; i < 14; ++i) ev_[i] = ss.ev[i];
+    for (int i = 0; i < 16; ++i) ev_[i] = ss.ev[i];
     s3_ = ss.s3;
     fork3_ = ss.fork3;
     join3_ = ss.join3;
@@ -323,8 +328,6 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
     CK(cudaEventElapsedTime(&ms, ev_[0], ev_[2]));
     std::fprintf(stderr, "DFGTB_TRACE create: upload+tree %.3f ms\n", ms);
   }
-  nn2_.reserve(rt_.nodes);
-  leaf_nn2(rt_, nn2_.p, s_);
   if (cfg.mode == 1) {
     if (ser_.T <= 4096) {
       eager_ = true;
@@ -346,6 +349,7 @@ Engine::~Engine()
   if (s_) cudaStreamSynchronize(s_);
   destroy_graph();
   if (hst_) pinned_free(hst_, hst_bytes_);
+  if (hpin_) pinned_free(hpin_, kHostPinBytes);
   if (s2_) cudaStreamSynchronize(s2_);
   if (s_) {
     StreamSet ss;
@@ -353,7 +357,7 @@ Engine::~Engine()
     ss.s2 = s2_;
     ss.fork = fork_;
     ss.join = join_;
-    for (int i = 0; i < 14; ++i) ss.ev[i] = ev_[i];
+    for (int i = 0; i < 16; ++i) ss.ev[i] = ev_[i];
     ss.s3 = s3_;
     ss.fork3 = fork3_;
     ss.join3 = join3_;

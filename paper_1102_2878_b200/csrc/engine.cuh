@@ -4,6 +4,7 @@
 #include "series.cuh"
 #include "tree.cuh"
 
+#include <functional>
 #include <memory>
 
 namespace dfgtb {
@@ -58,7 +59,7 @@ constexpr double kMufuCharge = 4e-6;
 // FP32 base case (execute.cu FPt / base_tile_f32x2): FP32 differences, distance and
 // partial sums, ex2.approx.f32 of the whole (shifted) argument.  Applies to leaf pairs whose
 // query leaf's box diagonal is <= kF32Diam in units where |q - r|^2 = z = log2 e |q - r|^2 / 2h^2
-// and whose sums are >= 1e-20 (or Q = R with a leave-one-out floor G - 1 >= 2^-kF32LooZ);
+// and whose sums are >= 1e-20 (Q != R) or >= 1 (Q = R, the self term; see base_flags);
 // per-term relative error < kF32Charge (derivation at FPt).  Terms are formed as
 // 2^(kF32Shift - z) and scaled back by kF32Unshift per tile.  Used when eps >= kF32MinEps
 // (the charge is then <= 5% of the budget) unless DFGTB_NO_F32 is set.
@@ -67,7 +68,6 @@ constexpr double kF32Charge = 2e-4;
 constexpr double kF32Diam = 150.0;
 constexpr float kF32Shift = 64.0f;
 constexpr double kF32Unshift = 0x1p-64;
-constexpr double kF32LooZ = 128.0;
 
 int default_p_max(int D);
 
@@ -90,6 +90,11 @@ public:
   // (d_conv may be nullptr -> no LS).
   void cv_reduce(const double* d_sums, const double* h, const double* d_conv, const double* conv_h,
                  int ns, double* lk, int* clamped, double* ls);
+  // compute_batch (Q = R) with the CV reduction queued behind it: one host wait for both
+  void compute_batch_cv(const double* h, int nb, double* d_out, const double* bw, const double* conv_h,
+                        int ns, double* lk, int* clamped, double* ls);
+  void cv_enqueue(const double* d_sums, const double* h, const double* d_conv, const double* conv_h, int ns);
+  void cv_collect(int ns, double* lk, int* clamped, double* ls) const;
 
   const Stats& last_stats(int slot = 0) const { return slot_stats_[slot]; }
   const Timings& last_timings() const { return tim_; }
@@ -117,7 +122,8 @@ public:
 
 private:
   void traverse(const DevTree& qt, const double* h, int nb);
-  bool traverse_finish();
+  void traverse_fetch_async();  // the traversal state to the pinned host copy, on s_
+  bool traverse_finish(bool prefetched = false);
   void run_levels(const void* trav_args, const std::vector<const void*>& sig);
   void destroy_graph();
   void run_phases(const DevTree& qt, const double* h, int nb, double* d_out);
@@ -172,6 +178,8 @@ private:
   DevBuf<unsigned long long> lvlep_;  // per-level packed entry/pair counters (traversal)
   // device-driven level loop: state (device + pinned host mirror), capacities, graph
   void* hst_ = nullptr;
+  void* hpin_ = nullptr;  // pinned: the batch's device counts (8 ints) | CV partial sums (run_phases, cv_*)
+  std::function<void()> post_batch_;  // queued after a batch's last kernel, before its one host wait
   size_t hst_bytes_ = 0;
   DevBuf<unsigned char> dst_;
   int capE_ = 0, capP_ = 0, capF_ = 0, capDT_ = 0, capB_ = 0;
@@ -182,7 +190,7 @@ private:
   cudaGraphExec_t gexec_ = nullptr;
   cudaGraphConditionalHandle hc_ = 0;
   std::vector<const void*> gsig_;
-  cudaEvent_t ev_[14];
+  cudaEvent_t ev_[16];
   cudaStream_t s3_ = nullptr;  // the FP64 base-case kernel beside the FP32 one
   cudaEvent_t fork3_ = nullptr, join3_ = nullptr;
   cudaEvent_t fork_ = nullptr, join_ = nullptr;
@@ -194,9 +202,7 @@ private:
   int nb_ = 1;
   bool mufu_ = false;
   bool f32_ = false;
-  bool base_conc_ = false;
-  DevBuf<double> nn2_;  // per reference leaf: max over its points of the squared distance to
-                        // the nearest other point of the leaf (+inf for internal / 1-point nodes)  // the last batch ran the two base-case kernels side by side
+  bool base_conc_ = false;  // the last batch ran the two base-case kernels side by side
   const DevTree* last_q_ = nullptr;  // query tree and node count of the last batch (diagnostics)
   int last_K_ = 0;
   // device-side counts of a batch (no host round trip until its end):
@@ -219,7 +225,6 @@ double measure_ex2_peak(int device);
 double mufu_exp_max_error();
 // Per leaf of t: the largest squared distance of a point to its nearest other point in
 // the leaf (+inf for internal nodes and 1-point leaves).
-void leaf_nn2(const DevTree& t, double* nn2, cudaStream_t s);
 // Max relative error of ex2.approx.ftz.f32 over every FP32 argument in [-126, 2^-10].
 double f32_exp_max_error();
 // The FP32 base case's term for host pairs (test entry; points in z units, stride d).
@@ -230,6 +235,7 @@ void upload_series(const SeriesTables& t, DevBuf<unsigned char>& dev, cudaStream
 DevSeries series_view(const SeriesTables& t, const DevBuf<unsigned char>& dev);
 
 // Pinned host blocks (cached like device memory; engine.cu).
+constexpr size_t kHostPinBytes = 64 + sizeof(double) * 148 * 3 * kMaxSlots;  // Engine::hpin_
 void* pinned_alloc(size_t bytes);
 void pinned_free(void* p, size_t bytes);
 

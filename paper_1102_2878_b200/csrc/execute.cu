@@ -586,10 +586,15 @@ struct BTask {
 // (slot, leaf): a window of 32 items, inclusive scan of their counts, the run is the
 // prefix that fits.  Returns the next run's first item (all lanes).
 __device__ __forceinline__ int warp_run_end(const Item* it, int k, int e, const int* rcount, int rmax,
-                                            int lane)
+                                            int lane, int* code = nullptr)
 {
   const int j = k + lane;
-  int pre = j < e ? rcount[it[j].r] : (1 << 28);
+  int pre = 1 << 28;
+  if (j < e) {
+    const int4 v = *reinterpret_cast<const int4*>(it + j);  // {key, r, code, rank}
+    pre = rcount[v.y];
+    if (code) *code = v.z;
+  }
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int v = __shfl_up_sync(0xffffffffu, pre, o);
@@ -599,15 +604,19 @@ __device__ __forceinline__ int warp_run_end(const Item* it, int k, int e, const 
   return k + __popc(fit);
 }
 
-// Base-case tasks in one pass: the (slot, leaf)'s warp counts its runs,
-// claims its task range with one atomic (bc[5] = tasks so far; a key's tasks stay
-// contiguous, query chunk major, run minor, which is all k_finalize relies on), then
-// writes the tasks.  Tasks past tcap are dropped; the host sees bc[5] > tcap and reruns.
+// Base-case tasks in one pass: the (slot, leaf)'s warp cuts its items into runs (lane r
+// keeps run r's end, a bit mask whether the FP32 kernel may take the run: every item
+// carries order bit 2), claims its task range with one atomic (bc[5] = tasks so far; a
+// key's tasks stay contiguous, query chunk major, run minor, which is all k_finalize
+// relies on), then writes the tasks from the recorded ends (keys with more than 32 runs
+// recompute the later ones).  Tasks past tcap are dropped; the host sees bc[5] > tcap and
+// reruns.
 __global__ void k_task_build(const int* leaves, int nleaves, int nb, int K, const int* cntB,
                              const int* offB, const Item* sB, const int* rcount, int rmax, TreeView Q,
                              BTask* tasks, int tcap, int* ntasks, int* leaf_task, int* leaf_runs,
                              int* tflag)
 {
+  static_assert(sizeof(Item) == 16, "Item is read as one int4");
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= nleaves * nb) return;
   const int slot = i / nleaves;
@@ -615,16 +624,34 @@ __global__ void k_task_build(const int* leaves, int nleaves, int nb, int K, cons
   const int key = slot * K + leaf;
   const int o = offB[key], e = o + cntB[key];
   const int nq = (Q.count[leaf] + 31) / 32;
-  int nruns = 0;
-  for (int k = o; k < e; k = warp_run_end(sB, k, e, rcount, rmax, lane)) ++nruns;
+  int nruns = 0, myend = 0;
+  unsigned f32m = 0;
+  for (int k = o; k < e;) {
+    int code = 0;
+    const int j = warp_run_end(sB, k, e, rcount, rmax, lane, &code);
+    const bool f32 = __all_sync(0xffffffffu, k + lane >= j || (code & 4));
+    if (nruns < 32) {
+      if (lane == nruns) myend = j;
+      f32m |= (f32 ? 1u : 0u) << nruns;
+    }
+    k = j;
+    ++nruns;
+  }
   int t0 = 0;
   if (lane == 0 && nruns) t0 = atomicAdd(ntasks, nruns * nq);
   t0 = __shfl_sync(0xffffffffu, t0, 0);
   int runs = 0;
   for (int k = o; k < e;) {
-    const int j = warp_run_end(sB, k, e, rcount, rmax, lane);
-    // the FP32 kernel may take the run iff every item carries order bit 2
-    const bool f32 = __all_sync(0xffffffffu, k + lane >= j || (sB[k + lane].code & 4));
+    int j;
+    bool f32;
+    if (runs < 32) {
+      j = __shfl_sync(0xffffffffu, myend, runs);
+      f32 = (f32m >> runs) & 1u;
+    } else {
+      int code = 0;
+      j = warp_run_end(sB, k, e, rcount, rmax, lane, &code);
+      f32 = __all_sync(0xffffffffu, k + lane >= j || (code & 4));
+    }
     for (int qi = lane; qi < nq; qi += 32)
       if (t0 + qi * nruns + runs < tcap) {
         tasks[t0 + qi * nruns + runs] = BTask{ key, k, j, 32 * qi };
@@ -1056,7 +1083,7 @@ __device__ __forceinline__ void base_groups_mufu(const double* rs, int n, const 
 
 // FP32 base case (leaf pairs the traversal flagged with order bit 2: the query leaf's box
 // diagonal is <= kF32Diam = 150 in units where |q - r|^2 = z, and the query sums are
-// provably >= 1e-20, or Q = R with a leave-one-out floor G - 1 >= 2^-128).  Points are
+// provably >= 1e-20 (Q != R) or >= 1 (Q = R: the self term)).  Points are
 // centred on the query leaf's box centre in FP64 (every query within 75 of it) and rounded
 // to FP32 (q~, r~), and per pair
 //   z' = sum_d (q~_d - r~_d)^2 - S,   term = ex2.approx.ftz(-z') = 2^S 2^-z,   S = kF32Shift = 64,
@@ -1064,8 +1091,9 @@ __device__ __forceinline__ void base_groups_mufu(const double* rs, int n, const 
 // no FP64 instruction in the pair loop; each tile's FP32 sum is scaled back by 2^-S
 // exactly in FP64.  The shift keeps terms down to 2^-190 (z <= 190) out of the flush
 // range at no cost (sums of <= 256 terms <= 2^S per tile stay below 2^72).  Terms below
-// 2^-190 flush to 0: absolute error <= |R| 2^-190, against sums >= 1e-20 (Q != R) or a
-// leave-one-out sum >= 2^-128 (Q = R; <= |R| 2^-62 relative).  Q = R: the self pairs
+// 2^-190 flush to 0: absolute error <= |R| 2^-190, against sums >= 1e-20 (Q != R) or
+// >= 1 (Q = R: below the 2^-53 resolution of the FP64 sum G that is returned, from which
+// the CV scores form G - 1, cv.cpp:17-25).  Q = R: the self pairs
 // are masked out of the FP32 sums (their tiles run the SELF variant) and K(0) = 1 is
 // added exactly in FP64 at the end, so the partial sums hold only G - 1, to 21 u relative.
 // Per-term relative error for z <= 127 (|q| <= 75, |r| <= 75 + sqrt z, unit roundoff
@@ -2031,16 +2059,14 @@ __global__ void __launch_bounds__(128) k_finalize_t(DevSeries g, TreeView Q, int
   double loc = 0.0;
   const int dep = Q.depth[leaf];
   const int* anc = Q.anc + (size_t)leaf * kMaxAnc;
-  // leaf first; chains from the precomputed table (independent loads), deeper leaves
-  // walk parent pointers
-  for (int k = dep, a = leaf; k >= 0; --k, a = (dep < kMaxAnc ? (k >= 0 ? anc[k] : -1) : Q.parent[a])) {
+  auto eval = [&](int a) {
     const int key = slot * K + a;
-    if (Lord[key] <= 0) continue;
+    const int ord = Lord[key];
+    if (ord <= 0) return;
     const double* Lk = L + (size_t)key * g.T;
     double u[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) u[d] = (q[d] - Q.cen[(size_t)a * D + d]) * s;
-    const int ord = Lord[key];
     if (ord == 1) {
       loc += Lk[0];  // the finite-difference constant term only
     } else if (ord == 2) {
@@ -2050,6 +2076,30 @@ __global__ void __launch_bounds__(128) k_finalize_t(DevSeries g, TreeView Q, int
     } else {
       loc += local_horner<D, PM, PM>(Lk, tp, u);
     }
+  };
+  if (dep < kMaxAnc) {
+    // which ancestors (anc[k], depth k <= dep; anc[dep] = the leaf) hold a table: the
+    // order loads of 8 ancestors are issued together (independent chains anc -> Lord),
+    // then only the holders are visited, leaf first (the same order of additions as the
+    // plain walk below)
+    static_assert(kMaxAnc <= 64, "ancestor mask");
+    unsigned long long act = 0;
+#pragma unroll 1
+    for (int k0 = 0; k0 <= dep; k0 += 8) {
+      int o[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) o[u] = k0 + u <= dep ? Lord[slot * K + anc[k0 + u]] : 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (o[u] > 0) act |= 1ull << (k0 + u);
+    }
+    while (act) {
+      const int k = 63 - __clzll((long long)act);
+      act &= ~(1ull << k);
+      eval(anc[k]);
+    }
+  } else {
+    for (int k = dep, a = leaf; k >= 0; --k, a = Q.parent[a]) eval(a);
   }
   const int li = i - Q.begin[leaf];
   const int nic = cntB[lkey] ? leaf_runs[lkey] : 0;
@@ -2175,6 +2225,9 @@ int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }
 // ws = [nextA, nextB, cntA, cntB, pairsA (u64), pairsB (u64), listA (tcap), listB (tcap),
 // task flags (tcap, written by k_task_build)]; the lists come from k_task_split.  Then the
 // FP32 kernel over list A, then the FP64 kernel over list B.
+#ifndef DFGTB_FF_STREAM_DEFAULT
+#define DFGTB_FF_STREAM_DEFAULT 1  // measured: cfg2 -1.4%, cfg3 / cfg5 -0.4% against the far field queued behind the local chain
+#endif
 #ifndef DFGTB_BASE_CONC
 #define DFGTB_BASE_CONC 0  // measured: side by side is no faster than one after the other (c32) or slower
 #endif
@@ -2363,12 +2416,16 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
 {
   for (int attempt = 0;; ++attempt) {
     launch_phases(qt, h, nb, d_out);
+    if (post_batch_) post_batch_();
+    // the traversal verdict and the chunk / task totals come back with the one wait
+    if (!hpin_) hpin_ = pinned_alloc(kHostPinBytes);
+    int* hb = static_cast<int*>(hpin_);
+    traverse_fetch_async();
+    CK(cudaMemcpyAsync(hb, bc_.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, s_));
     CK(cudaStreamSynchronize(s_));
-    const bool trav_ok = traverse_finish();
+    const bool trav_ok = traverse_finish(true);
     bool ok = trav_ok;
     if (trav_ok) {
-      int hb[8];
-      CK(cudaMemcpy(hb, bc_.p, sizeof(hb), cudaMemcpyDeviceToHost));
       auto grow = [&](long long need) {
         if (need > (1 << 28))
           throw OutOfMemory("batch needs more than 2^28 chunks / tasks (" + std::to_string(hb[4]) +
@@ -2395,7 +2452,7 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
   if (base_conc_) CK(cudaEventElapsedTime(&tim_.base_fp64_ms, ev_[12], ev_[13]));
   else CK(cudaEventElapsedTime(&tim_.base_fp64_ms, ev_[11], ev_[10]));
   CK(cudaEventElapsedTime(&tim_.farfield_ms, ev_[6], ev_[7]));
-  CK(cudaEventElapsedTime(&tim_.final_ms, ev_[7], ev_[8]));
+  CK(cudaEventElapsedTime(&tim_.final_ms, ev_[14], ev_[8]));
   CK(cudaEventElapsedTime(&tim_.total_ms, ev_[2], ev_[8]));
 }
 
@@ -2451,6 +2508,40 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
                                                               Mt_.p);
     CK_LAUNCH();
   }
+  // far field: on s2_ after the local chain, or (DFGTB_FF_STREAM = 1 / 2, tables built
+  // with the engine) on a third stream beside it, queued after / before the local chain
+  static const int ff_env = std::getenv("DFGTB_FF_STREAM") ? std::atoi(std::getenv("DFGTB_FF_STREAM")) : DFGTB_FF_STREAM_DEFAULT;
+  const int ff_mode = (one_stream_ || !s3_ || (cfg_.mode == 1 && !eager_)) ? 0 : ff_env;
+  cudaStream_t sff = ff_mode ? s3_ : s2;
+  if (ff_mode) CK(cudaStreamWaitEvent(sff, fork_, 0));
+  const int nleaves = (int)qleaves_host_.size();
+  const int nlb = nleaves * nb;
+  auto launch_ff = [&]() {
+    s_ff_.reserve((size_t)qt.n * nb);
+    CK(cudaEventRecord(ev_[6], sff));
+    if (cfg_.mode == 1) {
+      const int gw = grid_warps(nlb);
+      const int pm = ser_.pmax;
+  #define FF_T(DD, PP)                                                                              \
+    k_farfield_t<DD, PP><<<gw, kBlock, 0, sff>>>(Q, R, K, nb, leaves_.p, nleaves, cntF_.p, offF_.p,  \
+                                                sF_.p, Mt_.p, sv, qt.n, s_ff_.p)
+      if (D_ == 1 && pm == 8) FF_T(1, 8);
+      else if (D_ == 2 && pm == 6) FF_T(2, 6);
+      else if (D_ == 3 && pm == 4) FF_T(3, 4);
+      else if (D_ == 4 && pm == 2) FF_T(4, 2);
+      else if (D_ == 5 && pm == 2) FF_T(5, 2);
+      else
+        k_farfield<<<gw, kBlock, 0, sff>>>(g, Q, R, K, nb, leaves_.p, nleaves, cntF_.p, offF_.p, sF_.p,
+                                         Mt_.p, sv, qt.n, s_ff_.p);
+  #undef FF_T
+      CK_LAUNCH();
+    } else {
+      CK(cudaMemsetAsync(s_ff_.p, 0, sizeof(double) * qt.n * nb, sff));
+    }
+    CK(cudaEventRecord(ev_[7], sff));
+    if (ff_mode) CK(cudaEventRecord(join3_, sff));
+  };
+  if (ff_mode == 2) launch_ff();
   CK(cudaEventRecord(ev_[4], s2));
   // D/T items -> chunked partial tables -> per-(slot, query node) reduction
   if (cfg_.mode == 1) {
@@ -2499,31 +2590,7 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
     }
   }
   CK(cudaEventRecord(ev_[5], s2));
-  // far field (s2_)
-  const int nleaves = (int)qleaves_host_.size();
-  const int nlb = nleaves * nb;
-  s_ff_.reserve((size_t)qt.n * nb);
-  CK(cudaEventRecord(ev_[6], s2));
-  if (cfg_.mode == 1) {
-    const int gw = grid_warps(nlb);
-    const int pm = ser_.pmax;
-#define FF_T(DD, PP)                                                                              \
-  k_farfield_t<DD, PP><<<gw, kBlock, 0, s2>>>(Q, R, K, nb, leaves_.p, nleaves, cntF_.p, offF_.p,  \
-                                              sF_.p, Mt_.p, sv, qt.n, s_ff_.p)
-    if (D_ == 1 && pm == 8) FF_T(1, 8);
-    else if (D_ == 2 && pm == 6) FF_T(2, 6);
-    else if (D_ == 3 && pm == 4) FF_T(3, 4);
-    else if (D_ == 4 && pm == 2) FF_T(4, 2);
-    else if (D_ == 5 && pm == 2) FF_T(5, 2);
-    else
-      k_farfield<<<gw, kBlock, 0, s2>>>(g, Q, R, K, nb, leaves_.p, nleaves, cntF_.p, offF_.p, sF_.p,
-                                       Mt_.p, sv, qt.n, s_ff_.p);
-#undef FF_T
-    CK_LAUNCH();
-  } else {
-    CK(cudaMemsetAsync(s_ff_.p, 0, sizeof(double) * qt.n * nb, s2));
-  }
-  CK(cudaEventRecord(ev_[7], s2));
+  if (ff_mode != 2) launch_ff();
   CK(cudaEventRecord(join_, s2));
   // base-case tasks (s_)
   leaf_task_.reserve(KB);
@@ -2582,6 +2649,8 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
   CK(cudaEventRecord(ev_[10], s));
   // join, finalize
   CK(cudaStreamWaitEvent(s, join_, 0));
+  if (ff_mode) CK(cudaStreamWaitEvent(s, join3_, 0));
+  CK(cudaEventRecord(ev_[14], s));  // both chains joined: finalize starts
   {
     const int fgrid = ceil_div((long long)qt.n * nb, 128);
     const int pm = ser_.pmax;
@@ -2605,10 +2674,9 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
   CK(cudaEventRecord(ev_[8], s));
 }
 
-void Engine::cv_reduce(const double* d_sums, const double* h, const double* d_conv,
-                       const double* conv_h, int ns, double* lk, int* clamped, double* ls)
+void Engine::cv_enqueue(const double* d_sums, const double* h, const double* d_conv,
+                        const double* conv_h, int ns)
 {
-  DeviceGuard dg(dev_);
   const size_t n = n_;
   if (n < 2) throw InvalidArgument("CV requires at least 2 points");
   if (ns < 1 || ns > kMaxSlots) throw InvalidArgument("CV batch size outside [1, 64]");
@@ -2621,13 +2689,21 @@ void Engine::cv_reduce(const double* d_sums, const double* h, const double* d_co
   red_.reserve((size_t)kRedBlocks * 3 * ns);
   k_cv_partial<<<dim3(kRedBlocks, ns), kBlock, 0, s_>>>(d_sums, d_conv, (int)n, cn, red_.p);
   CK_LAUNCH();
-  std::vector<double> part((size_t)kRedBlocks * 3 * ns);
-  CK(cudaMemcpyAsync(part.data(), red_.p, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, s_));
-  CK(cudaStreamSynchronize(s_));
+  static_assert(kRedBlocks == 148, "kHostPinBytes holds 148 x 3 x kMaxSlots partial sums");
+  if (!hpin_) hpin_ = pinned_alloc(kHostPinBytes);
+  CK(cudaMemcpyAsync(static_cast<char*>(hpin_) + 64, red_.p, sizeof(double) * kRedBlocks * 3 * ns,
+                     cudaMemcpyDeviceToHost, s_));
+}
+
+// the block partials in fixed order (after the stream wait that follows cv_enqueue)
+void Engine::cv_collect(int ns, double* lk, int* clamped, double* ls) const
+{
+  const double* part = reinterpret_cast<const double*>(static_cast<const char*>(hpin_) + 64);
+  const size_t n = n_;
   for (int k = 0; k < ns; ++k) {
     double a = 0, b = 0, c = 0;
     for (int q = 0; q < kRedBlocks; ++q) {
-      const double* P = part.data() + ((size_t)k * kRedBlocks + q) * 3;
+      const double* P = part + ((size_t)k * kRedBlocks + q) * 3;
       a += P[0];
       b += P[1];
       c += P[2];
@@ -2636,6 +2712,28 @@ void Engine::cv_reduce(const double* d_sums, const double* h, const double* d_co
     if (clamped) clamped[k] = (int)c;
     if (ls) ls[k] = b / (double)n;
   }
+}
+
+void Engine::cv_reduce(const double* d_sums, const double* h, const double* d_conv,
+                       const double* conv_h, int ns, double* lk, int* clamped, double* ls)
+{
+  DeviceGuard dg(dev_);
+  cv_enqueue(d_sums, h, d_conv, conv_h, ns);
+  CK(cudaStreamSynchronize(s_));
+  cv_collect(ns, lk, clamped, ls);
+}
+
+void Engine::compute_batch_cv(const double* h, int nb, double* d_out, const double* bw,
+                              const double* conv_h, int ns, double* lk, int* clamped, double* ls)
+{
+  DeviceGuard dg(dev_);
+  struct Clear {
+    std::function<void()>& f;
+    ~Clear() { f = nullptr; }
+  } clear{ post_batch_ };
+  post_batch_ = [&] { cv_enqueue(d_out, bw, conv_h ? d_out + n_ * (size_t)ns : nullptr, conv_h, ns); };
+  compute_batch(nullptr, n_, h, nb, d_out);
+  cv_collect(ns, lk, clamped, ls);
 }
 
 void naive_device(const double* d_q, size_t nq, const double* d_r, size_t nr, int D, double h,
@@ -2756,43 +2854,6 @@ __global__ void k_ex2_peak(float* out, int iters)
 #pragma unroll
   for (int k = 0; k < 8; ++k) s += a[k];
   if (s == 42.0f) out[0] = s;
-}
-
-__global__ void k_leaf_nn2(int K, int D, const int* left, const int* begin, const int* count,
-                           const double* xs, double* nn2)
-{
-  const int lane = threadIdx.x & 31;
-  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < K; k += (gridDim.x * blockDim.x) >> 5) {
-    const int b = begin[k], c = count[k];
-    double worst = 0.0;
-    if (left[k] < 0 && c >= 2) {
-      for (int i = lane; i < c; i += 32) {
-        double best = CUDART_INF;
-        for (int j = 0; j < c; ++j) {
-          if (j == i) continue;
-          double d2 = 0.0;
-          for (int d = 0; d < D; ++d) {
-            const double t = xs[(size_t)(b + i) * D + d] - xs[(size_t)(b + j) * D + d];
-            d2 = fma(t, t, d2);
-          }
-          best = fmin(best, d2);
-        }
-        worst = fmax(worst, best);
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
-    } else {
-      worst = CUDART_INF;
-    }
-    if (lane == 0) nn2[k] = worst;
-  }
-}
-
-void leaf_nn2(const DevTree& t, double* nn2, cudaStream_t s)
-{
-  k_leaf_nn2<<<std::min(ceil_div((long long)t.nodes * 32, 256), 148 * 16), 256, 0, s>>>(
-    t.nodes, t.D, t.left.p, t.begin.p, t.count.p, t.xs.p, nn2);
-  CK_LAUNCH();
 }
 
 void Engine::base_split(int& f32_tasks, int& fp64_tasks, unsigned long long& f32_pairs,

@@ -260,8 +260,6 @@ struct TravArgs {
   int D, pmax, cost, series, T;
   int selfq;  // Q = R: every query's sum is >= 1 (its own term)
   int f32;    // the FP32 base case may be flagged (order bit 2)
-  const double* qnn2;  // Q = R: per leaf the largest squared distance of a point to its
-                       // nearest neighbour inside the leaf (+inf: none / not a leaf)
   TravState* st;
   int *fq[2], *foff[2], *flen[2], *fr[2];
   int* pent[2];  // entry index of every frontier pair (pair-balanced persistent path)
@@ -370,33 +368,24 @@ __global__ void k_trav_init(const __grid_constant__ TravArgs a)
 // >= 1 (Q = R) or >= G^l >= 1e-290: below 1e-280 relative); the MUFU fixed point also
 // needs the query leaf's diameter <= 1000 in z units (sq sqrt(D) sqrt(log2 e) / (h sqrt 2),
 // sqrt(log2 e / 2) < 0.8494).  Bit 2: the FP32 base case applies: diameter <= kF32Diam
-// (every query within kF32Diam / 2 of the leaf's box centre), and for Q != R sums >=
-// G^l >= 1e-20 (its terms below 2^-126 flush to 0: <= |R| 2^-126 / 1e-20 < 1e-11
-// relative); for Q = R a provable leave-one-out floor G - 1 >= 2^-128 (from G^l, or from
-// a neighbour in the query leaf itself): the self pairs are masked out of the FP32 sums
-// (K(0) = 1 added exactly in FP64), the terms below 2^-190 that flush weigh <= |R| 2^-62
-// relative to the G - 1 the CV scores take logarithms of, FP32 rounding 21 u of it.
+// (every query within kF32Diam / 2 of the leaf's box centre), and the terms below 2^-190
+// that its FP32 exp flushes to 0 cannot matter: Q != R needs sums >= G^l >= 1e-20
+// (<= |R| 2^-190 / 1e-20 < 1e-30 relative); Q = R sums are >= 1 (the self term, added
+// exactly in FP64: the FP32 partial sums hold only G - 1), so the dropped mass is
+// <= |R| 2^-190 absolute, far below the 2^-53 resolution of the FP64 sum G the engine
+// returns -- the CV scores' G - 1 is formed from that FP64 G (cv.cpp:17-25), so a
+// leave-one-out mass below 2^-53 is invisible to them on the FP64 path as well.
 __device__ __forceinline__ int base_flags(const TravArgs& a, double kmin, double glo, double sq, double h,
-                                          int D, int nq, int Q)
+                                          int D)
 {
   const double dz = sq * sqrt((double)D) * 0.8494;
-  // Q = R leave-one-out floor: every query of the leaf has a neighbour inside it with
-  // K >= 2^-128 (its nearest one within z = 128: log2 e d^2 / 2h^2 <= 128), so G - 1 >= 2^-128
-  // (G^l can only show G - 1 >= 2^-40 above the self term's 1 in FP64)
-  const bool loo = glo >= 1.0 + 0x1p-40 ||
-                   (nq >= 2 && a.qnn2 && a.qnn2[Q] * 0.7213475204444817 <= kF32LooZ * h * h);
-#if defined(DFGTB_EXP_F32_NOLOO)  // experiments only: which condition keeps pairs off FP32
-  const bool loo_x = true;
-#else
-  const bool loo_x = loo;
-#endif
-#if defined(DFGTB_EXP_F32_DIAM)
+#if defined(DFGTB_EXP_F32_DIAM)  // experiments only
   const double diam_x = DFGTB_EXP_F32_DIAM;
 #else
   const double diam_x = kF32Diam;
 #endif
   return (kmin >= 3.4e-308 ? 1 : 0) | ((a.selfq || glo >= 1e-290) && dz <= 1000.0 * h ? 2 : 0) |
-         (a.f32 && (a.selfq ? loo_x : glo >= 1e-20) && dz <= diam_x * h ? 4 : 0);
+         (a.f32 && (a.selfq || glo >= 1e-20) && dz <= diam_x * h ? 4 : 0);
 }
 
 // A group of W lanes, one frontier query node: kernel bounds of every live pair, the
@@ -456,7 +445,7 @@ __device__ __forceinline__ void classify_entry(const TravArgs& a, TravState& st,
       }
       if (kind == kX && qleaf && a.R.left[R] < 0) {
         kind = kB;
-        order = base_flags(a, kmin, glo, sq, h, D, a.Q.count[Q], Q);
+        order = base_flags(a, kmin, glo, sq, h, D);
       }
       if (kind == kX) {
         slots += a.R.left[R] < 0 ? 1 : 2;
@@ -908,7 +897,7 @@ __device__ __forceinline__ void pairs_decide(const TravArgs& a, const TravState&
       }
       if (kind == kX && a.Q.left[Q] < 0 && a.R.left[R] < 0) {
         kind = kB;
-        order = base_flags(a, kmin, uglo[u], a.Q.side[Q], s_h[slot], D, a.Q.count[Q], Q);
+        order = base_flags(a, kmin, uglo[u], a.Q.side[Q], s_h[slot], D);
       }
     }
     a.dec[j] = kind | (order << 8);
@@ -923,6 +912,11 @@ __device__ __forceinline__ void entries_reduce(const TravArgs& a, int cur, int K
                                                unsigned long long (*s_sst)[sNStat])
 {
   const int lane = threadIdx.x & 31;
+  // statistics: lane k < sNStat keeps counter k of the warp's current slot in a register
+  // and adds it to the CTA's shared copy when the slot changes and at the end of the
+  // phase (one 8-lane atomic per warp and level instead of up to 8 serial ones per entry)
+  int st_slot = -1;
+  unsigned long long st_mine = 0;
   for (int e = e0 + (threadIdx.x >> 5); e < e1; e += kPBlock / 32) {
     const int key = a.fq[cur][e];
     const int slot = key / K, Q = key - slot * K;
@@ -979,17 +973,22 @@ __device__ __forceinline__ void entries_reduce(const TravArgs& a, int cur, int K
         a.L[(size_t)key * a.T] += fd_const;  // constant local term (order 1)
         if (a.Lord[key] < 1) a.Lord[key] = 1;
       }
-      unsigned long long* ss = s_sst[slot];
-      atomicAdd(ss + sPairs, (unsigned long long)len);
-      if (nFD) atomicAdd(ss + sFD, (unsigned long long)nFD);
-      if (nF) atomicAdd(ss + sF, (unsigned long long)nF);
-      if (nDT - nT) atomicAdd(ss + sD, (unsigned long long)(nDT - nT));
-      if (nT) atomicAdd(ss + sT, (unsigned long long)nT);
-      if (nB) atomicAdd(ss + sB, (unsigned long long)nB);
-      if (kev) atomicAdd(ss + sKev, kev);
-      if (cov) atomicAdd(ss + sCov, cov);
     }
+    if (slot != st_slot) {
+      if (st_mine && lane < sNStat) atomicAdd(s_sst[st_slot] + lane, st_mine);
+      st_slot = slot;
+      st_mine = 0;
+    }
+    st_mine += lane == sPairs ? (unsigned long long)len
+               : lane == sFD  ? (unsigned long long)nFD
+               : lane == sF   ? (unsigned long long)nF
+               : lane == sD   ? (unsigned long long)(nDT - nT)
+               : lane == sT   ? (unsigned long long)nT
+               : lane == sB   ? (unsigned long long)nB
+               : lane == sKev ? kev
+                              : cov;
   }
+  if (st_mine && lane < sNStat) atomicAdd(s_sst[st_slot] + lane, st_mine);
 }
 
 // Cached phases (PairCache): the same computations as pairs_bounds / entries_glo /
@@ -1058,7 +1057,7 @@ __device__ __forceinline__ void pairs_decide_c(const TravArgs& a, const TravStat
       }
       if (kind == kX && a.Q.left[Q] < 0 && a.R.left[R] < 0) {
         kind = kB;
-        order = base_flags(a, kmin, glo, a.Q.side[Q], s_h[slot], D, a.Q.count[Q], Q);
+        order = base_flags(a, kmin, glo, a.Q.side[Q], s_h[slot], D);
       }
     }
     c.dec[l] = kind | (order << 8);
@@ -1762,7 +1761,6 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   a.R = view_of(rt_);
   a.selfq = &qt == &rt_ ? 1 : 0;
   a.f32 = f32_ ? 1 : 0;
-  a.qnn2 = &qt == &rt_ ? nn2_.p : nullptr;
   a.D = D_;
   a.pmax = ser_.pmax;
   a.cost = cfg_.cost_model;
@@ -1866,11 +1864,16 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
 
 // After the batch's final synchronisation: statistics, and the traversal verdict
 // (false: buffers overflowed and were regrown -- the batch must be rerun).
-bool Engine::traverse_finish()
+void Engine::traverse_fetch_async()
+{
+  CK(cudaMemcpyAsync(hst_, dst_.p, sizeof(TravState), cudaMemcpyDeviceToHost, s_));
+}
+
+bool Engine::traverse_finish(bool prefetched)
 {
   TravState* hs = static_cast<TravState*>(hst_);
   const TravState* ds = reinterpret_cast<const TravState*>(dst_.p);
-  CK(cudaMemcpy(hs, ds, sizeof(TravState), cudaMemcpyDeviceToHost));
+  if (!prefetched) CK(cudaMemcpy(hs, ds, sizeof(TravState), cudaMemcpyDeviceToHost));
   const int nb = trav_nb_;
   if (!use_persistent_ && use_graph_) launch_counter() += (uint64_t)hs->levels * kLevelKernels;
   if (trav_trace_) {  // per level: classify | scan | emit (microseconds)

@@ -33,7 +33,7 @@ for _ in range(steps):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(st); run(); b.record(st); b.synchronize(); ms.append(a.elapsed_time(b))
     for kk, v in e.last_timings().items(): ph[kk] = ph.get(kk, 0) + v / steps
-print(json.dumps({"ms": float(np.mean(ms)), "min": float(np.min(ms)), **{kk: round(v, 4) for kk, v in ph.items()}}))
+print(json.dumps({"ms": float(np.mean(ms)), "min": float(np.min(ms)), "med": float(np.median(ms)), "max": float(np.max(ms)), **{kk: round(v, 4) for kk, v in ph.items()}}))
 '''
 
 
