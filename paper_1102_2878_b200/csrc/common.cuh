@@ -51,6 +51,9 @@ uint64_t& launch_counter();
 // buffer freed while another device is current returns to its own device's pool.
 void* cache_alloc(size_t bytes);
 void cache_free(void* p, size_t bytes, int device);
+// pinned host blocks, pooled like device memory (engine.cu)
+void* pinned_alloc(size_t bytes);
+void pinned_free(void* p, size_t bytes);
 void cache_release_all();
 // Guard mode (DFGTB_GUARD set when the library first allocates): every device block gets a
 // kGuardBytes band past its end filled with kGuardByte; guard_check() synchronises and

@@ -2405,8 +2405,8 @@ void Engine::setup_leaves(const DevTree& t)
   CK(cudaMemcpyAsync(leaves_.p, qleaves_host_.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, s_));
   leaf_of_pos_.reserve(t.n);
   k_leaf_of_pos<<<nl, 64, 0, s_>>>(leaves_.p, nl, t.begin.p, t.count.p, leaf_of_pos_.p);
-  CK_LAUNCH();
-  CK(cudaStreamSynchronize(s_));
+  CK_LAUNCH();  // ordered on s_ before the batch that follows (qleaves_host_ is a member: the
+                // upload's source outlives the call)
 }
 
 // One batch: every launch is queued without a host round trip (counts live in bc_);

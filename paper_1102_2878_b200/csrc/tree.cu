@@ -23,6 +23,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <numeric>
@@ -1206,15 +1207,37 @@ static bool build_tree_persistent(DevTree& t, const double* d_x, int n, int D, i
       std::fprintf(stderr, "\n");
     }
   }
-  int K = 0;
-  CK(cudaMemcpyAsync(&K, kcount.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  // Node count and node arrays back in ONE round trip when the count fits the guess (the
+  // last tree's count plus a margin, per process): a pinned block of the count and the
+  // first `guess` entries of the four arrays; the remainder is fetched only on a miss.
+  static std::atomic<int> last_K{ 0 };
+  const int guess = std::min(maxK, std::max(1024, last_K.load() + last_K.load() / 8 + 64));
+  size_t pin_cap = 4096;  // block sizes in powers of two: the pinned pool reuses them across trees
+  while (pin_cap < (size_t)guess) pin_cap *= 2;
+  const size_t pin_bytes = sizeof(int) * (4 * pin_cap + 16);
+  int* pin = static_cast<int*>(pinned_alloc(pin_bytes));
+  struct PinFree {
+    int* p;
+    size_t b;
+    ~PinFree() { pinned_free(p, b); }
+  } pin_free{ pin, pin_bytes };
+  CK(cudaMemcpyAsync(pin, kcount.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  const int* d_arr[4] = { nleft.p, nright.p, nbeg.p, ncnt.p };
+  for (int k = 0; k < 4; ++k)
+    CK(cudaMemcpyAsync(pin + 16 + (size_t)k * guess, d_arr[k], sizeof(int) * guess, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  const int K = pin[0];
+  last_K.store(K);
   std::vector<int> h_left(K), h_right(K), h_beg(K), h_cnt(K);
-  CK(cudaMemcpyAsync(h_left.data(), nleft.p, sizeof(int) * K, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(h_right.data(), nright.p, sizeof(int) * K, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(h_beg.data(), nbeg.p, sizeof(int) * K, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(h_cnt.data(), ncnt.p, sizeof(int) * K, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  std::vector<int>* h_arr[4] = { &h_left, &h_right, &h_beg, &h_cnt };
+  for (int k = 0; k < 4; ++k)
+    std::copy(pin + 16 + (size_t)k * guess, pin + 16 + (size_t)k * guess + std::min(K, guess), h_arr[k]->begin());
+  if (K > guess) {
+    for (int k = 0; k < 4; ++k)
+      CK(cudaMemcpyAsync(h_arr[k]->data() + guess, d_arr[k] + guess, sizeof(int) * (K - guess),
+                         cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
   // depth of every node (children have larger ids than their parent), the depth-major
   // rank (BFS ids of the global levels keep their order) and the level offsets
   std::vector<int> h_dep(K, 0), cnt_d(1, 0);
@@ -1408,7 +1431,9 @@ static void finish_tree(DevTree& t, const double* d_x, int n, int D, int K,
   std::vector<int> sub(K, 1);
   for (int i = K - 1; i >= 0; --i)
     if (h_left[i] >= 0) sub[i] = 1 + sub[h_left[i]] + sub[h_right[i]];
-  std::vector<int> bfs2pre(K);
+  // (kept in the tree: the source of an asynchronous upload must outlive this call)
+  std::vector<int>& bfs2pre = t.h_pre;
+  bfs2pre.assign(K, 0);
   bfs2pre[0] = 0;
   for (int i = 0; i < K; ++i)
     if (h_left[i] >= 0) {
@@ -1419,8 +1444,9 @@ static void finish_tree(DevTree& t, const double* d_x, int n, int D, int K,
   d_map.reserve(K);
   CK(cudaMemcpyAsync(d_map.p, bfs2pre.data(), sizeof(int) * K, cudaMemcpyHostToDevice, s));
   if (rank) {
+    t.h_rank = *rank;
     d_rank.reserve(K);
-    CK(cudaMemcpyAsync(d_rank.p, rank->data(), sizeof(int) * K, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_rank.p, t.h_rank.data(), sizeof(int) * K, cudaMemcpyHostToDevice, s));
   }
   t.lo.reserve((size_t)K * D);
   t.hi.reserve((size_t)K * D);
@@ -1454,7 +1480,8 @@ static void finish_tree(DevTree& t, const double* d_x, int n, int D, int K,
     t.h_begin[bfs2pre[i]] = h_beg[i];
     t.h_left[bfs2pre[i]] = h_left[i] < 0 ? -1 : bfs2pre[h_left[i]];
   }
-  CK(cudaStreamSynchronize(s));
+  // no host wait: everything above is ordered on `s`; the temporaries of the build go to
+  // the allocator's pending list, which is only reused after a device synchronisation
 }
 
 }  // namespace dfgtb

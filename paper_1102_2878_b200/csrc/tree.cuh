@@ -24,6 +24,7 @@ struct DevTree {
   std::vector<int> h_count;   // host copy of count (preorder)
   std::vector<int> h_left;    // host copy of left (preorder)
   std::vector<int> h_begin;   // host copy of begin (preorder)
+  std::vector<int> h_pre, h_rank;  // build order -> preorder id / depth-major rank (upload sources)
 };
 
 // Builds the tree of the n x D row-major device points `d_x` (reference
