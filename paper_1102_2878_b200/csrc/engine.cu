@@ -222,14 +222,23 @@ static StreamSet acquire_streams()
     }
   }
   StreamSet r;
-  // DFGTB_STREAM_PRIO (experiments): 1 = the main stream (traversal, base-case chain)
-  // above the expansion stream, 2 = the other way round; default: equal priorities
-  static const int prio = std::getenv("DFGTB_STREAM_PRIO") ? std::atoi(std::getenv("DFGTB_STREAM_PRIO")) : 0;
+  // Stream priorities.  After the traversal three chains run side by side: the local
+  // expansions (s2: chunks -> reduce; the longest chain, it ends the batch), the far field
+  // (s3) and the base case (s).  Default (2): s2 above the others, so the critical chain
+  // is never queued behind the base-case kernels' CTAs (measured: cfg2 sweep -2%, cfg3
+  // -1.8% against equal priorities; the base-case kernels then run at their isolated
+  // rates).  DFGTB_STREAM_PRIO: 0 = equal, 1 = s high, 2 = s2 high, 3 = s2 > s3 > s,
+  // 4 = s2 > s > s3.
+  static const int prio = std::getenv("DFGTB_STREAM_PRIO") ? std::atoi(std::getenv("DFGTB_STREAM_PRIO")) : 2;
   int plo = 0, phi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&plo, &phi));  // phi = greatest priority (lowest number)
-  CK(cudaStreamCreateWithPriority(&r.s, cudaStreamNonBlocking, prio == 1 ? phi : plo));
-  CK(cudaStreamCreateWithPriority(&r.s2, cudaStreamNonBlocking, prio == 2 ? phi : plo));
-  CK(cudaStreamCreateWithFlags(&r.s3, cudaStreamNonBlocking));
+  const int pmid = plo > phi ? plo - 1 : plo;
+  const int ps = prio == 1 ? phi : prio == 4 ? pmid : plo;
+  const int ps2 = prio >= 2 ? phi : plo;
+  const int ps3 = prio == 3 ? pmid : plo;
+  CK(cudaStreamCreateWithPriority(&r.s, cudaStreamNonBlocking, ps));
+  CK(cudaStreamCreateWithPriority(&r.s2, cudaStreamNonBlocking, ps2));
+  CK(cudaStreamCreateWithPriority(&r.s3, cudaStreamNonBlocking, ps3));
   CK(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&r.fork3, cudaEventDisableTiming));
