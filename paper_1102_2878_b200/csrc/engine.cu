@@ -198,8 +198,8 @@ void pinned_free(void* p, size_t bytes)
 // costs ~0.1-0.2 ms per engine, which a CV call that builds an engine per dataset pays
 // every time.
 struct StreamSet {
-  cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
-  cudaEvent_t ev[16] = {}, fork = nullptr, join = nullptr, fork3 = nullptr, join3 = nullptr,
+  cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr, s4 = nullptr;
+  cudaEvent_t ev[16] = {}, fork = nullptr, join = nullptr, fork3 = nullptr, join3 = nullptr, prep = nullptr,
               legacy = nullptr, mom0 = nullptr, mom1 = nullptr;
 };
 static std::unordered_map<int, std::vector<StreamSet>>& stream_pool()
@@ -239,6 +239,10 @@ static StreamSet acquire_streams()
   CK(cudaStreamCreateWithPriority(&r.s, cudaStreamNonBlocking, ps));
   CK(cudaStreamCreateWithPriority(&r.s2, cudaStreamNonBlocking, ps2));
   CK(cudaStreamCreateWithPriority(&r.s3, cudaStreamNonBlocking, ps3));
+  // s4: the base case's short preparation kernels (task lists, records, scaled points),
+  // above everything so they are not queued behind the expansion kernels' CTAs
+  CK(cudaStreamCreateWithPriority(&r.s4, cudaStreamNonBlocking, phi));
+  CK(cudaEventCreateWithFlags(&r.prep, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&r.fork3, cudaEventDisableTiming));
@@ -315,6 +319,8 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
     join_ = ss.join;
     for (int i = 0; i < 16; ++i) ev_[i] = ss.ev[i];
     s3_ = ss.s3;
+    s4_ = ss.s4;
+    prep_ev_ = ss.prep;
     fork3_ = ss.fork3;
     join3_ = ss.join3;
     legacy_ev_ = ss.legacy;
@@ -368,6 +374,8 @@ Engine::~Engine()
     ss.join = join_;
     for (int i = 0; i < 16; ++i) ss.ev[i] = ev_[i];
     ss.s3 = s3_;
+    ss.s4 = s4_;
+    ss.prep = prep_ev_;
     ss.fork3 = fork3_;
     ss.join3 = join3_;
     ss.legacy = legacy_ev_;

@@ -193,6 +193,8 @@ private:
   cudaEvent_t ev_[16];
   cudaStream_t s3_ = nullptr;  // the FP64 base-case kernel beside the FP32 one
   cudaEvent_t fork3_ = nullptr, join3_ = nullptr;
+  cudaStream_t s4_ = nullptr;  // the base case's preparation kernels (highest priority)
+  cudaEvent_t prep_ev_ = nullptr;
   cudaEvent_t fork_ = nullptr, join_ = nullptr;
   cudaEvent_t legacy_ev_ = nullptr;
   cudaEvent_t mom_ev_[2] = { nullptr, nullptr };  // around the eager moment kernels (s2_)  // orders s_ after the legacy stream (wait_legacy_stream)

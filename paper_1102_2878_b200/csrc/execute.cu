@@ -2225,6 +2225,9 @@ int padded_dim(int D) { return D == 1 ? 1 : (D <= 5 ? (D + 1) / 2 * 2 : D); }
 // ws = [nextA, nextB, cntA, cntB, pairsA (u64), pairsB (u64), listA (tcap), listB (tcap),
 // task flags (tcap, written by k_task_build)]; the lists come from k_task_split.  Then the
 // FP32 kernel over list A, then the FP64 kernel over list B.
+#ifndef DFGTB_PREP_STREAM_DEFAULT
+#define DFGTB_PREP_STREAM_DEFAULT 1
+#endif
 #ifndef DFGTB_FF_STREAM_DEFAULT
 #define DFGTB_FF_STREAM_DEFAULT 1  // measured: cfg2 -1.4%, cfg3 / cfg5 -0.4% against the far field queued behind the local chain
 #endif
@@ -2454,6 +2457,18 @@ void Engine::run_phases(const DevTree& qt, const double* h, int nb, double* d_ou
   CK(cudaEventElapsedTime(&tim_.farfield_ms, ev_[6], ev_[7]));
   CK(cudaEventElapsedTime(&tim_.final_ms, ev_[14], ev_[8]));
   CK(cudaEventElapsedTime(&tim_.total_ms, ev_[2], ev_[8]));
+  if (std::getenv("DFGTB_TIMELINE")) {  // event times of the batch, ms after its start
+    const int ids[] = { 3, 4, 5, 6, 7, 9, 11, 10, 14, 8 };
+    const char* names[] = { "traversal_end", "local_start", "local_end", "ff_start", "ff_end", "base_start",
+                            "base_f32_end", "base_end", "joined", "end" };
+    std::fprintf(stderr, "DFGTB_TIMELINE");
+    for (int k = 0; k < 10; ++k) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, ev_[2], ev_[ids[k]]) != cudaSuccess) cudaGetLastError();
+      std::fprintf(stderr, " %s %.3f", names[k], ms);
+    }
+    std::fprintf(stderr, "\n");
+  }
 }
 
 void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d_out)
@@ -2494,6 +2509,62 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
   cudaStream_t s2 = one_stream_ ? s : s2_;  // DFGTB_ONE_STREAM: isolated kernel timings
   CK(cudaEventRecord(fork_, s));
   CK(cudaStreamWaitEvent(s2, fork_, 0));
+  const int nleaves = (int)qleaves_host_.size();
+  const int nlb = nleaves * nb;
+  // base-case tasks and records: queued first (host order) on the preparation stream
+  leaf_task_.reserve(KB);
+  leaf_runs_.reserve(KB);
+  const int rmax = base_rmax(D_);
+  capTask_ = std::max(capTask_, std::max(4096, capB_ / 8));
+  tasks_.reserve((size_t)capTask_ * 12);  // BTask array | packed list A | packed list B
+  bnext_.reserve(8 + 3 * (size_t)capTask_);  // base-case lists and task flags (launch_base_t)
+  // the preparation kernels run on their own top-priority stream (DFGTB_PREP_STREAM=0: on
+  // s): on s they were queued behind the expansion kernels and delayed the base case by
+  // ~0.15 ms on cfg2
+  static const int prep_env = std::getenv("DFGTB_PREP_STREAM") ? std::atoi(std::getenv("DFGTB_PREP_STREAM")) : DFGTB_PREP_STREAM_DEFAULT;
+  cudaStream_t sp = (prep_env && !one_stream_ && s4_) ? s4_ : s;
+  if (sp != s) CK(cudaStreamWaitEvent(sp, fork_, 0));
+  CK(cudaMemsetAsync(bc_.p + 5, 0, sizeof(int), sp));
+  k_task_build<<<ceil_div(nlb, 8), 256, 0, sp>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p, sB_.p,
+                                                  R.count, rmax, Q, reinterpret_cast<BTask*>(tasks_.p),
+                                                  capTask_, bc_.p + 5, leaf_task_.p, leaf_runs_.p,
+                                                  bnext_.p + 8 + 2 * (size_t)capTask_);
+  CK_LAUNCH();
+  CK(cudaMemsetAsync(bnext_.p, 0, 8 * sizeof(int), sp));
+  k_task_split<<<ceil_div(nlb, 8), 256, 0, sp>>>(leaves_.p, nleaves, nb, K, cntB_.p, leaf_task_.p, leaf_runs_.p, Q,
+                                                  capTask_, bnext_.p + 8 + 2 * (size_t)capTask_, f32_ ? 1 : 0,
+                                                  bnext_.p + 8, bnext_.p + 8 + capTask_, bnext_.p + 2,
+                                                  reinterpret_cast<const BTask*>(tasks_.p),
+                                                  reinterpret_cast<int4*>(tasks_.p + (size_t)capTask_ * 4),
+                                                  reinterpret_cast<int4*>(tasks_.p + (size_t)capTask_ * 8));
+  CK_LAUNCH();
+  bpart_.reserve((size_t)capTask_ * 32);
+  brec_.reserve((size_t)capB_ * 2 + 2);
+  k_base_records<<<148 * 4, 256, 0, sp>>>(sB_.p, dnB, capB_, R, reinterpret_cast<int2*>(brec_.p));
+  CK_LAUNCH();
+  // scaled, centred, padded coordinates per slot (Q and, if different, R)
+  const int DP = padded_dim(D_);
+  xq_.reserve((size_t)qt.n * DP * nb);
+  k_scale_points<<<ceil_div((long long)qt.n * DP * nb, 256), 256, 0, sp>>>(
+    qt.xs.p, qt.n, D_, DP, nb, rt_.centroid.p, sv, mufu_ ? kSqrtLog2e : 1.0, xq_.p);
+  CK_LAUNCH();
+  const double* xq = xq_.p;
+  const double* xr = xq_.p;
+  if (&qt != &rt_) {
+    xr_.reserve((size_t)rt_.n * DP * nb);
+    k_scale_points<<<ceil_div((long long)rt_.n * DP * nb, 256), 256, 0, sp>>>(
+      rt_.xs.p, rt_.n, D_, DP, nb, rt_.centroid.p, sv, mufu_ ? kSqrtLog2e : 1.0, xr_.p);
+    CK_LAUNCH();
+    xr = xr_.p;
+  }
+  if (sp != s) {
+    CK(cudaEventRecord(prep_ev_, sp));
+    CK(cudaStreamWaitEvent(s, prep_ev_, 0));
+    if (prep_env == 2) {  // the expansion chains start with the base case, after the preparation
+      CK(cudaStreamWaitEvent(s2, prep_ev_, 0));
+      if (s3_) CK(cudaStreamWaitEvent(s3_, prep_ev_, 0));
+    }
+  }
   // moments of the reference nodes used by F/T items (large tables only; small
   // tables were computed for every node when the engine was built)
   if (!eager_ && cfg_.mode == 1) {
@@ -2514,8 +2585,6 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
   const int ff_mode = (one_stream_ || !s3_ || (cfg_.mode == 1 && !eager_)) ? 0 : ff_env;
   cudaStream_t sff = ff_mode ? s3_ : s2;
   if (ff_mode) CK(cudaStreamWaitEvent(sff, fork_, 0));
-  const int nleaves = (int)qleaves_host_.size();
-  const int nlb = nleaves * nb;
   auto launch_ff = [&]() {
     s_ff_.reserve((size_t)qt.n * nb);
     CK(cudaEventRecord(ev_[6], sff));
@@ -2592,46 +2661,6 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
   CK(cudaEventRecord(ev_[5], s2));
   if (ff_mode != 2) launch_ff();
   CK(cudaEventRecord(join_, s2));
-  // base-case tasks (s_)
-  leaf_task_.reserve(KB);
-  leaf_runs_.reserve(KB);
-  const int rmax = base_rmax(D_);
-  capTask_ = std::max(capTask_, std::max(4096, capB_ / 8));
-  tasks_.reserve((size_t)capTask_ * 12);  // BTask array | packed list A | packed list B
-  bnext_.reserve(8 + 3 * (size_t)capTask_);  // base-case lists and task flags (launch_base_t)
-  CK(cudaMemsetAsync(bc_.p + 5, 0, sizeof(int), s));
-  k_task_build<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, offB_.p, sB_.p,
-                                                  R.count, rmax, Q, reinterpret_cast<BTask*>(tasks_.p),
-                                                  capTask_, bc_.p + 5, leaf_task_.p, leaf_runs_.p,
-                                                  bnext_.p + 8 + 2 * (size_t)capTask_);
-  CK_LAUNCH();
-  CK(cudaMemsetAsync(bnext_.p, 0, 8 * sizeof(int), s));
-  k_task_split<<<ceil_div(nlb, 8), 256, 0, s>>>(leaves_.p, nleaves, nb, K, cntB_.p, leaf_task_.p, leaf_runs_.p, Q,
-                                                  capTask_, bnext_.p + 8 + 2 * (size_t)capTask_, f32_ ? 1 : 0,
-                                                  bnext_.p + 8, bnext_.p + 8 + capTask_, bnext_.p + 2,
-                                                  reinterpret_cast<const BTask*>(tasks_.p),
-                                                  reinterpret_cast<int4*>(tasks_.p + (size_t)capTask_ * 4),
-                                                  reinterpret_cast<int4*>(tasks_.p + (size_t)capTask_ * 8));
-  CK_LAUNCH();
-  bpart_.reserve((size_t)capTask_ * 32);
-  brec_.reserve((size_t)capB_ * 2 + 2);
-  k_base_records<<<148 * 4, 256, 0, s>>>(sB_.p, dnB, capB_, R, reinterpret_cast<int2*>(brec_.p));
-  CK_LAUNCH();
-  // scaled, centred, padded coordinates per slot (Q and, if different, R)
-  const int DP = padded_dim(D_);
-  xq_.reserve((size_t)qt.n * DP * nb);
-  k_scale_points<<<ceil_div((long long)qt.n * DP * nb, 256), 256, 0, s>>>(
-    qt.xs.p, qt.n, D_, DP, nb, rt_.centroid.p, sv, mufu_ ? kSqrtLog2e : 1.0, xq_.p);
-  CK_LAUNCH();
-  const double* xq = xq_.p;
-  const double* xr = xq_.p;
-  if (&qt != &rt_) {
-    xr_.reserve((size_t)rt_.n * DP * nb);
-    k_scale_points<<<ceil_div((long long)rt_.n * DP * nb, 256), 256, 0, s>>>(
-      rt_.xs.p, rt_.n, D_, DP, nb, rt_.centroid.p, sv, mufu_ ? kSqrtLog2e : 1.0, xr_.p);
-    CK_LAUNCH();
-    xr = xr_.p;
-  }
   CK(cudaEventRecord(ev_[9], s));
   BaseConc conc;
   if (DFGTB_BASE_CONC && f32_ && !std::getenv("DFGTB_BASE_SERIAL")) {
