@@ -2034,8 +2034,12 @@ __device__ __forceinline__ double local_horner(const double* Lk, const int* tp, 
 // time (Horner per dimension, position layout via term_of_pos staged in shared
 // memory; entries beyond a table's order are zero).  Ancestors are walked from the
 // leaf up (no per-thread chain array).
+#ifndef DFGTB_FIN_MINB
+#define DFGTB_FIN_MINB 8  // 64 registers (the full-order Horner spills, it is rare): latency-bound, occupancy pays --
+                          // k_finalize_t 69 -> 57 us (cfg2), 0.54 -> 0.39 ms (cfg3) against 128 registers
+#endif
 template <int D, int PM>
-__global__ void __launch_bounds__(128) k_finalize_t(DevSeries g, TreeView Q, int K, int nb,
+__global__ void __launch_bounds__(128, DFGTB_FIN_MINB) k_finalize_t(DevSeries g, TreeView Q, int K, int nb,
                                                     const int* leaf_of_pos, const int* perm, int n,
                                                     const double* L, const int* Lord,
                                                     const int* cntB, const int* leaf_task,
