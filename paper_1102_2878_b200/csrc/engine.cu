@@ -274,6 +274,7 @@ void init_device_constants(cudaStream_t s)
   if (done[dev]) return;
   init_exp_constants(s);
   init_truncation_tables(s);
+  init_truncation_tables_small(s);
   CK(cudaStreamSynchronize(s));
   done[dev] = true;
 }

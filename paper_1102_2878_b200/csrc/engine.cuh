@@ -211,6 +211,7 @@ private:
   // [0] nF [1] nDT [2] nB [3] traversal overflow [4] local chunks [5] base tasks
   DevBuf<int> bc_;
   int trav_nb_ = 0;
+  int trav_nq_ = 0;  // query points of the batch being traversed
   bool trav_trace_ = false;
   int capCh_ = 0, capTask_ = 0;  // local chunks / base tasks (grown on overflow)
 };
@@ -245,6 +246,11 @@ void pinned_free(void* p, size_t bytes);
 void init_exp_constants(cudaStream_t s);
 // Constant tables of the error bounds (traverse.cu).
 void init_truncation_tables(cudaStream_t s);
+void init_truncation_tables_small(cudaStream_t s);  // traverse_small.cu's copies
+void* traverse_small_kernel(int D);
+int traverse_small_block();
+// batches with fewer slot x query points than this run the 768-thread traversal
+constexpr long long kTravSmallWork = 1000000;
 // Both of the above, once per device and process (engine.cu).
 void init_device_constants(cudaStream_t s);
 // Test entries (traverse.cu): choose_best_method / the least orders and

@@ -364,8 +364,11 @@ __global__ void __launch_bounds__(kLocThreads) k_local_chunks_t(DevSeries g, Tre
 // Both write the same unsigned partial table (term layout, terms < order^D) as
 // dev_direct_local_partial / dev_f2l_block.
 constexpr int kLocWarps = 4;
+#ifndef DFGTB_LOC_MINB
+#define DFGTB_LOC_MINB 4  // <= 128 registers (119 at D = 2; D = 3 spills 184 B): measured best of 2 / 4 / 6 / 8
+#endif
 template <int D, int PM>
-__global__ void __launch_bounds__(kLocWarps * 32) k_local_chunks_w(
+__global__ void __launch_bounds__(kLocWarps * 32, DFGTB_LOC_MINB) k_local_chunks_w(
   DevSeries g, TreeView Q, TreeView R, int K, const Item* items, const LChunk* ch, const int* nchp,
   int chcap, const double* Mt, SlotView sv, double* part)
 {

@@ -1439,7 +1439,15 @@ void launch_level(const TravArgs& a, int D, cudaStream_t s, cudaGraphConditional
 
 }  // namespace
 
-void init_truncation_tables(cudaStream_t s)
+// This file is compiled twice: as itself (1024-thread traversal CTAs, every host entry)
+// and through traverse_small.cu (KPBLOCK = 768, DFGTB_TRAV_SMALL_TU: only the kernels,
+// this upload into that unit's own __constant__ copies, and the kernel lookup below).
+#ifdef DFGTB_TRAV_SMALL_TU
+#define DFGTB_TRUNC_INIT init_truncation_tables_small
+#else
+#define DFGTB_TRUNC_INIT init_truncation_tables
+#endif
+void DFGTB_TRUNC_INIT(cudaStream_t s)
 {
   double isf[16], sf[16], bin[17][17];
   double f = 1.0;
@@ -1459,6 +1467,23 @@ void init_truncation_tables(cudaStream_t s)
   CK(cudaMemcpyToSymbolAsync(c_binom, bin, sizeof(bin), 0, cudaMemcpyHostToDevice, s));
 }
 
+#ifdef DFGTB_TRAV_SMALL_TU
+// k_traverse with kPBlock-thread CTAs (80 registers instead of 64: fewer spills, shorter
+// dependent chains per level -- faster where the levels are latency-bound, slower where
+// they are throughput-bound; Engine::run_levels chooses)
+void* traverse_small_kernel(int D)
+{
+  switch (D) {
+  case 1: return (void*)k_traverse<1>;
+  case 2: return (void*)k_traverse<2>;
+  case 3: return (void*)k_traverse<3>;
+  case 4: return (void*)k_traverse<4>;
+  case 5: return (void*)k_traverse<5>;
+  default: return (void*)k_traverse<0>;
+  }
+}
+int traverse_small_block() { return kPBlock; }
+#else
 // ------------------------------------------------------------------ test entries
 namespace {
 __global__ void k_choose_test(int n, const double* args, int* out)
@@ -1538,16 +1563,29 @@ void Engine::run_levels(const void* args, const std::vector<const void*>& sig)
     case 5: fn = (void*)k_traverse<5>; break;
     default: fn = (void*)k_traverse<0>; break;
     }
+    // Small batches (slots x query points below kTravSmallWork) are latency-bound at every
+    // level: the 768-thread build (80 registers) runs them faster (cfg2, 0.9M: 0.637 ->
+    // 0.604 ms; cfg1: 0.320 -> 0.282 ms); bigger ones need the 1024 threads (cfg4, 1.4M:
+    // 20.1 vs 23.6 ms; cfg3, 3.6M: 10.9 vs 12.3 ms; cfg5: 32.4 vs 37.3 ms).
+    // DFGTB_TRAV_BLOCK = 768 / 1024 forces one.
+    static const int blk_env = std::getenv("DFGTB_TRAV_BLOCK") ? std::atoi(std::getenv("DFGTB_TRAV_BLOCK")) : 0;
+    const bool small = !kUseCache && (blk_env ? blk_env == traverse_small_block()
+                                              : (long long)trav_nq_ * trav_nb_ < kTravSmallWork);
+    int block = kPBlock;
+    if (small) {
+      fn = traverse_small_kernel(D_);
+      block = traverse_small_block();
+    }
     int dev = 0, nsm = 0, per_sm = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     const int smem = kUseCache ? kCacheBytes : 0;
     if (smem) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPBlock, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
     if (per_sm >= 1) {
       TravArgs copy = a;
       void* kargs[] = { &copy };
-      CK(cudaLaunchCooperativeKernel(fn, nsm * std::min(per_sm, kPerSM), kPBlock, kargs, smem, s_));
+      CK(cudaLaunchCooperativeKernel(fn, nsm * std::min(per_sm, kPerSM), block, kargs, smem, s_));
       ++launch_counter();
       return;
     }
@@ -1833,6 +1871,8 @@ void Engine::traverse(const DevTree& qt, const double* h, int nb)
   start_frontier(qt, &a);
   k_trav_init<<<32, 256, 0, s>>>(a);
   CK_LAUNCH();
+  trav_nq_ = qt.n;
+  trav_nb_ = nb;
   run_levels(&a, sig);
   k_trav_publish<<<1, 1, 0, s>>>(ds, bc_.p);
   CK_LAUNCH();
@@ -1960,5 +2000,7 @@ bool Engine::traverse_finish(bool prefetched)
   nB_ = hs->nB;
   return true;
 }
+
+#endif  // DFGTB_TRAV_SMALL_TU
 
 }  // namespace dfgtb
