@@ -1440,7 +1440,7 @@ void launch_level(const TravArgs& a, int D, cudaStream_t s, cudaGraphConditional
 }  // namespace
 
 // This file is compiled twice: as itself (1024-thread traversal CTAs, every host entry)
-// and through traverse_small.cu (KPBLOCK = 768, DFGTB_TRAV_SMALL_TU: only the kernels,
+// and through traverse_small.cu (KPBLOCK = 640, DFGTB_TRAV_SMALL_TU: only the kernels,
 // this upload into that unit's own __constant__ copies, and the kernel lookup below).
 #ifdef DFGTB_TRAV_SMALL_TU
 #define DFGTB_TRUNC_INIT init_truncation_tables_small
@@ -1468,7 +1468,7 @@ void DFGTB_TRUNC_INIT(cudaStream_t s)
 }
 
 #ifdef DFGTB_TRAV_SMALL_TU
-// k_traverse with kPBlock-thread CTAs (80 registers instead of 64: fewer spills, shorter
+// k_traverse with kPBlock-thread CTAs (96 registers instead of 64: fewer spills, shorter
 // dependent chains per level -- faster where the levels are latency-bound, slower where
 // they are throughput-bound; Engine::run_levels chooses)
 void* traverse_small_kernel(int D)
@@ -1564,10 +1564,10 @@ void Engine::run_levels(const void* args, const std::vector<const void*>& sig)
     default: fn = (void*)k_traverse<0>; break;
     }
     // Small batches (slots x query points below kTravSmallWork) are latency-bound at every
-    // level: the 768-thread build (80 registers) runs them faster (cfg2, 0.9M: 0.637 ->
-    // 0.604 ms; cfg1: 0.320 -> 0.282 ms); bigger ones need the 1024 threads (cfg4, 1.4M:
-    // 20.1 vs 23.6 ms; cfg3, 3.6M: 10.9 vs 12.3 ms; cfg5: 32.4 vs 37.3 ms).
-    // DFGTB_TRAV_BLOCK = 768 / 1024 forces one.
+    // level: the small-CTA build (traverse_small.cu: 640 threads, 96 registers) runs them
+    // faster (cfg2, 0.9M: 0.637 -> 0.576 ms; cfg1: 0.320 -> 0.264 ms); bigger ones need the
+    // 1024 threads (768 vs 1024 threads: cfg4, 1.4M: 23.6 vs 20.1 ms; cfg3, 3.6M: 12.3 vs
+    // 10.9 ms; cfg5: 37.3 vs 32.4 ms).  DFGTB_TRAV_BLOCK = 640 / 1024 forces one.
     static const int blk_env = std::getenv("DFGTB_TRAV_BLOCK") ? std::atoi(std::getenv("DFGTB_TRAV_BLOCK")) : 0;
     const bool small = !kUseCache && (blk_env ? blk_env == traverse_small_block()
                                               : (long long)trav_nq_ * trav_nb_ < kTravSmallWork);
