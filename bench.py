@@ -293,6 +293,7 @@ def config_records(dfgtb, flush, steps):
             nbw = 2 * len(hs)
             fn = lambda: eng.sweep(w.scales, w.h_s)  # noqa: E731
         fn()
+        fn()  # two warm-up calls: the first grows the batch buffers, the second the pinned pools
         ms, dev_ms, base_ms, pairs = [], [], [], []
         for _ in range(steps):
             with torch.cuda.stream(stream):

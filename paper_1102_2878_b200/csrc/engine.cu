@@ -332,7 +332,7 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
   if (on_device) wait_legacy_stream();  // the caller's producer of refs
   CK(cudaMemcpyAsync(x_.p, refs, sizeof(double) * n * d,
                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s_));
-  upload_series(ser_, ser_dev_, s_);
+  upload_series(ser_, ser_dev_, s_, &ser_blob_);
   init_device_constants(s_);
   CK(cudaEventRecord(ev_[0], s_));
   build_tree(rt_, x_.p, (int)n, D_, cfg.leaf_threshold, s_);
@@ -354,6 +354,10 @@ Engine::Engine(const double* refs, size_t n, size_t d, const Config& cfg, bool o
       CK(cudaMemsetAsync(mdone_.p, 0, sizeof(int) * rt_.nodes, s_));
     }
   }
+  // the Q = R leaf list now, while the device builds the moments (the first batch finds it
+  // ready; a Q != R batch replaces it)
+  setup_leaves(rt_);
+  leaves_src_ = 0;
   CK(cudaStreamSynchronize(s_));
   CK(cudaEventElapsedTime(&tim_.tree_ms, ev_[0], ev_[1]));
   slot_stats_.assign(1, Stats{});
@@ -388,12 +392,17 @@ Engine::~Engine()
 
 DevSeries Engine::dev_series() const { return series_view(ser_, ser_dev_); }
 
-void upload_series(const SeriesTables& t, DevBuf<unsigned char>& dev, cudaStream_t s)
+void upload_series(const SeriesTables& t, DevBuf<unsigned char>& dev, cudaStream_t s,
+                   std::vector<unsigned char>* keep)
 {
   const int T = t.T;
   const size_t bytes = sizeof(uint64_t) * T + sizeof(double) * 2 * T + sizeof(int) * 3 * T;
   dev.reserve(bytes);
-  std::vector<unsigned char> blob(bytes);
+  // keep != nullptr: the caller owns the upload's source and orders itself on `s` (no
+  // host wait here: the engine's point upload is in flight on the same stream)
+  std::vector<unsigned char> local;
+  std::vector<unsigned char>& blob = keep ? *keep : local;
+  blob.assign(bytes, 0);
   unsigned char* p = blob.data();
   std::memcpy(p, t.dig.data(), sizeof(uint64_t) * T);
   p += sizeof(uint64_t) * T;
@@ -407,7 +416,7 @@ void upload_series(const SeriesTables& t, DevBuf<unsigned char>& dev, cudaStream
   p += sizeof(int) * T;
   std::memcpy(p, t.pos.data(), sizeof(int) * T);
   CK(cudaMemcpyAsync(dev.p, blob.data(), bytes, cudaMemcpyHostToDevice, s));
-  CK(cudaStreamSynchronize(s));
+  if (!keep) CK(cudaStreamSynchronize(s));
 }
 
 DevSeries series_view(const SeriesTables& t, const DevBuf<unsigned char>& dev)

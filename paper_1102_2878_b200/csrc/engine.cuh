@@ -147,6 +147,7 @@ private:
   DevBuf<double> qx_;       // query points (Q != R)
   SeriesTables ser_;
   DevBuf<unsigned char> ser_dev_;
+  std::vector<unsigned char> ser_blob_;  // host source of ser_dev_'s upload
   DevBuf<int> leaves_, leaf_of_pos_;  // of the current query tree
   DevBuf<int> mom_node_, mom_start_, mom_off_;  // eager moments: chunk lists
   DevBuf<double> mom_part_;                     // eager moments: chunk partials
@@ -234,7 +235,8 @@ double f32_exp_max_error();
 void f32_terms_host(int d, const double* q, const double* r, const double* c, size_t n, double* out);
 
 // Series term tables -> one device blob, and the device view over it.
-void upload_series(const SeriesTables& t, DevBuf<unsigned char>& dev, cudaStream_t s);
+void upload_series(const SeriesTables& t, DevBuf<unsigned char>& dev, cudaStream_t s,
+                   std::vector<unsigned char>* keep = nullptr);
 DevSeries series_view(const SeriesTables& t, const DevBuf<unsigned char>& dev);
 
 // Pinned host blocks (cached like device memory; engine.cu).

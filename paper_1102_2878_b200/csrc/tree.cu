@@ -437,7 +437,10 @@ __global__ void k_iota(int* p, int n)
 // Positions are statically chunked over the CTAs (C scans its chunk locally, D adds
 // the preceding chunks' totals), so the prefix P and the BFS child ids are exactly
 // those of a sequential scan.
-constexpr int kPB = 1024;        // threads per CTA of k_build
+#ifndef DFGTB_TREE_PB
+#define DFGTB_TREE_PB 1024
+#endif
+constexpr int kPB = DFGTB_TREE_PB;  // threads per CTA of k_build
 constexpr int kMaxTreeLevels = 256;
 
 struct BuildArgs {

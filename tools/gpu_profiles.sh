@@ -3,7 +3,7 @@
 # --set full captures of the hot kernels (cfg2: base case, traversal; cfg3: expansion
 # kernels and the FP32 base case), each only after its own command ran clean.
 #   tools/gpu_profiles.sh TAG
-TAG=${1:-r2c}
+TAG=${1:-r2d}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${TAG}_gpu.txt 2>&1
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest.log 2>&1
@@ -27,7 +27,7 @@ cap() {  # cap NAME REGEX SKIP CONFIG
   [ "$KEEP_REPS" = "1" ] || rm -f gpurun_out/${TAG}_$1.ncu-rep
 }
 cap cfg2_base_f32 "k_base_f32" 1 2
-cap cfg2_base_case "k_base_case<" 1 2
+cap cfg2_base_case "k_base_case$" 1 2
 cap cfg2_traverse "k_traverse" 1 2
 cap cfg2_farfield "k_farfield_t" 1 2
 cap cfg3_base_f32 "k_base_f32" 4 3
