@@ -500,18 +500,39 @@ __global__ void __launch_bounds__(kLocWarps * 32, DFGTB_LOC_MINB) k_local_chunks
   }
 }
 
-__global__ void k_local_reduce(DevSeries g, const int* nitems_p, int cap, const int* cnt,
+// One warp per (slot, query node) key that has D/T items.  The keys are found from the
+// per-key counts, kLrKeys keys per CTA round (coalesced loads, compacted in shared
+// memory, dealt to the CTA's warps) -- not by scanning the item list for first-of-key
+// items, which cost every warp a chain of dependent loads per item.
+constexpr int kLrKeys = 64;
+__global__ void k_local_reduce(DevSeries g, const int* nitems_p, int cap, int nkeys, const int* cnt,
                                const int* off, const Item* items, const int* choff,
                                const double* part, double* L, int* Lord)
 {
   const int nitems = min(*nitems_p, cap);
-  const int lane = threadIdx.x & 31;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nitems;
-       i += (gridDim.x * blockDim.x) >> 5) {
-  const int n = items[i].key;
-  const int i0 = off[n];
-  if (i != i0) continue;  // not the first item of its key
-  const int i1 = i0 + cnt[n];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  __shared__ int s_n, s_key[kLrKeys], s_i0[kLrKeys], s_c[kLrKeys];
+  for (int kb = blockIdx.x * kLrKeys; kb < nkeys; kb += gridDim.x * kLrKeys) {
+  __syncthreads();
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  if (threadIdx.x < kLrKeys && kb + threadIdx.x < nkeys) {
+    const int c = cnt[kb + threadIdx.x];
+    if (c > 0) {
+      const int o = off[kb + threadIdx.x];
+      if (o + c <= nitems) {
+        const int pos = atomicAdd(&s_n, 1);  // any order: every key's table is its own
+        s_key[pos] = kb + threadIdx.x;
+        s_i0[pos] = o;
+        s_c[pos] = c;
+      }
+    }
+  }
+  __syncthreads();
+  for (int j = wib; j < s_n; j += nwb) {
+  const int n = s_key[j];
+  const int i0 = s_i0[j];
+  const int i1 = i0 + s_c[j];
   int ord = 0, omin = 1 << 20;
   for (int k = i0 + lane; k < i1; k += 32) {
     ord = max(ord, items[k].code & 0xff);
@@ -549,6 +570,7 @@ __global__ void k_local_reduce(DevSeries g, const int* nitems_p, int cap, const 
     L[(size_t)n * g.T + t] += sg * g.invf[t] * acc;
   }
   if (lane == 0 && Lord[n] < ord) Lord[n] = ord;
+  }
   }
 }
 
@@ -2652,7 +2674,7 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
       k_local_chunks<<<gl, 64, smem, s2>>>(g, Q, R, K, sDT_.p, ch, dnch, capCh_, Mt_.p, sv, lpart_.p);
 #undef LOC_T
     CK_LAUNCH();
-    k_local_reduce<<<148 * 8, 256, 0, s2>>>(g, dnDT, capDT_, cntDT_.p, offDT_.p, sDT_.p, lchoff_.p,
+    k_local_reduce<<<148 * 8, 256, 0, s2>>>(g, dnDT, capDT_, (int)KB, cntDT_.p, offDT_.p, sDT_.p, lchoff_.p,
                                             lpart_.p, L_.p, Lord_.p);
     CK_LAUNCH();
   }

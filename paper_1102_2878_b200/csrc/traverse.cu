@@ -1713,8 +1713,9 @@ static void frontier_nodes(const DevTree& t, int d0, std::vector<int>& out)
 void Engine::start_frontier(const DevTree& qt, void* args)
 {
   TravArgs& a = *static_cast<TravArgs*>(args);
-  // measured (cfg2 sweep): depth 0 1.47 ms, 3 1.43, 4 1.39, 5 1.37, 6 1.38; cfg3 neutral
-  static const int d0 = std::getenv("DFGTB_TRAV_START_DEPTH") ? std::atoi(std::getenv("DFGTB_TRAV_START_DEPTH")) : 5;
+  // measured (cfg2 sweep): depth 0 1.47 ms, 3 1.43, 4 1.39, 5 1.37, 6 1.38 with 1024-thread
+  // CTAs; with the 640-thread small-batch build 4 1.135, 5 1.117, 6 1.105, 7 1.134; cfg3 neutral
+  static const int d0 = std::getenv("DFGTB_TRAV_START_DEPTH") ? std::atoi(std::getenv("DFGTB_TRAV_START_DEPTH")) : 6;
   a.sq = a.sr = nullptr;
   a.nsq = a.nsr = 1;
   // only deep trees have top levels worth skipping (a shallow tree keeps the reference's
