@@ -1,0 +1,44 @@
+"""Scheduling choices must not change results: the traversal with 640- and 1024-thread
+CTAs (traverse_small.cu / traverse.cu; items carry a per-key rank and are counting-sorted,
+so the CTA partition of a level is invisible), equal stream priorities and a single stream
+give the same sums bit for bit and the same TraversalStats (engine.cpp:113-195)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r'''
+import hashlib, os, sys
+sys.path.insert(0, os.environ["ROOT"])
+import numpy as np
+import paper_1102_2878_b200 as dfgtb
+from paper_1102_2878_b200 import datagen
+w = datagen.config(int(os.environ["CFG"]), scale_n=float(os.environ["SCALE"]))
+e = dfgtb.DualTreeEngine(w.refs, config=dfgtb.EngineConfig(epsilon=0.01, leaf_threshold=32))
+hs = [s * f * w.h_s for s in w.scales for f in (1.0, 2.0)]
+sums = e.compute_batch(None, hs)
+rows = e.sweep(w.scales, w.h_s)
+st = e.last_stats()
+print("RESULT", hashlib.sha256(np.ascontiguousarray(sums).tobytes()).hexdigest(),
+      [(r.lk_score, r.lk_clamped, r.ls_score) for r in rows], st)
+'''
+
+
+def _run(cfg, scale, **env):
+    e = dict(os.environ, ROOT=ROOT, CFG=str(cfg), SCALE=str(scale), **env)
+    out = subprocess.run([sys.executable, "-c", CHILD], env=e, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return [l for l in out.stdout.splitlines() if l.startswith("RESULT")][-1]
+
+
+@pytest.mark.parametrize("cfg,scale", [(2, 0.3), (3, 0.05)])
+def test_results_independent_of_schedule(cfg, scale):
+    base = _run(cfg, scale)
+    assert _run(cfg, scale, DFGTB_TRAV_BLOCK="1024") == base
+    assert _run(cfg, scale, DFGTB_TRAV_BLOCK="640") == base
+    assert _run(cfg, scale, DFGTB_STREAM_PRIO="0", DFGTB_FF_STREAM="0", DFGTB_PREP_STREAM="0") == base
+    assert _run(cfg, scale, DFGTB_ONE_STREAM="1") == base
