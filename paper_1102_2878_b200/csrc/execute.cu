@@ -504,7 +504,10 @@ __global__ void __launch_bounds__(kLocWarps * 32, DFGTB_LOC_MINB) k_local_chunks
 // per-key counts, kLrKeys keys per CTA round (coalesced loads, compacted in shared
 // memory, dealt to the CTA's warps) -- not by scanning the item list for first-of-key
 // items, which cost every warp a chain of dependent loads per item.
-constexpr int kLrKeys = 64;
+#ifndef DFGTB_LR_KEYS
+#define DFGTB_LR_KEYS 64
+#endif
+constexpr int kLrKeys = DFGTB_LR_KEYS;
 __global__ void k_local_reduce(DevSeries g, const int* nitems_p, int cap, int nkeys, const int* cnt,
                                const int* off, const Item* items, const int* choff,
                                const double* part, double* L, int* Lord)

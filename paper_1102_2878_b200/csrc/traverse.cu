@@ -770,7 +770,7 @@ struct PairCache {
 // charge: the per-entry phases -- G^l, counts, emission -- run one warp per entry, so a
 // range of many small entries costs more than its pairs say).
 #ifndef DFGTB_ENTRY_COST
-#define DFGTB_ENTRY_COST 8
+#define DFGTB_ENTRY_COST 16  // measured (cfg2 traversal ms, 640-thread build): 4 0.582, 8 0.557, 16 0.548, 24 0.558, 32 0.570
 #endif
 constexpr long long kEntryCost = DFGTB_ENTRY_COST;
 __device__ __forceinline__ void entry_bounds(const int* foff, int m, long long t0, long long t1,
