@@ -36,10 +36,15 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 // Every kernel launch of this library is followed by CK_LAUNCH(): it checks the
 // launch and counts it (dfgtb_launch_count reports the process-wide total).
 uint64_t& launch_counter();
+// DFGTB_SYNC_LAUNCH=1 (debugging): wait for the device after every launch, so a faulting
+// kernel is reported at its own launch site instead of at the batch's final wait.
+bool sync_launch_mode();
 #define CK_LAUNCH()                                                                    \
   do {                                                                                 \
     ::dfgtb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__);      \
     ++::dfgtb::launch_counter();                                                       \
+    if (::dfgtb::sync_launch_mode())                                                   \
+      ::dfgtb::cuda_check(cudaDeviceSynchronize(), "kernel execution", __FILE__, __LINE__); \
   } while (0)
 
 // Process-wide caching device allocator (power-of-two size classes, like PyTorch's

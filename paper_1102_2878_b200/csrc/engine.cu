@@ -109,6 +109,12 @@ void* cache_alloc(size_t bytes)
   return p;
 }
 
+bool sync_launch_mode()
+{
+  static const bool on = std::getenv("DFGTB_SYNC_LAUNCH") != nullptr;
+  return on;
+}
+
 bool guard_mode()
 {
   static const bool on = std::getenv("DFGTB_GUARD") != nullptr;

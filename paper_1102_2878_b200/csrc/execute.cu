@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kLocWarps * 32, DFGTB_LOC_MINB) k_local_chunks
 #endif
 constexpr int kLrKeys = DFGTB_LR_KEYS;
 __global__ void k_local_reduce(DevSeries g, const int* nitems_p, int cap, int nkeys, const int* cnt,
-                               const int* off, const Item* items, const int* choff,
+                               const int* off, const Item* items, const int* choff, int capch,
                                const double* part, double* L, int* Lord)
 {
   const int nitems = min(*nitems_p, cap);
@@ -547,6 +547,7 @@ __global__ void k_local_reduce(DevSeries g, const int* nitems_p, int cap, int nk
     omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, o));
   }
   const int q0 = choff[i0], q1 = choff[i1];
+  if (q1 > capch) continue;  // chunks past the chunk buffer were dropped: the batch is rerun
   const int nt = ipow_i(ord, g.D);
   for (int t = lane; t < nt; t += 32) {
     const uint64_t a = g.dig[t];
@@ -1986,7 +1987,7 @@ __global__ void __launch_bounds__(kBlock, DFGTB_FF_MINB) k_farfield_t(TreeView Q
 __global__ void k_finalize(DevSeries g, TreeView Q, int K, int nb, const int* leaf_of_pos,
                            const int* perm, int n, const double* L, const int* Lord,
                            const int* cntB, const int* leaf_task, const int* leaf_runs,
-                           const double* part,
+                           const double* part, int tcap,
                            const double* s_ff, SlotView sv, int direct, double* out)
 {
   const long long gi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -2017,7 +2018,9 @@ __global__ void k_finalize(DevSeries g, TreeView Q, int K, int nb, const int* le
   double ex = 0.0;
   if (nic) {
     const int t0 = leaf_task[lkey] + (li >> 5) * nic;
-    for (int k = 0; k < nic; ++k) ex += part[(size_t)(t0 + k) * 32 + (li & 31)];
+    // (tasks past the task buffer were dropped: the batch is rerun, nothing is read there)
+    if (t0 + nic <= tcap)
+      for (int k = 0; k < nic; ++k) ex += part[(size_t)(t0 + k) * 32 + (li & 31)];
   }
   out[(size_t)slot * n + perm[i]] = loc + s_ff[(size_t)slot * n + i] + ex;
 }
@@ -2071,7 +2074,7 @@ __global__ void __launch_bounds__(128, DFGTB_FIN_MINB) k_finalize_t(DevSeries g,
                                                     const int* leaf_of_pos, const int* perm, int n,
                                                     const double* L, const int* Lord,
                                                     const int* cntB, const int* leaf_task,
-                                                    const int* leaf_runs, const double* part,
+                                                    const int* leaf_runs, const double* part, int tcap,
                                                     const double* s_ff, SlotView sv, double* out)
 {
   constexpr int NP = ipow_c(PM, D);
@@ -2138,7 +2141,9 @@ __global__ void __launch_bounds__(128, DFGTB_FIN_MINB) k_finalize_t(DevSeries g,
   double ex = 0.0;
   if (nic) {
     const int t0 = leaf_task[lkey] + (li >> 5) * nic;
-    for (int k = 0; k < nic; ++k) ex += part[(size_t)(t0 + k) * 32 + (li & 31)];
+    // (tasks past the task buffer were dropped: the batch is rerun, nothing is read there)
+    if (t0 + nic <= tcap)
+      for (int k = 0; k < nic; ++k) ex += part[(size_t)(t0 + k) * 32 + (li & 31)];
   }
   out[(size_t)slot * n + perm[i]] = loc + s_ff[(size_t)slot * n + i] + ex;
 }
@@ -2678,7 +2683,7 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
 #undef LOC_T
     CK_LAUNCH();
     k_local_reduce<<<148 * 8, 256, 0, s2>>>(g, dnDT, capDT_, (int)KB, cntDT_.p, offDT_.p, sDT_.p, lchoff_.p,
-                                            lpart_.p, L_.p, Lord_.p);
+                                            capCh_, lpart_.p, L_.p, Lord_.p);
     CK_LAUNCH();
   }
   if (cfg_.local_pushdown == 1) {
@@ -2719,7 +2724,7 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
 #define FIN_T(DD, PP)                                                                             \
   k_finalize_t<DD, PP><<<fgrid, 128, 0, s>>>(g, Q, K, nb, leaf_of_pos_.p, qt.perm.p, qt.n, L_.p,  \
                                              Lord_.p, cntB_.p, leaf_task_.p, leaf_runs_.p,        \
-                                             bpart_.p, s_ff_.p, sv, d_out)
+                                             bpart_.p, capTask_, s_ff_.p, sv, d_out)
     if (direct && cfg_.mode == 1 && D_ == 1 && pm == 8) FIN_T(1, 8);
     else if (direct && cfg_.mode == 1 && D_ == 2 && pm == 6) FIN_T(2, 6);
     else if (direct && cfg_.mode == 1 && D_ == 3 && pm == 4) FIN_T(3, 4);
@@ -2727,8 +2732,8 @@ void Engine::launch_phases(const DevTree& qt, const double* h, int nb, double* d
     else if (direct && cfg_.mode == 1 && D_ == 5 && pm == 2) FIN_T(5, 2);
     else
       k_finalize<<<fgrid, 128, 0, s>>>(g, Q, K, nb, leaf_of_pos_.p, qt.perm.p, qt.n, L_.p, Lord_.p,
-                                       cntB_.p, leaf_task_.p, leaf_runs_.p, bpart_.p, s_ff_.p, sv,
-                                       direct, d_out);
+                                       cntB_.p, leaf_task_.p, leaf_runs_.p, bpart_.p, capTask_, s_ff_.p,
+                                       sv, direct, d_out);
 #undef FIN_T
   }
   CK_LAUNCH();

@@ -335,6 +335,29 @@ __global__ void k_trav_init(const __grid_constant__ TravArgs a)
   // valid dual-tree traversal whose first lower bounds already sum over many nodes)
   const int nq = a.sq ? a.nsq : 1, nr = a.sq ? a.nsr : 1;
   const int t0 = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  // the start frontier must fit the frontier buffers like any level: otherwise nothing is
+  // written, the traversal finds an empty frontier and the host regrows and reruns
+  const long long need_e = (long long)nb * nq, need_p = need_e * nr;
+  const bool fits = need_e <= st.capE && need_p <= st.capP;
+  if (!fits) {
+    if (blockIdx.x == 0) {
+      for (int b = threadIdx.x; b < nb; b += blockDim.x)
+        for (int k = 0; k < sNStat; ++k) st.sst[b][k] = 0;
+      if (threadIdx.x == 0) {
+        st.cur = 0;
+        st.m[0] = st.p[0] = st.m[1] = st.p[1] = 0;
+        st.nF = st.nDT = st.nB = 0;
+        st.levels = 0;
+        st.done = 0;
+        Cnt l{};
+        l.e = (int)min(need_e, (long long)(INT32_MAX / 4));
+        l.p = (int)min(need_p, (long long)(INT32_MAX / 4));
+        st.lvl = l;
+        st.overflow = 1;
+      }
+    }
+    return;
+  }
   for (int e = t0; e < nb * nq; e += nt) {
     const int b = e / nq, qi = e - b * nq;
     a.fq[0][e] = b * st.K + (a.sq ? a.sq[qi] : 0);

@@ -1,7 +1,7 @@
 """Scheduling choices must not change results: the traversal with 640- and 1024-thread
 CTAs (traverse_small.cu / traverse.cu; items carry a per-key rank and are counting-sorted,
-so the CTA partition of a level is invisible), equal stream priorities and a single stream
-give the same sums bit for bit and the same TraversalStats (engine.cpp:113-195)."""
+so the CTA partition of a level is invisible), equal stream priorities, a single stream and
+the overflow-and-rerun path give the same sums bit for bit and the same TraversalStats (engine.cpp:113-195)."""
 import os
 import subprocess
 import sys
@@ -42,3 +42,6 @@ def test_results_independent_of_schedule(cfg, scale):
     assert _run(cfg, scale, DFGTB_TRAV_BLOCK="640") == base
     assert _run(cfg, scale, DFGTB_STREAM_PRIO="0", DFGTB_FF_STREAM="0", DFGTB_PREP_STREAM="0") == base
     assert _run(cfg, scale, DFGTB_ONE_STREAM="1") == base
+    # tiny first buffers: every first batch overflows and is rerun (the CV partial sums queued
+    # behind it are recomputed with it): same sums, same CV rows, same statistics
+    assert _run(cfg, scale, DFGTB_TINY_CAPS="1") == base
