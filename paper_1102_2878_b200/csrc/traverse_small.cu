@@ -3,6 +3,7 @@
 #ifndef DFGTB_SMALL_BLOCK
 #define DFGTB_SMALL_BLOCK 640  // measured on cfg2 (traversal ms): 512 0.606, 640 0.576, 768 0.598, 896 0.614, 1024 0.637
 #endif
+#undef KPBLOCK
 #define KPBLOCK DFGTB_SMALL_BLOCK
 #define DFGTB_TRAV_SMALL_TU 1
 #include "traverse.cu"
